@@ -1,0 +1,63 @@
+// Shared device helpers for the parorb B200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace po {
+
+constexpr int kWarp = 32;
+
+// Grid geometry of one rank's slab. Points are lexicographic, axis 2 fastest
+// (include/parorb/grid.hpp:11-14); a block stores N orbitals with stride ld.
+struct SlabGeom {
+  int64_t n0, n1, n2;     // global interior points per axis
+  int64_t z0, nz;         // local planes [z0, z0 + nz) of axis 0
+  int64_t plane;          // n1 * n2
+  int64_t ngl;            // nz * plane (local points)
+  int64_t ld;             // orbital stride in a block (>= ngl, padded)
+  double ih2[3];          // 1 / h_a^2
+  double w;               // quadrature weight h0 h1 h2
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block reduction of NQ values; result valid in thread 0.
+template <int NQ>
+__device__ __forceinline__ void block_sum(double (&v)[NQ], double* smem /* >= 32*NQ */) {
+  const int lane = threadIdx.x & 31;
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int warp = tid >> 5;
+  const int nwarps = (blockDim.x * blockDim.y + 31) >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) v[q] = warp_sum(v[q]);
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) smem[q * 32 + warp] = v[q];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double x = lane < nwarps ? smem[q * 32 + lane] : 0.0;
+      v[q] = warp_sum(x);
+    }
+  }
+  __syncthreads();
+}
+
+// One warp mma.sync m8n8k4 fp64 (SASS DMMA.8x8x4): D = A(8x4, row) B(4x8, col) + C.
+// Fragments: a = A[lane/4][lane%4], b = B[lane%4][lane/4],
+//            c[j] = C[lane/4][2*(lane%4) + j].
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+}  // namespace po

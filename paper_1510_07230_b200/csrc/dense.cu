@@ -1,0 +1,314 @@
+// Small dense N x N kernels kept on the device (one CTA each; N <= a few
+// thousand). They replace the reference's Eigen calls:
+//   cholesky_pass      manifold.cpp:97-114   (LLT, pivot test, L^{-T})
+//   symmetric_fallback manifold.cpp:118-132  (eig, rank test, Q lam^-1/2 Q^T)
+//   subspace_rotate    manifold.cpp:218-247  (eig ascending + sign rule)
+//   deviation / near-identity diagnostics manifold.cpp:158, 249-259.
+// Matrices are row-major in global memory (L2-resident at these sizes).
+#include <math.h>
+
+#include "kernels.h"
+
+namespace po {
+
+namespace {
+
+constexpr int DT = 1024;
+
+// Left-looking Cholesky (same recurrence as the oracle's LLT), then
+// X = L^{-1} by column-parallel forward substitution and M = X^T.
+__global__ void __launch_bounds__(DT) cholesky_inv_kernel(int N, const double* __restrict__ G,
+                                                          double* __restrict__ L,
+                                                          double* __restrict__ M,
+                                                          double* __restrict__ stats) {
+  __shared__ int fail;
+  const int t = threadIdx.x;
+  const int lane = t & 31, warp = t >> 5;
+  for (int64_t e = t; e < (int64_t)N * N; e += DT) L[e] = G[e];
+  if (t == 0) fail = 0;
+  __syncthreads();
+  for (int j = 0; j < N; ++j) {
+    // d = L(j,j) - sum_k<j L(j,k)^2, by warp 0 (fixed order)
+    if (warp == 0) {
+      double s = 0.0;
+      for (int k = lane; k < j; k += 32) s += L[(int64_t)j * N + k] * L[(int64_t)j * N + k];
+      s = warp_sum(s);
+      if (lane == 0) {
+        const double d = L[(int64_t)j * N + j] - s;
+        if (!(d > 0.0)) fail = 1;
+        else L[(int64_t)j * N + j] = sqrt(d);
+      }
+    }
+    __syncthreads();
+    if (fail) break;
+    const double ljj = L[(int64_t)j * N + j];
+    for (int i = j + 1 + t; i < N; i += DT) {
+      double s = L[(int64_t)i * N + j];
+      const double* li = L + (int64_t)i * N;
+      const double* lj = L + (int64_t)j * N;
+      for (int k = 0; k < j; ++k) s -= li[k] * lj[k];
+      L[(int64_t)i * N + j] = s / ljj;
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (t == 0) {
+      stats[0] = 0.0;
+      stats[1] = 0.0;
+      stats[2] = INFINITY;
+      stats[3] = 0.0;
+    }
+    return;
+  }
+  if (t == 0) {
+    double pmin = L[0], pmax = L[0];
+    for (int i = 1; i < N; ++i) {
+      const double v = L[(int64_t)i * N + i];
+      pmin = v < pmin ? v : pmin;
+      pmax = v > pmax ? v : pmax;
+    }
+    const bool ok = (pmin > 0.0) && isfinite(pmax) && !(pmin * pmin < 1e-10 * pmax * pmax);
+    stats[0] = pmin;
+    stats[1] = pmax;
+    stats[2] = (pmax / pmin) * (pmax / pmin);
+    stats[3] = ok ? 1.0 : 0.0;
+  }
+  // X = L^{-1}: thread c owns column c; M(k, i) = X(i, k) -> M[k*N + i].
+  for (int c = t; c < N; c += DT) {
+    for (int i = 0; i < c; ++i) M[(int64_t)c * N + i] = 0.0;  // M(c, i) = X(i, c) = 0, i < c
+    for (int i = c; i < N; ++i) {
+      double acc = i == c ? 1.0 : 0.0;
+      const double* li = L + (int64_t)i * N;
+      for (int k = c; k < i; ++k) acc -= li[k] * M[(int64_t)c * N + k];
+      M[(int64_t)c * N + i] = acc / li[i];
+    }
+  }
+}
+
+// Parallel cyclic Jacobi (round-robin pairing) on S = 1/2 (A + A^T).
+// work: N*N (S) ; evecs N*N ; evals N.
+__global__ void __launch_bounds__(DT) syev_kernel(int N, const double* __restrict__ A,
+                                                  double* __restrict__ S, double* __restrict__ V,
+                                                  double* __restrict__ evals, int sign_rule,
+                                                  double* __restrict__ stats) {
+  extern __shared__ double sh[];  // cs[2 * npair] + pairs
+  const int t = threadIdx.x;
+  const int M = N + (N & 1);      // even player count (dummy index N when odd)
+  const int npair = M / 2;
+  double* cs = sh;                // c, s per pair
+  int* pp = reinterpret_cast<int*>(sh + 2 * npair);  // p, q per pair
+  __shared__ double red[64];
+  __shared__ int done;
+  // asymmetry (manifold.cpp:224) and symmetrised copy; V = I
+  double asym = 0.0;
+  for (int64_t e = t; e < (int64_t)N * N; e += DT) {
+    const int i = (int)(e / N), j = (int)(e % N);
+    const double a = A[(int64_t)i * N + j], b = A[(int64_t)j * N + i];
+    asym = fmax(asym, fabs(a - b));
+    S[e] = 0.5 * (a + b);
+    V[e] = i == j ? 1.0 : 0.0;
+  }
+  {
+    // block max of asym
+    for (int o = 16; o > 0; o >>= 1) asym = fmax(asym, __shfl_xor_sync(0xffffffffu, asym, o));
+    if ((t & 31) == 0) red[t >> 5] = asym;
+    __syncthreads();
+    if (t == 0) {
+      double m = 0.0;
+      for (int k = 0; k < DT / 32; ++k) m = fmax(m, red[k]);
+      stats[0] = m;
+    }
+    __syncthreads();
+  }
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    // convergence test: off-diagonal Frobenius^2 vs total
+    double off = 0.0, tot = 0.0;
+    for (int64_t e = t; e < (int64_t)N * N; e += DT) {
+      const double v = S[e] * S[e];
+      tot += v;
+      if (e / N != e % N) off += v;
+    }
+    double v2[2] = {off, tot};
+    block_sum<2>(v2, red);
+    if (t == 0) done = (v2[0] <= 1e-32 * v2[1]) || v2[0] == 0.0;
+    __syncthreads();
+    if (done) break;
+    for (int round = 0; round < M - 1; ++round) {
+      // round-robin: player 0 fixed, others rotate
+      for (int k = t; k < npair; k += DT) {
+        int a, b;
+        if (k == 0) {
+          a = 0;
+          b = 1 + (round % (M - 1));
+        } else {
+          a = 1 + ((round + k) % (M - 1));
+          b = 1 + ((round + M - 1 - k) % (M - 1));
+        }
+        const int p = a < b ? a : b, q = a < b ? b : a;
+        double c = 1.0, s = 0.0;
+        if (q < N) {
+          const double apq = S[(int64_t)p * N + q];
+          if (apq != 0.0) {
+            const double theta = (S[(int64_t)q * N + q] - S[(int64_t)p * N + p]) / (2.0 * apq);
+            const double tt = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(tt * tt + 1.0);
+            s = tt * c;
+          }
+        }
+        cs[2 * k] = c;
+        cs[2 * k + 1] = s;
+        pp[2 * k] = p;
+        pp[2 * k + 1] = q;
+      }
+      __syncthreads();
+      // columns: S <- S J, V <- V J
+      for (int64_t e = t; e < (int64_t)npair * N; e += DT) {
+        const int k = (int)(e / N), r = (int)(e % N);
+        const int p = pp[2 * k], q = pp[2 * k + 1];
+        if (q >= N) continue;
+        const double c = cs[2 * k], s = cs[2 * k + 1];
+        if (s == 0.0) continue;
+        const double sp = S[(int64_t)r * N + p], sq = S[(int64_t)r * N + q];
+        S[(int64_t)r * N + p] = c * sp - s * sq;
+        S[(int64_t)r * N + q] = s * sp + c * sq;
+        const double vp = V[(int64_t)r * N + p], vq = V[(int64_t)r * N + q];
+        V[(int64_t)r * N + p] = c * vp - s * vq;
+        V[(int64_t)r * N + q] = s * vp + c * vq;
+      }
+      __syncthreads();
+      // rows: S <- J^T S
+      for (int64_t e = t; e < (int64_t)npair * N; e += DT) {
+        const int k = (int)(e / N), r = (int)(e % N);
+        const int p = pp[2 * k], q = pp[2 * k + 1];
+        if (q >= N) continue;
+        const double c = cs[2 * k], s = cs[2 * k + 1];
+        if (s == 0.0) continue;
+        const double sp = S[(int64_t)p * N + r], sq = S[(int64_t)q * N + r];
+        S[(int64_t)p * N + r] = c * sp - s * sq;
+        S[(int64_t)q * N + r] = s * sp + c * sq;
+      }
+      __syncthreads();
+    }
+  }
+  // sort ascending (thread 0; N is small) into evals and permute V columns
+  if (t == 0) {
+    int* ord = pp;  // reuse (needs N ints <= 2*npair ints)
+    for (int i = 0; i < N; ++i) ord[i] = i;
+    for (int i = 1; i < N; ++i) {
+      const int x = ord[i];
+      const double dx = S[(int64_t)x * N + x];
+      int j = i;
+      while (j > 0 && S[(int64_t)ord[j - 1] * N + ord[j - 1]] > dx) {
+        ord[j] = ord[j - 1];
+        --j;
+      }
+      ord[j] = x;
+    }
+    for (int i = 0; i < N; ++i) evals[i] = S[(int64_t)ord[i] * N + ord[i]];
+    stats[1] = 1.0;
+  }
+  __syncthreads();
+  // permute columns of V into S (reuse S as output scratch), then copy back
+  for (int64_t e = t; e < (int64_t)N * N; e += DT) {
+    const int r = (int)(e / N), j = (int)(e % N);
+    S[e] = V[(int64_t)r * N + pp[j]];
+  }
+  __syncthreads();
+  for (int j = t; j < N; j += DT) {
+    double scale = 0.0;
+    for (int r = 0; r < N; ++r) scale = fmax(scale, fabs(S[(int64_t)r * N + j]));
+    double sign = 1.0;
+    if (sign_rule) {
+      for (int r = 0; r < N; ++r) {
+        const double v = S[(int64_t)r * N + j];
+        if (fabs(v) > 1e-12 * scale) {
+          sign = v < 0.0 ? -1.0 : 1.0;
+          break;
+        }
+      }
+    }
+    for (int r = 0; r < N; ++r) V[(int64_t)r * N + j] = sign * S[(int64_t)r * N + j];
+  }
+}
+
+__global__ void __launch_bounds__(256) inv_sqrt_kernel(int N, const double* __restrict__ lam,
+                                                       const double* __restrict__ Q,
+                                                       double* __restrict__ M,
+                                                       double* __restrict__ stats) {
+  const double lmax = lam[N - 1], lmin = lam[0];
+  const bool ok = (lmax > 0.0) && isfinite(lmax) && !(lmin < 1e-12 * lmax);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    stats[0] = lmin;
+    stats[1] = lmax;
+    stats[2] = ok ? 1.0 : 0.0;
+  }
+  if (!ok) return;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)N * N;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / N), j = (int)(e % N);
+    double acc = 0.0;
+    for (int k = 0; k < N; ++k)
+      acc += Q[(int64_t)i * N + k] * (1.0 / sqrt(lam[k])) * Q[(int64_t)j * N + k];
+    M[e] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) matrix_stats_kernel(int N, const double* __restrict__ G,
+                                                           double* __restrict__ out) {
+  __shared__ double red[4][32];
+  double dev = 0.0, asym = 0.0, off = 0.0, dg = 0.0;
+  for (int64_t e = threadIdx.x; e < (int64_t)N * N; e += blockDim.x) {
+    const int i = (int)(e / N), j = (int)(e % N);
+    const double v = G[e];
+    const double d = fabs(v - (i == j ? 1.0 : 0.0));
+    dev = (d > dev || isnan(d)) ? d : dev;
+    asym = fmax(asym, fabs(v - G[(int64_t)j * N + i]));
+    if (i == j) dg = fmax(dg, d);
+    else off = fmax(off, d);
+  }
+  double v[4] = {dev, asym, off, dg};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, v[q], o);
+      v[q] = (x > v[q] || isnan(x)) ? x : v[q];
+    }
+    if ((threadIdx.x & 31) == 0) red[q][threadIdx.x >> 5] = v[q];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 4; ++q) {
+      double m = 0.0;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = (red[q][k] > m || isnan(red[q][k])) ? red[q][k] : m;
+      out[q] = m;
+    }
+  }
+}
+
+}  // namespace
+
+void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, double* stats,
+                         cudaStream_t s) {
+  cholesky_inv_kernel<<<1, DT, 0, s>>>(N, G, Lscratch, M, stats);
+}
+
+void launch_syev(int N, const double* A, double* work, double* evals, double* evecs,
+                 int sign_rule, double* stats, cudaStream_t s) {
+  const int M = N + (N & 1);
+  const size_t shm = sizeof(double) * M + sizeof(int) * M + 64;
+  syev_kernel<<<1, DT, shm, s>>>(N, A, work, evecs, evals, sign_rule, stats);
+}
+
+void launch_inv_sqrt_from_eig(int N, const double* evals, const double* evecs, double* M,
+                              double* stats, cudaStream_t s) {
+  const int64_t total = (int64_t)N * N;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 1024) blocks = 1024;
+  inv_sqrt_kernel<<<blocks, 256, 0, s>>>(N, evals, evecs, M, stats);
+}
+
+void launch_matrix_stats(int N, const double* G, double* out, cudaStream_t s) {
+  matrix_stats_kernel<<<1, 256, 0, s>>>(N, G, out);
+}
+
+}  // namespace po

@@ -1,0 +1,383 @@
+// FP64 tensor-core contractions for the orbital block (sm_100a).
+//
+// tcgen05.mma has no f64 kind on sm_100a, so FP64 tensor math is the warp-level
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4). Two contractions dominate the
+// orthonormalisation step of the reference:
+//   gram  (manifold.cpp:41-61): G = w U^T V, a tall-skinny SYRK/GEMM with
+//         K = N_g up to 7e6 -> split-K over grid points, deterministic
+//         fixed-order reduction of the per-split partials;
+//   mix   (manifold.cpp:67-85): out = U M, (N_g x N)(N x N) — the rotation
+//         U L^{-T}, the residual HU - U Sigma and the subspace rotation W P.
+// Both stage tiles through shared memory with register double-buffering
+// (global loads of stage s+1 are in flight while stage s feeds the DMMAs).
+// Fusions: the trial point W - tau Z is formed while loading (no trial block
+// is ever written), and mix can add beta*C and emit per-orbital squared norms
+// of its result instead of storing it (grad-norm of HU - U Sigma).
+#include "kernels.h"
+
+namespace po {
+
+namespace {
+
+// ------------------------------------------------------------------- Gram
+constexpr int GB = 64;     // output tile (GB x GB)
+constexpr int GK = 32;     // points per stage
+constexpr int GKP = GK + 4;  // smem row stride (doubles): conflict-free fragment reads
+constexpr int GT = 256;    // 8 warps: 4 along m x 2 along n, warp tile 16 x 32
+
+struct GramPlan {
+  int mt;       // tiles per side
+  int ntiles;   // tiles computed (upper only if sym)
+  int nsplit;   // K splits
+  int64_t kchunk;
+};
+
+GramPlan gram_plan(const SlabGeom& g, int N, int sym) {
+  GramPlan p;
+  p.mt = (N + GB - 1) / GB;
+  p.ntiles = sym ? p.mt * (p.mt + 1) / 2 : p.mt * p.mt;
+  const int target = 148 * 3;
+  int ns = (target + p.ntiles - 1) / p.ntiles;
+  const int64_t kb = (g.ld + GK - 1) / GK;  // K blocks
+  if (ns > kb) ns = (int)kb;
+  if (ns < 1) ns = 1;
+  p.kchunk = ((kb + ns - 1) / ns) * GK;
+  p.nsplit = (int)((g.ld + p.kchunk - 1) / p.kchunk);
+  return p;
+}
+
+__device__ __forceinline__ void tile_index(int t, int mt, int sym, int& tm, int& tn) {
+  if (!sym) {
+    tm = t / mt;
+    tn = t % mt;
+    return;
+  }
+  // enumerate upper triangle row by row
+  int r = 0, rem = t;
+  while (rem >= mt - r) {
+    rem -= mt - r;
+    ++r;
+  }
+  tm = r;
+  tn = r + rem;
+}
+
+// Load a GB x GK tile of (X + s Xb) rows [r0, r0+GB), points [k0, k0+GK) into regs.
+__device__ __forceinline__ void gram_load(double (&reg)[8], const double* X, const double* Xb,
+                                          double s, int N, int64_t ld, int r0, int64_t k0,
+                                          int64_t kend) {
+  const int t = threadIdx.x;
+  const int row = t >> 2;           // 0..63
+  const int c0 = (t & 3) * 8;       // 0, 8, 16, 24
+  const int r = r0 + row;
+  const int64_t k = k0 + c0;
+  if (r < N && k < kend) {          // kend is a multiple of 8 (ld padded to 32)
+    const double2* src = reinterpret_cast<const double2*>(X + (int64_t)r * ld + k);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double2 v = __ldg(src + j);
+      reg[2 * j] = v.x;
+      reg[2 * j + 1] = v.y;
+    }
+    if (Xb) {
+      const double2* sb = reinterpret_cast<const double2*>(Xb + (int64_t)r * ld + k);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        double2 v = __ldg(sb + j);
+        reg[2 * j] += s * v.x;
+        reg[2 * j + 1] += s * v.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) reg[j] = 0.0;
+  }
+}
+
+__device__ __forceinline__ void gram_store(const double (&reg)[8], double* S) {
+  const int t = threadIdx.x;
+  const int row = t >> 2;
+  const int c0 = (t & 3) * 8;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) S[row * GKP + c0 + j] = reg[j];
+}
+
+__global__ void __launch_bounds__(GT) gram_kernel(int N, int64_t ld, int64_t kchunk, int mt,
+                                                  int sym, const double* __restrict__ A,
+                                                  const double* __restrict__ Ab, double sa,
+                                                  const double* __restrict__ B,
+                                                  const double* __restrict__ Bb, double sb,
+                                                  double* __restrict__ ws) {
+  extern __shared__ __align__(16) double gsm[];
+  double (*As)[GB * GKP] = reinterpret_cast<double (*)[GB * GKP]>(gsm);
+  double (*Bs)[GB * GKP] = reinterpret_cast<double (*)[GB * GKP]>(gsm + 2 * GB * GKP);
+  int tm, tn;
+  tile_index(blockIdx.x, mt, sym, tm, tn);
+  const int m0 = tm * GB, n0 = tn * GB;
+  const int64_t kbeg = (int64_t)blockIdx.y * kchunk;
+  const int64_t kend = min(kbeg + kchunk, ld);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps
+  const int gq = lane >> 2, t4 = lane & 3;
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  double ra[8], rb[8];
+  const bool same = sym && tm == tn;
+  gram_load(ra, A, Ab, sa, N, ld, m0, kbeg, kend);
+  if (!same) gram_load(rb, B, Bb, sb, N, ld, n0, kbeg, kend);
+  int buf = 0;
+  for (int64_t k0 = kbeg; k0 < kend; k0 += GK) {
+    gram_store(ra, As[buf]);
+    gram_store(same ? ra : rb, Bs[buf]);
+    __syncthreads();
+    if (k0 + GK < kend) {  // prefetch next stage into registers
+      gram_load(ra, A, Ab, sa, N, ld, m0, k0 + GK, kend);
+      if (!same) gram_load(rb, B, Bb, sb, N, ld, n0, k0 + GK, kend);
+    }
+    const double* as = As[buf];
+    const double* bs = Bs[buf];
+#pragma unroll
+    for (int kk = 0; kk < GK / 4; ++kk) {
+      double af[2], bf[4];
+#pragma unroll
+      for (int fm = 0; fm < 2; ++fm) af[fm] = as[(wm * 16 + fm * 8 + gq) * GKP + kk * 4 + t4];
+#pragma unroll
+      for (int fn = 0; fn < 4; ++fn) bf[fn] = bs[(wn * 32 + fn * 8 + gq) * GKP + kk * 4 + t4];
+#pragma unroll
+      for (int fm = 0; fm < 2; ++fm)
+#pragma unroll
+        for (int fn = 0; fn < 4; ++fn) dmma_8x8x4(acc[fm][fn], af[fm], bf[fn]);
+    }
+    buf ^= 1;
+  }
+  // partial tile -> ws[split][tile][GB][GB]
+  double* out = ws + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * (GB * GB);
+#pragma unroll
+  for (int fm = 0; fm < 2; ++fm)
+#pragma unroll
+    for (int fn = 0; fn < 4; ++fn) {
+      const int r = wm * 16 + fm * 8 + gq;
+      const int c = wn * 32 + fn * 8 + 2 * t4;
+      out[r * GB + c] = acc[fm][fn][0];
+      out[r * GB + c + 1] = acc[fm][fn][1];
+    }
+}
+
+__global__ void gram_reduce_kernel(int N, int mt, int sym, int ntiles, int nsplit, double w,
+                                   const double* __restrict__ ws, double* __restrict__ G) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)N * N) return;
+  int i = (int)(e / N), j = (int)(e % N);
+  if (sym && j < i) {
+    const int t = i;
+    i = j;
+    j = t;
+  }
+  const int tm = i / GB, tn = j / GB;
+  int tile;
+  if (!sym) {
+    tile = tm * mt + tn;
+  } else {
+    tile = 0;
+    for (int r = 0; r < tm; ++r) tile += mt - r;
+    tile += tn - tm;
+  }
+  const int r = i - tm * GB, c = j - tn * GB;
+  double s = 0.0;
+  for (int k = 0; k < nsplit; ++k) s += ws[((int64_t)k * ntiles + tile) * (GB * GB) + r * GB + c];
+  G[e] = w * s;
+}
+
+// -------------------------------------------------------------------- mix
+constexpr int MP = 128;       // points per CTA tile
+constexpr int MI = 64;        // orbitals per CTA tile
+constexpr int MK = 16;        // k (input orbitals) per stage
+constexpr int MPP = MP + 8;   // smem strides
+constexpr int MIP = MI + 8;
+constexpr int MT = 256;       // 8 warps: 4 along p x 2 along i; warp tile 32 x 32
+
+__device__ __forceinline__ void mix_load(double (&ra)[8], double (&rm)[4], const double* A,
+                                         const double* Ab, double sa, const double* M, int N,
+                                         int64_t ld, int64_t ngl, int64_t p0, int i0, int k0) {
+  const int t = threadIdx.x;
+  {  // A: MK rows (k) x MP points: thread -> row t/16, 8 points
+    const int row = t >> 4;
+    const int c0 = (t & 15) * 8;
+    const int k = k0 + row;
+    const int64_t p = p0 + c0;
+    if (k < N && p < ld) {
+      const double2* src = reinterpret_cast<const double2*>(A + (int64_t)k * ld + p);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        double2 v = __ldg(src + j);
+        ra[2 * j] = v.x;
+        ra[2 * j + 1] = v.y;
+      }
+      if (Ab) {
+        const double2* sb = reinterpret_cast<const double2*>(Ab + (int64_t)k * ld + p);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          double2 v = __ldg(sb + j);
+          ra[2 * j] += sa * v.x;
+          ra[2 * j + 1] += sa * v.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ra[j] = 0.0;
+    }
+  }
+  {  // M: MK rows (k) x MI cols (i): thread -> row t/16, 4 cols
+    const int row = t >> 4;
+    const int c0 = (t & 15) * 4;
+    const int k = k0 + row;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + c0 + j;
+      rm[j] = (k < N && i < N) ? __ldg(M + (int64_t)k * N + i) : 0.0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(MT) mix_kernel(int N, int64_t ld, int64_t ngl, int upper,
+                                                 const double* __restrict__ A,
+                                                 const double* __restrict__ Ab, double sa,
+                                                 const double* __restrict__ M, double alpha,
+                                                 const double* __restrict__ C, double beta,
+                                                 double* __restrict__ out,
+                                                 double* __restrict__ norms) {
+  extern __shared__ __align__(16) double msm[];
+  double (*As)[MK * MPP] = reinterpret_cast<double (*)[MK * MPP]>(msm);
+  double (*Ms)[MK * MIP] = reinterpret_cast<double (*)[MK * MIP]>(msm + 2 * MK * MPP);
+  double (*nred)[MI] = reinterpret_cast<double (*)[MI]>(msm + 2 * MK * MPP + 2 * MK * MIP);
+  const int64_t p0 = (int64_t)blockIdx.x * MP;
+  const int i0 = blockIdx.y * MI;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wp = warp >> 1, wi = warp & 1;
+  const int gq = lane >> 2, t4 = lane & 3;
+  int kend = N;
+  if (upper) kend = min(N, i0 + MI);  // M(k, i) = 0 for k > i
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  double ra[8], rm[4];
+  mix_load(ra, rm, A, Ab, sa, M, N, ld, ngl, p0, i0, 0);
+  int buf = 0;
+  for (int k0 = 0; k0 < kend; k0 += MK) {
+    {
+      const int t = threadIdx.x;
+      const int row = t >> 4;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) As[buf][row * MPP + (t & 15) * 8 + j] = ra[j];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) Ms[buf][row * MIP + (t & 15) * 4 + j] = rm[j];
+    }
+    __syncthreads();
+    if (k0 + MK < kend) mix_load(ra, rm, A, Ab, sa, M, N, ld, ngl, p0, i0, k0 + MK);
+    const double* as = As[buf];
+    const double* ms = Ms[buf];
+#pragma unroll
+    for (int kk = 0; kk < MK / 4; ++kk) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int fm = 0; fm < 4; ++fm) af[fm] = as[(kk * 4 + t4) * MPP + wp * 32 + fm * 8 + gq];
+#pragma unroll
+      for (int fn = 0; fn < 4; ++fn) bf[fn] = ms[(kk * 4 + t4) * MIP + wi * 32 + fn * 8 + gq];
+#pragma unroll
+      for (int fm = 0; fm < 4; ++fm)
+#pragma unroll
+        for (int fn = 0; fn < 4; ++fn) dmma_8x8x4(acc[fm][fn], af[fm], bf[fn]);
+    }
+    buf ^= 1;
+  }
+  // epilogue: acc[fm][fn][j] = Out[p = p0 + wp*32 + fm*8 + gq][i = i0 + wi*32 + fn*8 + 2*t4 + j]
+  double nrm[4][2];
+#pragma unroll
+  for (int fn = 0; fn < 4; ++fn) nrm[fn][0] = nrm[fn][1] = 0.0;
+#pragma unroll
+  for (int fm = 0; fm < 4; ++fm) {
+    const int64_t p = p0 + wp * 32 + fm * 8 + gq;
+#pragma unroll
+    for (int fn = 0; fn < 4; ++fn)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int i = i0 + wi * 32 + fn * 8 + 2 * t4 + j;
+        if (p < ngl && i < N) {
+          double v = alpha * acc[fm][fn][j];
+          if (C) v += beta * C[(int64_t)i * ld + p];
+          if (out) out[(int64_t)i * ld + p] = v;
+          nrm[fn][j] += v * v;
+        }
+      }
+  }
+  if (norms) {
+    // reduce over gq (lane bits 2..4), then over the 4 warps along p
+#pragma unroll
+    for (int fn = 0; fn < 4; ++fn)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        double v = nrm[fn][j];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        if (gq == 0) nred[wp][wi * 32 + fn * 8 + 2 * t4 + j] = v;
+      }
+    __syncthreads();
+    if (threadIdx.x < MI) {
+      const int i = i0 + threadIdx.x;
+      if (i < N) {
+        const double s = ((nred[0][threadIdx.x] + nred[1][threadIdx.x]) + nred[2][threadIdx.x]) +
+                         nred[3][threadIdx.x];
+        norms[(int64_t)i * gridDim.x + blockIdx.x] = s;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+size_t gram_workspace_doubles(const SlabGeom& g, int N) {
+  GramPlan p = gram_plan(g, N, 0);
+  return (size_t)p.nsplit * p.ntiles * GB * GB;
+}
+
+void launch_gram(const SlabGeom& g, int N, const double* A, const double* Ab, double sa,
+                 const double* B, const double* Bb, double sb, int sym, double* ws, double* G,
+                 cudaStream_t s) {
+  GramPlan p = gram_plan(g, N, sym);
+  dim3 grid(p.ntiles, p.nsplit);
+  constexpr size_t shm = sizeof(double) * 4 * GB * GKP;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+    attr = true;
+  }
+  gram_kernel<<<grid, GT, shm, s>>>(N, g.ld, p.kchunk, p.mt, sym, A, Ab, sa, B, Bb, sb, ws);
+  const int64_t total = (int64_t)N * N;
+  gram_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(N, p.mt, sym, p.ntiles,
+                                                                      p.nsplit, g.w, ws, G);
+}
+
+int mix_nblk(const SlabGeom& g) { return (int)((g.ngl + MP - 1) / MP); }
+
+void launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, double sa,
+                const double* M, double alpha, const double* C, double beta, int upper,
+                double* out, double* norms, cudaStream_t s) {
+  dim3 grid(mix_nblk(g), (N + MI - 1) / MI);
+  constexpr size_t shm = sizeof(double) * (2 * MK * MPP + 2 * MK * MIP + 4 * MI);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(mix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+    attr = true;
+  }
+  mix_kernel<<<grid, MT, shm, s>>>(N, g.ld, g.ngl, upper, A, Ab, sa, M, alpha, C, beta, out, norms);
+}
+
+}  // namespace po

@@ -1,0 +1,645 @@
+// Engine (device-resident rank state) and the operator-level C ABI
+// (include/parorb_gpu.h). Each po_* operator mirrors one reference function
+// (cited in the header); all arithmetic runs in the sm_100a kernels — there is
+// no host compute path.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "engine.h"
+
+namespace po {
+
+namespace {
+__global__ void copy_diag_kernel(int N, const double* __restrict__ M, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N) out[i] = M[(int64_t)i * N + i];
+}
+}  // namespace
+
+void launch_copy_diag(int N, const double* M, double* out, cudaStream_t s) {
+  copy_diag_kernel<<<(N + 255) / 256, 256, 0, s>>>(N, M, out);
+}
+
+static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist_desc* dist) {
+  if (!grid) throw Error(PO_EINVAL, "null grid");
+  for (int a = 0; a < 3; ++a) {
+    if (grid->n[a] < 1) throw Error(PO_EINVAL, "grid: points_per_axis must be >= 1");
+    if (!(grid->extent[a] > 0.0) || !std::isfinite(grid->extent[a]))
+      throw Error(PO_EINVAL, "grid: extents must be positive and finite");
+  }
+  if (n < 1) throw Error(PO_EINVAL, "make_problem: n_orbitals must be >= 1");
+  if (!(occupation > 0.0)) throw Error(PO_EINVAL, "occupation must be positive");
+  N = n;
+  occ = occupation;
+  if (dist && dist->device >= 0) PO_CUDA(cudaSetDevice(dist->device));
+  comm = make_comm(dist);
+  rank = comm->rank;
+  size = comm->size;
+
+  g.n0 = grid->n[0];
+  g.n1 = grid->n[1];
+  g.n2 = grid->n[2];
+  if (g.n0 < size) throw Error(PO_EINVAL, "fewer axis-0 planes than ranks");
+  if ((int64_t)n > g.n0 * g.n1 * g.n2)
+    throw Error(PO_EINVAL, "make_problem: more orbitals than grid points");
+  const int64_t base = g.n0 / size, rem = g.n0 % size;
+  g.nz = base + (rank < rem ? 1 : 0);
+  g.z0 = rank * base + (rank < rem ? rank : rem);
+  g.plane = g.n1 * g.n2;
+  g.ngl = g.nz * g.plane;
+  g.ld = round_up(g.ngl, 32);
+  g.w = 1.0;
+  for (int a = 0; a < 3; ++a) {
+    ext[a] = grid->extent[a];
+    h[a] = grid->extent[a] / (double)(grid->n[a] + 1);  // grid.cpp:33
+    g.ih2[a] = 1.0 / (h[a] * h[a]);
+    g.w *= h[a];
+  }
+  ng_full = g.n0 * g.n1 * g.n2;
+  max_slab_points = (base + (rem ? 1 : 0)) * g.plane;
+
+  PO_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const size_t fb = sizeof(double) * (size_t)g.ngl;
+  PO_CUDA(cudaMalloc(&v_ext, fb));
+  PO_CUDA(cudaMemsetAsync(v_ext, 0, fb, s));
+  def_state_ = new_state();
+
+  size_t pc = 0;
+  auto upd = [&](size_t v) { pc = v > pc ? v : pc; };
+  upd((size_t)3 * N * hamiltonian_nblk(g));
+  upd((size_t)N * mix_nblk(g));
+  upd((size_t)3 * N * per_orbital_nblk(g, N));
+  upd((size_t)2 * points_nblk(g));
+  partials_cap = pc;
+  PO_CUDA(cudaMalloc(&partials, pc * sizeof(double)));
+  PO_CUDA(cudaMalloc(&gram_ws, gram_workspace_doubles(g, N) * sizeof(double)));
+  PO_CUDA(cudaMalloc(&dvec, dvec_len() * sizeof(double)));
+  PO_CUDA(cudaMemsetAsync(dvec, 0, dvec_len() * sizeof(double), s));
+  PO_CUDA(cudaMallocHost(&hvec, dvec_len() * sizeof(double)));
+  const size_t nn = (size_t)N * N * sizeof(double);
+  for (auto& m : dmat) PO_CUDA(cudaMalloc(&m, nn));
+  PO_CUDA(cudaMalloc(&chol_L, nn));
+  PO_CUDA(cudaMalloc(&syev_work, nn));
+  PO_CUDA(cudaMallocHost(&hmat, nn));
+  if (size > 1) {
+    const size_t hb = (size_t)N * g.plane * sizeof(double);
+    PO_CUDA(cudaMalloc(&halo_lo, hb));
+    PO_CUDA(cudaMalloc(&halo_hi, hb));
+    PO_CUDA(cudaMalloc(&send_lo, hb));
+    PO_CUDA(cudaMalloc(&send_hi, hb));
+    PO_CUDA(cudaMemsetAsync(halo_lo, 0, hb, s));
+    PO_CUDA(cudaMemsetAsync(halo_hi, 0, hb, s));
+  }
+  // replicated full-grid Poisson buffers (+ gather staging for size > 1)
+  const size_t full = (size_t)ng_full + (size > 1 ? (size_t)size * max_slab_points : 0);
+  PO_CUDA(cudaMalloc(&cg_b, full * sizeof(double)));
+  PO_CUDA(cudaMalloc(&cg_x, (size_t)ng_full * sizeof(double)));
+  PO_CUDA(cudaMemsetAsync(cg_x, 0, (size_t)ng_full * sizeof(double), s));
+  PO_CUDA(cudaMalloc(&cg_ws, cg_workspace_doubles(ng_full) * sizeof(double)));
+  PO_CUDA(cudaMalloc(&cg_bar, 4 * sizeof(unsigned)));
+  PO_CUDA(cudaMalloc(&cg_out_i, 4 * sizeof(int)));
+  PO_CUDA(cudaMalloc(&cg_out_d, 4 * sizeof(double)));
+  PO_CUDA(cudaMallocHost(&h_cg_i, 4 * sizeof(int)));
+  PO_CUDA(cudaMallocHost(&h_cg_d, 4 * sizeof(double)));
+  PO_CUDA(cudaMemsetAsync(cg_out_i, 0, 4 * sizeof(int), s));
+  PO_CUDA(cudaMemsetAsync(cg_out_d, 0, 4 * sizeof(double), s));
+  sync();
+}
+
+Engine::~Engine() {
+  if (s) cudaStreamSynchronize(s);
+  for (double* b : blocks_)
+    if (b) cudaFree(b);
+  for (DevState* st : states_) {
+    if (!st) continue;
+    cudaFree(st->rho);
+    cudaFree(st->v_h);
+    cudaFree(st->v_xc);
+    cudaFree(st->v_local);
+    delete st;
+  }
+  double* bufs[] = {v_ext, partials, gram_ws, dvec, chol_L, syev_work, halo_lo, halo_hi,
+                    send_lo, send_hi, cg_b, cg_x, cg_ws, cg_out_d};
+  for (double* p : bufs)
+    if (p) cudaFree(p);
+  for (double* m : dmat)
+    if (m) cudaFree(m);
+  if (cg_bar) cudaFree(cg_bar);
+  if (cg_out_i) cudaFree(cg_out_i);
+  if (hvec) cudaFreeHost(hvec);
+  if (hmat) cudaFreeHost(hmat);
+  if (h_cg_i) cudaFreeHost(h_cg_i);
+  if (h_cg_d) cudaFreeHost(h_cg_d);
+  comm.reset();
+  if (s) cudaStreamDestroy(s);
+}
+
+void Engine::sync() {
+  PO_CUDA(cudaGetLastError());
+  PO_CUDA(cudaStreamSynchronize(s));
+}
+
+int Engine::alloc_block() {
+  double* p = nullptr;
+  const size_t bytes = sizeof(double) * (size_t)N * (size_t)g.ld;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(PO_ENOMEM, std::string("block allocation failed: ") + cudaGetErrorString(e));
+  }
+  PO_CUDA(cudaMemsetAsync(p, 0, bytes, s));  // padding stays zero forever
+  for (size_t i = 0; i < blocks_.size(); ++i)
+    if (!blocks_[i]) {
+      blocks_[i] = p;
+      return (int)i;
+    }
+  blocks_.push_back(p);
+  return (int)blocks_.size() - 1;
+}
+
+void Engine::free_block(int b) {
+  double* p = blk(b);
+  PO_CUDA(cudaStreamSynchronize(s));
+  PO_CUDA(cudaFree(p));
+  blocks_[b] = nullptr;
+}
+
+double* Engine::blk(int b) const {
+  if (b < 0 || b >= (int)blocks_.size() || !blocks_[b]) throw Error(PO_EINVAL, "invalid block handle");
+  return blocks_[b];
+}
+
+void Engine::zero_block(int b) {
+  PO_CUDA(cudaMemsetAsync(blk(b), 0, sizeof(double) * (size_t)N * g.ld, s));
+}
+
+DevState* Engine::new_state() {
+  auto* st = new DevState;
+  const size_t fb = sizeof(double) * (size_t)g.ngl;
+  PO_CUDA(cudaMalloc(&st->rho, fb));
+  PO_CUDA(cudaMalloc(&st->v_h, fb));
+  PO_CUDA(cudaMalloc(&st->v_xc, fb));
+  PO_CUDA(cudaMalloc(&st->v_local, fb));
+  for (double* p : {st->rho, st->v_h, st->v_xc, st->v_local}) PO_CUDA(cudaMemsetAsync(p, 0, fb, s));
+  states_.push_back(st);
+  return st;
+}
+
+void Engine::free_state(DevState* st) {
+  for (auto& x : states_)
+    if (x == st) {
+      PO_CUDA(cudaStreamSynchronize(s));
+      cudaFree(st->rho);
+      cudaFree(st->v_h);
+      cudaFree(st->v_xc);
+      cudaFree(st->v_local);
+      delete st;
+      x = nullptr;
+    }
+}
+
+void Engine::fetch(size_t off, size_t n) {
+  PO_CUDA(cudaMemcpyAsync(hvec + off, dvec + off, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  sync();
+}
+
+void Engine::reduce_rows(const double* parts, int rows, int nblk, double scale, double* out,
+                         bool allreduce) {
+  launch_reduce_rows(parts, rows, nblk, scale, out, s);
+  if (allreduce && size > 1) comm->allreduce_sum(out, (size_t)rows, s);
+}
+
+// energy.cpp:228-246
+void Engine::build_state(const double* u, int hartree, int xc, DevState* st, int warm) {
+  double* b_local = nullptr;
+  if (hartree) b_local = size > 1 ? cg_b + ng_full : cg_b + g.z0 * g.plane;
+  launch_density_xc(g, N, u, occ, xc, st->rho, st->v_xc, b_local, partials, s);
+  const int pn = points_nblk(g);
+  launch_reduce_rows(partials, 1, pn, g.w, scal() + S_EXC, s);  // E_xc = <eps, rho>
+  if (hartree) {
+    if (size > 1) {
+      comm->allgather(b_local, cg_b + ng_full, (size_t)max_slab_points, s);
+      // compact rank slabs (uneven split) into the full grid
+      const int64_t base = g.n0 / size, rem = g.n0 % size;
+      int64_t z = 0;
+      for (int r = 0; r < size; ++r) {
+        const int64_t nz = base + (r < rem ? 1 : 0);
+        PO_CUDA(cudaMemcpyAsync(cg_b + z * g.plane, cg_b + ng_full + (int64_t)r * max_slab_points,
+                                sizeof(double) * nz * g.plane, cudaMemcpyDeviceToDevice, s));
+        z += nz;
+      }
+    }
+    launch_cg(g.n0, g.n1, g.n2, g.ih2, cg_b, cg_x, warm, cg_ws, cg_bar, cg_out_i, cg_out_d, s);
+    PO_CUDA(cudaMemcpyAsync(st->v_h, cg_x + g.z0 * g.plane, sizeof(double) * g.ngl,
+                            cudaMemcpyDeviceToDevice, s));
+  } else {
+    PO_CUDA(cudaMemsetAsync(st->v_h, 0, sizeof(double) * g.ngl, s));
+    PO_CUDA(cudaMemsetAsync(cg_out_i, 0, 2 * sizeof(int), s));
+  }
+  launch_vlocal(g, v_ext, st->v_h, st->v_xc, st->rho, st->v_local, partials, s);
+  launch_reduce_rows(partials, 1, pn, 0.5 * g.w, scal() + S_EH, s);  // E_H = 1/2 <v_H, rho>
+  if (size > 1) comm->allreduce_sum(scal() + S_EXC, 3, s);          // S_EXC..S_EH
+  PO_CUDA(cudaMemcpyAsync(h_cg_i, cg_out_i, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  PO_CUDA(cudaGetLastError());
+  if (!xc) PO_CUDA(cudaMemsetAsync(scal() + S_EXC, 0, sizeof(double), s));
+  if (!hartree) PO_CUDA(cudaMemsetAsync(scal() + S_EH, 0, sizeof(double), s));
+}
+
+void Engine::finish_state(DevState* st) {
+  fetch_all();
+  if (h_cg_i[0] != 0) throw Error(PO_ESOLVER, "poisson: CG did not reach the requested residual");
+  st->cg_iters = h_cg_i[1];
+  st->e_xc = hvec[off_scal() + S_EXC];
+  st->e_hartree = hvec[off_scal() + S_EH];
+}
+
+void Engine::halo_exchange(const double* u) {
+  if (size <= 1) return;
+  launch_pack_plane(g, N, u, 0, send_lo, s);
+  launch_pack_plane(g, N, u, g.nz - 1, send_hi, s);
+  comm->halo(send_lo, send_hi, halo_lo, halo_hi, (size_t)N * g.plane, s);
+}
+
+void Engine::apply_h(const double* u, double* out, const double* v_local) {
+  halo_exchange(u);
+  const double* lo = (size > 1 && rank > 0) ? halo_lo : nullptr;
+  const double* hi = (size > 1 && rank + 1 < size) ? halo_hi : nullptr;
+  launch_hamiltonian(g, N, u, lo, hi, v_local, v_ext, out, partials, s);
+  const int nb = hamiltonian_nblk(g);
+  launch_reduce_rows(partials, N, nb, g.w, dvec + off_sig(), s);
+  launch_reduce_rows(partials + (size_t)N * nb, N, nb, -0.5 * g.w, dvec + off_kin(), s);
+  launch_reduce_rows(partials + (size_t)2 * N * nb, N, nb, g.w, dvec + off_ext(), s);
+  if (size > 1) comm->allreduce_sum(dvec + off_sig(), (size_t)3 * N, s);
+}
+
+void Engine::gram(const double* A, const double* Ab, double sa, const double* B, const double* Bb,
+                  double sb, int sym, double* Gdev) {
+  launch_gram(g, N, A, Ab, sa, B, Bb, sb, sym, gram_ws, Gdev, s);
+  if (size > 1) comm->allreduce_sum(Gdev, (size_t)N * N, s);
+}
+
+void Engine::mix(const double* A, const double* Ab, double sa, const double* M, double alpha,
+                 const double* C, double beta, int upper, double* out, double* norm_rows) {
+  launch_mix(g, N, A, Ab, sa, M, alpha, C, beta, upper, out, norm_rows ? partials : nullptr, s);
+  if (norm_rows) reduce_rows(partials, N, mix_nblk(g), g.w, norm_rows, true);
+}
+
+}  // namespace po
+
+// ============================================================== C ABI ====
+
+using po::Engine;
+using po::Error;
+
+#define API_TRY try {
+#define API_CATCH(h)                                   \
+  }                                                    \
+  catch (const po::Error& ex) {                        \
+    if (h) (h)->err = ex.what();                       \
+    return ex.code;                                    \
+  }                                                    \
+  catch (const std::exception& ex) {                   \
+    if (h) (h)->err = ex.what();                       \
+    return PO_EINVAL;                                  \
+  }                                                    \
+  return PO_OK;
+
+#define ENGINE_OR_EINVAL(h) \
+  if (!(h) || !(h)->e) return PO_EINVAL; \
+  Engine& E = *(h)->e;
+
+extern "C" {
+
+int po_abi_version(void) { return PO_ABI_VERSION; }
+
+int po_create(const po_grid_desc* grid, int n_orbitals, double occupation,
+              const po_dist_desc* dist, po_engine** out) {
+  if (!out) return PO_EINVAL;
+  *out = nullptr;
+  auto* h = new po_engine{nullptr, {}};
+  try {
+    h->e = new Engine(grid, n_orbitals, occupation, dist);
+  } catch (const Error& ex) {
+    h->err = ex.what();
+    *out = h;  // caller can read po_last_error, then po_destroy
+    return ex.code;
+  }
+  *out = h;
+  return PO_OK;
+}
+
+int po_destroy(po_engine* h) {
+  if (!h) return PO_OK;
+  delete h->e;
+  delete h;
+  return PO_OK;
+}
+
+const char* po_last_error(const po_engine* h) { return h ? h->err.c_str() : "null engine"; }
+
+int po_local_slab(const po_engine* h, int64_t* z0, int64_t* nz, int64_t* ngl) {
+  if (!h || !h->e) return PO_EINVAL;
+  if (z0) *z0 = h->e->g.z0;
+  if (nz) *nz = h->e->g.nz;
+  if (ngl) *ngl = h->e->g.ngl;
+  return PO_OK;
+}
+
+int64_t po_solver_bytes(const po_grid_desc* grid, int n, int size) {
+  if (!grid || n < 1 || size < 1) return -1;
+  const int64_t ng = grid->n[0] * grid->n[1] * grid->n[2];
+  const int64_t nzmax = (grid->n[0] + size - 1) / size;
+  const int64_t ngl = nzmax * grid->n[1] * grid->n[2];
+  const int64_t ld = (ngl + 31) / 32 * 32;
+  const int64_t block = (int64_t)n * ld * 8;
+  // W HW Z WP ZP WT HWT WT2 REC(+ shared) + scratch: ~10 blocks worst case
+  const int64_t fields = 8 * ngl * 8 * 3 + 7 * ng * 8;
+  return 10 * block + fields + (int64_t)n * n * 8 * 12;
+}
+
+void* po_stream(po_engine* h) { return (h && h->e) ? (void*)h->e->s : nullptr; }
+
+int po_synchronize(po_engine* h) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  E.sync();
+  API_CATCH(h)
+}
+
+int po_alloc_block(po_engine* h, int* block) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  *block = E.alloc_block();
+  API_CATCH(h)
+}
+
+int po_free_block(po_engine* h, int block) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  E.free_block(block);
+  API_CATCH(h)
+}
+
+int po_upload_block(po_engine* h, int block, const double* host) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  PO_CUDA(cudaMemcpy2DAsync(E.blk(block), E.g.ld * 8, host, E.g.ngl * 8, E.g.ngl * 8, E.N,
+                            cudaMemcpyHostToDevice, E.s));
+  E.sync();
+  API_CATCH(h)
+}
+
+int po_download_block(po_engine* h, int block, double* host) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  PO_CUDA(cudaMemcpy2DAsync(host, E.g.ngl * 8, E.blk(block), E.g.ld * 8, E.g.ngl * 8, E.N,
+                            cudaMemcpyDeviceToHost, E.s));
+  E.sync();
+  API_CATCH(h)
+}
+
+int po_copy_block(po_engine* h, int dst, int src) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  PO_CUDA(cudaMemcpyAsync(E.blk(dst), E.blk(src), sizeof(double) * E.N * E.g.ld,
+                          cudaMemcpyDeviceToDevice, E.s));
+  API_CATCH(h)
+}
+
+static double* field_ptr(Engine& E, int f) {
+  po::DevState* st = E.default_state();
+  switch (f) {
+    case PO_VEXT: return E.v_ext;
+    case PO_RHO: return st->rho;
+    case PO_VH: return st->v_h;
+    case PO_VXC: return st->v_xc;
+    case PO_VLOCAL: return st->v_local;
+  }
+  throw Error(PO_EINVAL, "unknown field");
+}
+
+int po_set_field(po_engine* h, int field, const double* host) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  PO_CUDA(cudaMemcpyAsync(field_ptr(E, field), host, sizeof(double) * E.g.ngl,
+                          cudaMemcpyHostToDevice, E.s));
+  E.sync();
+  API_CATCH(h)
+}
+
+int po_get_field(po_engine* h, int field, double* host) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  PO_CUDA(cudaMemcpyAsync(host, field_ptr(E, field), sizeof(double) * E.g.ngl,
+                          cudaMemcpyDeviceToHost, E.s));
+  E.sync();
+  API_CATCH(h)
+}
+
+static int set_potential(po_engine* h, const double* atoms, int n, int gaussian) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  if (n < 0 || (n > 0 && !atoms)) throw Error(PO_EINVAL, "invalid atom list");
+  for (int a = 0; a < n && !gaussian; ++a) {
+    const double* q = atoms + 5 * a;
+    if (!(q[3] > 0.0)) throw Error(PO_EINVAL, "make_problem: atom charge must be positive");
+    if (!(q[4] > 0.0)) throw Error(PO_EINVAL, "make_problem: atom softening must be positive");
+    for (int d = 0; d < 3; ++d)
+      if (!(q[d] >= 0.0) || !(q[d] <= E.ext[d]))
+        throw Error(PO_EINVAL, "make_problem: atom position outside the grid box");
+  }
+  double* d = nullptr;
+  if (n > 0) {
+    PO_CUDA(cudaMalloc(&d, sizeof(double) * 5 * n));
+    PO_CUDA(cudaMemcpyAsync(d, atoms, sizeof(double) * 5 * n, cudaMemcpyHostToDevice, E.s));
+  }
+  po::launch_external_potential(E.g, E.h, d, n, gaussian, E.v_ext, E.s);
+  E.sync();
+  if (d) cudaFree(d);
+  API_CATCH(h)
+}
+
+int po_external_potential(po_engine* h, const double* atoms, int natoms) {
+  return set_potential(h, atoms, natoms, 0);
+}
+
+int po_gaussian_potential(po_engine* h, const double* wells, int nwells) {
+  return set_potential(h, wells, nwells, 1);
+}
+
+int po_random_block(po_engine* h, int block, uint64_t seed) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  // The reference draws orbital-major over the whole grid (tests/problems.hpp:59-68);
+  // this rank keeps the values of its slab.
+  std::vector<double> host((size_t)E.N * E.g.ngl);
+  po::rng_normals_slab(seed, E.N, E.ng_full, E.g.z0 * E.g.plane, E.g.ngl, host.data());
+  PO_CUDA(cudaMemcpy2DAsync(E.blk(block), E.g.ld * 8, host.data(), E.g.ngl * 8, E.g.ngl * 8, E.N,
+                            cudaMemcpyHostToDevice, E.s));
+  E.sync();
+  API_CATCH(h)
+}
+
+int po_build_hamiltonian(po_engine* h, int u, int hartree, int xc, double* e_hartree,
+                         double* e_xc, int* cg_iters) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  po::DevState* st = E.default_state();
+  E.build_state(E.blk(u), hartree, xc, st, 0);
+  E.finish_state(st);
+  if (e_hartree) *e_hartree = st->e_hartree;
+  if (e_xc) *e_xc = st->e_xc;
+  if (cg_iters) *cg_iters = st->cg_iters;
+  API_CATCH(h)
+}
+
+int po_apply_hamiltonian(po_engine* h, int u, int out, double* sigma, double* kin, double* ext) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  E.apply_h(E.blk(u), out >= 0 ? E.blk(out) : nullptr, E.default_state()->v_local);
+  E.fetch(0, (size_t)3 * E.N);
+  if (sigma) std::memcpy(sigma, E.hvec + E.off_sig(), sizeof(double) * E.N);
+  if (kin) std::memcpy(kin, E.hvec + E.off_kin(), sizeof(double) * E.N);
+  if (ext) std::memcpy(ext, E.hvec + E.off_ext(), sizeof(double) * E.N);
+  API_CATCH(h)
+}
+
+int po_total_energy(po_engine* h, int u, int hartree, int xc, double* out5) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  po::DevState* st = E.default_state();
+  E.apply_h(E.blk(u), nullptr, st->v_local);
+  E.fetch(0, (size_t)3 * E.N);
+  double kin = 0.0, ext = 0.0;
+  for (int i = 0; i < E.N; ++i) kin += E.occ * E.hvec[E.off_kin() + i];
+  for (int i = 0; i < E.N; ++i) ext += E.occ * E.hvec[E.off_ext() + i];
+  out5[0] = kin;
+  out5[1] = ext;
+  out5[2] = hartree ? st->e_hartree : 0.0;
+  out5[3] = xc ? st->e_xc : 0.0;
+  out5[4] = out5[0] + out5[1] + out5[2] + out5[3];
+  API_CATCH(h)
+}
+
+int po_laplacian(po_engine* h, int u, int out) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  E.halo_exchange(E.blk(u));
+  const double* lo = (E.size > 1 && E.rank > 0) ? E.halo_lo : nullptr;
+  const double* hi = (E.size > 1 && E.rank + 1 < E.size) ? E.halo_hi : nullptr;
+  po::launch_laplacian(E.g, E.N, E.blk(u), lo, hi, E.blk(out), E.s);
+  E.sync();
+  API_CATCH(h)
+}
+
+static void fetch_matrix(Engine& E, const double* dm, double* host) {
+  PO_CUDA(cudaMemcpyAsync(E.hmat, dm, sizeof(double) * E.N * E.N, cudaMemcpyDeviceToHost, E.s));
+  E.sync();
+  std::memcpy(host, E.hmat, sizeof(double) * E.N * E.N);
+}
+
+static void put_matrix(Engine& E, const double* host, double* dm) {
+  std::memcpy(E.hmat, host, sizeof(double) * E.N * E.N);
+  PO_CUDA(cudaMemcpyAsync(dm, E.hmat, sizeof(double) * E.N * E.N, cudaMemcpyHostToDevice, E.s));
+  E.sync();
+}
+
+int po_gram(po_engine* h, int a, int b, double* g_host) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  E.gram(E.blk(a), nullptr, 0.0, E.blk(b), nullptr, 0.0, a == b, E.dmat[6]);
+  fetch_matrix(E, E.dmat[6], g_host);
+  API_CATCH(h)
+}
+
+int po_mix(po_engine* h, int in, const double* m_host, int out) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  if (in == out) throw Error(PO_EINVAL, "mix: in and out must differ");
+  put_matrix(E, m_host, E.dmat[6]);
+  E.mix(E.blk(in), nullptr, 0.0, E.dmat[6], 1.0, nullptr, 0.0, 0, E.blk(out), nullptr);
+  E.sync();
+  API_CATCH(h)
+}
+
+int po_linear_combination(po_engine* h, int a, double sc, int b, int out) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  po::launch_lincomb(E.g, E.N, E.blk(a), sc, E.blk(b), E.blk(out), E.s);
+  E.sync();
+  API_CATCH(h)
+}
+
+int po_bb_products(po_engine* h, int w, int wp, int z, int zp, double* ss, double* sy,
+                   double* yy) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  const int nb = po::per_orbital_nblk(E.g, E.N);
+  po::launch_bb(E.g, E.N, E.blk(w), E.blk(wp), E.blk(z), E.blk(zp), E.partials, E.s);
+  E.reduce_rows(E.partials, 3 * E.N, nb, E.g.w, E.dvec + E.off_ss(), true);
+  E.fetch(E.off_ss(), (size_t)3 * E.N);
+  if (ss) std::memcpy(ss, E.hvec + E.off_ss(), sizeof(double) * E.N);
+  if (sy) std::memcpy(sy, E.hvec + E.off_sy(), sizeof(double) * E.N);
+  if (yy) std::memcpy(yy, E.hvec + E.off_yy(), sizeof(double) * E.N);
+  API_CATCH(h)
+}
+
+int po_diagonal_residuals(po_engine* h, int u, int hu, int z, double* sigma, double* znorm2) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  const int nb = po::per_orbital_nblk(E.g, E.N);
+  // sigma_ii = <hu_i, u_i>: the s*y product of the BB kernel with zero "previous" blocks
+  po::launch_bb(E.g, E.N, E.blk(hu), nullptr, E.blk(u), nullptr, E.partials, E.s);
+  E.reduce_rows(E.partials + (size_t)E.N * nb, E.N, nb, E.g.w, E.dvec + E.off_sig(), true);
+  po::launch_residual_diag(E.g, E.N, E.blk(u), E.blk(hu), E.dvec + E.off_sig(), E.blk(z),
+                           E.partials, E.s);
+  E.reduce_rows(E.partials, E.N, nb, E.g.w, E.dvec + E.off_zz(), true);
+  E.fetch(0, E.off_dd());
+  if (sigma) std::memcpy(sigma, E.hvec + E.off_sig(), sizeof(double) * E.N);
+  if (znorm2) std::memcpy(znorm2, E.hvec + E.off_zz(), sizeof(double) * E.N);
+  API_CATCH(h)
+}
+
+int po_stiefel_gradient(po_engine* h, int u, int hu, double* sigma_host, double* dnorm2) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  E.gram(E.blk(hu), nullptr, 0.0, E.blk(u), nullptr, 0.0, 0, E.dmat[4]);
+  po::launch_matrix_stats(E.N, E.dmat[4], E.scal() + Engine::S_SYM, E.s);
+  E.mix(E.blk(u), nullptr, 0.0, E.dmat[4], -1.0, E.blk(hu), 1.0, 0, nullptr, E.dvec + E.off_dd());
+  E.fetch_all();
+  if (sigma_host) fetch_matrix(E, E.dmat[4], sigma_host);
+  if (dnorm2) std::memcpy(dnorm2, E.hvec + E.off_dd(), sizeof(double) * E.N);
+  if (E.hvec[E.off_scal() + Engine::S_SYM + 1] > 1e-10)
+    throw Error(PO_EINVAL, "stiefel_gradient: <(HU)^T U> is not symmetric; inconsistent H or U");
+  API_CATCH(h)
+}
+
+int po_subspace_rotate(po_engine* h, int w, const double* sigma_host, double* gamma,
+                       double* p_host) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  put_matrix(E, sigma_host, E.dmat[4]);
+  po::launch_syev(E.N, E.dmat[4], E.syev_work, E.dmat[6], E.dmat[5], 1, E.scal() + Engine::S_EIG,
+                  E.s);
+  E.fetch(E.off_scal(), 64);
+  if (E.hvec[E.off_scal() + Engine::S_EIG] > 1e-8)
+    throw Error(PO_EINVAL, "subspace_rotate: Sigma asymmetry exceeds tolerance");
+  int tmp = E.alloc_block();
+  E.mix(E.blk(w), nullptr, 0.0, E.dmat[5], 1.0, nullptr, 0.0, 0, E.blk(tmp), nullptr);
+  PO_CUDA(cudaMemcpyAsync(E.blk(w), E.blk(tmp), sizeof(double) * E.N * E.g.ld,
+                          cudaMemcpyDeviceToDevice, E.s));
+  E.free_block(tmp);
+  if (gamma) {
+    PO_CUDA(cudaMemcpyAsync(E.hmat, E.dmat[6], sizeof(double) * E.N, cudaMemcpyDeviceToHost, E.s));
+    E.sync();
+    std::memcpy(gamma, E.hmat, sizeof(double) * E.N);
+  }
+  if (p_host) fetch_matrix(E, E.dmat[5], p_host);
+  E.sync();
+  API_CATCH(h)
+}
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+// po_engine: device-resident state of one rank (one GPU) and the host-side
+// orchestration of the hot-path kernels. Internal C++ API used by the C ABI
+// (engine.cu) and the InnerLoop mirror (solver.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/parorb_gpu.h"
+#include "kernels.h"
+
+namespace po {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PO_CUDA(x)                                                                      \
+  do {                                                                                  \
+    cudaError_t _e = (x);                                                               \
+    if (_e != cudaSuccess)                                                              \
+      throw ::po::Error(PO_ECUDA, std::string(#x ": ") + cudaGetErrorString(_e));      \
+  } while (0)
+
+// Collectives between the ranks of one job (slab decomposition).
+struct Comm {
+  int rank = 0, size = 1;
+  virtual ~Comm() = default;
+  // in-place sum over ranks of n doubles on the device; identical result on all ranks
+  virtual void allreduce_sum(double* d, size_t n, cudaStream_t s) = 0;
+  // recv[r * n + k] = send_r[k]
+  virtual void allgather(const double* send, double* recv, size_t n, cudaStream_t s) = 0;
+  // exchange one plane block with the axis-0 neighbours: send_lo -> rank-1's recv_hi,
+  // send_hi -> rank+1's recv_lo (n doubles each)
+  virtual void halo(const double* send_lo, const double* send_hi, double* recv_lo,
+                    double* recv_hi, size_t n, cudaStream_t s) = 0;
+};
+std::unique_ptr<Comm> make_comm(const po_dist_desc* d);
+
+// A built Hamiltonian state (HamiltonianState, energy.hpp:41-50) on the device.
+struct DevState {
+  double* rho = nullptr;
+  double* v_h = nullptr;   // local slab
+  double* v_xc = nullptr;
+  double* v_local = nullptr;
+  double* vh_full = nullptr;  // full-grid v_H (warm start / replicated solve)
+  double e_hartree = 0.0, e_xc = 0.0;
+  int cg_iters = 0;
+};
+
+struct EnergyParts {  // EnergyBreakdown, energy.hpp:52-58
+  double kinetic = 0, external = 0, hartree = 0, xc = 0, total = 0;
+};
+
+class Engine {
+ public:
+  Engine(const po_grid_desc* grid, int n, double occupation, const po_dist_desc* dist);
+  ~Engine();
+
+  SlabGeom g;
+  int N;
+  double occ;
+  double h[3], ext[3];
+  int rank = 0, size = 1;
+  cudaStream_t s = nullptr;
+  std::unique_ptr<Comm> comm;
+  std::string err;
+
+  // ---- blocks (handles)
+  int alloc_block();
+  void free_block(int b);
+  double* blk(int b) const;
+  void zero_block(int b);
+
+  // ---- states
+  DevState* new_state();
+  void free_state(DevState* st);
+  DevState* default_state() { return def_state_; }
+  double* v_ext = nullptr;
+
+  // ---- operators (device-side results land in dvec_ regions; see *_result)
+  // density -> Poisson -> xc -> v_local; returns after queueing; results via sync_state
+  void build_state(const double* u, int hartree, int xc, DevState* st, int warm);
+  // CG outcome + E_H / E_xc of the last build (synchronises)
+  void finish_state(DevState* st);
+  // H u with fused reductions (sigma, kin, ext), scaled, into dvec rows
+  void apply_h(const double* u, double* out, const double* v_local);
+  void halo_exchange(const double* u);
+  void gram(const double* A, const double* Ab, double sa, const double* B, const double* Bb,
+            double sb, int sym, double* Gdev);
+  void mix(const double* A, const double* Ab, double sa, const double* M, double alpha,
+           const double* C, double beta, int upper, double* out, double* norm_rows);
+  void reduce_rows(const double* partials, int rows, int nblk, double scale, double* out,
+                   bool allreduce);
+
+  // device scratch
+  double* partials = nullptr;
+  size_t partials_cap = 0;
+  double* gram_ws = nullptr;
+  double* dvec = nullptr;      // small device vector scratch (kDvec doubles)
+  double* hvec = nullptr;      // pinned mirror of dvec
+  double* dmat[8] = {};        // N x N device matrices
+  double* hmat = nullptr;      // pinned N x N host
+  double* chol_L = nullptr;    // N x N scratch
+  double* syev_work = nullptr;
+  double* halo_lo = nullptr;   // recv planes (N x plane) or null
+  double* halo_hi = nullptr;
+  double* send_lo = nullptr;
+  double* send_hi = nullptr;
+  // Poisson (full grid, replicated across ranks)
+  double* cg_b = nullptr;
+  double* cg_x = nullptr;
+  double* cg_ws = nullptr;
+  unsigned* cg_bar = nullptr;
+  int* cg_out_i = nullptr;     // device {status, iters}
+  double* cg_out_d = nullptr;  // device {bnorm, relres}
+  int* h_cg_i = nullptr;       // pinned
+  double* h_cg_d = nullptr;
+  int64_t ng_full = 0;
+  int64_t max_slab_points = 0;
+
+  // dvec layout (offsets in doubles); N-length rows
+  size_t off_sig() const { return 0; }
+  size_t off_kin() const { return (size_t)N; }
+  size_t off_ext() const { return 2 * (size_t)N; }
+  size_t off_zz() const { return 3 * (size_t)N; }
+  size_t off_dd() const { return 4 * (size_t)N; }
+  size_t off_ss() const { return 5 * (size_t)N; }
+  size_t off_sy() const { return 6 * (size_t)N; }
+  size_t off_yy() const { return 7 * (size_t)N; }
+  size_t off_abs() const { return 8 * (size_t)N; }
+  size_t off_scal() const { return 9 * (size_t)N; }  // 64 scalars
+  size_t dvec_len() const { return 9 * (size_t)N + 64; }
+  // scalar slots
+  enum { S_EXC = 0, S_BB = 1, S_EH = 2, S_CHOL = 8, S_EIG = 12, S_INVS = 16, S_MSTAT = 20,
+         S_MSTAT2 = 24, S_SYM = 28 };
+  double* scal() { return dvec + off_scal(); }
+  // copy n doubles of dvec starting at off into hvec (same offsets) and synchronise
+  void fetch(size_t off, size_t n);
+  void fetch_all() { fetch(0, dvec_len()); }
+  void sync();
+
+ private:
+  std::vector<double*> blocks_;
+  std::vector<DevState*> states_;
+  DevState* def_state_ = nullptr;
+};
+
+}  // namespace po
+
+struct po_engine {
+  po::Engine* e;
+  std::string err;
+};

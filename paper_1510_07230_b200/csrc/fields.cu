@@ -1,0 +1,291 @@
+// Pointwise / per-orbital streaming kernels (HBM-bound) for the parorb hot path.
+// Each replaces a reference CPU loop, cited per kernel. Reductions produce
+// per-CTA partials that launch_reduce_rows sums in a fixed order, so every
+// result is bitwise reproducible run to run (the reference's determinism
+// contract, parallel.hpp:16-19).
+#include <math.h>
+
+#include "kernels.h"
+
+namespace po {
+
+namespace {
+
+constexpr int PT = 256;         // threads per CTA for point-parallel kernels
+constexpr int PMAXBLK = 148 * 8;
+
+__device__ __forceinline__ double dirac_cx() {
+  // kDiracCx = 0.75 * cbrt(3 / pi), energy.cpp:18
+  return 0.75 * cbrt(3.0 / 3.141592653589793238462643383279502884);
+}
+
+// energy.cpp:67-76 density + 212-226 Dirac exchange + 4 pi rho (energy.cpp:207-209)
+__global__ void __launch_bounds__(PT) density_xc_kernel(SlabGeom g, int N,
+                                                        const double* __restrict__ u, double occ,
+                                                        int xc, double* __restrict__ rho,
+                                                        double* __restrict__ vxc,
+                                                        double* __restrict__ b,
+                                                        double* __restrict__ partials) {
+  __shared__ double red[2 * 32];
+  double acc[2] = {0.0, 0.0};
+  const double cx = dirac_cx();
+  const double four_pi = 4.0 * 3.141592653589793238462643383279502884;
+  for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < g.ngl;
+       p += (int64_t)gridDim.x * PT) {
+    double s = 0.0;
+    int i = 0;
+    for (; i + 4 <= N; i += 4) {  // 4 independent loads in flight, ascending-i sum
+      const double a0 = __ldg(u + (int64_t)i * g.ld + p);
+      const double a1 = __ldg(u + (int64_t)(i + 1) * g.ld + p);
+      const double a2 = __ldg(u + (int64_t)(i + 2) * g.ld + p);
+      const double a3 = __ldg(u + (int64_t)(i + 3) * g.ld + p);
+      s += a0 * a0;
+      s += a1 * a1;
+      s += a2 * a2;
+      s += a3 * a3;
+    }
+    for (; i < N; ++i) {
+      const double a = __ldg(u + (int64_t)i * g.ld + p);
+      s += a * a;
+    }
+    const double r = occ == 1.0 ? s : s * occ;
+    rho[p] = r;
+    if (xc) {
+      const double eps = -cx * cbrt(r);
+      vxc[p] = eps * (4.0 / 3.0);
+      acc[0] += eps * r;
+    } else {
+      vxc[p] = 0.0;
+    }
+    if (b) {
+      const double bb = r * four_pi;
+      b[p] = bb;
+      acc[1] += bb * bb;
+    }
+  }
+  block_sum<2>(acc, red);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = acc[0];
+    partials[gridDim.x + blockIdx.x] = acc[1];
+  }
+}
+
+__global__ void __launch_bounds__(PT) vlocal_kernel(SlabGeom g, const double* __restrict__ vext,
+                                                    const double* __restrict__ vh,
+                                                    const double* __restrict__ vxc,
+                                                    const double* __restrict__ rho,
+                                                    double* __restrict__ vloc,
+                                                    double* __restrict__ partials) {
+  __shared__ double red[32];
+  double acc[1] = {0.0};
+  for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < g.ngl;
+       p += (int64_t)gridDim.x * PT) {
+    const double h = vh[p];
+    vloc[p] = vext[p] + (h + vxc[p]);
+    acc[0] += h * rho[p];
+  }
+  block_sum<1>(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc[0];
+}
+
+// grid: (nblk, N)
+__global__ void __launch_bounds__(PT) residual_diag_kernel(SlabGeom g, int N,
+                                                           const double* __restrict__ u,
+                                                           const double* __restrict__ hu,
+                                                           const double* __restrict__ sig,
+                                                           double* __restrict__ z,
+                                                           double* __restrict__ partials) {
+  __shared__ double red[32];
+  const int i = blockIdx.y;
+  const double ms = -sig[i];
+  const double* ui = u + (int64_t)i * g.ld;
+  const double* hi = hu + (int64_t)i * g.ld;
+  double* zi = z + (int64_t)i * g.ld;
+  double acc[1] = {0.0};
+  for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < g.ngl;
+       p += (int64_t)gridDim.x * PT) {
+    const double v = hi[p] + ms * ui[p];
+    zi[p] = v;
+    acc[0] += v * v;
+  }
+  block_sum<1>(acc, red);
+  if (threadIdx.x == 0) partials[(int64_t)i * gridDim.x + blockIdx.x] = acc[0];
+}
+
+__global__ void __launch_bounds__(PT) bb_kernel(SlabGeom g, int N, const double* __restrict__ w,
+                                                const double* __restrict__ wp,
+                                                const double* __restrict__ z,
+                                                const double* __restrict__ zp,
+                                                double* __restrict__ partials) {
+  __shared__ double red[3 * 32];
+  const int i = blockIdx.y;
+  const int64_t o = (int64_t)i * g.ld;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < g.ngl;
+       p += (int64_t)gridDim.x * PT) {
+    const double s = wp ? w[o + p] - wp[o + p] : w[o + p];
+    const double y = zp ? z[o + p] - zp[o + p] : z[o + p];
+    acc[0] += s * s;
+    acc[1] += s * y;
+    acc[2] += y * y;
+  }
+  block_sum<3>(acc, red);
+  if (threadIdx.x == 0) {
+    const int nb = gridDim.x;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) partials[((int64_t)q * N + i) * nb + blockIdx.x] = acc[q];
+  }
+}
+
+__global__ void __launch_bounds__(PT) abs_sum_kernel(SlabGeom g, int N,
+                                                     const double* __restrict__ x,
+                                                     double* __restrict__ partials) {
+  __shared__ double red[32];
+  const int i = blockIdx.y;
+  double acc[1] = {0.0};
+  for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < g.ngl;
+       p += (int64_t)gridDim.x * PT)
+    acc[0] += fabs(x[(int64_t)i * g.ld + p]);
+  block_sum<1>(acc, red);
+  if (threadIdx.x == 0) partials[(int64_t)i * gridDim.x + blockIdx.x] = acc[0];
+}
+
+__global__ void __launch_bounds__(PT) lincomb_kernel(int64_t total, const double* __restrict__ a,
+                                                     double sc, const double* __restrict__ b,
+                                                     double* __restrict__ out) {
+  for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < total;
+       p += (int64_t)gridDim.x * PT)
+    out[p] = a[p] + sc * b[p];
+}
+
+// One warp per row; lanes stride the partials, then a fixed shuffle tree.
+__global__ void reduce_rows_kernel(const double* __restrict__ partials, int rows, int nblk,
+                                   double scale, double* __restrict__ out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const double* p = partials + (int64_t)warp * nblk;
+  double s = 0.0;
+  for (int b = lane; b < nblk; b += 32) s += p[b];
+  s = warp_sum(s);
+  if (lane == 0) out[warp] = scale * s;
+}
+
+// energy.cpp:78-99 (softened Coulomb) or BASELINE C5 Gaussian wells.
+__global__ void __launch_bounds__(PT) potential_kernel(SlabGeom g, double h0, double h1,
+                                                       double h2, const double* __restrict__ at,
+                                                       int natoms, int gaussian,
+                                                       double* __restrict__ v) {
+  for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < g.ngl;
+       p += (int64_t)gridDim.x * PT) {
+    const int64_t k2 = p % g.n2;
+    const int64_t k1 = (p / g.n2) % g.n1;
+    const int64_t k0 = p / g.plane + g.z0;
+    const double xyz[3] = {(double)(k0 + 1) * h0, (double)(k1 + 1) * h1, (double)(k2 + 1) * h2};
+    double acc = 0.0;
+    for (int a = 0; a < natoms; ++a) {
+      const double* q = at + 5 * a;
+      if (!gaussian) {
+        double r2 = q[4] * q[4];
+        for (int d = 0; d < 3; ++d) {
+          const double dx = xyz[d] - q[d];
+          r2 += dx * dx;
+        }
+        acc -= q[3] / sqrt(r2);
+      } else {
+        double r2 = 0.0;
+        for (int d = 0; d < 3; ++d) {
+          const double dx = xyz[d] - q[d];
+          r2 += dx * dx;
+        }
+        acc += q[3] * exp(-r2 / (2.0 * q[4] * q[4]));
+      }
+    }
+    v[p] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(PT) pack_plane_kernel(SlabGeom g, int N,
+                                                        const double* __restrict__ u,
+                                                        int64_t plane_idx,
+                                                        double* __restrict__ dst) {
+  const int i = blockIdx.y;
+  for (int64_t q = (int64_t)blockIdx.x * PT + threadIdx.x; q < g.plane;
+       q += (int64_t)gridDim.x * PT)
+    dst[(int64_t)i * g.plane + q] = u[(int64_t)i * g.ld + plane_idx * g.plane + q];
+}
+
+int nblk_for(int64_t work) {
+  int64_t b = (work + PT - 1) / PT;
+  if (b > PMAXBLK) b = PMAXBLK;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+int points_nblk(const SlabGeom& g) { return nblk_for(g.ngl); }
+
+// Per-orbital kernels use fewer CTAs per orbital so N * nblk stays ~ a few waves.
+int per_orbital_nblk(const SlabGeom& g, int N) {
+  int64_t target = (148 * 8 + N - 1) / N;
+  if (target < 8) target = 8;
+  int64_t b = (g.ngl + PT - 1) / PT;
+  return (int)(b < target ? b : target);
+}
+
+void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupation, int xc,
+                       double* rho, double* v_xc, double* b, double* partials, cudaStream_t s) {
+  density_xc_kernel<<<points_nblk(g), PT, 0, s>>>(g, N, u, occupation, xc, rho, v_xc, b,
+                                                  partials);
+}
+
+void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h, const double* v_xc,
+                   const double* rho, double* v_local, double* partials, cudaStream_t s) {
+  vlocal_kernel<<<points_nblk(g), PT, 0, s>>>(g, v_ext, v_h, v_xc, rho, v_local, partials);
+}
+
+void launch_residual_diag(const SlabGeom& g, int N, const double* u, const double* hu,
+                          const double* sigma_diag, double* z, double* partials, cudaStream_t s) {
+  dim3 grid(per_orbital_nblk(g, N), N);
+  residual_diag_kernel<<<grid, PT, 0, s>>>(g, N, u, hu, sigma_diag, z, partials);
+}
+
+void launch_bb(const SlabGeom& g, int N, const double* w, const double* wp, const double* z,
+               const double* zp, double* partials, cudaStream_t s) {
+  dim3 grid(per_orbital_nblk(g, N), N);
+  bb_kernel<<<grid, PT, 0, s>>>(g, N, w, wp, z, zp, partials);
+}
+
+void launch_abs_sum(const SlabGeom& g, int N, const double* x, double* partials,
+                    cudaStream_t s) {
+  dim3 grid(per_orbital_nblk(g, N), N);
+  abs_sum_kernel<<<grid, PT, 0, s>>>(g, N, x, partials);
+}
+
+void launch_lincomb(const SlabGeom& g, int N, const double* a, double sc, const double* b,
+                    double* out, cudaStream_t s) {
+  const int64_t total = (int64_t)N * g.ld;
+  lincomb_kernel<<<nblk_for(total), PT, 0, s>>>(total, a, sc, b, out);
+}
+
+void launch_reduce_rows(const double* partials, int rows, int nblk, double scale, double* out,
+                        cudaStream_t s) {
+  const int threads = 256;
+  const int blocks = (rows * 32 + threads - 1) / threads;
+  reduce_rows_kernel<<<blocks, threads, 0, s>>>(partials, rows, nblk, scale, out);
+}
+
+void launch_external_potential(const SlabGeom& g, const double* h3, const double* atoms,
+                               int natoms, int gaussian, double* v, cudaStream_t s) {
+  potential_kernel<<<points_nblk(g), PT, 0, s>>>(g, h3[0], h3[1], h3[2], atoms, natoms, gaussian,
+                                                 v);
+}
+
+void launch_pack_plane(const SlabGeom& g, int N, const double* u, int64_t plane_idx, double* dst,
+                       cudaStream_t s) {
+  dim3 grid((unsigned)((g.plane + PT - 1) / PT), N);
+  pack_plane_kernel<<<grid, PT, 0, s>>>(g, N, u, plane_idx, dst);
+}
+
+}  // namespace po

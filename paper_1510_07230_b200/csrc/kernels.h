@@ -1,0 +1,114 @@
+// Host-side launchers of the parorb sm_100a kernels (internal to libparorb_b200).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace po {
+
+// ---------------------------------------------------------------- stencil.cu
+// Batched H u (energy.cpp:248-265) fused with the per-orbital reductions
+// sigma_ii, <lap u_i, u_i>, <V_ext u_i, u_i> (energy.cpp:267-280). Partials:
+// [3][N][nblk], raw (unweighted) sums. hu may be null (reductions only).
+int hamiltonian_nblk(const SlabGeom& g);
+void launch_hamiltonian(const SlabGeom& g, int N, const double* u, const double* halo_lo,
+                        const double* halo_hi, const double* v_local, const double* v_ext,
+                        double* hu, double* partials, cudaStream_t s);
+// Plain 7-point Dirichlet Laplacian of every orbital (grid.cpp:94-122).
+void launch_laplacian(const SlabGeom& g, int N, const double* u, const double* halo_lo,
+                      const double* halo_hi, double* out, cudaStream_t s);
+
+// ----------------------------------------------------------------- fields.cu
+int points_nblk(const SlabGeom& g);
+// CTAs per orbital of the per-orbital streaming kernels (partials row length).
+int per_orbital_nblk(const SlabGeom& g, int N);
+// rho = f sum_i u_i^2 (energy.cpp:67-76); v_xc, eps (energy.cpp:212-226);
+// b = 4 pi rho written at b (may be null). Partials [2][nblk]: sum eps*rho, sum b*b.
+void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupation, int xc,
+                       double* rho, double* v_xc, double* b, double* partials, cudaStream_t s);
+// v_local = v_ext + (v_h + v_xc) (energy.cpp:241-244); partials [1][nblk]: sum v_h*rho.
+void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h, const double* v_xc,
+                   const double* rho, double* v_local, double* partials, cudaStream_t s);
+// z_i = hu_i - sigma_ii u_i (manifold.cpp:204-216); partials [1][N][nblk]: sum z^2.
+void launch_residual_diag(const SlabGeom& g, int N, const double* u, const double* hu,
+                          const double* sigma_diag, double* z, double* partials, cudaStream_t s);
+// BB products (optimizer.cpp:386-397); partials [3][N][nblk]: ss, sy, yy (raw).
+void launch_bb(const SlabGeom& g, int N, const double* w, const double* wp, const double* z,
+               const double* zp, double* partials, cudaStream_t s);
+// out = a + s * b over a whole block (grid.cpp:219-228).
+void launch_lincomb(const SlabGeom& g, int N, const double* a, double sc, const double* b,
+                    double* out, cudaStream_t s);
+// Per-orbital sum of |x| (mean-abs convergence, optimizer.cpp:446-458): partials [1][N][nblk].
+void launch_abs_sum(const SlabGeom& g, int N, const double* x, double* partials, cudaStream_t s);
+// out[r] = scale * sum_b partials[r * nblk + b], fixed order (deterministic).
+void launch_reduce_rows(const double* partials, int rows, int nblk, double scale, double* out,
+                        cudaStream_t s);
+// V_ext from softened-Coulomb atoms (energy.cpp:78-99) / Gaussian wells (C5).
+void launch_external_potential(const SlabGeom& g, const double* h3, const double* atoms,
+                               int natoms, int gaussian, double* v, cudaStream_t s);
+// Pack plane `plane_idx` of every orbital into dst[N][plane] (halo send buffers).
+void launch_pack_plane(const SlabGeom& g, int N, const double* u, int64_t plane_idx,
+                       double* dst, cudaStream_t s);
+
+// ------------------------------------------------------------------ dmma.cu
+// Split-K tall-skinny Gram on the FP64 tensor cores (mma.sync f64):
+// G(i,j) = w * sum_p (A + sa Ab)_i[p] (B + sb Bb)_j[p]. Ab/Bb may be null.
+// sym: A == B (and Ab == Bb, sa == sb); only upper tiles are computed and
+// G is mirrored exactly (manifold.cpp:45-53). G: device N x N row-major.
+size_t gram_workspace_doubles(const SlabGeom& g, int N);
+void launch_gram(const SlabGeom& g, int N, const double* A, const double* Ab, double sa,
+                 const double* B, const double* Bb, double sb, int sym, double* ws,
+                 double* G, cudaStream_t s);
+// Column mixing on the FP64 tensor cores (manifold.cpp:67-85):
+// out_i = alpha * sum_k (A + sa Ab)_k M(k, i) + beta * C_i. M device row-major.
+// upper: M is upper triangular (skip zero k-blocks). out may be null; norms
+// (may be null) receives partials [N][nblk] of sum_p out_i[p]^2.
+int mix_nblk(const SlabGeom& g);
+void launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, double sa,
+                const double* M, double alpha, const double* C, double beta, int upper,
+                double* out, double* norms, cudaStream_t s);
+
+// ----------------------------------------------------------------- dense.cu
+// Cholesky G = L L^T (lower) and M = L^{-T} (upper, row-major M[k*N+i]),
+// following manifold.cpp:97-114. stats: {pmin, pmax, cond, ok}.
+void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, double* stats,
+                         cudaStream_t s);
+// Symmetric eigensolver (parallel cyclic Jacobi) on 1/2 (A + A^T):
+// evals ascending, evecs column j in evecs[i*N + j]; sign rule of
+// manifold.cpp:233-241 applied when sign_rule != 0. stats: {asym, ok}.
+void launch_syev(int N, const double* A, double* work, double* evals, double* evecs,
+                 int sign_rule, double* stats, cudaStream_t s);
+// M = Q diag(lam^{-1/2}) Q^T (manifold.cpp:128-130); stats: {lam_min, lam_max, ok}.
+void launch_inv_sqrt_from_eig(int N, const double* evals, const double* evecs, double* M,
+                              double* stats, cudaStream_t s);
+// max |G - I| (manifold.cpp:158) and max |S - S^T|, offdiag / diag deviation
+// (manifold.cpp:249-259): out {dev, asym, offdiag_max, diag_dev_max}.
+void launch_matrix_stats(int N, const double* G, double* out, cudaStream_t s);
+// out[i] = M(i, i)
+void launch_copy_diag(int N, const double* M, double* out, cudaStream_t s);
+
+// ------------------------------------------------------------------ rng.cu
+// parorb::Rng(seed) normals (rng.hpp:13-41) drawn orbital-major over the full
+// grid (tests/problems.hpp:59-68); keeps points [offset, offset+count) of each
+// of the N orbitals: out[i * count + k].
+void rng_normals_slab(uint64_t seed, int N, int64_t ng_full, int64_t offset, int64_t count,
+                      double* out);
+
+// --------------------------------------------------------------- poisson.cu
+struct CgResult {
+  int status;      // 0 ok, 3 solver error
+  int iters;       // CG iterations over all restarts
+  double bnorm;
+};
+// -lap x = b (Dirichlet) by CG on the full grid, x0 = 0 or warm (x holds the
+// guess), rel. tol 1e-10, <= 20000 its x <= 4 passes (energy.cpp:105-143).
+// One cooperative persistent kernel; work: ws >= 5 * ng doubles + scratch.
+size_t cg_workspace_doubles(int64_t ng);
+void launch_cg(int64_t n0, int64_t n1, int64_t n2, const double ih2[3], const double* b,
+               double* x, int warm, double* ws, unsigned* bar, int* out_i, double* out_d,
+               cudaStream_t s);
+int cg_grid_blocks();
+
+}  // namespace po

@@ -1,0 +1,624 @@
+// Host C++ mirror of the reference solver loop over device-resident blocks.
+//
+// Restates InnerLoop::run (optimizer.cpp:322-579), finalize (:581-597) and
+// run_single_level (:599-613) decision for decision — tau clamps (:25-28), BB
+// variants and the tr|.| reading (:30-41, :376-411), the raw-step growth cap
+// (:419-444), the delta^s search with the tau_min break (:455-484), recovery
+// from the last orthonormalised iterate (:485-508), the C/Q ledger (:509-521),
+// checkpoints / drift flags (:535-539) and the n_diag subspace rotation
+// (:550-561) — while every field / block operation runs on the GPU. Per
+// line-search trial the device pipeline is:
+//   Gram(W - tau Z)  ->  Cholesky + L^{-T} (device)  ->  (W - tau Z) L^{-T}
+//   [-> Gram -> CholeskyQR2 repair]  ->  rho, v_xc  ->  Poisson CG  ->  v_local
+//   ->  H W~ with fused sigma / kinetic / external reductions
+// and the trial's H W~ becomes the next iteration's HW when it is accepted, so
+// the reference's separate total_energy Laplacians and apply_hamiltonian pass
+// collapse into one stencil pass.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <memory>
+#include <vector>
+
+#include "engine.h"
+
+namespace po {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+using BRef = std::shared_ptr<int>;
+using SRef = std::shared_ptr<DevState>;
+
+struct BlockPool {
+  Engine& E;
+  std::vector<int> free_;
+  explicit BlockPool(Engine& e) : E(e) {}
+  ~BlockPool() {
+    for (int h : free_) {
+      try {
+        E.free_block(h);
+      } catch (...) {
+      }
+    }
+  }
+  BRef get() {
+    int h;
+    if (!free_.empty()) {
+      h = free_.back();
+      free_.pop_back();
+    } else {
+      h = E.alloc_block();
+    }
+    return BRef(new int(h), [this](int* p) {
+      free_.push_back(*p);
+      delete p;
+    });
+  }
+};
+
+struct StatePool {
+  Engine& E;
+  std::vector<DevState*> free_;
+  explicit StatePool(Engine& e) : E(e) {}
+  ~StatePool() {
+    for (DevState* s : free_) {
+      try {
+        E.free_state(s);
+      } catch (...) {
+      }
+    }
+  }
+  SRef get() {
+    DevState* s;
+    if (!free_.empty()) {
+      s = free_.back();
+      free_.pop_back();
+    } else {
+      s = E.new_state();
+    }
+    return SRef(s, [this](DevState* p) { free_.push_back(p); });
+  }
+};
+
+double clamp_tau(double raw, const po_params& p) {  // optimizer.cpp:25-28
+  if (!std::isfinite(raw)) return p.tau_max;
+  return std::min(std::max(raw, p.tau_min), p.tau_max);
+}
+
+bool use_bb1(int v, int iter) {  // optimizer.cpp:30-34
+  if (v == PO_BB1) return true;
+  if (v == PO_BB2) return false;
+  return iter % 2 == 0;
+}
+
+}  // namespace
+
+struct OrthOut {
+  double post_dev = 0.0;
+  double offdiag_max = 0.0;  // near_identity_from_gram(pre_gram), manifold.cpp:249-259
+  double diag_dev_max = 0.0;
+  bool fallback = false;
+};
+
+// manifold.cpp:136-169 on the device. in = A + sa * Ab (Ab may be null).
+// Returns false on DegenerateSetError. pre-Gram stays in E.dmat[0].
+bool orthonormalize_dev(Engine& E, const double* A, const double* Ab, double sa, double* out,
+                        const std::function<double*()>& scratch, bool measure, OrthOut& o) {
+  double* sc = E.scal();
+  E.gram(A, Ab, sa, A, Ab, sa, 1, E.dmat[0]);
+  launch_matrix_stats(E.N, E.dmat[0], sc + Engine::S_MSTAT, E.s);
+  launch_cholesky_inv(E.N, E.dmat[0], E.chol_L, E.dmat[1], sc + Engine::S_CHOL, E.s);
+  E.fetch(E.off_scal(), 64);
+  const double* hs = E.hvec + E.off_scal();
+  o.offdiag_max = hs[Engine::S_MSTAT + 2];
+  o.diag_dev_max = hs[Engine::S_MSTAT + 3];
+  double cond = std::numeric_limits<double>::infinity();
+  int upper = 1;
+  o.fallback = false;
+  if (hs[Engine::S_CHOL + 3] != 1.0) {
+    // symmetric_fallback, manifold.cpp:118-132
+    launch_syev(E.N, E.dmat[0], E.syev_work, E.dmat[6], E.dmat[5], 0, sc + Engine::S_EIG, E.s);
+    launch_inv_sqrt_from_eig(E.N, E.dmat[6], E.dmat[5], E.dmat[1], sc + Engine::S_INVS, E.s);
+    E.fetch(E.off_scal(), 64);
+    if (hs[Engine::S_INVS + 2] != 1.0) return false;
+    upper = 0;
+    o.fallback = true;
+  } else {
+    cond = hs[Engine::S_CHOL + 2];
+  }
+  E.mix(A, Ab, sa, E.dmat[1], 1.0, nullptr, 0.0, upper, out, nullptr);
+  if (!measure && cond <= 1e2) {
+    o.post_dev = -1.0;
+    return true;
+  }
+  E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2]);
+  launch_matrix_stats(E.N, E.dmat[2], sc + Engine::S_MSTAT2, E.s);
+  E.fetch(E.off_scal(), 64);
+  double dev = hs[Engine::S_MSTAT2];
+  if (!(dev <= 1e-12)) {  // CholeskyQR2 repair pass
+    launch_cholesky_inv(E.N, E.dmat[2], E.chol_L, E.dmat[3], sc + Engine::S_CHOL, E.s);
+    E.fetch(E.off_scal(), 64);
+    if (hs[Engine::S_CHOL + 3] != 1.0) return false;
+    double* tmp = scratch();
+    E.mix(out, nullptr, 0.0, E.dmat[3], 1.0, nullptr, 0.0, 1, tmp, nullptr);
+    PO_CUDA(cudaMemcpyAsync(out, tmp, sizeof(double) * E.N * E.g.ld, cudaMemcpyDeviceToDevice,
+                            E.s));
+    E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2]);
+    launch_matrix_stats(E.N, E.dmat[2], sc + Engine::S_MSTAT2, E.s);
+    E.fetch(E.off_scal(), 64);
+    dev = hs[Engine::S_MSTAT2];
+  }
+  o.post_dev = dev;
+  return true;
+}
+
+namespace {
+
+struct Solver {
+  Engine& E;
+  const po_params& p;
+  po_result* r;
+  BlockPool pool;
+  StatePool spool;
+  bool nonlinear;
+  SRef fixed_state;
+  bool have_prev_solve = false;
+
+  Solver(Engine& e, const po_params& pp, po_result* rr)
+      : E(e), p(pp), r(rr), pool(e), spool(e), nonlinear(pp.hartree || pp.xc) {}
+
+  double* P(const BRef& b) { return E.blk(*b); }
+
+  SRef make_state(const BRef& u) {  // optimizer.cpp:224-229
+    if (!nonlinear && fixed_state) return fixed_state;
+    SRef st = spool.get();
+    E.build_state(P(u), p.hartree, p.xc, st.get(), p.poisson_warm_start && have_prev_solve);
+    E.finish_state(st.get());
+    if (p.hartree) have_prev_solve = true;
+    r->cg_iters_total += st->cg_iters;
+    if (!nonlinear) fixed_state = st;
+    return st;
+  }
+
+  // apply H and return the energy breakdown (energy.cpp:282-314) of u
+  EnergyParts apply_and_energy(const BRef& u, const BRef& hu, const DevState& st) {
+    E.apply_h(P(u), hu ? P(hu) : nullptr, st.v_local);
+    E.fetch(0, (size_t)3 * E.N);
+    EnergyParts e;
+    for (int i = 0; i < E.N; ++i) e.kinetic += E.occ * E.hvec[E.off_kin() + i];
+    for (int i = 0; i < E.N; ++i) e.external += E.occ * E.hvec[E.off_ext() + i];
+    e.hartree = p.hartree ? st.e_hartree : 0.0;
+    e.xc = p.xc ? st.e_xc : 0.0;
+    e.total = e.kinetic + e.external + e.hartree + e.xc;
+    return e;
+  }
+
+  void set_energy(const EnergyParts& e) {
+    r->e_kinetic = e.kinetic;
+    r->e_external = e.external;
+    r->e_hartree = e.hartree;
+    r->e_xc = e.xc;
+    r->e_total = e.total;
+  }
+
+  int fail(int outcome, const char* msg) {
+    std::snprintf(r->message, sizeof r->message, "%s", msg);
+    r->outcome = outcome;
+    return outcome;
+  }
+
+  // Sigma = <(HW)^T W> into dmat[4]; max asymmetry into S_SYM+1
+  void sigma(const BRef& w, const BRef& hw) {
+    E.gram(P(hw), nullptr, 0.0, P(w), nullptr, 0.0, 0, E.dmat[4]);
+    launch_matrix_stats(E.N, E.dmat[4], E.scal() + Engine::S_SYM, E.s);
+  }
+
+  void trace_eigs(const BRef& w, const BRef& hw) {
+    if (!p.trace_sigma_eigs || !r->sigma_eigs) return;
+    sigma(w, hw);
+    launch_syev(E.N, E.dmat[4], E.syev_work, E.dmat[6], E.dmat[5], 1, E.scal() + Engine::S_EIG,
+                E.s);
+    PO_CUDA(cudaMemcpyAsync(E.hmat, E.dmat[6], sizeof(double) * E.N, cudaMemcpyDeviceToHost, E.s));
+    E.sync();
+    std::memcpy(r->sigma_eigs + (size_t)r->n_records * E.N, E.hmat, sizeof(double) * E.N);
+  }
+
+  int run(BRef& w);
+};
+
+int Solver::run(BRef& w) {
+  const int n = E.N;
+  const int n_org = p.algorithm == PO_ALG_OPT_PAR_MOD ? p.n_org : 1;
+  const bool full_grad = p.algorithm == PO_ALG_OPTM_QR;
+  const bool grad_style =
+      p.convergence_mode == PO_CONV_GRAD_NORM || p.convergence_mode == PO_CONV_MEAN_ABS;
+  const bool mean_abs = p.convergence_mode == PO_CONV_MEAN_ABS;
+  const double ngd = (double)E.g.n0 * (double)E.g.n1 * (double)E.g.n2;
+
+  SRef state = make_state(w);
+  BRef hw = pool.get();
+  const EnergyParts e0 = apply_and_energy(w, hw, *state);
+  if (!std::isfinite(e0.total)) return fail(PO_OUT_NUMERICAL_FAILURE, "non-finite total energy at the level start");
+  set_energy(e0);
+
+  double nm_c = e0.total, nm_q = 1.0;
+  std::vector<double> orth_energies{e0.total};
+  BRef prev_w, prev_z;
+  bool history_valid = false;
+  int last_rotation_iter = 0, steps_until_orth = 0;
+  bool converged = false;
+  bool sig_valid = true;  // dvec sigma row belongs to (w, hw)
+  BRef recovery_w = w;
+  SRef recovery_state = state;
+  int failed_searches = 0;
+  double last_accepted_tau = 0.0;
+
+  for (int l = 0; l < p.max_inner && !converged; ++l) {
+    const auto t0 = Clock::now();
+    const bool orth_iter = steps_until_orth == 0;
+    const bool need_full = orth_iter && grad_style;
+
+    // ---- compute_directions, optimizer.cpp:265-320
+    BRef z = pool.get();
+    BRef dscratch;
+    const int onb = per_orbital_nblk(E.g, n);
+    if (full_grad) {
+      sigma(w, hw);
+      E.mix(P(w), nullptr, 0.0, E.dmat[4], -1.0, P(hw), 1.0, 0, P(z), E.dvec + E.off_dd());
+      if (mean_abs && need_full) {
+        launch_abs_sum(E.g, n, P(z), E.partials, E.s);
+        E.reduce_rows(E.partials, n, onb, 1.0, E.dvec + E.off_abs(), true);
+      }
+    } else {
+      if (need_full || !sig_valid) {
+        sigma(w, hw);
+        launch_copy_diag(n, E.dmat[4], E.dvec + E.off_sig(), E.s);
+      }
+      launch_residual_diag(E.g, n, P(w), P(hw), E.dvec + E.off_sig(), P(z), E.partials, E.s);
+      E.reduce_rows(E.partials, n, onb, E.g.w, E.dvec + E.off_zz(), true);
+      if (need_full) {
+        if (mean_abs) dscratch = pool.get();
+        E.mix(P(w), nullptr, 0.0, E.dmat[4], -1.0, P(hw), 1.0, 0, dscratch ? P(dscratch) : nullptr,
+              E.dvec + E.off_dd());
+        if (mean_abs) {
+          launch_abs_sum(E.g, n, P(dscratch), E.partials, E.s);
+          E.reduce_rows(E.partials, n, onb, 1.0, E.dvec + E.off_abs(), true);
+        }
+      }
+    }
+    if (history_valid) {
+      launch_bb(E.g, n, P(w), P(prev_w), P(z), P(prev_z), E.partials, E.s);
+      E.reduce_rows(E.partials, 3 * n, onb, E.g.w, E.dvec + E.off_ss(), true);
+    }
+    E.fetch_all();
+    const double* hv = E.hvec;
+    if ((full_grad || need_full) && hv[E.off_scal() + Engine::S_SYM + 1] > 1e-10)
+      throw Error(PO_EINVAL, "stiefel_gradient: <(HU)^T U> is not symmetric; inconsistent H or U");
+    double znorm2 = 0.0, grad_norm = -1.0, mean_abs_v = -1.0;
+    if (full_grad) {
+      for (int i = 0; i < n; ++i) znorm2 += hv[E.off_dd() + i];
+      grad_norm = std::sqrt(std::max(0.0, znorm2));
+      if (mean_abs && need_full) {
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) acc += hv[E.off_abs() + i];
+        mean_abs_v = acc / ((double)n * ngd);
+      }
+    } else {
+      for (int i = 0; i < n; ++i) znorm2 += hv[E.off_zz() + i];
+      if (need_full) {
+        double acc = 0.0, abs_acc = 0.0;
+        for (int i = 0; i < n; ++i) {
+          acc += hv[E.off_dd() + i];
+          if (mean_abs) abs_acc += hv[E.off_abs() + i];
+        }
+        grad_norm = std::sqrt(std::max(0.0, acc));
+        if (mean_abs) mean_abs_v = abs_acc / ((double)n * ngd);
+      }
+    }
+    if (orth_iter && grad_style) {  // check_convergence, optimizer.cpp:126-148
+      const bool conv = p.convergence_mode == PO_CONV_GRAD_NORM
+                            ? (grad_norm >= 0.0 && grad_norm < p.grad_tol)
+                            : (mean_abs_v >= 0.0 && mean_abs_v < p.mean_abs_tol);
+      if (conv) {
+        converged = true;
+        break;
+      }
+    }
+    if (znorm2 == 0.0) {
+      converged = true;
+      break;
+    }
+
+    // ---- BB step, optimizer.cpp:376-411
+    double tau_raw;
+    if (history_valid) {
+      double tr_ss = 0.0, tr_yy = 0.0, sy_abs = 0.0, sy_tr = 0.0;
+      for (int i = 0; i < n; ++i) {
+        tr_ss += hv[E.off_ss() + i];
+        tr_yy += hv[E.off_yy() + i];
+        sy_abs += std::abs(hv[E.off_sy() + i]);
+        sy_tr += hv[E.off_sy() + i];
+      }
+      const double tr_abs_sy = p.bb_trace_abs == PO_TRACE_DIAG_ABS ? sy_abs : std::abs(sy_tr);
+      const double raw = use_bb1(p.bb_variant, l) ? tr_ss / tr_abs_sy : tr_abs_sy / tr_yy;
+      tau_raw = clamp_tau(raw, p);
+    } else {
+      tau_raw = clamp_tau(std::min(p.tau_max, 1.0 / std::sqrt(znorm2)), p);
+    }
+
+    po_record rec{};
+    rec.level = 0;
+    rec.iter = l;
+    rec.grad_norm = grad_norm >= 0.0 ? grad_norm : std::sqrt(std::max(0.0, znorm2));
+
+    if (!orth_iter) {  // raw step, optimizer.cpp:419-444
+      double tau = tau_raw;
+      if (last_accepted_tau > 0.0) tau = std::min(tau, 5.0 * last_accepted_tau);
+      BRef wn = pool.get();
+      launch_lincomb(E.g, n, P(w), -tau, P(z), P(wn), E.s);
+      prev_w = w;
+      prev_z = z;
+      w = wn;
+      history_valid = true;
+      state = make_state(w);
+      BRef hn = pool.get();
+      E.apply_h(P(w), P(hn), state->v_local);
+      hw = hn;
+      sig_valid = true;
+      --steps_until_orth;
+      rec.tau = tau;
+      rec.energy = orth_energies.back();
+    } else {  // backtracked orthogonalization step, optimizer.cpp:446-541
+      bool accepted = false;
+      int s = 0;
+      double tau = 0.0;
+      OrthOut orth;
+      BRef wt, hwt;
+      SRef tstate;
+      EnergyParts te;
+      for (s = 0; s <= p.max_backtracks; ++s) {
+        tau = tau_raw * std::pow(p.delta, s);
+        if (s > 0 && tau < p.tau_min) break;
+        wt = pool.get();
+        BRef rep;
+        auto scratch = [&]() -> double* {
+          rep = pool.get();
+          return P(rep);
+        };
+        if (!orthonormalize_dev(E, P(w), P(z), -tau, P(wt), scratch, p.verify_orthonormality != 0,
+                                orth))
+          continue;  // DegenerateSetError -> NaN trial energy
+        tstate = make_state(wt);
+        hwt = pool.get();
+        te = apply_and_energy(wt, hwt, *tstate);
+        if (std::isfinite(te.total) && te.total <= nm_c - p.rho1 * tau * znorm2) {
+          accepted = true;
+          break;
+        }
+      }
+      if (!accepted) {  // recovery, optimizer.cpp:485-508
+        if (++failed_searches > 8) {
+          char buf[200];
+          std::snprintf(buf, sizeof buf,
+                        "line search stagnated at level %d iteration %d (%d trials, C = %.17g)", 0,
+                        l, s, nm_c);
+          return fail(PO_OUT_STAGNATION, buf);
+        }
+        w = recovery_w;
+        state = recovery_state;
+        BRef hn = pool.get();
+        E.apply_h(P(w), P(hn), state->v_local);
+        hw = hn;
+        sig_valid = true;
+        history_valid = false;
+        prev_w.reset();
+        prev_z.reset();
+        steps_until_orth = 0;
+        continue;
+      }
+      failed_searches = 0;
+      const double c_before = nm_c, q_before = nm_q;
+      nm_q = p.eta * q_before + 1.0;
+      nm_c = (p.eta * q_before * c_before + te.total) / nm_q;
+      if (r->accepted && r->n_accepted < r->cap) {
+        double* a = r->accepted + 9 * (size_t)r->n_accepted;
+        const double v[9] = {0, (double)l, te.total, c_before, nm_c, q_before, nm_q, tau, znorm2};
+        std::memcpy(a, v, sizeof v);
+      }
+      r->n_accepted++;
+      if (te.total > nm_c + 1e-9 * (1.0 + std::abs(te.total)))
+        return fail(PO_OUT_NUMERICAL_FAILURE, "nonmonotone ledger violated (C < E after update)");
+      prev_w = w;
+      prev_z = z;
+      w = wt;
+      state = tstate;
+      hw = hwt;
+      sig_valid = true;
+      history_valid = true;
+      last_accepted_tau = tau;
+      set_energy(te);
+      orth_energies.push_back(te.total);
+      rec.did_orth = 1;
+      rec.tau = tau;
+      rec.backtracks = s;
+      rec.offdiag_max = orth.offdiag_max;
+      rec.energy = te.total;
+      steps_until_orth = n_org - 1;
+      if (p.n_diag > 0 && (l + 1 - last_rotation_iter) >= p.n_diag && !full_grad) {
+        // subspace diagonalization, optimizer.cpp:550-561 / manifold.cpp:218-247
+        sigma(w, hw);
+        launch_syev(n, E.dmat[4], E.syev_work, E.dmat[6], E.dmat[5], 1, E.scal() + Engine::S_EIG,
+                    E.s);
+        E.fetch(E.off_scal(), 64);
+        if (E.hvec[E.off_scal() + Engine::S_EIG] > 1e-8)
+          throw Error(PO_EINVAL, "subspace_rotate: Sigma asymmetry exceeds tolerance");
+        BRef wr = pool.get(), hr = pool.get();
+        E.mix(P(w), nullptr, 0.0, E.dmat[5], 1.0, nullptr, 0.0, 0, P(wr), nullptr);
+        E.mix(P(hw), nullptr, 0.0, E.dmat[5], 1.0, nullptr, 0.0, 0, P(hr), nullptr);
+        w = wr;
+        hw = hr;
+        last_rotation_iter = l + 1;
+        rec.did_diag = 1;
+        history_valid = false;
+        sig_valid = false;
+        prev_w.reset();
+        prev_z.reset();
+      }
+      recovery_w = w;
+      recovery_state = state;
+      trace_eigs(w, hw);
+      if (p.convergence_mode == PO_CONV_ENERGY_CHANGE && orth_energies.size() >= 4) {
+        double acc = 0.0;
+        const size_t m = orth_energies.size();
+        for (size_t k = 0; k < 3; ++k) {
+          const double e_new = orth_energies[m - 1 - k], e_old = orth_energies[m - 2 - k];
+          acc += std::abs(e_old - e_new) / (std::abs(e_old) + 1.0) / (double)std::max(1, n_org);
+        }
+        if (acc / 3.0 < p.energy_tol) converged = true;
+      }
+    }
+    E.sync();
+    rec.wall_ms = 1e3 * std::chrono::duration<double>(Clock::now() - t0).count();
+    if (r->n_records < r->cap) r->records[r->n_records] = rec;
+    r->n_records++;
+  }
+  r->outcome = converged ? PO_OUT_CONVERGED : PO_OUT_MAX_ITERATIONS;
+  return r->outcome;
+}
+
+}  // namespace
+
+}  // namespace po
+
+using po::Engine;
+using po::Error;
+
+extern "C" {
+
+void po_default_params(po_params* p) {  // optimizer.hpp:22-46
+  std::memset(p, 0, sizeof *p);
+  p->algorithm = PO_ALG_OPT_PAR_MOD;
+  p->bb_variant = PO_BB1;
+  p->bb_trace_abs = PO_TRACE_DIAG_ABS;
+  p->convergence_mode = PO_CONV_GRAD_NORM;
+  p->rho1 = 1e-4;
+  p->delta = 0.1;
+  p->eta = 0.85;
+  p->n_diag = 100;
+  p->n_org = 1;
+  p->max_inner = 10000;
+  p->max_backtracks = 20;
+  p->tau_min = 1e-10;
+  p->tau_max = 1e3;
+  p->grad_tol = 1e-6;
+  p->mean_abs_tol = 5e-9;
+  p->energy_tol = 1e-13;
+  p->verify_orthonormality = 1;
+  p->hartree = 1;
+  p->xc = 1;
+  p->trace_sigma_eigs = 0;
+  p->poisson_warm_start = 0;
+}
+
+int po_orthonormalize(po_engine* h, int in, int out, int measure, double* pre_gram,
+                      double* post_deviation, int* used_fallback) {
+  if (!h || !h->e) return PO_EINVAL;
+  Engine& E = *h->e;
+  try {
+    if (in == out) throw Error(PO_EINVAL, "orthonormalize: in and out must differ");
+    int tmp = -1;
+    auto scratch = [&]() -> double* {
+      tmp = E.alloc_block();
+      return E.blk(tmp);
+    };
+    po::OrthOut o;
+    const bool ok = po::orthonormalize_dev(E, E.blk(in), nullptr, 0.0, E.blk(out), scratch,
+                                           measure != 0, o);
+    if (tmp >= 0) E.free_block(tmp);
+    if (pre_gram) {
+      PO_CUDA(cudaMemcpyAsync(E.hmat, E.dmat[0], sizeof(double) * E.N * E.N,
+                              cudaMemcpyDeviceToHost, E.s));
+      E.sync();
+      std::memcpy(pre_gram, E.hmat, sizeof(double) * E.N * E.N);
+    }
+    if (!ok) throw Error(PO_EDEGENERATE, "orthonormalize: orbital set is numerically rank deficient");
+    if (post_deviation) *post_deviation = o.post_dev;
+    if (used_fallback) *used_fallback = o.fallback ? 1 : 0;
+    E.sync();
+  } catch (const Error& ex) {
+    h->err = ex.what();
+    return ex.code;
+  } catch (const std::exception& ex) {
+    h->err = ex.what();
+    return PO_EINVAL;
+  }
+  return PO_OK;
+}
+
+int po_solve(po_engine* h, const po_params* p, int w_handle, po_result* r) {
+  if (!h || !h->e || !p || !r) return PO_EINVAL;
+  Engine& E = *h->e;
+  const auto t0 = std::chrono::steady_clock::now();
+  r->n_records = r->n_accepted = 0;
+  r->cg_iters_total = 0;
+  r->message[0] = 0;
+  r->outcome = PO_OUT_MAX_ITERATIONS;
+  r->e_kinetic = r->e_external = r->e_hartree = r->e_xc = r->e_total = 0.0;
+  try {
+    // OptimizerParams::validate, optimizer.cpp:43-58
+    if (!(p->rho1 > 0.0)) throw Error(PO_EINVAL, "optimizer: rho1 must be positive");
+    if (!(p->delta > 0.0 && p->delta < 1.0)) throw Error(PO_EINVAL, "optimizer: delta must lie in (0, 1)");
+    if (!(p->eta >= 0.0 && p->eta < 1.0)) throw Error(PO_EINVAL, "optimizer: eta must lie in [0, 1)");
+    if (p->n_diag < 0) throw Error(PO_EINVAL, "optimizer: n_diag must be >= 0 (0 disables)");
+    if (p->n_org < 1) throw Error(PO_EINVAL, "optimizer: n_org must be >= 1");
+    if (p->max_inner < 1) throw Error(PO_EINVAL, "optimizer: max_inner must be >= 1");
+    if (p->max_backtracks < 0) throw Error(PO_EINVAL, "optimizer: max_backtracks must be >= 0");
+    if (!(p->tau_min > 0.0) || !(p->tau_max >= p->tau_min))
+      throw Error(PO_EINVAL, "optimizer: require 0 < tau_min <= tau_max");
+    if (!(p->grad_tol > 0.0)) throw Error(PO_EINVAL, "optimizer: grad_tol must be positive");
+    if (!(p->mean_abs_tol > 0.0)) throw Error(PO_EINVAL, "optimizer: mean_abs_tol must be positive");
+    if (!(p->energy_tol > 0.0)) throw Error(PO_EINVAL, "optimizer: energy_tol must be positive");
+    // run_single_level: u0 must be orthonormal (optimizer.cpp:601-603)
+    E.gram(E.blk(w_handle), nullptr, 0.0, E.blk(w_handle), nullptr, 0.0, 1, E.dmat[2]);
+    po::launch_matrix_stats(E.N, E.dmat[2], E.scal() + Engine::S_MSTAT2, E.s);
+    E.fetch(E.off_scal(), 64);
+    if (E.hvec[E.off_scal() + Engine::S_MSTAT2] > 1e-8)
+      throw Error(PO_EINVAL, "solver: initial orbital set is not orthonormal");
+
+    po::Solver S(E, *p, r);
+    std::shared_ptr<int> w(new int(w_handle), [](int* q) { delete q; });
+    S.run(w);
+    // finalize, optimizer.cpp:581-597: full Stiefel gradient at the final iterate
+    po::SRef st = S.make_state(w);
+    po::BRef hw = S.pool.get();
+    E.apply_h(E.blk(*w), E.blk(*hw), st->v_local);
+    S.sigma(w, hw);
+    E.mix(E.blk(*w), nullptr, 0.0, E.dmat[4], -1.0, E.blk(*hw), 1.0, 0, nullptr,
+          E.dvec + E.off_dd());
+    E.fetch_all();
+    if (E.hvec[E.off_scal() + Engine::S_SYM + 1] > 1e-10)
+      throw Error(PO_EINVAL, "stiefel_gradient: <(HU)^T U> is not symmetric; inconsistent H or U");
+    double acc = 0.0;
+    for (int i = 0; i < E.N; ++i) acc += E.hvec[E.off_dd() + i];
+    r->final_grad_norm = std::sqrt(std::max(0.0, acc));
+    if (*w != w_handle)
+      PO_CUDA(cudaMemcpyAsync(E.blk(w_handle), E.blk(*w), sizeof(double) * E.N * E.g.ld,
+                              cudaMemcpyDeviceToDevice, E.s));
+    E.sync();
+  } catch (const Error& ex) {
+    h->err = ex.what();
+    std::snprintf(r->message, sizeof r->message, "%s", ex.what());
+    return ex.code;
+  } catch (const std::exception& ex) {
+    h->err = ex.what();
+    return PO_EINVAL;
+  }
+  r->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return PO_OK;
+}
+
+}  // extern "C"

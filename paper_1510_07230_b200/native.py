@@ -1,0 +1,414 @@
+"""ctypes binding of the C ABI (include/parorb_gpu.h) and a thin Python mirror
+of the reference operator / solver API (energy.hpp, manifold.hpp,
+optimizer.hpp). Every call goes to the sm_100a kernels in libparorb_b200.so;
+there is no CPU fallback — a missing library or GPU raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libparorb_b200.so")
+_lib = None
+
+PO_OK, PO_EINVAL, PO_EDEGENERATE, PO_ESOLVER, PO_ESTAGNATION, PO_ECUDA, PO_ENCCL, PO_ENOMEM = range(8)
+PO_VEXT, PO_RHO, PO_VH, PO_VXC, PO_VLOCAL = range(5)
+PO_COMM_NONE, PO_COMM_NCCL, PO_COMM_THREADS = range(3)
+ALGORITHMS = {"optm_qr": 0, "opt_par": 1, "opt_par_mod": 2}
+OUTCOMES = {0: "converged", 1: "max_iterations", 2: "stagnation", 3: "numerical_failure"}
+CONVERGENCE = {"grad_norm": 0, "mean_abs": 1, "energy_change": 2}
+BB = {"bb1": 0, "bb2": 1, "alternate": 2}
+
+
+class InvalidArgument(ValueError):
+    """errors.hpp:13 InvalidArgument."""
+
+
+class DegenerateSetError(RuntimeError):
+    """errors.hpp:19 DegenerateSetError."""
+
+
+class SolverError(RuntimeError):
+    """errors.hpp:36 SolverError."""
+
+
+class StagnationError(RuntimeError):
+    """errors.hpp:25 StagnationError."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA / NCCL / allocation failure (no reference counterpart)."""
+
+
+_ERRORS = {PO_EINVAL: InvalidArgument, PO_EDEGENERATE: DegenerateSetError, PO_ESOLVER: SolverError,
+           PO_ESTAGNATION: StagnationError}
+
+
+class GridDesc(C.Structure):
+    _fields_ = [("n", C.c_int64 * 3), ("extent", C.c_double * 3)]
+
+
+class DistDesc(C.Structure):
+    _fields_ = [("rank", C.c_int), ("size", C.c_int), ("kind", C.c_int), ("handle", C.c_void_p),
+                ("device", C.c_int)]
+
+
+class Params(C.Structure):
+    _fields_ = [("algorithm", C.c_int), ("bb_variant", C.c_int), ("bb_trace_abs", C.c_int),
+                ("convergence_mode", C.c_int), ("rho1", C.c_double), ("delta", C.c_double),
+                ("eta", C.c_double), ("n_diag", C.c_int), ("n_org", C.c_int), ("max_inner", C.c_int),
+                ("max_backtracks", C.c_int), ("tau_min", C.c_double), ("tau_max", C.c_double),
+                ("grad_tol", C.c_double), ("mean_abs_tol", C.c_double), ("energy_tol", C.c_double),
+                ("verify_orthonormality", C.c_int), ("hartree", C.c_int), ("xc", C.c_int),
+                ("trace_sigma_eigs", C.c_int), ("poisson_warm_start", C.c_int)]
+
+
+class Record(C.Structure):
+    _fields_ = [("level", C.c_int), ("iter", C.c_int), ("energy", C.c_double),
+                ("grad_norm", C.c_double), ("tau", C.c_double), ("backtracks", C.c_int),
+                ("did_orth", C.c_int), ("did_diag", C.c_int), ("offdiag_max", C.c_double),
+                ("wall_ms", C.c_double)]
+
+
+class Result(C.Structure):
+    _fields_ = [("cap", C.c_int), ("records", C.POINTER(Record)), ("accepted", C.POINTER(C.c_double)),
+                ("sigma_eigs", C.POINTER(C.c_double)), ("n_records", C.c_int), ("n_accepted", C.c_int),
+                ("outcome", C.c_int), ("cg_iters_total", C.c_int64), ("e_kinetic", C.c_double),
+                ("e_external", C.c_double), ("e_hartree", C.c_double), ("e_xc", C.c_double),
+                ("e_total", C.c_double), ("final_grad_norm", C.c_double), ("wall_seconds", C.c_double),
+                ("par_seconds", C.c_double), ("sync_seconds", C.c_double), ("message", C.c_char * 200)]
+
+
+_SIGS = {
+    "po_abi_version": ([], C.c_int),
+    "po_create": ([C.POINTER(GridDesc), C.c_int, C.c_double, C.POINTER(DistDesc), C.POINTER(C.c_void_p)], C.c_int),
+    "po_destroy": ([C.c_void_p], C.c_int),
+    "po_last_error": ([C.c_void_p], C.c_char_p),
+    "po_local_slab": ([C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
+    "po_solver_bytes": ([C.POINTER(GridDesc), C.c_int, C.c_int], C.c_int64),
+    "po_stream": ([C.c_void_p], C.c_void_p),
+    "po_synchronize": ([C.c_void_p], C.c_int),
+    "po_thread_group_create": ([C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+    "po_thread_group_destroy": ([C.c_void_p], C.c_int),
+    "po_alloc_block": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
+    "po_free_block": ([C.c_void_p, C.c_int], C.c_int),
+    "po_upload_block": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
+    "po_download_block": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
+    "po_copy_block": ([C.c_void_p, C.c_int, C.c_int], C.c_int),
+    "po_set_field": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
+    "po_get_field": ([C.c_void_p, C.c_int, C.c_void_p], C.c_int),
+    "po_external_potential": ([C.c_void_p, C.c_void_p, C.c_int], C.c_int),
+    "po_gaussian_potential": ([C.c_void_p, C.c_void_p, C.c_int], C.c_int),
+    "po_random_block": ([C.c_void_p, C.c_int, C.c_uint64], C.c_int),
+    "po_build_hamiltonian": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
+                              C.POINTER(C.c_double), C.POINTER(C.c_int)], C.c_int),
+    "po_apply_hamiltonian": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "po_total_energy": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p], C.c_int),
+    "po_laplacian": ([C.c_void_p, C.c_int, C.c_int], C.c_int),
+    "po_gram": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p], C.c_int),
+    "po_mix": ([C.c_void_p, C.c_int, C.c_void_p, C.c_int], C.c_int),
+    "po_orthonormalize": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_double),
+                           C.POINTER(C.c_int)], C.c_int),
+    "po_diagonal_residuals": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
+    "po_stiefel_gradient": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
+    "po_subspace_rotate": ([C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "po_linear_combination": ([C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int], C.c_int),
+    "po_bb_products": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                        C.c_void_p], C.c_int),
+    "po_default_params": ([C.POINTER(Params)], None),
+    "po_solve": ([C.c_void_p, C.POINTER(Params), C.c_int, C.POINTER(Result)], C.c_int),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", _PKG, "-j8"], check=True)
+    return LIB_PATH
+
+
+def lib():
+    """Load libparorb_b200.so (raises if it is missing — there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `make -C {_PKG}` (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _dp(a: np.ndarray):
+    if a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise InvalidArgument("arrays must be C-contiguous float64")
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class Engine:
+    """One rank's device-resident state (po_engine)."""
+
+    def __init__(self, n, extent, n_orbitals: int, occupation: float = 1.0, rank: int = 0,
+                 size: int = 1, comm_kind: int = PO_COMM_NONE, comm_handle=None, device: int = -1):
+        L = lib()
+        self._lib = L
+        g = GridDesc((C.c_int64 * 3)(*[int(x) for x in n]), (C.c_double * 3)(*[float(x) for x in extent]))
+        self._keep = comm_handle
+        if isinstance(comm_handle, (bytes, bytearray)):
+            self._hbuf = C.create_string_buffer(bytes(comm_handle), len(comm_handle))
+            handle = C.cast(self._hbuf, C.c_void_p)
+        else:
+            handle = comm_handle
+        d = DistDesc(rank, size, comm_kind, handle, device)
+        h = C.c_void_p()
+        rc = L.po_create(C.byref(g), int(n_orbitals), float(occupation), C.byref(d), C.byref(h))
+        self.h = h
+        if rc != PO_OK:
+            msg = L.po_last_error(h).decode() if h else "po_create failed"
+            L.po_destroy(h)
+            self.h = None
+            raise _err(rc, msg)
+        self.n = tuple(int(x) for x in n)
+        self.extent = tuple(float(x) for x in extent)
+        self.N = int(n_orbitals)
+        self.occupation = float(occupation)
+        z0, nz, ngl = C.c_int64(), C.c_int64(), C.c_int64()
+        L.po_local_slab(h, C.byref(z0), C.byref(nz), C.byref(ngl))
+        self.z0, self.nz, self.ngl = z0.value, nz.value, ngl.value
+
+    def close(self):
+        if self.h:
+            self._lib.po_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, rc):
+        if rc != PO_OK:
+            raise _err(rc, self._lib.po_last_error(self.h).decode())
+
+    @property
+    def stream(self) -> int:
+        return self._lib.po_stream(self.h) or 0
+
+    def synchronize(self):
+        self._chk(self._lib.po_synchronize(self.h))
+
+    # ---- blocks
+    def alloc(self) -> int:
+        b = C.c_int()
+        self._chk(self._lib.po_alloc_block(self.h, C.byref(b)))
+        return b.value
+
+    def free(self, b: int):
+        self._chk(self._lib.po_free_block(self.h, b))
+
+    def upload(self, b: int, host: np.ndarray):
+        host = np.ascontiguousarray(host, dtype=np.float64)
+        if host.size != self.N * self.ngl:
+            raise InvalidArgument("block shape mismatch")
+        self._chk(self._lib.po_upload_block(self.h, b, _dp(host)))
+
+    def download(self, b: int, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.N, self.ngl))
+        self._chk(self._lib.po_download_block(self.h, b, _dp(out)))
+        return out
+
+    def block_from(self, host: np.ndarray) -> int:
+        b = self.alloc()
+        self.upload(b, host)
+        return b
+
+    def copy(self, dst: int, src: int):
+        self._chk(self._lib.po_copy_block(self.h, dst, src))
+
+    def random_block(self, b: int, seed: int):
+        self._chk(self._lib.po_random_block(self.h, b, C.c_uint64(seed)))
+
+    # ---- fields
+    def set_field(self, f: int, host: np.ndarray):
+        self._chk(self._lib.po_set_field(self.h, f, _dp(np.ascontiguousarray(host, dtype=np.float64))))
+
+    def get_field(self, f: int) -> np.ndarray:
+        out = np.empty(self.ngl)
+        self._chk(self._lib.po_get_field(self.h, f, _dp(out)))
+        return out
+
+    def external_potential(self, atoms):
+        a = np.ascontiguousarray(np.asarray(atoms, dtype=np.float64).reshape(-1, 5))
+        self._chk(self._lib.po_external_potential(self.h, _dp(a) if a.size else None, a.shape[0]))
+
+    def gaussian_potential(self, wells):
+        a = np.ascontiguousarray(np.asarray(wells, dtype=np.float64).reshape(-1, 5))
+        self._chk(self._lib.po_gaussian_potential(self.h, _dp(a), a.shape[0]))
+
+    # ---- operators
+    def build_hamiltonian(self, u: int, hartree=True, xc=True):
+        eh, exc, it = C.c_double(), C.c_double(), C.c_int()
+        self._chk(self._lib.po_build_hamiltonian(self.h, u, int(hartree), int(xc), C.byref(eh),
+                                                 C.byref(exc), C.byref(it)))
+        return eh.value, exc.value, it.value
+
+    def apply_hamiltonian(self, u: int, out: int = -1):
+        s, k, e = np.empty(self.N), np.empty(self.N), np.empty(self.N)
+        self._chk(self._lib.po_apply_hamiltonian(self.h, u, out, _dp(s), _dp(k), _dp(e)))
+        return s, k, e
+
+    def total_energy(self, u: int, hartree=True, xc=True) -> dict:
+        out = np.empty(5)
+        self._chk(self._lib.po_total_energy(self.h, u, int(hartree), int(xc), _dp(out)))
+        return dict(zip(("kinetic", "external", "hartree", "xc", "total"), out.tolist()))
+
+    def laplacian(self, u: int, out: int):
+        self._chk(self._lib.po_laplacian(self.h, u, out))
+
+    def gram(self, a: int, b: int) -> np.ndarray:
+        g = np.empty((self.N, self.N))
+        self._chk(self._lib.po_gram(self.h, a, b, _dp(g)))
+        return g
+
+    def mix(self, inp: int, m: np.ndarray, out: int):
+        self._chk(self._lib.po_mix(self.h, inp, _dp(np.ascontiguousarray(m, dtype=np.float64)), out))
+
+    def orthonormalize(self, inp: int, out: int, measure: bool = True):
+        pre = np.empty((self.N, self.N))
+        dev, fb = C.c_double(), C.c_int()
+        self._chk(self._lib.po_orthonormalize(self.h, inp, out, int(measure), _dp(pre), C.byref(dev),
+                                              C.byref(fb)))
+        return pre, dev.value, bool(fb.value)
+
+    def diagonal_residuals(self, u: int, hu: int, z: int):
+        s, zz = np.empty(self.N), np.empty(self.N)
+        self._chk(self._lib.po_diagonal_residuals(self.h, u, hu, z, _dp(s), _dp(zz)))
+        return s, zz
+
+    def stiefel_gradient(self, u: int, hu: int):
+        sig, dd = np.empty((self.N, self.N)), np.empty(self.N)
+        self._chk(self._lib.po_stiefel_gradient(self.h, u, hu, _dp(sig), _dp(dd)))
+        return sig, dd
+
+    def subspace_rotate(self, w: int, sigma: np.ndarray):
+        gam, p = np.empty(self.N), np.empty((self.N, self.N))
+        self._chk(self._lib.po_subspace_rotate(self.h, w, _dp(np.ascontiguousarray(sigma)), _dp(gam), _dp(p)))
+        return gam, p
+
+    def linear_combination(self, a: int, s: float, b: int, out: int):
+        self._chk(self._lib.po_linear_combination(self.h, a, float(s), b, out))
+
+    def bb_products(self, w: int, wp: int, z: int, zp: int):
+        ss, sy, yy = np.empty(self.N), np.empty(self.N), np.empty(self.N)
+        self._chk(self._lib.po_bb_products(self.h, w, wp, z, zp, _dp(ss), _dp(sy), _dp(yy)))
+        return ss, sy, yy
+
+    # ---- solver
+    def solve(self, w: int, algorithm="opt_par_mod", hartree=True, xc=True, trace_eigs=False,
+              warm_start=False, **over) -> "SolveResult":
+        p = default_params()
+        p.algorithm = ALGORITHMS[algorithm]
+        p.hartree, p.xc = int(hartree), int(xc)
+        p.trace_sigma_eigs = int(trace_eigs)
+        p.poisson_warm_start = int(warm_start)
+        for k, v in over.items():
+            if k == "convergence_mode":
+                v = CONVERGENCE[v]
+            elif k == "bb_variant":
+                v = BB[v]
+            elif k == "bb_trace_abs":
+                v = 1 if v == "abs_trace" else 0
+            elif k == "verify_orthonormality":
+                v = int(v)
+            setattr(p, k, v)
+        cap = p.max_inner + 1
+        recs = (Record * cap)()
+        acc = np.zeros(cap * 9)
+        eigs = np.full(cap * self.N, np.nan)
+        r = Result()
+        r.cap = cap
+        r.records = recs
+        r.accepted = acc.ctypes.data_as(C.POINTER(C.c_double))
+        r.sigma_eigs = eigs.ctypes.data_as(C.POINTER(C.c_double)) if trace_eigs else C.POINTER(C.c_double)()
+        rc = self._lib.po_solve(self.h, C.byref(p), w, C.byref(r))
+        if rc != PO_OK:
+            raise _err(rc, self._lib.po_last_error(self.h).decode() or r.message.decode())
+        nrec = min(r.n_records, cap)
+        records = [dict(level=x.level, iter=x.iter, energy=x.energy, grad_norm=x.grad_norm, tau=x.tau,
+                        backtracks=x.backtracks, did_orth=x.did_orth, did_diag=x.did_diag,
+                        offdiag_max=x.offdiag_max, wall_ms=x.wall_ms) for x in recs[:nrec]]
+        return SolveResult(
+            records=records, accepted=acc[: 9 * min(r.n_accepted, cap)].reshape(-1, 9),
+            sigma_eigs=eigs[: self.N * nrec].reshape(-1, self.N) if trace_eigs else None,
+            outcome=OUTCOMES[r.outcome], message=r.message.decode(),
+            energy=dict(kinetic=r.e_kinetic, external=r.e_external, hartree=r.e_hartree, xc=r.e_xc,
+                        total=r.e_total),
+            final_grad_norm=r.final_grad_norm, cg_iters_total=r.cg_iters_total,
+            wall_seconds=r.wall_seconds)
+
+
+@dataclass
+class SolveResult:
+    """SolveResult, optimizer.hpp:98-112 (orbitals stay on the device)."""
+    records: list
+    accepted: np.ndarray
+    sigma_eigs: np.ndarray | None
+    outcome: str
+    message: str
+    energy: dict
+    final_grad_norm: float
+    cg_iters_total: int
+    wall_seconds: float
+    extra: dict = field(default_factory=dict)
+
+
+def default_params() -> Params:
+    p = Params()
+    lib().po_default_params(C.byref(p))
+    return p
+
+
+def _err(rc: int, msg: str) -> Exception:
+    cls = _ERRORS.get(rc, DeviceError)
+    return cls(f"[{rc}] {msg}")
+
+
+def engine_for(spec, rank: int = 0, size: int = 1, comm_kind: int = PO_COMM_NONE, comm_handle=None,
+               device: int = -1) -> Engine:
+    """Engine with the spec's grid, orbital count, occupation and V_ext."""
+    e = Engine(spec.n, spec.extent, spec.n_orbitals, spec.occupation, rank, size, comm_kind, comm_handle,
+               device)
+    if spec.wells:
+        e.gaussian_potential(spec.wells)
+    else:
+        e.external_potential(spec.atoms)
+    return e
+
+
+def random_orthonormal(e: Engine, seed: int) -> int:
+    """tests/problems.hpp:59-68 on the device: Rng(seed) normals (the reference's exact
+    bits), then Orth (Cholesky-QR on the device). Returns a block handle."""
+    raw = e.alloc()
+    e.random_block(raw, seed)
+    w = e.alloc()
+    e.orthonormalize(raw, w, True)
+    e.free(raw)
+    return w
+
+
+def format_log_row(r: dict) -> str:
+    """driver.cpp:136-142 with wall_ms zeroed."""
+    g = lambda x: "%.17g" % x  # noqa: E731
+    return "%d,%d,%s,%s,%s,%d,%d,%d,%s,0.000" % (r["level"], r["iter"], g(r["energy"]), g(r["grad_norm"]),
+                                               g(r["tau"]), r["backtracks"], r["did_orth"], r["did_diag"],
+                                               g(r["offdiag_max"]))

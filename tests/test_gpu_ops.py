@@ -1,0 +1,200 @@
+"""Operator-level parity: CUDA path (through the C ABI) vs the C restatement
+(oracle/port), which is itself pinned byte-for-byte to the unmodified
+reference (tests/test_oracle_port.py). fp64 throughout; tolerances stated per
+check (the GPU sums in a different order and uses FMA, so agreement is to
+round-off, not bitwise)."""
+import numpy as np
+import pytest
+
+from paper_1510_07230_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+SPECS = [
+    configs.small_molecule(16, 4, L=8.0),
+    configs.ProblemSpec("skew", (12, 10, 14), (7.0, 6.0, 9.0),
+                        [(3.0, 2.5, 4.0, 3.0, 1.0), (4.5, 3.2, 5.5, 1.0, 0.7)], 5),
+]
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b)) / max(1e-300, np.max(np.abs(b))))
+
+
+@pytest.fixture(params=SPECS, ids=[s.name for s in SPECS])
+def setup(request, port, native):
+    spec = request.param
+    u0 = port.random_orthonormal(spec)
+    e = native.engine_for(spec)
+    yield spec, u0, e
+    e.close()
+
+
+def test_random_block_bits(port, native):
+    spec = SPECS[1]
+    e = native.engine_for(spec)
+    b = e.alloc()
+    e.random_block(b, 42)
+    got = e.download(b)
+    want = port.random_normals(42, spec.n_orbitals * spec.num_points).reshape(spec.n_orbitals, -1)
+    assert np.array_equal(got, want)  # same generator, same bits (rng.hpp:13-41)
+    e.close()
+
+
+def test_external_potential(setup, port, native):
+    spec, _, e = setup
+    got = e.get_field(native.PO_VEXT)
+    assert rel(got, port.external_potential(spec)) < 1e-14
+
+
+def test_laplacian(setup, port, native):
+    spec, u0, e = setup
+    u = e.block_from(u0)
+    out = e.alloc()
+    e.laplacian(u, out)
+    got = e.download(out)
+    want = np.stack([port.laplacian(spec, x) for x in u0])
+    assert rel(got, want) < 1e-13
+
+
+def test_build_hamiltonian_and_apply(setup, port, native):
+    spec, u0, e = setup
+    u = e.block_from(u0)
+    eh, exc, iters = e.build_hamiltonian(u, True, True)
+    st = port.build_hamiltonian(spec, u0)
+    assert rel(e.get_field(native.PO_RHO), st["rho"]) < 1e-14
+    assert rel(e.get_field(native.PO_VXC), st["v_xc"]) < 1e-13
+    # both CG solves stop at ||r|| <= 1e-10 ||b|| (energy.cpp:105-143)
+    assert rel(e.get_field(native.PO_VH), st["v_h"]) < 1e-8
+    assert rel(e.get_field(native.PO_VLOCAL), st["v_local"]) < 1e-8
+    assert iters > 0 and abs(iters - st["cg_iters"]) <= max(3, st["cg_iters"] // 10)
+    en, kin, ext = port.total_energy(spec, u0, st)
+    assert abs(eh - en["hartree"]) < 1e-9 * max(1.0, abs(en["hartree"]))
+    assert abs(exc - en["xc"]) < 1e-12 * max(1.0, abs(en["xc"]))
+    hu = e.alloc()
+    sig, k, x = e.apply_hamiltonian(u, hu)
+    want_hu = port.apply_hamiltonian(spec, e.get_field(native.PO_VLOCAL), u0)
+    assert rel(e.download(hu), want_hu) < 1e-12
+    assert np.allclose(k, kin, rtol=1e-11, atol=1e-12)
+    assert np.allclose(x, ext, rtol=1e-11, atol=1e-12)
+    wq = np.prod(spec.spacing)
+    assert np.allclose(sig, wq * np.einsum("ip,ip->i", want_hu, u0), rtol=1e-10, atol=1e-12)
+    tot = e.total_energy(u)
+    assert abs(tot["total"] - en["total"]) < 1e-8
+
+
+def test_gram_mix(setup, port, native):
+    spec, u0, e = setup
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal(u0.shape)
+    ba, bu = e.block_from(a), e.block_from(u0)
+    g_sym = e.gram(ba, ba)
+    assert np.array_equal(g_sym, g_sym.T)  # exact symmetric fill (manifold.cpp:45-53)
+    assert rel(g_sym, port.gram(spec, a, a, same=True)) < 1e-13
+    assert rel(e.gram(ba, bu), port.gram(spec, a, u0)) < 1e-12
+    m = rng.standard_normal((spec.n_orbitals, spec.n_orbitals))
+    out = e.alloc()
+    e.mix(ba, m, out)
+    assert rel(e.download(out), m.T @ a) < 1e-13
+
+
+@pytest.mark.parametrize("n_orb", [67, 130])
+def test_dmma_multitile(port, native, n_orb):
+    """N > 64 exercises several Gram tiles (upper-only in the symmetric path)
+    and several mix orbital tiles."""
+    spec = configs.ProblemSpec("tile", (9, 8, 10), (5.0, 5.0, 5.0), [], n_orb, hartree=False, xc=False)
+    e = native.engine_for(spec)
+    rng = np.random.default_rng(n_orb)
+    a = rng.standard_normal((n_orb, spec.num_points))
+    b = rng.standard_normal((n_orb, spec.num_points))
+    ba, bb = e.block_from(a), e.block_from(b)
+    wq = np.prod(spec.spacing)
+    assert rel(e.gram(ba, ba), wq * a @ a.T) < 1e-12
+    assert rel(e.gram(ba, bb), wq * a @ b.T) < 1e-12
+    m = rng.standard_normal((n_orb, n_orb))
+    out = e.alloc()
+    e.mix(ba, m, out)
+    assert rel(e.download(out), m.T @ a) < 1e-12
+    e.close()
+
+
+def test_orthonormalize(setup, port, native):
+    spec, u0, e = setup
+    rng = np.random.default_rng(5)
+    trial = u0 + 0.3 * rng.standard_normal(u0.shape)
+    bt, bo = e.block_from(trial), e.alloc()
+    pre, dev, fb = e.orthonormalize(bt, bo, True)
+    w_ref, pre_ref, dev_ref, fb_ref = port.orthonormalize(spec, trial)
+    assert not fb and not fb_ref
+    assert rel(pre, pre_ref) < 1e-13
+    assert rel(e.download(bo), w_ref) < 1e-10
+    assert 0.0 <= dev <= 1e-12 and dev_ref <= 1e-12
+
+
+def test_orthonormalize_degenerate(native):
+    spec = configs.small_molecule(8, 3, L=6.0)
+    e = native.engine_for(spec)
+    a = np.ones((3, spec.num_points))
+    with pytest.raises(native.DegenerateSetError):
+        e.orthonormalize(e.block_from(a), e.alloc(), True)
+    e.close()
+
+
+def test_residuals_gradient_rotation(setup, port, native):
+    spec, u0, e = setup
+    u = e.block_from(u0)
+    e.build_hamiltonian(u)
+    hu = e.alloc()
+    e.apply_hamiltonian(u, hu)
+    hu_h = e.download(hu)
+    z = e.alloc()
+    sig, zz = e.diagonal_residuals(u, hu, z)
+    wq = np.prod(spec.spacing)
+    s_ref = wq * np.einsum("ip,ip->i", hu_h, u0)
+    z_ref = hu_h - s_ref[:, None] * u0
+    assert np.allclose(sig, s_ref, rtol=1e-12, atol=1e-13)
+    assert rel(e.download(z), z_ref) < 1e-11
+    assert np.allclose(zz, wq * np.einsum("ip,ip->i", z_ref, z_ref), rtol=1e-10)
+    sigma, dd = e.stiefel_gradient(u, hu)
+    sigma_ref = port.gram(spec, hu_h, u0)
+    assert rel(sigma, sigma_ref) < 1e-12
+    d_ref = hu_h - sigma_ref.T @ u0
+    assert np.allclose(dd, wq * np.einsum("ip,ip->i", d_ref, d_ref), rtol=1e-9, atol=1e-14)
+    gam, p = e.subspace_rotate(u, 0.5 * (sigma + sigma.T))
+    gam_ref, p_ref = port.subspace_rotate(0.5 * (sigma + sigma.T))
+    assert np.allclose(gam, gam_ref, atol=1e-11)
+    assert np.allclose(p, p_ref, atol=1e-8)  # sign rule, manifold.cpp:233-241
+    assert rel(e.download(u), p_ref.T @ u0) < 1e-8
+
+
+def test_bb_products_and_lincomb(setup, native):
+    spec, u0, e = setup
+    rng = np.random.default_rng(9)
+    blocks = [rng.standard_normal(u0.shape) for _ in range(4)]
+    h = [e.block_from(x) for x in blocks]
+    ss, sy, yy = e.bb_products(*h)
+    wq = np.prod(spec.spacing)
+    s = blocks[0] - blocks[1]
+    y = blocks[2] - blocks[3]
+    assert np.allclose(ss, wq * (s * s).sum(1), rtol=1e-12)
+    assert np.allclose(sy, wq * (s * y).sum(1), rtol=1e-10, atol=1e-12)
+    assert np.allclose(yy, wq * (y * y).sum(1), rtol=1e-12)
+    out = e.alloc()
+    e.linear_combination(h[0], -0.25, h[1], out)
+    assert rel(e.download(out), blocks[0] - 0.25 * blocks[1]) < 1e-15
+
+
+def test_invalid_arguments(native):
+    with pytest.raises(native.InvalidArgument):
+        native.Engine((0, 4, 4), (1.0, 1.0, 1.0), 2)
+    with pytest.raises(native.InvalidArgument):
+        native.Engine((4, 4, 4), (1.0, -1.0, 1.0), 2)
+    with pytest.raises(native.InvalidArgument):
+        native.Engine((2, 2, 2), (1.0, 1.0, 1.0), 9)  # more orbitals than points
+    e = native.Engine((4, 4, 4), (4.0, 4.0, 4.0), 2)
+    with pytest.raises(native.InvalidArgument):
+        e.external_potential([(9.0, 1.0, 1.0, 1.0, 1.0)])  # outside the box (energy.cpp:20-30)
+    with pytest.raises(native.InvalidArgument):
+        e.download(17)  # bad handle
+    e.close()
