@@ -203,6 +203,44 @@ typedef struct {
 } po_result;
 
 void po_default_params(po_params* p);
+
+/* Iterator form of the same loop (one InnerLoop iteration per step), for
+ * callers that interleave their own work or time iterations individually.
+ * create = InnerLoop set-up (initial state, energy; optimizer.cpp:358-372);
+ * step = one iteration l (:374-576), *more = 0 once the loop has ended;
+ * current = handle of the block holding the current iterate W;
+ * finish = remaining iterations + finalize (:581-597), W copied into the
+ * block given to create. The po_result is filled progressively. */
+typedef struct po_solver po_solver;
+int po_solver_create(po_engine* e, const po_params* p, int w, po_result* r, po_solver** out);
+int po_solver_step(po_solver* s, int* more);
+int po_solver_current(po_solver* s, int* block);
+int po_solver_finish(po_solver* s);
+int po_solver_destroy(po_solver* s);
+/* Kernel launches issued by the library so far (process-wide). */
+long long po_launch_count(void);
+
+/* ------------------------------------------------- measurement helpers */
+
+/* Enqueue ONE hot-path kernel on the engine stream without synchronising, so
+ * a caller can bracket it with CUDA events on po_stream() (roofline timing,
+ * BASELINE config 5 microbenchmarks). M for the mix ops is the matrix set by
+ * po_set_matrix. */
+enum {
+  PO_OP_HAMILTONIAN = 0, /* out = H a (+ reductions), uses the default state's v_local */
+  PO_OP_GRAM_SYM = 1,    /* G = <a^T a> (symmetric path) */
+  PO_OP_GRAM = 2,        /* G = <a^T b> */
+  PO_OP_MIX = 3,         /* out = a M */
+  PO_OP_MIX_UPPER = 4,   /* out = a M, M upper triangular (the U L^{-T} rotation) */
+  PO_OP_DENSITY_XC = 5,  /* rho, v_xc, 4 pi rho from block a */
+  PO_OP_POISSON = 6,     /* CG solve on the last density (default state) */
+  PO_OP_CHOLESKY = 7,    /* device Cholesky + L^{-T} of the last Gram */
+  PO_OP_LAPLACIAN = 8    /* out = lap a */
+};
+int po_enqueue(po_engine* e, int op, int a, int b, int out);
+int po_set_matrix(po_engine* e, const double* m_host);
+/* 128-byte NCCL unique id for PO_COMM_NCCL (rank 0 creates, caller broadcasts). */
+int po_nccl_unique_id(void* out128);
 /* optimizer.cpp:599-613 run_single_level: u0 (orthonormal, block handle) is
  * iterated in place — on return block w holds the final orbitals. */
 int po_solve(po_engine* e, const po_params* p, int w, po_result* r);

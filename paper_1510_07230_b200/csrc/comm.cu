@@ -83,6 +83,7 @@ struct ThreadsComm : Comm {
     grp->barrier();  // every rank has read every buffer
     int blocks = (int)((n + 255) / 256);
     if (blocks > 1024) blocks = 1024;
+    ::po::count_launch();
     sum_rows_kernel<<<blocks, 256, 0, s>>>(stage, size, n, d);
     PO_CUDA(cudaGetLastError());
   }

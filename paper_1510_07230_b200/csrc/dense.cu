@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(256) matrix_stats_kernel(int N, const double* 
 
 void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, double* stats,
                          cudaStream_t s) {
+  ::po::count_launch();
   cholesky_inv_kernel<<<1, DT, 0, s>>>(N, G, Lscratch, M, stats);
 }
 
@@ -296,6 +297,7 @@ void launch_syev(int N, const double* A, double* work, double* evals, double* ev
                  int sign_rule, double* stats, cudaStream_t s) {
   const int M = N + (N & 1);
   const size_t shm = sizeof(double) * M + sizeof(int) * M + 64;
+  ::po::count_launch();
   syev_kernel<<<1, DT, shm, s>>>(N, A, work, evecs, evals, sign_rule, stats);
 }
 
@@ -304,10 +306,12 @@ void launch_inv_sqrt_from_eig(int N, const double* evals, const double* evecs, d
   const int64_t total = (int64_t)N * N;
   int blocks = (int)((total + 255) / 256);
   if (blocks > 1024) blocks = 1024;
+  ::po::count_launch();
   inv_sqrt_kernel<<<blocks, 256, 0, s>>>(N, evals, evecs, M, stats);
 }
 
 void launch_matrix_stats(int N, const double* G, double* out, cudaStream_t s) {
+  ::po::count_launch();
   matrix_stats_kernel<<<1, 256, 0, s>>>(N, G, out);
 }
 

@@ -359,8 +359,10 @@ void launch_gram(const SlabGeom& g, int N, const double* A, const double* Ab, do
     cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
     attr = true;
   }
+  ::po::count_launch();
   gram_kernel<<<grid, GT, shm, s>>>(N, g.ld, p.kchunk, p.mt, sym, A, Ab, sa, B, Bb, sb, ws);
   const int64_t total = (int64_t)N * N;
+  ::po::count_launch();
   gram_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(N, p.mt, sym, p.ntiles,
                                                                       p.nsplit, g.w, ws, G);
 }
@@ -377,6 +379,7 @@ void launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, dou
     cudaFuncSetAttribute(mix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
     attr = true;
   }
+  ::po::count_launch();
   mix_kernel<<<grid, MT, shm, s>>>(N, g.ld, g.ngl, upper, A, Ab, sa, M, alpha, C, beta, out, norms);
 }
 

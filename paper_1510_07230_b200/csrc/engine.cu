@@ -2,6 +2,9 @@
 // (include/parorb_gpu.h). Each po_* operator mirrors one reference function
 // (cited in the header); all arithmetic runs in the sm_100a kernels — there is
 // no host compute path.
+#include <dlfcn.h>
+
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -18,8 +21,13 @@ __global__ void copy_diag_kernel(int N, const double* __restrict__ M, double* __
 }  // namespace
 
 void launch_copy_diag(int N, const double* M, double* out, cudaStream_t s) {
+  ::po::count_launch();
   copy_diag_kernel<<<(N + 255) / 256, 256, 0, s>>>(N, M, out);
 }
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
 
 static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
@@ -314,6 +322,8 @@ using po::Error;
 extern "C" {
 
 int po_abi_version(void) { return PO_ABI_VERSION; }
+
+long long po_launch_count(void) { return po::launch_count(); }
 
 int po_create(const po_grid_desc* grid, int n_orbitals, double occupation,
               const po_dist_desc* dist, po_engine** out) {
@@ -643,3 +653,62 @@ int po_subspace_rotate(po_engine* h, int w, const double* sigma_host, double* ga
 }
 
 }  // extern "C"
+
+extern "C" int po_set_matrix(po_engine* h, const double* m_host) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  put_matrix(E, m_host, E.dmat[1]);
+  API_CATCH(h)
+}
+
+extern "C" int po_enqueue(po_engine* h, int op, int a, int b, int out) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  po::DevState* st = E.default_state();
+  switch (op) {
+    case PO_OP_HAMILTONIAN:
+      po::launch_hamiltonian(E.g, E.N, E.blk(a), nullptr, nullptr, st->v_local, E.v_ext,
+                             out >= 0 ? E.blk(out) : nullptr, E.partials, E.s);
+      break;
+    case PO_OP_GRAM_SYM:
+      po::launch_gram(E.g, E.N, E.blk(a), nullptr, 0.0, E.blk(a), nullptr, 0.0, 1, E.gram_ws,
+                      E.dmat[0], E.s);
+      break;
+    case PO_OP_GRAM:
+      po::launch_gram(E.g, E.N, E.blk(a), nullptr, 0.0, E.blk(b), nullptr, 0.0, 0, E.gram_ws,
+                      E.dmat[0], E.s);
+      break;
+    case PO_OP_MIX:
+    case PO_OP_MIX_UPPER:
+      po::launch_mix(E.g, E.N, E.blk(a), nullptr, 0.0, E.dmat[1], 1.0, nullptr, 0.0,
+                     op == PO_OP_MIX_UPPER, E.blk(out), nullptr, E.s);
+      break;
+    case PO_OP_DENSITY_XC:
+      po::launch_density_xc(E.g, E.N, E.blk(a), E.occ, 1, st->rho, st->v_xc,
+                            E.cg_b + E.g.z0 * E.g.plane, E.partials, E.s);
+      break;
+    case PO_OP_POISSON:
+      po::launch_cg(E.g.n0, E.g.n1, E.g.n2, E.g.ih2, E.cg_b, E.cg_x, 0, E.cg_ws, E.cg_bar,
+                    E.cg_out_i, E.cg_out_d, E.s);
+      break;
+    case PO_OP_CHOLESKY:
+      po::launch_cholesky_inv(E.N, E.dmat[0], E.chol_L, E.dmat[1], E.scal() + Engine::S_CHOL, E.s);
+      break;
+    case PO_OP_LAPLACIAN:
+      po::launch_laplacian(E.g, E.N, E.blk(a), nullptr, nullptr, E.blk(out), E.s);
+      break;
+    default:
+      throw Error(PO_EINVAL, "unknown op");
+  }
+  PO_CUDA(cudaGetLastError());
+  API_CATCH(h)
+}
+
+extern "C" int po_nccl_unique_id(void* out128) {
+  if (!out128) return PO_EINVAL;
+  void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) return PO_ENCCL;
+  auto fn = (int (*)(void*))dlsym(lib, "ncclGetUniqueId");
+  if (!fn) return PO_ENCCL;
+  return fn(out128) == 0 ? PO_OK : PO_ENCCL;
+}

@@ -236,36 +236,42 @@ int per_orbital_nblk(const SlabGeom& g, int N) {
 
 void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupation, int xc,
                        double* rho, double* v_xc, double* b, double* partials, cudaStream_t s) {
+  ::po::count_launch();
   density_xc_kernel<<<points_nblk(g), PT, 0, s>>>(g, N, u, occupation, xc, rho, v_xc, b,
                                                   partials);
 }
 
 void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h, const double* v_xc,
                    const double* rho, double* v_local, double* partials, cudaStream_t s) {
+  ::po::count_launch();
   vlocal_kernel<<<points_nblk(g), PT, 0, s>>>(g, v_ext, v_h, v_xc, rho, v_local, partials);
 }
 
 void launch_residual_diag(const SlabGeom& g, int N, const double* u, const double* hu,
                           const double* sigma_diag, double* z, double* partials, cudaStream_t s) {
   dim3 grid(per_orbital_nblk(g, N), N);
+  ::po::count_launch();
   residual_diag_kernel<<<grid, PT, 0, s>>>(g, N, u, hu, sigma_diag, z, partials);
 }
 
 void launch_bb(const SlabGeom& g, int N, const double* w, const double* wp, const double* z,
                const double* zp, double* partials, cudaStream_t s) {
   dim3 grid(per_orbital_nblk(g, N), N);
+  ::po::count_launch();
   bb_kernel<<<grid, PT, 0, s>>>(g, N, w, wp, z, zp, partials);
 }
 
 void launch_abs_sum(const SlabGeom& g, int N, const double* x, double* partials,
                     cudaStream_t s) {
   dim3 grid(per_orbital_nblk(g, N), N);
+  ::po::count_launch();
   abs_sum_kernel<<<grid, PT, 0, s>>>(g, N, x, partials);
 }
 
 void launch_lincomb(const SlabGeom& g, int N, const double* a, double sc, const double* b,
                     double* out, cudaStream_t s) {
   const int64_t total = (int64_t)N * g.ld;
+  ::po::count_launch();
   lincomb_kernel<<<nblk_for(total), PT, 0, s>>>(total, a, sc, b, out);
 }
 
@@ -273,11 +279,13 @@ void launch_reduce_rows(const double* partials, int rows, int nblk, double scale
                         cudaStream_t s) {
   const int threads = 256;
   const int blocks = (rows * 32 + threads - 1) / threads;
+  ::po::count_launch();
   reduce_rows_kernel<<<blocks, threads, 0, s>>>(partials, rows, nblk, scale, out);
 }
 
 void launch_external_potential(const SlabGeom& g, const double* h3, const double* atoms,
                                int natoms, int gaussian, double* v, cudaStream_t s) {
+  ::po::count_launch();
   potential_kernel<<<points_nblk(g), PT, 0, s>>>(g, h3[0], h3[1], h3[2], atoms, natoms, gaussian,
                                                  v);
 }
@@ -285,6 +293,7 @@ void launch_external_potential(const SlabGeom& g, const double* h3, const double
 void launch_pack_plane(const SlabGeom& g, int N, const double* u, int64_t plane_idx, double* dst,
                        cudaStream_t s) {
   dim3 grid((unsigned)((g.plane + PT - 1) / PT), N);
+  ::po::count_launch();
   pack_plane_kernel<<<grid, PT, 0, s>>>(g, N, u, plane_idx, dst);
 }
 

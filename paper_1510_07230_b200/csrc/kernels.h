@@ -8,6 +8,10 @@
 
 namespace po {
 
+// Number of kernel launches issued by this library (bench evidence of GPU work).
+void count_launch();
+long long launch_count();
+
 // ---------------------------------------------------------------- stencil.cu
 // Batched H u (energy.cpp:248-265) fused with the per-orbital reductions
 // sigma_ii, <lap u_i, u_i>, <V_ext u_i, u_i> (energy.cpp:267-280). Partials:

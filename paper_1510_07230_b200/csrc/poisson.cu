@@ -259,6 +259,7 @@ void launch_cg(int64_t n0, int64_t n1, int64_t n2, const double ih2[3], const do
   cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s);
   const int blocks = cg_grid_blocks();
   void* args[] = {&a};
+  ::po::count_launch();
   cudaLaunchCooperativeKernel((void*)cg_kernel, dim3(blocks), dim3(CT), args, 0, s);
 }
 

@@ -168,6 +168,19 @@ struct Solver {
   SRef fixed_state;
   bool have_prev_solve = false;
 
+  // InnerLoop::run state (optimizer.cpp:358-372), kept across step() calls
+  BRef w, hw, prev_w, prev_z, recovery_w;
+  SRef state, recovery_state;
+  double nm_c = 0.0, nm_q = 1.0;
+  std::vector<double> orth_energies;
+  bool history_valid = false, converged = false, finished = false;
+  bool sig_valid = true;  // dvec sigma row belongs to (w, hw)
+  int last_rotation_iter = 0, steps_until_orth = 0, failed_searches = 0, l = 0;
+  double last_accepted_tau = 0.0;
+  int n_org = 1;
+  bool full_grad = false, grad_style = true, mean_abs = false;
+  double ngd = 1.0;
+
   Solver(Engine& e, const po_params& pp, po_result* rr)
       : E(e), p(pp), r(rr), pool(e), spool(e), nonlinear(pp.hartree || pp.xc) {}
 
@@ -227,37 +240,44 @@ struct Solver {
     std::memcpy(r->sigma_eigs + (size_t)r->n_records * E.N, E.hmat, sizeof(double) * E.N);
   }
 
-  int run(BRef& w);
+  void init(const BRef& w0);
+  bool step();  // one InnerLoop iteration; false once the loop has ended
 };
 
-int Solver::run(BRef& w) {
+void Solver::init(const BRef& w0) {
   const int n = E.N;
-  const int n_org = p.algorithm == PO_ALG_OPT_PAR_MOD ? p.n_org : 1;
-  const bool full_grad = p.algorithm == PO_ALG_OPTM_QR;
-  const bool grad_style =
-      p.convergence_mode == PO_CONV_GRAD_NORM || p.convergence_mode == PO_CONV_MEAN_ABS;
-  const bool mean_abs = p.convergence_mode == PO_CONV_MEAN_ABS;
-  const double ngd = (double)E.g.n0 * (double)E.g.n1 * (double)E.g.n2;
-
-  SRef state = make_state(w);
-  BRef hw = pool.get();
+  n_org = p.algorithm == PO_ALG_OPT_PAR_MOD ? p.n_org : 1;
+  full_grad = p.algorithm == PO_ALG_OPTM_QR;
+  grad_style = p.convergence_mode == PO_CONV_GRAD_NORM || p.convergence_mode == PO_CONV_MEAN_ABS;
+  mean_abs = p.convergence_mode == PO_CONV_MEAN_ABS;
+  ngd = (double)E.g.n0 * (double)E.g.n1 * (double)E.g.n2;
+  (void)n;
+  w = w0;
+  state = make_state(w);
+  hw = pool.get();
   const EnergyParts e0 = apply_and_energy(w, hw, *state);
-  if (!std::isfinite(e0.total)) return fail(PO_OUT_NUMERICAL_FAILURE, "non-finite total energy at the level start");
+  if (!std::isfinite(e0.total)) {
+    fail(PO_OUT_NUMERICAL_FAILURE, "non-finite total energy at the level start");
+    finished = true;
+    return;
+  }
   set_energy(e0);
+  nm_c = e0.total;
+  nm_q = 1.0;
+  orth_energies.assign(1, e0.total);
+  recovery_w = w;
+  recovery_state = state;
+}
 
-  double nm_c = e0.total, nm_q = 1.0;
-  std::vector<double> orth_energies{e0.total};
-  BRef prev_w, prev_z;
-  bool history_valid = false;
-  int last_rotation_iter = 0, steps_until_orth = 0;
-  bool converged = false;
-  bool sig_valid = true;  // dvec sigma row belongs to (w, hw)
-  BRef recovery_w = w;
-  SRef recovery_state = state;
-  int failed_searches = 0;
-  double last_accepted_tau = 0.0;
-
-  for (int l = 0; l < p.max_inner && !converged; ++l) {
+bool Solver::step() {
+  const int n = E.N;
+  if (finished) return false;
+  if (!(l < p.max_inner && !converged)) {
+    r->outcome = converged ? PO_OUT_CONVERGED : PO_OUT_MAX_ITERATIONS;
+    finished = true;
+    return false;
+  }
+  {
     const auto t0 = Clock::now();
     const bool orth_iter = steps_until_orth == 0;
     const bool need_full = orth_iter && grad_style;
@@ -325,12 +345,16 @@ int Solver::run(BRef& w) {
                             : (mean_abs_v >= 0.0 && mean_abs_v < p.mean_abs_tol);
       if (conv) {
         converged = true;
-        break;
+        r->outcome = PO_OUT_CONVERGED;
+        finished = true;
+        return false;
       }
     }
     if (znorm2 == 0.0) {
       converged = true;
-      break;
+      r->outcome = PO_OUT_CONVERGED;
+      finished = true;
+      return false;
     }
 
     // ---- BB step, optimizer.cpp:376-411
@@ -406,7 +430,9 @@ int Solver::run(BRef& w) {
           std::snprintf(buf, sizeof buf,
                         "line search stagnated at level %d iteration %d (%d trials, C = %.17g)", 0,
                         l, s, nm_c);
-          return fail(PO_OUT_STAGNATION, buf);
+          fail(PO_OUT_STAGNATION, buf);
+          finished = true;
+          return false;
         }
         w = recovery_w;
         state = recovery_state;
@@ -418,7 +444,8 @@ int Solver::run(BRef& w) {
         prev_w.reset();
         prev_z.reset();
         steps_until_orth = 0;
-        continue;
+        ++l;
+        return true;  // no record for a failed search (optimizer.cpp:485-508)
       }
       failed_searches = 0;
       const double c_before = nm_c, q_before = nm_q;
@@ -431,7 +458,11 @@ int Solver::run(BRef& w) {
       }
       r->n_accepted++;
       if (te.total > nm_c + 1e-9 * (1.0 + std::abs(te.total)))
-        return fail(PO_OUT_NUMERICAL_FAILURE, "nonmonotone ledger violated (C < E after update)");
+      {
+        fail(PO_OUT_NUMERICAL_FAILURE, "nonmonotone ledger violated (C < E after update)");
+        finished = true;
+        return false;
+      }
       prev_w = w;
       prev_z = z;
       w = wt;
@@ -486,8 +517,8 @@ int Solver::run(BRef& w) {
     if (r->n_records < r->cap) r->records[r->n_records] = rec;
     r->n_records++;
   }
-  r->outcome = converged ? PO_OUT_CONVERGED : PO_OUT_MAX_ITERATIONS;
-  return r->outcome;
+  ++l;
+  return true;
 }
 
 }  // namespace
@@ -591,7 +622,10 @@ int po_solve(po_engine* h, const po_params* p, int w_handle, po_result* r) {
 
     po::Solver S(E, *p, r);
     std::shared_ptr<int> w(new int(w_handle), [](int* q) { delete q; });
-    S.run(w);
+    S.init(w);
+    while (S.step()) {
+    }
+    w = S.w;
     // finalize, optimizer.cpp:581-597: full Stiefel gradient at the final iterate
     po::SRef st = S.make_state(w);
     po::BRef hw = S.pool.get();
@@ -618,6 +652,109 @@ int po_solve(po_engine* h, const po_params* p, int w_handle, po_result* r) {
     return PO_EINVAL;
   }
   r->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return PO_OK;
+}
+
+struct po_solver {
+  po_engine* h;
+  po_params p;
+  po::Solver* S;
+  std::shared_ptr<int> w_user;
+  int w_handle;
+  std::chrono::steady_clock::time_point t0;
+};
+
+static int solver_error(po_engine* h, po_result* r, const std::exception& ex, int code) {
+  h->err = ex.what();
+  if (r) std::snprintf(r->message, sizeof r->message, "%s", ex.what());
+  return code;
+}
+
+int po_solver_create(po_engine* h, const po_params* p, int w_handle, po_result* r,
+                     po_solver** out) {
+  if (!h || !h->e || !p || !r || !out) return PO_EINVAL;
+  Engine& E = *h->e;
+  *out = nullptr;
+  r->n_records = r->n_accepted = 0;
+  r->cg_iters_total = 0;
+  r->message[0] = 0;
+  r->outcome = PO_OUT_MAX_ITERATIONS;
+  auto* sv = new po_solver{h, *p, nullptr, nullptr, w_handle, std::chrono::steady_clock::now()};
+  try {
+    E.blk(w_handle);
+    sv->S = new po::Solver(E, sv->p, r);
+    sv->w_user = std::shared_ptr<int>(new int(w_handle), [](int* q) { delete q; });
+    sv->S->init(sv->w_user);
+  } catch (const Error& ex) {
+    delete sv->S;
+    delete sv;
+    return solver_error(h, r, ex, ex.code);
+  } catch (const std::exception& ex) {
+    delete sv->S;
+    delete sv;
+    return solver_error(h, r, ex, PO_EINVAL);
+  }
+  *out = sv;
+  return PO_OK;
+}
+
+int po_solver_step(po_solver* sv, int* more) {
+  if (!sv || !sv->S) return PO_EINVAL;
+  try {
+    const bool m = sv->S->step();
+    if (more) *more = m ? 1 : 0;
+  } catch (const Error& ex) {
+    return solver_error(sv->h, sv->S->r, ex, ex.code);
+  } catch (const std::exception& ex) {
+    return solver_error(sv->h, sv->S->r, ex, PO_EINVAL);
+  }
+  return PO_OK;
+}
+
+int po_solver_current(po_solver* sv, int* block) {
+  if (!sv || !sv->S || !block || !sv->S->w) return PO_EINVAL;
+  *block = *sv->S->w;
+  return PO_OK;
+}
+
+int po_solver_finish(po_solver* sv) {
+  if (!sv || !sv->S) return PO_EINVAL;
+  Engine& E = *sv->h->e;
+  po::Solver& S = *sv->S;
+  po_result* r = S.r;
+  try {
+    while (S.step()) {
+    }
+    po::SRef st = S.make_state(S.w);
+    po::BRef hw = S.pool.get();
+    E.apply_h(E.blk(*S.w), E.blk(*hw), st->v_local);
+    S.sigma(S.w, hw);
+    E.mix(E.blk(*S.w), nullptr, 0.0, E.dmat[4], -1.0, E.blk(*hw), 1.0, 0, nullptr,
+          E.dvec + E.off_dd());
+    E.fetch_all();
+    if (E.hvec[E.off_scal() + Engine::S_SYM + 1] > 1e-10)
+      throw Error(PO_EINVAL, "stiefel_gradient: <(HU)^T U> is not symmetric; inconsistent H or U");
+    double acc = 0.0;
+    for (int i = 0; i < E.N; ++i) acc += E.hvec[E.off_dd() + i];
+    r->final_grad_norm = std::sqrt(std::max(0.0, acc));
+    if (*S.w != sv->w_handle)
+      PO_CUDA(cudaMemcpyAsync(E.blk(sv->w_handle), E.blk(*S.w), sizeof(double) * E.N * E.g.ld,
+                              cudaMemcpyDeviceToDevice, E.s));
+    E.sync();
+    r->wall_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - sv->t0).count();
+  } catch (const Error& ex) {
+    return solver_error(sv->h, r, ex, ex.code);
+  } catch (const std::exception& ex) {
+    return solver_error(sv->h, r, ex, PO_EINVAL);
+  }
+  return PO_OK;
+}
+
+int po_solver_destroy(po_solver* sv) {
+  if (!sv) return PO_OK;
+  delete sv->S;
+  delete sv;
   return PO_OK;
 }
 

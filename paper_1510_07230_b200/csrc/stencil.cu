@@ -107,6 +107,7 @@ void launch_hamiltonian(const SlabGeom& g, int N, const double* u, const double*
                         double* hu, double* partials, cudaStream_t s) {
   HGrid h = hgrid(g);
   dim3 grid(h.ntx * h.nty, h.nzc, N), block(TX, TY);
+  ::po::count_launch();
   hamiltonian_kernel<0><<<grid, block, 0, s>>>(g, N, h.ntx, u, halo_lo, halo_hi, v_local, v_ext,
                                                hu, partials);
 }
@@ -115,6 +116,7 @@ void launch_laplacian(const SlabGeom& g, int N, const double* u, const double* h
                       const double* halo_hi, double* out, cudaStream_t s) {
   HGrid h = hgrid(g);
   dim3 grid(h.ntx * h.nty, h.nzc, N), block(TX, TY);
+  ::po::count_launch();
   hamiltonian_kernel<1><<<grid, block, 0, s>>>(g, N, h.ntx, u, halo_lo, halo_hi, nullptr, nullptr,
                                                out, nullptr);
 }

@@ -122,7 +122,19 @@ _SIGS = {
                         C.c_void_p], C.c_int),
     "po_default_params": ([C.POINTER(Params)], None),
     "po_solve": ([C.c_void_p, C.POINTER(Params), C.c_int, C.POINTER(Result)], C.c_int),
+    "po_solver_create": ([C.c_void_p, C.POINTER(Params), C.c_int, C.POINTER(Result), C.POINTER(C.c_void_p)], C.c_int),
+    "po_solver_step": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
+    "po_solver_current": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
+    "po_solver_finish": ([C.c_void_p], C.c_int),
+    "po_solver_destroy": ([C.c_void_p], C.c_int),
+    "po_launch_count": ([], C.c_longlong),
+    "po_enqueue": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
+    "po_set_matrix": ([C.c_void_p, C.c_void_p], C.c_int),
+    "po_nccl_unique_id": ([C.c_void_p], C.c_int),
 }
+
+OPS = dict(hamiltonian=0, gram_sym=1, gram=2, mix=3, mix_upper=4, density_xc=5, poisson=6, cholesky=7,
+           laplacian=8)
 
 EXPORTED_SYMBOLS = tuple(_SIGS)
 
@@ -313,9 +325,17 @@ class Engine:
         self._chk(self._lib.po_bb_products(self.h, w, wp, z, zp, _dp(ss), _dp(sy), _dp(yy)))
         return ss, sy, yy
 
+    # ---- measurement helpers (pure launches on self.stream, no sync)
+    def enqueue(self, op: str, a: int = -1, b: int = -1, out: int = -1):
+        self._chk(self._lib.po_enqueue(self.h, OPS[op], a, b, out))
+
+    def set_matrix(self, m: np.ndarray):
+        self._chk(self._lib.po_set_matrix(self.h, _dp(np.ascontiguousarray(m, dtype=np.float64))))
+
     # ---- solver
-    def solve(self, w: int, algorithm="opt_par_mod", hartree=True, xc=True, trace_eigs=False,
-              warm_start=False, **over) -> "SolveResult":
+    @staticmethod
+    def make_params(algorithm="opt_par_mod", hartree=True, xc=True, trace_eigs=False, warm_start=False,
+                    **over) -> Params:
         p = default_params()
         p.algorithm = ALGORITHMS[algorithm]
         p.hartree, p.xc = int(hartree), int(xc)
@@ -331,6 +351,11 @@ class Engine:
             elif k == "verify_orthonormality":
                 v = int(v)
             setattr(p, k, v)
+        return p
+
+    def solve(self, w: int, algorithm="opt_par_mod", hartree=True, xc=True, trace_eigs=False,
+              warm_start=False, **over) -> "SolveResult":
+        p = self.make_params(algorithm, hartree, xc, trace_eigs, warm_start, **over)
         cap = p.max_inner + 1
         recs = (Record * cap)()
         acc = np.zeros(cap * 9)
@@ -355,6 +380,62 @@ class Engine:
                         total=r.e_total),
             final_grad_norm=r.final_grad_norm, cg_iters_total=r.cg_iters_total,
             wall_seconds=r.wall_seconds)
+
+
+class Stepper:
+    """po_solver_* iterator: one InnerLoop iteration per step() (bench / callers that
+    interleave work). Holds the engine's result struct alive."""
+
+    def __init__(self, e: Engine, w: int, params: Params):
+        self.e = e
+        self.p = params
+        cap = params.max_inner + 1
+        self._recs = (Record * cap)()
+        self._acc = np.zeros(cap * 9)
+        self.r = Result()
+        self.r.cap = cap
+        self.r.records = self._recs
+        self.r.accepted = self._acc.ctypes.data_as(C.POINTER(C.c_double))
+        self.r.sigma_eigs = C.POINTER(C.c_double)()
+        self.h = C.c_void_p()
+        rc = e._lib.po_solver_create(e.h, C.byref(self.p), w, C.byref(self.r), C.byref(self.h))
+        if rc != PO_OK:
+            raise _err(rc, e._lib.po_last_error(e.h).decode())
+
+    def step(self) -> bool:
+        more = C.c_int()
+        self.e._chk(self.e._lib.po_solver_step(self.h, C.byref(more)))
+        return bool(more.value)
+
+    def current(self) -> int:
+        b = C.c_int()
+        self.e._chk(self.e._lib.po_solver_current(self.h, C.byref(b)))
+        return b.value
+
+    def finish(self):
+        self.e._chk(self.e._lib.po_solver_finish(self.h))
+
+    def records(self):
+        n = min(self.r.n_records, self.r.cap)
+        return [dict(iter=x.iter, energy=x.energy, grad_norm=x.grad_norm, tau=x.tau, backtracks=x.backtracks,
+                     did_orth=x.did_orth, wall_ms=x.wall_ms) for x in self._recs[:n]]
+
+    def close(self):
+        if self.h:
+            self.e._lib.po_solver_destroy(self.h)
+            self.h = None
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    rc = lib().po_nccl_unique_id(buf)
+    if rc != PO_OK:
+        raise DeviceError("ncclGetUniqueId failed")
+    return buf.raw
+
+
+def launch_count() -> int:
+    return int(lib().po_launch_count())
 
 
 @dataclass
