@@ -210,7 +210,7 @@ def ours(args, spec):
     N, ng = spec.n_orbitals, spec.num_points
     w0 = native.random_orthonormal(e, spec.start_seed)
     total_steps = args.warmup + args.steps
-    params = e.make_params("opt_par_mod", True, True, False, False,
+    params = e.make_params("opt_par_mod", True, True, False, args.poisson,
                            max_inner=2 * total_steps + 4, n_org=1, n_diag=100)
     st = native.Stepper(e, w0, params)
     stream = torch.cuda.ExternalStream(e.stream)
@@ -275,6 +275,7 @@ def ours(args, spec):
     h_bytes = 16.0 * N * e.ngl + 8.0 * e.ngl  # read u + write Hu per orbital.point, + v_local
     g_ms = time_kernel(torch, native, e, "gram_sym", 20, a=cur)
     e.enqueue("density_xc", a=cur)
+    e.set_poisson_solver(args.poisson)
     p_ms = time_kernel(torch, native, e, "poisson", 5)
     st.close()
     roofline = {"kernel": "hamiltonian_kernel (batched H u + fused sigma/kinetic/external)",
@@ -320,6 +321,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--poisson", default="dst", choices=["dst", "cg", "cg_warm"])
     args = ap.parse_args()
     spec = configs.by_name(args.config)
     if args.impl == "reference":

@@ -165,6 +165,14 @@ enum { PO_ALG_OPTM_QR = 0, PO_ALG_OPT_PAR = 1, PO_ALG_OPT_PAR_MOD = 2 };
 enum { PO_BB1 = 0, PO_BB2 = 1, PO_BB_ALTERNATE = 2 };
 enum { PO_TRACE_DIAG_ABS = 0, PO_TRACE_ABS_TRACE = 1 };
 enum { PO_CONV_GRAD_NORM = 0, PO_CONV_MEAN_ABS = 1, PO_CONV_ENERGY_CHANGE = 2 };
+/* Hartree solve of -lap v = 4 pi rho (energy.cpp:105-143). All three stop on
+ * the reference's criterion ||b - A x|| <= 1e-10 ||b||, checked with the
+ * 7-point stencil; they differ only in the start point of the CG iteration. */
+enum {
+  PO_POISSON_CG = 0,       /* x0 = 0: the reference's algorithm */
+  PO_POISSON_CG_WARM = 1,  /* x0 = previous v_H */
+  PO_POISSON_DST = 2       /* x0 = fast-diagonalisation (DST-I) solve; CG verifies/refines */
+};
 enum { PO_OUT_CONVERGED = 0, PO_OUT_MAX_ITERATIONS = 1, PO_OUT_STAGNATION = 2,
        PO_OUT_NUMERICAL_FAILURE = 3 };
 
@@ -177,7 +185,7 @@ typedef struct {
   int verify_orthonormality;
   int hartree, xc;          /* Problem::hartree_enabled / xc_enabled */
   int trace_sigma_eigs;     /* record eig(<(HW)^T W>) after every accepted step */
-  int poisson_warm_start;   /* 0: x0 = 0 as the reference; 1: previous v_H */
+  int poisson_solver;       /* PO_POISSON_* (default PO_POISSON_DST) */
 } po_params;
 
 /* IterationRecord, optimizer.hpp:61-72. */
@@ -239,6 +247,8 @@ enum {
 };
 int po_enqueue(po_engine* e, int op, int a, int b, int out);
 int po_set_matrix(po_engine* e, const double* m_host);
+/* Poisson solver used by po_build_hamiltonian / po_enqueue(PO_OP_POISSON). */
+int po_set_poisson_solver(po_engine* e, int mode);
 /* 128-byte NCCL unique id for PO_COMM_NCCL (rank 0 creates, caller broadcasts). */
 int po_nccl_unique_id(void* out128);
 /* optimizer.cpp:599-613 run_single_level: u0 (orthonormal, block handle) is

@@ -243,7 +243,8 @@ __device__ __forceinline__ void mix_load(double (&ra)[8], double (&rm)[4], const
   }
 }
 
-__global__ void __launch_bounds__(MT) mix_kernel(int N, int64_t ld, int64_t ngl, int upper,
+__global__ void __launch_bounds__(MT) mix_kernel(int N, int64_t ld, int64_t ngl, int64_t bstride,
+                                                 int upper,
                                                  const double* __restrict__ A,
                                                  const double* __restrict__ Ab, double sa,
                                                  const double* __restrict__ M, double alpha,
@@ -255,6 +256,12 @@ __global__ void __launch_bounds__(MT) mix_kernel(int N, int64_t ld, int64_t ngl,
   double (*Ms)[MK * MIP] = reinterpret_cast<double (*)[MK * MIP]>(msm + 2 * MK * MPP);
   double (*nred)[MI] = reinterpret_cast<double (*)[MI]>(msm + 2 * MK * MPP + 2 * MK * MIP);
   const int64_t p0 = (int64_t)blockIdx.x * MP;
+  if (blockIdx.z) {  // batched left-multiplies (DST transforms): independent row sets
+    A += blockIdx.z * bstride;
+    if (Ab) Ab += blockIdx.z * bstride;
+    if (C) C += blockIdx.z * bstride;
+    if (out) out += blockIdx.z * bstride;
+  }
   const int i0 = blockIdx.y * MI;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wp = warp >> 1, wi = warp & 1;
@@ -380,7 +387,22 @@ void launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, dou
     attr = true;
   }
   ::po::count_launch();
-  mix_kernel<<<grid, MT, shm, s>>>(N, g.ld, g.ngl, upper, A, Ab, sa, M, alpha, C, beta, out, norms);
+  mix_kernel<<<grid, MT, shm, s>>>(N, g.ld, g.ngl, 0, upper, A, Ab, sa, M, alpha, C, beta, out,
+                                   norms);
+}
+
+void launch_mix_batched(int N, int64_t ld, int64_t ngl, int batch, int64_t bstride,
+                        const double* A, const double* M, double* out, cudaStream_t s) {
+  dim3 grid((unsigned)((ngl + MP - 1) / MP), (N + MI - 1) / MI, batch);
+  constexpr size_t shm = sizeof(double) * (2 * MK * MPP + 2 * MK * MIP + 4 * MI);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(mix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+    attr = true;
+  }
+  ::po::count_launch();
+  mix_kernel<<<grid, MT, shm, s>>>(N, ld, ngl, bstride, 0, A, nullptr, 0.0, M, 1.0, nullptr, 0.0,
+                                   out, nullptr);
 }
 
 }  // namespace po

@@ -115,6 +115,8 @@ Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist
   PO_CUDA(cudaMemsetAsync(cg_out_i, 0, 4 * sizeof(int), s));
   PO_CUDA(cudaMemsetAsync(cg_out_d, 0, 4 * sizeof(double), s));
   sync();
+  dst.init(g.n0, g.n1, g.n2, h);
+  PO_CUDA(cudaGetLastError());
 }
 
 Engine::~Engine() {
@@ -141,6 +143,7 @@ Engine::~Engine() {
   if (hmat) cudaFreeHost(hmat);
   if (h_cg_i) cudaFreeHost(h_cg_i);
   if (h_cg_d) cudaFreeHost(h_cg_d);
+  dst.release();
   comm.reset();
   if (s) cudaStreamDestroy(s);
 }
@@ -221,7 +224,17 @@ void Engine::reduce_rows(const double* parts, int rows, int nblk, double scale, 
 }
 
 // energy.cpp:228-246
-void Engine::build_state(const double* u, int hartree, int xc, DevState* st, int warm) {
+void Engine::poisson(int warm_ok) {
+  if (poisson_solver == PO_POISSON_DST) {
+    dst.solve(cg_b, cg_x, s);
+    launch_cg(g.n0, g.n1, g.n2, g.ih2, cg_b, cg_x, 1, cg_ws, cg_bar, cg_out_i, cg_out_d, s);
+  } else {
+    const int warm = poisson_solver == PO_POISSON_CG_WARM && warm_ok;
+    launch_cg(g.n0, g.n1, g.n2, g.ih2, cg_b, cg_x, warm, cg_ws, cg_bar, cg_out_i, cg_out_d, s);
+  }
+}
+
+void Engine::build_state(const double* u, int hartree, int xc, DevState* st, int warm_ok) {
   double* b_local = nullptr;
   if (hartree) b_local = size > 1 ? cg_b + ng_full : cg_b + g.z0 * g.plane;
   launch_density_xc(g, N, u, occ, xc, st->rho, st->v_xc, b_local, partials, s);
@@ -240,7 +253,7 @@ void Engine::build_state(const double* u, int hartree, int xc, DevState* st, int
         z += nz;
       }
     }
-    launch_cg(g.n0, g.n1, g.n2, g.ih2, cg_b, cg_x, warm, cg_ws, cg_bar, cg_out_i, cg_out_d, s);
+    poisson(warm_ok);
     PO_CUDA(cudaMemcpyAsync(st->v_h, cg_x + g.z0 * g.plane, sizeof(double) * g.ngl,
                             cudaMemcpyDeviceToDevice, s));
   } else {
@@ -688,8 +701,7 @@ extern "C" int po_enqueue(po_engine* h, int op, int a, int b, int out) {
                             E.cg_b + E.g.z0 * E.g.plane, E.partials, E.s);
       break;
     case PO_OP_POISSON:
-      po::launch_cg(E.g.n0, E.g.n1, E.g.n2, E.g.ih2, E.cg_b, E.cg_x, 0, E.cg_ws, E.cg_bar,
-                    E.cg_out_i, E.cg_out_d, E.s);
+      E.poisson(0);
       break;
     case PO_OP_CHOLESKY:
       po::launch_cholesky_inv(E.N, E.dmat[0], E.chol_L, E.dmat[1], E.scal() + Engine::S_CHOL, E.s);
@@ -702,6 +714,13 @@ extern "C" int po_enqueue(po_engine* h, int op, int a, int b, int out) {
   }
   PO_CUDA(cudaGetLastError());
   API_CATCH(h)
+}
+
+extern "C" int po_set_poisson_solver(po_engine* h, int mode) {
+  ENGINE_OR_EINVAL(h);
+  if (mode < PO_POISSON_CG || mode > PO_POISSON_DST) return PO_EINVAL;
+  E.poisson_solver = mode;
+  return PO_OK;
 }
 
 extern "C" int po_nccl_unique_id(void* out128) {

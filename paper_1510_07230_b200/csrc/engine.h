@@ -85,7 +85,8 @@ class Engine {
 
   // ---- operators (device-side results land in dvec_ regions; see *_result)
   // density -> Poisson -> xc -> v_local; returns after queueing; results via sync_state
-  void build_state(const double* u, int hartree, int xc, DevState* st, int warm);
+  void build_state(const double* u, int hartree, int xc, DevState* st, int warm_ok);
+  void poisson(int warm_ok);  // cg_b -> cg_x with the selected solver
   // CG outcome + E_H / E_xc of the last build (synchronises)
   void finish_state(DevState* st);
   // H u with fused reductions (sigma, kin, ext), scaled, into dvec rows
@@ -122,6 +123,8 @@ class Engine {
   int* h_cg_i = nullptr;       // pinned
   double* h_cg_d = nullptr;
   int64_t ng_full = 0;
+  DstPoisson dst;
+  int poisson_solver = PO_POISSON_DST;
   int64_t max_slab_points = 0;
 
   // dvec layout (offsets in doubles); N-length rows

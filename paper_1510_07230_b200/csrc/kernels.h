@@ -74,6 +74,11 @@ void launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, dou
                 const double* M, double alpha, const double* C, double beta, int upper,
                 double* out, double* norms, cudaStream_t s);
 
+// Batched left-multiply out_b = S X_b for X_b = rows [N][ld] at A + b * bstride
+// (valid row length ngl; ld multiple of 32, padding zero). DST transforms.
+void launch_mix_batched(int N, int64_t ld, int64_t ngl, int batch, int64_t bstride,
+                        const double* A, const double* M, double* out, cudaStream_t s);
+
 // ----------------------------------------------------------------- dense.cu
 // Cholesky G = L L^T (lower) and M = L^{-T} (upper, row-major M[k*N+i]),
 // following manifold.cpp:97-114. stats: {pmin, pmax, cond, ok}.
@@ -110,6 +115,19 @@ struct CgResult {
 // guess), rel. tol 1e-10, <= 20000 its x <= 4 passes (energy.cpp:105-143).
 // One cooperative persistent kernel; work: ws >= 5 * ng doubles + scratch.
 size_t cg_workspace_doubles(int64_t ng);
+// Fast-diagonalisation Poisson solve (DST-I along each axis as FP64 tensor-core
+// left-multiplies): x = A^{-1} b to round-off, used as the CG start point.
+struct DstPoisson {
+  int64_t n0 = 0, n1 = 0, n2 = 0, n1p = 0, n2p = 0, len = 0;
+  double* S[3] = {};     // DST-I matrices sin(pi (j+1)(k+1)/(n+1))
+  double* lam = nullptr; // [n0 + n1 + n2] eigenvalues of -lap_h per axis
+  double* t0 = nullptr;  // workspaces (len doubles each)
+  double* t1 = nullptr;
+  double norm = 1.0;
+  void init(int64_t n0, int64_t n1, int64_t n2, const double h[3]);
+  void release();
+  void solve(const double* b, double* x, cudaStream_t s);
+};
 void launch_cg(int64_t n0, int64_t n1, int64_t n2, const double ih2[3], const double* b,
                double* x, int warm, double* ws, unsigned* bar, int* out_i, double* out_d,
                cudaStream_t s);

@@ -15,6 +15,10 @@
 // are 35 MB — L2-resident on B200's 126 MB L2.
 #include <math.h>
 
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "kernels.h"
 
 namespace po {
@@ -261,6 +265,139 @@ void launch_cg(int64_t n0, int64_t n1, int64_t n2, const double ih2[3], const do
   void* args[] = {&a};
   ::po::count_launch();
   cudaLaunchCooperativeKernel((void*)cg_kernel, dim3(blocks), dim3(CT), args, 0, s);
+}
+
+}  // namespace po
+
+// ===================================================================== DST
+// Fast diagonalisation of the 7-point Dirichlet Laplacian (the same operator
+// as grid.cpp:94-122): -lap_h = (S0 x S1 x S2) diag(lam) (S0 x S1 x S2) * c,
+// S_a[j][k] = sin(pi (j+1)(k+1) / (n_a+1)), lam_a[j] = 4 sin^2(pi (j+1) /
+// (2 (n_a+1))) / h_a^2, c = prod_a 2 / (n_a + 1). The six axis transforms are
+// batched left-multiplies on the FP64 tensor cores (launch_mix_batched); the
+// contiguous axis is brought to the middle by an in-plane transpose.
+namespace po {
+
+namespace {
+
+constexpr int TT = 32;
+
+// dst[b][c][r] = src[b][r][c] (r < rows, c < cols); dst[b][c][r] = 0 for rows <= r < dstride
+__global__ void transpose_planes_kernel(const double* __restrict__ src, int64_t rows,
+                                        int64_t cols, int64_t sstride, int64_t splane,
+                                        double* __restrict__ dst, int64_t dstride,
+                                        int64_t dplane) {
+  __shared__ double tile[TT][TT + 1];
+  const int64_t b = blockIdx.z;
+  const int64_t r0 = (int64_t)blockIdx.x * TT, c0 = (int64_t)blockIdx.y * TT;
+  const double* sp = src + b * splane;
+  double* dp = dst + b * dplane;
+  for (int k = threadIdx.y; k < TT; k += blockDim.y) {
+    const int64_t r = r0 + k, c = c0 + threadIdx.x;
+    tile[k][threadIdx.x] = (r < rows && c < cols) ? sp[r * sstride + c] : 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < TT; k += blockDim.y) {
+    const int64_t c = c0 + k, r = r0 + threadIdx.x;
+    if (c < cols && r < dstride) dp[c * dstride + r] = tile[threadIdx.x][k];
+  }
+}
+
+// natural (unpadded) <-> natural padded rows
+__global__ void pad_rows_kernel(const double* __restrict__ src, int64_t nrows, int64_t w,
+                                int64_t sw, double* __restrict__ dst, int64_t dw) {
+  const int64_t total = nrows * dw;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / dw, c = e % dw;
+    dst[e] = c < w ? src[r * sw + c] : 0.0;
+  }
+}
+
+__global__ void dst_scale_kernel(double* __restrict__ t, int64_t n0, int64_t n1, int64_t n2,
+                                 int64_t n1p, const double* __restrict__ lam, double norm) {
+  const int64_t total = n0 * n2 * n1p;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k1 = e % n1p;
+    const int64_t k2 = (e / n1p) % n2;
+    const int64_t k0 = e / (n1p * n2);
+    if (k1 < n1) t[e] *= norm / ((lam[k0] + lam[n0 + k1]) + lam[n0 + n1 + k2]);
+  }
+}
+
+int64_t rup32(int64_t x) { return (x + 31) / 32 * 32; }
+
+}  // namespace
+
+void DstPoisson::init(int64_t a0, int64_t a1, int64_t a2, const double h[3]) {
+  n0 = a0;
+  n1 = a1;
+  n2 = a2;
+  n1p = rup32(n1);
+  n2p = rup32(n2);
+  len = n0 * std::max(n1 * n2p, n2 * n1p);
+  const int64_t ns[3] = {n0, n1, n2};
+  std::vector<double> lam_h;
+  const double pi = 3.141592653589793238462643383279502884;
+  norm = 1.0;
+  for (int a = 0; a < 3; ++a) {
+    const int64_t n = ns[a];
+    std::vector<double> S((size_t)(n * n));
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t k = 0; k < n; ++k)
+        S[(size_t)(j * n + k)] = std::sin(pi * (double)((j + 1) * (k + 1) % (2 * (n + 1))) /
+                                          (double)(n + 1));
+    cudaMalloc(&this->S[a], sizeof(double) * n * n);
+    cudaMemcpy(this->S[a], S.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice);
+    for (int64_t j = 0; j < n; ++j) {
+      const double sn = std::sin(pi * (double)(j + 1) / (2.0 * (double)(n + 1)));
+      lam_h.push_back(4.0 * sn * sn / (h[a] * h[a]));
+    }
+    norm *= 2.0 / (double)(n + 1);
+  }
+  cudaMalloc(&lam, sizeof(double) * lam_h.size());
+  cudaMemcpy(lam, lam_h.data(), sizeof(double) * lam_h.size(), cudaMemcpyHostToDevice);
+  cudaMalloc(&t0, sizeof(double) * len);
+  cudaMalloc(&t1, sizeof(double) * len);
+  cudaMemset(t0, 0, sizeof(double) * len);
+  cudaMemset(t1, 0, sizeof(double) * len);
+}
+
+void DstPoisson::release() {
+  for (auto& s : S)
+    if (s) cudaFree(s), s = nullptr;
+  if (lam) cudaFree(lam), lam = nullptr;
+  if (t0) cudaFree(t0), t0 = nullptr;
+  if (t1) cudaFree(t1), t1 = nullptr;
+}
+
+void DstPoisson::solve(const double* b, double* x, cudaStream_t s) {
+  const int64_t pn = n1 * n2p;  // natural padded plane
+  const int64_t pt = n2 * n1p;  // transposed padded plane
+  const dim3 tb(TT, 8);
+  auto blocks = [](int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16); };
+  // b -> t0 (natural padded)
+  ::po::count_launch();
+  pad_rows_kernel<<<blocks(n0 * n1 * n2p), 256, 0, s>>>(b, n0 * n1, n2, n2, t0, n2p);
+  // forward: axis 0, axis 1, transpose, axis 2
+  launch_mix_batched((int)n0, pn, pn, 1, 0, t0, S[0], t1, s);
+  launch_mix_batched((int)n1, n2p, n2p, (int)n0, pn, t1, S[1], t0, s);
+  ::po::count_launch();
+  transpose_planes_kernel<<<dim3((unsigned)((n1p + TT - 1) / TT), (unsigned)((n2 + TT - 1) / TT),
+                                 (unsigned)n0), tb, 0, s>>>(t0, n1, n2, n2p, pn, t1, n1p, pt);
+  launch_mix_batched((int)n2, n1p, n1p, (int)n0, pt, t1, S[2], t0, s);
+  ::po::count_launch();
+  dst_scale_kernel<<<blocks(n0 * pt), 256, 0, s>>>(t0, n0, n1, n2, n1p, lam, norm);
+  // inverse: axis 2, transpose back, axis 1, axis 0
+  launch_mix_batched((int)n2, n1p, n1p, (int)n0, pt, t0, S[2], t1, s);
+  ::po::count_launch();
+  transpose_planes_kernel<<<dim3((unsigned)((n2p + TT - 1) / TT), (unsigned)((n1 + TT - 1) / TT),
+                                 (unsigned)n0), tb, 0, s>>>(t1, n2, n1, n1p, pt, t0, n2p, pn);
+  launch_mix_batched((int)n1, n2p, n2p, (int)n0, pn, t0, S[1], t1, s);
+  launch_mix_batched((int)n0, pn, pn, 1, 0, t1, S[0], t0, s);
+  ::po::count_launch();
+  pad_rows_kernel<<<blocks(n0 * n1 * n2), 256, 0, s>>>(t0, n0 * n1, n2, n2p, x, n2);
 }
 
 }  // namespace po

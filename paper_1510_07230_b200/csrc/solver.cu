@@ -189,7 +189,8 @@ struct Solver {
   SRef make_state(const BRef& u) {  // optimizer.cpp:224-229
     if (!nonlinear && fixed_state) return fixed_state;
     SRef st = spool.get();
-    E.build_state(P(u), p.hartree, p.xc, st.get(), p.poisson_warm_start && have_prev_solve);
+    E.poisson_solver = p.poisson_solver;
+    E.build_state(P(u), p.hartree, p.xc, st.get(), have_prev_solve);
     E.finish_state(st.get());
     if (p.hartree) have_prev_solve = true;
     r->cg_iters_total += st->cg_iters;
@@ -552,7 +553,7 @@ void po_default_params(po_params* p) {  // optimizer.hpp:22-46
   p->hartree = 1;
   p->xc = 1;
   p->trace_sigma_eigs = 0;
-  p->poisson_warm_start = 0;
+  p->poisson_solver = PO_POISSON_DST;
 }
 
 int po_orthonormalize(po_engine* h, int in, int out, int measure, double* pre_gram,

@@ -23,6 +23,7 @@ ALGORITHMS = {"optm_qr": 0, "opt_par": 1, "opt_par_mod": 2}
 OUTCOMES = {0: "converged", 1: "max_iterations", 2: "stagnation", 3: "numerical_failure"}
 CONVERGENCE = {"grad_norm": 0, "mean_abs": 1, "energy_change": 2}
 BB = {"bb1": 0, "bb2": 1, "alternate": 2}
+POISSON = {"cg": 0, "cg_warm": 1, "dst": 2}
 
 
 class InvalidArgument(ValueError):
@@ -65,7 +66,7 @@ class Params(C.Structure):
                 ("max_backtracks", C.c_int), ("tau_min", C.c_double), ("tau_max", C.c_double),
                 ("grad_tol", C.c_double), ("mean_abs_tol", C.c_double), ("energy_tol", C.c_double),
                 ("verify_orthonormality", C.c_int), ("hartree", C.c_int), ("xc", C.c_int),
-                ("trace_sigma_eigs", C.c_int), ("poisson_warm_start", C.c_int)]
+                ("trace_sigma_eigs", C.c_int), ("poisson_solver", C.c_int)]
 
 
 class Record(C.Structure):
@@ -131,6 +132,7 @@ _SIGS = {
     "po_enqueue": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int], C.c_int),
     "po_set_matrix": ([C.c_void_p, C.c_void_p], C.c_int),
     "po_nccl_unique_id": ([C.c_void_p], C.c_int),
+    "po_set_poisson_solver": ([C.c_void_p, C.c_int], C.c_int),
 }
 
 OPS = dict(hamiltonian=0, gram_sym=1, gram=2, mix=3, mix_upper=4, density_xc=5, poisson=6, cholesky=7,
@@ -329,18 +331,21 @@ class Engine:
     def enqueue(self, op: str, a: int = -1, b: int = -1, out: int = -1):
         self._chk(self._lib.po_enqueue(self.h, OPS[op], a, b, out))
 
+    def set_poisson_solver(self, mode: str):
+        self._chk(self._lib.po_set_poisson_solver(self.h, POISSON[mode]))
+
     def set_matrix(self, m: np.ndarray):
         self._chk(self._lib.po_set_matrix(self.h, _dp(np.ascontiguousarray(m, dtype=np.float64))))
 
     # ---- solver
     @staticmethod
-    def make_params(algorithm="opt_par_mod", hartree=True, xc=True, trace_eigs=False, warm_start=False,
+    def make_params(algorithm="opt_par_mod", hartree=True, xc=True, trace_eigs=False, poisson="dst",
                     **over) -> Params:
         p = default_params()
         p.algorithm = ALGORITHMS[algorithm]
         p.hartree, p.xc = int(hartree), int(xc)
         p.trace_sigma_eigs = int(trace_eigs)
-        p.poisson_warm_start = int(warm_start)
+        p.poisson_solver = POISSON[poisson]
         for k, v in over.items():
             if k == "convergence_mode":
                 v = CONVERGENCE[v]
@@ -354,8 +359,8 @@ class Engine:
         return p
 
     def solve(self, w: int, algorithm="opt_par_mod", hartree=True, xc=True, trace_eigs=False,
-              warm_start=False, **over) -> "SolveResult":
-        p = self.make_params(algorithm, hartree, xc, trace_eigs, warm_start, **over)
+              poisson="dst", **over) -> "SolveResult":
+        p = self.make_params(algorithm, hartree, xc, trace_eigs, poisson, **over)
         cap = p.max_inner + 1
         recs = (Record * cap)()
         acc = np.zeros(cap * 9)

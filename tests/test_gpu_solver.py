@@ -15,7 +15,7 @@ TOL_E = 1e-6      # Ha, every iteration (north star)
 TOL_P = 1e-6      # projector Frobenius distance
 
 
-def run_both(port, native, spec, algorithm, **over):
+def run_both(port, native, spec, algorithm, poisson="dst", **over):
     spec.algorithm = algorithm
     u0 = port.random_orthonormal(spec)
     ref = port.solve(spec, u0=u0, trace_eigs=True, **over)
@@ -23,7 +23,8 @@ def run_both(port, native, spec, algorithm, **over):
     w = e.block_from(u0)
     kw = dict(spec.optimizer_params())
     kw.update(over)
-    got = e.solve(w, algorithm=algorithm, hartree=spec.hartree, xc=spec.xc, trace_eigs=True, **kw)
+    got = e.solve(w, algorithm=algorithm, hartree=spec.hartree, xc=spec.xc, trace_eigs=True,
+                  poisson=poisson, **kw)
     wg = e.download(w)
     e.close()
     return ref, got, wg
@@ -50,9 +51,10 @@ def check(ref, got, wg, spec, decisions=True):
     return dist
 
 
-def test_opt_par_small_molecule(port, native):
+@pytest.mark.parametrize("poisson", ["dst", "cg", "cg_warm"])
+def test_opt_par_small_molecule(port, native, poisson):
     spec = configs.small_molecule(16, 4, L=8.0, max_inner=15)
-    ref, got, wg = run_both(port, native, spec, "opt_par")
+    ref, got, wg = run_both(port, native, spec, "opt_par", poisson=poisson)
     check(ref, got, wg, spec)
 
 
