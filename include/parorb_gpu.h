@@ -137,6 +137,8 @@ int po_total_energy(po_engine* e, int u, int hartree, int xc, double* out5);
 int po_laplacian(po_engine* e, int u, int out);
 /* manifold.cpp:41-61 gram: G(i,j) = <a_i, b_j>; a == b uses the symmetric path. */
 int po_gram(po_engine* e, int a, int b, double* g_host);
+/* Gram of the fused trial point a + s b (no trial block written), symmetric. */
+int po_gram_lincomb(po_engine* e, int a, double s, int b, double* g_host);
 /* manifold.cpp:67-85 mix: out_i = sum_k in_k M(k, i). */
 int po_mix(po_engine* e, int in, const double* m_host, int out);
 /* manifold.cpp:136-169 orthonormalize_with_gram (Cholesky-QR on the device,

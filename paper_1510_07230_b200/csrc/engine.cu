@@ -78,7 +78,7 @@ Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist
   size_t pc = 0;
   auto upd = [&](size_t v) { pc = v > pc ? v : pc; };
   upd((size_t)3 * N * hamiltonian_nblk(g));
-  upd((size_t)N * mix_nblk(g));
+  upd((size_t)N * mix_nblk_max(g));
   upd((size_t)3 * N * per_orbital_nblk(g, N));
   upd((size_t)2 * points_nblk(g));
   partials_cap = pc;
@@ -304,8 +304,9 @@ void Engine::gram(const double* A, const double* Ab, double sa, const double* B,
 
 void Engine::mix(const double* A, const double* Ab, double sa, const double* M, double alpha,
                  const double* C, double beta, int upper, double* out, double* norm_rows) {
-  launch_mix(g, N, A, Ab, sa, M, alpha, C, beta, upper, out, norm_rows ? partials : nullptr, s);
-  if (norm_rows) reduce_rows(partials, N, mix_nblk(g), g.w, norm_rows, true);
+  const int nb =
+      launch_mix(g, N, A, Ab, sa, M, alpha, C, beta, upper, out, norm_rows ? partials : nullptr, s);
+  if (norm_rows) reduce_rows(partials, N, nb, g.w, norm_rows, true);
 }
 
 }  // namespace po
@@ -730,4 +731,15 @@ extern "C" int po_nccl_unique_id(void* out128) {
   auto fn = (int (*)(void*))dlsym(lib, "ncclGetUniqueId");
   if (!fn) return PO_ENCCL;
   return fn(out128) == 0 ? PO_OK : PO_ENCCL;
+}
+
+// Gram of the fused trial point (a + s b), symmetric path — the line-search
+// Gram of optimizer.cpp:459-463 + manifold.cpp:138 without materialising the
+// trial block. Exposed for parity tests of the fused load.
+extern "C" int po_gram_lincomb(po_engine* h, int a, double sc, int b, double* g_host) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  E.gram(E.blk(a), E.blk(b), sc, E.blk(a), E.blk(b), sc, 1, E.dmat[6]);
+  fetch_matrix(E, E.dmat[6], g_host);
+  API_CATCH(h)
 }

@@ -70,7 +70,8 @@ void launch_gram(const SlabGeom& g, int N, const double* A, const double* Ab, do
 // upper: M is upper triangular (skip zero k-blocks). out may be null; norms
 // (may be null) receives partials [N][nblk] of sum_p out_i[p]^2.
 int mix_nblk(const SlabGeom& g);
-void launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, double sa,
+int mix_nblk_max(const SlabGeom& g);  // partials buffer sizing (any mix path)
+int launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, double sa,
                 const double* M, double alpha, const double* C, double beta, int upper,
                 double* out, double* norms, cudaStream_t s);
 

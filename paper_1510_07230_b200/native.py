@@ -112,6 +112,7 @@ _SIGS = {
     "po_total_energy": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p], C.c_int),
     "po_laplacian": ([C.c_void_p, C.c_int, C.c_int], C.c_int),
     "po_gram": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p], C.c_int),
+    "po_gram_lincomb": ([C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_void_p], C.c_int),
     "po_mix": ([C.c_void_p, C.c_int, C.c_void_p, C.c_int], C.c_int),
     "po_orthonormalize": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_double),
                            C.POINTER(C.c_int)], C.c_int),
@@ -292,6 +293,11 @@ class Engine:
     def gram(self, a: int, b: int) -> np.ndarray:
         g = np.empty((self.N, self.N))
         self._chk(self._lib.po_gram(self.h, a, b, _dp(g)))
+        return g
+
+    def gram_lincomb(self, a: int, s: float, b: int) -> np.ndarray:
+        g = np.empty((self.N, self.N))
+        self._chk(self._lib.po_gram_lincomb(self.h, a, float(s), b, _dp(g)))
         return g
 
     def mix(self, inp: int, m: np.ndarray, out: int):

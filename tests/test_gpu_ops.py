@@ -162,6 +162,32 @@ def test_gram_mix(setup, port, native):
     assert rel(e.download(out), m.T @ a) < 1e-13
 
 
+@pytest.mark.parametrize("n_orb", [1, 8, 13, 33, 56, 64])
+def test_dmma_small_n(native, n_orb):
+    """Register-resident small-N Gram / mix paths (N <= 64), incl. the
+    triangular-skip rotation used for U L^{-T}."""
+    spec = configs.ProblemSpec("smalln", (10, 9, 11), (5.0, 5.0, 5.0), [], n_orb, hartree=False, xc=False)
+    e = native.engine_for(spec)
+    rng = np.random.default_rng(100 + n_orb)
+    a = rng.standard_normal((n_orb, spec.num_points))
+    b = rng.standard_normal((n_orb, spec.num_points))
+    ba, bb = e.block_from(a), e.block_from(b)
+    wq = np.prod(spec.spacing)
+    g = e.gram(ba, ba)
+    assert np.array_equal(g, g.T)
+    assert rel(g, wq * a @ a.T) < 1e-12
+    assert rel(e.gram(ba, bb), wq * a @ b.T) < 1e-12
+    out = e.alloc()
+    m = rng.standard_normal((n_orb, n_orb))
+    e.mix(ba, m, out)
+    assert rel(e.download(out), m.T @ a) < 1e-12
+    # orthonormalize exercises the upper-triangular (L^{-T}) skip path
+    pre, dev, fb = e.orthonormalize(ba, out, True)
+    w = e.download(out)
+    assert np.abs(wq * w @ w.T - np.eye(n_orb)).max() < 1e-12
+    e.close()
+
+
 @pytest.mark.parametrize("n_orb", [67, 130])
 def test_dmma_multitile(port, native, n_orb):
     """N > 64 exercises several Gram tiles (upper-only in the symmetric path)
@@ -260,4 +286,21 @@ def test_invalid_arguments(native):
         e.external_potential([(9.0, 1.0, 1.0, 1.0, 1.0)])  # outside the box (energy.cpp:20-30)
     with pytest.raises(native.InvalidArgument):
         e.download(17)  # bad handle
+    e.close()
+
+
+@pytest.mark.parametrize("n_orb", [1, 4, 5, 13, 33, 48, 67])
+def test_gram_fused_trial(native, n_orb):
+    """Gram of W - tau Z formed inside the load (optimizer.cpp:459-463)."""
+    spec = configs.ProblemSpec("trial", (10, 9, 11), (5.0, 5.0, 5.0), [], n_orb, hartree=False, xc=False)
+    e = native.engine_for(spec)
+    rng = np.random.default_rng(7 + n_orb)
+    w = rng.standard_normal((n_orb, spec.num_points))
+    z = rng.standard_normal((n_orb, spec.num_points))
+    bw, bz = e.block_from(w), e.block_from(z)
+    t = w - 0.37 * z
+    wq = np.prod(spec.spacing)
+    g = e.gram_lincomb(bw, -0.37, bz)
+    assert np.array_equal(g, g.T)
+    assert rel(g, wq * t @ t.T) < 1e-12
     e.close()
