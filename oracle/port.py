@@ -70,7 +70,21 @@ def lib():
         if not os.path.exists(_LIB_PATH):
             build()
         _lib = C.CDLL(_LIB_PATH)
+        _lib.pp_pairwise_dot.restype = C.c_double
+        _lib.pp_pairwise_dot.argtypes = [C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        _lib.pp_pairwise_sum.restype = C.c_double
+        _lib.pp_pairwise_sum.argtypes = [C.c_int64, C.POINTER(C.c_double)]
+        _lib.pp_xc_energy_density.argtypes = [C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        _lib.pp_xc_potential.argtypes = [C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        _lib.pp_rng_normals.argtypes = [C.c_uint64, C.c_int64, C.POINTER(C.c_double)]
     return _lib
+
+
+def pairwise_dot(a: np.ndarray, b: np.ndarray) -> float:
+    """numeric.hpp:30-34 stable_dot."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    return lib().pp_pairwise_dot(a.size, _dp(a), _dp(b))
 
 
 def _dp(a: np.ndarray):

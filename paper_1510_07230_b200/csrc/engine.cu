@@ -102,7 +102,8 @@ Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist
     PO_CUDA(cudaMemsetAsync(halo_hi, 0, hb, s));
   }
   // replicated full-grid Poisson buffers (+ gather staging for size > 1)
-  const size_t full = (size_t)ng_full + (size > 1 ? (size_t)size * max_slab_points : 0);
+  // [full grid | size x max_slab gather staging | max_slab local send slab]
+  const size_t full = (size_t)ng_full + (size > 1 ? (size_t)(size + 1) * max_slab_points : 0);
   PO_CUDA(cudaMalloc(&cg_b, full * sizeof(double)));
   PO_CUDA(cudaMalloc(&cg_x, (size_t)ng_full * sizeof(double)));
   PO_CUDA(cudaMemsetAsync(cg_x, 0, (size_t)ng_full * sizeof(double), s));
@@ -236,7 +237,8 @@ void Engine::poisson(int warm_ok) {
 
 void Engine::build_state(const double* u, int hartree, int xc, DevState* st, int warm_ok) {
   double* b_local = nullptr;
-  if (hartree) b_local = size > 1 ? cg_b + ng_full : cg_b + g.z0 * g.plane;
+  if (hartree)
+    b_local = size > 1 ? cg_b + ng_full + (int64_t)size * max_slab_points : cg_b + g.z0 * g.plane;
   launch_density_xc(g, N, u, occ, xc, st->rho, st->v_xc, b_local, partials, s);
   const int pn = points_nblk(g);
   launch_reduce_rows(partials, 1, pn, g.w, scal() + S_EXC, s);  // E_xc = <eps, rho>

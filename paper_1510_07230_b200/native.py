@@ -445,6 +445,19 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def thread_group(size: int) -> int:
+    """po_thread_group for in-process ranks (PO_COMM_THREADS); returns the handle."""
+    h = C.c_void_p()
+    rc = lib().po_thread_group_create(int(size), C.byref(h))
+    if rc != PO_OK:
+        raise InvalidArgument("thread group")
+    return h.value
+
+
+def thread_group_destroy(h: int):
+    lib().po_thread_group_destroy(C.c_void_p(h))
+
+
 def launch_count() -> int:
     return int(lib().po_launch_count())
 

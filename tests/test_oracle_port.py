@@ -1,0 +1,206 @@
+"""Pin the C restatement (oracle/port) to the UNMODIFIED reference.
+
+The fixtures in tests/golden were produced by oracle/make_golden.py from the
+reference sources compiled as-is (oracle/_ref). The port follows the
+reference's floating-point operation order, so most quantities agree BIT FOR
+BIT; the Cholesky/eigen pieces (Eigen in the reference, a clean-room subset
+here) agree to round-off. Also restates the reference's own known-answer tests
+(tests/test_grid.cpp, test_energy.cpp) against the port.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from paper_1510_07230_b200 import configs
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def spec_from(d):
+    d = dict(d)
+    for k in ("n", "extent"):
+        d[k] = tuple(d[k])
+    d["atoms"] = [tuple(a) for a in d["atoms"]]
+    if d.get("wells"):
+        d["wells"] = [tuple(w) for w in d["wells"]]
+    return configs.ProblemSpec(**d)
+
+
+@pytest.mark.parametrize("case", ["mol12", "skew"])
+def test_ops_match_reference(port, case):
+    g = np.load(os.path.join(GOLDEN, f"ops_{case}.npz"))
+    meta = json.load(open(os.path.join(GOLDEN, f"ops_{case}.json")))
+    spec = spec_from(meta["spec"])
+    u0 = g["u0"]
+    # start block itself: Rng(42) normals + orthonormalize (tests/problems.hpp:59-68)
+    assert np.max(np.abs(port.random_orthonormal(spec) - u0)) < 1e-14
+    assert np.array_equal(port.external_potential(spec), g["v_ext"])
+    st = port.build_hamiltonian(spec, u0)
+    assert np.array_equal(st["rho"], g["rho"])
+    assert np.array_equal(st["v_h"], g["v_h"])          # same CG, same op order
+    assert np.array_equal(st["v_xc"], g["v_xc"])
+    assert np.array_equal(st["v_local"], g["v_local"])
+    hw = port.apply_hamiltonian(spec, st["v_local"], u0)
+    assert np.array_equal(hw, g["hw"])
+    en, kin, ext = port.total_energy(spec, u0, st)
+    assert np.array_equal(kin, g["kin"]) and np.array_equal(ext, g["ext"])
+    for k in ("kinetic", "external", "hartree", "xc", "total"):
+        assert en[k] == meta["energy"][k]
+    assert np.array_equal(port.gram(spec, u0, u0, same=True), g["gram_ww"])
+    assert np.array_equal(port.gram(spec, hw, u0), g["sigma"])
+    # diagonal residuals: z = hw - sigma_ii u
+    wq = np.prod(spec.spacing)
+    sig = np.array([wq * port.pairwise_dot(hw[i], u0[i]) for i in range(u0.shape[0])])
+    assert np.array_equal(sig, g["sigma_diag"])
+    z = hw - sig[:, None] * u0
+    assert np.array_equal(z, g["z"])
+    # one line-search trial: Orth(W - tau Z) (Eigen LLT vs clean-room LLT: round-off)
+    tau = meta["trial_tau"]
+    w_t, pre, dev, fb = port.orthonormalize(spec, u0 + (-tau) * z)
+    assert np.array_equal(pre, g["orth_pre_gram"])
+    assert np.max(np.abs(w_t - g["orth_w"])) < 1e-13
+    st2 = port.build_hamiltonian(spec, w_t)
+    en2, _, _ = port.total_energy(spec, w_t, st2)
+    assert abs(en2["total"] - meta["trial_energy"]["total"]) < 1e-11
+    gam, _ = port.subspace_rotate(g["sigma"])
+    assert np.max(np.abs(gam - g["sigma_eig"])) < 1e-12
+
+
+SOLVE_CASES = ["mol14_opt_par", "mol14_opt_par_mod", "mol12_optm_qr", "box12_linear", "skew_opt_par"]
+
+
+@pytest.mark.parametrize("case", SOLVE_CASES)
+def test_solver_log_matches_reference(port, case):
+    """IterationRecord rows (driver.cpp:136-142, wall_ms zeroed) byte-identical to
+    the unmodified opt_par_inner / opt_par_mod_inner / optm_qr_solve."""
+    gold = json.load(open(os.path.join(GOLDEN, f"solve_{case}.json")))
+    spec = spec_from(gold["spec"])
+    r = port.solve(spec, trace_eigs=False)
+    rows = [port.format_log_row(x) for x in r["records"]]
+    want = [x["row"] for x in gold["records"]]
+    assert len(rows) == len(want)
+    # Byte-identical until the first subspace rotation; the eigensolver inside it
+    # (Eigen in the reference, Jacobi in the port) agrees only to round-off, so
+    # afterwards the trajectories agree to tolerance with identical decisions.
+    first_rot = next((k for k, x in enumerate(gold["records"]) if x["did_diag"]), len(want))
+    assert rows[: first_rot + 1] == want[: first_rot + 1]
+    for a, b in zip(r["records"][first_rot:], gold["records"][first_rot:]):
+        assert a["backtracks"] == b["backtracks"] and a["did_orth"] == b["did_orth"]
+        assert abs(a["energy"] - float(b["energy"])) < 1e-10 * max(1.0, abs(a["energy"]))
+    assert r["outcome"] == gold["summary"]["outcome"]
+    for k in ("kinetic", "external", "hartree", "xc", "total"):
+        assert abs(r["energy"][k] - gold["summary"]["energy"][k]) <= 1e-12 * max(1, abs(r["energy"][k]))
+    assert abs(r["final_grad_norm"] - gold["summary"]["final_grad_norm"]) < 1e-10
+    w_ref = np.load(os.path.join(GOLDEN, f"solve_{case}_w.npz"))["w"]
+    assert np.max(np.abs(r["w"] - w_ref)) < 1e-10
+
+
+@pytest.mark.parametrize("cname", ["C1"])
+def test_baseline_config_prefix(port, cname):
+    """First iterations of BASELINE configs[0] (64^3, N=5) byte-identical to the
+    reference's 50-iteration trajectory (full run: tests/test_gpu_configs.py)."""
+    gold = json.load(open(os.path.join(GOLDEN, f"{cname}_records.json")))
+    spec = configs.by_name(cname)
+    k = 2
+    r = port.solve(spec, trace_eigs=False, max_inner=k)
+    rows = [port.format_log_row(x) for x in r["records"]]
+    assert rows == [x["row"] for x in gold["records"][:k]]
+
+
+# ---------------------------------------------------------------- KATs
+def test_hand_stencil(port):
+    """test_grid.cpp:60-72: (0,1,0) -> (1,-2,1)/h^2 along a line."""
+    spec = configs.ProblemSpec("line", (3, 1, 1), (4.0, 2.0, 2.0), [], 1)
+    f = np.array([0.0, 1.0, 0.0])
+    lap = port.laplacian(spec, f)
+    h0, h1, h2 = spec.spacing
+    want = np.array([1.0, -2.0, 1.0]) / h0 ** 2 - 2.0 * f / h1 ** 2 - 2.0 * f / h2 ** 2
+    assert np.allclose(lap, want, rtol=0, atol=1e-13)
+
+
+def test_sine_eigenmodes(port):
+    """test_grid.cpp:74-91: discrete sine modes are eigenvectors to 1e-10."""
+    n, L = (9, 7, 11), (3.0, 2.5, 4.0)
+    spec = configs.ProblemSpec("sine", n, L, [], 1)
+    h = spec.spacing
+    for m in [(1, 1, 1), (2, 3, 1), (4, 1, 5)]:
+        s = [np.sin(np.pi * m[a] * np.arange(1, n[a] + 1) / (n[a] + 1)) for a in range(3)]
+        u = np.einsum("i,j,k->ijk", *s).ravel()
+        lam = sum((2 - 2 * np.cos(np.pi * m[a] / (n[a] + 1))) / h[a] ** 2 for a in range(3))
+        assert np.max(np.abs(port.laplacian(spec, u) + lam * u)) < 1e-10 * lam
+
+
+def test_laplacian_symmetric_negative(port):
+    """test_grid.cpp:93-105: symmetric and negative semidefinite to 1e-12."""
+    spec = configs.ProblemSpec("sym", (5, 4, 6), (2.0, 2.0, 2.0), [], 1)
+    rng = np.random.default_rng(0)
+    f, g = rng.standard_normal((2, spec.num_points))
+    a = np.dot(port.laplacian(spec, f), g)
+    b = np.dot(f, port.laplacian(spec, g))
+    assert abs(a - b) < 1e-12 * max(1, abs(a))
+    assert np.dot(port.laplacian(spec, f), f) <= 1e-12
+
+
+def test_pairwise_dot_long_double(port):
+    """test_grid.cpp:107-133: blocked pairwise dot vs a long-double reference."""
+    rng = np.random.default_rng(3)
+    a, b = rng.standard_normal((2, 100003))
+    got = port.pairwise_dot(a, b)
+    ref = float(np.sum(a.astype(np.longdouble) * b.astype(np.longdouble)))
+    assert abs(got - ref) < 1e-14 * np.sum(np.abs(a * b))
+
+
+def test_external_potential_on_atom(port):
+    """test_energy.cpp:145-176: V_ext = -Z/a on top of a softened atom, mirror symmetric."""
+    n, L = (7, 7, 7), (8.0, 8.0, 8.0)
+    h = L[0] / 8
+    spec = configs.ProblemSpec("at", n, L, [(4 * h, 4 * h, 4 * h, 1.0, 1.0)], 1)
+    v = port.external_potential(spec).reshape(n)
+    assert v[3, 3, 3] == -1.0
+    assert np.array_equal(v, v[::-1, :, :]) and np.array_equal(v, v[:, ::-1, :])
+
+
+def test_density_and_dirac(port):
+    """test_energy.cpp:117-143 (density by direct accumulation) and 288-316
+    (Dirac constants and the derivative v_x = d(rho eps_x)/d rho)."""
+    spec = configs.ProblemSpec("d", (4, 5, 3), (2.0, 2.0, 2.0), [], 3)
+    rng = np.random.default_rng(1)
+    u = rng.standard_normal((3, spec.num_points))
+    st = port.build_hamiltonian(spec, u, np.zeros(spec.num_points))
+    assert np.array_equal(st["rho"], (u[0] * u[0] + u[1] * u[1]) + u[2] * u[2])
+    cx = 0.75 * (3.0 / math.pi) ** (1.0 / 3.0)
+    rho = np.array([0.3, 1.7])
+    eps = np.empty(2)
+    port.lib().pp_xc_energy_density(2, port._dp(rho), port._dp(eps))
+    assert np.allclose(eps, -cx * np.cbrt(rho), rtol=1e-15)
+    v = np.empty(2)
+    port.lib().pp_xc_potential(2, port._dp(rho), port._dp(v))
+    d = 1e-6
+    fd = ((rho + d) * (-cx * np.cbrt(rho + d)) - (rho - d) * (-cx * np.cbrt(rho - d))) / (2 * d)
+    assert np.allclose(v, fd, rtol=1e-8)
+
+
+def test_poisson_closed_form(port):
+    """test_energy.cpp:229-286: CG vs the closed-form sine-transform solution
+    (relative <= 1e-8) with true residual <= 1e-10."""
+    n, L = (15, 13, 11), (6.0, 5.0, 4.0)
+    spec = configs.ProblemSpec("p", n, L, [], 1, xc=False)
+    h = spec.spacing
+    s = [np.sin(np.pi * (a + 1) * np.arange(1, n[a] + 1) / (n[a] + 1)) for a in range(3)]
+    u = np.einsum("i,j,k->ijk", *s).ravel()
+    rho = u * u
+    st = port.build_hamiltonian(spec, u[None, :], np.zeros(spec.num_points))
+    # exact discrete solution by dense DST-I in numpy (independent of the port)
+    def dst_matrix(m):
+        j = np.arange(1, m + 1)
+        return np.sin(np.pi * np.outer(j, j) / (m + 1))
+    b = (4 * np.pi * rho).reshape(n)
+    S = [dst_matrix(m) for m in n]
+    lam = [(2 - 2 * np.cos(np.pi * np.arange(1, m + 1) / (m + 1))) / h[a] ** 2 for a, m in enumerate(n)]
+    bh = np.einsum("ia,jb,kc,abc->ijk", S[0], S[1], S[2], b)
+    xh = bh / (lam[0][:, None, None] + lam[1][None, :, None] + lam[2][None, None, :])
+    x = np.einsum("ia,jb,kc,abc->ijk", S[0], S[1], S[2], xh) * np.prod([2.0 / (m + 1) for m in n])
+    assert np.linalg.norm(st["v_h"] - x.ravel()) <= 1e-8 * np.linalg.norm(x)
