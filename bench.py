@@ -239,6 +239,7 @@ def ours(args, spec):
         ms = float(t.item())
     recs = st.records()
     steps = max(done, 1)
+    step_wall = [r["wall_ms"] for r in recs[-steps:]] if recs else []
     value = N * ng * steps / (ms / 1e3)
 
     # ---- e2e: host buffers through the C ABI, H2D of the step input + D2H of the result
@@ -294,6 +295,8 @@ def ours(args, spec):
                        "l2": f"inputs larger than L2 (orbital block {block_bytes / 1e6:.0f} MB per copy)"},
             "s_per_outer_iteration": iter_ms / 1e3,
             "backtracks_in_timed_steps": int(sum(r["backtracks"] for r in recs[-steps:])),
+            "step_wall_ms": {"min": min(step_wall), "median": float(np.median(step_wall)),
+                             "max": max(step_wall)} if step_wall else None,
             "kernel_ms": {"hamiltonian": h_ms, "gram_sym": g_ms, "poisson_cg_solve": p_ms},
             "roofline": roofline,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": block_bytes,

@@ -20,7 +20,9 @@ constexpr int DT = 1024;
 __global__ void __launch_bounds__(DT) cholesky_inv_kernel(int N, const double* __restrict__ G,
                                                           double* __restrict__ L,
                                                           double* __restrict__ M,
-                                                          double* __restrict__ stats) {
+                                                          double* __restrict__ stats,
+                                                          const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;
   __shared__ int fail;
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
@@ -254,7 +256,9 @@ __global__ void __launch_bounds__(256) inv_sqrt_kernel(int N, const double* __re
 }
 
 __global__ void __launch_bounds__(256) matrix_stats_kernel(int N, const double* __restrict__ G,
-                                                           double* __restrict__ out) {
+                                                           double* __restrict__ out,
+                                                           const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;
   __shared__ double red[4][32];
   double dev = 0.0, asym = 0.0, off = 0.0, dg = 0.0;
   for (int64_t e = threadIdx.x; e < (int64_t)N * N; e += blockDim.x) {
@@ -285,12 +289,42 @@ __global__ void __launch_bounds__(256) matrix_stats_kernel(int N, const double* 
   }
 }
 
+__global__ void qr2_decision_kernel(const double* __restrict__ chol, const double* __restrict__ g2,
+                                    int measure, double* __restrict__ out) {
+  // manifold.cpp:150: skip verification iff !measure && cond <= 1e2; :159 repair iff !(dev <= 1e-12)
+  const bool verify = measure || !(chol[2] <= 1e2);
+  out[0] = (verify && !(g2[0] <= 1e-12)) ? 1.0 : 0.0;
+  out[1] = verify ? 1.0 : 0.0;
+}
+
+__global__ void copy_guarded_kernel(double* __restrict__ dst, const double* __restrict__ src,
+                                    int64_t n, const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = src[e];
+}
+
 }  // namespace
 
-void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, double* stats,
-                         cudaStream_t s) {
+void launch_qr2_decision(const double* chol_stats, const double* gram2_stats, int measure,
+                         double* out, cudaStream_t s) {
   ::po::count_launch();
-  cholesky_inv_kernel<<<1, DT, 0, s>>>(N, G, Lscratch, M, stats);
+  qr2_decision_kernel<<<1, 1, 0, s>>>(chol_stats, gram2_stats, measure, out);
+}
+
+void launch_copy_guarded(double* dst, const double* src, int64_t n, const double* guard,
+                         cudaStream_t s) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  ::po::count_launch();
+  copy_guarded_kernel<<<(unsigned)blocks, 256, 0, s>>>(dst, src, n, guard);
+}
+
+void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, double* stats,
+                         cudaStream_t s, const double* guard) {
+  ::po::count_launch();
+  cholesky_inv_kernel<<<1, DT, 0, s>>>(N, G, Lscratch, M, stats, guard);
 }
 
 void launch_syev(int N, const double* A, double* work, double* evals, double* evecs,
@@ -310,9 +344,10 @@ void launch_inv_sqrt_from_eig(int N, const double* evals, const double* evecs, d
   inv_sqrt_kernel<<<blocks, 256, 0, s>>>(N, evals, evecs, M, stats);
 }
 
-void launch_matrix_stats(int N, const double* G, double* out, cudaStream_t s) {
+void launch_matrix_stats(int N, const double* G, double* out, cudaStream_t s,
+                         const double* guard) {
   ::po::count_launch();
-  matrix_stats_kernel<<<1, 256, 0, s>>>(N, G, out);
+  matrix_stats_kernel<<<1, 256, 0, s>>>(N, G, out, guard);
 }
 
 }  // namespace po

@@ -107,7 +107,9 @@ __global__ void __launch_bounds__(GT) gram_kernel(int N, int64_t ld, int64_t kch
                                                   const double* __restrict__ Ab, double sa,
                                                   const double* __restrict__ B,
                                                   const double* __restrict__ Bb, double sb,
-                                                  double* __restrict__ ws) {
+                                                  double* __restrict__ ws,
+    const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;  // device-side branch (CholeskyQR2 repair)
   extern __shared__ __align__(16) double gsm[];
   double (*As)[GB * GKP] = reinterpret_cast<double (*)[GB * GKP]>(gsm);
   double (*Bs)[GB * GKP] = reinterpret_cast<double (*)[GB * GKP]>(gsm + 2 * GB * GKP);
@@ -168,7 +170,9 @@ __global__ void __launch_bounds__(GT) gram_kernel(int N, int64_t ld, int64_t kch
 }
 
 __global__ void gram_reduce_kernel(int N, int mt, int sym, int ntiles, int nsplit, double w,
-                                   const double* __restrict__ ws, double* __restrict__ G) {
+                                   const double* __restrict__ ws, double* __restrict__ G,
+    const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;  // device-side branch (CholeskyQR2 repair)
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)N * N) return;
   int i = (int)(e / N), j = (int)(e % N);
@@ -305,7 +309,9 @@ template <int F, bool SYM>
 __global__ void __launch_bounds__(RING_THREADS, 1) gram_ring_kernel(
     int N, int64_t ld, int64_t kchunk, int ks, int nst, const double* __restrict__ A,
     const double* __restrict__ Ab, double sa, const double* __restrict__ B,
-    const double* __restrict__ Bb, double sb, double* __restrict__ ws) {
+    const double* __restrict__ Bb, double sb, double* __restrict__ ws,
+    const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;  // device-side branch (CholeskyQR2 repair)
   constexpr int NP = SmallPairs<F, SYM>::NP;
   constexpr int NPAD = 8 * F;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -416,7 +422,9 @@ __global__ void __launch_bounds__(RING_THREADS, 1) gram_ring_kernel(
 
 // one warp per output element, lanes stride over the splits (fixed order)
 __global__ void gram_small_reduce_kernel(int N, int npad, int sym, int nsplit, double w,
-                                         const double* __restrict__ ws, double* __restrict__ G) {
+                                         const double* __restrict__ ws, double* __restrict__ G,
+    const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;  // device-side branch (CholeskyQR2 repair)
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (wid >= (int64_t)N * N) return;
@@ -447,7 +455,7 @@ constexpr int SMALL_SPLITS_PER_SM = 4;
 template <int F>
 void launch_gram_small_f(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                          const double* B, const double* Bb, double sb, double* ws, double* G,
-                         double w, cudaStream_t s) {
+                         double w, cudaStream_t s, const double* guard) {
   const int nsrc = 1 + (Ab ? 1 : 0) + (sym ? 0 : 1 + (Bb ? 1 : 0));
   const int np = sym ? F * (F + 1) / 2 : F * F;
   const RingCfg cfg = ring_cfg(nsrc, 8 * F, (size_t)SC * np * 64);
@@ -460,16 +468,16 @@ void launch_gram_small_f(int N, int64_t ld, int sym, const double* A, const doub
   if (sym) {
     auto k = gram_ring_kernel<F, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
-    k<<<nsplit, RING_THREADS, cfg.smem, s>>>(N, ld, kchunk, cfg.ks, cfg.nst, A, Ab, sa, A, Ab, sa, ws);
+    k<<<nsplit, RING_THREADS, cfg.smem, s>>>(N, ld, kchunk, cfg.ks, cfg.nst, A, Ab, sa, A, Ab, sa, ws, guard);
   } else {
     auto k = gram_ring_kernel<F, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
-    k<<<nsplit, RING_THREADS, cfg.smem, s>>>(N, ld, kchunk, cfg.ks, cfg.nst, A, Ab, sa, B, Bb, sb, ws);
+    k<<<nsplit, RING_THREADS, cfg.smem, s>>>(N, ld, kchunk, cfg.ks, cfg.nst, A, Ab, sa, B, Bb, sb, ws, guard);
   }
   const int64_t threads = (int64_t)N * N * 32;
   ::po::count_launch();
   gram_small_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(N, 8 * F, sym, nsplit,
-                                                                             w, ws, G);
+                                                                             w, ws, G, guard);
 }
 
 // Small-N mix: out_i[p] = alpha sum_k (A + sa Ab)_k[p] M(k, i) + beta C_i[p].
@@ -481,7 +489,8 @@ __global__ void __launch_bounds__(ST, 2) mix_small_kernel(
     int N, int64_t ld, int64_t ngl, int64_t pchunk, const double* __restrict__ A,
     const double* __restrict__ Ab, double sa, const double* __restrict__ M, double alpha,
     const double* __restrict__ C, double beta, double* __restrict__ out,
-    double* __restrict__ norms) {
+    double* __restrict__ norms, const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;  // device-side branch (CholeskyQR2 repair)
   constexpr int NPAD = 8 * F;
   constexpr int NV = Tile<NPAD>::NV;
   extern __shared__ __align__(16) double msmem[];
@@ -564,7 +573,8 @@ __global__ void __launch_bounds__(ST, 2) mix_small_kernel(
 template <int F>
 int launch_mix_small_f(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab,
                        double sa, const double* M, double alpha, const double* C, double beta,
-                       int upper, double* out, double* norms, cudaStream_t s) {
+                       int upper, double* out, double* norms, cudaStream_t s,
+                       const double* guard) {
   const size_t smem = sizeof(double) * ((size_t)(8 * F) * (8 * F) +
                                         (size_t)(C ? 2 : 1) * 8 * F * SKP + 8 * 8 * F);
   const int64_t kb = (ld + SK - 1) / SK;
@@ -576,11 +586,11 @@ int launch_mix_small_f(int N, int64_t ld, int64_t ngl, const double* A, const do
   if (upper) {
     auto k = mix_small_kernel<F, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<nblk, ST, smem, s>>>(N, ld, ngl, pchunk, A, Ab, sa, M, alpha, C, beta, out, norms);
+    k<<<nblk, ST, smem, s>>>(N, ld, ngl, pchunk, A, Ab, sa, M, alpha, C, beta, out, norms, guard);
   } else {
     auto k = mix_small_kernel<F, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<nblk, ST, smem, s>>>(N, ld, ngl, pchunk, A, Ab, sa, M, alpha, C, beta, out, norms);
+    k<<<nblk, ST, smem, s>>>(N, ld, ngl, pchunk, A, Ab, sa, M, alpha, C, beta, out, norms, guard);
   }
   return nblk;
 }
@@ -643,7 +653,9 @@ __global__ void __launch_bounds__(MT) mix_kernel(int N, int64_t ld, int64_t ngl,
                                                  const double* __restrict__ M, double alpha,
                                                  const double* __restrict__ C, double beta,
                                                  double* __restrict__ out,
-                                                 double* __restrict__ norms) {
+                                                 double* __restrict__ norms,
+                                                 const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;  // device-side branch (CholeskyQR2 repair)
   extern __shared__ __align__(16) double msm[];
   double (*As)[MK * MPP] = reinterpret_cast<double (*)[MK * MPP]>(msm);
   double (*Ms)[MK * MIP] = reinterpret_cast<double (*)[MK * MIP]>(msm + 2 * MK * MPP);
@@ -754,12 +766,12 @@ static bool gram_small_ok(int N, int sym) { return sym ? N <= 48 : N <= 40; }
 
 void launch_gram(const SlabGeom& g, int N, const double* A, const double* Ab, double sa,
                  const double* B, const double* Bb, double sb, int sym, double* ws, double* G,
-                 cudaStream_t s) {
+                 cudaStream_t s, const double* guard) {
   if (gram_small_ok(N, sym)) {
     switch ((N + 7) / 8) {
 #define PO_GS(F)                                                                  \
   case F:                                                                         \
-    launch_gram_small_f<F>(N, g.ld, sym, A, Ab, sa, B, Bb, sb, ws, G, g.w, s);    \
+    launch_gram_small_f<F>(N, g.ld, sym, A, Ab, sa, B, Bb, sb, ws, G, g.w, s, guard);    \
     return;
       PO_GS(1) PO_GS(2) PO_GS(3) PO_GS(4) PO_GS(5) PO_GS(6) PO_GS(7) PO_GS(8)
 #undef PO_GS
@@ -774,11 +786,11 @@ void launch_gram(const SlabGeom& g, int N, const double* A, const double* Ab, do
     attr = true;
   }
   ::po::count_launch();
-  gram_kernel<<<grid, GT, shm, s>>>(N, g.ld, p.kchunk, p.mt, sym, A, Ab, sa, B, Bb, sb, ws);
+  gram_kernel<<<grid, GT, shm, s>>>(N, g.ld, p.kchunk, p.mt, sym, A, Ab, sa, B, Bb, sb, ws, guard);
   const int64_t total = (int64_t)N * N;
   ::po::count_launch();
   gram_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(N, p.mt, sym, p.ntiles,
-                                                                      p.nsplit, g.w, ws, G);
+                                                                      p.nsplit, g.w, ws, G, guard);
 }
 
 int mix_nblk(const SlabGeom& g) { return (int)((g.ngl + MP - 1) / MP); }
@@ -793,12 +805,12 @@ int mix_nblk_max(const SlabGeom& g) {
 
 int launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, double sa,
                const double* M, double alpha, const double* C, double beta, int upper,
-               double* out, double* norms, cudaStream_t s) {
+               double* out, double* norms, cudaStream_t s, const double* guard) {
   if (N <= 64) {  // small-N LDG-staged path (returns its partials row length)
     switch ((N + 7) / 8) {
 #define PO_MS(F) \
   case F:        \
-    return launch_mix_small_f<F>(N, g.ld, g.ngl, A, Ab, sa, M, alpha, C, beta, upper, out, norms, s);
+    return launch_mix_small_f<F>(N, g.ld, g.ngl, A, Ab, sa, M, alpha, C, beta, upper, out, norms, s, guard);
       PO_MS(1) PO_MS(2) PO_MS(3) PO_MS(4) PO_MS(5) PO_MS(6) PO_MS(7) PO_MS(8)
 #undef PO_MS
     }
@@ -812,7 +824,7 @@ int launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, doub
   }
   ::po::count_launch();
   mix_kernel<<<grid, MT, shm, s>>>(N, g.ld, g.ngl, 0, upper, A, Ab, sa, M, alpha, C, beta, out,
-                                   norms);
+                                   norms, guard);
   return mix_nblk(g);
 }
 
@@ -827,7 +839,7 @@ void launch_mix_batched(int N, int64_t ld, int64_t ngl, int batch, int64_t bstri
   }
   ::po::count_launch();
   mix_kernel<<<grid, MT, shm, s>>>(N, ld, ngl, bstride, 0, A, nullptr, 0.0, M, 1.0, nullptr, 0.0,
-                                   out, nullptr);
+                                   out, nullptr, nullptr);
 }
 
 }  // namespace po

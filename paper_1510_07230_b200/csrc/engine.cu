@@ -149,9 +149,15 @@ Engine::~Engine() {
   if (s) cudaStreamDestroy(s);
 }
 
+// Spin on the stream instead of a blocking wait: the solver's per-trial
+// readback is on the critical path and blocking-sync wake-up jitter dominated
+// the iteration time on the host side.
 void Engine::sync() {
   PO_CUDA(cudaGetLastError());
-  PO_CUDA(cudaStreamSynchronize(s));
+  cudaError_t e;
+  while ((e = cudaStreamQuery(s)) == cudaErrorNotReady) {
+  }
+  if (e != cudaSuccess) throw Error(PO_ECUDA, std::string("stream: ") + cudaGetErrorString(e));
 }
 
 int Engine::alloc_block() {
@@ -239,9 +245,9 @@ void Engine::build_state(const double* u, int hartree, int xc, DevState* st, int
   double* b_local = nullptr;
   if (hartree)
     b_local = size > 1 ? cg_b + ng_full + (int64_t)size * max_slab_points : cg_b + g.z0 * g.plane;
-  launch_density_xc(g, N, u, occ, xc, st->rho, st->v_xc, b_local, partials, s);
+  launch_density_xc(g, N, u, occ, xc, st->rho, st->v_xc, b_local, v_ext, partials, s);
   const int pn = points_nblk(g);
-  launch_reduce_rows(partials, 1, pn, g.w, scal() + S_EXC, s);  // E_xc = <eps, rho>
+  launch_reduce_rows(partials, 2, pn, g.w, scal() + S_EXC, s);  // E_xc = <eps, rho>, E_ext
   if (hartree) {
     if (size > 1) {
       comm->allgather(b_local, cg_b + ng_full, (size_t)max_slab_points, s);
@@ -273,10 +279,15 @@ void Engine::build_state(const double* u, int hartree, int xc, DevState* st, int
 
 void Engine::finish_state(DevState* st) {
   fetch_all();
+  state_results(st);
+}
+
+void Engine::state_results(DevState* st) {
   if (h_cg_i[0] != 0) throw Error(PO_ESOLVER, "poisson: CG did not reach the requested residual");
   st->cg_iters = h_cg_i[1];
   st->e_xc = hvec[off_scal() + S_EXC];
   st->e_hartree = hvec[off_scal() + S_EH];
+  st->e_ext = hvec[off_scal() + S_EEXT];
 }
 
 void Engine::halo_exchange(const double* u) {
@@ -286,28 +297,29 @@ void Engine::halo_exchange(const double* u) {
   comm->halo(send_lo, send_hi, halo_lo, halo_hi, (size_t)N * g.plane, s);
 }
 
-void Engine::apply_h(const double* u, double* out, const double* v_local) {
+void Engine::apply_h(const double* u, double* out, const double* v_local, bool with_ext) {
   halo_exchange(u);
   const double* lo = (size > 1 && rank > 0) ? halo_lo : nullptr;
   const double* hi = (size > 1 && rank + 1 < size) ? halo_hi : nullptr;
-  launch_hamiltonian(g, N, u, lo, hi, v_local, v_ext, out, partials, s);
-  const int nb = hamiltonian_nblk(g);
+  launch_hamiltonian2(g, N, u, lo, hi, v_local, with_ext ? v_ext : nullptr, out, partials, s);
+  const int nb = hamiltonian2_nblk(g);
   launch_reduce_rows(partials, N, nb, g.w, dvec + off_sig(), s);
   launch_reduce_rows(partials + (size_t)N * nb, N, nb, -0.5 * g.w, dvec + off_kin(), s);
-  launch_reduce_rows(partials + (size_t)2 * N * nb, N, nb, g.w, dvec + off_ext(), s);
-  if (size > 1) comm->allreduce_sum(dvec + off_sig(), (size_t)3 * N, s);
+  if (with_ext) launch_reduce_rows(partials + (size_t)2 * N * nb, N, nb, g.w, dvec + off_ext(), s);
+  if (size > 1) comm->allreduce_sum(dvec + off_sig(), (size_t)(with_ext ? 3 : 2) * N, s);
 }
 
 void Engine::gram(const double* A, const double* Ab, double sa, const double* B, const double* Bb,
-                  double sb, int sym, double* Gdev) {
-  launch_gram(g, N, A, Ab, sa, B, Bb, sb, sym, gram_ws, Gdev, s);
+                  double sb, int sym, double* Gdev, const double* guard) {
+  launch_gram(g, N, A, Ab, sa, B, Bb, sb, sym, gram_ws, Gdev, s, guard);
   if (size > 1) comm->allreduce_sum(Gdev, (size_t)N * N, s);
 }
 
 void Engine::mix(const double* A, const double* Ab, double sa, const double* M, double alpha,
-                 const double* C, double beta, int upper, double* out, double* norm_rows) {
-  const int nb =
-      launch_mix(g, N, A, Ab, sa, M, alpha, C, beta, upper, out, norm_rows ? partials : nullptr, s);
+                 const double* C, double beta, int upper, double* out, double* norm_rows,
+                 const double* guard) {
+  const int nb = launch_mix(g, N, A, Ab, sa, M, alpha, C, beta, upper, out,
+                            norm_rows ? partials : nullptr, s, guard);
   if (norm_rows) reduce_rows(partials, N, nb, g.w, norm_rows, true);
 }
 
@@ -683,8 +695,8 @@ extern "C" int po_enqueue(po_engine* h, int op, int a, int b, int out) {
   po::DevState* st = E.default_state();
   switch (op) {
     case PO_OP_HAMILTONIAN:
-      po::launch_hamiltonian(E.g, E.N, E.blk(a), nullptr, nullptr, st->v_local, E.v_ext,
-                             out >= 0 ? E.blk(out) : nullptr, E.partials, E.s);
+      po::launch_hamiltonian2(E.g, E.N, E.blk(a), nullptr, nullptr, st->v_local, nullptr,
+                              out >= 0 ? E.blk(out) : nullptr, E.partials, E.s);
       break;
     case PO_OP_GRAM_SYM:
       po::launch_gram(E.g, E.N, E.blk(a), nullptr, 0.0, E.blk(a), nullptr, 0.0, 1, E.gram_ws,
@@ -701,7 +713,7 @@ extern "C" int po_enqueue(po_engine* h, int op, int a, int b, int out) {
       break;
     case PO_OP_DENSITY_XC:
       po::launch_density_xc(E.g, E.N, E.blk(a), E.occ, 1, st->rho, st->v_xc,
-                            E.cg_b + E.g.z0 * E.g.plane, E.partials, E.s);
+                            E.cg_b + E.g.z0 * E.g.plane, E.v_ext, E.partials, E.s);
       break;
     case PO_OP_POISSON:
       E.poisson(0);

@@ -50,6 +50,7 @@ struct DevState {
   double* v_local = nullptr;
   double* vh_full = nullptr;  // full-grid v_H (warm start / replicated solve)
   double e_hartree = 0.0, e_xc = 0.0;
+  double e_ext = 0.0;  // w <V_ext, rho> (= sum_i f <V_ext u_i, u_i>)
   int cg_iters = 0;
 };
 
@@ -90,12 +91,16 @@ class Engine {
   // CG outcome + E_H / E_xc of the last build (synchronises)
   void finish_state(DevState* st);
   // H u with fused reductions (sigma, kin, ext), scaled, into dvec rows
-  void apply_h(const double* u, double* out, const double* v_local);
+  // with_ext: also per-orbital <V_ext u_i, u_i> (else E_ext comes from the state)
+  void apply_h(const double* u, double* out, const double* v_local, bool with_ext = true);
   void halo_exchange(const double* u);
   void gram(const double* A, const double* Ab, double sa, const double* B, const double* Bb,
-            double sb, int sym, double* Gdev);
+            double sb, int sym, double* Gdev, const double* guard = nullptr);
   void mix(const double* A, const double* Ab, double sa, const double* M, double alpha,
-           const double* C, double beta, int upper, double* out, double* norm_rows);
+           const double* C, double beta, int upper, double* out, double* norm_rows,
+           const double* guard = nullptr);
+  // CG outcome + E_H / E_xc / E_ext of the last build from the last fetch (no sync)
+  void state_results(DevState* st);
   void reduce_rows(const double* partials, int rows, int nblk, double scale, double* out,
                    bool allreduce);
 
@@ -140,8 +145,8 @@ class Engine {
   size_t off_scal() const { return 9 * (size_t)N; }  // 64 scalars
   size_t dvec_len() const { return 9 * (size_t)N + 64; }
   // scalar slots
-  enum { S_EXC = 0, S_BB = 1, S_EH = 2, S_CHOL = 8, S_EIG = 12, S_INVS = 16, S_MSTAT = 20,
-         S_MSTAT2 = 24, S_SYM = 28 };
+  enum { S_EXC = 0, S_EEXT = 1, S_EH = 2, S_CHOL = 8, S_EIG = 12, S_INVS = 16, S_MSTAT = 20,
+         S_MSTAT2 = 24, S_SYM = 28, S_QR2 = 32, S_CHOL2 = 36 };
   double* scal() { return dvec + off_scal(); }
   // copy n doubles of dvec starting at off into hvec (same offsets) and synchronise
   void fetch(size_t off, size_t n);

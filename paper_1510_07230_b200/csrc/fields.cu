@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(PT) density_xc_kernel(SlabGeom g, int N,
                                                         int xc, double* __restrict__ rho,
                                                         double* __restrict__ vxc,
                                                         double* __restrict__ b,
+                                                        const double* __restrict__ vext,
                                                         double* __restrict__ partials) {
   __shared__ double red[2 * 32];
   double acc[2] = {0.0, 0.0};
@@ -60,8 +61,8 @@ __global__ void __launch_bounds__(PT) density_xc_kernel(SlabGeom g, int N,
     if (b) {
       const double bb = r * four_pi;
       b[p] = bb;
-      acc[1] += bb * bb;
     }
+    if (vext) acc[1] += __ldg(vext + p) * r;  // E_ext = w <V_ext, rho> (energy.cpp:286-291 summed)
   }
   block_sum<2>(acc, red);
   if (threadIdx.x == 0) {
@@ -235,9 +236,10 @@ int per_orbital_nblk(const SlabGeom& g, int N) {
 }
 
 void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupation, int xc,
-                       double* rho, double* v_xc, double* b, double* partials, cudaStream_t s) {
+                       double* rho, double* v_xc, double* b, const double* v_ext, double* partials,
+                       cudaStream_t s) {
   ::po::count_launch();
-  density_xc_kernel<<<points_nblk(g), PT, 0, s>>>(g, N, u, occupation, xc, rho, v_xc, b,
+  density_xc_kernel<<<points_nblk(g), PT, 0, s>>>(g, N, u, occupation, xc, rho, v_xc, b, v_ext,
                                                   partials);
 }
 

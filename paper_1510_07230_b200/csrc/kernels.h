@@ -20,6 +20,12 @@ int hamiltonian_nblk(const SlabGeom& g);
 void launch_hamiltonian(const SlabGeom& g, int N, const double* u, const double* halo_lo,
                         const double* halo_hi, const double* v_local, const double* v_ext,
                         double* hu, double* partials, cudaStream_t s);
+// v2: register-queue z-march, shuffle/smem neighbours; v_ext may be null (no
+// external partials). Partials [3][N][hamiltonian2_nblk].
+int hamiltonian2_nblk(const SlabGeom& g);
+void launch_hamiltonian2(const SlabGeom& g, int N, const double* u, const double* halo_lo,
+                         const double* halo_hi, const double* v_local, const double* v_ext,
+                         double* hu, double* partials, cudaStream_t s);
 // Plain 7-point Dirichlet Laplacian of every orbital (grid.cpp:94-122).
 void launch_laplacian(const SlabGeom& g, int N, const double* u, const double* halo_lo,
                       const double* halo_hi, double* out, cudaStream_t s);
@@ -29,9 +35,11 @@ int points_nblk(const SlabGeom& g);
 // CTAs per orbital of the per-orbital streaming kernels (partials row length).
 int per_orbital_nblk(const SlabGeom& g, int N);
 // rho = f sum_i u_i^2 (energy.cpp:67-76); v_xc, eps (energy.cpp:212-226);
-// b = 4 pi rho written at b (may be null). Partials [2][nblk]: sum eps*rho, sum b*b.
+// b = 4 pi rho written at b (may be null). Partials [2][nblk]: sum eps*rho, sum v_ext*rho
+// (v_ext may be null).
 void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupation, int xc,
-                       double* rho, double* v_xc, double* b, double* partials, cudaStream_t s);
+                       double* rho, double* v_xc, double* b, const double* v_ext, double* partials,
+                       cudaStream_t s);
 // v_local = v_ext + (v_h + v_xc) (energy.cpp:241-244); partials [1][nblk]: sum v_h*rho.
 void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h, const double* v_xc,
                    const double* rho, double* v_local, double* partials, cudaStream_t s);
@@ -64,7 +72,7 @@ void launch_pack_plane(const SlabGeom& g, int N, const double* u, int64_t plane_
 size_t gram_workspace_doubles(const SlabGeom& g, int N);
 void launch_gram(const SlabGeom& g, int N, const double* A, const double* Ab, double sa,
                  const double* B, const double* Bb, double sb, int sym, double* ws,
-                 double* G, cudaStream_t s);
+                 double* G, cudaStream_t s, const double* guard = nullptr);
 // Column mixing on the FP64 tensor cores (manifold.cpp:67-85):
 // out_i = alpha * sum_k (A + sa Ab)_k M(k, i) + beta * C_i. M device row-major.
 // upper: M is upper triangular (skip zero k-blocks). out may be null; norms
@@ -73,7 +81,7 @@ int mix_nblk(const SlabGeom& g);
 int mix_nblk_max(const SlabGeom& g);  // partials buffer sizing (any mix path)
 int launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, double sa,
                 const double* M, double alpha, const double* C, double beta, int upper,
-                double* out, double* norms, cudaStream_t s);
+                double* out, double* norms, cudaStream_t s, const double* guard = nullptr);
 
 // Batched left-multiply out_b = S X_b for X_b = rows [N][ld] at A + b * bstride
 // (valid row length ngl; ld multiple of 32, padding zero). DST transforms.
@@ -84,6 +92,14 @@ void launch_mix_batched(int N, int64_t ld, int64_t ngl, int batch, int64_t bstri
 // Cholesky G = L L^T (lower) and M = L^{-T} (upper, row-major M[k*N+i]),
 // following manifold.cpp:97-114. stats: {pmin, pmax, cond, ok}.
 void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, double* stats,
+                         cudaStream_t s, const double* guard = nullptr);
+// Device-side decisions of manifold.cpp:147-167 without a host round trip:
+// out[0] = 1 if the repair pass runs ((measure || cond > 100) && dev > 1e-12),
+// from the pass-1 Cholesky stats and the verification-Gram stats.
+void launch_qr2_decision(const double* chol_stats, const double* gram2_stats, int measure,
+                         double* out, cudaStream_t s);
+// dst = src (n doubles) if guard is null or *guard != 0
+void launch_copy_guarded(double* dst, const double* src, int64_t n, const double* guard,
                          cudaStream_t s);
 // Symmetric eigensolver (parallel cyclic Jacobi) on 1/2 (A + A^T):
 // evals ascending, evecs column j in evecs[i*N + j]; sign rule of
@@ -95,7 +111,8 @@ void launch_inv_sqrt_from_eig(int N, const double* evals, const double* evecs, d
                               double* stats, cudaStream_t s);
 // max |G - I| (manifold.cpp:158) and max |S - S^T|, offdiag / diag deviation
 // (manifold.cpp:249-259): out {dev, asym, offdiag_max, diag_dev_max}.
-void launch_matrix_stats(int N, const double* G, double* out, cudaStream_t s);
+void launch_matrix_stats(int N, const double* G, double* out, cudaStream_t s,
+                         const double* guard = nullptr);
 // out[i] = M(i, i)
 void launch_copy_diag(int N, const double* M, double* out, cudaStream_t s);
 

@@ -45,6 +45,9 @@ struct BlockPool {
       }
     }
   }
+  void reserve(int n) {  // allocate up front: no cudaMalloc inside the iteration loop
+    while ((int)free_.size() < n) free_.push_back(E.alloc_block());
+  }
   BRef get() {
     int h;
     if (!free_.empty()) {
@@ -71,6 +74,9 @@ struct StatePool {
       } catch (...) {
       }
     }
+  }
+  void reserve(int n) {
+    while ((int)free_.size() < n) free_.push_back(E.new_state());
   }
   SRef get() {
     DevState* s;
@@ -156,6 +162,46 @@ bool orthonormalize_dev(Engine& E, const double* A, const double* Ab, double sa,
   return true;
 }
 
+// Asynchronous form of manifold.cpp:136-169 for the line search: everything
+// is enqueued assuming the pass-1 Cholesky succeeds; whether the CholeskyQR2
+// repair runs ((measure || cond > 100) && dev > 1e-12) is decided on the device
+// and its kernels are guarded by that flag, so a trial needs no host round trip
+// before its energy. orth_outcome() interprets the scalars after the trial's
+// single readback; a failed pass-1 Cholesky (rare) is redone synchronously with
+// the symmetric-eigen fallback.
+void orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, double* out,
+                  double* tmp, bool measure) {
+  double* sc = E.scal();
+  E.gram(A, Ab, sa, A, Ab, sa, 1, E.dmat[0]);
+  launch_matrix_stats(E.N, E.dmat[0], sc + Engine::S_MSTAT, E.s);
+  launch_cholesky_inv(E.N, E.dmat[0], E.chol_L, E.dmat[1], sc + Engine::S_CHOL, E.s);
+  E.mix(A, Ab, sa, E.dmat[1], 1.0, nullptr, 0.0, 1, out, nullptr);
+  E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2]);
+  launch_matrix_stats(E.N, E.dmat[2], sc + Engine::S_MSTAT2, E.s);
+  const double* guard = sc + Engine::S_QR2;
+  launch_qr2_decision(sc + Engine::S_CHOL, sc + Engine::S_MSTAT2, measure ? 1 : 0,
+                      sc + Engine::S_QR2, E.s);
+  launch_cholesky_inv(E.N, E.dmat[2], E.chol_L, E.dmat[3], sc + Engine::S_CHOL2, E.s, guard);
+  E.mix(out, nullptr, 0.0, E.dmat[3], 1.0, nullptr, 0.0, 1, tmp, nullptr, guard);
+  launch_copy_guarded(out, tmp, (int64_t)E.N * E.g.ld, guard, E.s);
+  E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2], guard);
+  launch_matrix_stats(E.N, E.dmat[2], sc + Engine::S_MSTAT2, E.s, guard);
+}
+
+// 0 ok, 1 pass-1 Cholesky rejected (caller redoes the trial with the fallback),
+// 2 repair Cholesky rejected (DegenerateSetError).
+int orth_outcome(const Engine& E, OrthOut& o) {
+  const double* hs = E.hvec + E.off_scal();
+  o.offdiag_max = hs[Engine::S_MSTAT + 2];
+  o.diag_dev_max = hs[Engine::S_MSTAT + 3];
+  o.fallback = false;
+  if (hs[Engine::S_CHOL + 3] != 1.0) return 1;
+  const bool repaired = hs[Engine::S_QR2] != 0.0;
+  if (repaired && hs[Engine::S_CHOL2 + 3] != 1.0) return 2;
+  o.post_dev = hs[Engine::S_QR2 + 1] != 0.0 ? hs[Engine::S_MSTAT2] : -1.0;
+  return 0;
+}
+
 namespace {
 
 struct Solver {
@@ -187,24 +233,48 @@ struct Solver {
   double* P(const BRef& b) { return E.blk(*b); }
 
   SRef make_state(const BRef& u) {  // optimizer.cpp:224-229
+    SRef st = enqueue_state(u);
+    if (!st_fresh) return st;
+    E.fetch_all();
+    finish(st);
+    return st;
+  }
+
+  // enqueue build_hamiltonian(u) without waiting; finish() after the next fetch
+  bool st_fresh = false;
+  SRef enqueue_state(const BRef& u) {
+    st_fresh = false;
     if (!nonlinear && fixed_state) return fixed_state;
     SRef st = spool.get();
     E.poisson_solver = p.poisson_solver;
     E.build_state(P(u), p.hartree, p.xc, st.get(), have_prev_solve);
-    E.finish_state(st.get());
     if (p.hartree) have_prev_solve = true;
-    r->cg_iters_total += st->cg_iters;
     if (!nonlinear) fixed_state = st;
+    st_fresh = true;
     return st;
+  }
+  void finish(const SRef& st) {  // after a fetch covering the state build
+    E.state_results(st.get());
+    r->cg_iters_total += st->cg_iters;
   }
 
   // apply H and return the energy breakdown (energy.cpp:282-314) of u
+  // Nonlinear problems take E_ext = w <V_ext, rho> from the state built from u
+  // (energy.cpp:286-291 summed over orbitals); linear ones reuse a fixed state,
+  // so the stencil pass reduces <V_ext u_i, u_i> per orbital instead.
   EnergyParts apply_and_energy(const BRef& u, const BRef& hu, const DevState& st) {
-    E.apply_h(P(u), hu ? P(hu) : nullptr, st.v_local);
+    E.apply_h(P(u), hu ? P(hu) : nullptr, st.v_local, !nonlinear);
     E.fetch(0, (size_t)3 * E.N);
+    return energy_from_fetch(st);
+  }
+  EnergyParts energy_from_fetch(const DevState& st) {
     EnergyParts e;
     for (int i = 0; i < E.N; ++i) e.kinetic += E.occ * E.hvec[E.off_kin() + i];
-    for (int i = 0; i < E.N; ++i) e.external += E.occ * E.hvec[E.off_ext() + i];
+    if (nonlinear) {
+      e.external = st.e_ext;
+    } else {
+      for (int i = 0; i < E.N; ++i) e.external += E.occ * E.hvec[E.off_ext() + i];
+    }
     e.hartree = p.hartree ? st.e_hartree : 0.0;
     e.xc = p.xc ? st.e_xc : 0.0;
     e.total = e.kinetic + e.external + e.hartree + e.xc;
@@ -253,6 +323,11 @@ void Solver::init(const BRef& w0) {
   mean_abs = p.convergence_mode == PO_CONV_MEAN_ABS;
   ngd = (double)E.g.n0 * (double)E.g.n1 * (double)E.g.n2;
   (void)n;
+  // live blocks at most: w, hw, z, prev_w, prev_z, recovery, trial w/hw/scratch
+  // (+ rotation / mean-abs scratch); states: current, trial, recovery, spare
+  pool.reserve(p.n_diag > 0 || mean_abs ? 11 : 9);
+  spool.reserve(4);
+  E.sync();
   w = w0;
   state = make_state(w);
   hw = pool.get();
@@ -389,9 +464,11 @@ bool Solver::step() {
       prev_z = z;
       w = wn;
       history_valid = true;
-      state = make_state(w);
+      state = enqueue_state(w);
       BRef hn = pool.get();
-      E.apply_h(P(w), P(hn), state->v_local);
+      E.apply_h(P(w), P(hn), state->v_local, false);
+      E.fetch_all();
+      if (st_fresh) finish(state);
       hw = hn;
       sig_valid = true;
       --steps_until_orth;
@@ -409,17 +486,26 @@ bool Solver::step() {
         tau = tau_raw * std::pow(p.delta, s);
         if (s > 0 && tau < p.tau_min) break;
         wt = pool.get();
-        BRef rep;
-        auto scratch = [&]() -> double* {
-          rep = pool.get();
-          return P(rep);
-        };
-        if (!orthonormalize_dev(E, P(w), P(z), -tau, P(wt), scratch, p.verify_orthonormality != 0,
-                                orth))
-          continue;  // DegenerateSetError -> NaN trial energy
-        tstate = make_state(wt);
+        BRef rep = pool.get();
+        // one device pipeline per trial, one readback (energy + decisions)
+        orth_enqueue(E, P(w), P(z), -tau, P(wt), P(rep), p.verify_orthonormality != 0);
+        tstate = enqueue_state(wt);
         hwt = pool.get();
-        te = apply_and_energy(wt, hwt, *tstate);
+        E.apply_h(P(wt), P(hwt), tstate->v_local, !nonlinear);
+        E.fetch_all();
+        const int oc = orth_outcome(E, orth);
+        if (oc == 2) continue;  // DegenerateSetError -> NaN trial energy
+        if (oc == 1) {          // pass-1 Cholesky rejected: symmetric fallback, synchronously
+          auto scratch = [&]() -> double* { return P(rep); };
+          if (!orthonormalize_dev(E, P(w), P(z), -tau, P(wt), scratch,
+                                  p.verify_orthonormality != 0, orth))
+            continue;
+          tstate = make_state(wt);
+          te = apply_and_energy(wt, hwt, *tstate);
+        } else {
+          if (st_fresh) finish(tstate);
+          te = energy_from_fetch(*tstate);
+        }
         if (std::isfinite(te.total) && te.total <= nm_c - p.rho1 * tau * znorm2) {
           accepted = true;
           break;
@@ -438,7 +524,7 @@ bool Solver::step() {
         w = recovery_w;
         state = recovery_state;
         BRef hn = pool.get();
-        E.apply_h(P(w), P(hn), state->v_local);
+        E.apply_h(P(w), P(hn), state->v_local, false);
         hw = hn;
         sig_valid = true;
         history_valid = false;
@@ -630,7 +716,7 @@ int po_solve(po_engine* h, const po_params* p, int w_handle, po_result* r) {
     // finalize, optimizer.cpp:581-597: full Stiefel gradient at the final iterate
     po::SRef st = S.make_state(w);
     po::BRef hw = S.pool.get();
-    E.apply_h(E.blk(*w), E.blk(*hw), st->v_local);
+    E.apply_h(E.blk(*w), E.blk(*hw), st->v_local, false);
     S.sigma(w, hw);
     E.mix(E.blk(*w), nullptr, 0.0, E.dmat[4], -1.0, E.blk(*hw), 1.0, 0, nullptr,
           E.dvec + E.off_dd());
@@ -728,7 +814,7 @@ int po_solver_finish(po_solver* sv) {
     }
     po::SRef st = S.make_state(S.w);
     po::BRef hw = S.pool.get();
-    E.apply_h(E.blk(*S.w), E.blk(*hw), st->v_local);
+    E.apply_h(E.blk(*S.w), E.blk(*hw), st->v_local, false);
     S.sigma(S.w, hw);
     E.mix(E.blk(*S.w), nullptr, 0.0, E.dmat[4], -1.0, E.blk(*hw), 1.0, 0, nullptr,
           E.dvec + E.off_dd());

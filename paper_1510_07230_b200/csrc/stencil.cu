@@ -95,7 +95,120 @@ __global__ void __launch_bounds__(TX * TY) hamiltonian_kernel(
   }
 }
 
+// ---------------------------------------------------------------- v2
+// Same math, barrier-free and with deep memory-level parallelism: each thread
+// owns one (y, x) column and processes its z-range in groups of ZG planes.
+// For a group it issues ALL loads up front — own column z..z+ZG (the z-1 value
+// is carried), the y-1 / y+1 columns (L1/L2 hits: neighbouring warps stream
+// them), v_local (L2) and, when EXT, v_ext — then computes the ZG points.
+// x-neighbours come from warp shuffles (lane 0 / 31 load the tile edge).
+// Per orbital.point from HBM: one load, one store. EXT = per-orbital
+// <V_ext u, u> partials (C ABI / linear problems); the nonlinear solver takes
+// E_ext = w <V_ext, rho> from the density kernel instead.
+constexpr int ZG = 4;        // planes per load group
+constexpr int ZCHUNK2 = 32;  // planes per CTA
+
+template <bool EXT>
+__global__ void __launch_bounds__(TX * TY, 3) hamiltonian2_kernel(
+    SlabGeom g, int N, int ntx, const double* __restrict__ u, const double* __restrict__ halo_lo,
+    const double* __restrict__ halo_hi, const double* __restrict__ vloc,
+    const double* __restrict__ vext, double* __restrict__ out, double* __restrict__ partials) {
+  __shared__ double red[3 * 32];
+  const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
+  const int lane = threadIdx.x;
+  const int64_t x = (int64_t)tx * TX + lane;
+  const int64_t y = (int64_t)ty * TY + threadIdx.y;
+  const bool active = x < g.n2 && y < g.n1;
+  const int i = blockIdx.z;
+  const int64_t zs = (int64_t)blockIdx.y * ZCHUNK2;
+  const int64_t ze = min(zs + (int64_t)ZCHUNK2, g.nz);
+  const int64_t plane = g.plane;
+  const double* ui = u + (int64_t)i * g.ld;
+  double* oi = out ? out + (int64_t)i * g.ld : nullptr;
+  const int64_t col = y * g.n2 + x;
+  const double ih0 = g.ih2[0], ih1 = g.ih2[1], ih2 = g.ih2[2];
+  const bool has_ym = active && y > 0, has_yp = active && y + 1 < g.n1;
+  const bool has_xm = active && x > 0, has_xp = active && x + 1 < g.n2;
+
+  auto at = [&](int64_t z, int64_t c) -> double {  // u at (plane z, column c), halos/zero outside
+    if (z < 0) return halo_lo ? __ldg(halo_lo + (int64_t)i * plane + c) : 0.0;
+    if (z >= g.nz) return halo_hi ? __ldg(halo_hi + (int64_t)i * plane + c) : 0.0;
+    return __ldg(ui + z * plane + c);
+  };
+  double zm = active ? at(zs - 1, col) : 0.0;
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int64_t z0 = zs; z0 < ze; z0 += ZG) {
+    double cz[ZG + 1], ym[ZG], yp[ZG], v[ZG], ve[ZG], xe[ZG];
+#pragma unroll
+    for (int k = 0; k <= ZG; ++k) {
+      const int64_t z = z0 + k;
+      cz[k] = (active && z <= ze) ? at(z, col) : 0.0;  // plane ze = last point's z+1 neighbour
+    }
+#pragma unroll
+    for (int k = 0; k < ZG; ++k) {
+      const int64_t z = z0 + k;
+      const bool in = z < ze;
+      ym[k] = (in && has_ym) ? __ldg(ui + z * plane + col - g.n2) : 0.0;
+      yp[k] = (in && has_yp) ? __ldg(ui + z * plane + col + g.n2) : 0.0;
+      v[k] = (in && active) ? __ldg(vloc + z * plane + col) : 0.0;
+      if (EXT) ve[k] = (in && active) ? __ldg(vext + z * plane + col) : 0.0;
+      // tile-edge x neighbours (lane 0 needs x-1, lane 31 needs x+1)
+      xe[k] = 0.0;
+      if (in && lane == 0 && has_xm) xe[k] = __ldg(ui + z * plane + col - 1);
+      if (in && lane == TX - 1 && has_xp) xe[k] = __ldg(ui + z * plane + col + 1);
+    }
+#pragma unroll
+    for (int k = 0; k < ZG; ++k) {
+      const int64_t z = z0 + k;
+      if (z >= ze) break;
+      const double c = cz[k];
+      double xm = __shfl_up_sync(0xffffffffu, c, 1);
+      double xp = __shfl_down_sync(0xffffffffu, c, 1);
+      if (lane == 0) xm = xe[k];
+      if (lane == TX - 1) xp = xe[k];
+      if (!has_xp) xp = 0.0;
+      if (!has_xm) xm = 0.0;
+      if (active) {
+        const double lap = ((zm - 2.0 * c + cz[k + 1]) * ih0 + (ym[k] - 2.0 * c + yp[k]) * ih1) +
+                           (xm - 2.0 * c + xp) * ih2;
+        const double h = -0.5 * lap + v[k] * c;
+        if (oi) oi[z * plane + col] = h;
+        acc[0] += h * c;
+        acc[1] += lap * c;
+        if (EXT) acc[2] += ve[k] * c * c;
+      }
+      zm = c;
+    }
+  }
+  block_sum<3>(acc, &red[0]);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    const int nblk = gridDim.x * gridDim.y;
+    const int b = blockIdx.x + gridDim.x * blockIdx.y;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) partials[((int64_t)q * N + i) * nblk + b] = acc[q];
+  }
+}
+
 }  // namespace
+
+int hamiltonian2_nblk(const SlabGeom& g) {
+  HGrid h = hgrid(g);
+  return h.ntx * h.nty * (int)((g.nz + ZCHUNK2 - 1) / ZCHUNK2);
+}
+
+void launch_hamiltonian2(const SlabGeom& g, int N, const double* u, const double* halo_lo,
+                         const double* halo_hi, const double* v_local, const double* v_ext,
+                         double* hu, double* partials, cudaStream_t s) {
+  HGrid h = hgrid(g);
+  dim3 grid(h.ntx * h.nty, (unsigned)((g.nz + ZCHUNK2 - 1) / ZCHUNK2), N), block(TX, TY);
+  ::po::count_launch();
+  if (v_ext)
+    hamiltonian2_kernel<true><<<grid, block, 0, s>>>(g, N, h.ntx, u, halo_lo, halo_hi, v_local,
+                                                     v_ext, hu, partials);
+  else
+    hamiltonian2_kernel<false><<<grid, block, 0, s>>>(g, N, h.ntx, u, halo_lo, halo_hi, v_local,
+                                                      nullptr, hu, partials);
+}
 
 int hamiltonian_nblk(const SlabGeom& g) {
   HGrid h = hgrid(g);
