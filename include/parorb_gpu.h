@@ -245,7 +245,8 @@ enum {
   PO_OP_DENSITY_XC = 5,  /* rho, v_xc, 4 pi rho from block a */
   PO_OP_POISSON = 6,     /* CG solve on the last density (default state) */
   PO_OP_CHOLESKY = 7,    /* device Cholesky + L^{-T} of the last Gram */
-  PO_OP_LAPLACIAN = 8    /* out = lap a */
+  PO_OP_LAPLACIAN = 8,   /* out = lap a */
+  PO_OP_HAMILTONIAN_VARIANT = 100  /* + v: H a design-space variants (measurement only) */
 };
 int po_enqueue(po_engine* e, int op, int a, int b, int out);
 int po_set_matrix(po_engine* e, const double* m_host);

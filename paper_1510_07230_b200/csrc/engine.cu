@@ -725,6 +725,11 @@ extern "C" int po_enqueue(po_engine* h, int op, int a, int b, int out) {
       po::launch_laplacian(E.g, E.N, E.blk(a), nullptr, nullptr, E.blk(out), E.s);
       break;
     default:
+      if (op >= PO_OP_HAMILTONIAN_VARIANT &&
+          po::launch_hamiltonian_variant(op - PO_OP_HAMILTONIAN_VARIANT, E.g, E.N, E.blk(a),
+                                         st->v_local, E.v_ext, out >= 0 ? E.blk(out) : nullptr,
+                                         E.partials, E.s) == 0)
+        break;
       throw Error(PO_EINVAL, "unknown op");
   }
   PO_CUDA(cudaGetLastError());

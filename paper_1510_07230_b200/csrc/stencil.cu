@@ -105,11 +105,10 @@ __global__ void __launch_bounds__(TX * TY) hamiltonian_kernel(
 // Per orbital.point from HBM: one load, one store. EXT = per-orbital
 // <V_ext u, u> partials (C ABI / linear problems); the nonlinear solver takes
 // E_ext = w <V_ext, rho> from the density kernel instead.
-constexpr int ZG = 4;        // planes per load group
 constexpr int ZCHUNK2 = 32;  // planes per CTA
 
-template <bool EXT>
-__global__ void __launch_bounds__(TX * TY, 3) hamiltonian2_kernel(
+template <bool EXT, int ZG, int MINB>
+__global__ void __launch_bounds__(TX * TY, MINB) hamiltonian2_kernel(
     SlabGeom g, int N, int ntx, const double* __restrict__ u, const double* __restrict__ halo_lo,
     const double* __restrict__ halo_hi, const double* __restrict__ vloc,
     const double* __restrict__ vext, double* __restrict__ out, double* __restrict__ partials) {
@@ -189,9 +188,312 @@ __global__ void __launch_bounds__(TX * TY, 3) hamiltonian2_kernel(
   }
 }
 
+// ---------------------------------------------------------------- v3
+// Full-row tiles: a CTA owns TY whole x-rows (rows y0..y0+7 of a plane are one
+// contiguous TY*n2*8-byte chunk) for a z-range of one orbital; each thread holds
+// the J = ceil(n2/32) columns x = lane + 32 j of its row, so all x-neighbours
+// come from shuffles (chunk boundaries via lane-0/31 broadcasts) and every
+// plane is streamed as large contiguous pieces. y-neighbours are __ldg (L1:
+// the adjacent warps stream those rows). MAXJ bounds n2 <= 32 * MAXJ.
+constexpr int MAXJ = 8;
+
+template <int J, bool EXT>
+__global__ void __launch_bounds__(TX * TY, 2) hamiltonian3_kernel(
+    SlabGeom g, int N, const double* __restrict__ u, const double* __restrict__ halo_lo,
+    const double* __restrict__ halo_hi, const double* __restrict__ vloc,
+    const double* __restrict__ vext, double* __restrict__ out, double* __restrict__ partials) {
+  __shared__ double red[3 * 32];
+  const int lane = threadIdx.x;
+  const int64_t y = (int64_t)blockIdx.x * TY + threadIdx.y;
+  const bool yin = y < g.n1;
+  const int i = blockIdx.z;
+  const int64_t zs = (int64_t)blockIdx.y * ZCHUNK2;
+  const int64_t ze = min(zs + (int64_t)ZCHUNK2, g.nz);
+  const int64_t plane = g.plane;
+  const double* ui = u + (int64_t)i * g.ld;
+  double* oi = out ? out + (int64_t)i * g.ld : nullptr;
+  const double ih0 = g.ih2[0], ih1 = g.ih2[1], ih2 = g.ih2[2];
+  const bool has_ym = yin && y > 0, has_yp = yin && y + 1 < g.n1;
+  bool xin[J];
+  int64_t col[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int64_t x = lane + 32 * j;
+    xin[j] = yin && x < g.n2;
+    col[j] = y * g.n2 + x;
+  }
+  auto at = [&](int64_t z, int64_t c) -> double {
+    if (z < 0) return halo_lo ? __ldg(halo_lo + (int64_t)i * plane + c) : 0.0;
+    if (z >= g.nz) return halo_hi ? __ldg(halo_hi + (int64_t)i * plane + c) : 0.0;
+    return __ldg(ui + z * plane + c);
+  };
+  double zm[J], c[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    zm[j] = xin[j] ? at(zs - 1, col[j]) : 0.0;
+    c[j] = xin[j] ? at(zs, col[j]) : 0.0;
+  }
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int64_t z = zs; z < ze; ++z) {
+    double zp[J], ym[J], yp[J], v[J], ve[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      zp[j] = xin[j] ? at(z + 1, col[j]) : 0.0;
+      ym[j] = (xin[j] && has_ym) ? __ldg(ui + z * plane + col[j] - g.n2) : 0.0;
+      yp[j] = (xin[j] && has_yp) ? __ldg(ui + z * plane + col[j] + g.n2) : 0.0;
+      v[j] = xin[j] ? __ldg(vloc + z * plane + col[j]) : 0.0;
+      if (EXT) ve[j] = xin[j] ? __ldg(vext + z * plane + col[j]) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      double xm = __shfl_up_sync(0xffffffffu, c[j], 1);
+      double xp = __shfl_down_sync(0xffffffffu, c[j], 1);
+      const double prev31 = __shfl_sync(0xffffffffu, j > 0 ? c[j > 0 ? j - 1 : 0] : 0.0, 31);
+      const double next0 = __shfl_sync(0xffffffffu, j + 1 < J ? c[j + 1 < J ? j + 1 : 0] : 0.0, 0);
+      if (lane == 0) xm = prev31;        // x - 1 lives in the previous chunk (0 at x = 0)
+      if (lane == TX - 1) xp = next0;    // x + 1 lives in the next chunk
+      if (!(lane + 32 * j + 1 < g.n2)) xp = 0.0;
+      if (xin[j]) {
+        const double cc = c[j];
+        const double lap = ((zm[j] - 2.0 * cc + zp[j]) * ih0 + (ym[j] - 2.0 * cc + yp[j]) * ih1) +
+                           (xm - 2.0 * cc + xp) * ih2;
+        const double h = -0.5 * lap + v[j] * cc;
+        if (oi) oi[z * plane + col[j]] = h;
+        acc[0] += h * cc;
+        acc[1] += lap * cc;
+        if (EXT) acc[2] += ve[j] * cc * cc;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      zm[j] = c[j];
+      c[j] = zp[j];
+    }
+  }
+  block_sum<3>(acc, &red[0]);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    const int nblk = gridDim.x * gridDim.y;
+    const int b = blockIdx.x + gridDim.x * blockIdx.y;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) partials[((int64_t)q * N + i) * nblk + b] = acc[q];
+  }
+}
+
+template <bool EXT>
+void launch_h3(const SlabGeom& g, int N, const double* u, const double* lo, const double* hi,
+               const double* vloc, const double* vext, double* out, double* partials,
+               cudaStream_t s) {
+  dim3 grid((unsigned)((g.n1 + TY - 1) / TY), (unsigned)((g.nz + ZCHUNK2 - 1) / ZCHUNK2), N);
+  dim3 block(TX, TY);
+  switch ((g.n2 + 31) / 32) {
+#define PO_H3(JJ)                                                                               \
+  case JJ:                                                                                      \
+    hamiltonian3_kernel<JJ, EXT><<<grid, block, 0, s>>>(g, N, u, lo, hi, vloc, vext, out, partials); \
+    break;
+    PO_H3(1) PO_H3(2) PO_H3(3) PO_H3(4) PO_H3(5) PO_H3(6) PO_H3(7) PO_H3(8)
+#undef PO_H3
+  }
+}
+
+// ---------------------------------------------------------------- v4 (TMA)
+// Plane ring: a CTA owns TY full x-rows (y0 .. y0+TY-1) of ONE orbital over a
+// z-range. A producer warp streams, per plane, the contiguous block of rows
+// y0-1 .. y0+TY (one cp.async.bulk of (TY+2) * n2 * 8 bytes: 7.7 KB at 96^3,
+// far above the ~2 KB TMA efficiency threshold measured in
+// profiles/r1_tma_probe.txt) and the plane's v_local rows into an NST-deep
+// shared-memory ring; 8 consumer warps (one row each, x = lane + 32 j) read all
+// seven stencil taps from shared memory — no global loads in the compute —
+// and release a plane slot once the step that last needs it (z+1) is done.
+// Rows outside [0, n1) stay zero in the ring; planes outside the slab come
+// from the halo buffers (or are zero at the global boundary).
+constexpr int RTH = TX * TY + 32;  // 8 consumer warps + 1 producer warp
+
+struct PlaneRing {
+  int nst;
+  int64_t urow, vrow;  // doubles per u / v slot
+  size_t smem;
+};
+
+PlaneRing plane_ring(const SlabGeom& g) {
+  PlaneRing r;
+  r.urow = (TY + 2) * g.n2;
+  r.vrow = TY * g.n2;
+  const size_t per = (size_t)(r.urow + r.vrow) * 8;
+  int nst = (int)((100 * 1024) / per);
+  if (nst > 8) nst = 8;
+  if (nst < 4) nst = 4;
+  r.nst = nst;
+  r.smem = 256 + (size_t)nst * per;
+  return r;
+}
+
+__device__ __forceinline__ bool ring_plane_real(int64_t p, int64_t nz, const double* lo,
+                                                const double* hi) {
+  return (p >= 0 && p < nz) || (p < 0 && lo) || (p >= nz && hi);
+}
+
+template <int J, bool EXT>
+__global__ void __launch_bounds__(RTH, 1) hamiltonian4_kernel(
+    SlabGeom g, int N, int nst, const double* __restrict__ u, const double* __restrict__ halo_lo,
+    const double* __restrict__ halo_hi, const double* __restrict__ vloc,
+    const double* __restrict__ vext, double* __restrict__ out, double* __restrict__ partials) {
+  extern __shared__ __align__(128) unsigned char hsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(hsm);
+  uint64_t* empty = full + 8;
+  double* ring = reinterpret_cast<double*>(hsm + 256);
+  __shared__ double red[3 * 32];
+  const int64_t n1 = g.n1, n2 = g.n2, plane = g.plane;
+  const int64_t urow = (TY + 2) * n2, vrow = TY * n2;
+  const int64_t y0 = (int64_t)blockIdx.x * TY;
+  const int i = blockIdx.z;
+  const int64_t zs = (int64_t)blockIdx.y * ZCHUNK2;
+  const int64_t ze = min(zs + (int64_t)ZCHUNK2, g.nz);
+  const int nplanes = (int)(ze - zs) + 2;  // zs-1 .. ze
+  const double* ui = u + (int64_t)i * g.ld;
+  const int warp = threadIdx.y, lane = threadIdx.x;  // block (32, 9)
+  // valid row window [ra, rb) of the u slot (slot row r <-> grid row y0 - 1 + r)
+  const int64_t ra = y0 - 1 < 0 ? 1 : 0;
+  const int64_t rb = min((int64_t)TY + 2, n1 - (y0 - 1));
+  const int64_t vb = min((int64_t)TY, n1 - y0);
+  for (int64_t e = threadIdx.x + 32 * threadIdx.y; e < (int64_t)nst * (urow + vrow); e += RTH)
+    ring[e] = 0.0;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], TY);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == TY) {  // ------------------------------------------------ producer
+    if (lane == 0) {
+      // order the generic-proxy zero fill before the async-proxy (TMA) writes
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      for (int k = 0; k < nplanes; ++k) {
+        const int s = k % nst;
+        if (k >= nst) mbar_wait(&empty[s], (uint32_t)((k / nst) - 1) & 1u);
+        const int64_t p = zs - 1 + k;
+        double* us = ring + (int64_t)s * (urow + vrow);
+        const bool real = ring_plane_real(p, g.nz, halo_lo, halo_hi);
+        const bool center = p >= zs && p < ze;
+        uint32_t bytes = 0;
+        if (real) bytes += (uint32_t)((rb - ra) * n2 * 8);
+        if (center) bytes += (uint32_t)(vb * n2 * 8);
+        mbar_arrive_expect_tx(&full[s], bytes);
+        if (real) {
+          const double* src;
+          if (p < 0) src = halo_lo + (int64_t)i * plane;
+          else if (p >= g.nz) src = halo_hi + (int64_t)i * plane;
+          else src = ui + p * plane;
+          tma_load_1d(us + ra * n2, src + (y0 - 1 + ra) * n2, (uint32_t)((rb - ra) * n2 * 8),
+                      &full[s]);
+        }
+        if (center)
+          tma_load_1d(us + urow, vloc + p * plane + y0 * n2, (uint32_t)(vb * n2 * 8), &full[s]);
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------------ consumers
+  const int64_t y = y0 + warp;
+  const bool yin = y < n1;
+  const double ih0 = g.ih2[0], ih1 = g.ih2[1], ih2 = g.ih2[2];
+  double* oi = out ? out + (int64_t)i * g.ld : nullptr;
+  double acc[3] = {0.0, 0.0, 0.0};
+  auto slot = [&](int k) { return ring + (int64_t)(k % nst) * (urow + vrow); };
+  auto real_k = [&](int k) { return ring_plane_real(zs - 1 + k, g.nz, halo_lo, halo_hi); };
+  // planes k = 0 (zs-1) and 1 (zs) before the first step
+  mbar_wait(&full[0], 0);
+  mbar_wait(&full[1 % nst], (uint32_t)(1 / nst) & 1u);
+  for (int k = 1; k + 1 < nplanes; ++k) {  // step on plane z = zs - 1 + k
+    const int kn = k + 1;
+    mbar_wait(&full[kn % nst], (uint32_t)(kn / nst) & 1u);
+    const double* pm = slot(k - 1);
+    const double* pc = slot(k);
+    const double* pp = slot(kn);
+    const bool rm = real_k(k - 1), rp = real_k(kn);
+    const int64_t z = zs - 1 + k;
+    if (yin) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int64_t x = lane + 32 * j;
+        if (x < n2) {
+          const int64_t r = (warp + 1) * n2 + x;  // slot row of y
+          const double c = pc[r];
+          const double zm = rm ? pm[r] : 0.0;
+          const double zp = rp ? pp[r] : 0.0;
+          const double ym = pc[r - n2];  // zero rows outside the box
+          const double yp = pc[r + n2];
+          const double xm = x > 0 ? pc[r - 1] : 0.0;
+          const double xp = x + 1 < n2 ? pc[r + 1] : 0.0;
+          const double lap = ((zm - 2.0 * c + zp) * ih0 + (ym - 2.0 * c + yp) * ih1) +
+                             (xm - 2.0 * c + xp) * ih2;
+          const double h = -0.5 * lap + pc[urow + warp * n2 + x] * c;
+          if (oi) oi[z * plane + y * n2 + x] = h;
+          acc[0] += h * c;
+          acc[1] += lap * c;
+          if (EXT) acc[2] += __ldg(vext + z * plane + y * n2 + x) * c * c;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[(k - 1) % nst]);  // plane k-1 is no longer needed
+  }
+  // the last two planes' slots are never re-filled: no arrivals needed
+  {
+    // block reduction over the 8 consumer warps (the producer warp has exited)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) acc[q] = warp_sum(acc[q]);
+    if (lane == 0)
+      for (int q = 0; q < 3; ++q) red[q * 32 + warp] = acc[q];
+    asm volatile("bar.sync 1, %0;" ::"n"(TX * TY));
+    if (warp == 0) {
+      double v[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) v[q] = warp_sum(lane < TY ? red[q * 32 + lane] : 0.0);
+      if (lane == 0) {
+        const int nblk = gridDim.x * gridDim.y;
+        const int b = blockIdx.x + gridDim.x * blockIdx.y;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) partials[((int64_t)q * N + i) * nblk + b] = v[q];
+      }
+    }
+  }
+}
+
+template <bool EXT>
+void launch_h4(const SlabGeom& g, int N, const double* u, const double* lo, const double* hi,
+               const double* vloc, const double* vext, double* out, double* partials,
+               cudaStream_t s) {
+  const PlaneRing r = plane_ring(g);
+  dim3 grid((unsigned)((g.n1 + TY - 1) / TY), (unsigned)((g.nz + ZCHUNK2 - 1) / ZCHUNK2), N);
+  dim3 block(TX, TY + 1);
+  switch ((g.n2 + 31) / 32) {
+#define PO_H4(JJ)                                                                          \
+  case JJ: {                                                                               \
+    auto k = hamiltonian4_kernel<JJ, EXT>;                                                  \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r.smem);     \
+    k<<<grid, block, r.smem, s>>>(g, N, r.nst, u, lo, hi, vloc, vext, out, partials);      \
+    break;                                                                                 \
+  }
+    PO_H4(1) PO_H4(2) PO_H4(3) PO_H4(4) PO_H4(5) PO_H4(6) PO_H4(7) PO_H4(8)
+#undef PO_H4
+  }
+}
+
+bool h4_supported(const SlabGeom& g) {
+  // bulk copies need 16-byte multiples / alignment: even n2 (plane rows of 8 n2 bytes)
+  return g.n2 % 2 == 0 && g.n2 <= 32 * MAXJ && (g.ld % 2 == 0);
+}
+
 }  // namespace
 
+int hamiltonian3_nblk(const SlabGeom& g) {
+  return (int)((g.n1 + TY - 1) / TY) * (int)((g.nz + ZCHUNK2 - 1) / ZCHUNK2);
+}
+
 int hamiltonian2_nblk(const SlabGeom& g) {
+  if (h4_supported(g)) return hamiltonian3_nblk(g);  // TMA ring: same (y-tile, z-chunk) grid
   HGrid h = hgrid(g);
   return h.ntx * h.nty * (int)((g.nz + ZCHUNK2 - 1) / ZCHUNK2);
 }
@@ -199,15 +501,72 @@ int hamiltonian2_nblk(const SlabGeom& g) {
 void launch_hamiltonian2(const SlabGeom& g, int N, const double* u, const double* halo_lo,
                          const double* halo_hi, const double* v_local, const double* v_ext,
                          double* hu, double* partials, cudaStream_t s) {
+  if (h4_supported(g)) {  // production path: TMA plane ring
+    ::po::count_launch();
+    if (v_ext)
+      launch_h4<true>(g, N, u, halo_lo, halo_hi, v_local, v_ext, hu, partials, s);
+    else
+      launch_h4<false>(g, N, u, halo_lo, halo_hi, v_local, nullptr, hu, partials, s);
+    return;
+  }
   HGrid h = hgrid(g);
   dim3 grid(h.ntx * h.nty, (unsigned)((g.nz + ZCHUNK2 - 1) / ZCHUNK2), N), block(TX, TY);
   ::po::count_launch();
   if (v_ext)
-    hamiltonian2_kernel<true><<<grid, block, 0, s>>>(g, N, h.ntx, u, halo_lo, halo_hi, v_local,
-                                                     v_ext, hu, partials);
+    hamiltonian2_kernel<true, 4, 3><<<grid, block, 0, s>>>(g, N, h.ntx, u, halo_lo, halo_hi,
+                                                           v_local, v_ext, hu, partials);
   else
-    hamiltonian2_kernel<false><<<grid, block, 0, s>>>(g, N, h.ntx, u, halo_lo, halo_hi, v_local,
-                                                      nullptr, hu, partials);
+    hamiltonian2_kernel<false, 4, 3><<<grid, block, 0, s>>>(g, N, h.ntx, u, halo_lo, halo_hi,
+                                                            v_local, nullptr, hu, partials);
+}
+
+// Design-space probe (po_enqueue(PO_OP_HAMILTONIAN_VARIANT + v)): same math,
+// different register-group depth / occupancy; v = 0 is the first-generation
+// kernel (per-point neighbour loads, with V_ext).
+int launch_hamiltonian_variant(int v, const SlabGeom& g, int N, const double* u,
+                               const double* v_local, const double* v_ext, double* hu,
+                               double* partials, cudaStream_t s) {
+  HGrid h = hgrid(g);
+  dim3 grid(h.ntx * h.nty, (unsigned)((g.nz + ZCHUNK2 - 1) / ZCHUNK2), N), block(TX, TY);
+  ::po::count_launch();
+  switch (v) {
+    case 0:
+      launch_hamiltonian(g, N, u, nullptr, nullptr, v_local, v_ext, hu, partials, s);
+      return 0;
+    case 1:
+      hamiltonian2_kernel<false, 4, 3><<<grid, block, 0, s>>>(g, N, h.ntx, u, nullptr, nullptr,
+                                                              v_local, nullptr, hu, partials);
+      return 0;
+    case 2:
+      hamiltonian2_kernel<false, 2, 4><<<grid, block, 0, s>>>(g, N, h.ntx, u, nullptr, nullptr,
+                                                              v_local, nullptr, hu, partials);
+      return 0;
+    case 3:
+      hamiltonian2_kernel<false, 4, 2><<<grid, block, 0, s>>>(g, N, h.ntx, u, nullptr, nullptr,
+                                                              v_local, nullptr, hu, partials);
+      return 0;
+    case 4:
+      hamiltonian2_kernel<false, 8, 2><<<grid, block, 0, s>>>(g, N, h.ntx, u, nullptr, nullptr,
+                                                              v_local, nullptr, hu, partials);
+      return 0;
+    case 5:
+      hamiltonian2_kernel<false, 2, 5><<<grid, block, 0, s>>>(g, N, h.ntx, u, nullptr, nullptr,
+                                                              v_local, nullptr, hu, partials);
+      return 0;
+    case 6:
+      hamiltonian2_kernel<false, 1, 6><<<grid, block, 0, s>>>(g, N, h.ntx, u, nullptr, nullptr,
+                                                              v_local, nullptr, hu, partials);
+      return 0;
+    case 7:
+      if (g.n2 > 32 * MAXJ) return -1;
+      launch_h3<false>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s);
+      return 0;
+    case 8:
+      if (!h4_supported(g)) return -1;
+      launch_h4<false>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s);
+      return 0;
+  }
+  return -1;
 }
 
 int hamiltonian_nblk(const SlabGeom& g) {
