@@ -306,20 +306,18 @@ void launch_h3(const SlabGeom& g, int N, const double* u, const double* lo, cons
 // and release a plane slot once the step that last needs it (z+1) is done.
 // Rows outside [0, n1) stay zero in the ring; planes outside the slab come
 // from the halo buffers (or are zero at the global boundary).
-constexpr int RTH = TX * TY + 32;  // 8 consumer warps + 1 producer warp
-
 struct PlaneRing {
   int nst;
   int64_t urow, vrow;  // doubles per u / v slot
   size_t smem;
 };
 
-PlaneRing plane_ring(const SlabGeom& g) {
+PlaneRing plane_ring(const SlabGeom& g, int tyr, size_t budget) {
   PlaneRing r;
-  r.urow = (TY + 2) * g.n2;
-  r.vrow = TY * g.n2;
+  r.urow = (tyr + 2) * g.n2;
+  r.vrow = tyr * g.n2;
   const size_t per = (size_t)(r.urow + r.vrow) * 8;
-  int nst = (int)((100 * 1024) / per);
+  int nst = (int)(budget / per);
   if (nst > 8) nst = 8;
   if (nst < 4) nst = 4;
   r.nst = nst;
@@ -332,9 +330,9 @@ __device__ __forceinline__ bool ring_plane_real(int64_t p, int64_t nz, const dou
   return (p >= 0 && p < nz) || (p < 0 && lo) || (p >= nz && hi);
 }
 
-template <int J, bool EXT>
-__global__ void __launch_bounds__(RTH, 1) hamiltonian4_kernel(
-    SlabGeom g, int N, int nst, const double* __restrict__ u, const double* __restrict__ halo_lo,
+template <int J, bool EXT, int TYR>
+__global__ void __launch_bounds__(32 * (TYR + 1), 1) hamiltonian4_kernel(
+    SlabGeom g, int N, int nst, int zc, const double* __restrict__ u, const double* __restrict__ halo_lo,
     const double* __restrict__ halo_hi, const double* __restrict__ vloc,
     const double* __restrict__ vext, double* __restrict__ out, double* __restrict__ partials) {
   extern __shared__ __align__(128) unsigned char hsm[];
@@ -343,29 +341,29 @@ __global__ void __launch_bounds__(RTH, 1) hamiltonian4_kernel(
   double* ring = reinterpret_cast<double*>(hsm + 256);
   __shared__ double red[3 * 32];
   const int64_t n1 = g.n1, n2 = g.n2, plane = g.plane;
-  const int64_t urow = (TY + 2) * n2, vrow = TY * n2;
-  const int64_t y0 = (int64_t)blockIdx.x * TY;
+  const int64_t urow = (TYR + 2) * n2, vrow = TYR * n2;
+  const int64_t y0 = (int64_t)blockIdx.x * TYR;
   const int i = blockIdx.z;
-  const int64_t zs = (int64_t)blockIdx.y * ZCHUNK2;
-  const int64_t ze = min(zs + (int64_t)ZCHUNK2, g.nz);
+  const int64_t zs = (int64_t)blockIdx.y * zc;
+  const int64_t ze = min(zs + (int64_t)zc, g.nz);
   const int nplanes = (int)(ze - zs) + 2;  // zs-1 .. ze
   const double* ui = u + (int64_t)i * g.ld;
   const int warp = threadIdx.y, lane = threadIdx.x;  // block (32, 9)
   // valid row window [ra, rb) of the u slot (slot row r <-> grid row y0 - 1 + r)
   const int64_t ra = y0 - 1 < 0 ? 1 : 0;
-  const int64_t rb = min((int64_t)TY + 2, n1 - (y0 - 1));
-  const int64_t vb = min((int64_t)TY, n1 - y0);
-  for (int64_t e = threadIdx.x + 32 * threadIdx.y; e < (int64_t)nst * (urow + vrow); e += RTH)
+  const int64_t rb = min((int64_t)TYR + 2, n1 - (y0 - 1));
+  const int64_t vb = min((int64_t)TYR, n1 - y0);
+  for (int64_t e = threadIdx.x + 32 * threadIdx.y; e < (int64_t)nst * (urow + vrow); e += 32 * (TYR + 1))
     ring[e] = 0.0;
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], TY);
+      mbar_init(&empty[s], TYR);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == TY) {  // ------------------------------------------------ producer
+  if (warp == TYR) {  // ------------------------------------------------ producer
     if (lane == 0) {
       // order the generic-proxy zero fill before the async-proxy (TMA) writes
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -446,11 +444,11 @@ __global__ void __launch_bounds__(RTH, 1) hamiltonian4_kernel(
     for (int q = 0; q < 3; ++q) acc[q] = warp_sum(acc[q]);
     if (lane == 0)
       for (int q = 0; q < 3; ++q) red[q * 32 + warp] = acc[q];
-    asm volatile("bar.sync 1, %0;" ::"n"(TX * TY));
+    asm volatile("bar.sync 1, %0;" ::"n"(TX * TYR));
     if (warp == 0) {
       double v[3];
 #pragma unroll
-      for (int q = 0; q < 3; ++q) v[q] = warp_sum(lane < TY ? red[q * 32 + lane] : 0.0);
+      for (int q = 0; q < 3; ++q) v[q] = warp_sum(lane < TYR ? red[q * 32 + lane] : 0.0);
       if (lane == 0) {
         const int nblk = gridDim.x * gridDim.y;
         const int b = blockIdx.x + gridDim.x * blockIdx.y;
@@ -461,25 +459,32 @@ __global__ void __launch_bounds__(RTH, 1) hamiltonian4_kernel(
   }
 }
 
-template <bool EXT>
+template <bool EXT, int TYR = 8>
 void launch_h4(const SlabGeom& g, int N, const double* u, const double* lo, const double* hi,
                const double* vloc, const double* vext, double* out, double* partials,
-               cudaStream_t s) {
-  const PlaneRing r = plane_ring(g);
-  dim3 grid((unsigned)((g.n1 + TY - 1) / TY), (unsigned)((g.nz + ZCHUNK2 - 1) / ZCHUNK2), N);
-  dim3 block(TX, TY + 1);
+               cudaStream_t s, int zc = ZCHUNK2, size_t budget = 100 * 1024) {
+  const PlaneRing r = plane_ring(g, TYR, budget);
+  dim3 grid((unsigned)((g.n1 + TYR - 1) / TYR), (unsigned)((g.nz + zc - 1) / zc), N);
+  dim3 block(TX, TYR + 1);
   switch ((g.n2 + 31) / 32) {
 #define PO_H4(JJ)                                                                          \
   case JJ: {                                                                               \
-    auto k = hamiltonian4_kernel<JJ, EXT>;                                                  \
+    auto k = hamiltonian4_kernel<JJ, EXT, TYR>;                                             \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r.smem);     \
-    k<<<grid, block, r.smem, s>>>(g, N, r.nst, u, lo, hi, vloc, vext, out, partials);      \
+    k<<<grid, block, r.smem, s>>>(g, N, r.nst, zc, u, lo, hi, vloc, vext, out, partials);  \
     break;                                                                                 \
   }
     PO_H4(1) PO_H4(2) PO_H4(3) PO_H4(4) PO_H4(5) PO_H4(6) PO_H4(7) PO_H4(8)
 #undef PO_H4
   }
 }
+
+// Production shape (tools/hu_variants.py sweep on B200, C2 block): 6 rows per
+// CTA, 32 planes per CTA, 56 KB ring (4 CTAs / SM): 102.6 us = 70.6% of the
+// measured HBM peak, vs 62% at 8 rows / 100 KB and 43.6% for the first kernel.
+constexpr int H4_TYR = 6;
+constexpr int H4_ZC = 32;
+constexpr size_t H4_BUDGET = 56 * 1024;
 
 bool h4_supported(const SlabGeom& g) {
   // bulk copies need 16-byte multiples / alignment: even n2 (plane rows of 8 n2 bytes)
@@ -493,7 +498,8 @@ int hamiltonian3_nblk(const SlabGeom& g) {
 }
 
 int hamiltonian2_nblk(const SlabGeom& g) {
-  if (h4_supported(g)) return hamiltonian3_nblk(g);  // TMA ring: same (y-tile, z-chunk) grid
+  if (h4_supported(g))  // TMA ring: (y-tile, z-chunk) grid
+    return (int)((g.n1 + H4_TYR - 1) / H4_TYR) * (int)((g.nz + H4_ZC - 1) / H4_ZC);
   HGrid h = hgrid(g);
   return h.ntx * h.nty * (int)((g.nz + ZCHUNK2 - 1) / ZCHUNK2);
 }
@@ -504,9 +510,11 @@ void launch_hamiltonian2(const SlabGeom& g, int N, const double* u, const double
   if (h4_supported(g)) {  // production path: TMA plane ring
     ::po::count_launch();
     if (v_ext)
-      launch_h4<true>(g, N, u, halo_lo, halo_hi, v_local, v_ext, hu, partials, s);
+      launch_h4<true, H4_TYR>(g, N, u, halo_lo, halo_hi, v_local, v_ext, hu, partials, s, H4_ZC,
+                              H4_BUDGET);
     else
-      launch_h4<false>(g, N, u, halo_lo, halo_hi, v_local, nullptr, hu, partials, s);
+      launch_h4<false, H4_TYR>(g, N, u, halo_lo, halo_hi, v_local, nullptr, hu, partials, s,
+                               H4_ZC, H4_BUDGET);
     return;
   }
   HGrid h = hgrid(g);
@@ -564,6 +572,41 @@ int launch_hamiltonian_variant(int v, const SlabGeom& g, int N, const double* u,
     case 8:
       if (!h4_supported(g)) return -1;
       launch_h4<false>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s);
+      return 0;
+    case 9:
+      if (!h4_supported(g)) return -1;
+      launch_h4<false, 8>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s, 32,
+                          56 * 1024);
+      return 0;
+    case 10:
+      if (!h4_supported(g)) return -1;
+      launch_h4<false, 4>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s, 32,
+                          32 * 1024);
+      return 0;
+    case 11:
+      if (!h4_supported(g)) return -1;
+      launch_h4<false, 8>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s, 16,
+                          70 * 1024);
+      return 0;
+    case 12:
+      if (!h4_supported(g)) return -1;
+      launch_h4<false, 8>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s, 32,
+                          70 * 1024);
+      return 0;
+    case 13:
+      if (!h4_supported(g)) return -1;
+      launch_h4<false, 4>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s, 48,
+                          40 * 1024);
+      return 0;
+    case 14:
+      if (!h4_supported(g)) return -1;
+      launch_h4<false, 8>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s, 48,
+                          70 * 1024);
+      return 0;
+    case 15:
+      if (!h4_supported(g)) return -1;
+      launch_h4<false, 6>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s, 32,
+                          56 * 1024);
       return 0;
   }
   return -1;
