@@ -54,7 +54,9 @@ __device__ __forceinline__ void block_sum(double (&v)[NQ], double* smem /* >= 32
 // Fragments: a = A[lane/4][lane%4], b = B[lane%4][lane/4],
 //            c[j] = C[lane/4][2*(lane%4) + j].
 __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
-  asm volatile(
+  // not volatile: no side effects beyond its outputs, so the scheduler may
+  // interleave independent DMMAs with the fragment loads around them
+  asm(
       "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
       : "+d"(c[0]), "+d"(c[1])
       : "d"(a), "d"(b));

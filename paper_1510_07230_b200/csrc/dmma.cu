@@ -768,6 +768,7 @@ void launch_gram(const SlabGeom& g, int N, const double* A, const double* Ab, do
                  const double* B, const double* Bb, double sb, int sym, double* ws, double* G,
                  cudaStream_t s, const double* guard) {
   if (gram_small_ok(N, sym)) {
+    if (launch_gram_tma(N, g.ld, sym, A, Ab, sa, B, Bb, sb, ws, G, g.w, s, guard)) return;
     switch ((N + 7) / 8) {
 #define PO_GS(F)                                                                  \
   case F:                                                                         \
@@ -806,7 +807,10 @@ int mix_nblk_max(const SlabGeom& g) {
 int launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, double sa,
                const double* M, double alpha, const double* C, double beta, int upper,
                double* out, double* norms, cudaStream_t s, const double* guard) {
-  if (N <= 64) {  // small-N LDG-staged path (returns its partials row length)
+  if (N <= 64) {  // small-N paths (return their partials row length)
+    const int nb = launch_mix_tma(N, g.ld, g.ngl, A, Ab, sa, M, alpha, C, beta, upper, out, norms,
+                                  s, guard);
+    if (nb >= 0) return nb;
     switch ((N + 7) / 8) {
 #define PO_MS(F) \
   case F:        \

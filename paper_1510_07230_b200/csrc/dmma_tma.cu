@@ -1,0 +1,472 @@
+// Small-N (N <= 64) tall-skinny contractions fed by 2D tensor-map TMA.
+//
+// Measured on B200 (profiles/r1_tma_probe.txt): 1D bulk copies are request-rate
+// bound — one 512 B row segment per request caps a ring at ~2.1 TB/s — so the
+// stage of an N-row block is fetched as 2D boxes {16 points x NPAD rows}
+// (NPAD x 128 B = 5 KB at N = 33) with cp.async.bulk.tensor: one request per
+// box, rows >= N zero-filled by the TMA unit (out-of-bounds fill), 128-byte
+// swizzle so the DMMA fragment reads (8 rows x one 16-B chunk) are
+// bank-conflict free. A producer warp keeps an NST-deep ring full; eight
+// consumer warps run mma.sync.m8n8k4.f64 (DMMA) from shared memory.
+//   gram: G = w (A + sa Ab)^T (B + sb Bb)        (manifold.cpp:41-61)
+//   mix : out = alpha (A + sa Ab) M + beta C     (manifold.cpp:67-85, 181-202)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "kernels.h"
+
+namespace po {
+
+namespace {
+
+constexpr int BOX = 16;           // points per box (128 B rows, SWIZZLE_128B)
+constexpr int TKS = 64;           // points per stage (4 boxes)
+constexpr int TSC = 8;            // consumer warps
+constexpr int TTH = (TSC + 1) * 32;
+constexpr size_t TBUDGET = 180 * 1024;
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// rows x ld doubles, row stride ld; box {16, npad}
+bool make_map(CUtensorMap* m, const double* base, int64_t ld, int rows, int npad) {
+  auto fn = encode_fn();
+  if (!fn || !base) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {BOX, (cuuint32_t)npad};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct Maps {
+  CUtensorMap m[4];
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// swizzled address of element (row, point p in the stage) in a source's stage area:
+// [box b = p / 16][row][16 doubles], 16-byte chunk j = (p % 16) / 2 stored at j ^ (row & 7)
+__device__ __forceinline__ int swz(int row, int p, int npad) {
+  const int b = p >> 4, o = p & 15;
+  const int j = (o >> 1) ^ (row & 7);
+  return (b * npad + row) * BOX + j * 2 + (o & 1);
+}
+
+struct TCfg {
+  int nst;
+  size_t stage_doubles, smem;
+};
+
+TCfg tcfg(int nsrc, int npad, size_t extra_doubles) {
+  TCfg c;
+  c.stage_doubles = (size_t)nsrc * (TKS / BOX) * npad * BOX;
+  const size_t avail = TBUDGET / 8 - extra_doubles;
+  c.nst = (int)(avail / c.stage_doubles);
+  if (c.nst > 6) c.nst = 6;
+  if (c.nst < 2) c.nst = 2;
+  c.smem = 2048 /*barriers + alignment slack*/ + ((size_t)c.nst * c.stage_doubles + extra_doubles) * 8;
+  return c;
+}
+
+// producer warp, lane 0: one 2D box per (source, box) per stage
+__device__ __forceinline__ void tma_produce(const CUtensorMap* maps, int nsrc, int npad,
+                                            int64_t kbeg, int64_t kend, int nst, size_t sdoubles,
+                                            double* stage0, uint64_t* full, uint64_t* empty) {
+  const int nstage = kend > kbeg ? (int)((kend - kbeg + TKS - 1) / TKS) : 0;
+  const uint32_t bytes = (uint32_t)(nsrc * (TKS / BOX) * npad * BOX * 8);
+  for (int st = 0; st < nstage; ++st) {
+    const int s = st % nst;
+    if (st >= nst) mbar_wait(&empty[s], ((uint32_t)(st / nst) & 1u) ^ 1u);
+    mbar_arrive_expect_tx(&full[s], bytes);
+    const int64_t k0 = kbeg + (int64_t)st * TKS;
+    double* sb = stage0 + (size_t)s * sdoubles;
+    for (int q = 0; q < nsrc; ++q)
+      for (int b = 0; b < TKS / BOX; ++b)
+        tma_load_2d(sb + ((size_t)q * (TKS / BOX) + b) * npad * BOX, &maps[q], (int)(k0 + b * BOX),
+                    0, &full[s]);
+  }
+}
+
+template <int F, bool SYM>
+struct TPairs {
+  static constexpr int NP = SYM ? F * (F + 1) / 2 : F * F;
+};
+
+template <int F, bool SYM>
+__global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant__ Maps maps,
+                                                          int nsrc, int qa_b, int qb, int qb_b,
+                                                          int64_t ld, int64_t kchunk, int nst,
+                                                          double sa, double sb,
+                                                          double* __restrict__ ws,
+                                                          const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;
+  constexpr int NP = TPairs<F, SYM>::NP;
+  constexpr int NPAD = 8 * F;
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  // SWIZZLE_128B boxes need 1024-byte aligned destinations
+  unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
+  uint64_t* empty = full + 8;
+  double* stage0 = reinterpret_cast<double*>(tsm + 1024);
+  const size_t sdoubles = (size_t)nsrc * (TKS / BOX) * NPAD * BOX;
+  const size_t qstride = (size_t)(TKS / BOX) * NPAD * BOX;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], TSC);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t kbeg = (int64_t)blockIdx.x * kchunk;
+  const int64_t kend = min(kbeg + kchunk, ld);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, t4 = lane & 3;
+  double acc[NP][2];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) acc[q][0] = acc[q][1] = 0.0;
+  if (warp == TSC) {
+    if (lane == 0) {
+      for (int q = 0; q < nsrc; ++q)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[q])));
+      tma_produce(maps.m, nsrc, NPAD, kbeg, kend, nst, sdoubles, stage0, full, empty);
+    }
+  } else {
+    const int nstage = kend > kbeg ? (int)((kend - kbeg + TKS - 1) / TKS) : 0;
+    const int c = warp * 8;  // this warp's 8-point chunk of every stage
+    for (int st = 0; st < nstage; ++st) {
+      const int s = st % nst;
+      mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+      const double* sbuf = stage0 + (size_t)s * sdoubles;
+      double2 a[F], b[SYM ? 1 : F];
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const int off = swz(8 * f + gq, c + 2 * t4, NPAD);  // 16-B aligned pair of points
+        a[f] = *reinterpret_cast<const double2*>(sbuf + off);
+        if (qa_b >= 0) {
+          const double2 z = *reinterpret_cast<const double2*>(sbuf + qa_b * qstride + off);
+          a[f].x += sa * z.x;
+          a[f].y += sa * z.y;
+        }
+        if constexpr (!SYM) {
+          b[f] = *reinterpret_cast<const double2*>(sbuf + qb * qstride + off);
+          if (qb_b >= 0) {
+            const double2 z = *reinterpret_cast<const double2*>(sbuf + qb_b * qstride + off);
+            b[f].x += sb * z.x;
+            b[f].y += sb * z.y;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // fragments are in registers: release early
+      int q = 0;
+#pragma unroll
+      for (int fm = 0; fm < F; ++fm)
+#pragma unroll
+        for (int fn = SYM ? fm : 0; fn < F; ++fn, ++q) {
+          const double2 bv = SYM ? a[fn] : b[SYM ? 0 : fn];
+          dmma_8x8x4(acc[q], a[fm].x, bv.x);
+          dmma_8x8x4(acc[q], a[fm].y, bv.y);
+        }
+    }
+  }
+  __syncthreads();
+  double* red = stage0;  // reuse the ring: [8 warps][NP * 64]
+  if (warp < TSC) {
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      red[(warp * NP + q) * 64 + lane * 2] = acc[q][0];
+      red[(warp * NP + q) * 64 + lane * 2 + 1] = acc[q][1];
+    }
+  }
+  __syncthreads();
+  double* out = ws + (int64_t)blockIdx.x * NPAD * NPAD;
+  for (int e = threadIdx.x; e < NP * 64; e += TTH) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < TSC; ++w) sum += red[(w * NP) * 64 + e];
+    const int q = e / 64, l = (e % 64) / 2, j = e % 2;
+    int fm = 0, fn = 0, cq = 0;
+    for (int m = 0; m < F; ++m)
+      for (int n = SYM ? m : 0; n < F; ++n, ++cq)
+        if (cq == q) {
+          fm = m;
+          fn = n;
+        }
+    out[(8 * fm + (l >> 2)) * NPAD + 8 * fn + 2 * (l & 3) + j] = sum;
+  }
+}
+
+__global__ void gram_tma_reduce_kernel(int N, int npad, int sym, int nsplit, double w,
+                                       const double* __restrict__ ws, double* __restrict__ G,
+                                       const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= (int64_t)N * N) return;
+  int i = (int)(wid / N), j = (int)(wid % N);
+  if (sym && j < i) {
+    const int t = i;
+    i = j;
+    j = t;
+  }
+  double s = 0.0;
+  for (int k = lane; k < nsplit; k += 32) s += ws[(int64_t)k * npad * npad + i * npad + j];
+  s = warp_sum(s);
+  if (lane == 0) G[wid] = w * s;
+}
+
+int g_nsm = 0;
+int nsm() {
+  if (!g_nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_nsm;
+}
+
+template <int F>
+bool launch_gram_tma_f(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
+                       const double* B, const double* Bb, double sb, double* ws, double* G,
+                       double w, cudaStream_t s, const double* guard) {
+  constexpr int NPAD = 8 * F;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  int nsrc = 0, qa_b = -1, qb = 0, qb_b = -1;
+  if (!make_map(&maps.m[nsrc++], A, ld, N, NPAD)) return false;
+  if (Ab) {
+    qa_b = nsrc;
+    if (!make_map(&maps.m[nsrc++], Ab, ld, N, NPAD)) return false;
+  }
+  if (!sym) {
+    qb = nsrc;
+    if (!make_map(&maps.m[nsrc++], B, ld, N, NPAD)) return false;
+    if (Bb) {
+      qb_b = nsrc;
+      if (!make_map(&maps.m[nsrc++], Bb, ld, N, NPAD)) return false;
+    }
+  }
+  const int np = sym ? F * (F + 1) / 2 : F * F;
+  const size_t red = (size_t)TSC * np * 64;
+  TCfg cfg = tcfg(nsrc, NPAD, 0);
+  if (cfg.smem < 2048 + red * 8) cfg.smem = 2048 + red * 8;
+  const int64_t kblocks = (ld + TKS - 1) / TKS;
+  int nsplit = nsm();
+  if (nsplit > kblocks) nsplit = (int)kblocks;
+  const int64_t kchunk = ((kblocks + nsplit - 1) / nsplit) * TKS;
+  nsplit = (int)((ld + kchunk - 1) / kchunk);
+  ::po::count_launch();
+  if (sym) {
+    auto k = gram_tma_kernel<F, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
+    k<<<nsplit, TTH, cfg.smem, s>>>(maps, nsrc, qa_b, qb, qb_b, ld, kchunk, cfg.nst, sa, sb, ws,
+                                     guard);
+  } else {
+    auto k = gram_tma_kernel<F, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
+    k<<<nsplit, TTH, cfg.smem, s>>>(maps, nsrc, qa_b, qb, qb_b, ld, kchunk, cfg.nst, sa, sb, ws,
+                                     guard);
+  }
+  const int64_t threads = (int64_t)N * N * 32;
+  ::po::count_launch();
+  gram_tma_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(N, NPAD, sym, nsplit, w,
+                                                                           ws, G, guard);
+  return true;
+}
+
+// ------------------------------------------------------------------- mix
+// Warp w owns the 8 points [8w, 8w+8) of each 64-point stage (one DMMA row
+// fragment) and all N outputs; M (N x N) is in shared memory for the CTA.
+template <int F, bool UPPER>
+__global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
+    const __grid_constant__ Maps maps, int nsrc, int qc, int N, int64_t ld, int64_t ngl,
+    int64_t pchunk, int nst, double sa, const double* __restrict__ M, double alpha, double beta,
+    double* __restrict__ out, double* __restrict__ norms, const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;
+  constexpr int NPAD = 8 * F;
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  // SWIZZLE_128B boxes need 1024-byte aligned destinations
+  unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
+  uint64_t* empty = full + 8;
+  double* stage0 = reinterpret_cast<double*>(tsm + 1024);
+  const size_t sdoubles = (size_t)nsrc * (TKS / BOX) * NPAD * BOX;
+  const size_t qstride = (size_t)(TKS / BOX) * NPAD * BOX;
+  double* Ms = stage0 + (size_t)nst * sdoubles;  // [NPAD][NPAD]
+  double* nred = Ms + NPAD * NPAD;               // [8][NPAD]
+  for (int e = threadIdx.x; e < NPAD * NPAD; e += TTH) {
+    const int k = e / NPAD, i = e % NPAD;
+    Ms[e] = (k < N && i < N) ? M[(int64_t)k * N + i] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], TSC);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t pbeg = (int64_t)blockIdx.x * pchunk;
+  const int64_t pend = min(pbeg + pchunk, ld);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, t4 = lane & 3;
+  const bool has_ab = nsrc - (qc >= 0 ? 1 : 0) == 2;
+  double nrm[F][2];
+#pragma unroll
+  for (int fi = 0; fi < F; ++fi) nrm[fi][0] = nrm[fi][1] = 0.0;
+  if (warp == TSC) {
+    if (lane == 0) tma_produce(maps.m, nsrc, NPAD, pbeg, pend, nst, sdoubles, stage0, full, empty);
+  } else {
+    const int nstage = pend > pbeg ? (int)((pend - pbeg + TKS - 1) / TKS) : 0;
+    const int ksteps = (N + 3) / 4;
+    const int c = warp * 8;
+    for (int st = 0; st < nstage; ++st) {
+      const int s = st % nst;
+      mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+      const double* sbuf = stage0 + (size_t)s * sdoubles;
+      const int64_t k0 = pbeg + (int64_t)st * TKS;
+      double acc[F][2];
+#pragma unroll
+      for (int f = 0; f < F; ++f) acc[f][0] = acc[f][1] = 0.0;
+      for (int ks = 0; ks < ksteps; ++ks) {
+        const int krow = 4 * ks + t4;
+        const int off = swz(krow, c + gq, NPAD);
+        double av = sbuf[off];
+        if (has_ab) av += sa * sbuf[qstride + off];
+#pragma unroll
+        for (int fi = 0; fi < F; ++fi) {
+          if (UPPER && 4 * ks > 8 * fi + 7) continue;
+          dmma_8x8x4(acc[fi], av, Ms[krow * NPAD + 8 * fi + gq]);
+        }
+      }
+      const int64_t p = k0 + c + gq;
+#pragma unroll
+      for (int fi = 0; fi < F; ++fi)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = 8 * fi + 2 * t4 + j;
+          if (p < ngl && i < N) {
+            double v = alpha * acc[fi][j];
+            if (qc >= 0) v += beta * sbuf[qc * qstride + swz(i, c + gq, NPAD)];
+            if (out) out[(int64_t)i * ld + p] = v;
+            nrm[fi][j] += v * v;
+          }
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (norms) {
+#pragma unroll
+      for (int fi = 0; fi < F; ++fi)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          double v = nrm[fi][j];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          if (gq == 0) nred[warp * NPAD + 8 * fi + 2 * t4 + j] = v;
+        }
+    }
+  }
+  if (norms) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < N; i += TTH) {
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < TSC; ++w) sum += nred[w * NPAD + i];
+      norms[(int64_t)i * gridDim.x + blockIdx.x] = sum;
+    }
+  }
+}
+
+template <int F>
+int launch_mix_tma_f(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
+                     const double* M, double alpha, const double* C, double beta, int upper,
+                     double* out, double* norms, cudaStream_t s, const double* guard) {
+  constexpr int NPAD = 8 * F;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  int nsrc = 0, qc = -1;
+  if (!make_map(&maps.m[nsrc++], A, ld, N, NPAD)) return -1;
+  if (Ab && !make_map(&maps.m[nsrc++], Ab, ld, N, NPAD)) return -1;
+  if (C) {
+    qc = nsrc;
+    if (!make_map(&maps.m[nsrc++], C, ld, N, NPAD)) return -1;
+  }
+  const size_t extra = (size_t)NPAD * NPAD + (size_t)TSC * NPAD;
+  const TCfg cfg = tcfg(nsrc, NPAD, extra);
+  const int64_t kb = (ld + TKS - 1) / TKS;
+  int nblk = nsm();
+  if (nblk > kb) nblk = (int)kb;
+  const int64_t pchunk = ((kb + nblk - 1) / nblk) * TKS;
+  nblk = (int)((ld + pchunk - 1) / pchunk);
+  ::po::count_launch();
+  if (upper) {
+    auto k = mix_tma_kernel<F, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
+    k<<<nblk, TTH, cfg.smem, s>>>(maps, nsrc, qc, N, ld, ngl, pchunk, cfg.nst, sa, M, alpha, beta,
+                                   out, norms, guard);
+  } else {
+    auto k = mix_tma_kernel<F, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
+    k<<<nblk, TTH, cfg.smem, s>>>(maps, nsrc, qc, N, ld, ngl, pchunk, cfg.nst, sa, M, alpha, beta,
+                                   out, norms, guard);
+  }
+  return nblk;
+}
+
+}  // namespace
+
+bool tma2d_available() { return encode_fn() != nullptr; }
+
+bool launch_gram_tma(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
+                     const double* B, const double* Bb, double sb, double* ws, double* G, double w,
+                     cudaStream_t s, const double* guard) {
+  switch ((N + 7) / 8) {
+#define PO_GT(F) \
+  case F:        \
+    return launch_gram_tma_f<F>(N, ld, sym, A, Ab, sa, B, Bb, sb, ws, G, w, s, guard);
+    PO_GT(1) PO_GT(2) PO_GT(3) PO_GT(4) PO_GT(5) PO_GT(6)
+#undef PO_GT
+  }
+  return false;
+}
+
+int launch_mix_tma(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
+                   const double* M, double alpha, const double* C, double beta, int upper,
+                   double* out, double* norms, cudaStream_t s, const double* guard) {
+  switch ((N + 7) / 8) {
+#define PO_MT(F) \
+  case F:        \
+    return launch_mix_tma_f<F>(N, ld, ngl, A, Ab, sa, M, alpha, C, beta, upper, out, norms, s, guard);
+    PO_MT(1) PO_MT(2) PO_MT(3) PO_MT(4) PO_MT(5) PO_MT(6) PO_MT(7) PO_MT(8)
+#undef PO_MT
+  }
+  return -1;
+}
+
+}  // namespace po

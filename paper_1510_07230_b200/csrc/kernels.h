@@ -86,6 +86,15 @@ int launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, doub
                 const double* M, double alpha, const double* C, double beta, int upper,
                 double* out, double* norms, cudaStream_t s, const double* guard = nullptr);
 
+// dmma_tma.cu: 2D tensor-map TMA versions of the small-N Gram / mix (false / -1
+// when unavailable: no driver entry point or N out of range).
+bool tma2d_available();
+bool launch_gram_tma(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
+                     const double* B, const double* Bb, double sb, double* ws, double* G, double w,
+                     cudaStream_t s, const double* guard);
+int launch_mix_tma(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
+                   const double* M, double alpha, const double* C, double beta, int upper,
+                   double* out, double* norms, cudaStream_t s, const double* guard);
 // Batched left-multiply out_b = S X_b for X_b = rows [N][ld] at A + b * bstride
 // (valid row length ngl; ld multiple of 32, padding zero). DST transforms.
 void launch_mix_batched(int N, int64_t ld, int64_t ngl, int batch, int64_t bstride,
