@@ -759,7 +759,9 @@ size_t gram_workspace_doubles(const SlabGeom& g, int N) {
   GramPlan p = gram_plan(g, N, 0);
   const size_t tiled = (size_t)p.nsplit * p.ntiles * GB * GB;
   const size_t small = (size_t)148 * 4 * 64 * 64;
-  return tiled > small ? tiled : small;
+  size_t w = tiled > small ? tiled : small;
+  const size_t big = gram_big_workspace_doubles(g.ld, N);
+  return big > w ? big : w;
 }
 
 static bool gram_small_ok(int N, int sym) { return sym ? N <= 48 : N <= 40; }
@@ -778,6 +780,9 @@ void launch_gram(const SlabGeom& g, int N, const double* A, const double* Ab, do
 #undef PO_GS
     }
   }
+  if (launch_gram_big(N, g.ld, sym, A, Ab, sa, B, Bb, sb, ws, gram_workspace_doubles(g, N), G,
+                      g.w, s, guard))
+    return;
   GramPlan p = gram_plan(g, N, sym);
   dim3 grid(p.ntiles, p.nsplit);
   constexpr size_t shm = sizeof(double) * 4 * GB * GKP;

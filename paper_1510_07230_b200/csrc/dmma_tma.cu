@@ -13,6 +13,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -439,7 +440,301 @@ int launch_mix_tma_f(int N, int64_t ld, int64_t ngl, const double* A, const doub
   return nblk;
 }
 
+// ------------------------------------------------------- large-N tiled Gram
+// G = w (A + sa Ab)^T (B + sb Bb) for N > 48, tiled 128 x 128 over orbital
+// pairs and split over points (deterministic fixed-order reduction of the
+// per-split partial tiles). Each 16-point stage of a source is ONE box
+// {16 points x 128 rows} (16 KB, SWIZZLE_128B, rows >= N zero-filled), so a
+// producer warp keeps up to 8 stages in flight with a handful of requests.
+// Eight consumer warps own 32 x 64 sub-tiles (4 x 8 DMMA fragments): per 8
+// points a warp loads 4 + 8 double2 fragments and issues 64 DMMAs. In the
+// symmetric case only tiles on/above the diagonal exist, diagonal tiles skip
+// fragment pairs below the diagonal and never load B.
+
+__device__ __forceinline__ void big_tile_index(int t, int mt, int sym, int& tm, int& tn) {
+  if (!sym) {
+    tm = t / mt;
+    tn = t % mt;
+    return;
+  }
+  int r = 0, rem = t;
+  while (rem >= mt - r) {
+    rem -= mt - r;
+    ++r;
+  }
+  tm = r;
+  tn = r + rem;
+}
+
+// T = 128: a producer warpgroup (one lane issues the boxes) that hands its
+// registers to the two consumer warpgroups (setmaxnreg 40 / 232), so the
+// 32 x 64 warp tiles keep their 128 accumulator registers; T = 64: one
+// producer warp.
+template <int GT_T>
+struct BigCfg {  // consumer warps WM x WN, warp tile (T/WM) x (T/WN)
+  static constexpr int WM = 4, WN = 2;
+  static constexpr int NW = WM * WN;
+  static constexpr int PW = GT_T == 128 ? 4 : 1;  // producer warps (first)
+  static constexpr int THREADS = (NW + PW) * 32;
+  static constexpr int FM = GT_T / (8 * WM), FN = GT_T / (8 * WN);
+};
+
+template <int GT_T>
+__global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(const __grid_constant__ Maps maps,
+                                                          int nsrc, int qa_b, int qb, int qb_b,
+                                                          int mt, int sym, int64_t ld,
+                                                          int64_t kchunk, int nst, double sa,
+                                                          double sb, double* __restrict__ ws,
+                                                          const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
+  uint64_t* empty = full + 8;
+  double* stage0 = reinterpret_cast<double*>(tsm + 1024);
+  constexpr size_t QS = (size_t)GT_T * BOX;  // doubles per source per stage
+  const size_t sdoubles = (size_t)nsrc * QS;
+  int tm, tn;
+  big_tile_index(blockIdx.x, mt, sym, tm, tn);
+  const bool diag = sym && tm == tn;
+  // sources actually fetched: A (+Ab); B (+Bb) unless this is a symmetric diagonal tile
+  const int nload = diag ? (qa_b >= 0 ? 2 : 1) : nsrc;
+  using Cfg = BigCfg<GT_T>;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], Cfg::NW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t kbeg = (int64_t)blockIdx.y * kchunk;
+  const int64_t kend = min(kbeg + kchunk, ld);
+  const int nstage = kend > kbeg ? (int)((kend - kbeg + BOX - 1) / BOX) : 0;
+  const int lane = threadIdx.x & 31;
+  int warp = threadIdx.x >> 5;
+  if (warp < Cfg::PW) {
+    if constexpr (Cfg::PW == 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (warp == 0 && lane == 0) {
+      for (int q = 0; q < nload; ++q)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[q])));
+      const uint32_t bytes = (uint32_t)(nload * QS * 8);
+      for (int st = 0; st < nstage; ++st) {
+        const int s = st % nst;
+        if (st >= nst) mbar_wait(&empty[s], ((uint32_t)(st / nst) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&full[s], bytes);
+        const int x = (int)(kbeg + (int64_t)st * BOX);
+        double* sbuf = stage0 + (size_t)s * sdoubles;
+        for (int q = 0; q < nload; ++q) {
+          const int row0 = (q == qb || q == qb_b) ? tn * GT_T : tm * GT_T;
+          tma_load_2d(sbuf + q * QS, &maps.m[q], x, row0, &full[s]);
+        }
+      }
+    }
+  } else {
+    if constexpr (Cfg::PW == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    warp -= Cfg::PW;
+    const int gq = lane >> 2, t4 = lane & 3;
+    constexpr int FM = Cfg::FM, FN = Cfg::FN;
+    const int wm = warp / Cfg::WN, wn = warp % Cfg::WN;
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int a = 0; a < FM; ++a)
+#pragma unroll
+      for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    // on a diagonal tile: warp entirely below the diagonal has nothing to do
+    const bool idle = diag && (8 * FM * wm >= 8 * FN * wn + 8 * FN);
+    const int bq = diag ? 0 : qb, bqb = diag ? qa_b : qb_b;
+    const double bs = diag ? sa : sb;
+    for (int st = 0; st < nstage; ++st) {
+      const int s = st % nst;
+      mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+      const double* sbuf = stage0 + (size_t)s * sdoubles;
+#pragma unroll
+      for (int kg = 0; kg < 2; ++kg) {
+        if (idle) break;
+        const int p = 8 * kg + 2 * t4;
+        double2 a[FM], b[FN];
+#pragma unroll
+        for (int f = 0; f < FM; ++f) {
+          const int off = swz(8 * FM * wm + 8 * f + gq, p, GT_T);
+          a[f] = *reinterpret_cast<const double2*>(sbuf + off);
+          if (qa_b >= 0) {
+            const double2 z = *reinterpret_cast<const double2*>(sbuf + qa_b * QS + off);
+            a[f].x += sa * z.x;
+            a[f].y += sa * z.y;
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < FN; ++f) {
+          const int off = swz(8 * FN * wn + 8 * f + gq, p, GT_T);
+          b[f] = *reinterpret_cast<const double2*>(sbuf + bq * QS + off);
+          if (bqb >= 0) {
+            const double2 z = *reinterpret_cast<const double2*>(sbuf + bqb * QS + off);
+            b[f].x += bs * z.x;
+            b[f].y += bs * z.y;
+          }
+        }
+        if (kg == 1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);  // all fragments of the stage are in registers
+        }
+#pragma unroll
+        for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+          for (int fn = 0; fn < FN; ++fn) {
+            if (diag && FM * wm + fm > FN * wn + fn) continue;
+            dmma_8x8x4(acc[fm][fn], a[fm].x, b[fn].x);
+            dmma_8x8x4(acc[fm][fn], a[fm].y, b[fn].y);
+          }
+      }
+      if (idle) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+    }
+    double* out = ws + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * (GT_T * GT_T);
+#pragma unroll
+    for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+      for (int fn = 0; fn < FN; ++fn) {
+        const int r = 8 * FM * wm + 8 * fm + gq, c = 8 * FN * wn + 8 * fn + 2 * t4;
+        *reinterpret_cast<double2*>(out + r * GT_T + c) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
+      }
+  }
+}
+
+__global__ void gram_big_reduce_kernel(int GT_T, int N, int mt, int sym, int ntiles, int nsplit, double w,
+                                       const double* __restrict__ ws, double* __restrict__ G,
+                                       const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)N * N) return;
+  int i = (int)(e / N), j = (int)(e % N);
+  if (sym && j < i) {
+    const int t = i;
+    i = j;
+    j = t;
+  }
+  const int tm = i / GT_T, tn = j / GT_T;
+  int tile;
+  if (!sym) {
+    tile = tm * mt + tn;
+  } else {
+    tile = 0;
+    for (int r = 0; r < tm; ++r) tile += mt - r;
+    tile += tn - tm;
+  }
+  const int64_t off = (int64_t)tile * GT_T * GT_T + (i - tm * GT_T) * GT_T + (j - tn * GT_T);
+  double s = 0.0;
+  for (int k = 0; k < nsplit; ++k) s += ws[(int64_t)k * ntiles * GT_T * GT_T + off];
+  G[e] = w * s;
+}
+
+struct BigPlan {
+  int mt, ntiles, nsplit;
+  int64_t kchunk;
+};
+
+// splits so that tiles x splits fills whole waves of one CTA per SM
+int big_tile(int N) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("PO_GRAM_TILE");  // measurement override: 64 or 128
+    forced = e ? atoi(e) : 0;
+  }
+  if (forced == 64 || forced == 128) return forced;
+  return N <= 192 ? 64 : 128;
+}
+
+BigPlan big_plan(int64_t ld, int N, int sym, int sms) {
+  const int GT_T = big_tile(N);
+  BigPlan p;
+  p.mt = (N + GT_T - 1) / GT_T;
+  p.ntiles = sym ? p.mt * (p.mt + 1) / 2 : p.mt * p.mt;
+  const int64_t kb = (ld + BOX - 1) / BOX;
+  int cap = 4096 / p.ntiles;
+  if (cap < 1) cap = 1;
+  if (cap > kb) cap = (int)kb;
+  int best = 1;
+  double beste = 0.0;
+  for (int ns = 1; ns <= cap; ++ns) {
+    const int64_t units = (int64_t)p.ntiles * ns;
+    const int64_t waves = (units + sms - 1) / sms;
+    const double eff = (double)units / (double)(waves * sms);
+    if (eff > beste + 0.02) {
+      beste = eff;
+      best = ns;
+    }
+    if (eff >= 0.97) break;
+  }
+  p.kchunk = ((kb + best - 1) / best) * BOX;
+  p.nsplit = (int)((ld + p.kchunk - 1) / p.kchunk);
+  return p;
+}
+
 }  // namespace
+
+size_t gram_big_workspace_doubles(int64_t ld, int N) {
+  if (N <= 48) return 0;
+  const int GT_T = big_tile(N);
+  BigPlan p = big_plan(ld, N, 0, nsm());
+  BigPlan q = big_plan(ld, N, 1, nsm());
+  const size_t a = (size_t)p.nsplit * p.ntiles * GT_T * GT_T;
+  const size_t b = (size_t)q.nsplit * q.ntiles * GT_T * GT_T;
+  return a > b ? a : b;
+}
+
+bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
+                     const double* B, const double* Bb, double sb, double* ws, size_t ws_doubles,
+                     double* G, double w, cudaStream_t s, const double* guard) {
+  const int GT_T = big_tile(N);
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  int nsrc = 0, qa_b = -1, qb = 0, qb_b = -1;
+  if (!make_map(&maps.m[nsrc++], A, ld, N, GT_T)) return false;
+  if (Ab) {
+    qa_b = nsrc;
+    if (!make_map(&maps.m[nsrc++], Ab, ld, N, GT_T)) return false;
+  }
+  if (sym) {
+    qb = 0;
+  } else {
+    qb = nsrc;
+    if (!make_map(&maps.m[nsrc++], B, ld, N, GT_T)) return false;
+    if (Bb) {
+      qb_b = nsrc;
+      if (!make_map(&maps.m[nsrc++], Bb, ld, N, GT_T)) return false;
+    }
+  }
+  if (sym) {  // off-diagonal symmetric tiles read the B side from the same block
+    qb = nsrc;
+    maps.m[nsrc++] = maps.m[0];
+    if (Ab) {
+      qb_b = nsrc;
+      maps.m[nsrc++] = maps.m[qa_b];
+    }
+    sb = sa;
+  }
+  const BigPlan p = big_plan(ld, N, sym, nsm());
+  if ((size_t)p.nsplit * p.ntiles * GT_T * GT_T > ws_doubles) return false;
+  const size_t sdoubles = (size_t)nsrc * GT_T * BOX;
+  int nst = (int)((200 * 1024 / 8) / sdoubles);
+  if (nst > 8) nst = 8;
+  if (nst < 2) return false;
+  const size_t smem = 2048 + (size_t)nst * sdoubles * 8;
+  ::po::count_launch();
+  auto k = GT_T == 64 ? gram_big_kernel<64> : gram_big_kernel<128>;
+  const int threads = GT_T == 64 ? BigCfg<64>::THREADS : BigCfg<128>::THREADS;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<dim3(p.ntiles, p.nsplit), threads, smem, s>>>(maps, nsrc, qa_b, qb, qb_b, p.mt, sym, ld, p.kchunk,
+                                                 nst, sa, sb, ws, guard);
+  const int64_t total = (int64_t)N * N;
+  ::po::count_launch();
+  gram_big_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(GT_T, N, p.mt, sym, p.ntiles,
+                                                                         p.nsplit, w, ws, G, guard);
+  return true;
+}
 
 bool tma2d_available() { return encode_fn() != nullptr; }
 

@@ -92,6 +92,12 @@ bool tma2d_available();
 bool launch_gram_tma(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                      const double* B, const double* Bb, double sb, double* ws, double* G, double w,
                      cudaStream_t s, const double* guard);
+// Large-N (N > 48) Gram: 128x128 (or 64x64) orbital tiles x point splits,
+// one 16-point 2D box per source per stage; returns false when unavailable.
+size_t gram_big_workspace_doubles(int64_t ld, int N);
+bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
+                     const double* B, const double* Bb, double sb, double* ws, size_t ws_doubles,
+                     double* G, double w, cudaStream_t s, const double* guard);
 int launch_mix_tma(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
                    const double* M, double alpha, const double* C, double beta, int upper,
                    double* out, double* norms, cudaStream_t s, const double* guard);

@@ -188,18 +188,22 @@ def test_dmma_small_n(native, n_orb):
     e.close()
 
 
-@pytest.mark.parametrize("n_orb", [67, 130])
-def test_dmma_multitile(port, native, n_orb):
-    """N > 64 exercises several Gram tiles (upper-only in the symmetric path)
-    and several mix orbital tiles."""
-    spec = configs.ProblemSpec("tile", (9, 8, 10), (5.0, 5.0, 5.0), [], n_orb, hartree=False, xc=False)
+@pytest.mark.parametrize("n_orb,n", [(49, (9, 8, 10)), (67, (9, 8, 10)), (130, (9, 8, 10)),
+                                     (200, (24, 20, 22)), (300, (12, 13, 14))])
+def test_dmma_multitile(port, native, n_orb, n):
+    """N > 48 exercises the tiled TMA Gram (64- and 128-wide tiles, upper-only
+    in the symmetric path, diagonal tiles skipping the lower fragments) and
+    several mix orbital tiles."""
+    spec = configs.ProblemSpec("tile", n, (5.0, 5.0, 5.0), [], n_orb, hartree=False, xc=False)
     e = native.engine_for(spec)
     rng = np.random.default_rng(n_orb)
     a = rng.standard_normal((n_orb, spec.num_points))
     b = rng.standard_normal((n_orb, spec.num_points))
     ba, bb = e.block_from(a), e.block_from(b)
     wq = np.prod(spec.spacing)
-    assert rel(e.gram(ba, ba), wq * a @ a.T) < 1e-12
+    g = e.gram(ba, ba)
+    assert np.array_equal(g, g.T)
+    assert rel(g, wq * a @ a.T) < 1e-12
     assert rel(e.gram(ba, bb), wq * a @ b.T) < 1e-12
     m = rng.standard_normal((n_orb, n_orb))
     out = e.alloc()
@@ -289,7 +293,7 @@ def test_invalid_arguments(native):
     e.close()
 
 
-@pytest.mark.parametrize("n_orb", [1, 4, 5, 13, 33, 48, 67])
+@pytest.mark.parametrize("n_orb", [1, 4, 5, 13, 33, 48, 67, 200, 260])
 def test_gram_fused_trial(native, n_orb):
     """Gram of W - tau Z formed inside the load (optimizer.cpp:459-463)."""
     spec = configs.ProblemSpec("trial", (10, 9, 11), (5.0, 5.0, 5.0), [], n_orb, hartree=False, xc=False)
