@@ -404,6 +404,164 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
   }
 }
 
+// ---------------------------------------------------------- fused directions
+// compute_directions + the BB products in ONE pass over the blocks
+// (optimizer.cpp:265-320 and 376-411; manifold.cpp:181-202):
+//   z_i  = HW_i - sigma_ii W_i                  (written; ||z_i||^2)
+//   D_i  = HW_i - sum_k Sigma_ki W_k  [DD]      (DMMA, not written; ||D_i||^2)
+//   s_i  = W_i - WP_i, y_i = z_i - ZP_i [HIST]  (<s,s>, <s,y>, <y,y>)
+// Sources in the ring: 0 = W, 1 = HW, 2 = WP, 3 = ZP. Per-orbital partial rows
+// [zz | dd | ss | sy | yy] x gridDim.x (dd = 0 without DD).
+template <int F, bool DD, bool HIST>
+__global__ void __launch_bounds__(TTH, 1) directions_tma_kernel(
+    const __grid_constant__ Maps maps, int N, int64_t ld, int64_t ngl, int64_t pchunk, int nst,
+    const double* __restrict__ Sigma, const double* __restrict__ sig, double* __restrict__ Z,
+    double* __restrict__ partials) {
+  constexpr int NPAD = 8 * F;
+  constexpr int NSRC = HIST ? 4 : 2;
+  constexpr int NQ = HIST ? 5 : 2;
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
+  uint64_t* empty = full + 8;
+  double* stage0 = reinterpret_cast<double*>(tsm + 1024);
+  constexpr size_t qstride = (size_t)(TKS / BOX) * NPAD * BOX;
+  constexpr size_t sdoubles = NSRC * qstride;
+  double* Ms = stage0 + (size_t)nst * sdoubles;  // [NPAD][NPAD] (DD)
+  double* msig = Ms + NPAD * NPAD;               // [NPAD]: -sigma_ii
+  double* nred = msig + NPAD;                    // [8][NQ][NPAD]
+  for (int e = threadIdx.x; e < NPAD * NPAD; e += TTH) {
+    const int k = e / NPAD, i = e % NPAD;
+    Ms[e] = (DD && k < N && i < N) ? Sigma[(int64_t)k * N + i] : 0.0;
+  }
+  for (int i = threadIdx.x; i < NPAD; i += TTH) msig[i] = i < N ? -sig[i] : 0.0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], TSC);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t pbeg = (int64_t)blockIdx.x * pchunk;
+  const int64_t pend = min(pbeg + pchunk, ld);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, t4 = lane & 3;
+  double nrm[NQ][F][2];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int fi = 0; fi < F; ++fi) nrm[q][fi][0] = nrm[q][fi][1] = 0.0;
+  if (warp == TSC) {
+    if (lane == 0) tma_produce(maps.m, NSRC, NPAD, pbeg, pend, nst, sdoubles, stage0, full, empty);
+  } else {
+    const int nstage = pend > pbeg ? (int)((pend - pbeg + TKS - 1) / TKS) : 0;
+    const int ksteps = (N + 3) / 4;
+    const int c = warp * 8;
+    for (int st = 0; st < nstage; ++st) {
+      const int s = st % nst;
+      mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+      const double* sbuf = stage0 + (size_t)s * sdoubles;
+      const int64_t p = pbeg + (int64_t)st * TKS + c + gq;
+      double acc[F][2];
+#pragma unroll
+      for (int f = 0; f < F; ++f) acc[f][0] = acc[f][1] = 0.0;
+      if constexpr (DD) {
+        for (int ks = 0; ks < ksteps; ++ks) {
+          const int krow = 4 * ks + t4;
+          const double av = sbuf[swz(krow, c + gq, NPAD)];
+#pragma unroll
+          for (int fi = 0; fi < F; ++fi) dmma_8x8x4(acc[fi], av, Ms[krow * NPAD + 8 * fi + gq]);
+        }
+      }
+#pragma unroll
+      for (int fi = 0; fi < F; ++fi)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = 8 * fi + 2 * t4 + j;
+          if (p < ngl && i < N) {
+            const int off = swz(i, c + gq, NPAD);
+            const double wv = sbuf[off], hv = sbuf[qstride + off];
+            if constexpr (DD) {
+              double d = -acc[fi][j];
+              d += hv;
+              nrm[1][fi][j] += d * d;
+            }
+            const double z = hv + msig[i] * wv;
+            Z[(int64_t)i * ld + p] = z;
+            nrm[0][fi][j] += z * z;
+            if constexpr (HIST) {
+              const double sv = wv - sbuf[2 * qstride + off];
+              const double yv = z - sbuf[3 * qstride + off];
+              nrm[2][fi][j] += sv * sv;
+              nrm[3][fi][j] += sv * yv;
+              nrm[4][fi][j] += yv * yv;
+            }
+          }
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int fi = 0; fi < F; ++fi)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          double v = nrm[q][fi][j];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          if (gq == 0) nred[(warp * NQ + q) * NPAD + 8 * fi + 2 * t4 + j] = v;
+        }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NQ * N; e += TTH) {
+    const int q = e / N, i = e % N;
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < TSC; ++w) sum += nred[(w * NQ + q) * NPAD + i];
+    partials[((int64_t)q * N + i) * gridDim.x + blockIdx.x] = sum;
+  }
+}
+
+template <int F, bool DD, bool HIST>
+int launch_directions_fdh(const Maps& maps, int N, int64_t ld, int64_t ngl, const double* Sigma,
+                          const double* sig, double* Z, double* partials, cudaStream_t s) {
+  constexpr int NPAD = 8 * F;
+  constexpr int NQ = HIST ? 5 : 2;
+  const size_t extra = (size_t)NPAD * NPAD + NPAD + (size_t)TSC * NQ * NPAD;
+  const TCfg cfg = tcfg(HIST ? 4 : 2, NPAD, extra);
+  const int64_t kb = (ld + TKS - 1) / TKS;
+  int nblk = nsm();
+  if (nblk > kb) nblk = (int)kb;
+  const int64_t pchunk = ((kb + nblk - 1) / nblk) * TKS;
+  nblk = (int)((ld + pchunk - 1) / pchunk);
+  ::po::count_launch();
+  auto k = directions_tma_kernel<F, DD, HIST>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
+  k<<<nblk, TTH, cfg.smem, s>>>(maps, N, ld, ngl, pchunk, cfg.nst, Sigma, sig, Z, partials);
+  return nblk;
+}
+
+template <int F>
+int launch_directions_f(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
+                        const double* WP, const double* ZP, const double* Sigma, const double* sig,
+                        double* Z, double* partials, cudaStream_t s) {
+  constexpr int NPAD = 8 * F;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  const bool hist = WP && ZP;
+  if (!make_map(&maps.m[0], W, ld, N, NPAD) || !make_map(&maps.m[1], HW, ld, N, NPAD)) return -1;
+  if (hist && (!make_map(&maps.m[2], WP, ld, N, NPAD) || !make_map(&maps.m[3], ZP, ld, N, NPAD)))
+    return -1;
+  if (Sigma)
+    return hist ? launch_directions_fdh<F, true, true>(maps, N, ld, ngl, Sigma, sig, Z, partials, s)
+                : launch_directions_fdh<F, true, false>(maps, N, ld, ngl, Sigma, sig, Z, partials, s);
+  return hist ? launch_directions_fdh<F, false, true>(maps, N, ld, ngl, Sigma, sig, Z, partials, s)
+              : launch_directions_fdh<F, false, false>(maps, N, ld, ngl, Sigma, sig, Z, partials, s);
+}
+
 template <int F>
 int launch_mix_tma_f(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
                      const double* M, double alpha, const double* C, double beta, int upper,
@@ -737,6 +895,19 @@ bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* 
 }
 
 bool tma2d_available() { return encode_fn() != nullptr; }
+
+int launch_directions(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
+                      const double* WP, const double* ZP, const double* Sigma, const double* sig,
+                      double* Z, double* partials, cudaStream_t s) {
+  switch ((N + 7) / 8) {
+#define PO_DR(F) \
+  case F:        \
+    return launch_directions_f<F>(N, ld, ngl, W, HW, WP, ZP, Sigma, sig, Z, partials, s);
+    PO_DR(1) PO_DR(2) PO_DR(3) PO_DR(4) PO_DR(5) PO_DR(6)
+#undef PO_DR
+  }
+  return -1;
+}
 
 bool launch_gram_tma(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                      const double* B, const double* Bb, double sb, double* ws, double* G, double w,

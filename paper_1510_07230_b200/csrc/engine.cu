@@ -78,7 +78,7 @@ Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist
   size_t pc = 0;
   auto upd = [&](size_t v) { pc = v > pc ? v : pc; };
   upd((size_t)3 * N * hamiltonian_nblk(g));
-  upd((size_t)N * mix_nblk_max(g));
+  upd((size_t)5 * N * mix_nblk_max(g));  // fused directions: 5 partial rows
   upd((size_t)3 * N * per_orbital_nblk(g, N));
   upd((size_t)2 * points_nblk(g));
   partials_cap = pc;

@@ -98,6 +98,14 @@ size_t gram_big_workspace_doubles(int64_t ld, int N);
 bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                      const double* B, const double* Bb, double sb, double* ws, size_t ws_doubles,
                      double* G, double w, cudaStream_t s, const double* guard);
+// Fused compute_directions + BB products for N <= 48 (one pass over W, HW
+// [, WP, ZP]): writes Z = HW - diag(sig) W and per-orbital partial rows
+// [zz | dd | ss | sy | yy] (dd = ||HW - W Sigma||^2 when Sigma != null; the
+// last three only with WP/ZP). Returns the partials row length, -1 if N is
+// out of range or 2D TMA is unavailable.
+int launch_directions(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
+                      const double* WP, const double* ZP, const double* Sigma, const double* sig,
+                      double* Z, double* partials, cudaStream_t s);
 int launch_mix_tma(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
                    const double* M, double alpha, const double* C, double beta, int upper,
                    double* out, double* norms, cudaStream_t s, const double* guard);

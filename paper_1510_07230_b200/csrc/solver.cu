@@ -362,7 +362,24 @@ bool Solver::step() {
     BRef z = pool.get();
     BRef dscratch;
     const int onb = per_orbital_nblk(E.g, n);
-    if (full_grad) {
+    bool fused = false;
+    if (!full_grad && !(mean_abs && need_full) && n <= 48 && tma2d_available()) {
+      // one pass: z, ||z||^2, ||HW - W Sigma||^2 and the BB products
+      if (need_full || !sig_valid) {
+        sigma(w, hw);
+        launch_copy_diag(n, E.dmat[4], E.dvec + E.off_sig(), E.s);
+      }
+      const int nb = launch_directions(
+          n, E.g.ld, E.g.ngl, P(w), P(hw), history_valid ? P(prev_w) : nullptr,
+          history_valid ? P(prev_z) : nullptr, need_full ? E.dmat[4] : nullptr,
+          E.dvec + E.off_sig(), P(z), E.partials, E.s);
+      if (nb >= 0) {
+        E.reduce_rows(E.partials, (history_valid ? 5 : 2) * n, nb, E.g.w, E.dvec + E.off_zz(), true);
+        fused = true;
+      }
+    }
+    if (fused) {
+    } else if (full_grad) {
       sigma(w, hw);
       E.mix(P(w), nullptr, 0.0, E.dmat[4], -1.0, P(hw), 1.0, 0, P(z), E.dvec + E.off_dd());
       if (mean_abs && need_full) {
@@ -386,7 +403,7 @@ bool Solver::step() {
         }
       }
     }
-    if (history_valid) {
+    if (history_valid && !fused) {
       launch_bb(E.g, n, P(w), P(prev_w), P(z), P(prev_z), E.partials, E.s);
       E.reduce_rows(E.partials, 3 * n, onb, E.g.w, E.dvec + E.off_ss(), true);
     }
