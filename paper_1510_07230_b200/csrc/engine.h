@@ -75,12 +75,27 @@ class Engine {
   // ---- blocks (handles)
   int alloc_block();
   void free_block(int b);
+  // solver scratch kept across solves (no cudaMalloc in a warm po_solve)
+  int take_block() {
+    if (spare_blocks_.empty()) return alloc_block();
+    const int b = spare_blocks_.back();
+    spare_blocks_.pop_back();
+    return b;
+  }
+  void give_block(int b) { spare_blocks_.push_back(b); }
   double* blk(int b) const;
   void zero_block(int b);
 
   // ---- states
   DevState* new_state();
   void free_state(DevState* st);
+  DevState* take_state() {
+    if (spare_states_.empty()) return new_state();
+    DevState* st = spare_states_.back();
+    spare_states_.pop_back();
+    return st;
+  }
+  void give_state(DevState* st) { spare_states_.push_back(st); }
   DevState* default_state() { return def_state_; }
   double* v_ext = nullptr;
 
@@ -157,6 +172,8 @@ class Engine {
   std::vector<double*> blocks_;
   std::vector<DevState*> states_;
   DevState* def_state_ = nullptr;
+  std::vector<int> spare_blocks_;
+  std::vector<DevState*> spare_states_;
 };
 
 }  // namespace po

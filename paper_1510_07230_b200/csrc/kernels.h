@@ -172,6 +172,10 @@ struct DstPoisson {
   void release();
   void solve(const double* b, double* x, cudaStream_t s);
 };
+// three-kernel DST solve (axis-0 GEMM, per-plane shared-memory kernel, axis-0
+// GEMM) for grids up to 128 points per axis; false when unsupported.
+bool dst_fused_supported(int64_t n0, int64_t n1, int64_t n2);
+bool launch_dst_fused(const DstPoisson& d, const double* b, double* x, cudaStream_t s);
 void launch_cg(int64_t n0, int64_t n1, int64_t n2, const double ih2[3], const double* b,
                double* x, int warm, double* ws, unsigned* bar, int* out_i, double* out_d,
                cudaStream_t s);

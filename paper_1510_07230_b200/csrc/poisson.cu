@@ -83,6 +83,36 @@ __device__ double grid_sum(double v, const CgArgs& a, unsigned& slot, double* sh
   return out;
 }
 
+// Two deterministic grid-wide sums with one barrier.
+__device__ void grid_sum2(double& v0, double& v1, const CgArgs& a, unsigned& slot, double* sh) {
+  double vv[2] = {v0, v1};
+  block_sum<2>(vv, sh);
+  double* red = a.red + (slot & 1u) * 2 * gridDim.x;
+  if (threadIdx.x == 0) {
+    red[2 * blockIdx.x] = vv[0];
+    red[2 * blockIdx.x + 1] = vv[1];
+  }
+  ++slot;
+  grid_barrier(a.bar, gridDim.x);
+  if (threadIdx.x < 32) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += 32) {
+      s0 += __ldcg(red + 2 * k);
+      s1 += __ldcg(red + 2 * k + 1);
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    if (threadIdx.x == 0) {
+      sh[64] = s0;
+      sh[65] = s1;
+    }
+  }
+  __syncthreads();
+  v0 = sh[64];
+  v1 = sh[65];
+  __syncthreads();
+}
+
 // -lap f at point q (Dirichlet zero outside), f given by a functor of the index.
 template <class F>
 __device__ __forceinline__ double neg_lap(const CgArgs& a, int64_t q, F f) {
@@ -102,7 +132,7 @@ __device__ __forceinline__ double neg_lap(const CgArgs& a, int64_t q, F f) {
 }
 
 __global__ void __launch_bounds__(CT) cg_kernel(CgArgs a) {
-  __shared__ double sh[33];
+  __shared__ double sh[66];
   unsigned slot = 0;
   const int64_t stride = (int64_t)gridDim.x * CT;
   const int64_t t0 = (int64_t)blockIdx.x * CT + threadIdx.x;
@@ -111,13 +141,22 @@ __global__ void __launch_bounds__(CT) cg_kernel(CgArgs a) {
   double* __restrict__ r = a.r;
   double* __restrict__ ap = a.ap;
 
-  // b norm and initial residual
-  double acc = 0.0;
+  // b norm and initial residual (one pass and one barrier for a warm start:
+  // after the DST solve this is usually the whole kernel)
+  double acc = 0.0, acc_r = 0.0;
   for (int64_t q = t0; q < a.ng; q += stride) {
-    if (!a.warm) x[q] = 0.0;
-    acc += b[q] * b[q];
+    const double bq = b[q];
+    if (!a.warm) {
+      x[q] = 0.0;
+    } else {
+      const double rt = bq - neg_lap(a, q, [&](int64_t k) { return __ldcg(x + k); });
+      r[q] = rt;
+      acc_r += rt * rt;
+    }
+    acc += bq * bq;
   }
-  const double bb = grid_sum(acc, a, slot, sh);
+  double bb = acc, rr0 = acc_r;
+  grid_sum2(bb, rr0, a, slot, sh);
   const double bnorm = sqrt(bb);
   if (bnorm == 0.0) {
     for (int64_t q = t0; q < a.ng; q += stride) x[q] = 0.0;
@@ -135,13 +174,16 @@ __global__ void __launch_bounds__(CT) cg_kernel(CgArgs a) {
     for (int64_t q = t0; q < a.ng; q += stride) r[q] = b[q];
     rr = bb;  // r = b: same sum as b.b
   } else {
-    acc = 0.0;
-    for (int64_t q = t0; q < a.ng; q += stride) {
-      const double rt = b[q] - neg_lap(a, q, [&](int64_t k) { return __ldcg(x + k); });
-      r[q] = rt;
-      acc += rt * rt;
+    rr = rr0;
+    if (sqrt(rr) <= thr) {  // converged at iteration 0: the true residual is this one
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.out_i[0] = 0;
+        a.out_i[1] = 0;
+        a.out_d[0] = bnorm;
+        a.out_d[1] = sqrt(rr) / bnorm;
+      }
+      return;
     }
-    rr = grid_sum(acc, a, slot, sh);
   }
   int iters = 0, status = 3;
   double final_rr = rr;
@@ -235,7 +277,7 @@ int cg_grid_blocks() {
   return g_cg_blocks;
 }
 
-size_t cg_workspace_doubles(int64_t ng) { return (size_t)4 * ng + 2 * 4096; }
+size_t cg_workspace_doubles(int64_t ng) { return (size_t)4 * ng + 4 * 4096; }
 
 void launch_cg(int64_t n0, int64_t n1, int64_t n2, const double ih2[3], const double* b,
                double* x, int warm, double* ws, unsigned* bar, int* out_i, double* out_d,
@@ -373,6 +415,7 @@ void DstPoisson::release() {
 }
 
 void DstPoisson::solve(const double* b, double* x, cudaStream_t s) {
+  if (launch_dst_fused(*this, b, x, s)) return;
   const int64_t pn = n1 * n2p;  // natural padded plane
   const int64_t pt = n2 * n1p;  // transposed padded plane
   const dim3 tb(TT, 8);

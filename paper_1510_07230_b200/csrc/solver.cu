@@ -37,16 +37,11 @@ struct BlockPool {
   Engine& E;
   std::vector<int> free_;
   explicit BlockPool(Engine& e) : E(e) {}
-  ~BlockPool() {
-    for (int h : free_) {
-      try {
-        E.free_block(h);
-      } catch (...) {
-      }
-    }
+  ~BlockPool() {  // back to the engine's cache: the next solve allocates nothing
+    for (int h : free_) E.give_block(h);
   }
   void reserve(int n) {  // allocate up front: no cudaMalloc inside the iteration loop
-    while ((int)free_.size() < n) free_.push_back(E.alloc_block());
+    while ((int)free_.size() < n) free_.push_back(E.take_block());
   }
   BRef get() {
     int h;
@@ -54,7 +49,7 @@ struct BlockPool {
       h = free_.back();
       free_.pop_back();
     } else {
-      h = E.alloc_block();
+      h = E.take_block();
     }
     return BRef(new int(h), [this](int* p) {
       free_.push_back(*p);
@@ -68,15 +63,10 @@ struct StatePool {
   std::vector<DevState*> free_;
   explicit StatePool(Engine& e) : E(e) {}
   ~StatePool() {
-    for (DevState* s : free_) {
-      try {
-        E.free_state(s);
-      } catch (...) {
-      }
-    }
+    for (DevState* s : free_) E.give_state(s);
   }
   void reserve(int n) {
-    while ((int)free_.size() < n) free_.push_back(E.new_state());
+    while ((int)free_.size() < n) free_.push_back(E.take_state());
   }
   SRef get() {
     DevState* s;
@@ -84,7 +74,7 @@ struct StatePool {
       s = free_.back();
       free_.pop_back();
     } else {
-      s = E.new_state();
+      s = E.take_state();
     }
     return SRef(s, [this](DevState* p) { free_.push_back(p); });
   }
