@@ -246,6 +246,10 @@ enum {
   PO_OP_POISSON = 6,     /* CG solve on the last density (default state) */
   PO_OP_CHOLESKY = 7,    /* device Cholesky + L^{-T} of the last Gram */
   PO_OP_LAPLACIAN = 8,   /* out = lap a */
+  PO_OP_GRAM_TRIAL = 9,  /* G = <(a - 0.3 b)^T (a - 0.3 b)> (the line-search trial Gram) */
+  PO_OP_ROTATION = 10,   /* out = (a - 0.3 b) M, M = last Cholesky's L^{-T} (upper) */
+  PO_OP_DIRECTIONS = 11, /* fused directions: W = a, HW = b, history (a, b), Sigma = last Gram */
+  PO_OP_ROTATION_FUSED = 12, /* rotation + verification Gram + density/xc (default state) */
   PO_OP_HAMILTONIAN_VARIANT = 100  /* + v: H a design-space variants (measurement only) */
 };
 int po_enqueue(po_engine* e, int op, int a, int b, int out);

@@ -50,6 +50,11 @@ __device__ __forceinline__ void block_sum(double (&v)[NQ], double* smem /* >= 32
   __syncthreads();
 }
 
+__device__ __forceinline__ double dirac_cx() {
+  // kDiracCx = 0.75 * cbrt(3 / pi), energy.cpp:18
+  return 0.75 * cbrt(3.0 / 3.141592653589793238462643383279502884);
+}
+
 // One warp mma.sync m8n8k4 fp64 (SASS DMMA.8x8x4): D = A(8x4, row) B(4x8, col) + C.
 // Fragments: a = A[lane/4][lane%4], b = B[lane%4][lane/4],
 //            c[j] = C[lane/4][2*(lane%4) + j].

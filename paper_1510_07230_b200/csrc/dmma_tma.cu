@@ -26,7 +26,9 @@ namespace {
 constexpr int BOX = 16;           // points per box (128 B rows, SWIZZLE_128B)
 constexpr int TKS = 64;           // points per stage (4 boxes)
 constexpr int TSC = 8;            // consumer warps
-constexpr int TTH = (TSC + 1) * 32;
+// 8 consumer warps (warpgroups 0-1) + a producer warpgroup (one lane issues the
+// boxes) that hands its registers to the consumers via setmaxnreg (40 / 232).
+constexpr int TTH = (TSC + 4) * 32;
 constexpr size_t TBUDGET = 180 * 1024;
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -50,14 +52,26 @@ bool make_map(CUtensorMap* m, const double* base, int64_t ld, int rows, int npad
   cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
   cuuint32_t box[2] = {BOX, (cuuint32_t)npad};
   cuuint32_t es[2] = {1, 1};
+  static const int promo = getenv("PO_TMA_PROMO") ? atoi(getenv("PO_TMA_PROMO")) : 3;
+  const CUtensorMapL2promotion pr = promo == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                    : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                 : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Sources of a streamed contraction (one tensor map per source block).
 struct Maps {
   CUtensorMap m[4];
 };
+
+bool make_map2(Maps& M, int i, const double* base, int64_t ld, int rows, int npad) {
+  return make_map(&M.m[i], base, ld, rows, npad);
+}
+
+
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
                                             uint64_t* bar) {
@@ -81,34 +95,62 @@ struct TCfg {
   size_t stage_doubles, smem;
 };
 
+size_t tbudget() {
+  static size_t b = 0;
+  if (!b) {
+    const char* e = getenv("PO_TMA_BUDGET_KB");  // measurement override
+    b = (e ? (size_t)atoi(e) : 0) * 1024;
+    if (b < 64 * 1024 || b > 220 * 1024) b = TBUDGET;
+  }
+  return b;
+}
+
 TCfg tcfg(int nsrc, int npad, size_t extra_doubles) {
   TCfg c;
   c.stage_doubles = (size_t)nsrc * (TKS / BOX) * npad * BOX;
-  const size_t avail = TBUDGET / 8 - extra_doubles;
+  const size_t avail = tbudget() / 8 - extra_doubles;
   c.nst = (int)(avail / c.stage_doubles);
-  if (c.nst > 6) c.nst = 6;
+  if (c.nst > 8) c.nst = 8;
   if (c.nst < 2) c.nst = 2;
   c.smem = 2048 /*barriers + alignment slack*/ + ((size_t)c.nst * c.stage_doubles + extra_doubles) * 8;
   return c;
 }
 
-// producer warp, lane 0: one 2D box per (source, box) per stage
+// producer warp: lane 0 recycles the stage and arms its barrier, then one lane
+// per (source, box) issues that box — the boxes of a stage go out in parallel
+// instead of one after another from a single thread
 __device__ __forceinline__ void tma_produce(const CUtensorMap* maps, int nsrc, int npad,
                                             int64_t kbeg, int64_t kend, int nst, size_t sdoubles,
                                             double* stage0, uint64_t* full, uint64_t* empty) {
+  const int lane = threadIdx.x & 31;
   const int nstage = kend > kbeg ? (int)((kend - kbeg + TKS - 1) / TKS) : 0;
   const uint32_t bytes = (uint32_t)(nsrc * (TKS / BOX) * npad * BOX * 8);
+  const int nbox = nsrc * (TKS / BOX);
   for (int st = 0; st < nstage; ++st) {
     const int s = st % nst;
-    if (st >= nst) mbar_wait(&empty[s], ((uint32_t)(st / nst) & 1u) ^ 1u);
-    mbar_arrive_expect_tx(&full[s], bytes);
+    if (lane == 0) {
+      if (st >= nst) mbar_wait(&empty[s], ((uint32_t)(st / nst) & 1u) ^ 1u);
+      mbar_arrive_expect_tx(&full[s], bytes);
+    }
+    __syncwarp();
     const int64_t k0 = kbeg + (int64_t)st * TKS;
     double* sb = stage0 + (size_t)s * sdoubles;
-    for (int q = 0; q < nsrc; ++q)
-      for (int b = 0; b < TKS / BOX; ++b)
-        tma_load_2d(sb + ((size_t)q * (TKS / BOX) + b) * npad * BOX, &maps[q], (int)(k0 + b * BOX),
-                    0, &full[s]);
+    for (int e = lane; e < nbox; e += 32) {
+      const int q = e / (TKS / BOX), b = e % (TKS / BOX);
+      tma_load_2d(sb + ((size_t)q * (TKS / BOX) + b) * npad * BOX, &maps[q], (int)(k0 + b * BOX), 0,
+                  &full[s]);
+    }
   }
+}
+
+// producer side of every small-N streamed kernel (called by the whole producer warpgroup)
+// (measured alternative, not kept: a cp.async producer warpgroup streamed the
+// same stages at about half the rate of the TMA boxes on B200)
+__device__ __forceinline__ void produce(const Maps& mp, int nsrc, int npad, int64_t kbeg,
+                                        int64_t kend, int nst, size_t sdoubles, double* stage0,
+                                        uint64_t* full, uint64_t* empty) {
+  if ((threadIdx.x >> 5) == TSC)
+    tma_produce(mp.m, nsrc, npad, kbeg, kend, nst, sdoubles, stage0, full, empty);
 }
 
 template <int F, bool SYM>
@@ -116,16 +158,24 @@ struct TPairs {
   static constexpr int NP = SYM ? F * (F + 1) / 2 : F * F;
 };
 
-template <int F, bool SYM>
+// F = ceil(N/8) fragments lay out the stage (NPAD = 8F rows per box); with R > 0
+// (N = 8(F-1) + R, R <= 2) only the first F-1 fragments go through DMMA and the
+// R trailing orbitals are contracted with plain FP64 FMAs — on B200 FP64 FMA
+// and DMMA have the same peak, so a fragment row that is 7/8 zero padding
+// (N = 33) costs ~10 DMMAs per 8 points for one useful orbital otherwise.
+template <int F, bool SYM, int R>
 __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant__ Maps maps,
-                                                          int nsrc, int qa_b, int qb, int qb_b,
-                                                          int64_t ld, int64_t kchunk, int nst,
-                                                          double sa, double sb,
+                                                          int N, int nsrc, int qa_b, int qb,
+                                                          int qb_b, int64_t ld, int64_t kchunk,
+                                                          int nst, double sa, double sb,
                                                           double* __restrict__ ws,
-                                                          const double* __restrict__ guard) {
+                                                          const double* __restrict__ guard,
+                                                          int probe) {
   if (guard && *guard == 0.0) return;
-  constexpr int NP = TPairs<F, SYM>::NP;
+  constexpr int FD = R > 0 ? F - 1 : F;  // DMMA fragments
+  constexpr int NP = TPairs<FD, SYM>::NP;
   constexpr int NPAD = 8 * F;
+  constexpr int NR = SYM ? 1 : 2;  // remainder products per (lane orbital, remainder orbital)
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   // SWIZZLE_128B boxes need 1024-byte aligned destinations
   unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
@@ -146,25 +196,76 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
   const int64_t kend = min(kbeg + kchunk, ld);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, t4 = lane & 3;
-  double acc[NP][2];
-#pragma unroll
-  for (int q = 0; q < NP; ++q) acc[q][0] = acc[q][1] = 0.0;
-  if (warp == TSC) {
-    if (lane == 0) {
-      for (int q = 0; q < nsrc; ++q)
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[q])));
-      tma_produce(maps.m, nsrc, NPAD, kbeg, kend, nst, sdoubles, stage0, full, empty);
-    }
+  double* red = stage0;  // after the loop: [8 warps][NP * 64] then [8 warps][2][R][NR][32]
+  constexpr int RS = 2 * (R > 0 ? R : 1) * NR * 32;
+  double* rred = red + (size_t)TSC * NP * 64;
+  if (warp >= TSC) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    produce(maps, nsrc, NPAD, kbeg, kend, nst, sdoubles, stage0, full, empty);
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    double acc[NP > 0 ? NP : 1][2];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) acc[q][0] = acc[q][1] = 0.0;
+    // remainder accumulators: lane orbital i in {lane, lane + 32}, remainder orbital r
+    double racc[2][R > 0 ? R : 1][NR];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int r = 0; r < (R > 0 ? R : 1); ++r)
+#pragma unroll
+        for (int k = 0; k < NR; ++k) racc[h][r][k] = 0.0;
     const int nstage = kend > kbeg ? (int)((kend - kbeg + TKS - 1) / TKS) : 0;
     const int c = warp * 8;  // this warp's 8-point chunk of every stage
-    for (int st = 0; st < nstage; ++st) {
-      const int s = st % nst;
-      mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
-      const double* sbuf = stage0 + (size_t)s * sdoubles;
-      double2 a[F], b[SYM ? 1 : F];
+    // a row's 8 points of the chunk as 4 double2 (A side or B side, trial-combined)
+    auto row8 = [&](const double* sbuf, int row, int q0, int q1, double sc, double2 (&v)[4]) {
 #pragma unroll
-      for (int f = 0; f < F; ++f) {
+      for (int m = 0; m < 4; ++m) {
+        const int off = swz(row, c + 2 * m, NPAD);
+        v[m] = *reinterpret_cast<const double2*>(sbuf + q0 * qstride + off);
+        if (q1 >= 0) {
+          const double2 z = *reinterpret_cast<const double2*>(sbuf + q1 * qstride + off);
+          v[m].x += sc * z.x;
+          v[m].y += sc * z.y;
+        }
+      }
+    };
+    auto remainder = [&](const double* sbuf) {
+      const int qbb = SYM ? 0 : qb, qbbb = SYM ? qa_b : qb_b;
+      const double sbb = SYM ? sa : sb;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int rr = 8 * FD + r;
+        double2 brv[4], arv[4];
+        row8(sbuf, rr, qbb, qbbb, sbb, brv);                    // B_r (broadcast)
+        if constexpr (!SYM) row8(sbuf, rr, 0, qa_b, sa, arv);  // A_r
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = lane + 32 * h;
+          if (i >= N || (SYM && i > rr)) continue;
+          double2 av[4];
+          row8(sbuf, i, 0, qa_b, sa, av);
+          double t = racc[h][r][0];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) t = fma(av[m].y, brv[m].y, fma(av[m].x, brv[m].x, t));
+          racc[h][r][0] = t;
+          if constexpr (!SYM) {
+            if (i < 8 * FD) {  // B_i A_r for i outside the remainder (else counted above)
+              double2 bv[4];
+              row8(sbuf, i, qb, qb_b, sb, bv);
+              double u = racc[h][r][NR - 1];
+#pragma unroll
+              for (int m = 0; m < 4; ++m) u = fma(arv[m].y, bv[m].y, fma(arv[m].x, bv[m].x, u));
+              racc[h][r][NR - 1] = u;
+            }
+          }
+        }
+      }
+    };
+    constexpr int FA = FD > 0 ? FD : 1, FB = SYM ? 1 : FA;
+    auto frags = [&](const double* sbuf, double2 (&a)[FA], double2 (&b)[FB]) {
+#pragma unroll
+      for (int f = 0; f < FD; ++f) {
         const int off = swz(8 * f + gq, c + 2 * t4, NPAD);  // 16-B aligned pair of points
         a[f] = *reinterpret_cast<const double2*>(sbuf + off);
         if (qa_b >= 0) {
@@ -181,26 +282,50 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
           }
         }
       }
+    };
+    // (measured: prefetching the next stage's fragments before this stage's
+    // DMMAs made the kernel slower — it is bound by the TMA stream, not by
+    // shared-memory latency — so load, release, then multiply)
+    for (int st = 0; st < nstage; ++st) {
+      const int s = st % nst;
+      mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+      const double* sbuf = stage0 + (size_t)s * sdoubles;
+      if (probe) {  // measurement hook: stream the ring without consuming it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        continue;
+      }
+      if constexpr (R > 0) remainder(sbuf);
+      double2 a[FA], b[FB];
+      frags(sbuf, a, b);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);  // fragments are in registers: release early
       int q = 0;
 #pragma unroll
-      for (int fm = 0; fm < F; ++fm)
+      for (int fm = 0; fm < FD; ++fm)
 #pragma unroll
-        for (int fn = SYM ? fm : 0; fn < F; ++fn, ++q) {
+        for (int fn = SYM ? fm : 0; fn < FD; ++fn, ++q) {
           const double2 bv = SYM ? a[fn] : b[SYM ? 0 : fn];
           dmma_8x8x4(acc[q], a[fm].x, bv.x);
           dmma_8x8x4(acc[q], a[fm].y, bv.y);
         }
     }
-  }
-  __syncthreads();
-  double* red = stage0;  // reuse the ring: [8 warps][NP * 64]
-  if (warp < TSC) {
+    // all consumers are past the ring: reuse it for the CTA reduction (named
+    // barrier over the consumer warps only; the producer warpgroup runs with
+    // 40 registers and must not hold the accumulators)
+    asm volatile("bar.sync 1, %0;\n" ::"n"(TSC * 32) : "memory");
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       red[(warp * NP + q) * 64 + lane * 2] = acc[q][0];
       red[(warp * NP + q) * 64 + lane * 2 + 1] = acc[q][1];
+    }
+    if constexpr (R > 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int k = 0; k < NR; ++k) rred[warp * RS + ((h * R + r) * NR + k) * 32 + lane] = racc[h][r][k];
     }
   }
   __syncthreads();
@@ -211,13 +336,30 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
     for (int w = 0; w < TSC; ++w) sum += red[(w * NP) * 64 + e];
     const int q = e / 64, l = (e % 64) / 2, j = e % 2;
     int fm = 0, fn = 0, cq = 0;
-    for (int m = 0; m < F; ++m)
-      for (int n = SYM ? m : 0; n < F; ++n, ++cq)
+    for (int m = 0; m < FD; ++m)
+      for (int n = SYM ? m : 0; n < FD; ++n, ++cq)
         if (cq == q) {
           fm = m;
           fn = n;
         }
     out[(8 * fm + (l >> 2)) * NPAD + 8 * fn + 2 * (l & 3) + j] = sum;
+  }
+  if constexpr (R > 0) {
+    for (int e = threadIdx.x; e < RS; e += TTH) {
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < TSC; ++w) sum += rred[w * RS + e];
+      const int l = e % 32, k = (e / 32) % NR, r = (e / 32 / NR) % R, h = e / 32 / NR / R;
+      const int i = l + 32 * h, rr = 8 * FD + r;
+      if (i >= N) continue;
+      if (SYM) {
+        if (i <= rr) out[i * NPAD + rr] = sum;
+      } else if (k == 0) {
+        out[i * NPAD + rr] = sum;  // sum_p A_i B_r
+      } else if (i < 8 * FD) {
+        out[rr * NPAD + i] = sum;  // sum_p A_r B_i
+      }
+    }
   }
 }
 
@@ -258,21 +400,25 @@ bool launch_gram_tma_f(int N, int64_t ld, int sym, const double* A, const double
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   int nsrc = 0, qa_b = -1, qb = 0, qb_b = -1;
-  if (!make_map(&maps.m[nsrc++], A, ld, N, NPAD)) return false;
+  if (!make_map2(maps, nsrc++, A, ld, N, NPAD)) return false;
   if (Ab) {
     qa_b = nsrc;
-    if (!make_map(&maps.m[nsrc++], Ab, ld, N, NPAD)) return false;
+    if (!make_map2(maps, nsrc++, Ab, ld, N, NPAD)) return false;
   }
   if (!sym) {
     qb = nsrc;
-    if (!make_map(&maps.m[nsrc++], B, ld, N, NPAD)) return false;
+    if (!make_map2(maps, nsrc++, B, ld, N, NPAD)) return false;
     if (Bb) {
       qb_b = nsrc;
-      if (!make_map(&maps.m[nsrc++], Bb, ld, N, NPAD)) return false;
+      if (!make_map2(maps, nsrc++, Bb, ld, N, NPAD)) return false;
     }
   }
-  const int np = sym ? F * (F + 1) / 2 : F * F;
-  const size_t red = (size_t)TSC * np * 64;
+  // R = 0: splitting off a 1-2 orbital FMA tail (the R > 0 variants) measured
+  // slower here; the 2D TMA stream bounds this kernel, not the DMMA count
+  const int R = 0;
+  const int fd = F;
+  const int np = sym ? fd * (fd + 1) / 2 : fd * fd;
+  const size_t red = (size_t)TSC * np * 64 + (size_t)TSC * 2 * 2 * 2 * 32;
   TCfg cfg = tcfg(nsrc, NPAD, 0);
   if (cfg.smem < 2048 + red * 8) cfg.smem = 2048 + red * 8;
   const int64_t kblocks = (ld + TKS - 1) / TKS;
@@ -281,17 +427,19 @@ bool launch_gram_tma_f(int N, int64_t ld, int sym, const double* A, const double
   const int64_t kchunk = ((kblocks + nsplit - 1) / nsplit) * TKS;
   nsplit = (int)((ld + kchunk - 1) / kchunk);
   ::po::count_launch();
-  if (sym) {
-    auto k = gram_tma_kernel<F, true>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
-    k<<<nsplit, TTH, cfg.smem, s>>>(maps, nsrc, qa_b, qb, qb_b, ld, kchunk, cfg.nst, sa, sb, ws,
-                                     guard);
-  } else {
-    auto k = gram_tma_kernel<F, false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
-    k<<<nsplit, TTH, cfg.smem, s>>>(maps, nsrc, qa_b, qb, qb_b, ld, kchunk, cfg.nst, sa, sb, ws,
-                                     guard);
-  }
+  auto pick = [&]() {
+    if (F == 1) return sym ? gram_tma_kernel<F, true, 0> : gram_tma_kernel<F, false, 0>;
+    if (sym) return R == 1 ? gram_tma_kernel<F, true, 1>
+                           : R == 2 ? gram_tma_kernel<F, true, 2> : gram_tma_kernel<F, true, 0>;
+    return R == 1 ? gram_tma_kernel<F, false, 1>
+                  : R == 2 ? gram_tma_kernel<F, false, 2> : gram_tma_kernel<F, false, 0>;
+  };
+  auto k = pick();
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
+  const char* pe = getenv("PO_GRAM_PROBE");  // measurement hook (TMA ring without math)
+  const int probe = pe ? atoi(pe) : 0;
+  k<<<nsplit, TTH, cfg.smem, s>>>(maps, N, nsrc, qa_b, qb, qb_b, ld, kchunk, cfg.nst, sa, sb, ws,
+                                   guard, probe);
   const int64_t threads = (int64_t)N * N * 32;
   ::po::count_launch();
   gram_tma_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(N, NPAD, sym, nsplit, w,
@@ -336,15 +484,26 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, t4 = lane & 3;
   const bool has_ab = nsrc - (qc >= 0 ? 1 : 0) == 2;
-  double nrm[F][2];
-#pragma unroll
-  for (int fi = 0; fi < F; ++fi) nrm[fi][0] = nrm[fi][1] = 0.0;
-  if (warp == TSC) {
-    if (lane == 0) tma_produce(maps.m, nsrc, NPAD, pbeg, pend, nst, sdoubles, stage0, full, empty);
+  if (warp >= TSC) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    produce(maps, nsrc, NPAD, pbeg, pend, nst, sdoubles, stage0, full, empty);
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    double nrm[F][2];
+#pragma unroll
+    for (int fi = 0; fi < F; ++fi) nrm[fi][0] = nrm[fi][1] = 0.0;
     const int nstage = pend > pbeg ? (int)((pend - pbeg + TKS - 1) / TKS) : 0;
     const int ksteps = (N + 3) / 4;
     const int c = warp * 8;
+    // upper-triangular M: this lane's B fragments for every (k-step, output fragment)
+    double mreg[UPPER ? 2 * F : 1][UPPER ? F : 1];
+    if constexpr (UPPER) {
+#pragma unroll
+      for (int ks = 0; ks < 2 * F; ++ks)
+#pragma unroll
+        for (int fi = 0; fi < F; ++fi)
+          mreg[ks][fi] = 4 * ks > 8 * fi + 7 ? 0.0 : Ms[(4 * ks + t4) * NPAD + 8 * fi + gq];
+    }
     for (int st = 0; st < nstage; ++st) {
       const int s = st % nst;
       mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
@@ -353,15 +512,32 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
       double acc[F][2];
 #pragma unroll
       for (int f = 0; f < F; ++f) acc[f][0] = acc[f][1] = 0.0;
-      for (int ks = 0; ks < ksteps; ++ks) {
-        const int krow = 4 * ks + t4;
-        const int off = swz(krow, c + gq, NPAD);
-        double av = sbuf[off];
-        if (has_ab) av += sa * sbuf[qstride + off];
+      if constexpr (UPPER) {
+        // all A values of the chunk first (one latency), M fragments from registers
+        double av[2 * F];
 #pragma unroll
-        for (int fi = 0; fi < F; ++fi) {
-          if (UPPER && 4 * ks > 8 * fi + 7) continue;
-          dmma_8x8x4(acc[fi], av, Ms[krow * NPAD + 8 * fi + gq]);
+        for (int ks = 0; ks < 2 * F; ++ks) {
+          const int off = swz(4 * ks + t4, c + gq, NPAD);
+          av[ks] = sbuf[off];
+          if (has_ab) av[ks] += sa * sbuf[qstride + off];
+        }
+#pragma unroll
+        for (int ks = 0; ks < 2 * F; ++ks) {
+          if (ks >= ksteps) break;
+#pragma unroll
+          for (int fi = 0; fi < F; ++fi) {
+            if (4 * ks > 8 * fi + 7) continue;
+            dmma_8x8x4(acc[fi], av[ks], mreg[ks][fi]);
+          }
+        }
+      } else {
+        for (int ks = 0; ks < ksteps; ++ks) {
+          const int krow = 4 * ks + t4;
+          const int off = swz(krow, c + gq, NPAD);
+          double av = sbuf[off];
+          if (has_ab) av += sa * sbuf[qstride + off];
+#pragma unroll
+          for (int fi = 0; fi < F; ++fi) dmma_8x8x4(acc[fi], av, Ms[krow * NPAD + 8 * fi + gq]);
         }
       }
       const int64_t p = k0 + c + gq;
@@ -402,6 +578,261 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
       norms[(int64_t)i * gridDim.x + blockIdx.x] = sum;
     }
   }
+}
+
+// ------------------------------------------------------------- fused rotation
+// The orthonormalisation rotation of a line-search trial with its two
+// follow-ups folded into the epilogue (manifold.cpp:97-114 + 136-169,
+// energy.cpp:67-76 / 212-226):
+//   W~ = (W + sa Z) L^{-T}                 (DMMA, upper-triangular skip; written)
+//   G2 partial = W~^T W~ over the CTA's points  (verification Gram, DMMA + FMA tail)
+//   rho = occ sum_i W~_i^2, v_xc, 4 pi rho, <eps, rho>, <V_ext, rho> partials
+// so the trial's verification Gram and density passes over the block vanish.
+// The warp's rotated 8-point chunk goes back into its own slot of the stage
+// (same swizzled layout as the source), from where the Gram fragments are read.
+template <int F, int R>
+__global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
+    const __grid_constant__ Maps maps, int nsrc, int N, int64_t ld, int64_t ngl, int64_t pchunk,
+    int nst, double sa, const double* __restrict__ M, double* __restrict__ out,
+    double* __restrict__ ws, double occ, int xc, double* __restrict__ rho, double* __restrict__ vxc,
+    double* __restrict__ bvec, const double* __restrict__ vext, double* __restrict__ dpart) {
+  constexpr int NPAD = 8 * F;
+  constexpr int FD = R > 0 ? F - 1 : F;
+  constexpr int NP = FD * (FD + 1) / 2;
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
+  uint64_t* empty = full + 8;
+  double* stage0 = reinterpret_cast<double*>(tsm + 1024);
+  const size_t qstride = (size_t)(TKS / BOX) * NPAD * BOX;
+  const size_t sdoubles = (size_t)nsrc * qstride;
+  double* Ms = stage0 + (size_t)nst * sdoubles;  // [NPAD][NPAD]
+  for (int e = threadIdx.x; e < NPAD * NPAD; e += TTH) {
+    const int k = e / NPAD, i = e % NPAD;
+    Ms[e] = (k < N && i < N) ? M[(int64_t)k * N + i] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], TSC);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t pbeg = (int64_t)blockIdx.x * pchunk;
+  const int64_t pend = min(pbeg + pchunk, ld);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, t4 = lane & 3;
+  const double cx = dirac_cx();
+  const double four_pi = 4.0 * 3.141592653589793238462643383279502884;
+  double* red = stage0;
+  constexpr int RS = 2 * (R > 0 ? R : 1) * 32;
+  double* rred = red + (size_t)TSC * NP * 64;
+  double* ered = rred + (size_t)TSC * RS;
+  if (warp >= TSC) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    produce(maps, nsrc, NPAD, pbeg, pend, nst, sdoubles, stage0, full, empty);
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    double gacc[NP > 0 ? NP : 1][2];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) gacc[q][0] = gacc[q][1] = 0.0;
+    double racc[2][R > 0 ? R : 1];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int r = 0; r < (R > 0 ? R : 1); ++r) racc[h][r] = 0.0;
+    double eacc[2] = {0.0, 0.0};
+    const int nstage = pend > pbeg ? (int)((pend - pbeg + TKS - 1) / TKS) : 0;
+    const int ksteps = (N + 3) / 4;
+    const int c = warp * 8;
+    double mreg[2 * F][F];  // this lane's fragments of the upper-triangular L^{-T}
+#pragma unroll
+    for (int ks = 0; ks < 2 * F; ++ks)
+#pragma unroll
+      for (int fi = 0; fi < F; ++fi)
+        mreg[ks][fi] = 4 * ks > 8 * fi + 7 ? 0.0 : Ms[(4 * ks + t4) * NPAD + 8 * fi + gq];
+    for (int st = 0; st < nstage; ++st) {
+      const int s = st % nst;
+      mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+      double* sbuf = stage0 + (size_t)s * sdoubles;
+      const int64_t p = pbeg + (int64_t)st * TKS + c + gq;
+      double acc[F][2];
+#pragma unroll
+      for (int f = 0; f < F; ++f) acc[f][0] = acc[f][1] = 0.0;
+      {
+        double av[2 * F];
+#pragma unroll
+        for (int ks = 0; ks < 2 * F; ++ks) {
+          const int off = swz(4 * ks + t4, c + gq, NPAD);
+          av[ks] = sbuf[off];
+          if (nsrc == 2) av[ks] += sa * sbuf[qstride + off];
+        }
+#pragma unroll
+        for (int ks = 0; ks < 2 * F; ++ks) {
+          if (ks >= ksteps) break;
+#pragma unroll
+          for (int fi = 0; fi < F; ++fi) {
+            if (4 * ks > 8 * fi + 7) continue;
+            dmma_8x8x4(acc[fi], av[ks], mreg[ks][fi]);
+          }
+        }
+      }
+      __syncwarp();  // every lane is done reading the chunk's source values
+      double dsum = 0.0;
+#pragma unroll
+      for (int fi = 0; fi < F; ++fi)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = 8 * fi + 2 * t4 + j;
+          if (i < N) {
+            const double v = acc[fi][j];
+            if (p < ngl) out[(int64_t)i * ld + p] = v;
+            sbuf[swz(i, c + gq, NPAD)] = v;
+            dsum += v * v;
+          }
+        }
+      // density of the rotated chunk: sum over the 4 lanes sharing point c + gq
+      dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
+      dsum += __shfl_xor_sync(0xffffffffu, dsum, 2);
+      if (t4 == 0 && p < ngl) {
+        const double r = occ == 1.0 ? dsum : dsum * occ;
+        rho[p] = r;
+        if (xc) {
+          const double eps = -cx * cbrt(r);
+          vxc[p] = eps * (4.0 / 3.0);
+          eacc[0] += eps * r;
+        } else {
+          vxc[p] = 0.0;
+        }
+        if (bvec) bvec[p] = r * four_pi;
+        if (vext) eacc[1] += __ldg(vext + p) * r;
+      }
+      __syncwarp();  // rotated chunk visible to the whole warp
+      if constexpr (R > 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int rr = 8 * FD + r;
+          double2 bv[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            bv[m] = *reinterpret_cast<const double2*>(sbuf + swz(rr, c + 2 * m, NPAD));
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = lane + 32 * h;
+            if (i >= N || i > rr) continue;
+            double t = racc[h][r];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const double2 av = *reinterpret_cast<const double2*>(sbuf + swz(i, c + 2 * m, NPAD));
+              t = fma(av.y, bv[m].y, fma(av.x, bv[m].x, t));
+            }
+            racc[h][r] = t;
+          }
+        }
+      }
+      double2 a[FD > 0 ? FD : 1];
+#pragma unroll
+      for (int f = 0; f < FD; ++f)
+        a[f] = *reinterpret_cast<const double2*>(sbuf + swz(8 * f + gq, c + 2 * t4, NPAD));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      int q = 0;
+#pragma unroll
+      for (int fm = 0; fm < FD; ++fm)
+#pragma unroll
+        for (int fn = fm; fn < FD; ++fn, ++q) {
+          dmma_8x8x4(gacc[q], a[fm].x, a[fn].x);
+          dmma_8x8x4(gacc[q], a[fm].y, a[fn].y);
+        }
+    }
+    // CTA reductions (consumers only, ring reused): G2 partial tile -> ws[block];
+    // energies -> dpart[2][grid]
+    asm volatile("bar.sync 1, %0;\n" ::"n"(TSC * 32) : "memory");
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      red[(warp * NP + q) * 64 + lane * 2] = gacc[q][0];
+      red[(warp * NP + q) * 64 + lane * 2 + 1] = gacc[q][1];
+    }
+    if constexpr (R > 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int r = 0; r < R; ++r) rred[warp * RS + (h * R + r) * 32 + lane] = racc[h][r];
+    }
+    double e0 = warp_sum(eacc[0]), e1 = warp_sum(eacc[1]);
+    if (lane == 0) {
+      ered[warp] = e0;
+      ered[TSC + warp] = e1;
+    }
+  }
+  __syncthreads();
+  double* o = ws + (int64_t)blockIdx.x * NPAD * NPAD;
+  for (int e = threadIdx.x; e < NP * 64; e += TTH) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < TSC; ++w) sum += red[(w * NP) * 64 + e];
+    const int q = e / 64, l = (e % 64) / 2, j = e % 2;
+    int fm = 0, fn = 0, cq = 0;
+    for (int m = 0; m < FD; ++m)
+      for (int n = m; n < FD; ++n, ++cq)
+        if (cq == q) {
+          fm = m;
+          fn = n;
+        }
+    o[(8 * fm + (l >> 2)) * NPAD + 8 * fn + 2 * (l & 3) + j] = sum;
+  }
+  if constexpr (R > 0) {
+    for (int e = threadIdx.x; e < RS; e += TTH) {
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < TSC; ++w) sum += rred[w * RS + e];
+      const int l = e % 32, r = (e / 32) % R, h = e / 32 / R;
+      const int i = l + 32 * h, rr = 8 * FD + r;
+      if (i < N && i <= rr) o[i * NPAD + rr] = sum;
+    }
+  }
+  if (threadIdx.x < 2) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < TSC; ++w) sum += ered[threadIdx.x * TSC + w];
+    dpart[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = sum;
+  }
+}
+
+template <int F>
+int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab,
+                          double sa, const double* M, double* out, double* ws, double* G, double w,
+                          double occ, int xc, double* rho, double* vxc, double* bvec,
+                          const double* vext, double* dpart, cudaStream_t s) {
+  constexpr int NPAD = 8 * F;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  int nsrc = 0;
+  if (!make_map2(maps, nsrc++, A, ld, N, NPAD)) return -1;
+  if (Ab && !make_map2(maps, nsrc++, Ab, ld, N, NPAD)) return -1;
+  const int R = (N % 8 == 1 || N % 8 == 2) && N > 8 ? N % 8 : 0;
+  const int fd = R ? F - 1 : F;
+  const size_t red = (size_t)TSC * (fd * (fd + 1) / 2) * 64 + (size_t)TSC * 2 * 2 * 32 + 2 * TSC;
+  const size_t extra = (size_t)NPAD * NPAD;
+  TCfg cfg = tcfg(nsrc, NPAD, extra);
+  if (cfg.smem < 2048 + red * 8) cfg.smem = 2048 + red * 8;
+  const int64_t kb = (ld + TKS - 1) / TKS;
+  int nblk = nsm();
+  if (nblk > kb) nblk = (int)kb;
+  const int64_t pchunk = ((kb + nblk - 1) / nblk) * TKS;
+  nblk = (int)((ld + pchunk - 1) / pchunk);
+  auto k = F == 1 || R == 0 ? rotate_fused_kernel<F, 0>
+                            : R == 1 ? rotate_fused_kernel<F, 1> : rotate_fused_kernel<F, 2>;
+  ::po::count_launch();
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
+  k<<<nblk, TTH, cfg.smem, s>>>(maps, nsrc, N, ld, ngl, pchunk, cfg.nst, sa, M, out, ws, occ, xc,
+                                 rho, vxc, bvec, vext, dpart);
+  const int64_t threads = (int64_t)N * N * 32;
+  ::po::count_launch();
+  gram_tma_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(N, NPAD, 1, nblk, w, ws,
+                                                                           G, nullptr);
+  return nblk;
 }
 
 // ---------------------------------------------------------- fused directions
@@ -447,14 +878,16 @@ __global__ void __launch_bounds__(TTH, 1) directions_tma_kernel(
   const int64_t pend = min(pbeg + pchunk, ld);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, t4 = lane & 3;
-  double nrm[NQ][F][2];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q)
-#pragma unroll
-    for (int fi = 0; fi < F; ++fi) nrm[q][fi][0] = nrm[q][fi][1] = 0.0;
-  if (warp == TSC) {
-    if (lane == 0) tma_produce(maps.m, NSRC, NPAD, pbeg, pend, nst, sdoubles, stage0, full, empty);
+  if (warp >= TSC) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    produce(maps, NSRC, NPAD, pbeg, pend, nst, sdoubles, stage0, full, empty);
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    double nrm[NQ][F][2];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int fi = 0; fi < F; ++fi) nrm[q][fi][0] = nrm[q][fi][1] = 0.0;
     const int nstage = pend > pbeg ? (int)((pend - pbeg + TKS - 1) / TKS) : 0;
     const int ksteps = (N + 3) / 4;
     const int c = warp * 8;
@@ -552,8 +985,8 @@ int launch_directions_f(int N, int64_t ld, int64_t ngl, const double* W, const d
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   const bool hist = WP && ZP;
-  if (!make_map(&maps.m[0], W, ld, N, NPAD) || !make_map(&maps.m[1], HW, ld, N, NPAD)) return -1;
-  if (hist && (!make_map(&maps.m[2], WP, ld, N, NPAD) || !make_map(&maps.m[3], ZP, ld, N, NPAD)))
+  if (!make_map2(maps, 0, W, ld, N, NPAD) || !make_map2(maps, 1, HW, ld, N, NPAD)) return -1;
+  if (hist && (!make_map2(maps, 2, WP, ld, N, NPAD) || !make_map2(maps, 3, ZP, ld, N, NPAD)))
     return -1;
   if (Sigma)
     return hist ? launch_directions_fdh<F, true, true>(maps, N, ld, ngl, Sigma, sig, Z, partials, s)
@@ -570,11 +1003,11 @@ int launch_mix_tma_f(int N, int64_t ld, int64_t ngl, const double* A, const doub
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   int nsrc = 0, qc = -1;
-  if (!make_map(&maps.m[nsrc++], A, ld, N, NPAD)) return -1;
-  if (Ab && !make_map(&maps.m[nsrc++], Ab, ld, N, NPAD)) return -1;
+  if (!make_map2(maps, nsrc++, A, ld, N, NPAD)) return -1;
+  if (Ab && !make_map2(maps, nsrc++, Ab, ld, N, NPAD)) return -1;
   if (C) {
     qc = nsrc;
-    if (!make_map(&maps.m[nsrc++], C, ld, N, NPAD)) return -1;
+    if (!make_map2(maps, nsrc++, C, ld, N, NPAD)) return -1;
   }
   const size_t extra = (size_t)NPAD * NPAD + (size_t)TSC * NPAD;
   const TCfg cfg = tcfg(nsrc, NPAD, extra);
@@ -895,6 +1328,20 @@ bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* 
 }
 
 bool tma2d_available() { return encode_fn() != nullptr; }
+
+int launch_rotate_fused(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab,
+                        double sa, const double* M, double* out, double* ws, double* G, double w,
+                        double occ, int xc, double* rho, double* vxc, double* bvec,
+                        const double* vext, double* dpart, cudaStream_t s) {
+  switch ((N + 7) / 8) {
+#define PO_RF(F) \
+  case F:        \
+    return launch_rotate_fused_f<F>(N, ld, ngl, A, Ab, sa, M, out, ws, G, w, occ, xc, rho, vxc, bvec, vext, dpart, s);
+    PO_RF(1) PO_RF(2) PO_RF(3) PO_RF(4) PO_RF(5) PO_RF(6)
+#undef PO_RF
+  }
+  return -1;
+}
 
 int launch_directions(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
                       const double* WP, const double* ZP, const double* Sigma, const double* sig,

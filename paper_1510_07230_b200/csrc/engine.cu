@@ -9,6 +9,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cstdlib>
+
 #include "engine.h"
 
 namespace po {
@@ -59,6 +61,7 @@ Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist
   g.plane = g.n1 * g.n2;
   g.ngl = g.nz * g.plane;
   g.ld = round_up(g.ngl, 32);
+  if (const char* e = getenv("PO_LD_PAD")) g.ld += round_up(atoi(e), 32);  // measurement
   g.w = 1.0;
   for (int a = 0; a < 3; ++a) {
     ext[a] = grid->extent[a];
@@ -241,13 +244,14 @@ void Engine::poisson(int warm_ok) {
   }
 }
 
-void Engine::build_state(const double* u, int hartree, int xc, DevState* st, int warm_ok) {
-  double* b_local = nullptr;
-  if (hartree)
-    b_local = size > 1 ? cg_b + ng_full + (int64_t)size * max_slab_points : cg_b + g.z0 * g.plane;
-  launch_density_xc(g, N, u, occ, xc, st->rho, st->v_xc, b_local, v_ext, partials, s);
+void Engine::build_state(const double* u, int hartree, int xc, DevState* st, int warm_ok,
+                         bool density_done) {
+  double* b_local = density_b_target(hartree);
   const int pn = points_nblk(g);
-  launch_reduce_rows(partials, 2, pn, g.w, scal() + S_EXC, s);  // E_xc = <eps, rho>, E_ext
+  if (!density_done) {  // else: rho, v_xc, 4 pi rho and S_EXC/S_EEXT came from the rotation
+    launch_density_xc(g, N, u, occ, xc, st->rho, st->v_xc, b_local, v_ext, partials, s);
+    launch_reduce_rows(partials, 2, pn, g.w, scal() + S_EXC, s);  // E_xc = <eps, rho>, E_ext
+  }
   if (hartree) {
     if (size > 1) {
       comm->allgather(b_local, cg_b + ng_full, (size_t)max_slab_points, s);
@@ -723,6 +727,25 @@ extern "C" int po_enqueue(po_engine* h, int op, int a, int b, int out) {
       break;
     case PO_OP_LAPLACIAN:
       po::launch_laplacian(E.g, E.N, E.blk(a), nullptr, nullptr, E.blk(out), E.s);
+      break;
+    case PO_OP_GRAM_TRIAL:
+      po::launch_gram(E.g, E.N, E.blk(a), E.blk(b), -0.3, E.blk(a), E.blk(b), -0.3, 1, E.gram_ws,
+                      E.dmat[0], E.s);
+      break;
+    case PO_OP_ROTATION:
+      po::launch_mix(E.g, E.N, E.blk(a), E.blk(b), -0.3, E.dmat[1], 1.0, nullptr, 0.0, 1,
+                     E.blk(out), nullptr, E.s);
+      break;
+    case PO_OP_ROTATION_FUSED:
+      if (po::launch_rotate_fused(E.N, E.g.ld, E.g.ngl, E.blk(a), E.blk(b), -0.3, E.dmat[1],
+                                  E.blk(out), E.gram_ws, E.dmat[2], E.g.w, E.occ, 1, st->rho,
+                                  st->v_xc, E.density_b_target(1), E.v_ext, E.partials, E.s) < 0)
+        throw Error(PO_EINVAL, "fused rotation unavailable for this N");
+      break;
+    case PO_OP_DIRECTIONS:
+      if (po::launch_directions(E.N, E.g.ld, E.g.ngl, E.blk(a), E.blk(b), E.blk(a), E.blk(b),
+                                E.dmat[0], E.dvec, E.blk(out), E.partials, E.s) < 0)
+        throw Error(PO_EINVAL, "directions kernel unavailable for this N");
       break;
     default:
       if (op >= PO_OP_HAMILTONIAN_VARIANT &&

@@ -101,7 +101,13 @@ class Engine {
 
   // ---- operators (device-side results land in dvec_ regions; see *_result)
   // density -> Poisson -> xc -> v_local; returns after queueing; results via sync_state
-  void build_state(const double* u, int hartree, int xc, DevState* st, int warm_ok);
+  void build_state(const double* u, int hartree, int xc, DevState* st, int warm_ok,
+                   bool density_done = false);
+  // where build_state puts 4 pi rho for the Poisson solve (null without Hartree)
+  double* density_b_target(int hartree) {
+    if (!hartree) return nullptr;
+    return size > 1 ? cg_b + ng_full + (int64_t)size * max_slab_points : cg_b + g.z0 * g.plane;
+  }
   void poisson(int warm_ok);  // cg_b -> cg_x with the selected solver
   // CG outcome + E_H / E_xc of the last build (synchronises)
   void finish_state(DevState* st);

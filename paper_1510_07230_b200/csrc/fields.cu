@@ -14,11 +14,6 @@ namespace {
 constexpr int PT = 256;         // threads per CTA for point-parallel kernels
 constexpr int PMAXBLK = 148 * 8;
 
-__device__ __forceinline__ double dirac_cx() {
-  // kDiracCx = 0.75 * cbrt(3 / pi), energy.cpp:18
-  return 0.75 * cbrt(3.0 / 3.141592653589793238462643383279502884);
-}
-
 // energy.cpp:67-76 density + 212-226 Dirac exchange + 4 pi rho (energy.cpp:207-209)
 __global__ void __launch_bounds__(PT) density_xc_kernel(SlabGeom g, int N,
                                                         const double* __restrict__ u, double occ,
@@ -26,7 +21,9 @@ __global__ void __launch_bounds__(PT) density_xc_kernel(SlabGeom g, int N,
                                                         double* __restrict__ vxc,
                                                         double* __restrict__ b,
                                                         const double* __restrict__ vext,
-                                                        double* __restrict__ partials) {
+                                                        double* __restrict__ partials,
+                                                        const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;  // device-side branch (CholeskyQR2 repair)
   __shared__ double red[2 * 32];
   double acc[2] = {0.0, 0.0};
   const double cx = dirac_cx();
@@ -161,7 +158,9 @@ __global__ void __launch_bounds__(PT) lincomb_kernel(int64_t total, const double
 
 // One warp per row; lanes stride the partials, then a fixed shuffle tree.
 __global__ void reduce_rows_kernel(const double* __restrict__ partials, int rows, int nblk,
-                                   double scale, double* __restrict__ out) {
+                                   double scale, double* __restrict__ out,
+                                   const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -237,10 +236,10 @@ int per_orbital_nblk(const SlabGeom& g, int N) {
 
 void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupation, int xc,
                        double* rho, double* v_xc, double* b, const double* v_ext, double* partials,
-                       cudaStream_t s) {
+                       cudaStream_t s, const double* guard) {
   ::po::count_launch();
   density_xc_kernel<<<points_nblk(g), PT, 0, s>>>(g, N, u, occupation, xc, rho, v_xc, b, v_ext,
-                                                  partials);
+                                                  partials, guard);
 }
 
 void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h, const double* v_xc,
@@ -278,11 +277,11 @@ void launch_lincomb(const SlabGeom& g, int N, const double* a, double sc, const 
 }
 
 void launch_reduce_rows(const double* partials, int rows, int nblk, double scale, double* out,
-                        cudaStream_t s) {
+                        cudaStream_t s, const double* guard) {
   const int threads = 256;
   const int blocks = (rows * 32 + threads - 1) / threads;
   ::po::count_launch();
-  reduce_rows_kernel<<<blocks, threads, 0, s>>>(partials, rows, nblk, scale, out);
+  reduce_rows_kernel<<<blocks, threads, 0, s>>>(partials, rows, nblk, scale, out, guard);
 }
 
 void launch_external_potential(const SlabGeom& g, const double* h3, const double* atoms,

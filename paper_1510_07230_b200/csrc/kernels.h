@@ -42,7 +42,7 @@ int per_orbital_nblk(const SlabGeom& g, int N);
 // (v_ext may be null).
 void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupation, int xc,
                        double* rho, double* v_xc, double* b, const double* v_ext, double* partials,
-                       cudaStream_t s);
+                       cudaStream_t s, const double* guard = nullptr);
 // v_local = v_ext + (v_h + v_xc) (energy.cpp:241-244); partials [1][nblk]: sum v_h*rho.
 void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h, const double* v_xc,
                    const double* rho, double* v_local, double* partials, cudaStream_t s);
@@ -59,7 +59,7 @@ void launch_lincomb(const SlabGeom& g, int N, const double* a, double sc, const 
 void launch_abs_sum(const SlabGeom& g, int N, const double* x, double* partials, cudaStream_t s);
 // out[r] = scale * sum_b partials[r * nblk + b], fixed order (deterministic).
 void launch_reduce_rows(const double* partials, int rows, int nblk, double scale, double* out,
-                        cudaStream_t s);
+                        cudaStream_t s, const double* guard = nullptr);
 // V_ext from softened-Coulomb atoms (energy.cpp:78-99) / Gaussian wells (C5).
 void launch_external_potential(const SlabGeom& g, const double* h3, const double* atoms,
                                int natoms, int gaussian, double* v, cudaStream_t s);
@@ -103,6 +103,14 @@ bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* 
 // [zz | dd | ss | sy | yy] (dd = ||HW - W Sigma||^2 when Sigma != null; the
 // last three only with WP/ZP). Returns the partials row length, -1 if N is
 // out of range or 2D TMA is unavailable.
+// Line-search rotation W~ = (A + sa Ab) M (M upper) fused with the
+// verification Gram G = w W~^T W~ (written to G) and the density / Dirac xc of
+// W~ (rho, v_xc, 4 pi rho into bvec when non-null, partial rows [<eps,rho> |
+// <V_ext,rho>] x grid in dpart). N <= 48; returns the partials row length or -1.
+int launch_rotate_fused(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab,
+                        double sa, const double* M, double* out, double* ws, double* G, double w,
+                        double occ, int xc, double* rho, double* vxc, double* bvec,
+                        const double* vext, double* dpart, cudaStream_t s);
 int launch_directions(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
                       const double* WP, const double* ZP, const double* Sigma, const double* sig,
                       double* Z, double* partials, cudaStream_t s);

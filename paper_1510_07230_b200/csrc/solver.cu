@@ -159,14 +159,28 @@ bool orthonormalize_dev(Engine& E, const double* A, const double* Ab, double sa,
 // before its energy. orth_outcome() interprets the scalars after the trial's
 // single readback; a failed pass-1 Cholesky (rare) is redone synchronously with
 // the symmetric-eigen fallback.
-void orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, double* out,
-                  double* tmp, bool measure) {
+bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, double* out,
+                  double* tmp, bool measure, DevState* st = nullptr, int hartree = 0, int xc = 0) {
   double* sc = E.scal();
   E.gram(A, Ab, sa, A, Ab, sa, 1, E.dmat[0]);
   launch_matrix_stats(E.N, E.dmat[0], sc + Engine::S_MSTAT, E.s);
   launch_cholesky_inv(E.N, E.dmat[0], E.chol_L, E.dmat[1], sc + Engine::S_CHOL, E.s);
-  E.mix(A, Ab, sa, E.dmat[1], 1.0, nullptr, 0.0, 1, out, nullptr);
-  E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2]);
+  bool fused = false;
+  if (st && E.N <= 48 && tma2d_available()) {
+    // rotation + verification Gram + density/xc of the rotated block in one pass
+    const int nb = launch_rotate_fused(E.N, E.g.ld, E.g.ngl, A, Ab, sa, E.dmat[1], out, E.gram_ws,
+                                       E.dmat[2], E.g.w, E.occ, xc, st->rho, st->v_xc,
+                                       E.density_b_target(hartree), E.v_ext, E.partials, E.s);
+    if (nb >= 0) {
+      if (E.size > 1) E.comm->allreduce_sum(E.dmat[2], (size_t)E.N * E.N, E.s);
+      launch_reduce_rows(E.partials, 2, nb, E.g.w, sc + Engine::S_EXC, E.s);
+      fused = true;
+    }
+  }
+  if (!fused) {
+    E.mix(A, Ab, sa, E.dmat[1], 1.0, nullptr, 0.0, 1, out, nullptr);
+    E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2]);
+  }
   launch_matrix_stats(E.N, E.dmat[2], sc + Engine::S_MSTAT2, E.s);
   const double* guard = sc + Engine::S_QR2;
   launch_qr2_decision(sc + Engine::S_CHOL, sc + Engine::S_MSTAT2, measure ? 1 : 0,
@@ -176,6 +190,12 @@ void orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, doubl
   launch_copy_guarded(out, tmp, (int64_t)E.N * E.g.ld, guard, E.s);
   E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2], guard);
   launch_matrix_stats(E.N, E.dmat[2], sc + Engine::S_MSTAT2, E.s, guard);
+  if (fused) {  // a CholeskyQR2 repair changed the block: its density again
+    launch_density_xc(E.g, E.N, out, E.occ, xc, st->rho, st->v_xc, E.density_b_target(hartree),
+                      E.v_ext, E.partials, E.s, guard);
+    launch_reduce_rows(E.partials, 2, points_nblk(E.g), E.g.w, sc + Engine::S_EXC, E.s, guard);
+  }
+  return fused;
 }
 
 // 0 ok, 1 pass-1 Cholesky rejected (caller redoes the trial with the fallback),
@@ -232,12 +252,12 @@ struct Solver {
 
   // enqueue build_hamiltonian(u) without waiting; finish() after the next fetch
   bool st_fresh = false;
-  SRef enqueue_state(const BRef& u) {
+  SRef enqueue_state(const BRef& u, SRef pre = SRef(), bool density_done = false) {
     st_fresh = false;
     if (!nonlinear && fixed_state) return fixed_state;
-    SRef st = spool.get();
+    SRef st = pre ? pre : spool.get();
     E.poisson_solver = p.poisson_solver;
-    E.build_state(P(u), p.hartree, p.xc, st.get(), have_prev_solve);
+    E.build_state(P(u), p.hartree, p.xc, st.get(), have_prev_solve, density_done);
     if (p.hartree) have_prev_solve = true;
     if (!nonlinear) fixed_state = st;
     st_fresh = true;
@@ -495,8 +515,10 @@ bool Solver::step() {
         wt = pool.get();
         BRef rep = pool.get();
         // one device pipeline per trial, one readback (energy + decisions)
-        orth_enqueue(E, P(w), P(z), -tau, P(wt), P(rep), p.verify_orthonormality != 0);
-        tstate = enqueue_state(wt);
+        SRef pre = nonlinear ? spool.get() : SRef();
+        const bool dens = orth_enqueue(E, P(w), P(z), -tau, P(wt), P(rep),
+                                       p.verify_orthonormality != 0, pre.get(), p.hartree, p.xc);
+        tstate = enqueue_state(wt, pre, dens);
         hwt = pool.get();
         E.apply_h(P(wt), P(hwt), tstate->v_local, !nonlinear);
         E.fetch_all();

@@ -162,7 +162,7 @@ def test_gram_mix(setup, port, native):
     assert rel(e.download(out), m.T @ a) < 1e-13
 
 
-@pytest.mark.parametrize("n_orb", [1, 8, 13, 33, 56, 64])
+@pytest.mark.parametrize("n_orb", [1, 8, 9, 13, 17, 33, 34, 42, 56, 64])
 def test_dmma_small_n(native, n_orb):
     """Register-resident small-N Gram / mix paths (N <= 64), incl. the
     triangular-skip rotation used for U L^{-T}."""
@@ -293,7 +293,7 @@ def test_invalid_arguments(native):
     e.close()
 
 
-@pytest.mark.parametrize("n_orb", [1, 4, 5, 13, 33, 48, 67, 200, 260])
+@pytest.mark.parametrize("n_orb", [1, 4, 5, 9, 13, 17, 33, 34, 48, 67, 200, 260])
 def test_gram_fused_trial(native, n_orb):
     """Gram of W - tau Z formed inside the load (optimizer.cpp:459-463)."""
     spec = configs.ProblemSpec("trial", (10, 9, 11), (5.0, 5.0, 5.0), [], n_orb, hartree=False, xc=False)
