@@ -13,6 +13,8 @@
 // Fusions: the trial point W - tau Z is formed while loading (no trial block
 // is ever written), and mix can add beta*C and emit per-orbital squared norms
 // of its result instead of storing it (grad-norm of HU - U Sigma).
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace po {
@@ -770,7 +772,8 @@ void launch_gram(const SlabGeom& g, int N, const double* A, const double* Ab, do
                  const double* B, const double* Bb, double sb, int sym, double* ws, double* G,
                  cudaStream_t s, const double* guard) {
   if (gram_small_ok(N, sym)) {
-    if (launch_gram_tma(N, g.ld, sym, A, Ab, sa, B, Bb, sb, ws, G, g.w, s, guard)) return;
+    static const bool no_tma = getenv("PO_NO_TMA") != nullptr;  // measurement: LDG paths
+    if (!no_tma && launch_gram_tma(N, g.ld, sym, A, Ab, sa, B, Bb, sb, ws, G, g.w, s, guard)) return;
     switch ((N + 7) / 8) {
 #define PO_GS(F)                                                                  \
   case F:                                                                         \
@@ -813,7 +816,8 @@ int launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, doub
                const double* M, double alpha, const double* C, double beta, int upper,
                double* out, double* norms, cudaStream_t s, const double* guard) {
   if (N <= 64) {  // small-N paths (return their partials row length)
-    const int nb = launch_mix_tma(N, g.ld, g.ngl, A, Ab, sa, M, alpha, C, beta, upper, out, norms,
+    static const bool no_tma = getenv("PO_NO_TMA") != nullptr;
+    const int nb = no_tma ? -1 : launch_mix_tma(N, g.ld, g.ngl, A, Ab, sa, M, alpha, C, beta, upper, out, norms,
                                   s, guard);
     if (nb >= 0) return nb;
     switch ((N + 7) / 8) {

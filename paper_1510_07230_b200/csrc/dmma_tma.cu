@@ -67,8 +67,8 @@ struct Maps {
   CUtensorMap m[4];
 };
 
-bool make_map2(Maps& M, int i, const double* base, int64_t ld, int rows, int npad) {
-  return make_map(&M.m[i], base, ld, rows, npad);
+bool make_map2(Maps& M, int i, const double* base, int64_t ld, int rows, int /*npad*/) {
+  return make_map(&M.m[i], base, ld, rows, rows);  // boxes of exactly N rows
 }
 
 
@@ -82,12 +82,21 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// swizzled address of element (row, point p in the stage) in a source's stage area:
-// [box b = p / 16][row][16 doubles], 16-byte chunk j = (p % 16) / 2 stored at j ^ (row & 7)
-__device__ __forceinline__ int swz(int row, int p, int npad) {
+// swizzled address of element (row, point p in the stage) in a source's stage
+// area: 4 boxes of nb rows x 16 doubles back to back (the area is padded to a
+// multiple of 8 rows, so it starts 1024-B aligned); the hardware XORs the
+// 16-byte chunk index with bits [7:9] of the shared address, i.e. with the
+// area row (b * nb + row) mod 8.
+__device__ __forceinline__ int swz(int row, int p, int nb) {
   const int b = p >> 4, o = p & 15;
-  const int j = (o >> 1) ^ (row & 7);
-  return (b * npad + row) * BOX + j * 2 + (o & 1);
+  const int r = b * nb + row;
+  const int j = (o >> 1) ^ (r & 7);
+  return r * BOX + j * 2 + (o & 1);
+}
+
+// doubles per source per stage (4 boxes of nb rows, padded to 8 rows)
+__host__ __device__ constexpr size_t qs_of(int nb) {
+  return (size_t)((4 * nb + 7) & ~7) * BOX;
 }
 
 struct TCfg {
@@ -107,12 +116,13 @@ size_t tbudget() {
 
 TCfg tcfg(int nsrc, int npad, size_t extra_doubles) {
   TCfg c;
-  c.stage_doubles = (size_t)nsrc * (TKS / BOX) * npad * BOX;
+  c.stage_doubles = (size_t)nsrc * qs_of(npad);
   const size_t avail = tbudget() / 8 - extra_doubles;
   c.nst = (int)(avail / c.stage_doubles);
   if (c.nst > 8) c.nst = 8;
   if (c.nst < 2) c.nst = 2;
-  c.smem = 2048 /*barriers + alignment slack*/ + ((size_t)c.nst * c.stage_doubles + extra_doubles) * 8;
+  // + barriers / alignment slack + 1 KB tail (fragment rows past the last box)
+  c.smem = 3072 + ((size_t)c.nst * c.stage_doubles + extra_doubles) * 8;
   return c;
 }
 
@@ -126,6 +136,7 @@ __device__ __forceinline__ void tma_produce(const CUtensorMap* maps, int nsrc, i
   const int nstage = kend > kbeg ? (int)((kend - kbeg + TKS - 1) / TKS) : 0;
   const uint32_t bytes = (uint32_t)(nsrc * (TKS / BOX) * npad * BOX * 8);
   const int nbox = nsrc * (TKS / BOX);
+  const size_t qs = qs_of(npad);
   for (int st = 0; st < nstage; ++st) {
     const int s = st % nst;
     if (lane == 0) {
@@ -137,8 +148,7 @@ __device__ __forceinline__ void tma_produce(const CUtensorMap* maps, int nsrc, i
     double* sb = stage0 + (size_t)s * sdoubles;
     for (int e = lane; e < nbox; e += 32) {
       const int q = e / (TKS / BOX), b = e % (TKS / BOX);
-      tma_load_2d(sb + ((size_t)q * (TKS / BOX) + b) * npad * BOX, &maps[q], (int)(k0 + b * BOX), 0,
-                  &full[s]);
+      tma_load_2d(sb + q * qs + (size_t)b * npad * BOX, &maps[q], (int)(k0 + b * BOX), 0, &full[s]);
     }
   }
 }
@@ -182,8 +192,9 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
   uint64_t* empty = full + 8;
   double* stage0 = reinterpret_cast<double*>(tsm + 1024);
-  const size_t sdoubles = (size_t)nsrc * (TKS / BOX) * NPAD * BOX;
-  const size_t qstride = (size_t)(TKS / BOX) * NPAD * BOX;
+  const int NB = N;  // box rows: no zero-filled padding rows in the stream
+  const size_t qstride = qs_of(NB);
+  const size_t sdoubles = (size_t)nsrc * qstride;
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
@@ -201,7 +212,7 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
   double* rred = red + (size_t)TSC * NP * 64;
   if (warp >= TSC) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-    produce(maps, nsrc, NPAD, kbeg, kend, nst, sdoubles, stage0, full, empty);
+    produce(maps, nsrc, NB, kbeg, kend, nst, sdoubles, stage0, full, empty);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
     double acc[NP > 0 ? NP : 1][2];
@@ -221,7 +232,7 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
     auto row8 = [&](const double* sbuf, int row, int q0, int q1, double sc, double2 (&v)[4]) {
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        const int off = swz(row, c + 2 * m, NPAD);
+        const int off = swz(row, c + 2 * m, NB);
         v[m] = *reinterpret_cast<const double2*>(sbuf + q0 * qstride + off);
         if (q1 >= 0) {
           const double2 z = *reinterpret_cast<const double2*>(sbuf + q1 * qstride + off);
@@ -266,7 +277,7 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
     auto frags = [&](const double* sbuf, double2 (&a)[FA], double2 (&b)[FB]) {
 #pragma unroll
       for (int f = 0; f < FD; ++f) {
-        const int off = swz(8 * f + gq, c + 2 * t4, NPAD);  // 16-B aligned pair of points
+        const int off = swz(8 * f + gq, c + 2 * t4, NB);  // 16-B aligned pair of points
         a[f] = *reinterpret_cast<const double2*>(sbuf + off);
         if (qa_b >= 0) {
           const double2 z = *reinterpret_cast<const double2*>(sbuf + qa_b * qstride + off);
@@ -419,7 +430,7 @@ bool launch_gram_tma_f(int N, int64_t ld, int sym, const double* A, const double
   const int fd = F;
   const int np = sym ? fd * (fd + 1) / 2 : fd * fd;
   const size_t red = (size_t)TSC * np * 64 + (size_t)TSC * 2 * 2 * 2 * 32;
-  TCfg cfg = tcfg(nsrc, NPAD, 0);
+  TCfg cfg = tcfg(nsrc, N, 0);
   if (cfg.smem < 2048 + red * 8) cfg.smem = 2048 + red * 8;
   const int64_t kblocks = (ld + TKS - 1) / TKS;
   int nsplit = nsm();
@@ -463,8 +474,9 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
   uint64_t* empty = full + 8;
   double* stage0 = reinterpret_cast<double*>(tsm + 1024);
-  const size_t sdoubles = (size_t)nsrc * (TKS / BOX) * NPAD * BOX;
-  const size_t qstride = (size_t)(TKS / BOX) * NPAD * BOX;
+  const int NB = N;  // box rows: no zero-filled padding rows in the stream
+  const size_t qstride = qs_of(NB);
+  const size_t sdoubles = (size_t)nsrc * qstride;
   double* Ms = stage0 + (size_t)nst * sdoubles;  // [NPAD][NPAD]
   double* nred = Ms + NPAD * NPAD;               // [8][NPAD]
   for (int e = threadIdx.x; e < NPAD * NPAD; e += TTH) {
@@ -486,7 +498,7 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
   const bool has_ab = nsrc - (qc >= 0 ? 1 : 0) == 2;
   if (warp >= TSC) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-    produce(maps, nsrc, NPAD, pbeg, pend, nst, sdoubles, stage0, full, empty);
+    produce(maps, nsrc, NB, pbeg, pend, nst, sdoubles, stage0, full, empty);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
     double nrm[F][2];
@@ -517,9 +529,10 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
         double av[2 * F];
 #pragma unroll
         for (int ks = 0; ks < 2 * F; ++ks) {
-          const int off = swz(4 * ks + t4, c + gq, NPAD);
+          const int off = swz(4 * ks + t4, c + gq, NB);
           av[ks] = sbuf[off];
           if (has_ab) av[ks] += sa * sbuf[qstride + off];
+          if (4 * ks + t4 >= N) av[ks] = 0.0;  // rows past N alias the next box
         }
 #pragma unroll
         for (int ks = 0; ks < 2 * F; ++ks) {
@@ -533,9 +546,10 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
       } else {
         for (int ks = 0; ks < ksteps; ++ks) {
           const int krow = 4 * ks + t4;
-          const int off = swz(krow, c + gq, NPAD);
+          const int off = swz(krow, c + gq, NB);
           double av = sbuf[off];
           if (has_ab) av += sa * sbuf[qstride + off];
+          if (krow >= N) av = 0.0;
 #pragma unroll
           for (int fi = 0; fi < F; ++fi) dmma_8x8x4(acc[fi], av, Ms[krow * NPAD + 8 * fi + gq]);
         }
@@ -548,7 +562,7 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
           const int i = 8 * fi + 2 * t4 + j;
           if (p < ngl && i < N) {
             double v = alpha * acc[fi][j];
-            if (qc >= 0) v += beta * sbuf[qc * qstride + swz(i, c + gq, NPAD)];
+            if (qc >= 0) v += beta * sbuf[qc * qstride + swz(i, c + gq, NB)];
             if (out) out[(int64_t)i * ld + p] = v;
             nrm[fi][j] += v * v;
           }
@@ -604,7 +618,8 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
   uint64_t* empty = full + 8;
   double* stage0 = reinterpret_cast<double*>(tsm + 1024);
-  const size_t qstride = (size_t)(TKS / BOX) * NPAD * BOX;
+  const int NB = N;  // box rows: no zero-filled padding rows in the stream
+  const size_t qstride = qs_of(NB);
   const size_t sdoubles = (size_t)nsrc * qstride;
   double* Ms = stage0 + (size_t)nst * sdoubles;  // [NPAD][NPAD]
   for (int e = threadIdx.x; e < NPAD * NPAD; e += TTH) {
@@ -631,7 +646,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
   double* ered = rred + (size_t)TSC * RS;
   if (warp >= TSC) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-    produce(maps, nsrc, NPAD, pbeg, pend, nst, sdoubles, stage0, full, empty);
+    produce(maps, nsrc, NB, pbeg, pend, nst, sdoubles, stage0, full, empty);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
     double gacc[NP > 0 ? NP : 1][2];
@@ -664,9 +679,10 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
         double av[2 * F];
 #pragma unroll
         for (int ks = 0; ks < 2 * F; ++ks) {
-          const int off = swz(4 * ks + t4, c + gq, NPAD);
+          const int off = swz(4 * ks + t4, c + gq, NB);
           av[ks] = sbuf[off];
           if (nsrc == 2) av[ks] += sa * sbuf[qstride + off];
+          if (4 * ks + t4 >= N) av[ks] = 0.0;  // rows past N alias the next box
         }
 #pragma unroll
         for (int ks = 0; ks < 2 * F; ++ks) {
@@ -688,7 +704,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
           if (i < N) {
             const double v = acc[fi][j];
             if (p < ngl) out[(int64_t)i * ld + p] = v;
-            sbuf[swz(i, c + gq, NPAD)] = v;
+            sbuf[swz(i, c + gq, NB)] = v;
             dsum += v * v;
           }
         }
@@ -716,7 +732,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
           double2 bv[4];
 #pragma unroll
           for (int m = 0; m < 4; ++m)
-            bv[m] = *reinterpret_cast<const double2*>(sbuf + swz(rr, c + 2 * m, NPAD));
+            bv[m] = *reinterpret_cast<const double2*>(sbuf + swz(rr, c + 2 * m, NB));
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int i = lane + 32 * h;
@@ -724,7 +740,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
             double t = racc[h][r];
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
-              const double2 av = *reinterpret_cast<const double2*>(sbuf + swz(i, c + 2 * m, NPAD));
+              const double2 av = *reinterpret_cast<const double2*>(sbuf + swz(i, c + 2 * m, NB));
               t = fma(av.y, bv[m].y, fma(av.x, bv[m].x, t));
             }
             racc[h][r] = t;
@@ -734,7 +750,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
       double2 a[FD > 0 ? FD : 1];
 #pragma unroll
       for (int f = 0; f < FD; ++f)
-        a[f] = *reinterpret_cast<const double2*>(sbuf + swz(8 * f + gq, c + 2 * t4, NPAD));
+        a[f] = *reinterpret_cast<const double2*>(sbuf + swz(8 * f + gq, c + 2 * t4, NB));
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       int q = 0;
@@ -815,7 +831,7 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
   const int fd = R ? F - 1 : F;
   const size_t red = (size_t)TSC * (fd * (fd + 1) / 2) * 64 + (size_t)TSC * 2 * 2 * 32 + 2 * TSC;
   const size_t extra = (size_t)NPAD * NPAD;
-  TCfg cfg = tcfg(nsrc, NPAD, extra);
+  TCfg cfg = tcfg(nsrc, N, extra);
   if (cfg.smem < 2048 + red * 8) cfg.smem = 2048 + red * 8;
   const int64_t kb = (ld + TKS - 1) / TKS;
   int nblk = nsm();
@@ -856,8 +872,9 @@ __global__ void __launch_bounds__(TTH, 1) directions_tma_kernel(
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
   uint64_t* empty = full + 8;
   double* stage0 = reinterpret_cast<double*>(tsm + 1024);
-  constexpr size_t qstride = (size_t)(TKS / BOX) * NPAD * BOX;
-  constexpr size_t sdoubles = NSRC * qstride;
+  const int NB = N;  // box rows: no zero-filled padding rows in the stream
+  const size_t qstride = qs_of(NB);
+  const size_t sdoubles = NSRC * qstride;
   double* Ms = stage0 + (size_t)nst * sdoubles;  // [NPAD][NPAD] (DD)
   double* msig = Ms + NPAD * NPAD;               // [NPAD]: -sigma_ii
   double* nred = msig + NPAD;                    // [8][NQ][NPAD]
@@ -880,7 +897,7 @@ __global__ void __launch_bounds__(TTH, 1) directions_tma_kernel(
   const int gq = lane >> 2, t4 = lane & 3;
   if (warp >= TSC) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-    produce(maps, NSRC, NPAD, pbeg, pend, nst, sdoubles, stage0, full, empty);
+    produce(maps, NSRC, NB, pbeg, pend, nst, sdoubles, stage0, full, empty);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
     double nrm[NQ][F][2];
@@ -902,7 +919,7 @@ __global__ void __launch_bounds__(TTH, 1) directions_tma_kernel(
       if constexpr (DD) {
         for (int ks = 0; ks < ksteps; ++ks) {
           const int krow = 4 * ks + t4;
-          const double av = sbuf[swz(krow, c + gq, NPAD)];
+          const double av = krow < N ? sbuf[swz(krow, c + gq, NB)] : 0.0;
 #pragma unroll
           for (int fi = 0; fi < F; ++fi) dmma_8x8x4(acc[fi], av, Ms[krow * NPAD + 8 * fi + gq]);
         }
@@ -913,7 +930,7 @@ __global__ void __launch_bounds__(TTH, 1) directions_tma_kernel(
         for (int j = 0; j < 2; ++j) {
           const int i = 8 * fi + 2 * t4 + j;
           if (p < ngl && i < N) {
-            const int off = swz(i, c + gq, NPAD);
+            const int off = swz(i, c + gq, NB);
             const double wv = sbuf[off], hv = sbuf[qstride + off];
             if constexpr (DD) {
               double d = -acc[fi][j];
@@ -964,7 +981,7 @@ int launch_directions_fdh(const Maps& maps, int N, int64_t ld, int64_t ngl, cons
   constexpr int NPAD = 8 * F;
   constexpr int NQ = HIST ? 5 : 2;
   const size_t extra = (size_t)NPAD * NPAD + NPAD + (size_t)TSC * NQ * NPAD;
-  const TCfg cfg = tcfg(HIST ? 4 : 2, NPAD, extra);
+  const TCfg cfg = tcfg(HIST ? 4 : 2, N, extra);
   const int64_t kb = (ld + TKS - 1) / TKS;
   int nblk = nsm();
   if (nblk > kb) nblk = (int)kb;
@@ -1010,7 +1027,7 @@ int launch_mix_tma_f(int N, int64_t ld, int64_t ngl, const double* A, const doub
     if (!make_map2(maps, nsrc++, C, ld, N, NPAD)) return -1;
   }
   const size_t extra = (size_t)NPAD * NPAD + (size_t)TSC * NPAD;
-  const TCfg cfg = tcfg(nsrc, NPAD, extra);
+  const TCfg cfg = tcfg(nsrc, N, extra);
   const int64_t kb = (ld + TKS - 1) / TKS;
   int nblk = nsm();
   if (nblk > kb) nblk = (int)kb;
