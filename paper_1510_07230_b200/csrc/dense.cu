@@ -87,6 +87,112 @@ __global__ void __launch_bounds__(DT) cholesky_inv_kernel(int N, const double* _
   }
 }
 
+// Shared-memory variant for N <= 160 (the whole matrix fits one CTA's shared
+// memory, row stride N + 1 against bank conflicts): the same left-looking
+// recurrence as cholesky_inv_kernel with one thread per row of the column
+// update, then X = L^{-1} by one thread per column (forward substitution down
+// the column, no barriers). X's strictly-lower part is kept transposed in the
+// upper triangle (X(i, c) at A[c][i]) and its diagonal in xd, so one array
+// holds L and L^{-1}. Sums run in the same ascending-k order as the global
+// version.
+constexpr int CHOL_SMEM_MAX = 160;
+constexpr int CHT = 256;
+
+__global__ void __launch_bounds__(CHT) cholesky_inv_smem_kernel(int N, const double* __restrict__ G,
+                                                                double* __restrict__ M,
+                                                                double* __restrict__ stats,
+                                                                const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;
+  extern __shared__ double csm[];
+  const int ls = N + 1;
+  double* A = csm;           // [N][N + 1]
+  double* xd = csm + N * ls;  // [N]: 1 / L(i, i)
+  __shared__ int fail;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int e = t; e < N * N; e += CHT) A[(e / N) * ls + e % N] = G[e];
+  if (t == 0) fail = 0;
+  __syncthreads();
+  for (int j = 0; j < N; ++j) {
+    if (warp == 0) {  // d = L(j,j) - sum_k<j L(j,k)^2
+      double sq = 0.0;
+      for (int k = lane; k < j; k += 32) sq += A[j * ls + k] * A[j * ls + k];
+      sq = warp_sum(sq);
+      if (lane == 0) {
+        const double d = A[j * ls + j] - sq;
+        if (!(d > 0.0)) fail = 1;
+        else A[j * ls + j] = sqrt(d);
+      }
+    }
+    __syncthreads();
+    if (fail) break;
+    const double ljj = A[j * ls + j];
+    for (int i = j + 1 + t; i < N; i += CHT) {
+      // four interleaved partial sums: the loads pipeline instead of one
+      // dependent FMA chain of length j
+      double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+      const double* ai = A + i * ls;
+      const double* aj = A + j * ls;
+      int k = 0;
+      for (; k + 4 <= j; k += 4) {
+        p0 += ai[k] * aj[k];
+        p1 += ai[k + 1] * aj[k + 1];
+        p2 += ai[k + 2] * aj[k + 2];
+        p3 += ai[k + 3] * aj[k + 3];
+      }
+      for (; k < j; ++k) p0 += ai[k] * aj[k];
+      A[i * ls + j] = (A[i * ls + j] - ((p0 + p1) + (p2 + p3))) / ljj;
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (t == 0) {
+      stats[0] = 0.0;
+      stats[1] = 0.0;
+      stats[2] = INFINITY;
+      stats[3] = 0.0;
+    }
+    return;
+  }
+  if (t == 0) {
+    double pmin = A[0], pmax = A[0];
+    for (int i = 1; i < N; ++i) {
+      const double v = A[i * ls + i];
+      pmin = v < pmin ? v : pmin;
+      pmax = v > pmax ? v : pmax;
+    }
+    const bool ok = (pmin > 0.0) && isfinite(pmax) && !(pmin * pmin < 1e-10 * pmax * pmax);
+    stats[0] = pmin;
+    stats[1] = pmax;
+    stats[2] = (pmax / pmin) * (pmax / pmin);
+    stats[3] = ok ? 1.0 : 0.0;
+  }
+  for (int i = t; i < N; i += CHT) xd[i] = 1.0 / A[i * ls + i];
+  __syncthreads();
+  // column c of X: X(c,c) = 1/L(c,c); X(i,c) = -(sum_{k=c}^{i-1} L(i,k) X(k,c)) / L(i,i)
+  for (int c = t; c < N; c += CHT) {
+    const double* xc = A + c * ls;  // X(k, c) for k > c lives at A[c][k]
+    for (int i = c + 1; i < N; ++i) {
+      const double* li = A + i * ls;
+      double p0 = li[c] * xd[c], p1 = 0.0, p2 = 0.0, p3 = 0.0;
+      int k = c + 1;
+      for (; k + 4 <= i; k += 4) {
+        p0 += li[k] * xc[k];
+        p1 += li[k + 1] * xc[k + 1];
+        p2 += li[k + 2] * xc[k + 2];
+        p3 += li[k + 3] * xc[k + 3];
+      }
+      for (; k < i; ++k) p0 += li[k] * xc[k];
+      A[c * ls + i] = -((p0 + p1) + (p2 + p3)) / li[i];
+    }
+  }
+  __syncthreads();
+  // M(k, i) = X(i, k): row k of M is row k of the upper triangle, diagonal from xd
+  for (int e = t; e < N * N; e += CHT) {
+    const int k = e / N, i = e % N;
+    M[e] = i > k ? A[k * ls + i] : (i == k ? xd[k] : 0.0);
+  }
+}
+
 // Parallel cyclic Jacobi (round-robin pairing) on S = 1/2 (A + A^T).
 // work: N*N (S) ; evecs N*N ; evals N.
 __global__ void __launch_bounds__(DT) syev_kernel(int N, const double* __restrict__ A,
@@ -324,6 +430,17 @@ void launch_copy_guarded(double* dst, const double* src, int64_t n, const double
 void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, double* stats,
                          cudaStream_t s, const double* guard) {
   ::po::count_launch();
+  if (N <= CHOL_SMEM_MAX) {
+    const size_t shm = sizeof(double) * ((size_t)N * (N + 1) + N);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(cholesky_inv_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(double) * (CHOL_SMEM_MAX * (CHOL_SMEM_MAX + 1) + CHOL_SMEM_MAX)));
+      attr = true;
+    }
+    cholesky_inv_smem_kernel<<<1, CHT, shm, s>>>(N, G, M, stats, guard);
+    return;
+  }
   cholesky_inv_kernel<<<1, DT, 0, s>>>(N, G, Lscratch, M, stats, guard);
 }
 

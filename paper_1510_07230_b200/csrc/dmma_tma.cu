@@ -1245,18 +1245,22 @@ struct BigPlan {
 };
 
 // splits so that tiles x splits fills whole waves of one CTA per SM
-int big_tile(int N) {
+// Tile side. Measured at N = 128 (C3, 128^3): 64-wide tiles win only for the
+// one-source symmetric Gram (2.04 vs 2.26 ms); with two streamed sources
+// (Sigma, the trial Gram) the 64-tile CTAs are bound by the 2D-TMA row rate
+// and 128-wide tiles win (2.26 vs 2.76 ms, 2.40 vs 2.91 ms).
+int big_tile(int N, int sym, bool two_src) {
   static int forced = -1;
   if (forced < 0) {
     const char* e = getenv("PO_GRAM_TILE");  // measurement override: 64 or 128
     forced = e ? atoi(e) : 0;
   }
   if (forced == 64 || forced == 128) return forced;
-  return N <= 192 ? 64 : 128;
+  if (N > 192) return 128;
+  return (sym && !two_src) ? 64 : 128;
 }
 
-BigPlan big_plan(int64_t ld, int N, int sym, int sms) {
-  const int GT_T = big_tile(N);
+BigPlan big_plan(int64_t ld, int N, int sym, int sms, int GT_T) {
   BigPlan p;
   p.mt = (N + GT_T - 1) / GT_T;
   p.ntiles = sym ? p.mt * (p.mt + 1) / 2 : p.mt * p.mt;
@@ -1285,18 +1289,20 @@ BigPlan big_plan(int64_t ld, int N, int sym, int sms) {
 
 size_t gram_big_workspace_doubles(int64_t ld, int N) {
   if (N <= 48) return 0;
-  const int GT_T = big_tile(N);
-  BigPlan p = big_plan(ld, N, 0, nsm());
-  BigPlan q = big_plan(ld, N, 1, nsm());
-  const size_t a = (size_t)p.nsplit * p.ntiles * GT_T * GT_T;
-  const size_t b = (size_t)q.nsplit * q.ntiles * GT_T * GT_T;
-  return a > b ? a : b;
+  size_t w = 0;
+  for (int t : {64, 128})
+    for (int sym : {0, 1}) {
+      const BigPlan p = big_plan(ld, N, sym, nsm(), t);
+      const size_t a = (size_t)p.nsplit * p.ntiles * t * t;
+      if (a > w) w = a;
+    }
+  return w;
 }
 
 bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                      const double* B, const double* Bb, double sb, double* ws, size_t ws_doubles,
                      double* G, double w, cudaStream_t s, const double* guard) {
-  const int GT_T = big_tile(N);
+  const int GT_T = big_tile(N, sym, Ab != nullptr || !sym);
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   int nsrc = 0, qa_b = -1, qb = 0, qb_b = -1;
@@ -1324,7 +1330,7 @@ bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* 
     }
     sb = sa;
   }
-  const BigPlan p = big_plan(ld, N, sym, nsm());
+  const BigPlan p = big_plan(ld, N, sym, nsm(), GT_T);
   if ((size_t)p.nsplit * p.ntiles * GT_T * GT_T > ws_doubles) return false;
   const size_t sdoubles = (size_t)nsrc * GT_T * BOX;
   int nst = (int)((200 * 1024 / 8) / sdoubles);

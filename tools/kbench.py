@@ -14,6 +14,14 @@ from paper_1510_07230_b200 import configs, native  # noqa: E402
 
 
 def timeit(e, fn, reps=20):
+    try:
+        return _timeit(e, fn, reps)
+    except Exception as ex:  # op unavailable at this N
+        print("  (skipped:", str(ex)[:60], ")")
+        return float("nan")
+
+
+def _timeit(e, fn, reps=20):
     st = torch.cuda.ExternalStream(e.stream)
     for _ in range(3):
         fn()
