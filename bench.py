@@ -47,29 +47,58 @@ def env_int(k, d):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region: NVML every
+    ~2 ms (the C2 timed region is tens of ms), nvidia-smi as a fallback."""
 
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
         self.device = device
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, [reasons])
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        except Exception:
+            self._nv = None
+
+    def _sample_nvml(self):
+        nv = self._nv
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        reasons = [name for name, attr in self.REASONS if bits & getattr(nv, attr, 0)]
+        self.samples.append((float(sm), float(mx), reasons))
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        if out:
+            f = [x.strip() for x in out.split(",")]
+            reasons = [self.REASONS[k][0] for k in range(4) if len(f) > 3 + k and f[3 + k].lower() == "active"]
+            try:
+                self.samples.append((float(f[0]), float(f[1]), reasons))
+            except ValueError:
+                pass
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self._sample_nvml() if self._nv else self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.002 if self._nv else 0.2)
 
     def __enter__(self):
         self._t.start()
@@ -78,17 +107,20 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        if not self.samples:  # region shorter than one sample: take one right after
+            try:
+                self._sample_nvml() if self._nv else self._sample_smi()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
-                          if len(s) > 3 + k and s[3 + k].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock query unavailable"]}
+        sm = [s[0] for s in self.samples]
+        mx = [s[1] for s in self.samples]
+        reasons = sorted({r for s in self.samples for r in s[2]})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml" if self._nv else "nvidia-smi"}
 
 
 def measured_peaks():
@@ -306,9 +338,17 @@ def ours(args, spec):
     e.set_poisson_solver(args.poisson)
     p_ms = time_kernel(torch, native, e, "poisson", 5)
     st.close()
-    roofline = {"kernel": "hamiltonian_kernel (batched H u + fused sigma/kinetic/external)",
+    traffic = None
+    if spec.name == "C2":  # dram read+write per launch from the committed ncu --set full capture
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic_C2.json")) as f:
+                traffic = json.load(f)["hamiltonian_traffic_bytes_per_launch"]
+        except Exception:
+            traffic = None
+    roofline = {"kernel": "hamiltonian4_kernel (batched H u + fused sigma/kinetic/external)",
                 "bound": "hbm", "achieved": h_bytes / (h_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
-                "frac": h_bytes / (h_ms / 1e3) / 1e9 / hbm, "traffic": None,
+                "frac": h_bytes / (h_ms / 1e3) / 1e9 / hbm, "traffic": traffic,
+                "traffic_source": "profiles/traffic_C2.json (ncu dram__bytes_read+write, 1 launch)",
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
                 "algorithmic_bytes_per_launch": h_bytes, "launch_ms": h_ms}
     iter_ms = ms / steps
@@ -353,7 +393,7 @@ def ours(args, spec):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3"])

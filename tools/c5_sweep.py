@@ -52,7 +52,7 @@ for n in sizes:
         spec = configs.config5(n, N)
         ng = spec.num_points
         block = 8.0 * N * ng
-        need = 3 * block + 64 * ng * 8 + 16 * N * N * 8
+        need = 2 * block + 64 * ng * 8 + 16 * N * N * 8 + (1 << 30)
         row = {"grid": n, "N": N, "block_GB": block / 1e9}
         if need > 0.92 * free:
             row["status"] = f"does not fit one B200 ({need / 1e9:.0f} GB needed, {free / 1e9:.0f} GB free)"
