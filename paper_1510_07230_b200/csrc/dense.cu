@@ -411,7 +411,31 @@ __global__ void copy_guarded_kernel(double* __restrict__ dst, const double* __re
     dst[e] = src[e];
 }
 
+__global__ void trial_gram_kernel(int N, const double* __restrict__ gww,
+                                  const double* __restrict__ S, const double* __restrict__ ghh,
+                                  double tau, double* __restrict__ G0) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)N * N) return;
+  const int i = (int)(e / N), j = (int)(e % N);
+  if (j < i) return;  // (i, j) with i <= j computes both mirror entries
+  const double si = S[(int64_t)i * N + i], sj = S[(int64_t)j * N + j];
+  const double sij = S[(int64_t)i * N + j], sji = S[(int64_t)j * N + i];
+  const double g = gww[(int64_t)i * N + j];
+  const double wz = (sji - sj * g) + (sij - si * g);  // (W^T Z + Z^T W)_ij
+  const double zz = ((ghh[(int64_t)i * N + j] - sj * sij) - si * sji) + (si * sj) * g;
+  const double v = (g - tau * wz) + (tau * tau) * zz;
+  G0[(int64_t)i * N + j] = v;
+  G0[(int64_t)j * N + i] = v;
+}
+
 }  // namespace
+
+void launch_trial_gram(int N, const double* gww, const double* sigma, const double* ghh,
+                       double tau, double* G0, cudaStream_t s) {
+  const int64_t total = (int64_t)N * N;
+  ::po::count_launch();
+  trial_gram_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(N, gww, sigma, ghh, tau, G0);
+}
 
 void launch_qr2_decision(const double* chol_stats, const double* gram2_stats, int measure,
                          double* out, cudaStream_t s) {

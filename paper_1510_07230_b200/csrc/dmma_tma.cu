@@ -168,12 +168,11 @@ struct TPairs {
   static constexpr int NP = SYM ? F * (F + 1) / 2 : F * F;
 };
 
-// F = ceil(N/8) fragments lay out the stage (NPAD = 8F rows per box); with R > 0
-// (N = 8(F-1) + R, R <= 2) only the first F-1 fragments go through DMMA and the
-// R trailing orbitals are contracted with plain FP64 FMAs — on B200 FP64 FMA
-// and DMMA have the same peak, so a fragment row that is 7/8 zero padding
-// (N = 33) costs ~10 DMMAs per 8 points for one useful orbital otherwise.
-template <int F, bool SYM, int R>
+// G = w (A + sa Ab)^T (B + sb Bb) over the CTA's point range; with DUAL
+// (non-symmetric call only) the same pass also accumulates A^T A, so
+// Sigma = (HW)^T W and G_HH = (HW)^T (HW) come from one read of HW and W.
+// F = ceil(N/8) fragments; NPAD = 8F.
+template <int F, bool SYM, bool DUAL>
 __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant__ Maps maps,
                                                           int N, int nsrc, int qa_b, int qb,
                                                           int qb_b, int64_t ld, int64_t kchunk,
@@ -182,10 +181,9 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
                                                           const double* __restrict__ guard,
                                                           int probe) {
   if (guard && *guard == 0.0) return;
-  constexpr int FD = R > 0 ? F - 1 : F;  // DMMA fragments
-  constexpr int NP = TPairs<FD, SYM>::NP;
+  constexpr int NP = TPairs<F, SYM>::NP;
+  constexpr int NP2 = DUAL ? F * (F + 1) / 2 : 0;
   constexpr int NPAD = 8 * F;
-  constexpr int NR = SYM ? 1 : 2;  // remainder products per (lane orbital, remainder orbital)
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   // SWIZZLE_128B boxes need 1024-byte aligned destinations
   unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
@@ -207,76 +205,34 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
   const int64_t kend = min(kbeg + kchunk, ld);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, t4 = lane & 3;
-  double* red = stage0;  // after the loop: [8 warps][NP * 64] then [8 warps][2][R][NR][32]
-  constexpr int RS = 2 * (R > 0 ? R : 1) * NR * 32;
-  double* rred = red + (size_t)TSC * NP * 64;
+  double* red = stage0;  // after the loop: [8 warps][(NP + NP2) * 64]
   if (warp >= TSC) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     produce(maps, nsrc, NB, kbeg, kend, nst, sdoubles, stage0, full, empty);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
-    double acc[NP > 0 ? NP : 1][2];
+    double acc[NP][2], acc2[NP2 > 0 ? NP2 : 1][2];
 #pragma unroll
     for (int q = 0; q < NP; ++q) acc[q][0] = acc[q][1] = 0.0;
-    // remainder accumulators: lane orbital i in {lane, lane + 32}, remainder orbital r
-    double racc[2][R > 0 ? R : 1][NR];
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int r = 0; r < (R > 0 ? R : 1); ++r)
-#pragma unroll
-        for (int k = 0; k < NR; ++k) racc[h][r][k] = 0.0;
+    for (int q = 0; q < NP2; ++q) acc2[q][0] = acc2[q][1] = 0.0;
     const int nstage = kend > kbeg ? (int)((kend - kbeg + TKS - 1) / TKS) : 0;
     const int c = warp * 8;  // this warp's 8-point chunk of every stage
-    // a row's 8 points of the chunk as 4 double2 (A side or B side, trial-combined)
-    auto row8 = [&](const double* sbuf, int row, int q0, int q1, double sc, double2 (&v)[4]) {
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int off = swz(row, c + 2 * m, NB);
-        v[m] = *reinterpret_cast<const double2*>(sbuf + q0 * qstride + off);
-        if (q1 >= 0) {
-          const double2 z = *reinterpret_cast<const double2*>(sbuf + q1 * qstride + off);
-          v[m].x += sc * z.x;
-          v[m].y += sc * z.y;
-        }
+    // (measured: prefetching the next stage's fragments before this stage's
+    // DMMAs made the kernel slower — it is bound by the TMA stream, not by
+    // shared-memory latency — so load, release, then multiply)
+    for (int st = 0; st < nstage; ++st) {
+      const int s = st % nst;
+      mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+      const double* sbuf = stage0 + (size_t)s * sdoubles;
+      if (probe) {  // measurement hook: stream the ring without consuming it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        continue;
       }
-    };
-    auto remainder = [&](const double* sbuf) {
-      const int qbb = SYM ? 0 : qb, qbbb = SYM ? qa_b : qb_b;
-      const double sbb = SYM ? sa : sb;
+      double2 a[F], b[SYM ? 1 : F];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int rr = 8 * FD + r;
-        double2 brv[4], arv[4];
-        row8(sbuf, rr, qbb, qbbb, sbb, brv);                    // B_r (broadcast)
-        if constexpr (!SYM) row8(sbuf, rr, 0, qa_b, sa, arv);  // A_r
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int i = lane + 32 * h;
-          if (i >= N || (SYM && i > rr)) continue;
-          double2 av[4];
-          row8(sbuf, i, 0, qa_b, sa, av);
-          double t = racc[h][r][0];
-#pragma unroll
-          for (int m = 0; m < 4; ++m) t = fma(av[m].y, brv[m].y, fma(av[m].x, brv[m].x, t));
-          racc[h][r][0] = t;
-          if constexpr (!SYM) {
-            if (i < 8 * FD) {  // B_i A_r for i outside the remainder (else counted above)
-              double2 bv[4];
-              row8(sbuf, i, qb, qb_b, sb, bv);
-              double u = racc[h][r][NR - 1];
-#pragma unroll
-              for (int m = 0; m < 4; ++m) u = fma(arv[m].y, bv[m].y, fma(arv[m].x, bv[m].x, u));
-              racc[h][r][NR - 1] = u;
-            }
-          }
-        }
-      }
-    };
-    constexpr int FA = FD > 0 ? FD : 1, FB = SYM ? 1 : FA;
-    auto frags = [&](const double* sbuf, double2 (&a)[FA], double2 (&b)[FB]) {
-#pragma unroll
-      for (int f = 0; f < FD; ++f) {
+      for (int f = 0; f < F; ++f) {
         const int off = swz(8 * f + gq, c + 2 * t4, NB);  // 16-B aligned pair of points
         a[f] = *reinterpret_cast<const double2*>(sbuf + off);
         if (qa_b >= 0) {
@@ -293,33 +249,27 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
           }
         }
       }
-    };
-    // (measured: prefetching the next stage's fragments before this stage's
-    // DMMAs made the kernel slower — it is bound by the TMA stream, not by
-    // shared-memory latency — so load, release, then multiply)
-    for (int st = 0; st < nstage; ++st) {
-      const int s = st % nst;
-      mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
-      const double* sbuf = stage0 + (size_t)s * sdoubles;
-      if (probe) {  // measurement hook: stream the ring without consuming it
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        continue;
-      }
-      if constexpr (R > 0) remainder(sbuf);
-      double2 a[FA], b[FB];
-      frags(sbuf, a, b);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);  // fragments are in registers: release early
       int q = 0;
 #pragma unroll
-      for (int fm = 0; fm < FD; ++fm)
+      for (int fm = 0; fm < F; ++fm)
 #pragma unroll
-        for (int fn = SYM ? fm : 0; fn < FD; ++fn, ++q) {
+        for (int fn = SYM ? fm : 0; fn < F; ++fn, ++q) {
           const double2 bv = SYM ? a[fn] : b[SYM ? 0 : fn];
           dmma_8x8x4(acc[q], a[fm].x, bv.x);
           dmma_8x8x4(acc[q], a[fm].y, bv.y);
         }
+      if constexpr (DUAL) {
+        int q2 = 0;
+#pragma unroll
+        for (int fm = 0; fm < F; ++fm)
+#pragma unroll
+          for (int fn = fm; fn < F; ++fn, ++q2) {
+            dmma_8x8x4(acc2[q2], a[fm].x, a[fn].x);
+            dmma_8x8x4(acc2[q2], a[fm].y, a[fn].y);
+          }
+      }
     }
     // all consumers are past the ring: reuse it for the CTA reduction (named
     // barrier over the consumer warps only; the producer warpgroup runs with
@@ -327,50 +277,33 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
     asm volatile("bar.sync 1, %0;\n" ::"n"(TSC * 32) : "memory");
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-      red[(warp * NP + q) * 64 + lane * 2] = acc[q][0];
-      red[(warp * NP + q) * 64 + lane * 2 + 1] = acc[q][1];
+      red[(warp * (NP + NP2) + q) * 64 + lane * 2] = acc[q][0];
+      red[(warp * (NP + NP2) + q) * 64 + lane * 2 + 1] = acc[q][1];
     }
-    if constexpr (R > 0) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-#pragma unroll
-          for (int k = 0; k < NR; ++k) rred[warp * RS + ((h * R + r) * NR + k) * 32 + lane] = racc[h][r][k];
+    for (int q = 0; q < NP2; ++q) {
+      red[(warp * (NP + NP2) + NP + q) * 64 + lane * 2] = acc2[q][0];
+      red[(warp * (NP + NP2) + NP + q) * 64 + lane * 2 + 1] = acc2[q][1];
     }
   }
   __syncthreads();
-  double* out = ws + (int64_t)blockIdx.x * NPAD * NPAD;
-  for (int e = threadIdx.x; e < NP * 64; e += TTH) {
+  for (int e = threadIdx.x; e < (NP + NP2) * 64; e += TTH) {
     double sum = 0.0;
 #pragma unroll
-    for (int w = 0; w < TSC; ++w) sum += red[(w * NP) * 64 + e];
-    const int q = e / 64, l = (e % 64) / 2, j = e % 2;
+    for (int w = 0; w < TSC; ++w) sum += red[(w * (NP + NP2)) * 64 + e];
+    const int qq = e / 64, l = (e % 64) / 2, j = e % 2;
+    const bool second = qq >= NP;
+    const int q = second ? qq - NP : qq;
+    const bool sym = second || SYM;
     int fm = 0, fn = 0, cq = 0;
-    for (int m = 0; m < FD; ++m)
-      for (int n = SYM ? m : 0; n < FD; ++n, ++cq)
+    for (int m = 0; m < F; ++m)
+      for (int n = sym ? m : 0; n < F; ++n, ++cq)
         if (cq == q) {
           fm = m;
           fn = n;
         }
+    double* out = ws + ((second ? gridDim.x : 0) + (int64_t)blockIdx.x) * NPAD * NPAD;
     out[(8 * fm + (l >> 2)) * NPAD + 8 * fn + 2 * (l & 3) + j] = sum;
-  }
-  if constexpr (R > 0) {
-    for (int e = threadIdx.x; e < RS; e += TTH) {
-      double sum = 0.0;
-#pragma unroll
-      for (int w = 0; w < TSC; ++w) sum += rred[w * RS + e];
-      const int l = e % 32, k = (e / 32) % NR, r = (e / 32 / NR) % R, h = e / 32 / NR / R;
-      const int i = l + 32 * h, rr = 8 * FD + r;
-      if (i >= N) continue;
-      if (SYM) {
-        if (i <= rr) out[i * NPAD + rr] = sum;
-      } else if (k == 0) {
-        out[i * NPAD + rr] = sum;  // sum_p A_i B_r
-      } else if (i < 8 * FD) {
-        out[rr * NPAD + i] = sum;  // sum_p A_r B_i
-      }
-    }
   }
 }
 
@@ -406,7 +339,7 @@ int nsm() {
 template <int F>
 bool launch_gram_tma_f(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                        const double* B, const double* Bb, double sb, double* ws, double* G,
-                       double w, cudaStream_t s, const double* guard) {
+                       double w, cudaStream_t s, const double* guard, double* G2) {
   constexpr int NPAD = 8 * F;
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
@@ -424,28 +357,19 @@ bool launch_gram_tma_f(int N, int64_t ld, int sym, const double* A, const double
       if (!make_map2(maps, nsrc++, Bb, ld, N, NPAD)) return false;
     }
   }
-  // R = 0: splitting off a 1-2 orbital FMA tail (the R > 0 variants) measured
-  // slower here; the 2D TMA stream bounds this kernel, not the DMMA count
-  const int R = 0;
-  const int fd = F;
-  const int np = sym ? fd * (fd + 1) / 2 : fd * fd;
-  const size_t red = (size_t)TSC * np * 64 + (size_t)TSC * 2 * 2 * 2 * 32;
+  const bool dual = G2 != nullptr && !sym;
+  const int np = (sym ? F * (F + 1) / 2 : F * F) + (dual ? F * (F + 1) / 2 : 0);
+  const size_t red = (size_t)TSC * np * 64;
   TCfg cfg = tcfg(nsrc, N, 0);
-  if (cfg.smem < 2048 + red * 8) cfg.smem = 2048 + red * 8;
+  if (cfg.smem < 3072 + red * 8) cfg.smem = 3072 + red * 8;
   const int64_t kblocks = (ld + TKS - 1) / TKS;
   int nsplit = nsm();
   if (nsplit > kblocks) nsplit = (int)kblocks;
   const int64_t kchunk = ((kblocks + nsplit - 1) / nsplit) * TKS;
   nsplit = (int)((ld + kchunk - 1) / kchunk);
   ::po::count_launch();
-  auto pick = [&]() {
-    if (F == 1) return sym ? gram_tma_kernel<F, true, 0> : gram_tma_kernel<F, false, 0>;
-    if (sym) return R == 1 ? gram_tma_kernel<F, true, 1>
-                           : R == 2 ? gram_tma_kernel<F, true, 2> : gram_tma_kernel<F, true, 0>;
-    return R == 1 ? gram_tma_kernel<F, false, 1>
-                  : R == 2 ? gram_tma_kernel<F, false, 2> : gram_tma_kernel<F, false, 0>;
-  };
-  auto k = pick();
+  auto k = sym ? gram_tma_kernel<F, true, false>
+               : dual ? gram_tma_kernel<F, false, true> : gram_tma_kernel<F, false, false>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
   const char* pe = getenv("PO_GRAM_PROBE");  // measurement hook (TMA ring without math)
   const int probe = pe ? atoi(pe) : 0;
@@ -455,6 +379,11 @@ bool launch_gram_tma_f(int N, int64_t ld, int sym, const double* A, const double
   ::po::count_launch();
   gram_tma_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(N, NPAD, sym, nsplit, w,
                                                                            ws, G, guard);
+  if (dual) {
+    ::po::count_launch();
+    gram_tma_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+        N, NPAD, 1, nsplit, w, ws + (size_t)nsplit * NPAD * NPAD, G2, guard);
+  }
   return true;
 }
 
@@ -1381,11 +1310,11 @@ int launch_directions(int N, int64_t ld, int64_t ngl, const double* W, const dou
 
 bool launch_gram_tma(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                      const double* B, const double* Bb, double sb, double* ws, double* G, double w,
-                     cudaStream_t s, const double* guard) {
+                     cudaStream_t s, const double* guard, double* G2) {
   switch ((N + 7) / 8) {
 #define PO_GT(F) \
   case F:        \
-    return launch_gram_tma_f<F>(N, ld, sym, A, Ab, sa, B, Bb, sb, ws, G, w, s, guard);
+    return launch_gram_tma_f<F>(N, ld, sym, A, Ab, sa, B, Bb, sb, ws, G, w, s, guard, G2);
     PO_GT(1) PO_GT(2) PO_GT(3) PO_GT(4) PO_GT(5) PO_GT(6)
 #undef PO_GT
   }

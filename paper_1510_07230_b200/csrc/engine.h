@@ -131,7 +131,7 @@ class Engine {
   double* gram_ws = nullptr;
   double* dvec = nullptr;      // small device vector scratch (kDvec doubles)
   double* hvec = nullptr;      // pinned mirror of dvec
-  double* dmat[8] = {};        // N x N device matrices
+  double* dmat[10] = {};       // N x N device matrices ([7] G_HH, [8] G_WW of the iterate)
   double* hmat = nullptr;      // pinned N x N host
   double* chol_L = nullptr;    // N x N scratch
   double* syev_work = nullptr;

@@ -89,9 +89,16 @@ int launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, doub
 // dmma_tma.cu: 2D tensor-map TMA versions of the small-N Gram / mix (false / -1
 // when unavailable: no driver entry point or N out of range).
 bool tma2d_available();
+// G2 != null with sym = 0: the same pass also writes G2 = w A^T A (symmetric).
 bool launch_gram_tma(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                      const double* B, const double* Bb, double sb, double* ws, double* G, double w,
-                     cudaStream_t s, const double* guard);
+                     cudaStream_t s, const double* guard, double* G2 = nullptr);
+// Trial Gram of W - tau Z from the iteration's Grams, Z = HW - W diag(sigma):
+//   G0 = G_WW - tau (W^T Z + Z^T W) + tau^2 Z^T Z with W^T Z = Sigma^T - G_WW diag(sigma),
+//   Z^T Z = G_HH - Sigma diag(sigma) - diag(sigma) Sigma^T + diag(sigma) G_WW diag(sigma)
+// (Sigma_ij = <HW_i, W_j>). Exactly symmetric.
+void launch_trial_gram(int N, const double* gww, const double* sigma, const double* ghh,
+                       double tau, double* G0, cudaStream_t s);
 // Large-N (N > 48) Gram: 128x128 (or 64x64) orbital tiles x point splits,
 // one 16-point 2D box per source per stage; returns false when unavailable.
 size_t gram_big_workspace_doubles(int64_t ld, int N);

@@ -160,9 +160,13 @@ bool orthonormalize_dev(Engine& E, const double* A, const double* Ab, double sa,
 // single readback; a failed pass-1 Cholesky (rare) is redone synchronously with
 // the symmetric-eigen fallback.
 bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, double* out,
-                  double* tmp, bool measure, DevState* st = nullptr, int hartree = 0, int xc = 0) {
+                  double* tmp, bool measure, DevState* st = nullptr, int hartree = 0, int xc = 0,
+                  bool g0_from_grams = false) {
   double* sc = E.scal();
-  E.gram(A, Ab, sa, A, Ab, sa, 1, E.dmat[0]);
+  if (g0_from_grams)  // G0 of W - tau Z from G_WW (dmat[8]), Sigma (dmat[4]), G_HH (dmat[7])
+    launch_trial_gram(E.N, E.dmat[8], E.dmat[4], E.dmat[7], -sa, E.dmat[0], E.s);
+  else
+    E.gram(A, Ab, sa, A, Ab, sa, 1, E.dmat[0]);
   launch_matrix_stats(E.N, E.dmat[0], sc + Engine::S_MSTAT, E.s);
   launch_cholesky_inv(E.N, E.dmat[0], E.chol_L, E.dmat[1], sc + Engine::S_CHOL, E.s);
   bool fused = false;
@@ -231,6 +235,9 @@ struct Solver {
   std::vector<double> orth_energies;
   bool history_valid = false, converged = false, finished = false;
   bool sig_valid = true;  // dvec sigma row belongs to (w, hw)
+  // trial Grams from the iteration's Grams (no pass over W - tau Z): G_WW of the
+  // iterate in dmat[8] (the accepted trial's verification Gram), G_HH in dmat[7]
+  bool gww_valid = false, ghh_fresh = false;
   int last_rotation_iter = 0, steps_until_orth = 0, failed_searches = 0, l = 0;
   double last_accepted_tau = 0.0;
   int n_org = 1;
@@ -311,6 +318,19 @@ struct Solver {
     launch_matrix_stats(E.N, E.dmat[4], E.scal() + Engine::S_SYM, E.s);
   }
 
+  // Sigma and G_HH = w (HW)^T HW in one pass (small N); false if unavailable
+  bool sigma_dual(const BRef& w, const BRef& hw) {
+    if (!launch_gram_tma(E.N, E.g.ld, 0, P(hw), nullptr, 0.0, P(w), nullptr, 0.0, E.gram_ws,
+                         E.dmat[4], E.g.w, E.s, nullptr, E.dmat[7]))
+      return false;
+    if (E.size > 1) {
+      E.comm->allreduce_sum(E.dmat[4], (size_t)E.N * E.N, E.s);
+      E.comm->allreduce_sum(E.dmat[7], (size_t)E.N * E.N, E.s);
+    }
+    launch_matrix_stats(E.N, E.dmat[4], E.scal() + Engine::S_SYM, E.s);
+    return true;
+  }
+
   void trace_eigs(const BRef& w, const BRef& hw) {
     if (!p.trace_sigma_eigs || !r->sigma_eigs) return;
     sigma(w, hw);
@@ -353,6 +373,10 @@ void Solver::init(const BRef& w0) {
   orth_energies.assign(1, e0.total);
   recovery_w = w;
   recovery_state = state;
+  if (E.N <= 48 && tma2d_available()) {
+    E.gram(P(w), nullptr, 0.0, P(w), nullptr, 0.0, 1, E.dmat[8]);
+    gww_valid = true;
+  }
 }
 
 bool Solver::step() {
@@ -375,8 +399,10 @@ bool Solver::step() {
     bool fused = false;
     if (!full_grad && !(mean_abs && need_full) && n <= 48 && tma2d_available()) {
       // one pass: z, ||z||^2, ||HW - W Sigma||^2 and the BB products
+      ghh_fresh = false;
       if (need_full || !sig_valid) {
-        sigma(w, hw);
+        ghh_fresh = gww_valid && sigma_dual(w, hw);
+        if (!ghh_fresh) sigma(w, hw);
         launch_copy_diag(n, E.dmat[4], E.dvec + E.off_sig(), E.s);
       }
       const int nb = launch_directions(
@@ -491,6 +517,7 @@ bool Solver::step() {
       prev_z = z;
       w = wn;
       history_valid = true;
+      gww_valid = false;  // a raw step leaves the manifold
       state = enqueue_state(w);
       BRef hn = pool.get();
       E.apply_h(P(w), P(hn), state->v_local, false);
@@ -509,7 +536,9 @@ bool Solver::step() {
       BRef wt, hwt;
       SRef tstate;
       EnergyParts te;
+      bool sync_orth = false;  // the accepted trial went through orthonormalize_dev
       for (s = 0; s <= p.max_backtracks; ++s) {
+        sync_orth = false;
         tau = tau_raw * std::pow(p.delta, s);
         if (s > 0 && tau < p.tau_min) break;
         wt = pool.get();
@@ -517,7 +546,8 @@ bool Solver::step() {
         // one device pipeline per trial, one readback (energy + decisions)
         SRef pre = nonlinear ? spool.get() : SRef();
         const bool dens = orth_enqueue(E, P(w), P(z), -tau, P(wt), P(rep),
-                                       p.verify_orthonormality != 0, pre.get(), p.hartree, p.xc);
+                                       p.verify_orthonormality != 0, pre.get(), p.hartree, p.xc,
+                                       gww_valid && ghh_fresh);
         tstate = enqueue_state(wt, pre, dens);
         hwt = pool.get();
         E.apply_h(P(wt), P(hwt), tstate->v_local, !nonlinear);
@@ -529,6 +559,7 @@ bool Solver::step() {
           if (!orthonormalize_dev(E, P(w), P(z), -tau, P(wt), scratch,
                                   p.verify_orthonormality != 0, orth))
             continue;
+          sync_orth = true;
           tstate = make_state(wt);
           te = apply_and_energy(wt, hwt, *tstate);
         } else {
@@ -556,6 +587,7 @@ bool Solver::step() {
         E.apply_h(P(w), P(hn), state->v_local, false);
         hw = hn;
         sig_valid = true;
+        gww_valid = false;
         history_valid = false;
         prev_w.reset();
         prev_z.reset();
@@ -587,6 +619,11 @@ bool Solver::step() {
       sig_valid = true;
       history_valid = true;
       last_accepted_tau = tau;
+      // the accepted trial's verification Gram (post-repair if repaired) is G_WW of w
+      gww_valid = !sync_orth && E.N <= 48 && tma2d_available();
+      if (gww_valid)
+        PO_CUDA(cudaMemcpyAsync(E.dmat[8], E.dmat[2], sizeof(double) * n * n,
+                                cudaMemcpyDeviceToDevice, E.s));
       set_energy(te);
       orth_energies.push_back(te.total);
       rec.did_orth = 1;
@@ -612,6 +649,7 @@ bool Solver::step() {
         rec.did_diag = 1;
         history_valid = false;
         sig_valid = false;
+        gww_valid = false;
         prev_w.reset();
         prev_z.reset();
       }
