@@ -413,7 +413,9 @@ __global__ void copy_guarded_kernel(double* __restrict__ dst, const double* __re
 
 __global__ void trial_gram_kernel(int N, const double* __restrict__ gww,
                                   const double* __restrict__ S, const double* __restrict__ ghh,
-                                  double tau, double* __restrict__ G0) {
+                                  double tau, double* __restrict__ G0,
+                                  const double* __restrict__ tau_dev) {
+  if (tau_dev) tau = *tau_dev;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)N * N) return;
   const int i = (int)(e / N), j = (int)(e % N);
@@ -428,13 +430,50 @@ __global__ void trial_gram_kernel(int N, const double* __restrict__ gww,
   G0[(int64_t)j * N + i] = v;
 }
 
+// one thread: the host mirror's loops, in the same order (bitwise-equal tau)
+__global__ void bb_tau_kernel(int N, const double* __restrict__ zz, const double* __restrict__ ss,
+                              const double* __restrict__ sy, const double* __restrict__ yy,
+                              int history, int use_bb1, int trace_abs_diag, double tau_min,
+                              double tau_max, double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double znorm2 = 0.0;
+  for (int i = 0; i < N; ++i) znorm2 += zz[i];
+  double raw;
+  if (history) {
+    double tr_ss = 0.0, tr_yy = 0.0, sy_abs = 0.0, sy_tr = 0.0;
+    for (int i = 0; i < N; ++i) {
+      tr_ss += ss[i];
+      tr_yy += yy[i];
+      sy_abs += fabs(sy[i]);
+      sy_tr += sy[i];
+    }
+    const double tr_abs_sy = trace_abs_diag ? sy_abs : fabs(sy_tr);
+    raw = use_bb1 ? tr_ss / tr_abs_sy : tr_abs_sy / tr_yy;
+  } else {
+    raw = fmin(tau_max, 1.0 / sqrt(znorm2));
+  }
+  const double tau = isfinite(raw) ? fmin(fmax(raw, tau_min), tau_max) : tau_max;
+  out[0] = tau;
+  out[1] = -tau;
+  out[2] = znorm2;
+}
+
 }  // namespace
 
+void launch_bb_tau(int N, const double* zz, const double* ss, const double* sy, const double* yy,
+                   int history, int use_bb1, int trace_abs_diag, double tau_min, double tau_max,
+                   double* out, cudaStream_t s) {
+  ::po::count_launch();
+  bb_tau_kernel<<<1, 32, 0, s>>>(N, zz, ss, sy, yy, history, use_bb1, trace_abs_diag, tau_min,
+                                 tau_max, out);
+}
+
 void launch_trial_gram(int N, const double* gww, const double* sigma, const double* ghh,
-                       double tau, double* G0, cudaStream_t s) {
+                       double tau, double* G0, cudaStream_t s, const double* tau_dev) {
   const int64_t total = (int64_t)N * N;
   ::po::count_launch();
-  trial_gram_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(N, gww, sigma, ghh, tau, G0);
+  trial_gram_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(N, gww, sigma, ghh, tau, G0,
+                                                                    tau_dev);
 }
 
 void launch_qr2_decision(const double* chol_stats, const double* gram2_stats, int measure,
@@ -458,8 +497,7 @@ void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, do
     const size_t shm = sizeof(double) * ((size_t)N * (N + 1) + N);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(cholesky_inv_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(sizeof(double) * (CHOL_SMEM_MAX * (CHOL_SMEM_MAX + 1) + CHOL_SMEM_MAX)));
+      set_smem(reinterpret_cast<const void*>(cholesky_inv_smem_kernel), (int)(sizeof(double) * (CHOL_SMEM_MAX * (CHOL_SMEM_MAX + 1) + CHOL_SMEM_MAX)));
       attr = true;
     }
     cholesky_inv_smem_kernel<<<1, CHT, shm, s>>>(N, G, M, stats, guard);

@@ -469,11 +469,11 @@ void launch_gram_small_f(int N, int64_t ld, int sym, const double* A, const doub
   ::po::count_launch();
   if (sym) {
     auto k = gram_ring_kernel<F, true>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
+    set_smem(reinterpret_cast<const void*>(k), (int)(cfg.smem));
     k<<<nsplit, RING_THREADS, cfg.smem, s>>>(N, ld, kchunk, cfg.ks, cfg.nst, A, Ab, sa, A, Ab, sa, ws, guard);
   } else {
     auto k = gram_ring_kernel<F, false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
+    set_smem(reinterpret_cast<const void*>(k), (int)(cfg.smem));
     k<<<nsplit, RING_THREADS, cfg.smem, s>>>(N, ld, kchunk, cfg.ks, cfg.nst, A, Ab, sa, B, Bb, sb, ws, guard);
   }
   const int64_t threads = (int64_t)N * N * 32;
@@ -587,11 +587,11 @@ int launch_mix_small_f(int N, int64_t ld, int64_t ngl, const double* A, const do
   ::po::count_launch();
   if (upper) {
     auto k = mix_small_kernel<F, true>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem(reinterpret_cast<const void*>(k), (int)(smem));
     k<<<nblk, ST, smem, s>>>(N, ld, ngl, pchunk, A, Ab, sa, M, alpha, C, beta, out, norms, guard);
   } else {
     auto k = mix_small_kernel<F, false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem(reinterpret_cast<const void*>(k), (int)(smem));
     k<<<nblk, ST, smem, s>>>(N, ld, ngl, pchunk, A, Ab, sa, M, alpha, C, beta, out, norms, guard);
   }
   return nblk;
@@ -791,7 +791,7 @@ void launch_gram(const SlabGeom& g, int N, const double* A, const double* Ab, do
   constexpr size_t shm = sizeof(double) * 4 * GB * GKP;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+    set_smem(reinterpret_cast<const void*>(gram_kernel), (int)(shm));
     attr = true;
   }
   ::po::count_launch();
@@ -832,7 +832,7 @@ int launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, doub
   constexpr size_t shm = sizeof(double) * (2 * MK * MPP + 2 * MK * MIP + 4 * MI);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(mix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+    set_smem(reinterpret_cast<const void*>(mix_kernel), (int)(shm));
     attr = true;
   }
   ::po::count_launch();
@@ -847,7 +847,7 @@ void launch_mix_batched(int N, int64_t ld, int64_t ngl, int batch, int64_t bstri
   constexpr size_t shm = sizeof(double) * (2 * MK * MPP + 2 * MK * MIP + 4 * MI);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(mix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+    set_smem(reinterpret_cast<const void*>(mix_kernel), (int)(shm));
     attr = true;
   }
   ::po::count_launch();

@@ -268,8 +268,8 @@ void launch_fused(const DstPoisson& d, const double* b, double* x, cudaStream_t 
   const size_t sh1 = p_sg ? pl : 2 * pl;
   auto ka = a_sg ? dst_axis0_kernel<NF, true> : dst_axis0_kernel<NF, false>;
   auto kp = p_sg ? dst_plane_kernel<NF, true> : dst_plane_kernel<NF, false>;
-  cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh0);
-  cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh1);
+  set_smem(reinterpret_cast<const void*>(ka), (int)(sh0));
+  set_smem(reinterpret_cast<const void*>(kp), (int)(sh1));
   const unsigned g0 = (unsigned)((plane + A0P - 1) / A0P);
   ::po::count_launch();
   ka<<<g0, AW * 32, sh0, s>>>(b, d.t0, (int)d.n0, plane, d.S[0]);

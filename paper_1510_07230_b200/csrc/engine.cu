@@ -89,7 +89,11 @@ Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist
   PO_CUDA(cudaMalloc(&gram_ws, gram_workspace_doubles(g, N) * sizeof(double)));
   PO_CUDA(cudaMalloc(&dvec, dvec_len() * sizeof(double)));
   PO_CUDA(cudaMemsetAsync(dvec, 0, dvec_len() * sizeof(double), s));
-  PO_CUDA(cudaMallocHost(&hvec, dvec_len() * sizeof(double)));
+  PO_CUDA(cudaHostAlloc(&hvec, dvec_len() * sizeof(double), cudaHostAllocMapped));
+  PO_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hvec_dev), hvec, 0));
+  PO_CUDA(cudaHostAlloc(&hflag, sizeof(unsigned long long), cudaHostAllocMapped));
+  PO_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hflag_dev), hflag, 0));
+  *hflag = 0;
   const size_t nn = (size_t)N * N * sizeof(double);
   for (auto& m : dmat) PO_CUDA(cudaMalloc(&m, nn));
   PO_CUDA(cudaMalloc(&chol_L, nn));
@@ -114,7 +118,9 @@ Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist
   PO_CUDA(cudaMalloc(&cg_bar, 4 * sizeof(unsigned)));
   PO_CUDA(cudaMalloc(&cg_out_i, 4 * sizeof(int)));
   PO_CUDA(cudaMalloc(&cg_out_d, 4 * sizeof(double)));
-  PO_CUDA(cudaMallocHost(&h_cg_i, 4 * sizeof(int)));
+  PO_CUDA(cudaHostAlloc(&h_cg_i, 4 * sizeof(int), cudaHostAllocMapped));
+  PO_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_cg_i_dev), h_cg_i, 0));
+  std::memset(h_cg_i, 0, 4 * sizeof(int));
   PO_CUDA(cudaMallocHost(&h_cg_d, 4 * sizeof(double)));
   PO_CUDA(cudaMemsetAsync(cg_out_i, 0, 4 * sizeof(int), s));
   PO_CUDA(cudaMemsetAsync(cg_out_d, 0, 4 * sizeof(double), s));
@@ -146,6 +152,7 @@ Engine::~Engine() {
   if (hvec) cudaFreeHost(hvec);
   if (hmat) cudaFreeHost(hmat);
   if (h_cg_i) cudaFreeHost(h_cg_i);
+  if (hflag) cudaFreeHost(hflag);
   if (h_cg_d) cudaFreeHost(h_cg_d);
   dst.release();
   comm.reset();
@@ -222,9 +229,41 @@ void Engine::free_state(DevState* st) {
     }
 }
 
+// Readback without the copy engine: one small kernel stores the scalars (and
+// the Poisson status) straight into mapped pinned memory, then a sequence flag;
+// the host spins on the flag (a cudaMemcpyAsync D2H + stream query costs
+// 7-9 us of copy-engine latency plus the polling interval per readback).
+__global__ void publish_kernel(const double* __restrict__ src, double* dst, int n,
+                               const int* __restrict__ isrc, int* idst,
+                               volatile unsigned long long* flag, unsigned long long seq) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  if (threadIdx.x < 2) idst[threadIdx.x] = isrc[threadIdx.x];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *flag = seq;
+    __threadfence_system();
+  }
+}
+
 void Engine::fetch(size_t off, size_t n) {
-  PO_CUDA(cudaMemcpyAsync(hvec + off, dvec + off, n * sizeof(double), cudaMemcpyDeviceToHost, s));
-  sync();
+  PO_CUDA(cudaGetLastError());
+  const unsigned long long seq = ++pub_seq;
+  ::po::count_launch();
+  publish_kernel<<<1, 256, 0, s>>>(dvec + off, hvec_dev + off, (int)n, cg_out_i, h_cg_i_dev,
+                                   hflag_dev, seq);
+  PO_CUDA(cudaGetLastError());
+  volatile unsigned long long* f = hflag;
+  for (unsigned spins = 1; *f != seq; ++spins) {
+    if ((spins & 1023u) == 0) {  // surface stream errors instead of spinning forever
+      const cudaError_t e = cudaStreamQuery(s);
+      if (e != cudaSuccess && e != cudaErrorNotReady)
+        throw Error(PO_ECUDA, std::string("stream: ") + cudaGetErrorString(e));
+      if (e == cudaSuccess && *f != seq) break;
+    }
+  }
+  if (*f != seq) sync();
+  std::atomic_thread_fence(std::memory_order_acquire);
 }
 
 void Engine::reduce_rows(const double* parts, int rows, int nblk, double scale, double* out,
@@ -266,16 +305,14 @@ void Engine::build_state(const double* u, int hartree, int xc, DevState* st, int
       }
     }
     poisson(warm_ok);
-    PO_CUDA(cudaMemcpyAsync(st->v_h, cg_x + g.z0 * g.plane, sizeof(double) * g.ngl,
-                            cudaMemcpyDeviceToDevice, s));
   } else {
-    PO_CUDA(cudaMemsetAsync(st->v_h, 0, sizeof(double) * g.ngl, s));
     PO_CUDA(cudaMemsetAsync(cg_out_i, 0, 2 * sizeof(int), s));
   }
-  launch_vlocal(g, v_ext, st->v_h, st->v_xc, st->rho, st->v_local, partials, s);
+  // v_H slab copied out of the Poisson solution by the same pass that forms v_local
+  launch_vlocal(g, v_ext, hartree ? cg_x + g.z0 * g.plane : nullptr, st->v_h, st->v_xc, st->rho,
+               st->v_local, partials, s);
   launch_reduce_rows(partials, 1, pn, 0.5 * g.w, scal() + S_EH, s);  // E_H = 1/2 <v_H, rho>
   if (size > 1) comm->allreduce_sum(scal() + S_EXC, 3, s);          // S_EXC..S_EH
-  PO_CUDA(cudaMemcpyAsync(h_cg_i, cg_out_i, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
   PO_CUDA(cudaGetLastError());
   if (!xc) PO_CUDA(cudaMemsetAsync(scal() + S_EXC, 0, sizeof(double), s));
   if (!hartree) PO_CUDA(cudaMemsetAsync(scal() + S_EH, 0, sizeof(double), s));

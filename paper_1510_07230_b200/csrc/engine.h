@@ -130,7 +130,12 @@ class Engine {
   size_t partials_cap = 0;
   double* gram_ws = nullptr;
   double* dvec = nullptr;      // small device vector scratch (kDvec doubles)
-  double* hvec = nullptr;      // pinned mirror of dvec
+  double* hvec = nullptr;      // pinned, device-mapped mirror of dvec
+  double* hvec_dev = nullptr;  // its device alias (written by the publish kernel)
+  unsigned long long* hflag = nullptr;      // mapped: sequence number of the last publish
+  unsigned long long* hflag_dev = nullptr;
+  int* h_cg_i_dev = nullptr;
+  unsigned long long pub_seq = 0;
   double* dmat[10] = {};       // N x N device matrices ([7] G_HH, [8] G_WW of the iterate)
   double* hmat = nullptr;      // pinned N x N host
   double* chol_L = nullptr;    // N x N scratch
@@ -167,7 +172,8 @@ class Engine {
   size_t dvec_len() const { return 9 * (size_t)N + 64; }
   // scalar slots
   enum { S_EXC = 0, S_EEXT = 1, S_EH = 2, S_CHOL = 8, S_EIG = 12, S_INVS = 16, S_MSTAT = 20,
-         S_MSTAT2 = 24, S_SYM = 28, S_QR2 = 32, S_CHOL2 = 36 };
+         S_MSTAT2 = 24, S_SYM = 28, S_QR2 = 32, S_CHOL2 = 36,
+         S_TAU = 40 /* [0] tau_raw, [1] -tau_raw (trial scale), [2] znorm2 */ };
   double* scal() { return dvec + off_scal(); }
   // copy n doubles of dvec starting at off into hvec (same offsets) and synchronise
   void fetch(size_t off, size_t n);

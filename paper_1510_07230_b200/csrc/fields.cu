@@ -68,8 +68,11 @@ __global__ void __launch_bounds__(PT) density_xc_kernel(SlabGeom g, int N,
   }
 }
 
+// vh_src: the Poisson solution slab (copied into the state's v_H here) or null
+// for "no Hartree" (v_H = 0 written).
 __global__ void __launch_bounds__(PT) vlocal_kernel(SlabGeom g, const double* __restrict__ vext,
-                                                    const double* __restrict__ vh,
+                                                    const double* __restrict__ vh_src,
+                                                    double* __restrict__ vh,
                                                     const double* __restrict__ vxc,
                                                     const double* __restrict__ rho,
                                                     double* __restrict__ vloc,
@@ -78,7 +81,8 @@ __global__ void __launch_bounds__(PT) vlocal_kernel(SlabGeom g, const double* __
   double acc[1] = {0.0};
   for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < g.ngl;
        p += (int64_t)gridDim.x * PT) {
-    const double h = vh[p];
+    const double h = vh_src ? vh_src[p] : 0.0;
+    vh[p] = h;
     vloc[p] = vext[p] + (h + vxc[p]);
     acc[0] += h * rho[p];
   }
@@ -242,10 +246,12 @@ void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupat
                                                   partials, guard);
 }
 
-void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h, const double* v_xc,
-                   const double* rho, double* v_local, double* partials, cudaStream_t s) {
+void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h_src, double* v_h,
+                   const double* v_xc, const double* rho, double* v_local, double* partials,
+                   cudaStream_t s) {
   ::po::count_launch();
-  vlocal_kernel<<<points_nblk(g), PT, 0, s>>>(g, v_ext, v_h, v_xc, rho, v_local, partials);
+  vlocal_kernel<<<points_nblk(g), PT, 0, s>>>(g, v_ext, v_h_src, v_h, v_xc, rho, v_local,
+                                              partials);
 }
 
 void launch_residual_diag(const SlabGeom& g, int N, const double* u, const double* hu,

@@ -44,8 +44,9 @@ void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupat
                        double* rho, double* v_xc, double* b, const double* v_ext, double* partials,
                        cudaStream_t s, const double* guard = nullptr);
 // v_local = v_ext + (v_h + v_xc) (energy.cpp:241-244); partials [1][nblk]: sum v_h*rho.
-void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h, const double* v_xc,
-                   const double* rho, double* v_local, double* partials, cudaStream_t s);
+void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h_src, double* v_h,
+                   const double* v_xc, const double* rho, double* v_local, double* partials,
+                   cudaStream_t s);
 // z_i = hu_i - sigma_ii u_i (manifold.cpp:204-216); partials [1][N][nblk]: sum z^2.
 void launch_residual_diag(const SlabGeom& g, int N, const double* u, const double* hu,
                           const double* sigma_diag, double* z, double* partials, cudaStream_t s);
@@ -89,6 +90,8 @@ int launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, doub
 // dmma_tma.cu: 2D tensor-map TMA versions of the small-N Gram / mix (false / -1
 // when unavailable: no driver entry point or N out of range).
 bool tma2d_available();
+// once per kernel: max-shared carveout + dynamic shared-memory limit (bytes may be 0)
+void set_smem(const void* k, int bytes);
 // G2 != null with sym = 0: the same pass also writes G2 = w A^T A (symmetric).
 bool launch_gram_tma(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                      const double* B, const double* Bb, double sb, double* ws, double* G, double w,
@@ -98,7 +101,14 @@ bool launch_gram_tma(int N, int64_t ld, int sym, const double* A, const double* 
 //   Z^T Z = G_HH - Sigma diag(sigma) - diag(sigma) Sigma^T + diag(sigma) G_WW diag(sigma)
 // (Sigma_ij = <HW_i, W_j>). Exactly symmetric.
 void launch_trial_gram(int N, const double* gww, const double* sigma, const double* ghh,
-                       double tau, double* G0, cudaStream_t s);
+                       double tau, double* G0, cudaStream_t s, const double* tau_dev = nullptr);
+// Barzilai-Borwein step on the device (optimizer.cpp:25-41, 376-411), same
+// sequential sums as the host mirror: out[0] = tau_raw, out[1] = -tau_raw,
+// out[2] = sum_i zz_i. zz/ss/sy/yy are per-orbital rows (ss/sy/yy unused
+// without history).
+void launch_bb_tau(int N, const double* zz, const double* ss, const double* sy, const double* yy,
+                   int history, int use_bb1, int trace_abs_diag, double tau_min, double tau_max,
+                   double* out, cudaStream_t s);
 // Large-N (N > 48) Gram: 128x128 (or 64x64) orbital tiles x point splits,
 // one 16-point 2D box per source per stage; returns false when unavailable.
 size_t gram_big_workspace_doubles(int64_t ld, int N);
@@ -117,7 +127,8 @@ bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* 
 int launch_rotate_fused(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab,
                         double sa, const double* M, double* out, double* ws, double* G, double w,
                         double occ, int xc, double* rho, double* vxc, double* bvec,
-                        const double* vext, double* dpart, cudaStream_t s);
+                        const double* vext, double* dpart, cudaStream_t s,
+                        const double* sa_dev = nullptr);
 int launch_directions(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
                       const double* WP, const double* ZP, const double* Sigma, const double* sig,
                       double* Z, double* partials, cudaStream_t s);

@@ -21,6 +21,7 @@
 #include <functional>
 #include <limits>
 #include <memory>
+#include <utility>
 #include <vector>
 
 #include "engine.h"
@@ -161,10 +162,10 @@ bool orthonormalize_dev(Engine& E, const double* A, const double* Ab, double sa,
 // the symmetric-eigen fallback.
 bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, double* out,
                   double* tmp, bool measure, DevState* st = nullptr, int hartree = 0, int xc = 0,
-                  bool g0_from_grams = false) {
+                  bool g0_from_grams = false, const double* tau_dev = nullptr) {
   double* sc = E.scal();
   if (g0_from_grams)  // G0 of W - tau Z from G_WW (dmat[8]), Sigma (dmat[4]), G_HH (dmat[7])
-    launch_trial_gram(E.N, E.dmat[8], E.dmat[4], E.dmat[7], -sa, E.dmat[0], E.s);
+    launch_trial_gram(E.N, E.dmat[8], E.dmat[4], E.dmat[7], -sa, E.dmat[0], E.s, tau_dev);
   else
     E.gram(A, Ab, sa, A, Ab, sa, 1, E.dmat[0]);
   launch_matrix_stats(E.N, E.dmat[0], sc + Engine::S_MSTAT, E.s);
@@ -174,7 +175,8 @@ bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, doubl
     // rotation + verification Gram + density/xc of the rotated block in one pass
     const int nb = launch_rotate_fused(E.N, E.g.ld, E.g.ngl, A, Ab, sa, E.dmat[1], out, E.gram_ws,
                                        E.dmat[2], E.g.w, E.occ, xc, st->rho, st->v_xc,
-                                       E.density_b_target(hartree), E.v_ext, E.partials, E.s);
+                                       E.density_b_target(hartree), E.v_ext, E.partials, E.s,
+                                       tau_dev ? tau_dev + 1 : nullptr);
     if (nb >= 0) {
       if (E.size > 1) E.comm->allreduce_sum(E.dmat[2], (size_t)E.N * E.N, E.s);
       launch_reduce_rows(E.partials, 2, nb, E.g.w, sc + Engine::S_EXC, E.s);
@@ -182,6 +184,7 @@ bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, doubl
     }
   }
   if (!fused) {
+    if (tau_dev) throw Error(PO_EINVAL, "device-side trial scale needs the fused rotation");
     E.mix(A, Ab, sa, E.dmat[1], 1.0, nullptr, 0.0, 1, out, nullptr);
     E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2]);
   }
@@ -341,6 +344,26 @@ struct Solver {
     std::memcpy(r->sigma_eigs + (size_t)r->n_records * E.N, E.hmat, sizeof(double) * E.N);
   }
 
+  // Phase 1 of an iteration (directions + the speculative first trial), enqueued
+  // either at the start of step() or already at the end of the previous step,
+  // so the GPU never waits for the host between iterations
+  struct Phase1 {
+    bool valid = false;
+    Clock::time_point t0;
+    bool orth_iter = false, need_full = false, fused = false;
+    BRef z, dscratch;
+    struct {
+      BRef wt, rep, hwt;
+      SRef pre, tstate;
+      bool on = false;
+    } spec;
+  };
+  Phase1 ph1;
+  void enqueue_phase1(int iter);  // iter: the iteration these directions belong to
+  void prefetch_next() {
+    if (!ph1.valid && !finished && !converged && l < p.max_inner) enqueue_phase1(l);
+  }
+
   void init(const BRef& w0);
   bool step();  // one InnerLoop iteration; false once the loop has ended
 };
@@ -379,24 +402,21 @@ void Solver::init(const BRef& w0) {
   }
 }
 
-bool Solver::step() {
+void Solver::enqueue_phase1(int iter) {
   const int n = E.N;
-  if (finished) return false;
-  if (!(l < p.max_inner && !converged)) {
-    r->outcome = converged ? PO_OUT_CONVERGED : PO_OUT_MAX_ITERATIONS;
-    finished = true;
-    return false;
-  }
-  {
-    const auto t0 = Clock::now();
-    const bool orth_iter = steps_until_orth == 0;
-    const bool need_full = orth_iter && grad_style;
+  Phase1& ph = ph1;
+  ph = Phase1();
+  ph.valid = true;
+  ph.t0 = Clock::now();
+  const bool orth_iter = ph.orth_iter = steps_until_orth == 0;
+  const bool need_full = ph.need_full = orth_iter && grad_style;
 
     // ---- compute_directions, optimizer.cpp:265-320
-    BRef z = pool.get();
-    BRef dscratch;
+    BRef& z = ph.z;
+    z = pool.get();
+    BRef& dscratch = ph.dscratch;
     const int onb = per_orbital_nblk(E.g, n);
-    bool fused = false;
+    bool& fused = ph.fused;
     if (!full_grad && !(mean_abs && need_full) && n <= 48 && tma2d_available()) {
       // one pass: z, ||z||^2, ||HW - W Sigma||^2 and the BB products
       ghh_fresh = false;
@@ -443,6 +463,52 @@ bool Solver::step() {
       launch_bb(E.g, n, P(w), P(prev_w), P(z), P(prev_z), E.partials, E.s);
       E.reduce_rows(E.partials, 3 * n, onb, E.g.w, E.dvec + E.off_ss(), true);
     }
+    // First trial of an orthonormalisation iteration without a host round trip:
+    // the BB step is taken on the device (bb_tau_kernel, the host's sums in the
+    // host's order) and the trial pipeline reads tau from there. The host then
+    // reads the directions and the trial together; a converged / failing
+    // iteration simply discards the speculative trial.
+    auto& spec = ph.spec;
+    if (orth_iter && fused && gww_valid && ghh_fresh && nonlinear && E.N <= 48 &&
+        tma2d_available()) {
+      double* st_tau = E.scal() + Engine::S_TAU;
+      launch_bb_tau(n, E.dvec + E.off_zz(), E.dvec + E.off_ss(), E.dvec + E.off_sy(),
+                    E.dvec + E.off_yy(), history_valid ? 1 : 0, use_bb1(p.bb_variant, iter) ? 1 : 0,
+                    p.bb_trace_abs == PO_TRACE_DIAG_ABS ? 1 : 0, p.tau_min, p.tau_max, st_tau,
+                    E.s);
+      spec.wt = pool.get();
+      spec.rep = pool.get();
+      spec.pre = spool.get();
+      const bool dens = orth_enqueue(E, P(w), P(z), 0.0, P(spec.wt), P(spec.rep),
+                                     p.verify_orthonormality != 0, spec.pre.get(), p.hartree,
+                                     p.xc, true, st_tau);
+      spec.tstate = enqueue_state(spec.wt, spec.pre, dens);
+      spec.hwt = pool.get();
+      E.apply_h(P(spec.wt), P(spec.hwt), spec.tstate->v_local, false);
+      spec.on = true;
+    }
+}
+
+bool Solver::step() {
+  const int n = E.N;
+  if (finished) return false;
+  if (!(l < p.max_inner && !converged)) {
+    r->outcome = converged ? PO_OUT_CONVERGED : PO_OUT_MAX_ITERATIONS;
+    finished = true;
+    return false;
+  }
+  {
+    if (!ph1.valid) enqueue_phase1(l);
+    Phase1 ph = std::move(ph1);
+    ph1 = Phase1();
+    const auto t0 = ph.t0;
+    const bool orth_iter = ph.orth_iter;
+    const bool need_full = ph.need_full;
+    BRef z = ph.z;
+    BRef dscratch = ph.dscratch;
+    const bool fused = ph.fused;
+    auto& spec = ph.spec;
+    (void)dscratch;
     E.fetch_all();
     const double* hv = E.hvec;
     if ((full_grad || need_full) && hv[E.off_scal() + Engine::S_SYM + 1] > 1e-10)
@@ -502,6 +568,7 @@ bool Solver::step() {
     } else {
       tau_raw = clamp_tau(std::min(p.tau_max, 1.0 / std::sqrt(znorm2)), p);
     }
+    if (spec.on) tau_raw = hv[E.off_scal() + Engine::S_TAU];  // the value the trial used
 
     po_record rec{};
     rec.level = 0;
@@ -541,17 +608,26 @@ bool Solver::step() {
         sync_orth = false;
         tau = tau_raw * std::pow(p.delta, s);
         if (s > 0 && tau < p.tau_min) break;
-        wt = pool.get();
-        BRef rep = pool.get();
-        // one device pipeline per trial, one readback (energy + decisions)
-        SRef pre = nonlinear ? spool.get() : SRef();
-        const bool dens = orth_enqueue(E, P(w), P(z), -tau, P(wt), P(rep),
-                                       p.verify_orthonormality != 0, pre.get(), p.hartree, p.xc,
-                                       gww_valid && ghh_fresh);
-        tstate = enqueue_state(wt, pre, dens);
-        hwt = pool.get();
-        E.apply_h(P(wt), P(hwt), tstate->v_local, !nonlinear);
-        E.fetch_all();
+        BRef rep;
+        if (s == 0 && spec.on) {  // enqueued and read back with the directions
+          wt = spec.wt;
+          rep = spec.rep;
+          tstate = spec.tstate;
+          hwt = spec.hwt;
+          spec = {};
+        } else {
+          wt = pool.get();
+          rep = pool.get();
+          // one device pipeline per trial, one readback (energy + decisions)
+          SRef pre = nonlinear ? spool.get() : SRef();
+          const bool dens = orth_enqueue(E, P(w), P(z), -tau, P(wt), P(rep),
+                                         p.verify_orthonormality != 0, pre.get(), p.hartree, p.xc,
+                                         gww_valid && ghh_fresh);
+          tstate = enqueue_state(wt, pre, dens);
+          hwt = pool.get();
+          E.apply_h(P(wt), P(hwt), tstate->v_local, !nonlinear);
+          E.fetch_all();
+        }
         const int oc = orth_outcome(E, orth);
         if (oc == 2) continue;  // DegenerateSetError -> NaN trial energy
         if (oc == 1) {          // pass-1 Cholesky rejected: symmetric fallback, synchronously
@@ -593,6 +669,7 @@ bool Solver::step() {
         prev_z.reset();
         steps_until_orth = 0;
         ++l;
+        prefetch_next();
         return true;  // no record for a failed search (optimizer.cpp:485-508)
       }
       failed_searches = 0;
@@ -621,9 +698,13 @@ bool Solver::step() {
       last_accepted_tau = tau;
       // the accepted trial's verification Gram (post-repair if repaired) is G_WW of w
       gww_valid = !sync_orth && E.N <= 48 && tma2d_available();
-      if (gww_valid)
-        PO_CUDA(cudaMemcpyAsync(E.dmat[8], E.dmat[2], sizeof(double) * n * n,
-                                cudaMemcpyDeviceToDevice, E.s));
+      if (gww_valid) std::swap(E.dmat[8], E.dmat[2]);  // no copy: exchange the buffers
+      steps_until_orth = n_org - 1;
+      const bool rotation_due =
+          p.n_diag > 0 && (l + 1 - last_rotation_iter) >= p.n_diag && !full_grad;
+      // the next iteration's directions + first trial go to the GPU now; the
+      // bookkeeping below overlaps with them
+      if (!rotation_due && l + 1 < p.max_inner) enqueue_phase1(l + 1);
       set_energy(te);
       orth_energies.push_back(te.total);
       rec.did_orth = 1;
@@ -666,12 +747,13 @@ bool Solver::step() {
         if (acc / 3.0 < p.energy_tol) converged = true;
       }
     }
-    E.sync();
+    if (!ph1.valid) E.sync();  // else the next iteration is already running on the stream
     rec.wall_ms = 1e3 * std::chrono::duration<double>(Clock::now() - t0).count();
     if (r->n_records < r->cap) r->records[r->n_records] = rec;
     r->n_records++;
   }
   ++l;
+  prefetch_next();
   return true;
 }
 

@@ -470,7 +470,7 @@ void launch_h4(const SlabGeom& g, int N, const double* u, const double* lo, cons
 #define PO_H4(JJ)                                                                          \
   case JJ: {                                                                               \
     auto k = hamiltonian4_kernel<JJ, EXT, TYR>;                                             \
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r.smem);     \
+    set_smem(reinterpret_cast<const void*>(k), (int)r.smem);                               \
     k<<<grid, block, r.smem, s>>>(g, N, r.nst, zc, u, lo, hi, vloc, vext, out, partials);  \
     break;                                                                                 \
   }
