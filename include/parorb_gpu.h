@@ -116,6 +116,17 @@ int po_gaussian_potential(po_engine* e, const double* wells, int nwells);
 /* i.i.d. N(0,1) block from parorb::Rng(seed) (rng.hpp:13-41), orbital-major,
  * exactly the reference's bits; generated on the host for this rank's slab. */
 int po_random_block(po_engine* e, int block, uint64_t seed);
+/* optimizer.cpp:156-197 initialize_orbitals: Gaussians centred on the atoms
+ * (x, y, z, Z, a per atom, cycled over the orbitals; the box centre without
+ * atoms) with widths ~ U(0.5, 2) and 1e-2 U(-1, 1) noise from Rng(seed +
+ * attempt), orthonormalised; up to 5 attempts. Result in block w. */
+int po_initialize_orbitals(po_engine* e, const double* atoms, int natoms, uint64_t seed, int w);
+/* grid.cpp:137-149 refine_uniform: n -> 2n + 1 per axis, same extents. */
+int po_refine_grid(const po_grid_desc* grid, po_grid_desc* fine);
+/* grid.cpp:151-203 prolongate, every orbital of block cblock (engine coarse)
+ * into block fblock of engine fine (its grid = po_refine_grid of the coarse
+ * one); bitwise the reference's values. Single-rank engines. */
+int po_prolongate(po_engine* coarse, int cblock, po_engine* fine, int fblock);
 
 /* ------------------------------------------------------------ operators */
 
@@ -188,6 +199,8 @@ typedef struct {
   int hartree, xc;          /* Problem::hartree_enabled / xc_enabled */
   int trace_sigma_eigs;     /* record eig(<(HW)^T W>) after every accepted step */
   int poisson_solver;       /* PO_POISSON_* (default PO_POISSON_DST) */
+  int outer_levels;         /* optimizer.hpp:39 (po_solve_levels) */
+  uint64_t seed;            /* optimizer.hpp:40 initialize_orbitals seed (po_solve_levels) */
 } po_params;
 
 /* IterationRecord, optimizer.hpp:61-72. */
@@ -261,6 +274,22 @@ int po_nccl_unique_id(void* out128);
 /* optimizer.cpp:599-613 run_single_level: u0 (orthonormal, block handle) is
  * iterated in place — on return block w holds the final orbitals. */
 int po_solve(po_engine* e, const po_params* p, int w, po_result* r);
+/* optimizer.cpp:638-669 solve: initialize_orbitals(p->seed) on grid0 (atoms as
+ * in po_external_potential), then p->outer_levels levels — from the second on,
+ * refine_uniform + prolongate + orthonormalize — one InnerLoop each (records
+ * carry the level), early stop on stagnation / numerical failure, finalize on
+ * the last grid. Returns the final engine (caller po_destroy's it; also on
+ * error, for po_last_error) and the block holding the final orbitals. */
+int po_solve_levels(const po_grid_desc* grid0, int n_orbitals, double occupation,
+                    const double* atoms, int natoms, const po_params* p, po_result* r,
+                    po_engine** out_engine, int* out_block);
+/* driver.cpp:131-142 log row "level,iter,energy,grad_norm,tau,backtracks,did_orth,
+ * did_diag,offdiag_max,wall_ms" (no newline); returns the length or -1. */
+int po_format_log_row(const po_record* rec, char* buf, int len);
+/* driver.cpp:152-165 write_log (header + every log_every-th row + each level's last);
+ * driver.cpp:199-215 write_reduction (final level, orthonormalisation steps). */
+int po_write_log(const char* path, const po_record* recs, int n, int log_every);
+int po_write_reduction(const char* path, const po_record* recs, int n, double e_min);
 
 #ifdef __cplusplus
 }

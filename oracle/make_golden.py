@@ -124,6 +124,36 @@ def gen_solve(name, spec, keep_w=True, threads=1, src_dir=None):
         collect(d)
 
 
+def gen_levels(name, spec, outer_levels, seed):
+    """optimizer.cpp:638-669 solve (initialize_orbitals + refinement levels)."""
+    d_spec = spec.trace_ref_spec(start={"kind": "initialize", "seed": seed})
+    d_spec["params"]["outer_levels"] = outer_levels
+    d_spec["params"]["seed"] = seed
+    with tempfile.TemporaryDirectory() as d:
+        run("levels", d_spec, d)
+        summ = json.load(open(os.path.join(d, "summary.json")))
+        recs = read_records(os.path.join(d, "records.csv"))
+        w = load_bin(os.path.join(d, "final_w.bin"), (spec.n_orbitals, summ["final_points"]))
+    with open(os.path.join(GOLDEN, f"{name}.json"), "w") as f:
+        json.dump({"spec": json.loads(spec.to_json()), "outer_levels": outer_levels, "seed": seed,
+                   "records": recs, "summary": summ}, f, indent=1)
+    np.savez_compressed(os.path.join(GOLDEN, f"{name}_w.npz"), w=w)
+
+
+def gen_prolong(name, spec, start):
+    """initialize_orbitals (start kind "initialize") or a random start, and its
+    refine_uniform + prolongate (grid.cpp:137-212)."""
+    with tempfile.TemporaryDirectory() as d:
+        run("prolong", spec.trace_ref_spec(start=start), d)
+        n = spec.n_orbitals
+        fine = [2 * x + 1 for x in spec.n]
+        u0 = load_bin(os.path.join(d, "u0.bin"), (n, spec.num_points))
+        pr = load_bin(os.path.join(d, "prolong.bin"), (n, fine[0] * fine[1] * fine[2]))
+    np.savez_compressed(os.path.join(GOLDEN, f"{name}.npz"), u0=u0, prolong=pr)
+    with open(os.path.join(GOLDEN, f"{name}.json"), "w") as f:
+        json.dump({"spec": json.loads(spec.to_json()), "start": start}, f, indent=1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true", help="skip the C1/C2 trajectories")
@@ -136,6 +166,11 @@ def main():
     gen_ops("skew", cases()["skew_opt_par"])
     for name, spec in cases().items():
         gen_solve(f"solve_{name}", spec)
+    mol8 = configs.small_molecule(8, 3, L=6.0, max_inner=6)
+    gen_levels("levels_mol8", mol8, 2, 5)
+    gen_prolong("prolong_init_mol8", mol8, {"kind": "initialize", "seed": 5})
+    skew = configs.ProblemSpec("skewp", (6, 5, 7), (4.0, 3.5, 5.0), [(2.0, 1.5, 2.5, 1.0, 1.0)], 2)
+    gen_prolong("prolong_skew", skew, {"kind": "random_orthonormal", "seed": 9})
     if not args.quick:
         for cname, fn in (("C1", configs.config1), ("C2", configs.config2)):
             spec = fn()

@@ -146,6 +146,8 @@ Setup load(const std::string& spec_path) {
   q.mean_abs_tol = p.value("mean_abs_tol", q.mean_abs_tol);
   q.energy_tol = p.value("energy_tol", q.energy_tol);
   q.verify_orthonormality = p.value("verify_orthonormality", q.verify_orthonormality);
+  q.outer_levels = p.value("outer_levels", q.outer_levels);
+  q.seed = p.value("seed", q.seed);
   const std::string bb = p.value("bb_variant", "bb1");
   q.bb_variant = bb == "bb2" ? BbVariant::kBb2 : bb == "alternate" ? BbVariant::kAlternate : BbVariant::kBb1;
   q.bb_trace_abs = p.value("bb_trace_abs", "diag_abs") == "abs_trace" ? BbTraceAbs::kAbsTrace
@@ -289,11 +291,46 @@ int cmd_ops(const Setup& s, const std::string& out) {
   return 0;
 }
 
+// The reference's multi-level solve (optimizer.cpp:638-669) from its own
+// initialize_orbitals(params.seed): records, final orbitals and summary.
+int cmd_levels(const Setup& s, const std::string& out) {
+  Executor ex(s.threads);
+  OptimizerParams q = s.params;
+  q.algorithm = s.algorithm == "opt_par" ? Algorithm::kOptPar
+                : s.algorithm == "optm_qr" ? Algorithm::kOptmQr
+                                           : Algorithm::kOptParMod;
+  SolveResult r = solve(s.problem, q, ex);
+  {
+    std::ofstream f(out + "/records.csv");
+    f << log_header() << '\n';
+    for (const IterationRecord& rec : r.records) f << format_log_row(rec) << '\n';
+  }
+  write_set(out + "/final_w.bin", r.orbitals.orbitals);
+  json sum{{"outcome", outcome_name(r.outcome)},
+           {"message", r.message},
+           {"energy", energy_json(r.energy)},
+           {"iterations_total", r.iterations_total},
+           {"final_grad_norm", r.final_grad_norm},
+           {"final_points", r.orbitals.grid().num_points()}};
+  std::ofstream(out + "/summary.json") << sum.dump(1) << '\n';
+  return 0;
+}
+
+// refine_uniform + prolongate (grid.cpp:137-212) of the start orbitals
+int cmd_prolong(const Setup& s, const std::string& out) {
+  GridPtr fine = refine_uniform(s.u0.grid());
+  FieldSet p;
+  for (const Field& f : s.u0.orbitals) p.push_back(prolongate(f, fine));
+  write_set(out + "/u0.bin", s.u0.orbitals);
+  write_set(out + "/prolong.bin", p);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
   if (argc != 4) {
-    std::fprintf(stderr, "usage: trace_ref solve|ops <spec.json> <outdir>\n");
+    std::fprintf(stderr, "usage: trace_ref solve|ops|levels|prolong <spec.json> <outdir>\n");
     return 1;
   }
   try {
@@ -301,6 +338,8 @@ int main(int argc, char** argv) {
     Setup s = load(argv[2]);
     if (cmd == "solve") return cmd_solve(s, argv[3]);
     if (cmd == "ops") return cmd_ops(s, argv[3]);
+    if (cmd == "levels") return cmd_levels(s, argv[3]);
+    if (cmd == "prolong") return cmd_prolong(s, argv[3]);
     std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
     return 1;
   } catch (const std::exception& e) {

@@ -7,6 +7,8 @@
 // Matrices are row-major in global memory (L2-resident at these sizes).
 #include <math.h>
 
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace po {
@@ -96,8 +98,8 @@ __global__ void __launch_bounds__(DT) cholesky_inv_kernel(int N, const double* _
 // holds L and L^{-1}. Sums run in the same ascending-k order as the global
 // version.
 constexpr int CHOL_SMEM_MAX = 160;
-constexpr int CHT = 256;
 
+template <int CHT>
 __global__ void __launch_bounds__(CHT) cholesky_inv_smem_kernel(int N, const double* __restrict__ G,
                                                                 double* __restrict__ M,
                                                                 double* __restrict__ stats,
@@ -495,12 +497,23 @@ void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, do
   ::po::count_launch();
   if (N <= CHOL_SMEM_MAX) {
     const size_t shm = sizeof(double) * ((size_t)N * (N + 1) + N);
-    static bool attr = false;
-    if (!attr) {
-      set_smem(reinterpret_cast<const void*>(cholesky_inv_smem_kernel), (int)(sizeof(double) * (CHOL_SMEM_MAX * (CHOL_SMEM_MAX + 1) + CHOL_SMEM_MAX)));
-      attr = true;
+    const int amax = (int)(sizeof(double) * (CHOL_SMEM_MAX * (CHOL_SMEM_MAX + 1) + CHOL_SMEM_MAX));
+    static int ct = 0;
+    if (!ct) {
+      const char* e = getenv("PO_CHOL_THREADS");  // measurement override
+      ct = e ? atoi(e) : 0;
     }
-    cholesky_inv_smem_kernel<<<1, CHT, shm, s>>>(N, G, M, stats, guard);
+    const int t = ct ? ct : (N <= 64 ? 64 : 256);
+#define PO_CH(T)                                                                  \
+  if (t == T) {                                                                   \
+    set_smem(reinterpret_cast<const void*>(cholesky_inv_smem_kernel<T>), amax);   \
+    cholesky_inv_smem_kernel<T><<<1, T, shm, s>>>(N, G, M, stats, guard);         \
+    return;                                                                       \
+  }
+    PO_CH(32) PO_CH(64) PO_CH(128) PO_CH(256)
+#undef PO_CH
+    set_smem(reinterpret_cast<const void*>(cholesky_inv_smem_kernel<256>), amax);
+    cholesky_inv_smem_kernel<256><<<1, 256, shm, s>>>(N, G, M, stats, guard);
     return;
   }
   cholesky_inv_kernel<<<1, DT, 0, s>>>(N, G, Lscratch, M, stats, guard);

@@ -242,11 +242,12 @@ __global__ void __launch_bounds__(AW * 32) dst_axis0_kernel(const double* __rest
       const int j = 8 * (wr * RB + a) + gq;
       const int64_t p = p0 + 8 * (wc * CB + b) + 2 * t4;
       if (j < n0) {
-        if (p + 1 < plane) {
-          *reinterpret_cast<double2*>(y + (int64_t)j * plane + p) =
-              make_double2(acc[a][b][0], acc[a][b][1]);
-        } else if (p < plane) {
-          y[(int64_t)j * plane + p] = acc[a][b][0];
+        double* yp = y + (int64_t)j * plane + p;
+        if (p + 1 < plane && (plane & 1) == 0) {  // 16-B aligned only for even planes
+          *reinterpret_cast<double2*>(yp) = make_double2(acc[a][b][0], acc[a][b][1]);
+        } else {
+          if (p < plane) yp[0] = acc[a][b][0];
+          if (p + 1 < plane) yp[1] = acc[a][b][1];
         }
       }
     }

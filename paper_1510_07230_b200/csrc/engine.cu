@@ -562,6 +562,89 @@ int po_random_block(po_engine* h, int block, uint64_t seed) {
   API_CATCH(h)
 }
 
+// optimizer.cpp:156-197: Gaussians at the atoms (cycled; the box centre without
+// atoms), widths and 1e-2 uniform noise from Rng(seed + attempt), orthonormalised
+// (manifold.cpp:171), retried with the next derived seed on a rank-deficient set.
+int po_initialize_orbitals(po_engine* h, const double* atoms, int natoms, uint64_t seed, int w) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  if (natoms < 0 || (natoms > 0 && !atoms)) throw Error(PO_EINVAL, "invalid atom list");
+  if ((int64_t)E.N > E.ng_full)
+    throw Error(PO_EINVAL, "initialize_orbitals: more orbitals than grid points");
+  std::vector<double> centers(3 * (size_t)E.N);
+  for (int i = 0; i < E.N; ++i)
+    for (int d = 0; d < 3; ++d)
+      centers[3 * i + d] = natoms > 0 ? atoms[5 * (i % natoms) + d] : 0.5 * E.ext[d];
+  double* dc = nullptr;
+  double* dw = nullptr;
+  PO_CUDA(cudaMalloc(&dc, sizeof(double) * 3 * E.N));
+  PO_CUDA(cudaMalloc(&dw, sizeof(double) * E.N));
+  PO_CUDA(cudaMemcpy(dc, centers.data(), sizeof(double) * 3 * E.N, cudaMemcpyHostToDevice));
+  std::vector<double> widths(E.N);
+  std::vector<double> noise((size_t)E.N * E.g.ngl);
+  const int raw = E.alloc_block();
+  bool done = false;
+  try {
+    for (int attempt = 0; attempt < 5 && !done; ++attempt) {
+      po::rng_init_noise_slab(seed + (uint64_t)attempt, E.N, E.ng_full, E.g.z0 * E.g.plane,
+                              E.g.ngl, widths.data(), noise.data());
+      PO_CUDA(cudaMemcpyAsync(dw, widths.data(), sizeof(double) * E.N, cudaMemcpyHostToDevice,
+                              E.s));
+      PO_CUDA(cudaMemcpy2DAsync(E.blk(raw), E.g.ld * 8, noise.data(), E.g.ngl * 8, E.g.ngl * 8,
+                                E.N, cudaMemcpyHostToDevice, E.s));
+      po::launch_init_orbitals(E.g, E.N, E.h, dc, dw, E.blk(raw), E.s);
+      E.sync();
+      const int rc = po_orthonormalize(h, raw, w, 1, nullptr, nullptr, nullptr);
+      if (rc == PO_OK) done = true;
+      else if (rc != PO_EDEGENERATE) throw Error(rc, h->err);
+    }
+  } catch (...) {
+    E.free_block(raw);
+    cudaFree(dc);
+    cudaFree(dw);
+    throw;
+  }
+  E.free_block(raw);
+  cudaFree(dc);
+  cudaFree(dw);
+  if (!done) throw Error(PO_EDEGENERATE, "initialize_orbitals: no full-rank start in 5 attempts");
+  API_CATCH(h)
+}
+
+// grid.cpp:137-149
+int po_refine_grid(const po_grid_desc* g, po_grid_desc* fine) {
+  if (!g || !fine) return PO_EINVAL;
+  for (int a = 0; a < 3; ++a) {
+    if (g->n[a] < 1 || g->n[a] > (INT64_MAX - 1) / 2) return PO_EINVAL;
+    fine->n[a] = 2 * g->n[a] + 1;
+    fine->extent[a] = g->extent[a];
+  }
+  return PO_OK;
+}
+
+// grid.cpp:151-203 on every orbital of a block (single-rank engines)
+int po_prolongate(po_engine* coarse, int cblock, po_engine* fine, int fblock) {
+  if (!coarse || !coarse->e || !fine || !fine->e) return PO_EINVAL;
+  Engine& C = *coarse->e;
+  Engine& F = *fine->e;
+  try {
+    if (C.size != 1 || F.size != 1)
+      throw Error(PO_EINVAL, "prolongate: sharded engines are not supported");
+    if (C.N != F.N) throw Error(PO_EINVAL, "prolongate: orbital counts differ");
+    const int64_t nc[3] = {C.g.n0, C.g.n1, C.g.n2}, nf[3] = {F.g.n0, F.g.n1, F.g.n2};
+    for (int a = 0; a < 3; ++a)
+      if (nf[a] != 2 * nc[a] + 1 || F.ext[a] != C.ext[a])
+        throw Error(PO_EINVAL, "prolongate: grids are not in refinement relation");
+    C.sync();
+    po::launch_prolongate(C.N, nc, C.g.ld, C.blk(cblock), nf, F.g.ld, F.blk(fblock), F.s);
+    F.sync();
+  } catch (const Error& ex) {
+    fine->err = ex.what();
+    return ex.code;
+  }
+  return PO_OK;
+}
+
 int po_build_hamiltonian(po_engine* h, int u, int hartree, int xc, double* e_hartree,
                          double* e_xc, int* cg_iters) {
   ENGINE_OR_EINVAL(h);

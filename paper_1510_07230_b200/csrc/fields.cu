@@ -226,7 +226,89 @@ int nblk_for(int64_t work) {
   return (int)b;
 }
 
+// u holds the noise on entry; adds the Gaussian in the reference's operation
+// order (no contraction: r2 and the exponent argument rounded step by step)
+__global__ void __launch_bounds__(PT) init_orbitals_kernel(SlabGeom g, int N, double h0, double h1,
+                                                           double h2,
+                                                           const double* __restrict__ centers,
+                                                           const double* __restrict__ widths,
+                                                           double* __restrict__ u) {
+  const int i = blockIdx.y;
+  const double cx = centers[3 * i], cy = centers[3 * i + 1], cz = centers[3 * i + 2];
+  const double w = widths[i];
+  const double den = __dmul_rn(__dmul_rn(2.0, w), w);
+  double* ui = u + (int64_t)i * g.ld;
+  for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < g.ngl;
+       p += (int64_t)gridDim.x * PT) {
+    const int64_t k2 = p % g.n2;
+    const int64_t k1 = (p / g.n2) % g.n1;
+    const int64_t k0 = p / g.plane + g.z0;
+    const double d0 = __dsub_rn(__dmul_rn((double)(k0 + 1), h0), cx);
+    const double d1 = __dsub_rn(__dmul_rn((double)(k1 + 1), h1), cy);
+    const double d2 = __dsub_rn(__dmul_rn((double)(k2 + 1), h2), cz);
+    double r2 = __dmul_rn(d0, d0);
+    r2 = __dadd_rn(r2, __dmul_rn(d1, d1));
+    r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
+    ui[p] = __dadd_rn(exp(__ddiv_rn(-r2, den)), ui[p]);
+  }
+}
+
+// one coarse line value with the reference's virtual end points (grid.cpp:178-189)
+template <class L>
+__device__ __forceinline__ double pline(int64_t i, int64_t n, L line) {
+  if (i < 0) return n >= 2 ? __dsub_rn(__dmul_rn(2.0, line(0)), line(1)) : line(0);
+  if (i >= n)
+    return n >= 2 ? __dsub_rn(__dmul_rn(2.0, line(n - 1)), line(n - 2)) : line(n - 1);
+  return line(i);
+}
+
+// fine index j of a line of n coarse values (grid.cpp:190-194)
+template <class L>
+__device__ __forceinline__ double pfine(int64_t j, int64_t n, L line) {
+  if (j % 2 == 1) return pline((j - 1) / 2, n, line);
+  return __dmul_rn(0.5, __dadd_rn(pline(j / 2 - 1, n, line), pline(j / 2, n, line)));
+}
+
+// Every fine value is the reference's three passes (axis 0, then 1, then 2)
+// evaluated for that point only: the same operations on the same operands, so
+// the result is bitwise that of prolongate().
+__global__ void __launch_bounds__(PT) prolongate_kernel(int N, int64_t c0, int64_t c1, int64_t c2,
+                                                        int64_t ldc, const double* __restrict__ C,
+                                                        int64_t f0, int64_t f1, int64_t f2,
+                                                        int64_t ldf, double* __restrict__ F) {
+  const int i = blockIdx.y;
+  const double* ci = C + (int64_t)i * ldc;
+  double* fi = F + (int64_t)i * ldf;
+  const int64_t nf = f0 * f1 * f2;
+  for (int64_t q = (int64_t)blockIdx.x * PT + threadIdx.x; q < nf; q += (int64_t)gridDim.x * PT) {
+    const int64_t j2 = q % f2, j1 = (q / f2) % f1, j0 = q / (f1 * f2);
+    fi[q] = pfine(j2, c2, [&](int64_t k2) {
+      return pfine(j1, c1, [&](int64_t k1) {
+        return pfine(j0, c0, [&](int64_t k0) { return ci[(k0 * c1 + k1) * c2 + k2]; });
+      });
+    });
+  }
+}
+
 }  // namespace
+
+void launch_init_orbitals(const SlabGeom& g, int N, const double* h3, const double* centers,
+                          const double* widths, double* u, cudaStream_t s) {
+  dim3 grid(per_orbital_nblk(g, N), N);
+  ::po::count_launch();
+  init_orbitals_kernel<<<grid, PT, 0, s>>>(g, N, h3[0], h3[1], h3[2], centers, widths, u);
+}
+
+void launch_prolongate(int N, const int64_t nc[3], int64_t ldc, const double* C,
+                       const int64_t nf[3], int64_t ldf, double* F, cudaStream_t s) {
+  const int64_t total = nf[0] * nf[1] * nf[2];
+  int64_t b = (total + PT - 1) / PT;
+  if (b > 2048) b = 2048;
+  dim3 grid((unsigned)b, N);
+  ::po::count_launch();
+  prolongate_kernel<<<grid, PT, 0, s>>>(N, nc[0], nc[1], nc[2], ldc, C, nf[0], nf[1], nf[2], ldf,
+                                        F);
+}
 
 int points_nblk(const SlabGeom& g) { return nblk_for(g.ngl); }
 

@@ -198,6 +198,16 @@ struct DstPoisson {
   void release();
   void solve(const double* b, double* x, cudaStream_t s);
 };
+// initialize_orbitals (optimizer.cpp:156-197): u_i = exp(-|x - c_i|^2 / (2 w_i^2)) + noise_i
+// (centers [N][3], widths [N] on the device; noise is a block with stride ld).
+void rng_init_noise_slab(uint64_t seed, int N, int64_t ng_full, int64_t offset, int64_t count,
+                         double* widths, double* noise);
+void launch_init_orbitals(const SlabGeom& g, int N, const double* h3, const double* centers,
+                          const double* widths, double* u, cudaStream_t s);
+// prolongate (grid.cpp:151-203) of every orbital of a block: coarse n_a -> fine 2 n_a + 1,
+// separable linear interpolation with linear extrapolation past the ends, axes 0, 1, 2.
+void launch_prolongate(int N, const int64_t nc[3], int64_t ldc, const double* C,
+                       const int64_t nf[3], int64_t ldf, double* F, cudaStream_t s);
 // three-kernel DST solve (axis-0 GEMM, per-plane shared-memory kernel, axis-0
 // GEMM) for grids up to 128 points per axis; false when unsupported.
 bool dst_fused_supported(int64_t n0, int64_t n1, int64_t n2);

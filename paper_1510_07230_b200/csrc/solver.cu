@@ -247,8 +247,9 @@ struct Solver {
   bool full_grad = false, grad_style = true, mean_abs = false;
   double ngd = 1.0;
 
-  Solver(Engine& e, const po_params& pp, po_result* rr)
-      : E(e), p(pp), r(rr), pool(e), spool(e), nonlinear(pp.hartree || pp.xc) {}
+  Solver(Engine& e, const po_params& pp, po_result* rr, int lvl = 0)
+      : E(e), p(pp), r(rr), pool(e), spool(e), nonlinear(pp.hartree || pp.xc), level(lvl) {}
+  int level = 0;  // outer refinement level (optimizer.cpp:654-664)
 
   double* P(const BRef& b) { return E.blk(*b); }
 
@@ -571,7 +572,7 @@ bool Solver::step() {
     if (spec.on) tau_raw = hv[E.off_scal() + Engine::S_TAU];  // the value the trial used
 
     po_record rec{};
-    rec.level = 0;
+    rec.level = level;
     rec.iter = l;
     rec.grad_norm = grad_norm >= 0.0 ? grad_norm : std::sqrt(std::max(0.0, znorm2));
 
@@ -651,7 +652,7 @@ bool Solver::step() {
         if (++failed_searches > 8) {
           char buf[200];
           std::snprintf(buf, sizeof buf,
-                        "line search stagnated at level %d iteration %d (%d trials, C = %.17g)", 0,
+                        "line search stagnated at level %d iteration %d (%d trials, C = %.17g)", level,
                         l, s, nm_c);
           fail(PO_OUT_STAGNATION, buf);
           finished = true;
@@ -678,7 +679,7 @@ bool Solver::step() {
       nm_c = (p.eta * q_before * c_before + te.total) / nm_q;
       if (r->accepted && r->n_accepted < r->cap) {
         double* a = r->accepted + 9 * (size_t)r->n_accepted;
-        const double v[9] = {0, (double)l, te.total, c_before, nm_c, q_before, nm_q, tau, znorm2};
+        const double v[9] = {(double)level, (double)l, te.total, c_before, nm_c, q_before, nm_q, tau, znorm2};
         std::memcpy(a, v, sizeof v);
       }
       r->n_accepted++;
@@ -789,6 +790,8 @@ void po_default_params(po_params* p) {  // optimizer.hpp:22-46
   p->xc = 1;
   p->trace_sigma_eigs = 0;
   p->poisson_solver = PO_POISSON_DST;
+  p->outer_levels = 1;
+  p->seed = 1;
 }
 
 int po_orthonormalize(po_engine* h, int in, int out, int measure, double* pre_gram,
@@ -826,59 +829,79 @@ int po_orthonormalize(po_engine* h, int in, int out, int measure, double* pre_gr
   return PO_OK;
 }
 
-int po_solve(po_engine* h, const po_params* p, int w_handle, po_result* r) {
-  if (!h || !h->e || !p || !r) return PO_EINVAL;
-  Engine& E = *h->e;
-  const auto t0 = std::chrono::steady_clock::now();
+static void validate_params(const po_params* p) {  // OptimizerParams::validate, optimizer.cpp:43-58
+  if (!(p->rho1 > 0.0)) throw Error(PO_EINVAL, "optimizer: rho1 must be positive");
+  if (!(p->delta > 0.0 && p->delta < 1.0)) throw Error(PO_EINVAL, "optimizer: delta must lie in (0, 1)");
+  if (!(p->eta >= 0.0 && p->eta < 1.0)) throw Error(PO_EINVAL, "optimizer: eta must lie in [0, 1)");
+  if (p->n_diag < 0) throw Error(PO_EINVAL, "optimizer: n_diag must be >= 0 (0 disables)");
+  if (p->n_org < 1) throw Error(PO_EINVAL, "optimizer: n_org must be >= 1");
+  if (p->max_inner < 1) throw Error(PO_EINVAL, "optimizer: max_inner must be >= 1");
+  if (p->max_backtracks < 0) throw Error(PO_EINVAL, "optimizer: max_backtracks must be >= 0");
+  if (!(p->tau_min > 0.0) || !(p->tau_max >= p->tau_min))
+    throw Error(PO_EINVAL, "optimizer: require 0 < tau_min <= tau_max");
+  if (!(p->grad_tol > 0.0)) throw Error(PO_EINVAL, "optimizer: grad_tol must be positive");
+  if (!(p->mean_abs_tol > 0.0)) throw Error(PO_EINVAL, "optimizer: mean_abs_tol must be positive");
+  if (!(p->energy_tol > 0.0)) throw Error(PO_EINVAL, "optimizer: energy_tol must be positive");
+  if (p->outer_levels < 1) throw Error(PO_EINVAL, "optimizer: outer_levels must be >= 1");
+}
+
+static void reset_result(po_result* r) {
   r->n_records = r->n_accepted = 0;
   r->cg_iters_total = 0;
   r->message[0] = 0;
   r->outcome = PO_OUT_MAX_ITERATIONS;
   r->e_kinetic = r->e_external = r->e_hartree = r->e_xc = r->e_total = 0.0;
+  r->final_grad_norm = 0.0;
+}
+
+// One InnerLoop level on block w_handle (iterated in place).
+static void run_level(Engine& E, const po_params* p, int w_handle, po_result* r, int level) {
+  po::Solver S(E, *p, r, level);
+  std::shared_ptr<int> w(new int(w_handle), [](int* q) { delete q; });
+  S.init(w);
+  while (S.step()) {
+  }
+  w = S.w;
+  if (*w != w_handle)
+    PO_CUDA(cudaMemcpyAsync(E.blk(w_handle), E.blk(*w), sizeof(double) * E.N * E.g.ld,
+                            cudaMemcpyDeviceToDevice, E.s));
+  E.sync();
+}
+
+// finalize, optimizer.cpp:581-597: full Stiefel gradient norm at the final iterate
+static void finalize_grad(Engine& E, const po_params* p, int w_handle, po_result* r) {
+  po::Solver S(E, *p, r);
+  std::shared_ptr<int> w(new int(w_handle), [](int* q) { delete q; });
+  po::SRef st = S.make_state(w);
+  po::BRef hw = S.pool.get();
+  E.apply_h(E.blk(*w), E.blk(*hw), st->v_local, false);
+  S.sigma(w, hw);
+  E.mix(E.blk(*w), nullptr, 0.0, E.dmat[4], -1.0, E.blk(*hw), 1.0, 0, nullptr,
+        E.dvec + E.off_dd());
+  E.fetch_all();
+  if (E.hvec[E.off_scal() + Engine::S_SYM + 1] > 1e-10)
+    throw Error(PO_EINVAL, "stiefel_gradient: <(HU)^T U> is not symmetric; inconsistent H or U");
+  double acc = 0.0;
+  for (int i = 0; i < E.N; ++i) acc += E.hvec[E.off_dd() + i];
+  r->final_grad_norm = std::sqrt(std::max(0.0, acc));
+  E.sync();
+}
+
+int po_solve(po_engine* h, const po_params* p, int w_handle, po_result* r) {
+  if (!h || !h->e || !p || !r) return PO_EINVAL;
+  Engine& E = *h->e;
+  const auto t0 = std::chrono::steady_clock::now();
+  reset_result(r);
   try {
-    // OptimizerParams::validate, optimizer.cpp:43-58
-    if (!(p->rho1 > 0.0)) throw Error(PO_EINVAL, "optimizer: rho1 must be positive");
-    if (!(p->delta > 0.0 && p->delta < 1.0)) throw Error(PO_EINVAL, "optimizer: delta must lie in (0, 1)");
-    if (!(p->eta >= 0.0 && p->eta < 1.0)) throw Error(PO_EINVAL, "optimizer: eta must lie in [0, 1)");
-    if (p->n_diag < 0) throw Error(PO_EINVAL, "optimizer: n_diag must be >= 0 (0 disables)");
-    if (p->n_org < 1) throw Error(PO_EINVAL, "optimizer: n_org must be >= 1");
-    if (p->max_inner < 1) throw Error(PO_EINVAL, "optimizer: max_inner must be >= 1");
-    if (p->max_backtracks < 0) throw Error(PO_EINVAL, "optimizer: max_backtracks must be >= 0");
-    if (!(p->tau_min > 0.0) || !(p->tau_max >= p->tau_min))
-      throw Error(PO_EINVAL, "optimizer: require 0 < tau_min <= tau_max");
-    if (!(p->grad_tol > 0.0)) throw Error(PO_EINVAL, "optimizer: grad_tol must be positive");
-    if (!(p->mean_abs_tol > 0.0)) throw Error(PO_EINVAL, "optimizer: mean_abs_tol must be positive");
-    if (!(p->energy_tol > 0.0)) throw Error(PO_EINVAL, "optimizer: energy_tol must be positive");
+    validate_params(p);
     // run_single_level: u0 must be orthonormal (optimizer.cpp:601-603)
     E.gram(E.blk(w_handle), nullptr, 0.0, E.blk(w_handle), nullptr, 0.0, 1, E.dmat[2]);
     po::launch_matrix_stats(E.N, E.dmat[2], E.scal() + Engine::S_MSTAT2, E.s);
     E.fetch(E.off_scal(), 64);
     if (E.hvec[E.off_scal() + Engine::S_MSTAT2] > 1e-8)
       throw Error(PO_EINVAL, "solver: initial orbital set is not orthonormal");
-
-    po::Solver S(E, *p, r);
-    std::shared_ptr<int> w(new int(w_handle), [](int* q) { delete q; });
-    S.init(w);
-    while (S.step()) {
-    }
-    w = S.w;
-    // finalize, optimizer.cpp:581-597: full Stiefel gradient at the final iterate
-    po::SRef st = S.make_state(w);
-    po::BRef hw = S.pool.get();
-    E.apply_h(E.blk(*w), E.blk(*hw), st->v_local, false);
-    S.sigma(w, hw);
-    E.mix(E.blk(*w), nullptr, 0.0, E.dmat[4], -1.0, E.blk(*hw), 1.0, 0, nullptr,
-          E.dvec + E.off_dd());
-    E.fetch_all();
-    if (E.hvec[E.off_scal() + Engine::S_SYM + 1] > 1e-10)
-      throw Error(PO_EINVAL, "stiefel_gradient: <(HU)^T U> is not symmetric; inconsistent H or U");
-    double acc = 0.0;
-    for (int i = 0; i < E.N; ++i) acc += E.hvec[E.off_dd() + i];
-    r->final_grad_norm = std::sqrt(std::max(0.0, acc));
-    if (*w != w_handle)
-      PO_CUDA(cudaMemcpyAsync(E.blk(w_handle), E.blk(*w), sizeof(double) * E.N * E.g.ld,
-                              cudaMemcpyDeviceToDevice, E.s));
-    E.sync();
+    run_level(E, p, w_handle, r, 0);
+    finalize_grad(E, p, w_handle, r);
   } catch (const Error& ex) {
     h->err = ex.what();
     std::snprintf(r->message, sizeof r->message, "%s", ex.what());
@@ -888,6 +911,77 @@ int po_solve(po_engine* h, const po_params* p, int w_handle, po_result* r) {
     return PO_EINVAL;
   }
   r->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return PO_OK;
+}
+
+// optimizer.cpp:638-669 solve: initialize_orbitals on level 0, then per level
+// refine_uniform + prolongate + orthonormalize (level > 0) and one InnerLoop;
+// stops early on stagnation / numerical failure; finalize on the last grid.
+int po_solve_levels(const po_grid_desc* grid0, int n_orbitals, double occupation,
+                    const double* atoms, int natoms, const po_params* p, po_result* r,
+                    po_engine** out_engine, int* out_block) {
+  if (!grid0 || !p || !r || !out_engine || !out_block) return PO_EINVAL;
+  *out_engine = nullptr;
+  *out_block = -1;
+  const auto t0 = std::chrono::steady_clock::now();
+  reset_result(r);
+  po_engine* cur = nullptr;
+  int w = -1;
+  auto fail = [&](int code, const std::string& msg) {
+    std::snprintf(r->message, sizeof r->message, "%s", msg.c_str());
+    if (cur) {
+      cur->err = msg;
+      *out_engine = cur;  // caller reads po_last_error, then po_destroy
+    }
+    return code;
+  };
+  try {
+    validate_params(p);
+    po_grid_desc g = *grid0;
+    int rc = po_create(&g, n_orbitals, occupation, nullptr, &cur);
+    if (rc != PO_OK) return fail(rc, cur ? cur->err : "po_create failed");
+    if ((rc = po_external_potential(cur, atoms, natoms)) != PO_OK) return fail(rc, cur->err);
+    if ((rc = po_alloc_block(cur, &w)) != PO_OK) return fail(rc, cur->err);
+    if ((rc = po_initialize_orbitals(cur, atoms, natoms, p->seed, w)) != PO_OK)
+      return fail(rc, cur->err);
+    for (int level = 0; level < p->outer_levels; ++level) {
+      if (level > 0) {
+        po_grid_desc fg;
+        if ((rc = po_refine_grid(&g, &fg)) != PO_OK) return fail(rc, "refine_uniform: invalid grid");
+        po_engine* fine = nullptr;
+        rc = po_create(&fg, n_orbitals, occupation, nullptr, &fine);
+        if (rc != PO_OK) {
+          const std::string m = fine ? fine->err : "po_create failed";
+          po_destroy(fine);
+          return fail(rc, m);
+        }
+        int fw = -1, raw = -1;
+        if ((rc = po_external_potential(fine, atoms, natoms)) != PO_OK ||
+            (rc = po_alloc_block(fine, &raw)) != PO_OK || (rc = po_alloc_block(fine, &fw)) != PO_OK ||
+            (rc = po_prolongate(cur, w, fine, raw)) != PO_OK ||
+            (rc = po_orthonormalize(fine, raw, fw, 1, nullptr, nullptr, nullptr)) != PO_OK) {
+          const std::string m = fine->err;
+          po_destroy(fine);
+          return fail(rc, m);
+        }
+        po_free_block(fine, raw);
+        po_destroy(cur);
+        cur = fine;
+        w = fw;
+        g = fg;
+      }
+      run_level(*cur->e, p, w, r, level);
+      if (r->outcome == PO_OUT_STAGNATION || r->outcome == PO_OUT_NUMERICAL_FAILURE) break;
+    }
+    finalize_grad(*cur->e, p, w, r);
+  } catch (const Error& ex) {
+    return fail(ex.code, ex.what());
+  } catch (const std::exception& ex) {
+    return fail(PO_EINVAL, ex.what());
+  }
+  r->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *out_engine = cur;
+  *out_block = w;
   return PO_OK;
 }
 

@@ -66,7 +66,8 @@ class Params(C.Structure):
                 ("max_backtracks", C.c_int), ("tau_min", C.c_double), ("tau_max", C.c_double),
                 ("grad_tol", C.c_double), ("mean_abs_tol", C.c_double), ("energy_tol", C.c_double),
                 ("verify_orthonormality", C.c_int), ("hartree", C.c_int), ("xc", C.c_int),
-                ("trace_sigma_eigs", C.c_int), ("poisson_solver", C.c_int)]
+                ("trace_sigma_eigs", C.c_int), ("poisson_solver", C.c_int), ("outer_levels", C.c_int),
+                ("seed", C.c_uint64)]
 
 
 class Record(C.Structure):
@@ -134,6 +135,14 @@ _SIGS = {
     "po_set_matrix": ([C.c_void_p, C.c_void_p], C.c_int),
     "po_nccl_unique_id": ([C.c_void_p], C.c_int),
     "po_set_poisson_solver": ([C.c_void_p, C.c_int], C.c_int),
+    "po_initialize_orbitals": ([C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, C.c_int], C.c_int),
+    "po_refine_grid": ([C.POINTER(GridDesc), C.POINTER(GridDesc)], C.c_int),
+    "po_prolongate": ([C.c_void_p, C.c_int, C.c_void_p, C.c_int], C.c_int),
+    "po_solve_levels": ([C.POINTER(GridDesc), C.c_int, C.c_double, C.c_void_p, C.c_int, C.POINTER(Params),
+                         C.POINTER(Result), C.POINTER(C.c_void_p), C.POINTER(C.c_int)], C.c_int),
+    "po_format_log_row": ([C.POINTER(Record), C.c_char_p, C.c_int], C.c_int),
+    "po_write_log": ([C.c_char_p, C.POINTER(Record), C.c_int, C.c_int], C.c_int),
+    "po_write_reduction": ([C.c_char_p, C.POINTER(Record), C.c_int, C.c_double], C.c_int),
 }
 
 OPS = dict(hamiltonian=0, gram_sym=1, gram=2, mix=3, mix_upper=4, density_xc=5, poisson=6, cholesky=7,
@@ -379,18 +388,18 @@ class Engine:
         rc = self._lib.po_solve(self.h, C.byref(p), w, C.byref(r))
         if rc != PO_OK:
             raise _err(rc, self._lib.po_last_error(self.h).decode() or r.message.decode())
-        nrec = min(r.n_records, cap)
-        records = [dict(level=x.level, iter=x.iter, energy=x.energy, grad_norm=x.grad_norm, tau=x.tau,
-                        backtracks=x.backtracks, did_orth=x.did_orth, did_diag=x.did_diag,
-                        offdiag_max=x.offdiag_max, wall_ms=x.wall_ms) for x in recs[:nrec]]
-        return SolveResult(
-            records=records, accepted=acc[: 9 * min(r.n_accepted, cap)].reshape(-1, 9),
-            sigma_eigs=eigs[: self.N * nrec].reshape(-1, self.N) if trace_eigs else None,
-            outcome=OUTCOMES[r.outcome], message=r.message.decode(),
-            energy=dict(kinetic=r.e_kinetic, external=r.e_external, hartree=r.e_hartree, xc=r.e_xc,
-                        total=r.e_total),
-            final_grad_norm=r.final_grad_norm, cg_iters_total=r.cg_iters_total,
-            wall_seconds=r.wall_seconds)
+        return _solve_result(r, recs, acc, eigs, cap, self.N, trace_eigs)
+
+    # ---- outer refinement (optimizer.cpp:638-669, grid.cpp:137-212)
+    def initialize_orbitals(self, atoms, seed: int, w: int):
+        a = np.ascontiguousarray(np.asarray(atoms, dtype=np.float64).reshape(-1, 5))
+        self._chk(self._lib.po_initialize_orbitals(self.h, _dp(a) if len(a) else None, len(a),
+                                                   C.c_uint64(seed), w))
+
+    def prolongate(self, cblock: int, fine: "Engine", fblock: int):
+        rc = self._lib.po_prolongate(self.h, cblock, fine.h, fblock)
+        if rc != PO_OK:
+            raise _err(rc, self._lib.po_last_error(fine.h).decode())
 
 
 class Stepper:
@@ -475,6 +484,102 @@ class SolveResult:
     cg_iters_total: int
     wall_seconds: float
     extra: dict = field(default_factory=dict)
+
+
+def _solve_result(r, recs, acc, eigs, cap, N, trace_eigs) -> SolveResult:
+    nrec = min(r.n_records, cap)
+    records = [dict(level=x.level, iter=x.iter, energy=x.energy, grad_norm=x.grad_norm, tau=x.tau,
+                    backtracks=x.backtracks, did_orth=x.did_orth, did_diag=x.did_diag,
+                    offdiag_max=x.offdiag_max, wall_ms=x.wall_ms) for x in recs[:nrec]]
+    return SolveResult(
+        records=records, accepted=acc[: 9 * min(r.n_accepted, cap)].reshape(-1, 9),
+        sigma_eigs=eigs[: N * nrec].reshape(-1, N) if trace_eigs else None,
+        outcome=OUTCOMES[r.outcome], message=r.message.decode(),
+        energy=dict(kinetic=r.e_kinetic, external=r.e_external, hartree=r.e_hartree, xc=r.e_xc,
+                    total=r.e_total),
+        final_grad_norm=r.final_grad_norm, cg_iters_total=r.cg_iters_total,
+        wall_seconds=r.wall_seconds)
+
+
+def refine_grid(n, extent):
+    """grid.cpp:137-149 refine_uniform."""
+    g = GridDesc((C.c_int64 * 3)(*[int(x) for x in n]), (C.c_double * 3)(*[float(x) for x in extent]))
+    f = GridDesc()
+    rc = lib().po_refine_grid(C.byref(g), C.byref(f))
+    if rc != PO_OK:
+        raise _err(rc, "refine_uniform: invalid grid")
+    return tuple(f.n), tuple(f.extent)
+
+
+def solve_levels(spec, outer_levels: int, seed: int, algorithm="opt_par_mod", poisson="dst",
+                 **over):
+    """optimizer.cpp:638-669 solve on the GPU: returns (SolveResult, final Engine, block)."""
+    L = lib()
+    p = Engine.make_params(algorithm, spec.hartree, spec.xc, False, poisson, **over)
+    p.outer_levels, p.seed = int(outer_levels), int(seed)
+    cap = outer_levels * p.max_inner + 1
+    recs = (Record * cap)()
+    acc = np.zeros(cap * 9)
+    eigs = np.zeros(1)
+    r = Result()
+    r.cap = cap
+    r.records = recs
+    r.accepted = acc.ctypes.data_as(C.POINTER(C.c_double))
+    r.sigma_eigs = C.POINTER(C.c_double)()
+    g = GridDesc((C.c_int64 * 3)(*[int(x) for x in spec.n]),
+                 (C.c_double * 3)(*[float(x) for x in spec.extent]))
+    atoms = np.ascontiguousarray(np.asarray(spec.atoms, dtype=np.float64).reshape(-1, 5))
+    h, blk = C.c_void_p(), C.c_int()
+    rc = L.po_solve_levels(C.byref(g), spec.n_orbitals, float(spec.occupation),
+                           _dp(atoms) if len(atoms) else None, len(atoms), C.byref(p), C.byref(r),
+                           C.byref(h), C.byref(blk))
+    if rc != PO_OK:
+        msg = L.po_last_error(h).decode() if h else r.message.decode()
+        if h:
+            L.po_destroy(h)
+        raise _err(rc, msg or r.message.decode())
+    n = list(spec.n)
+    for _ in range(outer_levels - 1):
+        n = [2 * x + 1 for x in n]
+    e = Engine.__new__(Engine)
+    e._lib, e.h, e._keep = L, h, None
+    e.n, e.extent, e.N, e.occupation = tuple(n), tuple(spec.extent), spec.n_orbitals, spec.occupation
+    z0, nz, ngl = C.c_int64(), C.c_int64(), C.c_int64()
+    L.po_local_slab(h, C.byref(z0), C.byref(nz), C.byref(ngl))
+    e.z0, e.nz, e.ngl = z0.value, nz.value, ngl.value
+    return _solve_result(r, recs, acc, eigs, cap, spec.n_orbitals, False), e, blk.value
+
+
+def _records_array(records):
+    arr = (Record * len(records))()
+    for k, x in enumerate(records):
+        arr[k] = Record(x["level"], x["iter"], x["energy"], x["grad_norm"], x["tau"], x["backtracks"],
+                        x["did_orth"], x["did_diag"], x["offdiag_max"], x["wall_ms"])
+    return arr
+
+
+def format_log_row(rec: dict) -> str:
+    """driver.cpp:136-142 through the C ABI."""
+    arr = _records_array([rec])
+    buf = C.create_string_buffer(320)
+    n = lib().po_format_log_row(arr, buf, 320)
+    if n < 0:
+        raise InvalidArgument("format_log_row: buffer too small")
+    return buf.value.decode()
+
+
+def write_log(path: str, records: list, log_every: int = 1):
+    arr = _records_array(records)
+    rc = lib().po_write_log(path.encode(), arr, len(records), int(log_every))
+    if rc != PO_OK:
+        raise _err(rc, f"cannot write {path}")
+
+
+def write_reduction(path: str, records: list, e_min: float):
+    arr = _records_array(records)
+    rc = lib().po_write_reduction(path.encode(), arr, len(records), float(e_min))
+    if rc != PO_OK:
+        raise _err(rc, f"cannot write {path}")
 
 
 def default_params() -> Params:

@@ -103,10 +103,11 @@ def test_poisson_modes(setup, port, native, mode):
         assert iters > 0
 
 
-def test_poisson_closed_form(native):
+@pytest.mark.parametrize("n", [(15, 12, 10), (9, 7, 13)])  # even / odd plane sizes
+def test_poisson_closed_form(native, n):
     """KAT after test_energy.cpp:229-286: rho = sin-mode product has the exact
     discrete solution v = 4 pi rho / lambda (relative error <= 1e-8)."""
-    n, L = (15, 12, 10), (6.0, 5.0, 4.0)
+    L = (6.0, 5.0, 4.0)
     spec = configs.ProblemSpec("kat", n, L, [], 1)
     e = native.engine_for(spec)
     h = [L[a] / (n[a] + 1) for a in range(3)]
