@@ -20,6 +20,7 @@ int main(int argc, char** argv) {
   const int n = argc > 1 ? std::atoi(argv[1]) : 16;
   const int norb = argc > 2 ? std::atoi(argv[2]) : 4;
   const int iters = argc > 3 ? std::atoi(argv[3]) : 12;
+  const int levels = argc > 4 ? std::atoi(argv[4]) : 1;  // > 1: the multi-level solve()
   const double L = n >= 64 ? 20.0 : 8.0;
   const double ext[] = {L, L, L};
   const std::int64_t pts[] = {n, n, n};
@@ -34,15 +35,18 @@ int main(int argc, char** argv) {
   OrbitalSet u0 = testing::random_orthonormal(g, norb, 42);
   OptimizerParams params;
   params.max_inner = iters;
-  SolveResult cpu = opt_par_mod_inner(u0, p, params);
-  SolveResult gpu = gpu::opt_par_mod_inner(u0, p, params);
+  params.outer_levels = levels;
+  params.seed = 7;
+  Executor ex(1);
+  SolveResult cpu = levels > 1 ? solve(p, params, ex) : opt_par_mod_inner(u0, p, params, ex);
+  SolveResult gpu = levels > 1 ? gpu::solve(p, params) : gpu::opt_par_mod_inner(u0, p, params);
   double worst = 0.0;
   const std::size_t m = std::min(cpu.records.size(), gpu.records.size());
   for (std::size_t k = 0; k < m; ++k) {
     const double d = std::abs(cpu.records[k].energy - gpu.records[k].energy);
     worst = std::max(worst, d);
-    std::printf("iter %3d  E_ref % .15f  E_gpu % .15f  |dE| %.2e  backtracks %d/%d\n",
-                cpu.records[k].iter, cpu.records[k].energy, gpu.records[k].energy, d,
+    std::printf("level %d iter %3d  E_ref % .15f  E_gpu % .15f  |dE| %.2e  backtracks %d/%d\n",
+                cpu.records[k].level, cpu.records[k].iter, cpu.records[k].energy, gpu.records[k].energy, d,
                 cpu.records[k].backtracks, gpu.records[k].backtracks);
   }
   const bool ok = cpu.records.size() == gpu.records.size() && worst < 1e-6 &&

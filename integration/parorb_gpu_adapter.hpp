@@ -67,7 +67,31 @@ inline po_params to_params(const OptimizerParams& p, Algorithm alg, const Proble
   q.verify_orthonormality = p.verify_orthonormality ? 1 : 0;
   q.hartree = prob.hartree_enabled ? 1 : 0;
   q.xc = prob.xc_enabled ? 1 : 0;
+  q.outer_levels = p.outer_levels;
+  q.seed = p.seed;
   return q;
+}
+
+// po_result -> the reference's SolveResult fields (optimizer.hpp:98-112)
+inline void fill_result(SolveResult& out, const po_result& r, const std::vector<po_record>& recs,
+                        const std::vector<double>& acc) {
+  out.energy = EnergyBreakdown{r.e_kinetic, r.e_external, r.e_hartree, r.e_xc, r.e_total};
+  out.outcome = static_cast<SolveOutcome>(r.outcome);  // same enumerator order
+  out.message = r.message;
+  for (int k = 0; k < r.n_records && k < r.cap; ++k) {
+    const po_record& x = recs[k];
+    out.records.push_back(IterationRecord{x.level, x.iter, x.energy, x.grad_norm, x.tau,
+                                          x.backtracks, x.did_orth != 0, x.did_diag != 0,
+                                          x.offdiag_max, x.wall_ms});
+  }
+  for (int k = 0; k < r.n_accepted && k < r.cap; ++k) {
+    const double* a = acc.data() + 9 * k;
+    out.accepted_steps.push_back(AcceptedStep{static_cast<int>(a[0]), static_cast<int>(a[1]), a[2],
+                                              a[3], a[4], a[5], a[6], a[7], a[8]});
+  }
+  out.iterations_total = static_cast<int>(out.records.size());
+  out.final_grad_norm = r.final_grad_norm;
+  out.wall_seconds = r.wall_seconds;
 }
 
 inline SolveResult run(const OrbitalSet& u0, const Problem& prob, const OptimizerParams& params,
@@ -111,23 +135,7 @@ inline SolveResult run(const OrbitalSet& u0, const Problem& prob, const Optimize
     fields.push_back(std::move(f));
   }
   out.orbitals = OrbitalSet{std::move(fields)};
-  out.energy = EnergyBreakdown{r.e_kinetic, r.e_external, r.e_hartree, r.e_xc, r.e_total};
-  out.outcome = static_cast<SolveOutcome>(r.outcome);  // same enumerator order
-  out.message = r.message;
-  for (int k = 0; k < r.n_records && k < r.cap; ++k) {
-    const po_record& x = recs[k];
-    out.records.push_back(IterationRecord{x.level, x.iter, x.energy, x.grad_norm, x.tau,
-                                          x.backtracks, x.did_orth != 0, x.did_diag != 0,
-                                          x.offdiag_max, x.wall_ms});
-  }
-  for (int k = 0; k < r.n_accepted && k < r.cap; ++k) {
-    const double* a = acc.data() + 9 * k;
-    out.accepted_steps.push_back(AcceptedStep{static_cast<int>(a[0]), static_cast<int>(a[1]), a[2],
-                                              a[3], a[4], a[5], a[6], a[7], a[8]});
-  }
-  out.iterations_total = static_cast<int>(out.records.size());
-  out.final_grad_norm = r.final_grad_norm;
-  out.wall_seconds = r.wall_seconds;
+  fill_result(out, r, recs, acc);
   return out;
 }
 
@@ -143,6 +151,52 @@ inline SolveResult opt_par_inner(const OrbitalSet& u0, const Problem& p, const O
 inline SolveResult opt_par_mod_inner(const OrbitalSet& u0, const Problem& p,
                                      const OptimizerParams& q) {
   return detail::run(u0, p, q, Algorithm::kOptParMod);
+}
+
+// Drop-in for optimizer.hpp:163-167 solve (initialize_orbitals + outer levels).
+inline SolveResult solve(const Problem& level0, const OptimizerParams& params) {
+  params.validate();
+  const Grid& g = *level0.grid;
+  if (g.dimension() != 3) throw InvalidArgument("parorb_gpu: 3D grids only");
+  po_grid_desc gd;
+  for (int a = 0; a < 3; ++a) {
+    gd.n[a] = g.points(a);
+    gd.extent[a] = g.extent(a);
+  }
+  std::vector<double> atoms;
+  for (const Atom& at : level0.atoms) {
+    atoms.insert(atoms.end(), {at.position[0], at.position[1], at.position[2], at.charge,
+                               at.softening});
+  }
+  const po_params q = detail::to_params(params, params.algorithm, level0);
+  std::vector<po_record> recs(static_cast<std::size_t>(q.max_inner) * q.outer_levels + 1);
+  std::vector<double> acc(9 * recs.size());
+  po_result r{};
+  r.cap = static_cast<int>(recs.size());
+  r.records = recs.data();
+  r.accepted = acc.data();
+  po_engine* raw = nullptr;
+  int w = -1;
+  const int rc = po_solve_levels(&gd, level0.n_orbitals, 1.0, atoms.data(),
+                                 static_cast<int>(level0.atoms.size()), &q, &r, &raw, &w);
+  std::unique_ptr<po_engine, detail::EngineDeleter> e(raw);
+  detail::check(rc, raw);
+  // the final grid: refine_uniform applied outer_levels - 1 times (grid.cpp:137-149)
+  GridPtr grid = level0.grid;
+  for (int l = 1; l < params.outer_levels; ++l) grid = refine_uniform(*grid);
+  const std::int64_t ng = grid->num_points();
+  std::vector<double> host(static_cast<std::size_t>(level0.n_orbitals * ng));
+  detail::check(po_download_block(raw, w, host.data()), raw);
+  SolveResult out;
+  std::vector<Field> fields;
+  for (int i = 0; i < level0.n_orbitals; ++i) {
+    Field f = make_field(grid);
+    std::memcpy(f.values.data(), host.data() + i * ng, sizeof(double) * ng);
+    fields.push_back(std::move(f));
+  }
+  out.orbitals = OrbitalSet{std::move(fields)};
+  detail::fill_result(out, r, recs, acc);
+  return out;
 }
 
 }  // namespace parorb::gpu

@@ -12,7 +12,7 @@ DEMO = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
 
 
 @pytest.mark.skipif(not os.path.exists(DEMO), reason="dropin_demo is built only where /root/reference exists")
-@pytest.mark.parametrize("args", [("16", "4", "12"), ("24", "6", "10")])
+@pytest.mark.parametrize("args", [("16", "4", "12"), ("24", "6", "10"), ("9", "4", "6", "2")])
 def test_reference_api_dropin(args):
     r = subprocess.run([DEMO, *args], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
