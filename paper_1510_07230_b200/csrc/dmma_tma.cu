@@ -637,11 +637,17 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
 #pragma unroll
       for (int fi = 0; fi < F; ++fi)
         mreg[ks][fi] = 4 * ks > 8 * fi + 7 ? 0.0 : Ms[(4 * ks + t4) * NPAD + 8 * fi + gq];
+    // V_ext of the next chunk is requested one stage ahead (a global load in
+    // the epilogue stalled every warp for its full latency)
+    double vx_next = (vext && t4 == 0 && pbeg + c + gq < ngl) ? __ldg(vext + pbeg + c + gq) : 0.0;
     for (int st = 0; st < nstage; ++st) {
       const int s = st % nst;
+      const int64_t p = pbeg + (int64_t)st * TKS + c + gq;
+      const double vx = vx_next;
+      const int64_t pn = p + TKS;
+      if (vext && t4 == 0 && st + 1 < nstage && pn < ngl) vx_next = __ldg(vext + pn);
       mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
       double* sbuf = stage0 + (size_t)s * sdoubles;
-      const int64_t p = pbeg + (int64_t)st * TKS + c + gq;
       double acc[F][2];
 #pragma unroll
       for (int f = 0; f < F; ++f) acc[f][0] = acc[f][1] = 0.0;
@@ -692,7 +698,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
           vxc[p] = 0.0;
         }
         if (bvec) bvec[p] = r * four_pi;
-        if (vext) eacc[1] += __ldg(vext + p) * r;
+        if (vext) eacc[1] += vx * r;
       }
       __syncwarp();  // rotated chunk visible to the whole warp
       if constexpr (R > 0) {
