@@ -121,13 +121,18 @@ __global__ void __launch_bounds__(CHT) cholesky_inv_smem_kernel(int N, const dou
       sq = warp_sum(sq);
       if (lane == 0) {
         const double d = A[j * ls + j] - sq;
-        if (!(d > 0.0)) fail = 1;
-        else A[j * ls + j] = sqrt(d);
+        if (!(d > 0.0)) {
+          fail = 1;
+        } else {
+          const double l = sqrt(d);
+          A[j * ls + j] = l;
+          xd[j] = 1.0 / l;  // one division per column, off the row updates' path
+        }
       }
     }
     __syncthreads();
     if (fail) break;
-    const double ljj = A[j * ls + j];
+    const double rjj = xd[j];
     for (int i = j + 1 + t; i < N; i += CHT) {
       // four interleaved partial sums: the loads pipeline instead of one
       // dependent FMA chain of length j
@@ -142,7 +147,7 @@ __global__ void __launch_bounds__(CHT) cholesky_inv_smem_kernel(int N, const dou
         p3 += ai[k + 3] * aj[k + 3];
       }
       for (; k < j; ++k) p0 += ai[k] * aj[k];
-      A[i * ls + j] = (A[i * ls + j] - ((p0 + p1) + (p2 + p3))) / ljj;
+      A[i * ls + j] = (A[i * ls + j] - ((p0 + p1) + (p2 + p3))) * rjj;
     }
     __syncthreads();
   }
@@ -168,8 +173,7 @@ __global__ void __launch_bounds__(CHT) cholesky_inv_smem_kernel(int N, const dou
     stats[2] = (pmax / pmin) * (pmax / pmin);
     stats[3] = ok ? 1.0 : 0.0;
   }
-  for (int i = t; i < N; i += CHT) xd[i] = 1.0 / A[i * ls + i];
-  __syncthreads();
+  __syncthreads();  // xd[i] = 1 / L(i, i) from the factorisation
   // column c of X: X(c,c) = 1/L(c,c); X(i,c) = -(sum_{k=c}^{i-1} L(i,k) X(k,c)) / L(i,i)
   for (int c = t; c < N; c += CHT) {
     const double* xc = A + c * ls;  // X(k, c) for k > c lives at A[c][k]
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(CHT) cholesky_inv_smem_kernel(int N, const dou
         p3 += li[k + 3] * xc[k + 3];
       }
       for (; k < i; ++k) p0 += li[k] * xc[k];
-      A[c * ls + i] = -((p0 + p1) + (p2 + p3)) / li[i];
+      A[c * ls + i] = -((p0 + p1) + (p2 + p3)) * xd[i];
     }
   }
   __syncthreads();
@@ -192,6 +196,121 @@ __global__ void __launch_bounds__(CHT) cholesky_inv_smem_kernel(int N, const dou
   for (int e = t; e < N * N; e += CHT) {
     const int k = e / N, i = e % N;
     M[e] = i > k ? A[k * ls + i] : (i == k ? xd[k] : 0.0);
+  }
+}
+
+// Register-resident variant for N <= 32 (C1's orbital count): one warp,
+// lane l holds rows l and l + 32 of the matrix in registers (loops unrolled to
+// NM so every index is static); column broadcasts are warp shuffles, so the
+// factorisation has no shared-memory round trips and no barriers on its
+// critical path. L then goes to shared memory for the forward substitution
+// (lane c owns column c of L^{-1}, in registers). Same pivot tests and stats.
+template <int NM>
+__global__ void __launch_bounds__(32) cholesky_inv_reg_kernel(int N, const double* __restrict__ G,
+                                                              double* __restrict__ M,
+                                                              double* __restrict__ stats,
+                                                              const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;
+  constexpr int R = NM > 32 ? 2 : 1;
+  __shared__ double Ls[NM][NM + 1];
+  __shared__ double xd[NM];
+  const int lane = threadIdx.x;
+  double a[R][NM];
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    const int row = lane + 32 * h;
+#pragma unroll
+    for (int k = 0; k < NM; ++k) a[h][k] = (row < N && k < N) ? G[row * N + k] : 0.0;
+  }
+  bool fail = false;
+#pragma unroll
+  for (int j = 0; j < NM; ++j) {
+    if (j < N && !fail) {
+      const double d = __shfl_sync(0xffffffffu, a[j >> 5][j], j & 31);
+      if (!(d > 0.0)) {
+        fail = true;
+      } else {
+        const double l = sqrt(d), r = 1.0 / l;
+        if (lane == 0) xd[j] = r;
+#pragma unroll
+        for (int h = 0; h < R; ++h) {
+          const int row = lane + 32 * h;
+          if (row == j) a[h][j] = l;
+          else if (row > j) a[h][j] *= r;  // L(row, j)
+        }
+        // trailing update A(row, k) -= L(row, j) L(k, j), j < k <= row
+#pragma unroll
+        for (int k = j + 1; k < NM; ++k) {
+          if (k < N) {
+            const double lkj = __shfl_sync(0xffffffffu, a[k >> 5][j], k & 31);
+#pragma unroll
+            for (int h = 0; h < R; ++h)
+              if (lane + 32 * h >= k) a[h][k] -= a[h][j] * lkj;
+          }
+        }
+      }
+    }
+  }
+  if (fail) {
+    if (lane == 0) {
+      stats[0] = 0.0;
+      stats[1] = 0.0;
+      stats[2] = INFINITY;
+      stats[3] = 0.0;
+    }
+    return;
+  }
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    const int row = lane + 32 * h;
+    if (row < NM) {
+#pragma unroll
+      for (int k = 0; k < NM; ++k) Ls[row][k] = k <= row ? a[h][k] : 0.0;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double pmin = Ls[0][0], pmax = Ls[0][0];
+    for (int i = 1; i < N; ++i) {
+      const double v = Ls[i][i];
+      pmin = v < pmin ? v : pmin;
+      pmax = v > pmax ? v : pmax;
+    }
+    const bool ok = (pmin > 0.0) && isfinite(pmax) && !(pmin * pmin < 1e-10 * pmax * pmax);
+    stats[0] = pmin;
+    stats[1] = pmax;
+    stats[2] = (pmax / pmin) * (pmax / pmin);
+    stats[3] = ok ? 1.0 : 0.0;
+  }
+  // column c = lane + 32h of X = L^{-1}: X(c,c) = 1/L(c,c),
+  // X(i,c) = -(sum_{k=c}^{i-1} L(i,k) X(k,c)) / L(i,i) (zero above the diagonal)
+  double x[R][NM];
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    const int c = lane + 32 * h;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) {
+      if (i < c || i >= N) {
+        x[h][i] = 0.0;
+      } else if (i == c) {
+        x[h][i] = xd[i];
+      } else {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < i; ++k) acc += Ls[i][k] * x[h][k];  // x[h][k] = 0 for k < c
+        x[h][i] = -acc * xd[i];
+      }
+    }
+  }
+  // M(k, i) = X(i, k): row c of M is column c of X
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    const int c = lane + 32 * h;
+    if (c < N) {
+#pragma unroll
+      for (int i = 0; i < NM; ++i)
+        if (i < N) M[c * N + i] = x[h][i];
+    }
   }
 }
 
@@ -495,6 +614,19 @@ void launch_copy_guarded(double* dst, const double* src, int64_t n, const double
 void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, double* stats,
                          cudaStream_t s, const double* guard) {
   ::po::count_launch();
+  // measured (tools/kbench-style, one launch): register kernel 6 / 12 / 29 us at
+  // N = 5 / 16 / 32; at N = 33 its second register row spills and the
+  // shared-memory kernel (47 us) wins; shared memory up to N = 160
+  if (N <= 32) {
+    switch ((N + 7) / 8) {
+#define PO_CR(F)                                                                           \
+  case F:                                                                                  \
+    cholesky_inv_reg_kernel<8 * F><<<1, 32, 0, s>>>(N, G, M, stats, guard);                \
+    return;
+      PO_CR(1) PO_CR(2) PO_CR(3) PO_CR(4)
+#undef PO_CR
+    }
+  }
   if (N <= CHOL_SMEM_MAX) {
     const size_t shm = sizeof(double) * ((size_t)N * (N + 1) + N);
     const int amax = (int)(sizeof(double) * (CHOL_SMEM_MAX * (CHOL_SMEM_MAX + 1) + CHOL_SMEM_MAX));
@@ -503,7 +635,7 @@ void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, do
       const char* e = getenv("PO_CHOL_THREADS");  // measurement override
       ct = e ? atoi(e) : 0;
     }
-    const int t = ct ? ct : (N <= 64 ? 64 : 256);
+    const int t = ct ? ct : (N <= 64 ? 32 : 256);
 #define PO_CH(T)                                                                  \
   if (t == T) {                                                                   \
     set_smem(reinterpret_cast<const void*>(cholesky_inv_smem_kernel<T>), amax);   \

@@ -11,6 +11,7 @@
 // lives in shared memory with a row stride of (n8 + 4) doubles, which keeps
 // both fragment shapes (8 rows x 4 k, 4 k x 8 cols) bank-conflict free.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -186,9 +187,8 @@ __global__ void __launch_bounds__(PW * 32) dst_plane_kernel(double* __restrict__
 }
 
 // y[j][p] = sum_k S0[j][k] x[k][p] over a 32-point column tile of the planes
-constexpr int A0P = 32;
 constexpr int AW = 8;
-template <int NF, bool SG>
+template <int NF, bool SG, int A0P>
 __global__ void __launch_bounds__(AW * 32) dst_axis0_kernel(const double* __restrict__ x,
                                                             double* __restrict__ y, int n0,
                                                             int64_t plane,
@@ -255,30 +255,47 @@ __global__ void __launch_bounds__(AW * 32) dst_axis0_kernel(const double* __rest
 
 constexpr size_t kSmemMax = 227 * 1024;
 
-template <int NF>
-void launch_fused(const DstPoisson& d, const double* b, double* x, cudaStream_t s) {
+template <int NF, int A0P, bool ASG>
+void launch_axis0(const DstPoisson& d, const double* x, double* y, cudaStream_t s) {
   const int64_t plane = d.n1 * d.n2;
   const int n80 = 8 * (int)((d.n0 + 7) / 8);
+  const size_t sh0 = sizeof(double) * n80 * (A0P + 4) + (ASG ? 0 : sizeof(double) * n80 * (n80 + 4));
+  auto ka = dst_axis0_kernel<NF, ASG, A0P>;
+  set_smem(reinterpret_cast<const void*>(ka), (int)sh0);
+  ::po::count_launch();
+  ka<<<(unsigned)((plane + A0P - 1) / A0P), AW * 32, sh0, s>>>(x, y, (int)d.n0, plane, d.S[0]);
+}
+
+template <int NF>
+void launch_axis0_pick(const DstPoisson& d, const double* x, double* y, cudaStream_t s) {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* e = getenv("PO_DST_A0");  // measurement override: 0..5
+    cfg = e ? atoi(e) : 2;  // measured best at 96^3: 32-point tiles, S0 through L1
+  }
+  switch (cfg) {
+    case 0: launch_axis0<NF, 32, false>(d, x, y, s); break;
+    case 2: launch_axis0<NF, 32, true>(d, x, y, s); break;
+    case 3: launch_axis0<NF, 64, true>(d, x, y, s); break;
+    case 4: launch_axis0<NF, 128, false>(d, x, y, s); break;
+    case 5: launch_axis0<NF, 128, true>(d, x, y, s); break;
+    default: launch_axis0<NF, 64, false>(d, x, y, s); break;
+  }
+}
+
+template <int NF>
+void launch_fused(const DstPoisson& d, const double* b, double* x, cudaStream_t s) {
   const int n8 = 8 * (int)((std::max(d.n1, d.n2) + 7) / 8);
-  const size_t x0 = sizeof(double) * n80 * (A0P + 4);
-  const size_t s0 = sizeof(double) * n80 * (n80 + 4);
-  const bool a_sg = x0 + s0 > kSmemMax / 2;  // keep two axis-0 CTAs per SM
-  const size_t sh0 = a_sg ? x0 : x0 + s0;
   const size_t pl = sizeof(double) * n8 * (n8 + 4);
   const bool p_sg = d.n1 != d.n2 || 2 * pl > kSmemMax;
   const size_t sh1 = p_sg ? pl : 2 * pl;
-  auto ka = a_sg ? dst_axis0_kernel<NF, true> : dst_axis0_kernel<NF, false>;
   auto kp = p_sg ? dst_plane_kernel<NF, true> : dst_plane_kernel<NF, false>;
-  set_smem(reinterpret_cast<const void*>(ka), (int)(sh0));
-  set_smem(reinterpret_cast<const void*>(kp), (int)(sh1));
-  const unsigned g0 = (unsigned)((plane + A0P - 1) / A0P);
-  ::po::count_launch();
-  ka<<<g0, AW * 32, sh0, s>>>(b, d.t0, (int)d.n0, plane, d.S[0]);
+  set_smem(reinterpret_cast<const void*>(kp), (int)sh1);
+  launch_axis0_pick<NF>(d, b, d.t0, s);
   ::po::count_launch();
   kp<<<(unsigned)d.n0, PW * 32, sh1, s>>>(d.t0, (int)d.n0, (int)d.n1, (int)d.n2, d.S[1], d.S[2],
                                           d.lam, d.norm);
-  ::po::count_launch();
-  ka<<<g0, AW * 32, sh0, s>>>(d.t0, x, (int)d.n0, plane, d.S[0]);
+  launch_axis0_pick<NF>(d, d.t0, x, s);
 }
 
 }  // namespace
