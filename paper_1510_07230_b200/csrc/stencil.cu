@@ -393,49 +393,66 @@ __global__ void __launch_bounds__(32 * (TYR + 1), 1) hamiltonian4_kernel(
     return;
   }
   // ------------------------------------------------------------------ consumers
+  // (ring slots and phases advance incrementally and all in-slot offsets are
+  // 32-bit: the per-plane index arithmetic — runtime modulo by nst — used to
+  // outweigh the stencil math; ncu showed the kernel issue-bound at 71%)
   const int64_t y = y0 + warp;
   const bool yin = y < n1;
   const double ih0 = g.ih2[0], ih1 = g.ih2[1], ih2 = g.ih2[2];
-  double* oi = out ? out + (int64_t)i * g.ld : nullptr;
+  const int n2i = (int)n2;
+  const int slot_stride = (int)(urow + vrow);
+  const int rrow = (warp + 1) * n2i;           // slot row of y
+  const int vrow_off = (int)urow + warp * n2i;  // v_local row of y
   double acc[3] = {0.0, 0.0, 0.0};
-  auto slot = [&](int k) { return ring + (int64_t)(k % nst) * (urow + vrow); };
-  auto real_k = [&](int k) { return ring_plane_real(zs - 1 + k, g.nz, halo_lo, halo_hi); };
   // planes k = 0 (zs-1) and 1 (zs) before the first step
   mbar_wait(&full[0], 0);
   mbar_wait(&full[1 % nst], (uint32_t)(1 / nst) & 1u);
+  int sm = 0, sc = 1 % nst, sp = 2 % nst;  // slots of planes k-1, k, k+1
+  uint32_t php = (uint32_t)(2 / nst) & 1u;   // phase of plane k+1's slot
+  bool rm = ring_plane_real(zs - 1, g.nz, halo_lo, halo_hi), rc = true;
+  double* orow = (out && yin) ? out + (int64_t)i * g.ld + zs * plane + y * n2 : nullptr;
+  const double* xrow = (EXT && yin) ? vext + zs * plane + y * n2 : nullptr;
   for (int k = 1; k + 1 < nplanes; ++k) {  // step on plane z = zs - 1 + k
-    const int kn = k + 1;
-    mbar_wait(&full[kn % nst], (uint32_t)(kn / nst) & 1u);
-    const double* pm = slot(k - 1);
-    const double* pc = slot(k);
-    const double* pp = slot(kn);
-    const bool rm = real_k(k - 1), rp = real_k(kn);
-    const int64_t z = zs - 1 + k;
+    mbar_wait(&full[sp], php);
+    const double* pm = ring + sm * slot_stride;
+    const double* pc = ring + sc * slot_stride;
+    const double* pp = ring + sp * slot_stride;
+    const bool rp = ring_plane_real(zs + k, g.nz, halo_lo, halo_hi);
     if (yin) {
 #pragma unroll
       for (int j = 0; j < J; ++j) {
-        const int64_t x = lane + 32 * j;
-        if (x < n2) {
-          const int64_t r = (warp + 1) * n2 + x;  // slot row of y
+        const int x = lane + 32 * j;
+        if (x < n2i) {
+          const int r = rrow + x;
           const double c = pc[r];
           const double zm = rm ? pm[r] : 0.0;
           const double zp = rp ? pp[r] : 0.0;
-          const double ym = pc[r - n2];  // zero rows outside the box
-          const double yp = pc[r + n2];
+          const double ym = pc[r - n2i];  // zero rows outside the box
+          const double yp = pc[r + n2i];
           const double xm = x > 0 ? pc[r - 1] : 0.0;
-          const double xp = x + 1 < n2 ? pc[r + 1] : 0.0;
+          const double xp = x + 1 < n2i ? pc[r + 1] : 0.0;
           const double lap = ((zm - 2.0 * c + zp) * ih0 + (ym - 2.0 * c + yp) * ih1) +
                              (xm - 2.0 * c + xp) * ih2;
-          const double h = -0.5 * lap + pc[urow + warp * n2 + x] * c;
-          if (oi) oi[z * plane + y * n2 + x] = h;
+          const double h = -0.5 * lap + pc[vrow_off + x] * c;
+          if (orow) orow[x] = h;
           acc[0] += h * c;
           acc[1] += lap * c;
-          if (EXT) acc[2] += __ldg(vext + z * plane + y * n2 + x) * c * c;
+          if (EXT) acc[2] += __ldg(xrow + x) * c * c;
         }
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[(k - 1) % nst]);  // plane k-1 is no longer needed
+    if (lane == 0) mbar_arrive(&empty[sm]);  // plane k-1 is no longer needed
+    if (orow) orow += plane;
+    if (EXT && xrow) xrow += plane;
+    rm = rc;
+    rc = rp;
+    sm = sc;
+    sc = sp;
+    if (++sp == nst) {
+      sp = 0;
+      php ^= 1u;
+    }
   }
   // the last two planes' slots are never re-filled: no arrivals needed
   {
