@@ -625,6 +625,30 @@ int launch_hamiltonian_variant(int v, const SlabGeom& g, int N, const double* u,
       launch_h4<false, 6>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s, 32,
                           56 * 1024);
       return 0;
+    case 16:
+    case 17:
+    case 18:
+    case 19:
+    case 20:
+    case 21: {
+      if (!h4_supported(g)) return -1;
+      static const int zcs[6] = {16, 48, 64, 32, 32, 96};
+      static const int kbs[6] = {56, 56, 56, 40, 84, 56};
+      const int q = v - 16;
+      launch_h4<false, 6>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s, zcs[q],
+                          (size_t)kbs[q] * 1024);
+      return 0;
+    }
+    case 22:
+      if (!h4_supported(g)) return -1;
+      launch_h4<false, 4>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s, 32,
+                          40 * 1024);
+      return 0;
+    case 23:
+      if (!h4_supported(g)) return -1;
+      launch_h4<false, 8>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s, 32,
+                          72 * 1024);
+      return 0;
   }
   return -1;
 }
