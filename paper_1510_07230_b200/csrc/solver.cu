@@ -16,6 +16,7 @@
 // collapse into one stencil pass.
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -153,16 +154,19 @@ bool orthonormalize_dev(Engine& E, const double* A, const double* Ab, double sa,
   return true;
 }
 
-// Asynchronous form of manifold.cpp:136-169 for the line search: everything
-// is enqueued assuming the pass-1 Cholesky succeeds; whether the CholeskyQR2
-// repair runs ((measure || cond > 100) && dev > 1e-12) is decided on the device
-// and its kernels are guarded by that flag, so a trial needs no host round trip
-// before its energy. orth_outcome() interprets the scalars after the trial's
-// single readback; a failed pass-1 Cholesky (rare) is redone synchronously with
-// the symmetric-eigen fallback.
+// Asynchronous form of manifold.cpp:136-169 for the line search: pass 1
+// (Gram -> Cholesky -> rotation -> verification Gram) is enqueued assuming the
+// Cholesky succeeds, with no host round trip before the trial's energy. Whether
+// the CholeskyQR2 repair is due ((measure || cond > 100) && dev > 1e-12) is
+// decided on the host from the trial's single readback (orth_outcome); the
+// repair itself (rare: dev is ~1e-15 for the well-conditioned trial Grams of a
+// line search) then runs synchronously (orth_repair) and the trial's state and
+// H W~ are rebuilt. A failed pass-1 Cholesky is redone with the symmetric-eigen
+// fallback (orthonormalize_dev).
 bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, double* out,
-                  double* tmp, bool measure, DevState* st = nullptr, int hartree = 0, int xc = 0,
+                  bool measure, DevState* st = nullptr, int hartree = 0, int xc = 0,
                   bool g0_from_grams = false, const double* tau_dev = nullptr) {
+  (void)measure;
   double* sc = E.scal();
   if (g0_from_grams)  // G0 of W - tau Z from G_WW (dmat[8]), Sigma (dmat[4]), G_HH (dmat[7])
     launch_trial_gram(E.N, E.dmat[8], E.dmat[4], E.dmat[7], -sa, E.dmat[0], E.s, tau_dev);
@@ -189,34 +193,39 @@ bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, doubl
     E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2]);
   }
   launch_matrix_stats(E.N, E.dmat[2], sc + Engine::S_MSTAT2, E.s);
-  const double* guard = sc + Engine::S_QR2;
-  launch_qr2_decision(sc + Engine::S_CHOL, sc + Engine::S_MSTAT2, measure ? 1 : 0,
-                      sc + Engine::S_QR2, E.s);
-  launch_cholesky_inv(E.N, E.dmat[2], E.chol_L, E.dmat[3], sc + Engine::S_CHOL2, E.s, guard);
-  E.mix(out, nullptr, 0.0, E.dmat[3], 1.0, nullptr, 0.0, 1, tmp, nullptr, guard);
-  launch_copy_guarded(out, tmp, (int64_t)E.N * E.g.ld, guard, E.s);
-  E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2], guard);
-  launch_matrix_stats(E.N, E.dmat[2], sc + Engine::S_MSTAT2, E.s, guard);
-  if (fused) {  // a CholeskyQR2 repair changed the block: its density again
-    launch_density_xc(E.g, E.N, out, E.occ, xc, st->rho, st->v_xc, E.density_b_target(hartree),
-                      E.v_ext, E.partials, E.s, guard);
-    launch_reduce_rows(E.partials, 2, points_nblk(E.g), E.g.w, sc + Engine::S_EXC, E.s, guard);
-  }
   return fused;
 }
 
 // 0 ok, 1 pass-1 Cholesky rejected (caller redoes the trial with the fallback),
-// 2 repair Cholesky rejected (DegenerateSetError).
-int orth_outcome(const Engine& E, OrthOut& o) {
+// 3 the CholeskyQR2 repair is due (caller runs orth_repair).
+int orth_outcome(const Engine& E, bool measure, OrthOut& o) {
   const double* hs = E.hvec + E.off_scal();
   o.offdiag_max = hs[Engine::S_MSTAT + 2];
   o.diag_dev_max = hs[Engine::S_MSTAT + 3];
   o.fallback = false;
   if (hs[Engine::S_CHOL + 3] != 1.0) return 1;
-  const bool repaired = hs[Engine::S_QR2] != 0.0;
-  if (repaired && hs[Engine::S_CHOL2 + 3] != 1.0) return 2;
-  o.post_dev = hs[Engine::S_QR2 + 1] != 0.0 ? hs[Engine::S_MSTAT2] : -1.0;
-  return 0;
+  // manifold.cpp:150: verification unless !measure && cond <= 1e2; :159 repair iff !(dev <= 1e-12)
+  const bool verify = measure || !(hs[Engine::S_CHOL + 2] <= 1e2);
+  const double dev = hs[Engine::S_MSTAT2];
+  o.post_dev = verify ? dev : -1.0;
+  static const bool force = std::getenv("PO_FORCE_QR2") != nullptr;  // test hook: exercise the repair
+  return verify && (force || !(dev <= 1e-12)) ? 3 : 0;
+}
+
+// CholeskyQR2 second pass on block out (manifold.cpp:159-166), synchronously;
+// false on a rejected repair Cholesky (DegenerateSetError).
+bool orth_repair(Engine& E, double* out, double* tmp, OrthOut& o) {
+  double* sc = E.scal();
+  launch_cholesky_inv(E.N, E.dmat[2], E.chol_L, E.dmat[3], sc + Engine::S_CHOL2, E.s);
+  E.fetch(E.off_scal(), 64);
+  if (E.hvec[E.off_scal() + Engine::S_CHOL2 + 3] != 1.0) return false;
+  E.mix(out, nullptr, 0.0, E.dmat[3], 1.0, nullptr, 0.0, 1, tmp, nullptr);
+  PO_CUDA(cudaMemcpyAsync(out, tmp, sizeof(double) * E.N * E.g.ld, cudaMemcpyDeviceToDevice, E.s));
+  E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2]);
+  launch_matrix_stats(E.N, E.dmat[2], sc + Engine::S_MSTAT2, E.s);
+  E.fetch(E.off_scal(), 64);
+  o.post_dev = E.hvec[E.off_scal() + Engine::S_MSTAT2];
+  return true;
 }
 
 namespace {
@@ -480,7 +489,7 @@ void Solver::enqueue_phase1(int iter) {
       spec.wt = pool.get();
       spec.rep = pool.get();
       spec.pre = spool.get();
-      const bool dens = orth_enqueue(E, P(w), P(z), 0.0, P(spec.wt), P(spec.rep),
+      const bool dens = orth_enqueue(E, P(w), P(z), 0.0, P(spec.wt),
                                      p.verify_orthonormality != 0, spec.pre.get(), p.hartree,
                                      p.xc, true, st_tau);
       spec.tstate = enqueue_state(spec.wt, spec.pre, dens);
@@ -621,7 +630,7 @@ bool Solver::step() {
           rep = pool.get();
           // one device pipeline per trial, one readback (energy + decisions)
           SRef pre = nonlinear ? spool.get() : SRef();
-          const bool dens = orth_enqueue(E, P(w), P(z), -tau, P(wt), P(rep),
+          const bool dens = orth_enqueue(E, P(w), P(z), -tau, P(wt),
                                          p.verify_orthonormality != 0, pre.get(), p.hartree, p.xc,
                                          gww_valid && ghh_fresh);
           tstate = enqueue_state(wt, pre, dens);
@@ -629,9 +638,13 @@ bool Solver::step() {
           E.apply_h(P(wt), P(hwt), tstate->v_local, !nonlinear);
           E.fetch_all();
         }
-        const int oc = orth_outcome(E, orth);
-        if (oc == 2) continue;  // DegenerateSetError -> NaN trial energy
-        if (oc == 1) {          // pass-1 Cholesky rejected: symmetric fallback, synchronously
+        const int oc = orth_outcome(E, p.verify_orthonormality != 0, orth);
+        if (oc == 3) {  // CholeskyQR2 repair (rare): redo the trial's tail on the repaired block
+          if (!orth_repair(E, P(wt), P(rep), orth)) continue;  // DegenerateSetError -> NaN energy
+          sync_orth = false;
+          tstate = make_state(wt);
+          te = apply_and_energy(wt, hwt, *tstate);
+        } else if (oc == 1) {  // pass-1 Cholesky rejected: symmetric fallback, synchronously
           auto scratch = [&]() -> double* { return P(rep); };
           if (!orthonormalize_dev(E, P(w), P(z), -tau, P(wt), scratch,
                                   p.verify_orthonormality != 0, orth))

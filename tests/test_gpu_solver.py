@@ -3,6 +3,8 @@ C restatement on identical seeded inputs — per-iteration total energy and
 orbital eigenvalues within 1e-6 Ha (BASELINE north star; observed ~1e-10),
 identical line-search decisions, and the subspace projector
 ||P_gpu - P_ref||_F <= 1e-6."""
+import os
+
 import numpy as np
 import pytest
 
@@ -82,3 +84,34 @@ def test_linear_box_converges(port, native):
     ref, got, wg = run_both(port, native, spec, "opt_par", grad_tol=1e-6)
     assert ref["outcome"] == "converged"
     check(ref, got, wg, spec, decisions=False)
+
+
+def test_cholesky_qr2_repair_path(tmp_path):
+    """manifold.cpp:159-166 second pass: forced on every verified trial (test hook
+    PO_FORCE_QR2) in a subprocess; the repair changes W~ only at round-off, so the
+    trajectory equals the unforced one."""
+    import json
+    import subprocess
+    import sys
+    code = r'''
+import json, sys
+sys.path.insert(0, %r)
+from paper_1510_07230_b200 import configs, native
+spec = configs.small_molecule(12, 4, L=8.0)
+e = native.engine_for(spec)
+w = native.random_orthonormal(e, 42)
+r = e.solve(w, "opt_par_mod", True, True, max_inner=8, n_org=1, n_diag=100)
+print(json.dumps([x["energy"] for x in r.records] + [r.energy["total"]]))
+''' % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),)
+    outs = []
+    for force in (False, True):
+        env = dict(os.environ)
+        env.pop("PO_FORCE_QR2", None)
+        if force:
+            env["PO_FORCE_QR2"] = "1"
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().split("\n")[-1]))
+    a, b = outs
+    assert len(a) == len(b)
+    assert max(abs(x - y) for x, y in zip(a, b)) < 1e-10
