@@ -193,8 +193,11 @@ __device__ __forceinline__ void tma_produce(const CUtensorMap* maps, int nsrc, i
 }
 
 // producer side of every small-N streamed kernel (called by the whole producer warpgroup)
-// (measured alternative, not kept: a cp.async producer warpgroup streamed the
-// same stages at about half the rate of the TMA boxes on B200)
+// (measured alternatives, not kept: a cp.async producer warpgroup streamed the
+// same stages at about half the rate of the TMA boxes on B200; splitting the
+// sources between TMA (half) and cp.async from the idle producer warps (half)
+// was slower than TMA alone for every kernel: e.g. Sigma 113 -> 142 us,
+// directions 234 -> 266 us)
 __device__ __forceinline__ void produce(const Maps& mp, int nsrc, int npad, int64_t kbeg,
                                         int64_t kend, int nst, size_t sdoubles, double* stage0,
                                         uint64_t* full, uint64_t* empty) {
