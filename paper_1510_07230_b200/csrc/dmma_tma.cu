@@ -197,7 +197,8 @@ __device__ __forceinline__ void tma_produce(const CUtensorMap* maps, int nsrc, i
 // same stages at about half the rate of the TMA boxes on B200; splitting the
 // sources between TMA (half) and cp.async from the idle producer warps (half)
 // was slower than TMA alone for every kernel: e.g. Sigma 113 -> 142 us,
-// directions 234 -> 266 us)
+// directions 234 -> 266 us; an interleaved stage schedule across CTAs — all
+// CTAs reading neighbouring segments of each row — made no difference)
 __device__ __forceinline__ void produce(const Maps& mp, int nsrc, int npad, int64_t kbeg,
                                         int64_t kend, int nst, size_t sdoubles, double* stage0,
                                         uint64_t* full, uint64_t* empty) {
