@@ -1334,17 +1334,16 @@ bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* 
 bool tma2d_available() { return encode_fn() != nullptr; }
 
 // Dynamic shared-memory limit, set once per kernel and size (a driver call kept
-// off the launch path), plus the max-shared carveout for every kernel that
-// goes through here: consecutive kernels then need no L1/shared
-// reconfiguration between them (measured: 12-19 us gaps before the Gram that
-// follows the stencil otherwise).
+// off the launch path), plus the max-shared carveout for the big-ring kernels.
 void set_smem(const void* k, int bytes) {
   static std::mutex mu;
   static std::unordered_map<const void*, int> done;
   std::lock_guard<std::mutex> g(mu);
   auto it = done.find(k);
   if (it != done.end() && it->second >= bytes) return;
-  if (it == done.end())
+  // (kernels staging through registers / L1 keep the default carveout: the
+  // tiled LDG mix lost 20% at C3 with the max-shared carveout)
+  if (it == done.end() && bytes >= 64 * 1024)
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
   if (bytes > 0) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
