@@ -86,6 +86,23 @@ def test_linear_box_converges(port, native):
     check(ref, got, wg, spec, decisions=False)
 
 
+@pytest.mark.parametrize("over", [
+    dict(bb_variant="bb2"),
+    dict(bb_variant="alternate", bb_trace_abs="abs_trace"),
+    dict(convergence_mode="mean_abs"),
+    dict(convergence_mode="energy_change"),
+    dict(verify_orthonormality=False),
+])
+def test_opt_par_mod_options(port, native, over):
+    """BB variants / trace reading (the device-side BB step mirrors
+    optimizer.cpp:30-41, 376-411), the three convergence modes
+    (optimizer.cpp:126-148) and the unverified orthonormalisation
+    (manifold.cpp:150) against the C restatement."""
+    spec = configs.small_molecule(14, 4, L=8.0, max_inner=12)
+    ref, got, wg = run_both(port, native, spec, "opt_par_mod", n_org=1, n_diag=100, **over)
+    check(ref, got, wg, spec)
+
+
 def test_cholesky_qr2_repair_path(tmp_path):
     """manifold.cpp:159-166 second pass: forced on every verified trial (test hook
     PO_FORCE_QR2) in a subprocess; the repair changes W~ only at round-off, so the
