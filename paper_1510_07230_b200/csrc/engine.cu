@@ -82,7 +82,7 @@ Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist
   auto upd = [&](size_t v) { pc = v > pc ? v : pc; };
   upd((size_t)3 * N * hamiltonian_nblk(g));
   upd((size_t)5 * N * mix_nblk_max(g));  // fused directions: 5 partial rows
-  upd((size_t)3 * N * per_orbital_nblk(g, N));
+  upd((size_t)4 * N * per_orbital_nblk(g, N));  // residual + BB rows
   upd((size_t)2 * points_nblk(g));
   partials_cap = pc;
   PO_CUDA(cudaMalloc(&partials, pc * sizeof(double)));

@@ -139,6 +139,44 @@ __global__ void __launch_bounds__(PT) bb_kernel(SlabGeom g, int N, const double*
   }
 }
 
+// residual_diag + BB products in one pass (N > 48 path; the small-N path does
+// this inside directions_tma_kernel): z_i = hu_i - sigma_ii u_i written, partial
+// rows [zz | ss | sy | yy] with s = u - u_prev, y = z - z_prev
+// (manifold.cpp:204-216, optimizer.cpp:386-397).
+__global__ void __launch_bounds__(PT) residual_bb_kernel(SlabGeom g, int N,
+                                                         const double* __restrict__ u,
+                                                         const double* __restrict__ hu,
+                                                         const double* __restrict__ sig,
+                                                         const double* __restrict__ up,
+                                                         const double* __restrict__ zp,
+                                                         double* __restrict__ z,
+                                                         double* __restrict__ partials) {
+  __shared__ double red[4 * 32];
+  const int i = blockIdx.y;
+  const double ms = -sig[i];
+  const int64_t o = (int64_t)i * g.ld;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < g.ngl;
+       p += (int64_t)gridDim.x * PT) {
+    const double w = u[o + p];
+    const double v = hu[o + p] + ms * w;
+    z[o + p] = v;
+    acc[0] += v * v;
+    const double sv = w - up[o + p];
+    const double yv = v - zp[o + p];
+    acc[1] += sv * sv;
+    acc[2] += sv * yv;
+    acc[3] += yv * yv;
+  }
+  block_sum<4>(acc, red);
+  if (threadIdx.x == 0) {
+    const int nb = gridDim.x;
+    partials[(int64_t)i * nb + blockIdx.x] = acc[0];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) partials[((int64_t)(1 + q) * N + i) * nb + blockIdx.x] = acc[1 + q];
+  }
+}
+
 __global__ void __launch_bounds__(PT) abs_sum_kernel(SlabGeom g, int N,
                                                      const double* __restrict__ x,
                                                      double* __restrict__ partials) {
@@ -341,6 +379,14 @@ void launch_residual_diag(const SlabGeom& g, int N, const double* u, const doubl
   dim3 grid(per_orbital_nblk(g, N), N);
   ::po::count_launch();
   residual_diag_kernel<<<grid, PT, 0, s>>>(g, N, u, hu, sigma_diag, z, partials);
+}
+
+void launch_residual_bb(const SlabGeom& g, int N, const double* u, const double* hu,
+                        const double* sigma_diag, const double* up, const double* zp, double* z,
+                        double* partials, cudaStream_t s) {
+  dim3 grid(per_orbital_nblk(g, N), N);
+  ::po::count_launch();
+  residual_bb_kernel<<<grid, PT, 0, s>>>(g, N, u, hu, sigma_diag, up, zp, z, partials);
 }
 
 void launch_bb(const SlabGeom& g, int N, const double* w, const double* wp, const double* z,

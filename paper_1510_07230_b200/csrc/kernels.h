@@ -50,6 +50,10 @@ void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h_src
 // z_i = hu_i - sigma_ii u_i (manifold.cpp:204-216); partials [1][N][nblk]: sum z^2.
 void launch_residual_diag(const SlabGeom& g, int N, const double* u, const double* hu,
                           const double* sigma_diag, double* z, double* partials, cudaStream_t s);
+// residual + BB products in one pass; partials [4][N][nblk]: zz, ss, sy, yy (raw).
+void launch_residual_bb(const SlabGeom& g, int N, const double* u, const double* hu,
+                        const double* sigma_diag, const double* up, const double* zp, double* z,
+                        double* partials, cudaStream_t s);
 // BB products (optimizer.cpp:386-397); partials [3][N][nblk]: ss, sy, yy (raw).
 void launch_bb(const SlabGeom& g, int N, const double* w, const double* wp, const double* z,
                const double* zp, double* partials, cudaStream_t s);

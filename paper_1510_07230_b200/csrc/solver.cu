@@ -427,6 +427,7 @@ void Solver::enqueue_phase1(int iter) {
     BRef& dscratch = ph.dscratch;
     const int onb = per_orbital_nblk(E.g, n);
     bool& fused = ph.fused;
+    bool bb_done = false;
     if (!full_grad && !(mean_abs && need_full) && n <= 48 && tma2d_available()) {
       // one pass: z, ||z||^2, ||HW - W Sigma||^2 and the BB products
       ghh_fresh = false;
@@ -457,8 +458,16 @@ void Solver::enqueue_phase1(int iter) {
         sigma(w, hw);
         launch_copy_diag(n, E.dmat[4], E.dvec + E.off_sig(), E.s);
       }
-      launch_residual_diag(E.g, n, P(w), P(hw), E.dvec + E.off_sig(), P(z), E.partials, E.s);
-      E.reduce_rows(E.partials, n, onb, E.g.w, E.dvec + E.off_zz(), true);
+      if (history_valid) {  // z, ||z||^2 and the BB products in one pass
+        launch_residual_bb(E.g, n, P(w), P(hw), E.dvec + E.off_sig(), P(prev_w), P(prev_z), P(z),
+                           E.partials, E.s);
+        E.reduce_rows(E.partials, n, onb, E.g.w, E.dvec + E.off_zz(), true);
+        E.reduce_rows(E.partials + (size_t)n * onb, 3 * n, onb, E.g.w, E.dvec + E.off_ss(), true);
+        bb_done = true;
+      } else {
+        launch_residual_diag(E.g, n, P(w), P(hw), E.dvec + E.off_sig(), P(z), E.partials, E.s);
+        E.reduce_rows(E.partials, n, onb, E.g.w, E.dvec + E.off_zz(), true);
+      }
       if (need_full) {
         if (mean_abs) dscratch = pool.get();
         E.mix(P(w), nullptr, 0.0, E.dmat[4], -1.0, P(hw), 1.0, 0, dscratch ? P(dscratch) : nullptr,
@@ -469,7 +478,7 @@ void Solver::enqueue_phase1(int iter) {
         }
       }
     }
-    if (history_valid && !fused) {
+    if (history_valid && !fused && !bb_done) {
       launch_bb(E.g, n, P(w), P(prev_w), P(z), P(prev_z), E.partials, E.s);
       E.reduce_rows(E.partials, 3 * n, onb, E.g.w, E.dvec + E.off_ss(), true);
     }

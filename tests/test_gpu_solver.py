@@ -103,6 +103,15 @@ def test_opt_par_mod_options(port, native, over):
     check(ref, got, wg, spec)
 
 
+@pytest.mark.parametrize("n_org", [1, 2])
+def test_large_n_paths(port, native, n_org):
+    """N > 48: tiled Gram/mix kernels, the per-orbital residual + BB pass,
+    explicit trial Grams and the separate density pass (the C3/C4 code paths)."""
+    spec = configs.small_molecule(14, 52, L=8.0, max_inner=6)
+    ref, got, wg = run_both(port, native, spec, "opt_par_mod", n_org=n_org, n_diag=100)
+    check(ref, got, wg, spec)
+
+
 def test_cholesky_qr2_repair_path(tmp_path):
     """manifold.cpp:159-166 second pass: forced on every verified trial (test hook
     PO_FORCE_QR2) in a subprocess; the repair changes W~ only at round-off, so the
