@@ -214,8 +214,11 @@ struct TPairs {
 // G = w (A + sa Ab)^T (B + sb Bb) over the CTA's point range; with DUAL
 // (non-symmetric call only) the same pass also accumulates A^T A, so
 // Sigma = (HW)^T W and G_HH = (HW)^T (HW) come from one read of HW and W.
-// F = ceil(N/8) fragments; NPAD = 8F.
-template <int F, bool SYM, bool DUAL>
+// F = ceil(N/8) fragments; NPAD = 8F. With DUAL and R > 0 (N = 8(F-1) + R,
+// R <= 2) the last fragment row — R real orbitals and 8 - R padding ones — is
+// contracted with FP64 FMAs instead of DMMA: this pass is DMMA-bound (two
+// Grams), and for N = 33 the padding row would cost 18 of its 80 DMMAs.
+template <int F, bool SYM, bool DUAL, int R = 0>
 __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant__ Maps maps,
                                                           int N, int nsrc, int qa_b, int qb,
                                                           int qb_b, int64_t ld, int64_t kchunk,
@@ -224,9 +227,12 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
                                                           const double* __restrict__ guard,
                                                           int probe) {
   if (guard && *guard == 0.0) return;
-  constexpr int NP = TPairs<F, SYM>::NP;
-  constexpr int NP2 = DUAL ? F * (F + 1) / 2 : 0;
+  constexpr bool REM = DUAL && R > 0;
+  constexpr int FD = REM ? F - 1 : F;  // DMMA fragments
+  constexpr int NP = TPairs<FD, SYM>::NP;
+  constexpr int NP2 = DUAL ? FD * (FD + 1) / 2 : 0;
   constexpr int NPAD = 8 * F;
+  constexpr int RQ = REM ? 2 * R * 3 : 0;  // remainder partials per lane: [h][r][3]
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   // SWIZZLE_128B boxes need 1024-byte aligned destinations
   unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
@@ -248,17 +254,23 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
   const int64_t kend = min(kbeg + kchunk, ld);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, t4 = lane & 3;
-  double* red = stage0;  // after the loop: [8 warps][(NP + NP2) * 64]
+  double* red = stage0;  // after the loop: [8 warps][(NP + NP2) * 64] then [8][RQ][32]
+  double* rred = red + (size_t)TSC * (NP + NP2) * 64;
   if (warp >= TSC) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     produce(maps, nsrc, NB, kbeg, kend, nst, sdoubles, stage0, full, empty);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
-    double acc[NP][2], acc2[NP2 > 0 ? NP2 : 1][2];
+    double acc[NP > 0 ? NP : 1][2], acc2[NP2 > 0 ? NP2 : 1][2];
 #pragma unroll
     for (int q = 0; q < NP; ++q) acc[q][0] = acc[q][1] = 0.0;
 #pragma unroll
     for (int q = 0; q < NP2; ++q) acc2[q][0] = acc2[q][1] = 0.0;
+    double racc[REM ? 2 : 1][REM ? R : 1][3];
+#pragma unroll
+    for (int h = 0; h < (REM ? 2 : 1); ++h)
+#pragma unroll
+      for (int r = 0; r < (REM ? R : 1); ++r) racc[h][r][0] = racc[h][r][1] = racc[h][r][2] = 0.0;
     const int nstage = kend > kbeg ? (int)((kend - kbeg + TKS - 1) / TKS) : 0;
     const int c = warp * 8;  // this warp's 8-point chunk of every stage
     // (measured: prefetching the next stage's fragments before this stage's
@@ -273,9 +285,43 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
         if (lane == 0) mbar_arrive(&empty[s]);
         continue;
       }
-      double2 a[F], b[SYM ? 1 : F];
+      if constexpr (REM) {
+        // 8 points of one row of source q as 4 double2
+        auto row8 = [&](int row, int q, double2 (&v)[4]) {
 #pragma unroll
-      for (int f = 0; f < F; ++f) {
+          for (int m = 0; m < 4; ++m)
+            v[m] = *reinterpret_cast<const double2*>(sbuf + q * qstride + swz(row, c + 2 * m, NB));
+        };
+        auto dot8 = [](const double2 (&x)[4], const double2 (&y)[4], double t) {
+#pragma unroll
+          for (int m = 0; m < 4; ++m) t = fma(x[m].y, y[m].y, fma(x[m].x, y[m].x, t));
+          return t;
+        };
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int rr = 8 * FD + r;
+          double2 ar[4], br[4];
+          row8(rr, 0, ar);
+          row8(rr, qb, br);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = lane + 32 * h;
+            if (i >= N) continue;
+            double2 ai[4];
+            row8(i, 0, ai);
+            racc[h][r][0] = dot8(ai, br, racc[h][r][0]);  // Sigma(i, rr)
+            if (i <= rr) racc[h][r][2] = dot8(ai, ar, racc[h][r][2]);  // G_HH(i, rr)
+            if (i < 8 * FD) {
+              double2 bi[4];
+              row8(i, qb, bi);
+              racc[h][r][1] = dot8(ar, bi, racc[h][r][1]);  // Sigma(rr, i)
+            }
+          }
+        }
+      }
+      double2 a[FD > 0 ? FD : 1], b[SYM ? 1 : (FD > 0 ? FD : 1)];
+#pragma unroll
+      for (int f = 0; f < FD; ++f) {
         const int off = swz(8 * f + gq, c + 2 * t4, NB);  // 16-B aligned pair of points
         a[f] = *reinterpret_cast<const double2*>(sbuf + off);
         if (qa_b >= 0) {
@@ -296,9 +342,9 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
       if (lane == 0) mbar_arrive(&empty[s]);  // fragments are in registers: release early
       int q = 0;
 #pragma unroll
-      for (int fm = 0; fm < F; ++fm)
+      for (int fm = 0; fm < FD; ++fm)
 #pragma unroll
-        for (int fn = SYM ? fm : 0; fn < F; ++fn, ++q) {
+        for (int fn = SYM ? fm : 0; fn < FD; ++fn, ++q) {
           const double2 bv = SYM ? a[fn] : b[SYM ? 0 : fn];
           dmma_8x8x4(acc[q], a[fm].x, bv.x);
           dmma_8x8x4(acc[q], a[fm].y, bv.y);
@@ -306,9 +352,9 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
       if constexpr (DUAL) {
         int q2 = 0;
 #pragma unroll
-        for (int fm = 0; fm < F; ++fm)
+        for (int fm = 0; fm < FD; ++fm)
 #pragma unroll
-          for (int fn = fm; fn < F; ++fn, ++q2) {
+          for (int fn = fm; fn < FD; ++fn, ++q2) {
             dmma_8x8x4(acc2[q2], a[fm].x, a[fn].x);
             dmma_8x8x4(acc2[q2], a[fm].y, a[fn].y);
           }
@@ -328,8 +374,17 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
       red[(warp * (NP + NP2) + NP + q) * 64 + lane * 2] = acc2[q][0];
       red[(warp * (NP + NP2) + NP + q) * 64 + lane * 2 + 1] = acc2[q][1];
     }
+    if constexpr (REM) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) rred[(warp * RQ + (h * R + r) * 3 + k) * 32 + lane] = racc[h][r][k];
+    }
   }
   __syncthreads();
+  // zero the tiles first when a remainder row exists (its entries come from racc)
   for (int e = threadIdx.x; e < (NP + NP2) * 64; e += TTH) {
     double sum = 0.0;
 #pragma unroll
@@ -339,14 +394,29 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
     const int q = second ? qq - NP : qq;
     const bool sym = second || SYM;
     int fm = 0, fn = 0, cq = 0;
-    for (int m = 0; m < F; ++m)
-      for (int n = sym ? m : 0; n < F; ++n, ++cq)
+    for (int m = 0; m < FD; ++m)
+      for (int n = sym ? m : 0; n < FD; ++n, ++cq)
         if (cq == q) {
           fm = m;
           fn = n;
         }
     double* out = ws + ((second ? gridDim.x : 0) + (int64_t)blockIdx.x) * NPAD * NPAD;
     out[(8 * fm + (l >> 2)) * NPAD + 8 * fn + 2 * (l & 3) + j] = sum;
+  }
+  if constexpr (REM) {
+    for (int e = threadIdx.x; e < RQ * 32; e += TTH) {
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < TSC; ++w) sum += rred[w * RQ * 32 + e];
+      const int l = e % 32, k = (e / 32) % 3, r = (e / 32 / 3) % R, h = e / 32 / 3 / R;
+      const int i = l + 32 * h, rr = 8 * FD + r;
+      if (i >= N) continue;
+      double* o1 = ws + (int64_t)blockIdx.x * NPAD * NPAD;
+      double* o2 = ws + ((int64_t)gridDim.x + blockIdx.x) * NPAD * NPAD;
+      if (k == 0) o1[i * NPAD + rr] = sum;                      // Sigma(i, rr)
+      else if (k == 1 && i < 8 * FD) o1[rr * NPAD + i] = sum;   // Sigma(rr, i)
+      else if (k == 2 && i <= rr) o2[i * NPAD + rr] = sum;      // G_HH(i, rr)
+    }
   }
 }
 
@@ -401,8 +471,11 @@ bool launch_gram_tma_f(int N, int64_t ld, int sym, const double* A, const double
     }
   }
   const bool dual = G2 != nullptr && !sym;
-  const int np = (sym ? F * (F + 1) / 2 : F * F) + (dual ? F * (F + 1) / 2 : 0);
-  const size_t red = (size_t)TSC * np * 64;
+  const int R = dual && F > 1 && (N % 8 == 1 || N % 8 == 2) ? N % 8 : 0;
+  const int fd = R ? F - 1 : F;
+  const int np = (sym ? fd * (fd + 1) / 2 : fd * fd) + (dual ? fd * (fd + 1) / 2 : 0);
+  const size_t red = (size_t)TSC * np * 64 + (size_t)TSC * 12 * 32;
+  if (3072 + red * 8 > 220 * 1024) return false;  // reduction scratch > shared memory
   TCfg cfg = tcfg(nsrc, N, 0);
   if (cfg.smem < 3072 + red * 8) cfg.smem = 3072 + red * 8;
   const int64_t kblocks = (ld + TKS - 1) / TKS;
@@ -411,8 +484,11 @@ bool launch_gram_tma_f(int N, int64_t ld, int sym, const double* A, const double
   const int64_t kchunk = ((kblocks + nsplit - 1) / nsplit) * TKS;
   nsplit = (int)((ld + kchunk - 1) / kchunk);
   ::po::count_launch();
-  auto k = sym ? gram_tma_kernel<F, true, false>
-               : dual ? gram_tma_kernel<F, false, true> : gram_tma_kernel<F, false, false>;
+  auto k = sym    ? gram_tma_kernel<F, true, false>
+           : !dual ? gram_tma_kernel<F, false, false>
+           : R == 1 ? gram_tma_kernel<F, false, true, (F > 1 ? 1 : 0)>
+           : R == 2 ? gram_tma_kernel<F, false, true, (F > 1 ? 2 : 0)>
+                    : gram_tma_kernel<F, false, true, 0>;
   set_smem(reinterpret_cast<const void*>(k), (int)cfg.smem);
   const char* pe = getenv("PO_GRAM_PROBE");  // measurement hook (TMA ring without math)
   const int probe = pe ? atoi(pe) : 0;

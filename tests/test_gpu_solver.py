@@ -103,6 +103,15 @@ def test_opt_par_mod_options(port, native, over):
     check(ref, got, wg, spec)
 
 
+@pytest.mark.parametrize("n_orb", [9, 17, 34, 41])
+def test_remainder_orbital_counts(port, native, n_orb):
+    """N = 8k + 1 / 8k + 2: the FMA tail of the dual Sigma/G_HH pass and of the
+    fused rotation's verification Gram (N = 33 is covered by the C2 runs)."""
+    spec = configs.small_molecule(12, n_orb, L=8.0, max_inner=6)
+    ref, got, wg = run_both(port, native, spec, "opt_par_mod", n_org=1, n_diag=100)
+    check(ref, got, wg, spec)
+
+
 @pytest.mark.parametrize("n_org", [1, 2])
 def test_large_n_paths(port, native, n_org):
     """N > 48: tiled Gram/mix kernels, the per-orbital residual + BB pass,
