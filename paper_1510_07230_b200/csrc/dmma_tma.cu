@@ -711,12 +711,20 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
     const int nstage = pend > pbeg ? (int)((pend - pbeg + TKS - 1) / TKS) : 0;
     const int ksteps = (N + 3) / 4;
     const int c = warp * 8;
-    double mreg[2 * F][F];  // this lane's fragments of the upper-triangular L^{-T}
+    // this lane's fragments of the upper-triangular L^{-T}; with R > 0 the last
+    // fragment column (R real orbitals) is a per-lane FMA dot instead of DMMA
+    double mreg[2 * F][F];
 #pragma unroll
     for (int ks = 0; ks < 2 * F; ++ks)
 #pragma unroll
       for (int fi = 0; fi < F; ++fi)
         mreg[ks][fi] = 4 * ks > 8 * fi + 7 ? 0.0 : Ms[(4 * ks + t4) * NPAD + 8 * fi + gq];
+    double mrem[R > 0 ? R : 1][2 * F];
+#pragma unroll
+    for (int r = 0; r < (R > 0 ? R : 1); ++r)
+#pragma unroll
+      for (int ks = 0; ks < 2 * F; ++ks)
+        mrem[r][ks] = (R > 0 && 4 * ks + t4 < N) ? Ms[(4 * ks + t4) * NPAD + 8 * FD + r] : 0.0;
     // V_ext of the next chunk is requested one stage ahead (a global load in
     // the epilogue stalled every warp for its full latency)
     double vx_next = (vext && t4 == 0 && pbeg + c + gq < ngl) ? __ldg(vext + pbeg + c + gq) : 0.0;
@@ -744,9 +752,20 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
         for (int ks = 0; ks < 2 * F; ++ks) {
           if (ks >= ksteps) break;
 #pragma unroll
-          for (int fi = 0; fi < F; ++fi) {
+          for (int fi = 0; fi < FD; ++fi) {
             if (4 * ks > 8 * fi + 7) continue;
             dmma_8x8x4(acc[fi], av[ks], mreg[ks][fi]);
+          }
+        }
+        if constexpr (R > 0) {  // out_rr(point c + gq) = sum_k A_k M(k, rr), k split over t4
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            double t = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 2 * F; ++ks) t = fma(av[ks], mrem[r][ks], t);
+            t += __shfl_xor_sync(0xffffffffu, t, 1);
+            t += __shfl_xor_sync(0xffffffffu, t, 2);
+            acc[FD][r] = t;  // read back below for i = 8 FD + r (lanes with t4 == 0)
           }
         }
       }
