@@ -104,8 +104,7 @@ __device__ __forceinline__ void mul_left(const double* X, int ps, const double* 
 template <int RB, int CB, int WC>
 __device__ __forceinline__ void store_tiles(double* X, int ps, int nr, int nc, int nf,
                                             const double (&acc)[RB][CB][2],
-                                            const double* __restrict__ lam, int k0, int n0,
-                                            double norm) {
+                                            const double* __restrict__ scale) {
   const int lane = threadIdx.x & 31, gq = lane >> 2, t4 = lane & 3;
   int wr, wc;
   warp_pos<WC>(wr, wc);
@@ -120,7 +119,7 @@ __device__ __forceinline__ void store_tiles(double* X, int ps, int nr, int nc, i
       for (int j = 0; j < 2; ++j) {
         const int c = 8 * cf + 2 * t4 + j;
         double v = acc[a][b][j];
-        if (lam && r < nr && c < nc) v *= norm / ((lam[k0] + lam[n0 + r]) + lam[n0 + nr + c]);
+        if (scale && r < nr && c < nc) v *= __ldg(scale + r * nc + c);
         X[r * ps + c] = (r < nr && c < nc) ? v : 0.0;
       }
     }
@@ -143,8 +142,7 @@ template <int NF, bool SG>
 __global__ void __launch_bounds__(PW * 32) dst_plane_kernel(double* __restrict__ t, int n0, int n1,
                                                             int n2, const double* __restrict__ S1,
                                                             const double* __restrict__ S2,
-                                                            const double* __restrict__ lam,
-                                                            double norm) {
+                                                            const double* __restrict__ scale) {
   constexpr int WC = 4, RB = (NF + 3) / 4, CB = (NF + WC - 1) / WC;
   extern __shared__ double dsm[];
   const int nf = (max(n1, n2) + 7) / 8;
@@ -169,19 +167,19 @@ __global__ void __launch_bounds__(PW * 32) dst_plane_kernel(double* __restrict__
   // forward: axis 2 (X S2), axis 1 (S1 X) + spectral scale; inverse: axis 1, axis 2
   mul_right<RB, CB, WC, SG>(X, ps, s2, ps, n2, nf, acc);
   __syncthreads();
-  store_tiles<RB, CB, WC>(X, ps, n1, n2, nf, acc, nullptr, 0, 0, 0.0);
+  store_tiles<RB, CB, WC>(X, ps, n1, n2, nf, acc, nullptr);
   __syncthreads();
   mul_left<RB, CB, WC, SG>(X, ps, s1, ps, n1, nf, acc);
   __syncthreads();
-  store_tiles<RB, CB, WC>(X, ps, n1, n2, nf, acc, lam, k0, n0, norm);
+  store_tiles<RB, CB, WC>(X, ps, n1, n2, nf, acc, scale + (int64_t)k0 * n1 * n2);
   __syncthreads();
   mul_left<RB, CB, WC, SG>(X, ps, s1, ps, n1, nf, acc);
   __syncthreads();
-  store_tiles<RB, CB, WC>(X, ps, n1, n2, nf, acc, nullptr, 0, 0, 0.0);
+  store_tiles<RB, CB, WC>(X, ps, n1, n2, nf, acc, nullptr);
   __syncthreads();
   mul_right<RB, CB, WC, SG>(X, ps, s2, ps, n2, nf, acc);
   __syncthreads();
-  store_tiles<RB, CB, WC>(X, ps, n1, n2, nf, acc, nullptr, 0, 0, 0.0);
+  store_tiles<RB, CB, WC>(X, ps, n1, n2, nf, acc, nullptr);
   __syncthreads();
   for (int e = threadIdx.x; e < n1 * n2; e += blockDim.x) tp[e] = X[(e / n2) * ps + e % n2];
 }
@@ -294,7 +292,7 @@ void launch_fused(const DstPoisson& d, const double* b, double* x, cudaStream_t 
   launch_axis0_pick<NF>(d, b, d.t0, s);
   ::po::count_launch();
   kp<<<(unsigned)d.n0, PW * 32, sh1, s>>>(d.t0, (int)d.n0, (int)d.n1, (int)d.n2, d.S[1], d.S[2],
-                                          d.lam, d.norm);
+                                          d.scale);
   launch_axis0_pick<NF>(d, d.t0, x, s);
 }
 

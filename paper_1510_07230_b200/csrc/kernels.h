@@ -195,6 +195,7 @@ struct DstPoisson {
   int64_t n0 = 0, n1 = 0, n2 = 0, n1p = 0, n2p = 0, len = 0;
   double* S[3] = {};     // DST-I matrices sin(pi (j+1)(k+1)/(n+1))
   double* lam = nullptr; // [n0 + n1 + n2] eigenvalues of -lap_h per axis
+  double* scale = nullptr;  // [n0][n1][n2] c / (lam0 + lam1 + lam2), precomputed once
   double* t0 = nullptr;  // workspaces (len doubles each)
   double* t1 = nullptr;
   double norm = 1.0;

@@ -400,6 +400,16 @@ void DstPoisson::init(int64_t a0, int64_t a1, int64_t a2, const double h[3]) {
   }
   cudaMalloc(&lam, sizeof(double) * lam_h.size());
   cudaMemcpy(lam, lam_h.data(), sizeof(double) * lam_h.size(), cudaMemcpyHostToDevice);
+  if (dst_fused_supported(n0, n1, n2)) {  // spectral factors of the plane kernel, same rounding
+    std::vector<double> sc((size_t)(n0 * n1 * n2));
+    for (int64_t k0 = 0; k0 < n0; ++k0)
+      for (int64_t k1 = 0; k1 < n1; ++k1)
+        for (int64_t k2 = 0; k2 < n2; ++k2)
+          sc[(size_t)((k0 * n1 + k1) * n2 + k2)] =
+              norm / ((lam_h[(size_t)k0] + lam_h[(size_t)(n0 + k1)]) + lam_h[(size_t)(n0 + n1 + k2)]);
+    cudaMalloc(&scale, sizeof(double) * sc.size());
+    cudaMemcpy(scale, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice);
+  }
   cudaMalloc(&t0, sizeof(double) * len);
   cudaMalloc(&t1, sizeof(double) * len);
   cudaMemset(t0, 0, sizeof(double) * len);
@@ -410,6 +420,7 @@ void DstPoisson::release() {
   for (auto& s : S)
     if (s) cudaFree(s), s = nullptr;
   if (lam) cudaFree(lam), lam = nullptr;
+  if (scale) cudaFree(scale), scale = nullptr;
   if (t0) cudaFree(t0), t0 = nullptr;
   if (t1) cudaFree(t1), t1 = nullptr;
 }
