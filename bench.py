@@ -280,21 +280,19 @@ def ours(args, spec):
     # reads its energy record back to the host), and downloads the final W.
     host = torch.empty(N * e.ngl, dtype=torch.float64, pin_memory=True).numpy().reshape(N, e.ngl)
     e.download(st.current(), host)
-    blk = e.alloc()
     e2e_steps = max(1, args.steps)
     # untimed warm-up call: the engine keeps solver scratch across calls (as a
     # long-lived drop-in engine does), so the timed call allocates nothing
-    e.upload(blk, host)
-    e.solve(blk, "opt_par_mod", True, True, False, args.poisson, max_inner=1, n_org=1, n_diag=100)
+    e.solve_host(host, host, "opt_par_mod", True, True, args.poisson, max_inner=1, n_org=1, n_diag=100)
+    e.download(st.current(), host)
     e.synchronize()
     barrier()
     t0 = time.perf_counter()
     ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev2.record(stream)
-    e.upload(blk, host)
-    res = e.solve(blk, "opt_par_mod", True, True, False, args.poisson, max_inner=e2e_steps, n_org=1,
-                  n_diag=100)
-    e.download(blk, host)
+    # po_solve_host: upload, K iterations, finalize with the download overlapped
+    res = e.solve_host(host, host, "opt_par_mod", True, True, args.poisson, max_inner=e2e_steps,
+                       n_org=1, n_diag=100)
     ev3.record(stream)
     ev3.synchronize()
     e2e_ms = ev2.elapsed_time(ev3)
@@ -370,8 +368,9 @@ def ours(args, spec):
                     "h2d_bytes_per_step": block_bytes / e2e_iters,
                     "d2h_bytes_per_step": block_bytes / e2e_iters + 2 * (9 * N + 64) * 8,
                     "steps": e2e_iters, "wall_s": wall_e2e,
-                    "how": "po_solve on a host block: pinned H2D of W, K outer iterations (energy "
-                           "record read back each), D2H of the final W, CUDA events around all of it",
+                    "how": "po_solve_host on pinned host buffers: H2D of W, K outer iterations (decision "
+                           "scalars read back each), D2H of the final W overlapped with the finalize "
+                           "pass, CUDA events around all of it",
                     "roundtrip_every_step": {"value": rt_value, "unit": UNIT, "steps": rt_steps,
                                              "h2d_bytes_per_step": block_bytes,
                                              "d2h_bytes_per_step": block_bytes}},

@@ -274,6 +274,10 @@ int po_nccl_unique_id(void* out128);
 /* optimizer.cpp:599-613 run_single_level: u0 (orthonormal, block handle) is
  * iterated in place — on return block w holds the final orbitals. */
 int po_solve(po_engine* e, const po_params* p, int w, po_result* r);
+/* The same on host buffers (N x ng_local, orbital-major): w_in uploaded, the
+ * final orbitals written to w_out — the download overlaps the finalize pass. */
+int po_solve_host(po_engine* e, const po_params* p, const double* w_in, double* w_out,
+                  po_result* r);
 /* optimizer.cpp:638-669 solve: initialize_orbitals(p->seed) on grid0 (atoms as
  * in po_external_potential), then p->outer_levels levels — from the second on,
  * refine_uniform + prolongate + orthonormalize — one InnerLoop each (records

@@ -936,6 +936,53 @@ int po_solve(po_engine* h, const po_params* p, int w_handle, po_result* r) {
   return PO_OK;
 }
 
+// po_solve on host buffers: W uploaded, iterated, and downloaded on a side
+// stream while the finalize kernels (which only read W) run — the drop-in's
+// whole reference-facing call in one entry.
+int po_solve_host(po_engine* h, const po_params* p, const double* w_in, double* w_out,
+                  po_result* r) {
+  if (!h || !h->e || !p || !r || !w_in || !w_out) return PO_EINVAL;
+  Engine& E = *h->e;
+  const auto t0 = std::chrono::steady_clock::now();
+  reset_result(r);
+  int w_handle = -1;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev = nullptr;
+  try {
+    validate_params(p);
+    w_handle = E.take_block();
+    PO_CUDA(cudaMemcpy2DAsync(E.blk(w_handle), E.g.ld * 8, w_in, E.g.ngl * 8, E.g.ngl * 8, E.N,
+                              cudaMemcpyHostToDevice, E.s));
+    E.gram(E.blk(w_handle), nullptr, 0.0, E.blk(w_handle), nullptr, 0.0, 1, E.dmat[2]);
+    po::launch_matrix_stats(E.N, E.dmat[2], E.scal() + Engine::S_MSTAT2, E.s);
+    E.fetch(E.off_scal(), 64);
+    if (E.hvec[E.off_scal() + Engine::S_MSTAT2] > 1e-8)
+      throw Error(PO_EINVAL, "solver: initial orbital set is not orthonormal");
+    run_level(E, p, w_handle, r, 0);
+    PO_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    PO_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    PO_CUDA(cudaEventRecord(ev, E.s));
+    PO_CUDA(cudaStreamWaitEvent(side, ev, 0));
+    PO_CUDA(cudaMemcpy2DAsync(w_out, E.g.ngl * 8, E.blk(w_handle), E.g.ld * 8, E.g.ngl * 8, E.N,
+                              cudaMemcpyDeviceToHost, side));
+    finalize_grad(E, p, w_handle, r);
+    PO_CUDA(cudaStreamSynchronize(side));
+  } catch (const Error& ex) {
+    if (side) cudaStreamSynchronize(side);
+    if (side) cudaStreamDestroy(side);
+    if (ev) cudaEventDestroy(ev);
+    if (w_handle >= 0) E.give_block(w_handle);
+    h->err = ex.what();
+    std::snprintf(r->message, sizeof r->message, "%s", ex.what());
+    return ex.code;
+  }
+  cudaStreamDestroy(side);
+  cudaEventDestroy(ev);
+  E.give_block(w_handle);
+  r->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return PO_OK;
+}
+
 // optimizer.cpp:638-669 solve: initialize_orbitals on level 0, then per level
 // refine_uniform + prolongate + orthonormalize (level > 0) and one InnerLoop;
 // stops early on stagnation / numerical failure; finalize on the last grid.

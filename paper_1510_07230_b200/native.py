@@ -125,6 +125,7 @@ _SIGS = {
                         C.c_void_p], C.c_int),
     "po_default_params": ([C.POINTER(Params)], None),
     "po_solve": ([C.c_void_p, C.POINTER(Params), C.c_int, C.POINTER(Result)], C.c_int),
+    "po_solve_host": ([C.c_void_p, C.POINTER(Params), C.c_void_p, C.c_void_p, C.POINTER(Result)], C.c_int),
     "po_solver_create": ([C.c_void_p, C.POINTER(Params), C.c_int, C.POINTER(Result), C.POINTER(C.c_void_p)], C.c_int),
     "po_solver_step": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
     "po_solver_current": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
@@ -389,6 +390,26 @@ class Engine:
         if rc != PO_OK:
             raise _err(rc, self._lib.po_last_error(self.h).decode() or r.message.decode())
         return _solve_result(r, recs, acc, eigs, cap, self.N, trace_eigs)
+
+    def solve_host(self, w_in: np.ndarray, w_out: np.ndarray, algorithm="opt_par_mod", hartree=True,
+                   xc=True, poisson="dst", **over) -> "SolveResult":
+        """po_solve_host: host orbitals in, final orbitals out (pinned buffers are fastest)."""
+        p = self.make_params(algorithm, hartree, xc, False, poisson, **over)
+        cap = p.max_inner + 1
+        recs = (Record * cap)()
+        acc = np.zeros(cap * 9)
+        eigs = np.zeros(1)
+        r = Result()
+        r.cap = cap
+        r.records = recs
+        r.accepted = acc.ctypes.data_as(C.POINTER(C.c_double))
+        r.sigma_eigs = C.POINTER(C.c_double)()
+        if w_in.size != self.N * self.ngl or w_out.size != self.N * self.ngl:
+            raise InvalidArgument("block shape mismatch")
+        rc = self._lib.po_solve_host(self.h, C.byref(p), _dp(w_in), _dp(w_out), C.byref(r))
+        if rc != PO_OK:
+            raise _err(rc, self._lib.po_last_error(self.h).decode() or r.message.decode())
+        return _solve_result(r, recs, acc, eigs, cap, self.N, False)
 
     # ---- outer refinement (optimizer.cpp:638-669, grid.cpp:137-212)
     def initialize_orbitals(self, atoms, seed: int, w: int):

@@ -121,6 +121,23 @@ def test_large_n_paths(port, native, n_org):
     check(ref, got, wg, spec)
 
 
+def test_solve_host_matches_solve(port, native):
+    """po_solve_host (host buffers, overlapped download) = po_solve on a block."""
+    spec = configs.small_molecule(12, 4, L=8.0, max_inner=6)
+    u0 = port.random_orthonormal(spec)
+    e = native.engine_for(spec)
+    w = e.block_from(u0)
+    a = e.solve(w, "opt_par_mod", True, True, max_inner=6, n_org=1, n_diag=100)
+    wa = e.download(w)
+    out = np.empty_like(u0)
+    b = e.solve_host(np.ascontiguousarray(u0), out, "opt_par_mod", True, True, max_inner=6, n_org=1,
+                     n_diag=100)
+    assert [r["energy"] for r in a.records] == [r["energy"] for r in b.records]
+    assert np.array_equal(wa, out)
+    assert a.final_grad_norm == b.final_grad_norm
+    e.close()
+
+
 def test_cholesky_qr2_repair_path(tmp_path):
     """manifold.cpp:159-166 second pass: forced on every verified trial (test hook
     PO_FORCE_QR2) in a subprocess; the repair changes W~ only at round-off, so the
