@@ -113,10 +113,6 @@ inline SolveResult run(const OrbitalSet& u0, const Problem& prob, const Optimize
   std::vector<double> host(static_cast<std::size_t>(u0.n() * ng));
   for (int i = 0; i < u0.n(); ++i)
     std::memcpy(host.data() + i * ng, u0.orbitals[i].values.data(), sizeof(double) * ng);
-  int w = -1;
-  check(po_alloc_block(raw, &w), raw);
-  check(po_upload_block(raw, w, host.data()), raw);
-
   const po_params q = to_params(params, alg, prob);
   std::vector<po_record> recs(static_cast<std::size_t>(q.max_inner) + 1);
   std::vector<double> acc(9 * recs.size());
@@ -124,8 +120,8 @@ inline SolveResult run(const OrbitalSet& u0, const Problem& prob, const Optimize
   r.cap = static_cast<int>(recs.size());
   r.records = recs.data();
   r.accepted = acc.data();
-  check(po_solve(raw, &q, w, &r), raw);
-  check(po_download_block(raw, w, host.data()), raw);
+  // upload, InnerLoop, finalize with the final download overlapped: one call
+  check(po_solve_host(raw, &q, host.data(), host.data(), &r), raw);
 
   SolveResult out;  // optimizer.hpp:98-112
   std::vector<Field> fields;
