@@ -412,9 +412,23 @@ __global__ void __launch_bounds__(32 * (TYR + 1), 1) hamiltonian4_kernel(
   bool rm = ring_plane_real(zs - 1, g.nz, halo_lo, halo_hi), rc = true;
   double* orow = (out && yin) ? out + (int64_t)i * g.ld + zs * plane + y * n2 : nullptr;
   const double* xrow = (EXT && yin) ? vext + zs * plane + y * n2 : nullptr;
+  // z-march with register rotation: each lane keeps its points' values of
+  // planes k-1 and k in registers, so a step reads only plane k+1 (z+1), the
+  // y/x neighbours in plane k and v_local from shared memory (6 instead of 8
+  // loads per point: ncu had the kernel bound by shared-memory bandwidth), and
+  // plane k-1's slot is released before the step instead of after it
+  double zr_m[J], zr_c[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int x = lane + 32 * j;
+    const bool ok = yin && x < n2i;
+    zr_m[j] = (ok && rm) ? ring[sm * slot_stride + rrow + x] : 0.0;
+    zr_c[j] = ok ? ring[sc * slot_stride + rrow + x] : 0.0;
+  }
   for (int k = 1; k + 1 < nplanes; ++k) {  // step on plane z = zs - 1 + k
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[sm]);  // plane k-1 lives on in registers only
     mbar_wait(&full[sp], php);
-    const double* pm = ring + sm * slot_stride;
     const double* pc = ring + sc * slot_stride;
     const double* pp = ring + sp * slot_stride;
     const bool rp = ring_plane_real(zs + k, g.nz, halo_lo, halo_hi);
@@ -424,8 +438,8 @@ __global__ void __launch_bounds__(32 * (TYR + 1), 1) hamiltonian4_kernel(
         const int x = lane + 32 * j;
         if (x < n2i) {
           const int r = rrow + x;
-          const double c = pc[r];
-          const double zm = rm ? pm[r] : 0.0;
+          const double c = zr_c[j];
+          const double zm = zr_m[j];
           const double zp = rp ? pp[r] : 0.0;
           const double ym = pc[r - n2i];  // zero rows outside the box
           const double yp = pc[r + n2i];
@@ -438,11 +452,11 @@ __global__ void __launch_bounds__(32 * (TYR + 1), 1) hamiltonian4_kernel(
           acc[0] += h * c;
           acc[1] += lap * c;
           if (EXT) acc[2] += __ldg(xrow + x) * c * c;
+          zr_m[j] = c;
+          zr_c[j] = zp;
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[sm]);  // plane k-1 is no longer needed
     if (orow) orow += plane;
     if (EXT && xrow) xrow += plane;
     rm = rc;
