@@ -511,8 +511,11 @@ void launch_h4(const SlabGeom& g, int N, const double* u, const double* lo, cons
 }
 
 // Production shape (tools/hu_variants.py sweep on B200, C2 block): 6 rows per
-// CTA, 32 planes per CTA, 56 KB ring (4 CTAs / SM): 102.6 us = 70.6% of the
-// measured HBM peak, vs 62% at 8 rows / 100 KB and 43.6% for the first kernel.
+// CTA, 32 planes per CTA, 56 KB ring (4 CTAs / SM): 85 us = 85% of the measured
+// HBM peak after the register z-march (70.6% before it, 62% at 8 rows / 100 KB,
+// 43.6% for the first kernel). Measured and dropped: two or three rows per
+// consumer warp (y neighbours from registers, 5 loads per point): 81% / 71% —
+// fewer warps per SM hide less latency than the saved loads buy.
 constexpr int H4_TYR = 6;
 constexpr int H4_ZC = 32;
 constexpr size_t H4_BUDGET = 56 * 1024;
