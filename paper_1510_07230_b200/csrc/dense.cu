@@ -314,6 +314,119 @@ __global__ void __launch_bounds__(32) cholesky_inv_reg_kernel(int N, const doubl
   }
 }
 
+// Register-resident Cholesky + inverse factor for N <= 128 in N barrier steps
+// (manifold.cpp:97-114). The same elimination yields L^{-T} directly:
+// with G^(0) = G and V = I (unit upper triangular), step j takes the pivot
+// d_j = G^(j)(j, j) and, for q > j, c_q = G^(j)(q, j) / d_j,
+//   G^(j+1)(p, q) = G^(j)(p, q) - G^(j)(p, j) c_q   (Schur complement, p >= q > j)
+//   V(p, q)      -= c_q V(p, j)                       (p <= j < q),
+// so V^T G V = diag(d), L(j, j) = sqrt(d_j) (the LLT pivots) and
+// M = L^{-T} = V diag(d)^{-1/2}. Element (p, q) of the N x N square lives in a
+// register of exactly one thread — the Schur element when p >= q, the V
+// element otherwise — with p = tr + TR a, q = lane + 32 b; only column j of
+// both goes through shared memory (double-buffered), so a step is one
+// barrier and independent FMAs. Pivot failure (d_j <= 0 or NaN) is the LLT
+// failure; the stats follow manifold.cpp:106-112.
+template <int TR, int A, int B>
+__global__ void __launch_bounds__(TR * 32) cholesky_inv_gs_kernel(int N, const double* __restrict__ G,
+                                                                 double* __restrict__ M,
+                                                                 double* __restrict__ stats,
+                                                                 const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;
+  constexpr int NMAX = TR * A;
+  static_assert(TR * A == 32 * B, "square slot grid");
+  __shared__ double cg[2][NMAX], cv[2][NMAX], dj[NMAX];
+  const int tc = threadIdx.x & 31, tr = threadIdx.x >> 5;
+  double x[A][B];
+#pragma unroll
+  for (int a = 0; a < A; ++a)
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int p = tr + TR * a, q = tc + 32 * b;
+      x[a][b] = (p < N && q < N && p >= q) ? G[p * N + q] : 0.0;
+      if (q == 0 && p < N) cg[0][p] = x[a][b];
+    }
+  if (threadIdx.x == 0) cv[0][0] = 1.0;
+  __syncthreads();
+  bool fail = false;
+  for (int j = 0; j < N; ++j) {
+    const int buf = j & 1;
+    const double d = cg[buf][j];
+    if (!(d > 0.0)) {  // uniform: every thread reads the same pivot
+      fail = true;
+      break;
+    }
+    const double dinv = 1.0 / d;
+    if (threadIdx.x == 0) dj[j] = d;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int q = tc + 32 * b;
+      if (q <= j || q >= N) continue;
+      const double cq = cg[buf][q] * dinv;
+#pragma unroll
+      for (int a = 0; a < A; ++a) {
+        const int p = tr + TR * a;
+        if (p >= N) continue;
+        if (p >= q) {
+          x[a][b] -= cg[buf][p] * cq;
+        } else if (p <= j) {
+          x[a][b] -= cv[buf][p] * cq;
+        } else {
+          continue;
+        }
+        if (q == j + 1) {  // column j + 1 is final: publish it for the next step
+          if (p >= q) {
+            cg[buf ^ 1][p] = x[a][b];
+            if (p == q) cv[buf ^ 1][p] = 1.0;
+          } else {
+            cv[buf ^ 1][p] = x[a][b];
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (threadIdx.x == 0) {
+      stats[0] = 0.0;
+      stats[1] = 0.0;
+      stats[2] = INFINITY;
+      stats[3] = 0.0;
+    }
+    return;
+  }
+  __shared__ double rsq[NMAX];
+  for (int i = threadIdx.x; i < N; i += TR * 32) rsq[i] = 1.0 / sqrt(dj[i]);
+  if (threadIdx.x < 32) {  // pivots L(j, j) = sqrt(d_j): min / max over j
+    double pmin = INFINITY, pmax = -INFINITY;
+    for (int i = threadIdx.x; i < N; i += 32) {
+      const double v = sqrt(dj[i]);
+      pmin = fmin(pmin, v);
+      pmax = fmax(pmax, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      pmin = fmin(pmin, __shfl_xor_sync(0xffffffffu, pmin, o));
+      pmax = fmax(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+    }
+    if (threadIdx.x == 0) {
+      const bool ok = (pmin > 0.0) && isfinite(pmax) && !(pmin * pmin < 1e-10 * pmax * pmax);
+      stats[0] = pmin;
+      stats[1] = pmax;
+      stats[2] = (pmax / pmin) * (pmax / pmin);
+      stats[3] = ok ? 1.0 : 0.0;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int a = 0; a < A; ++a)
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int p = tr + TR * a, q = tc + 32 * b;
+      if (p < N && q < N) M[p * N + q] = p < q ? x[a][b] * rsq[q] : (p == q ? rsq[q] : 0.0);
+    }
+}
+
 // Parallel cyclic Jacobi (round-robin pairing) on S = 1/2 (A + A^T).
 // work: N*N (S) ; evecs N*N ; evals N.
 __global__ void __launch_bounds__(DT) syev_kernel(int N, const double* __restrict__ A,
@@ -614,6 +727,16 @@ void launch_copy_guarded(double* dst, const double* src, int64_t n, const double
 void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, double* stats,
                          cudaStream_t s, const double* guard) {
   ::po::count_launch();
+  static const int variant = getenv("PO_CHOL") ? atoi(getenv("PO_CHOL")) : 0;  // measurement
+  if (variant == 0 && N <= 128) {  // one barrier per column, registers only
+    if (N <= 32)
+      cholesky_inv_gs_kernel<32, 1, 1><<<1, 1024, 0, s>>>(N, G, M, stats, guard);
+    else if (N <= 64)
+      cholesky_inv_gs_kernel<16, 4, 2><<<1, 512, 0, s>>>(N, G, M, stats, guard);
+    else
+      cholesky_inv_gs_kernel<16, 8, 4><<<1, 512, 0, s>>>(N, G, M, stats, guard);
+    return;
+  }
   // measured (tools/kbench-style, one launch): register kernel 6 / 12 / 29 us at
   // N = 5 / 16 / 32; at N = 33 its second register row spills and the
   // shared-memory kernel (47 us) wins; shared memory up to N = 160

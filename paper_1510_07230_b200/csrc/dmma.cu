@@ -828,6 +828,11 @@ int launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, doub
 #undef PO_MS
     }
   }
+  {
+    const int nb = launch_mix_big(N, g.ld, g.ngl, A, Ab, sa, M, alpha, C, beta, upper, out, norms, s,
+                                  guard);
+    if (nb >= 0) return nb;
+  }
   dim3 grid(mix_nblk(g), (N + MI - 1) / MI);
   constexpr size_t shm = sizeof(double) * (2 * MK * MPP + 2 * MK * MIP + 4 * MI);
   static bool attr = false;

@@ -13,6 +13,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -1151,9 +1153,11 @@ __device__ __forceinline__ void big_tile_index(int t, int mt, int sym, int& tm, 
 }
 
 // T = 128: a producer warpgroup (one lane issues the boxes) that hands its
-// registers to the two consumer warpgroups (setmaxnreg 40 / 232), so the
-// 32 x 64 warp tiles keep their 128 accumulator registers; T = 64: one
-// producer warp.
+// registers to the two consumer warpgroups (setmaxnreg 40 / 232); T = 64: one
+// producer warp. (ptxas still compiles the whole kernel for 168 registers, and
+// a 9-warp block cannot have more: the register file is split over the four
+// SM sub-partitions and one of them holds 3 of the 9 warps — measured as a
+// launch failure at 216 registers x 288 threads.)
 template <int GT_T>
 struct BigCfg {  // consumer warps WM x WN, warp tile (T/WM) x (T/WN)
   static constexpr int WM = 4, WN = 2;
@@ -1181,7 +1185,7 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
   int tm, tn;
   big_tile_index(blockIdx.x, mt, sym, tm, tn);
   const bool diag = sym && tm == tn;
-  // sources actually fetched: A (+Ab); B (+Bb) unless this is a symmetric diagonal tile
+  // sources fetched per 16-point half: A (+Ab); B (+Bb) unless this is a symmetric diagonal tile
   const int nload = diag ? (qa_b >= 0 ? 2 : 1) : nsrc;
   using Cfg = BigCfg<GT_T>;
   if (threadIdx.x == 0) {
@@ -1194,7 +1198,9 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
   __syncthreads();
   const int64_t kbeg = (int64_t)blockIdx.y * kchunk;
   const int64_t kend = min(kbeg + kchunk, ld);
-  const int nstage = kend > kbeg ? (int)((kend - kbeg + BOX - 1) / BOX) : 0;
+  // a diagonal tile consumes 32 points per stage (two 16-point halves, see below)
+  const int pps = diag ? 2 * BOX : BOX;
+  const int nstage = kend > kbeg ? (int)((kend - kbeg + pps - 1) / pps) : 0;
   const int lane = threadIdx.x & 31;
   int warp = threadIdx.x >> 5;
   if (warp < Cfg::PW) {
@@ -1202,16 +1208,23 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
     if (warp == 0 && lane == 0) {
       for (int q = 0; q < nload; ++q)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[q])));
-      const uint32_t bytes = (uint32_t)(nload * QS * 8);
+      const int nbox = diag ? 2 * nload : nload;
+      const uint32_t bytes = (uint32_t)(nbox * QS * 8);
       for (int st = 0; st < nstage; ++st) {
         const int s = st % nst;
         if (st >= nst) mbar_wait(&empty[s], ((uint32_t)(st / nst) & 1u) ^ 1u);
         mbar_arrive_expect_tx(&full[s], bytes);
-        const int x = (int)(kbeg + (int64_t)st * BOX);
+        const int x = (int)(kbeg + (int64_t)st * pps);
         double* sbuf = stage0 + (size_t)s * sdoubles;
-        for (int q = 0; q < nload; ++q) {
-          const int row0 = (q == qb || q == qb_b) ? tn * GT_T : tm * GT_T;
-          tma_load_2d(sbuf + q * QS, &maps.m[q], x, row0, &full[s]);
+        if (diag) {  // areas [A(x), Ab(x)?, A(x+16), Ab(x+16)?], all rows of tile tm
+          for (int h = 0; h < 2; ++h)
+            for (int q = 0; q < nload; ++q)
+              tma_load_2d(sbuf + (h * nload + q) * QS, &maps.m[q], x + h * BOX, tm * GT_T, &full[s]);
+        } else {
+          for (int q = 0; q < nload; ++q) {
+            const int row0 = (q == qb || q == qb_b) ? tn * GT_T : tm * GT_T;
+            tma_load_2d(sbuf + q * QS, &maps.m[q], x, row0, &full[s]);
+          }
         }
       }
     }
@@ -1219,70 +1232,156 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
     if constexpr (Cfg::PW == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
     warp -= Cfg::PW;
     const int gq = lane >> 2, t4 = lane & 3;
-    constexpr int FM = Cfg::FM, FN = Cfg::FN;
-    const int wm = warp / Cfg::WN, wn = warp % Cfg::WN;
+    constexpr int FM = Cfg::FM, FN = Cfg::FN, WM = Cfg::WM, WN = Cfg::WN;
+    const int wm = warp / WN, wn = warp % WN;
     double acc[FM][FN][2];
 #pragma unroll
     for (int a = 0; a < FM; ++a)
 #pragma unroll
       for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    // on a diagonal tile: warp entirely below the diagonal has nothing to do
-    const bool idle = diag && (8 * FM * wm >= 8 * FN * wn + 8 * FN);
-    const int bq = diag ? 0 : qb, bqb = diag ? qa_b : qb_b;
-    const double bs = diag ? sa : sb;
-    for (int st = 0; st < nstage; ++st) {
-      const int s = st % nst;
-      mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
-      const double* sbuf = stage0 + (size_t)s * sdoubles;
-#pragma unroll
-      for (int kg = 0; kg < 2; ++kg) {
-        if (idle) break;
-        const int p = 8 * kg + 2 * t4;
-        double2 a[FM], b[FN];
-#pragma unroll
-        for (int f = 0; f < FM; ++f) {
-          const int off = swz(8 * FM * wm + 8 * f + gq, p, GT_T);
-          a[f] = *reinterpret_cast<const double2*>(sbuf + off);
-          if (qa_b >= 0) {
-            const double2 z = *reinterpret_cast<const double2*>(sbuf + qa_b * QS + off);
-            a[f].x += sa * z.x;
-            a[f].y += sa * z.y;
-          }
-        }
-#pragma unroll
-        for (int f = 0; f < FN; ++f) {
-          const int off = swz(8 * FN * wn + 8 * f + gq, p, GT_T);
-          b[f] = *reinterpret_cast<const double2*>(sbuf + bq * QS + off);
-          if (bqb >= 0) {
-            const double2 z = *reinterpret_cast<const double2*>(sbuf + bqb * QS + off);
-            b[f].x += bs * z.x;
-            b[f].y += bs * z.y;
-          }
-        }
-        if (kg == 1) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[s]);  // all fragments of the stage are in registers
-        }
-#pragma unroll
-        for (int fm = 0; fm < FM; ++fm)
-#pragma unroll
-          for (int fn = 0; fn < FN; ++fn) {
-            if (diag && FM * wm + fm > FN * wn + fn) continue;
-            dmma_8x8x4(acc[fm][fn], a[fm].x, b[fn].x);
-            dmma_8x8x4(acc[fm][fn], a[fm].y, b[fn].y);
-          }
+    // fragment row / column f of this warp: WM f + wm / WN f + wn (interleaved)
+    auto load_frag = [&](const double* base, int qa, int qb2, double sc, int frag, int p) {
+      const int off = swz(8 * frag + gq, p, GT_T);
+      double2 v = *reinterpret_cast<const double2*>(base + qa * QS + off);
+      if (qb2 >= 0) {
+        const double2 z = *reinterpret_cast<const double2*>(base + qb2 * QS + off);
+        v.x += sc * z.x;
+        v.y += sc * z.y;
       }
-      if (idle) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+      return v;
+    };
+    if (!diag) {
+      for (int st = 0; st < nstage; ++st) {
+        const int s = st % nst;
+        mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+        const double* sbuf = stage0 + (size_t)s * sdoubles;
+#pragma unroll
+        for (int kg = 0; kg < 2; ++kg) {
+          const int p = 8 * kg + 2 * t4;
+          double2 a[FM], b[FN];
+#pragma unroll
+          for (int f = 0; f < FM; ++f) a[f] = load_frag(sbuf, 0, qa_b, sa, WM * f + wm, p);
+#pragma unroll
+          for (int f = 0; f < FN; ++f) b[f] = load_frag(sbuf, qb, qb_b, sb, WN * f + wn, p);
+          if (kg == 1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);  // all fragments of the stage are in registers
+          }
+#pragma unroll
+          for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+            for (int fn = 0; fn < FN; ++fn) {
+              dmma_8x8x4(acc[fm][fn], a[fm].x, b[fn].x);
+              dmma_8x8x4(acc[fm][fn], a[fm].y, b[fn].y);
+            }
+        }
       }
+    } else {
+      // Diagonal tile of a symmetric Gram with no wasted DMMA and one code path
+      // for all warps. Each stage holds two 16-point halves. With R = T / 8
+      // fragment rows, warp w owns rows r = w + 8 m (m < R / 8) and the R
+      // circulant offsets k: slot (m, k) accumulates block (r, c = (r + k) mod R).
+      // Every unordered pair {x, y} of fragments appears in exactly two slots,
+      // (x, y - x) and (y, x - y) (mod R): offsets 1 .. R/2 - 1 take the first
+      // half, R/2 + 1 .. R - 1 the second, offset R/2 the first half on rows
+      // < R/2 (its partner slot has row >= R/2); offset 0 (the diagonal
+      // blocks) takes both. So each slot's half is fixed per (m, k) — the same
+      // for every warp — and the two contributions of a pair meet in the
+      // epilogue (shared memory, transposed where r > c).
+      constexpr int R = GT_T / 8, RW = R / 8;
+      const int wq = warp;  // 0..7
+      double gacc[RW][R][2];
+#pragma unroll
+      for (int m = 0; m < RW; ++m)
+#pragma unroll
+        for (int k = 0; k < R; ++k) gacc[m][k][0] = gacc[m][k][1] = 0.0;
+      const int h1 = nload;  // first area of the second half
+      for (int st = 0; st < nstage; ++st) {
+        const int s = st % nst;
+        mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+        const double* sbuf = stage0 + (size_t)s * sdoubles;
+#pragma unroll
+        for (int kg = 0; kg < 2; ++kg) {
+          const int p = 8 * kg + 2 * t4;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int q0 = h * h1, qb2 = qa_b >= 0 ? h * h1 + qa_b : -1;
+            const double* base = sbuf;
+            double2 ar[RW];
+#pragma unroll
+            for (int m = 0; m < RW; ++m) ar[m] = load_frag(base, q0, qb2, sa, wq + 8 * m, p);
+#pragma unroll
+            for (int m = 0; m < RW; ++m)
+#pragma unroll
+              for (int k = 0; k < R; ++k) {
+                // half of slot (m, k); -1: offset R/2 with a runtime row test (RW == 1)
+                constexpr int dummy = 0;
+                (void)dummy;
+                const int hs = k == 0 ? 2 : (k < R / 2 ? 0 : (k > R / 2 ? 1 : (RW == 2 ? m : -1)));
+                if (hs == 2 || hs == h) {
+                  const double2 bc = load_frag(base, q0, qb2, sa, (wq + 8 * m + k) % R, p);
+                  dmma_8x8x4(gacc[m][k], ar[m].x, bc.x);
+                  dmma_8x8x4(gacc[m][k], ar[m].y, bc.y);
+                } else if (hs == -1 && h == 0) {
+                  // offset R/2 with one row per warp: rows < R/2 use the first
+                  // half, the others the second (operands selected, no predicate)
+                  const bool first = wq < R / 2;
+                  const int qs = first ? 0 : h1, qsb = qa_b >= 0 ? qs + qa_b : -1;
+                  const double2 ra = load_frag(base, qs, qsb, sa, wq, p);
+                  const double2 bc = load_frag(base, qs, qsb, sa, (wq + R / 2) % R, p);
+                  dmma_8x8x4(gacc[m][k], ra.x, bc.x);
+                  dmma_8x8x4(gacc[m][k], ra.y, bc.y);
+                }
+              }
+            asm volatile("" ::: "memory");
+          }
+          if (kg == 1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+          }
+        }
+      }
+      constexpr int SP = GT_T + 8;
+      double* S = stage0;
+      asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NW * 32) : "memory");  // ring fully consumed
+      // pass 0: first-half and diagonal slots store; pass 1: second-half slots add
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+        for (int m = 0; m < RW; ++m)
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            const int r = wq + 8 * m, c = (r + k) % R;
+            const int hs = k == 0 ? 0 : (k < R / 2 ? 0 : (k > R / 2 ? 1 : (r < R / 2 ? 0 : 1)));
+            if (hs != pass) continue;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int idx = r <= c ? (8 * r + gq) * SP + 8 * c + 2 * t4 + j
+                                     : (8 * c + 2 * t4 + j) * SP + 8 * r + gq;
+              if (pass == 0)
+                S[idx] = gacc[m][k][j];
+              else
+                S[idx] += gacc[m][k][j];
+            }
+          }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NW * 32) : "memory");
+      }
+      double* outd = ws + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * (GT_T * GT_T);
+      const int ct = threadIdx.x - Cfg::PW * 32;
+      for (int e = ct; e < GT_T * GT_T / 2; e += Cfg::NW * 32) {
+        const int r = (2 * e) / GT_T, c = (2 * e) % GT_T;
+        *reinterpret_cast<double2*>(outd + r * GT_T + c) =
+            make_double2(S[r * SP + c], S[r * SP + c + 1]);
+      }
+      return;
     }
     double* out = ws + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * (GT_T * GT_T);
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm)
 #pragma unroll
       for (int fn = 0; fn < FN; ++fn) {
-        const int r = 8 * FM * wm + 8 * fm + gq, c = 8 * FN * wn + 8 * fn + 2 * t4;
+        const int r = 8 * (WM * fm + wm) + gq, c = 8 * (WN * fn + wn) + 2 * t4;
+        // (lower blocks of a diagonal tile hold the transposed second half: never read)
         *reinterpret_cast<double2*>(out + r * GT_T + c) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
       }
   }
@@ -1321,10 +1420,10 @@ struct BigPlan {
 };
 
 // splits so that tiles x splits fills whole waves of one CTA per SM
-// Tile side. Measured at N = 128 (C3, 128^3): 64-wide tiles win only for the
-// one-source symmetric Gram (2.04 vs 2.26 ms); with two streamed sources
-// (Sigma, the trial Gram) the 64-tile CTAs are bound by the 2D-TMA row rate
-// and 128-wide tiles win (2.26 vs 2.76 ms, 2.40 vs 2.91 ms).
+// Tile side. Measured at N = 128 (C3, 128^3): 128-wide tiles win for every
+// Gram once diagonal tiles stopped issuing wasted DMMAs (symmetric 1.45 ms vs
+// 1.74 ms with 64-wide tiles; before, 64 won at 2.04 vs 2.26 ms); with two
+// streamed sources the 64-tile CTAs are bound by the 2D-TMA row rate.
 int big_tile(int N, int sym, bool two_src) {
   static int forced = -1;
   if (forced < 0) {
@@ -1332,8 +1431,9 @@ int big_tile(int N, int sym, bool two_src) {
     forced = e ? atoi(e) : 0;
   }
   if (forced == 64 || forced == 128) return forced;
-  if (N > 192) return 128;
-  return (sym && !two_src) ? 64 : 128;
+  (void)sym;
+  (void)two_src;
+  return N <= 64 ? 64 : 128;
 }
 
 BigPlan big_plan(int64_t ld, int N, int sym, int sms, int GT_T) {
@@ -1356,12 +1456,315 @@ BigPlan big_plan(int64_t ld, int N, int sym, int sms, int GT_T) {
     }
     if (eff >= 0.97) break;
   }
-  p.kchunk = ((kb + best - 1) / best) * BOX;
+  // chunks of a multiple of 32 points: diagonal tiles consume 32-point stages
+  p.kchunk = (((kb + best - 1) / best + 1) / 2) * 2 * BOX;
   p.nsplit = (int)((ld + p.kchunk - 1) / p.kchunk);
   return p;
 }
 
+// ------------------------------------------------------------------ large-N mix
+// out_i = alpha sum_k (A + sa Ab)_k M(k, i) + beta C_i for N > 64
+// (manifold.cpp:67-85; the orthonormalisation rotation W L^{-T} with M upper
+// triangular, manifold.cpp:97-114, and the gradient D = HW - W Sigma,
+// manifold.cpp:181-202). Persistent CTAs walk 128-point x 128-orbital output
+// tiles; each stage brings 16 input orbitals of the tile's 128 points
+// (8 boxes {16 points x 16 rows}, 128-B swizzle) per source plus the matching
+// 16 columns of M^T (one box {16 k x 128 i}) — M is transposed into a padded
+// scratch by the launcher so that one 16-byte shared load gives a lane the B
+// fragments of two k-steps. The A side pairs points instead: a lane's 16-byte
+// load holds points 2q, 2q+1, i.e. the same (row, k) element of two DMMA row
+// fragments.
+// Consumer warp w owns the output fragments F = w and F = 15 - w (8 orbitals
+// each) over all 128 points of the tile. With an upper-triangular M the
+// 8-input block kb of the tile's diagonal block only meets fragments F >= kb,
+// so the pair does kb-blocks 0..w and 0..15-w: 17 per warp, balanced, and
+// every skipped block is a warp-uniform branch around whole DMMA groups (a
+// predicated-off DMMA still occupies the tensor pipe; per-stage code variants
+// thrashed the instruction cache: ncu "no instruction" stalls).
+constexpr int XP = 128;  // points per tile
+constexpr int XI = 128;  // orbitals per tile
+constexpr int XK = 16;   // input orbitals per stage
+constexpr int XTH = 384;
+
+// one 8-input block (k8 .. k8 + 7 = stage rows 8h ..) for the warp's active fragments
+template <bool A0, bool A1>
+__device__ __forceinline__ void mix_big_slice(double (&acc)[2][16][2], const double* sb,
+                                              const double* sbb, double sa, double2 b0, double2 b1,
+                                              int h, int gq, int t4) {
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    double2 a[2];
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const int off = swz(8 * h + 2 * t4 + s2, 16 * g + 2 * gq, XK);
+      a[s2] = *reinterpret_cast<const double2*>(sb + off);
+      if (sbb) {
+        const double2 z = *reinterpret_cast<const double2*>(sbb + off);
+        a[s2].x += sa * z.x;
+        a[s2].y += sa * z.y;
+      }
+    }
+    if (A0) {
+      dmma_8x8x4(acc[0][2 * g], a[0].x, b0.x);
+      dmma_8x8x4(acc[0][2 * g + 1], a[0].y, b0.x);
+      dmma_8x8x4(acc[0][2 * g], a[1].x, b0.y);
+      dmma_8x8x4(acc[0][2 * g + 1], a[1].y, b0.y);
+    }
+    if (A1) {
+      dmma_8x8x4(acc[1][2 * g], a[0].x, b1.x);
+      dmma_8x8x4(acc[1][2 * g + 1], a[0].y, b1.x);
+      dmma_8x8x4(acc[1][2 * g], a[1].x, b1.y);
+      dmma_8x8x4(acc[1][2 * g + 1], a[1].y, b1.y);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(XTH, 1) mix_big_kernel(
+    const __grid_constant__ Maps maps, int has_ab, int N, int64_t ld, int64_t ngl, int n_pt,
+    int n_it, int upper, int nst, double sa, double alpha, const double* __restrict__ C,
+    double beta, double* __restrict__ out, double* __restrict__ norms,
+    const double* __restrict__ guard) {
+  if (guard && *guard == 0.0) return;
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
+  uint64_t* empty = full + 8;
+  uint64_t* ready = full + 16;  // two-source stages: A + sa Ab formed in place
+  double* stage0 = reinterpret_cast<double*>(tsm + 1024);
+  constexpr size_t QA = (size_t)XP * XK;  // doubles per source per stage
+  const int nsrc = has_ab ? 2 : 1;
+  const size_t sdoubles = (size_t)(nsrc + 1) * QA;  // + the M^T box
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+      mbar_init(&ready[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int ntiles = n_pt * n_it;
+  // heavy (last) orbital tiles first: with the triangular skip their k range is longest
+  auto tile_of = [&](int t, int& pt, int& it) {
+    it = n_it - 1 - t / n_pt;
+    pt = t % n_pt;
+  };
+  auto kend_of = [&](int it) { return upper ? min(N, (it + 1) * XI) : N; };
+  const int lane = threadIdx.x & 31;
+  int warp = threadIdx.x >> 5;
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (warp == 0 && lane == 0) {
+      for (int q = 0; q <= nsrc; ++q)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[q])));
+      const uint32_t bytes = (uint32_t)((nsrc + 1) * QA * 8);
+      int g = 0;  // global stage counter (ring position)
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int pt, it;
+        tile_of(t, pt, it);
+        const int nk = (kend_of(it) + XK - 1) / XK;
+        for (int c = 0; c < nk; ++c, ++g) {
+          const int s = g % nst;
+          if (g >= nst) mbar_wait(&empty[s], ((uint32_t)(g / nst) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&full[s], bytes);
+          double* sb = stage0 + (size_t)s * sdoubles;
+          for (int q = 0; q < nsrc; ++q)
+            for (int b = 0; b < XP / BOX; ++b)
+              tma_load_2d(sb + q * QA + b * BOX * XK, &maps.m[q], pt * XP + b * BOX, c * XK, &full[s]);
+          tma_load_2d(sb + nsrc * QA, &maps.m[nsrc], c * XK, it * XI, &full[s]);
+        }
+      }
+    } else if (warp > 0 && has_ab) {
+      // the other three producer warps form A + sa Ab in place for every stage
+      // (the trial rotation's W - tau Z), so the consumers read one source
+      const int ct = threadIdx.x - 32;  // 0..95
+      int g = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int pt, it;
+        tile_of(t, pt, it);
+        const int nk = (kend_of(it) + XK - 1) / XK;
+        for (int c = 0; c < nk; ++c, ++g) {
+          const int s = g % nst;
+          mbar_wait(&full[s], (uint32_t)(g / nst) & 1u);
+          double2* a2 = reinterpret_cast<double2*>(stage0 + (size_t)s * sdoubles);
+          const double2* b2 = reinterpret_cast<const double2*>(stage0 + (size_t)s * sdoubles + QA);
+          for (int e = ct; e < (int)(QA / 2); e += 96) {
+            double2 v = a2[e];
+            const double2 z = b2[e];
+            v.x += sa * z.x;
+            v.y += sa * z.y;
+            a2[e] = v;
+          }
+          // generic writes into a TMA-filled slot: ordered before the slot's refill
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          asm volatile("bar.sync 2, 96;\n" ::: "memory");
+          if (ct == 0) mbar_arrive(&ready[s]);
+        }
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    warp -= 4;
+    const int gq = lane >> 2, t4 = lane & 3;
+    const int F0 = warp, F1 = 15 - warp;  // this warp's output fragments
+    int g = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int pt, it;
+      tile_of(t, pt, it);
+      const int i0 = it * XI;
+      const int kend = kend_of(it);
+      const int nk = (kend + XK - 1) / XK;
+      const bool real0 = i0 + 8 * F0 < N, real1 = i0 + 8 * F1 < N;  // padding fragments
+      double acc[2][16][2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 16; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+      for (int c = 0; c < nk; ++c, ++g) {
+        const int s = g % nst;
+        mbar_wait(has_ab ? &ready[s] : &full[s], (uint32_t)(g / nst) & 1u);
+        const double* sb = stage0 + (size_t)s * sdoubles;
+        const double* sbb = nullptr;
+        const double* mt = sb + nsrc * QA;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k8 = c * XK + 8 * h;
+          if (k8 >= kend) break;
+          const int kb = (k8 - i0) >> 3;  // 8-block index relative to the tile's orbitals
+          const bool a0 = real0 && (!upper || kb <= F0);
+          const bool a1 = real1 && (!upper || kb <= F1);
+          const double2 b0 = *reinterpret_cast<const double2*>(mt + swz(8 * F0 + gq, 8 * h + 2 * t4, XI));
+          const double2 b1 = *reinterpret_cast<const double2*>(mt + swz(8 * F1 + gq, 8 * h + 2 * t4, XI));
+          if (a0 && a1)
+            mix_big_slice<true, true>(acc, sb, sbb, sa, b0, b1, h, gq, t4);
+          else if (a1)
+            mix_big_slice<false, true>(acc, sb, sbb, sa, b0, b1, h, gq, t4);
+          else if (a0)
+            mix_big_slice<true, false>(acc, sb, sbb, sa, b0, b1, h, gq, t4);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);  // the stage's fragments were consumed
+      }
+      // epilogue: acc[q][2 g + e][j] = out(point 16 g + 2 gq + e, orbital i0 + 8 F_q + 2 t4 + j)
+      const int64_t pb = (int64_t)pt * XP + 2 * gq;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (!(q ? real1 : real0)) continue;
+        const int F = q ? F1 : F0;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = i0 + 8 * F + 2 * t4 + j;
+          double nrm = 0.0;
+          if (i < N) {
+#pragma unroll
+            for (int gg = 0; gg < 8; ++gg) {
+              const int64_t p = pb + 16 * gg;
+              if (p >= ngl) continue;
+              double v0 = alpha * acc[q][2 * gg][j], v1 = alpha * acc[q][2 * gg + 1][j];
+              const bool two = p + 1 < ngl;
+              if (C) {
+                if (two) {
+                  const double2 cv = *reinterpret_cast<const double2*>(C + (int64_t)i * ld + p);
+                  v0 += beta * cv.x;
+                  v1 += beta * cv.y;
+                } else {
+                  v0 += beta * C[(int64_t)i * ld + p];
+                }
+              }
+              if (!two) v1 = 0.0;
+              if (out) {
+                if (two)
+                  *reinterpret_cast<double2*>(out + (int64_t)i * ld + p) = make_double2(v0, v1);
+                else
+                  out[(int64_t)i * ld + p] = v0;
+              }
+              nrm += v0 * v0 + v1 * v1;
+            }
+          }
+          if (norms) {
+            nrm += __shfl_xor_sync(0xffffffffu, nrm, 4);
+            nrm += __shfl_xor_sync(0xffffffffu, nrm, 8);
+            nrm += __shfl_xor_sync(0xffffffffu, nrm, 16);
+            if (gq == 0 && i < N) norms[(int64_t)i * n_pt + pt] = nrm;
+          }
+        }
+      }
+    }
+  }
+}
+
+__global__ void transpose_pad_kernel(int N, int np, const double* __restrict__ M,
+                                     double* __restrict__ Mt) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)np * np) return;
+  const int i = (int)(e / np), k = (int)(e % np);
+  Mt[e] = (i < N && k < N) ? M[(int64_t)k * N + i] : 0.0;
+}
+
 }  // namespace
+
+// per-stream padded M^T scratch of the large-N mix (engines on different
+// streams / host threads never share one)
+static double* mix_big_scratch(cudaStream_t s, size_t doubles) {
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, std::pair<double*, size_t>> bufs;
+  std::lock_guard<std::mutex> g(mu);
+  auto& b = bufs[s];
+  if (b.second < doubles) {
+    if (b.first) {
+      cudaStreamSynchronize(s);
+      cudaFree(b.first);
+    }
+    b.first = nullptr;
+    b.second = 0;
+    if (cudaMalloc(&b.first, doubles * 8) != cudaSuccess) return nullptr;
+    b.second = doubles;
+  }
+  return b.first;
+}
+
+int mix_big_nblk(int64_t ngl) { return (int)((ngl + XP - 1) / XP); }
+
+int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
+                   const double* M, double alpha, const double* C, double beta, int upper,
+                   double* out, double* norms, cudaStream_t s, const double* guard) {
+  static const bool off = getenv("PO_NO_MIX_BIG") != nullptr;  // measurement: tiled LDG mix
+  static const bool dbg = getenv("PO_MIX_DEBUG") != nullptr;
+#define PO_MB_FAIL(why)                                                 \
+  do {                                                                  \
+    if (dbg) fprintf(stderr, "launch_mix_big(N=%d): %s\n", N, why);     \
+    return -1;                                                          \
+  } while (0)
+  if (off || !tma2d_available()) PO_MB_FAIL("disabled / no TMA");
+  const int np = (N + 15) & ~15;
+  double* mt = mix_big_scratch(s, (size_t)np * np);
+  if (!mt) PO_MB_FAIL("scratch");
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  int q = 0;
+  if (!make_map(&maps.m[q++], A, ld, N, XK)) PO_MB_FAIL("map A");
+  if (Ab && !make_map(&maps.m[q++], Ab, ld, N, XK)) PO_MB_FAIL("map Ab");
+  if (!make_map(&maps.m[q++], mt, np, np, XI)) PO_MB_FAIL("map Mt");
+  const int nsrc = Ab ? 2 : 1;
+  const size_t sdoubles = (size_t)(nsrc + 1) * XP * XK;
+  const size_t fixed = 1024 + 1024;  // barriers, alignment slack
+  int nst = (int)((200 * 1024 - fixed) / (sdoubles * 8));
+  if (nst > 8) nst = 8;
+  if (nst < 2) PO_MB_FAIL("shared memory");
+#undef PO_MB_FAIL
+  const size_t smem = fixed + (size_t)nst * sdoubles * 8;
+  ::po::count_launch();
+  transpose_pad_kernel<<<(unsigned)(((int64_t)np * np + 255) / 256), 256, 0, s>>>(N, np, M, mt);
+  const int n_pt = mix_big_nblk(ngl);
+  const int n_it = (N + XI - 1) / XI;
+  const int ntiles = n_pt * n_it;
+  const int grid = ntiles < nsm() ? ntiles : nsm();
+  set_smem(reinterpret_cast<const void*>(mix_big_kernel), (int)smem);
+  ::po::count_launch();
+  mix_big_kernel<<<grid, XTH, smem, s>>>(maps, Ab ? 1 : 0, N, ld, ngl, n_pt, n_it, upper, nst, sa,
+                                         alpha, C, beta, out, norms, guard);
+  return n_pt;
+}
 
 size_t gram_big_workspace_doubles(int64_t ld, int N) {
   if (N <= 48) return 0;

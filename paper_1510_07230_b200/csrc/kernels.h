@@ -139,6 +139,12 @@ int launch_directions(int N, int64_t ld, int64_t ngl, const double* W, const dou
 int launch_mix_tma(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
                    const double* M, double alpha, const double* C, double beta, int upper,
                    double* out, double* norms, cudaStream_t s, const double* guard);
+// Large-N (N > 64) mix: persistent 128-point x 128-orbital DMMA tiles fed by
+// 2D TMA (A, Ab and a padded M^T). Same contract as launch_mix; returns the
+// norm-partials row length (= mix_nblk) or -1 when unavailable.
+int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
+                   const double* M, double alpha, const double* C, double beta, int upper,
+                   double* out, double* norms, cudaStream_t s, const double* guard);
 // Batched left-multiply out_b = S X_b for X_b = rows [N][ld] at A + b * bstride
 // (valid row length ngl; ld multiple of 32, padding zero). DST transforms.
 void launch_mix_batched(int N, int64_t ld, int64_t ngl, int batch, int64_t bstride,

@@ -406,7 +406,7 @@ void Solver::init(const BRef& w0) {
   orth_energies.assign(1, e0.total);
   recovery_w = w;
   recovery_state = state;
-  if (E.N <= 48 && tma2d_available()) {
+  if (tma2d_available()) {
     E.gram(P(w), nullptr, 0.0, P(w), nullptr, 0.0, 1, E.dmat[8]);
     gww_valid = true;
   }
@@ -428,9 +428,9 @@ void Solver::enqueue_phase1(int iter) {
     const int onb = per_orbital_nblk(E.g, n);
     bool& fused = ph.fused;
     bool bb_done = false;
+    ghh_fresh = false;  // G_HH (dmat[7]) belongs to this iteration's HW only
     if (!full_grad && !(mean_abs && need_full) && n <= 48 && tma2d_available()) {
       // one pass: z, ||z||^2, ||HW - W Sigma||^2 and the BB products
-      ghh_fresh = false;
       if (need_full || !sig_valid) {
         ghh_fresh = gww_valid && sigma_dual(w, hw);
         if (!ghh_fresh) sigma(w, hw);
@@ -456,6 +456,13 @@ void Solver::enqueue_phase1(int iter) {
     } else {
       if (need_full || !sig_valid) {
         sigma(w, hw);
+        if (gww_valid) {
+          // G_HH = w (HW)^T HW: the line search's trial Grams then come from
+          // G_WW, Sigma and G_HH (launch_trial_gram) instead of a two-source
+          // pass over W - tau Z per trial
+          E.gram(P(hw), nullptr, 0.0, P(hw), nullptr, 0.0, 1, E.dmat[7]);
+          ghh_fresh = true;
+        }
         launch_copy_diag(n, E.dmat[4], E.dvec + E.off_sig(), E.s);
       }
       if (history_valid) {  // z, ||z||^2 and the BB products in one pass
@@ -720,7 +727,7 @@ bool Solver::step() {
       history_valid = true;
       last_accepted_tau = tau;
       // the accepted trial's verification Gram (post-repair if repaired) is G_WW of w
-      gww_valid = !sync_orth && E.N <= 48 && tma2d_available();
+      gww_valid = !sync_orth && tma2d_available();
       if (gww_valid) std::swap(E.dmat[8], E.dmat[2]);  // no copy: exchange the buffers
       steps_until_orth = n_org - 1;
       const bool rotation_due =

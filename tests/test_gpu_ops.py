@@ -213,6 +213,49 @@ def test_dmma_multitile(port, native, n_orb, n):
     e.close()
 
 
+@pytest.mark.parametrize("n_orb,n", [(65, (9, 9, 11)), (67, (9, 9, 11)), (128, (12, 13, 14)),
+                                     (130, (9, 9, 11)), (200, (24, 20, 22)), (260, (10, 9, 11))])
+def test_mix_big(native, n_orb, n):
+    """Large-N TMA mix (N > 64, manifold.cpp:67-85): full, upper-triangular
+    (L^{-T}, manifold.cpp:97-114), the trial rotation (W - tau Z) L^{-T} and the
+    gradient norms of D = HW - W Sigma (manifold.cpp:181-202); odd point counts
+    exercise the ragged last tile, N > 128 several orbital tiles."""
+    spec = configs.ProblemSpec("mixbig", n, (5.0, 5.0, 5.0), [], n_orb, hartree=False, xc=False)
+    e = native.engine_for(spec)
+    rng = np.random.default_rng(11 + n_orb)
+    a = rng.standard_normal((n_orb, spec.num_points))
+    b = rng.standard_normal((n_orb, spec.num_points))
+    ba, bb, out = e.block_from(a), e.block_from(b), e.alloc()
+    m = rng.standard_normal((n_orb, n_orb))
+    e.mix(ba, m, out)
+    assert rel(e.download(out), m.T @ a) < 1e-12
+    mu = np.triu(m)
+    e.set_matrix(mu)
+    e.enqueue("mix_upper", a=ba, out=out)
+    assert rel(e.download(out), mu.T @ a) < 1e-12
+    e.enqueue("rotation", a=ba, b=bb, out=out)
+    assert rel(e.download(out), mu.T @ (a - 0.3 * b)) < 1e-12
+    # orthonormalisation: Cholesky + L^{-T} on the device, then the triangular mix
+    wq = np.prod(spec.spacing)
+    pre, dev, fb = e.orthonormalize(ba, out, True)
+    assert not fb and 0.0 <= dev <= 1e-12
+    wo = e.download(out)
+    assert np.abs(wq * wo @ wo.T - np.eye(n_orb)).max() < 1e-12
+    l_ref = np.linalg.cholesky(wq * a @ a.T)
+    assert rel(wo, np.linalg.solve(l_ref, a)) < 1e-9
+    # ||HW - W Sigma||^2 per orbital on an orthonormal W with HW = S W (S symmetric)
+    q, _ = np.linalg.qr(a.T)
+    w = q.T / np.sqrt(wq)
+    s = rng.standard_normal((n_orb, n_orb))
+    s = s + s.T
+    hw = s @ w + 1e-3 * rng.standard_normal(w.shape)
+    hw = hw - 0.5 * ((hw @ w.T) * wq - (w @ hw.T) * wq) @ w  # keep <HW, W> symmetric
+    sig, dd = e.stiefel_gradient(e.block_from(w), e.block_from(hw))
+    d_ref = hw - sig.T @ w
+    assert np.allclose(dd, wq * np.einsum("ip,ip->i", d_ref, d_ref), rtol=1e-9, atol=1e-14)
+    e.close()
+
+
 def test_orthonormalize(setup, port, native):
     spec, u0, e = setup
     rng = np.random.default_rng(5)

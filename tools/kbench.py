@@ -55,16 +55,25 @@ e.enqueue("gram_sym", a=w)
 e.enqueue("cholesky")
 res["cholesky"] = timeit(e, lambda: e.enqueue("cholesky"))
 res["rotation"] = timeit(e, lambda: e.enqueue("rotation", a=w, b=z, out=out))
+res["mix_upper"] = timeit(e, lambda: e.enqueue("mix_upper", a=w, out=out))
+res["mix_full"] = timeit(e, lambda: e.enqueue("mix", a=w, out=out))
 res["rotation_fused"] = timeit(e, lambda: e.enqueue("rotation_fused", a=w, b=z, out=out))
 e.enqueue("gram", a=hw, b=w)
 res["directions"] = timeit(e, lambda: e.enqueue("directions", a=w, b=hw, out=out))
 res["density_xc"] = timeit(e, lambda: e.enqueue("density_xc", a=w))
 res["poisson"] = timeit(e, lambda: e.enqueue("poisson"), reps=10)
-hbm = 6547.2
+hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6547.2
+fp64 = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["fp64_tflops"]
+ng = spec.num_points
+tri, full = N * (N + 1) * ng, 2 * N * N * ng
+flops = {"gram_sym(G2)": tri, "gram_trial(G0)": tri, "gram_nonsym(Sigma)": full, "rotation": tri,
+         "mix_upper": tri, "mix_full": full, "rotation_fused": 2 * tri}
 bytes_ = {"hamiltonian": 2 * blk, "gram_sym(G2)": blk, "gram_trial(G0)": 2 * blk,
           "gram_nonsym(Sigma)": 2 * blk, "rotation": 3 * blk, "rotation_fused": 3 * blk, "directions": 5 * blk,
-          "density_xc": blk}
+          "density_xc": blk, "mix_upper": 2 * blk, "mix_full": 2 * blk}
 for k, v in res.items():
     frac = f"{bytes_[k] / v / 1e3 / hbm:.2f} of HBM" if k in bytes_ else ""
-    print(f"{k:22s} {v:8.1f} us  {frac}")
+    tf = f"  {flops[k] / v / 1e6:6.2f} TF/s = {flops[k] / v / 1e6 / fp64:.2f} of FP64" if k in flops else ""
+    print(f"{k:22s} {v:8.1f} us  {frac}{tf}")
 e.close()
