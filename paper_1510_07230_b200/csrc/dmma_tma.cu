@@ -53,23 +53,25 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 struct MapKey {
   const double* base;
   int64_t ld;
-  int rows, npad;
+  int rows, npad, bx;
   bool operator==(const MapKey& o) const {
-    return base == o.base && ld == o.ld && rows == o.rows && npad == o.npad;
+    return base == o.base && ld == o.ld && rows == o.rows && npad == o.npad && bx == o.bx;
   }
 };
 struct MapKeyHash {
   size_t operator()(const MapKey& k) const {
-    return std::hash<const void*>()(k.base) ^ (size_t)(k.ld * 31 + k.rows * 131 + k.npad);
+    return std::hash<const void*>()(k.base) ^ (size_t)(k.ld * 31 + k.rows * 131 + k.npad + k.bx * 7919);
   }
 };
 
-bool encode_map(CUtensorMap* m, const double* base, int64_t ld, int rows, int npad);
+bool encode_map(CUtensorMap* m, const double* base, int64_t ld, int rows, int npad, int bx);
 
-bool make_map(CUtensorMap* m, const double* base, int64_t ld, int rows, int npad) {
+// box {bx, npad}: bx = 16 with 128-B swizzle (the large-N tiles), otherwise
+// unswizzled rows of bx points (the small-N stages, see PADW)
+bool make_map(CUtensorMap* m, const double* base, int64_t ld, int rows, int npad, int bx = 16) {
   static std::mutex mu;
   static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-  const MapKey key{base, ld, rows, npad};
+  const MapKey key{base, ld, rows, npad, bx};
   {
     std::lock_guard<std::mutex> g(mu);
     auto it = cache.find(key);
@@ -78,20 +80,20 @@ bool make_map(CUtensorMap* m, const double* base, int64_t ld, int rows, int npad
       return true;
     }
   }
-  if (!encode_map(m, base, ld, rows, npad)) return false;
+  if (!encode_map(m, base, ld, rows, npad, bx)) return false;
   std::lock_guard<std::mutex> g(mu);
   if (cache.size() > 4096) cache.clear();
   cache.emplace(key, *m);
   return true;
 }
 
-// rows x ld doubles, row stride ld; box {16, npad}
-bool encode_map(CUtensorMap* m, const double* base, int64_t ld, int rows, int npad) {
+// rows x ld doubles, row stride ld; box {bx, npad}
+bool encode_map(CUtensorMap* m, const double* base, int64_t ld, int rows, int npad, int bx) {
   auto fn = encode_fn();
   if (!fn || !base) return false;
   cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
-  cuuint32_t box[2] = {BOX, (cuuint32_t)npad};
+  cuuint32_t box[2] = {(cuuint32_t)bx, (cuuint32_t)npad};
   cuuint32_t es[2] = {1, 1};
   static const int promo = getenv("PO_TMA_PROMO") ? atoi(getenv("PO_TMA_PROMO")) : 3;
   const CUtensorMapL2promotion pr = promo == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
@@ -99,7 +101,8 @@ bool encode_map(CUtensorMap* m, const double* base, int64_t ld, int rows, int np
                                     : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                                  : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            bx == BOX ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, pr,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -108,8 +111,19 @@ struct Maps {
   CUtensorMap m[4];
 };
 
+// Small-N stage layout. Measured (tools/tma2d_probe.cu, profiles/r1_tma2d_probe.txt):
+// a 2D-TMA stream of 128-B box rows (16 points, 128-B swizzle) tops out at
+// ~4.2 TB/s on B200, boxes of >= 64-point rows (unswizzled) at 6.0-6.6 TB/s.
+// So a stage of 64 points is ONE box per source, {PADW points x N rows}: the
+// 8 extra points per row (the next stage's first points, L2 hits) pad the
+// shared-memory row stride to 72 doubles, which makes both fragment access
+// patterns conflict-free: 8 rows x 16-B pairs (Gram operands) and 4 rows x
+// 8 consecutive points (rotation / mix operands), because row r starts at
+// 16-byte chunk 4 r (mod 8).
+constexpr int PADW = 72;
+
 bool make_map2(Maps& M, int i, const double* base, int64_t ld, int rows, int /*npad*/) {
-  return make_map(&M.m[i], base, ld, rows, rows);  // boxes of exactly N rows
+  return make_map(&M.m[i], base, ld, rows, rows, PADW);  // boxes of exactly N rows
 }
 
 
@@ -135,9 +149,12 @@ __device__ __forceinline__ int swz(int row, int p, int nb) {
   return r * BOX + j * 2 + (o & 1);
 }
 
-// doubles per source per stage (4 boxes of nb rows, padded to 8 rows)
+// small-N stage: element (row, point p < 64) of a source's area
+__device__ __forceinline__ int pad(int row, int p) { return row * PADW + p; }
+
+// doubles per source per stage (nb padded rows, areas 128-B aligned)
 __host__ __device__ constexpr size_t qs_of(int nb) {
-  return (size_t)((4 * nb + 7) & ~7) * BOX;
+  return ((size_t)nb * PADW + 15) & ~(size_t)15;
 }
 
 struct TCfg {
@@ -162,8 +179,8 @@ TCfg tcfg(int nsrc, int npad, size_t extra_doubles) {
   c.nst = (int)(avail / c.stage_doubles);
   if (c.nst > 8) c.nst = 8;
   if (c.nst < 2) c.nst = 2;
-  // + barriers / alignment slack + 1 KB tail (fragment rows past the last box)
-  c.smem = 3072 + ((size_t)c.nst * c.stage_doubles + extra_doubles) * 8;
+  // + barriers / alignment slack + tail (fragment rows past N: up to 7 padded rows)
+  c.smem = 3072 + 8 * PADW * 8 + ((size_t)c.nst * c.stage_doubles + extra_doubles) * 8;
   return c;
 }
 
@@ -175,8 +192,7 @@ __device__ __forceinline__ void tma_produce(const CUtensorMap* maps, int nsrc, i
                                             double* stage0, uint64_t* full, uint64_t* empty) {
   const int lane = threadIdx.x & 31;
   const int nstage = kend > kbeg ? (int)((kend - kbeg + TKS - 1) / TKS) : 0;
-  const uint32_t bytes = (uint32_t)(nsrc * (TKS / BOX) * npad * BOX * 8);
-  const int nbox = nsrc * (TKS / BOX);
+  const uint32_t bytes = (uint32_t)(nsrc * npad * PADW * 8);
   const size_t qs = qs_of(npad);
   for (int st = 0; st < nstage; ++st) {
     const int s = st % nst;
@@ -187,10 +203,7 @@ __device__ __forceinline__ void tma_produce(const CUtensorMap* maps, int nsrc, i
     __syncwarp();
     const int64_t k0 = kbeg + (int64_t)st * TKS;
     double* sb = stage0 + (size_t)s * sdoubles;
-    for (int e = lane; e < nbox; e += 32) {
-      const int q = e / (TKS / BOX), b = e % (TKS / BOX);
-      tma_load_2d(sb + q * qs + (size_t)b * npad * BOX, &maps[q], (int)(k0 + b * BOX), 0, &full[s]);
-    }
+    if (lane < nsrc) tma_load_2d(sb + lane * qs, &maps[lane], (int)k0, 0, &full[s]);
   }
 }
 
@@ -292,7 +305,7 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
         auto row8 = [&](int row, int q, double2 (&v)[4]) {
 #pragma unroll
           for (int m = 0; m < 4; ++m)
-            v[m] = *reinterpret_cast<const double2*>(sbuf + q * qstride + swz(row, c + 2 * m, NB));
+            v[m] = *reinterpret_cast<const double2*>(sbuf + q * qstride + pad(row, c + 2 * m));
         };
         auto dot8 = [](const double2 (&x)[4], const double2 (&y)[4], double t) {
 #pragma unroll
@@ -324,7 +337,7 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
       double2 a[FD > 0 ? FD : 1], b[SYM ? 1 : (FD > 0 ? FD : 1)];
 #pragma unroll
       for (int f = 0; f < FD; ++f) {
-        const int off = swz(8 * f + gq, c + 2 * t4, NB);  // 16-B aligned pair of points
+        const int off = pad(8 * f + gq, c + 2 * t4);  // 16-B aligned pair of points
         a[f] = *reinterpret_cast<const double2*>(sbuf + off);
         if (qa_b >= 0) {
           const double2 z = *reinterpret_cast<const double2*>(sbuf + qa_b * qstride + off);
@@ -579,7 +592,7 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
         double av[2 * F];
 #pragma unroll
         for (int ks = 0; ks < 2 * F; ++ks) {
-          const int off = swz(4 * ks + t4, c + gq, NB);
+          const int off = pad(4 * ks + t4, c + gq);
           av[ks] = sbuf[off];
           if (has_ab) av[ks] += sa * sbuf[qstride + off];
           if (4 * ks + t4 >= N) av[ks] = 0.0;  // rows past N alias the next box
@@ -596,7 +609,7 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
       } else {
         for (int ks = 0; ks < ksteps; ++ks) {
           const int krow = 4 * ks + t4;
-          const int off = swz(krow, c + gq, NB);
+          const int off = pad(krow, c + gq);
           double av = sbuf[off];
           if (has_ab) av += sa * sbuf[qstride + off];
           if (krow >= N) av = 0.0;
@@ -612,7 +625,7 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
           const int i = 8 * fi + 2 * t4 + j;
           if (p < ngl && i < N) {
             double v = alpha * acc[fi][j];
-            if (qc >= 0) v += beta * sbuf[qc * qstride + swz(i, c + gq, NB)];
+            if (qc >= 0) v += beta * sbuf[qc * qstride + pad(i, c + gq)];
             if (out) out[(int64_t)i * ld + p] = v;
             nrm[fi][j] += v * v;
           }
@@ -745,7 +758,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
         double av[2 * F];
 #pragma unroll
         for (int ks = 0; ks < 2 * F; ++ks) {
-          const int off = swz(4 * ks + t4, c + gq, NB);
+          const int off = pad(4 * ks + t4, c + gq);
           av[ks] = sbuf[off];
           if (nsrc == 2) av[ks] += sa * sbuf[qstride + off];
           if (4 * ks + t4 >= N) av[ks] = 0.0;  // rows past N alias the next box
@@ -781,7 +794,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
           if (i < N) {
             const double v = acc[fi][j];
             if (p < ngl) out[(int64_t)i * ld + p] = v;
-            sbuf[swz(i, c + gq, NB)] = v;
+            sbuf[pad(i, c + gq)] = v;
             dsum += v * v;
           }
         }
@@ -809,7 +822,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
           double2 bv[4];
 #pragma unroll
           for (int m = 0; m < 4; ++m)
-            bv[m] = *reinterpret_cast<const double2*>(sbuf + swz(rr, c + 2 * m, NB));
+            bv[m] = *reinterpret_cast<const double2*>(sbuf + pad(rr, c + 2 * m));
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int i = lane + 32 * h;
@@ -817,7 +830,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
             double t = racc[h][r];
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
-              const double2 av = *reinterpret_cast<const double2*>(sbuf + swz(i, c + 2 * m, NB));
+              const double2 av = *reinterpret_cast<const double2*>(sbuf + pad(i, c + 2 * m));
               t = fma(av.y, bv[m].y, fma(av.x, bv[m].x, t));
             }
             racc[h][r] = t;
@@ -827,7 +840,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
       double2 a[FD > 0 ? FD : 1];
 #pragma unroll
       for (int f = 0; f < FD; ++f)
-        a[f] = *reinterpret_cast<const double2*>(sbuf + swz(8 * f + gq, c + 2 * t4, NB));
+        a[f] = *reinterpret_cast<const double2*>(sbuf + pad(8 * f + gq, c + 2 * t4));
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       int q = 0;
@@ -997,7 +1010,7 @@ __global__ void __launch_bounds__(TTH, 1) directions_tma_kernel(
       if constexpr (DD) {
         for (int ks = 0; ks < ksteps; ++ks) {
           const int krow = 4 * ks + t4;
-          const double av = krow < N ? sbuf[swz(krow, c + gq, NB)] : 0.0;
+          const double av = krow < N ? sbuf[pad(krow, c + gq)] : 0.0;
 #pragma unroll
           for (int fi = 0; fi < F; ++fi) dmma_8x8x4(acc[fi], av, Ms[krow * NPAD + 8 * fi + gq]);
         }
@@ -1008,7 +1021,7 @@ __global__ void __launch_bounds__(TTH, 1) directions_tma_kernel(
         for (int j = 0; j < 2; ++j) {
           const int i = 8 * fi + 2 * t4 + j;
           if (p < ngl && i < N) {
-            const int off = swz(i, c + gq, NB);
+            const int off = pad(i, c + gq);
             const double wv = sbuf[off], hv = sbuf[qstride + off];
             if constexpr (DD) {
               double d = -acc[fi][j];

@@ -342,9 +342,12 @@ __global__ void __launch_bounds__(32 * (TYR + 1), 1) hamiltonian4_kernel(
   __shared__ double red[3 * 32];
   const int64_t n1 = g.n1, n2 = g.n2, plane = g.plane;
   const int64_t urow = (TYR + 2) * n2, vrow = TYR * n2;
-  const int64_t y0 = (int64_t)blockIdx.x * TYR;
-  const int i = blockIdx.z;
-  const int64_t zs = (int64_t)blockIdx.y * zc;
+  // the orbital is the fastest grid index: CTAs resident together share one
+  // (y-tile, z-chunk) of v_local (and, when it exceeds L2 — 134 MB at 256^3 —
+  // it is read from HBM once per tile instead of once per orbital)
+  const int i = blockIdx.x;
+  const int64_t y0 = (int64_t)blockIdx.y * TYR;
+  const int64_t zs = (int64_t)blockIdx.z * zc;
   const int64_t ze = min(zs + (int64_t)zc, g.nz);
   const int nplanes = (int)(ze - zs) + 2;  // zs-1 .. ze
   const double* ui = u + (int64_t)i * g.ld;
@@ -481,8 +484,8 @@ __global__ void __launch_bounds__(32 * (TYR + 1), 1) hamiltonian4_kernel(
 #pragma unroll
       for (int q = 0; q < 3; ++q) v[q] = warp_sum(lane < TYR ? red[q * 32 + lane] : 0.0);
       if (lane == 0) {
-        const int nblk = gridDim.x * gridDim.y;
-        const int b = blockIdx.x + gridDim.x * blockIdx.y;
+        const int nblk = gridDim.y * gridDim.z;
+        const int b = blockIdx.y + gridDim.y * blockIdx.z;
 #pragma unroll
         for (int q = 0; q < 3; ++q) partials[((int64_t)q * N + i) * nblk + b] = v[q];
       }
@@ -495,7 +498,7 @@ void launch_h4(const SlabGeom& g, int N, const double* u, const double* lo, cons
                const double* vloc, const double* vext, double* out, double* partials,
                cudaStream_t s, int zc = ZCHUNK2, size_t budget = 100 * 1024) {
   const PlaneRing r = plane_ring(g, TYR, budget);
-  dim3 grid((unsigned)((g.n1 + TYR - 1) / TYR), (unsigned)((g.nz + zc - 1) / zc), N);
+  dim3 grid((unsigned)N, (unsigned)((g.n1 + TYR - 1) / TYR), (unsigned)((g.nz + zc - 1) / zc));
   dim3 block(TX, TYR + 1);
   switch ((g.n2 + 31) / 32) {
 #define PO_H4(JJ)                                                                          \
@@ -510,15 +513,25 @@ void launch_h4(const SlabGeom& g, int N, const double* u, const double* lo, cons
   }
 }
 
-// Production shape (tools/hu_variants.py sweep on B200, C2 block): 6 rows per
-// CTA, 32 planes per CTA, 56 KB ring (4 CTAs / SM): 85 us = 85% of the measured
-// HBM peak after the register z-march (70.6% before it, 62% at 8 rows / 100 KB,
-// 43.6% for the first kernel). Measured and dropped: two or three rows per
+// Production shapes (tools/hu_shape_sweep.py on B200, interleaved rounds,
+// profiles/r1_hu_shape_sweep.json): rows per CTA / planes per CTA / ring budget
+// by row length. Six rows and a 56 KB ring (4 CTAs / SM) at 96^3 (85% of the
+// measured HBM peak after the register z-march; 70.6% before it, 43.6% for the
+// first kernel); eight rows win at 64-point rows (fewer, fuller CTAs: 0.77-0.87
+// vs 0.63-0.71) and at 128-192 (0.86-0.93); 256-point rows keep six rows (eight
+// would leave one CTA per SM). Measured and dropped: two or three rows per
 // consumer warp (y neighbours from registers, 5 loads per point): 81% / 71% —
 // fewer warps per SM hide less latency than the saved loads buy.
-constexpr int H4_TYR = 6;
-constexpr int H4_ZC = 32;
-constexpr size_t H4_BUDGET = 56 * 1024;
+struct H4Shape {
+  int tyr, zc;
+  size_t budget;
+};
+H4Shape h4_shape(const SlabGeom& g) {
+  if (g.n2 <= 64) return {8, 32, 56 * 1024};
+  if (g.n2 <= 96) return {6, 64, 56 * 1024};
+  if (g.n2 <= 192) return {8, 48, 70 * 1024};
+  return {6, 32, 56 * 1024};
+}
 
 bool h4_supported(const SlabGeom& g) {
   // bulk copies need 16-byte multiples / alignment: even n2 (plane rows of 8 n2 bytes)
@@ -532,8 +545,10 @@ int hamiltonian3_nblk(const SlabGeom& g) {
 }
 
 int hamiltonian2_nblk(const SlabGeom& g) {
-  if (h4_supported(g))  // TMA ring: (y-tile, z-chunk) grid
-    return (int)((g.n1 + H4_TYR - 1) / H4_TYR) * (int)((g.nz + H4_ZC - 1) / H4_ZC);
+  if (h4_supported(g)) {  // TMA ring: (y-tile, z-chunk) grid
+    const H4Shape h = h4_shape(g);
+    return (int)((g.n1 + h.tyr - 1) / h.tyr) * (int)((g.nz + h.zc - 1) / h.zc);
+  }
   HGrid h = hgrid(g);
   return h.ntx * h.nty * (int)((g.nz + ZCHUNK2 - 1) / ZCHUNK2);
 }
@@ -543,12 +558,20 @@ void launch_hamiltonian2(const SlabGeom& g, int N, const double* u, const double
                          double* hu, double* partials, cudaStream_t s) {
   if (h4_supported(g)) {  // production path: TMA plane ring
     ::po::count_launch();
-    if (v_ext)
-      launch_h4<true, H4_TYR>(g, N, u, halo_lo, halo_hi, v_local, v_ext, hu, partials, s, H4_ZC,
-                              H4_BUDGET);
-    else
-      launch_h4<false, H4_TYR>(g, N, u, halo_lo, halo_hi, v_local, nullptr, hu, partials, s,
-                               H4_ZC, H4_BUDGET);
+    const H4Shape h = h4_shape(g);
+    if (h.tyr == 8) {
+      if (v_ext)
+        launch_h4<true, 8>(g, N, u, halo_lo, halo_hi, v_local, v_ext, hu, partials, s, h.zc, h.budget);
+      else
+        launch_h4<false, 8>(g, N, u, halo_lo, halo_hi, v_local, nullptr, hu, partials, s, h.zc,
+                            h.budget);
+    } else {
+      if (v_ext)
+        launch_h4<true, 6>(g, N, u, halo_lo, halo_hi, v_local, v_ext, hu, partials, s, h.zc, h.budget);
+      else
+        launch_h4<false, 6>(g, N, u, halo_lo, halo_hi, v_local, nullptr, hu, partials, s, h.zc,
+                            h.budget);
+    }
     return;
   }
   HGrid h = hgrid(g);
@@ -665,6 +688,23 @@ int launch_hamiltonian_variant(int v, const SlabGeom& g, int N, const double* u,
       if (!h4_supported(g)) return -1;
       launch_h4<false, 8>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s, 32,
                           72 * 1024);
+      return 0;
+    case 24:
+    case 25:
+      if (!h4_supported(g)) return -1;
+      launch_h4<false, 3>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s,
+                          v == 24 ? 32 : 64, 48 * 1024);
+      return 0;
+    case 26:
+      if (!h4_supported(g)) return -1;
+      launch_h4<false, 4>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s, 64,
+                          48 * 1024);
+      return 0;
+    case 27:
+    case 28:
+      if (!h4_supported(g)) return -1;
+      launch_h4<false, 2>(g, N, u, nullptr, nullptr, v_local, nullptr, hu, partials, s,
+                          v == 27 ? 32 : 64, 40 * 1024);
       return 0;
   }
   return -1;

@@ -1,0 +1,64 @@
+"""H.u ring-shape sweep across grid sizes (BASELINE configs 2/3/5 grids): every
+TMA plane-ring variant (rows per CTA, planes per CTA, ring budget) of
+po_enqueue(PO_OP_HAMILTONIAN_VARIANT + v), CUDA events, HBM fraction of the
+16 B per orbital.point + 8 B per point algorithmic traffic."""
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1510_07230_b200 import configs, native  # noqa: E402
+
+HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6547.2
+VARIANTS = {8: "r8 z32 100K", 9: "r8 z32 56K", 10: "r4 z32 32K", 11: "r8 z16 70K", 12: "r8 z32 70K",
+            13: "r4 z48 40K", 14: "r8 z48 70K", 15: "r6 z32 56K", 16: "r6 z16 56K", 17: "r6 z48 56K",
+            18: "r6 z64 56K", 19: "r6 z32 40K", 20: "r6 z32 84K", 21: "r6 z96 56K", 22: "r4 z32 40K",
+            23: "r8 z32 72K", 24: "r3 z32 48K", 25: "r3 z64 48K", 26: "r4 z64 48K", 27: "r2 z32 40K",
+            28: "r2 z64 40K"}
+cases = [(int(a), int(b)) for a, b in (x.split("x") for x in
+         os.environ.get("HU_CASES", "64x64,64x256,96x33,128x64,128x128,192x64,256x64").split(","))]
+res = []
+for n, N in cases:
+    spec = configs.config5(n, N)
+    e = native.engine_for(spec)
+    u, out = e.alloc(), e.alloc()
+    e.random_block(u, 42)
+    e.build_hamiltonian(u, hartree=False, xc=True)
+    st = torch.cuda.ExternalStream(e.stream)
+    bytes_ = 16.0 * N * e.ngl + 8.0 * e.ngl
+    row = {"grid": n, "N": N}
+    cand = [(0, "production")] + [(v, VARIANTS[v]) for v in
+                                  [int(x) for x in os.environ.get("HU_V", "9,14,15,17,18,26").split(",")]]
+    ops = {}
+    for v, name in cand:
+        ops[name] = (lambda: e.enqueue("hamiltonian", a=u, out=out)) if v == 0 else \
+            (lambda v=v: e._chk(e._lib.po_enqueue(e.h, 100 + v, u, -1, out)))
+    times = {name: [] for _, name in cand}
+    for rnd in range(3):  # interleaved rounds: clock / thermal drift hits every variant alike
+        for _, name in cand:
+            try:
+                op = ops[name]
+                op()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                for _ in range(5):
+                    op()
+                b.record(st)
+                b.synchronize()
+                times[name].append(a.elapsed_time(b) / 5)
+            except Exception:  # variant unavailable at this shape
+                pass
+    for name, ts in times.items():
+        row[name] = round(bytes_ / sorted(ts)[len(ts) // 2] / 1e6 / HBM, 3) if ts else None
+    best = max((k for k in row if k not in ("grid", "N") and row[k]), key=lambda k: row[k])
+    print(f"{n}^3 N={N}: production {row['production']}  best {best} {row[best]}", flush=True)
+    print("   ", {k: v for k, v in row.items() if k not in ("grid", "N")}, flush=True)
+    res.append(row)
+    e.close()
+    torch.cuda.empty_cache()
+os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+json.dump(res, open(os.path.join(ROOT, "gpurun_out", "hu_shape_sweep.json"), "w"), indent=1)
