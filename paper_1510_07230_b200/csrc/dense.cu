@@ -335,7 +335,9 @@ __global__ void __launch_bounds__(TR * 32) cholesky_inv_gs_kernel(int N, const d
   if (guard && *guard == 0.0) return;
   constexpr int NMAX = TR * A;
   static_assert(TR * A == 32 * B, "square slot grid");
-  __shared__ double cg[2][NMAX], cv[2][NMAX], dj[NMAX];
+  // column j of the working square, one array: col[p] = V(p, j) for p < j,
+  // 1 for p == j, G^(j)(p, j) for p > j; the pivot d_j and 1 / d_j beside it
+  __shared__ double col[2][NMAX], piv[2][2], dj[NMAX];
   const int tc = threadIdx.x & 31, tr = threadIdx.x >> 5;
   double x[A][B];
 #pragma unroll
@@ -344,42 +346,50 @@ __global__ void __launch_bounds__(TR * 32) cholesky_inv_gs_kernel(int N, const d
     for (int b = 0; b < B; ++b) {
       const int p = tr + TR * a, q = tc + 32 * b;
       x[a][b] = (p < N && q < N && p >= q) ? G[p * N + q] : 0.0;
-      if (q == 0 && p < N) cg[0][p] = x[a][b];
+      if (q == 0 && p < N) {
+        col[0][p] = p == 0 ? 1.0 : x[a][b];
+        if (p == 0) {
+          piv[0][0] = x[a][b];
+          piv[0][1] = 1.0 / x[a][b];
+        }
+      }
     }
-  if (threadIdx.x == 0) cv[0][0] = 1.0;
   __syncthreads();
   bool fail = false;
   for (int j = 0; j < N; ++j) {
     const int buf = j & 1;
-    const double d = cg[buf][j];
+    const double d = piv[buf][0];
     if (!(d > 0.0)) {  // uniform: every thread reads the same pivot
       fail = true;
       break;
     }
-    const double dinv = 1.0 / d;
+    const double dinv = piv[buf][1];
     if (threadIdx.x == 0) dj[j] = d;
+    double cp[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int p = tr + TR * a;
+      cp[a] = p < N ? col[buf][p] : 0.0;
+    }
 #pragma unroll
     for (int b = 0; b < B; ++b) {
+      if (32 * b + 31 <= j) continue;  // whole warp-column already final
       const int q = tc + 32 * b;
-      if (q <= j || q >= N) continue;
-      const double cq = cg[buf][q] * dinv;
+      const bool qa = q > j && q < N;
+      const double cq = qa ? col[buf][q] * dinv : 0.0;
 #pragma unroll
       for (int a = 0; a < A; ++a) {
         const int p = tr + TR * a;
-        if (p >= N) continue;
-        if (p >= q) {
-          x[a][b] -= cg[buf][p] * cq;
-        } else if (p <= j) {
-          x[a][b] -= cv[buf][p] * cq;
-        } else {
-          continue;
-        }
-        if (q == j + 1) {  // column j + 1 is final: publish it for the next step
-          if (p >= q) {
-            cg[buf ^ 1][p] = x[a][b];
-            if (p == q) cv[buf ^ 1][p] = 1.0;
+        // Schur element (p >= q > j) or V element (p <= j < q); rows in (j, q) wait
+        const bool act = qa && (p >= q || p <= j);
+        x[a][b] = fma(-(act ? cp[a] : 0.0), cq, x[a][b]);
+        if (q == j + 1 && p < N) {  // column j + 1 is final: publish it
+          if (p == q) {
+            col[buf ^ 1][p] = 1.0;
+            piv[buf ^ 1][0] = x[a][b];
+            piv[buf ^ 1][1] = 1.0 / x[a][b];
           } else {
-            cv[buf ^ 1][p] = x[a][b];
+            col[buf ^ 1][p] = x[a][b];
           }
         }
       }
@@ -595,21 +605,24 @@ __global__ void __launch_bounds__(256) inv_sqrt_kernel(int N, const double* __re
   }
 }
 
-__global__ void __launch_bounds__(256) matrix_stats_kernel(int N, const double* __restrict__ G,
-                                                           double* __restrict__ out,
-                                                           const double* __restrict__ guard) {
+__global__ void __launch_bounds__(1024) matrix_stats_kernel(int N, const double* __restrict__ G,
+                                                            double* __restrict__ out,
+                                                            const double* __restrict__ guard) {
   if (guard && *guard == 0.0) return;
   __shared__ double red[4][32];
   double dev = 0.0, asym = 0.0, off = 0.0, dg = 0.0;
-  for (int64_t e = threadIdx.x; e < (int64_t)N * N; e += blockDim.x) {
-    const int i = (int)(e / N), j = (int)(e % N);
-    const double v = G[e];
-    const double d = fabs(v - (i == j ? 1.0 : 0.0));
-    dev = (d > dev || isnan(d)) ? d : dev;
-    asym = fmax(asym, fabs(v - G[(int64_t)j * N + i]));
-    if (i == j) dg = fmax(dg, d);
-    else off = fmax(off, d);
-  }
+  // warp per row, lanes along the row (32-bit index math; the transposed
+  // element comes from L1/L2)
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = threadIdx.x >> 5; i < N; i += nw)
+    for (int j = lane; j < N; j += 32) {
+      const double v = G[i * N + j];
+      const double d = fabs(v - (i == j ? 1.0 : 0.0));
+      dev = (d > dev || isnan(d)) ? d : dev;
+      asym = fmax(asym, fabs(v - G[j * N + i]));
+      if (i == j) dg = fmax(dg, d);
+      else off = fmax(off, d);
+    }
   double v[4] = {dev, asym, off, dg};
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -617,13 +630,13 @@ __global__ void __launch_bounds__(256) matrix_stats_kernel(int N, const double* 
       const double x = __shfl_xor_sync(0xffffffffu, v[q], o);
       v[q] = (x > v[q] || isnan(x)) ? x : v[q];
     }
-    if ((threadIdx.x & 31) == 0) red[q][threadIdx.x >> 5] = v[q];
+    if (lane == 0) red[q][threadIdx.x >> 5] = v[q];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int q = 0; q < 4; ++q) {
       double m = 0.0;
-      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = (red[q][k] > m || isnan(red[q][k])) ? red[q][k] : m;
+      for (int k = 0; k < nw; ++k) m = (red[q][k] > m || isnan(red[q][k])) ? red[q][k] : m;
       out[q] = m;
     }
   }
@@ -734,7 +747,7 @@ void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, do
     else if (N <= 64)
       cholesky_inv_gs_kernel<16, 4, 2><<<1, 512, 0, s>>>(N, G, M, stats, guard);
     else
-      cholesky_inv_gs_kernel<16, 8, 4><<<1, 512, 0, s>>>(N, G, M, stats, guard);
+      cholesky_inv_gs_kernel<32, 4, 4><<<1, 1024, 0, s>>>(N, G, M, stats, guard);
     return;
   }
   // measured (tools/kbench-style, one launch): register kernel 6 / 12 / 29 us at
@@ -794,7 +807,7 @@ void launch_inv_sqrt_from_eig(int N, const double* evals, const double* evecs, d
 void launch_matrix_stats(int N, const double* G, double* out, cudaStream_t s,
                          const double* guard) {
   ::po::count_launch();
-  matrix_stats_kernel<<<1, 256, 0, s>>>(N, G, out, guard);
+  matrix_stats_kernel<<<1, N <= 32 ? 256 : 1024, 0, s>>>(N, G, out, guard);
 }
 
 }  // namespace po

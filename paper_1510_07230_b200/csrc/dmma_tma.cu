@@ -1,13 +1,15 @@
-// Small-N (N <= 64) tall-skinny contractions fed by 2D tensor-map TMA.
+// Tall-skinny FP64 tensor-core contractions fed by 2D tensor-map TMA: small-N (N <= 64)
+// streamed stages (first part of this file) and large-N tiles (gram_big / mix_big).
 //
-// Measured on B200 (profiles/r1_tma_probe.txt): 1D bulk copies are request-rate
-// bound — one 512 B row segment per request caps a ring at ~2.1 TB/s — so the
-// stage of an N-row block is fetched as 2D boxes {16 points x NPAD rows}
-// (NPAD x 128 B = 5 KB at N = 33) with cp.async.bulk.tensor: one request per
-// box, rows >= N zero-filled by the TMA unit (out-of-bounds fill), 128-byte
-// swizzle so the DMMA fragment reads (8 rows x one 16-B chunk) are
-// bank-conflict free. A producer warp keeps an NST-deep ring full; eight
-// consumer warps run mma.sync.m8n8k4.f64 (DMMA) from shared memory.
+// Small-N stages (measured on B200, profiles/r1_tma_probe.txt and
+// r1_tma2d_probe.txt): 1D bulk copies are request-rate bound (512 B per request
+// caps a ring at ~2.1 TB/s), and so are 2D boxes of 128-B rows (16 points,
+// 128-B swizzle: ~4.2 TB/s); rows of >= 64 points reach 6+ TB/s. So a stage of
+// 64 points is one cp.async.bulk.tensor box {72 points x N rows} per source
+// (rows >= N never read; the 8 extra points pad the shared-memory row stride so
+// the DMMA fragment reads are bank-conflict free, see PADW). A producer warp
+// keeps an NST-deep ring full; eight consumer warps run mma.sync.m8n8k4.f64
+// (DMMA) from shared memory.
 //   gram: G = w (A + sa Ab)^T (B + sb Bb)        (manifold.cpp:41-61)
 //   mix : out = alpha (A + sa Ab) M + beta C     (manifold.cpp:67-85, 181-202)
 #include <cuda.h>
@@ -202,6 +204,28 @@ __device__ __forceinline__ void tma_produce(const CUtensorMap* maps, int nsrc, i
     }
     __syncwarp();
     const int64_t k0 = kbeg + (int64_t)st * TKS;
+    double* sb = stage0 + (size_t)s * sdoubles;
+    if (lane < nsrc) tma_load_2d(sb + lane * qs, &maps[lane], (int)k0, 0, &full[s]);
+  }
+}
+
+// producer of a small-N stage of ks points (one box {pw points x npad rows} per source)
+__device__ __forceinline__ void tma_produce_w(const CUtensorMap* maps, int nsrc, int npad,
+                                              int64_t kbeg, int64_t kend, int nst, size_t sdoubles,
+                                              double* stage0, uint64_t* full, uint64_t* empty, int ks,
+                                              int pw) {
+  const int lane = threadIdx.x & 31;
+  const int nstage = kend > kbeg ? (int)((kend - kbeg + ks - 1) / ks) : 0;
+  const uint32_t bytes = (uint32_t)(nsrc * npad * pw * 8);
+  const size_t qs = ((size_t)npad * pw + 15) & ~(size_t)15;
+  for (int st = 0; st < nstage; ++st) {
+    const int s = st % nst;
+    if (lane == 0) {
+      if (st >= nst) mbar_wait(&empty[s], ((uint32_t)(st / nst) & 1u) ^ 1u);
+      mbar_arrive_expect_tx(&full[s], bytes);
+    }
+    __syncwarp();
+    const int64_t k0 = kbeg + (int64_t)st * ks;
     double* sb = stage0 + (size_t)s * sdoubles;
     if (lane < nsrc) tma_load_2d(sb + lane * qs, &maps[lane], (int)k0, 0, &full[s]);
   }
@@ -667,8 +691,13 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
 // so the trial's verification Gram and density passes over the block vanish.
 // The warp's rotated 8-point chunk goes back into its own slot of the stage
 // (same swizzled layout as the source), from where the Gram fragments are read.
-template <int F, int R>
-__global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
+// CW consumer warps of 8 points each (stage = 8 CW points): CW = 8 keeps L^{-T}
+// in registers next to a producer warpgroup (setmaxnreg); CW = 12 reads it from
+// shared memory and has one producer warp (13 warps, at most 4 per SM
+// sub-partition: 128 registers; 1.5x the warps in flight for this
+// latency-bound pass)
+template <int F, int R, int CW>
+__global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused_kernel(
     const __grid_constant__ Maps maps, int nsrc, int N, int64_t ld, int64_t ngl, int64_t pchunk,
     int nst, double sa, const double* __restrict__ M, double* __restrict__ out,
     double* __restrict__ ws, double occ, int xc, double* __restrict__ rho, double* __restrict__ vxc,
@@ -677,6 +706,9 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
   if (sa_dev) sa = *sa_dev;  // trial scale decided on the device (bb_tau_kernel)
   constexpr int NPAD = 8 * F;
   constexpr int FD = R > 0 ? F - 1 : F;
+  constexpr int KS = 8 * CW;                 // points per stage
+  constexpr int PW = KS + 8;                 // padded row (conflict-free, see PADW)
+  constexpr int NT = CW == 8 ? TTH : (CW + 1) * 32;
   constexpr int NP = FD * (FD + 1) / 2;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
@@ -684,17 +716,17 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
   uint64_t* empty = full + 8;
   double* stage0 = reinterpret_cast<double*>(tsm + 1024);
   const int NB = N;  // box rows: no zero-filled padding rows in the stream
-  const size_t qstride = qs_of(NB);
+  const size_t qstride = ((size_t)NB * PW + 15) & ~(size_t)15;
   const size_t sdoubles = (size_t)nsrc * qstride;
   double* Ms = stage0 + (size_t)nst * sdoubles;  // [NPAD][NPAD]
-  for (int e = threadIdx.x; e < NPAD * NPAD; e += TTH) {
+  for (int e = threadIdx.x; e < NPAD * NPAD; e += NT) {
     const int k = e / NPAD, i = e % NPAD;
     Ms[e] = (k < N && i < N) ? M[(int64_t)k * N + i] : 0.0;
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], TSC);
+      mbar_init(&empty[s], CW);
     }
     fence_mbar_init();
   }
@@ -707,13 +739,13 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
   const double four_pi = 4.0 * 3.141592653589793238462643383279502884;
   double* red = stage0;
   constexpr int RS = 2 * (R > 0 ? R : 1) * 32;
-  double* rred = red + (size_t)TSC * NP * 64;
-  double* ered = rred + (size_t)TSC * RS;
-  if (warp >= TSC) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-    produce(maps, nsrc, NB, pbeg, pend, nst, sdoubles, stage0, full, empty);
+  double* rred = red + (size_t)CW * NP * 64;
+  double* ered = rred + (size_t)CW * RS;
+  if (warp >= CW) {
+    if constexpr (CW == 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (warp == CW) tma_produce_w(maps.m, nsrc, NB, pbeg, pend, nst, sdoubles, stage0, full, empty, KS, PW);
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    if constexpr (CW == 8) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
     double gacc[NP > 0 ? NP : 1][2];
 #pragma unroll
     for (int q = 0; q < NP; ++q) gacc[q][0] = gacc[q][1] = 0.0;
@@ -723,17 +755,19 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
 #pragma unroll
       for (int r = 0; r < (R > 0 ? R : 1); ++r) racc[h][r] = 0.0;
     double eacc[2] = {0.0, 0.0};
-    const int nstage = pend > pbeg ? (int)((pend - pbeg + TKS - 1) / TKS) : 0;
+    const int nstage = pend > pbeg ? (int)((pend - pbeg + KS - 1) / KS) : 0;
     const int ksteps = (N + 3) / 4;
     const int c = warp * 8;
     // this lane's fragments of the upper-triangular L^{-T}; with R > 0 the last
     // fragment column (R real orbitals) is a per-lane FMA dot instead of DMMA
-    double mreg[2 * F][F];
+    double mreg[CW == 8 ? 2 * F : 1][CW == 8 ? F : 1];
+    if constexpr (CW == 8) {
 #pragma unroll
-    for (int ks = 0; ks < 2 * F; ++ks)
+      for (int ks = 0; ks < 2 * F; ++ks)
 #pragma unroll
-      for (int fi = 0; fi < F; ++fi)
-        mreg[ks][fi] = 4 * ks > 8 * fi + 7 ? 0.0 : Ms[(4 * ks + t4) * NPAD + 8 * fi + gq];
+        for (int fi = 0; fi < F; ++fi)
+          mreg[ks][fi] = 4 * ks > 8 * fi + 7 ? 0.0 : Ms[(4 * ks + t4) * NPAD + 8 * fi + gq];
+    }
     double mrem[R > 0 ? R : 1][2 * F];
 #pragma unroll
     for (int r = 0; r < (R > 0 ? R : 1); ++r)
@@ -745,9 +779,9 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
     double vx_next = (vext && t4 == 0 && pbeg + c + gq < ngl) ? __ldg(vext + pbeg + c + gq) : 0.0;
     for (int st = 0; st < nstage; ++st) {
       const int s = st % nst;
-      const int64_t p = pbeg + (int64_t)st * TKS + c + gq;
+      const int64_t p = pbeg + (int64_t)st * KS + c + gq;
       const double vx = vx_next;
-      const int64_t pn = p + TKS;
+      const int64_t pn = p + KS;
       if (vext && t4 == 0 && st + 1 < nstage && pn < ngl) vx_next = __ldg(vext + pn);
       mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
       double* sbuf = stage0 + (size_t)s * sdoubles;
@@ -758,7 +792,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
         double av[2 * F];
 #pragma unroll
         for (int ks = 0; ks < 2 * F; ++ks) {
-          const int off = pad(4 * ks + t4, c + gq);
+          const int off = (4 * ks + t4) * PW + c + gq;
           av[ks] = sbuf[off];
           if (nsrc == 2) av[ks] += sa * sbuf[qstride + off];
           if (4 * ks + t4 >= N) av[ks] = 0.0;  // rows past N alias the next box
@@ -769,7 +803,10 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
 #pragma unroll
           for (int fi = 0; fi < FD; ++fi) {
             if (4 * ks > 8 * fi + 7) continue;
-            dmma_8x8x4(acc[fi], av[ks], mreg[ks][fi]);
+            if constexpr (CW == 8)
+              dmma_8x8x4(acc[fi], av[ks], mreg[ks][fi]);
+            else
+              dmma_8x8x4(acc[fi], av[ks], Ms[(4 * ks + t4) * NPAD + 8 * fi + gq]);
           }
         }
         if constexpr (R > 0) {  // out_rr(point c + gq) = sum_k A_k M(k, rr), k split over t4
@@ -794,7 +831,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
           if (i < N) {
             const double v = acc[fi][j];
             if (p < ngl) out[(int64_t)i * ld + p] = v;
-            sbuf[pad(i, c + gq)] = v;
+            sbuf[(i) * PW + c + gq] = v;
             dsum += v * v;
           }
         }
@@ -822,7 +859,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
           double2 bv[4];
 #pragma unroll
           for (int m = 0; m < 4; ++m)
-            bv[m] = *reinterpret_cast<const double2*>(sbuf + pad(rr, c + 2 * m));
+            bv[m] = *reinterpret_cast<const double2*>(sbuf + (rr) * PW + c + 2 * m);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int i = lane + 32 * h;
@@ -830,7 +867,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
             double t = racc[h][r];
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
-              const double2 av = *reinterpret_cast<const double2*>(sbuf + pad(i, c + 2 * m));
+              const double2 av = *reinterpret_cast<const double2*>(sbuf + (i) * PW + c + 2 * m);
               t = fma(av.y, bv[m].y, fma(av.x, bv[m].x, t));
             }
             racc[h][r] = t;
@@ -840,7 +877,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
       double2 a[FD > 0 ? FD : 1];
 #pragma unroll
       for (int f = 0; f < FD; ++f)
-        a[f] = *reinterpret_cast<const double2*>(sbuf + pad(8 * f + gq, c + 2 * t4));
+        a[f] = *reinterpret_cast<const double2*>(sbuf + (8 * f + gq) * PW + c + 2 * t4);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       int q = 0;
@@ -854,7 +891,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
     }
     // CTA reductions (consumers only, ring reused): G2 partial tile -> ws[block];
     // energies -> dpart[2][grid]
-    asm volatile("bar.sync 1, %0;\n" ::"n"(TSC * 32) : "memory");
+    asm volatile("bar.sync 1, %0;\n" ::"n"(CW * 32) : "memory");
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       red[(warp * NP + q) * 64 + lane * 2] = gacc[q][0];
@@ -869,15 +906,15 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
     double e0 = warp_sum(eacc[0]), e1 = warp_sum(eacc[1]);
     if (lane == 0) {
       ered[warp] = e0;
-      ered[TSC + warp] = e1;
+      ered[CW + warp] = e1;
     }
   }
   __syncthreads();
   double* o = ws + (int64_t)blockIdx.x * NPAD * NPAD;
-  for (int e = threadIdx.x; e < NP * 64; e += TTH) {
+  for (int e = threadIdx.x; e < NP * 64; e += NT) {
     double sum = 0.0;
 #pragma unroll
-    for (int w = 0; w < TSC; ++w) sum += red[(w * NP) * 64 + e];
+    for (int w = 0; w < CW; ++w) sum += red[(w * NP) * 64 + e];
     const int q = e / 64, l = (e % 64) / 2, j = e % 2;
     int fm = 0, fn = 0, cq = 0;
     for (int m = 0; m < FD; ++m)
@@ -889,10 +926,10 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
     o[(8 * fm + (l >> 2)) * NPAD + 8 * fn + 2 * (l & 3) + j] = sum;
   }
   if constexpr (R > 0) {
-    for (int e = threadIdx.x; e < RS; e += TTH) {
+    for (int e = threadIdx.x; e < RS; e += NT) {
       double sum = 0.0;
 #pragma unroll
-      for (int w = 0; w < TSC; ++w) sum += rred[w * RS + e];
+      for (int w = 0; w < CW; ++w) sum += rred[w * RS + e];
       const int l = e % 32, r = (e / 32) % R, h = e / 32 / R;
       const int i = l + 32 * h, rr = 8 * FD + r;
       if (i < N && i <= rr) o[i * NPAD + rr] = sum;
@@ -901,7 +938,7 @@ __global__ void __launch_bounds__(TTH, 1) rotate_fused_kernel(
   if (threadIdx.x < 2) {
     double sum = 0.0;
 #pragma unroll
-    for (int w = 0; w < TSC; ++w) sum += ered[threadIdx.x * TSC + w];
+    for (int w = 0; w < CW; ++w) sum += ered[threadIdx.x * CW + w];
     dpart[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = sum;
   }
 }
@@ -913,27 +950,41 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
                           const double* vext, double* dpart, cudaStream_t s,
                           const double* sa_dev) {
   constexpr int NPAD = 8 * F;
+  static const int cw_env = getenv("PO_RF_CW") ? atoi(getenv("PO_RF_CW")) : 8;  // measurement (12: slower, 228 vs 215 us at C2)
+  const int R = (N % 8 == 1 || N % 8 == 2) && N > 8 ? N % 8 : 0;
+  // 12 consumer warps where they fit 128 registers without spilling (N <= 33)
+  const int CW = cw_env == 8 || F > 5 || (F == 5 && R == 2) ? 8 : 12;
+  const int KS = 8 * CW, PW = KS + 8;
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   int nsrc = 0;
-  if (!make_map2(maps, nsrc++, A, ld, N, NPAD)) return -1;
-  if (Ab && !make_map2(maps, nsrc++, Ab, ld, N, NPAD)) return -1;
-  const int R = (N % 8 == 1 || N % 8 == 2) && N > 8 ? N % 8 : 0;
+  if (!make_map(&maps.m[nsrc++], A, ld, N, N, PW)) return -1;
+  if (Ab && !make_map(&maps.m[nsrc++], Ab, ld, N, N, PW)) return -1;
   const int fd = R ? F - 1 : F;
-  const size_t red = (size_t)TSC * (fd * (fd + 1) / 2) * 64 + (size_t)TSC * 2 * 2 * 32 + 2 * TSC;
+  const size_t red = (size_t)CW * (fd * (fd + 1) / 2) * 64 + (size_t)CW * 2 * 2 * 32 + 2 * CW;
   const size_t extra = (size_t)NPAD * NPAD;
-  TCfg cfg = tcfg(nsrc, N, extra);
-  if (cfg.smem < 2048 + red * 8) cfg.smem = 2048 + red * 8;
-  const int64_t kb = (ld + TKS - 1) / TKS;
+  // ring: stages of KS points, padded rows; tail for fragment rows past N
+  const size_t qs = ((size_t)N * PW + 15) & ~(size_t)15;
+  const size_t sd = (size_t)nsrc * qs;
+  int nst = (int)((tbudget() / 8 - extra) / sd);
+  if (nst > 8) nst = 8;
+  if (nst < 2) nst = 2;
+  size_t smem = 3072 + (size_t)8 * PW * 8 + ((size_t)nst * sd + extra) * 8;
+  if (smem < 2048 + red * 8) smem = 2048 + red * 8;
+  const int64_t kb = (ld + KS - 1) / KS;
   int nblk = nsm();
   if (nblk > kb) nblk = (int)kb;
-  const int64_t pchunk = ((kb + nblk - 1) / nblk) * TKS;
+  const int64_t pchunk = ((kb + nblk - 1) / nblk) * KS;
   nblk = (int)((ld + pchunk - 1) / pchunk);
-  auto k = F == 1 || R == 0 ? rotate_fused_kernel<F, 0>
-                            : R == 1 ? rotate_fused_kernel<F, 1> : rotate_fused_kernel<F, 2>;
+  auto k = CW == 8 ? (F == 1 || R == 0 ? rotate_fused_kernel<F, 0, 8>
+                                       : R == 1 ? rotate_fused_kernel<F, 1, 8> : rotate_fused_kernel<F, 2, 8>)
+                   : (F == 1 || R == 0 ? rotate_fused_kernel<F, 0, 12>
+                                       : rotate_fused_kernel<F, 1, (F <= 5 ? 12 : 8)>);
+  const int nthreads = CW == 8 ? TTH : (CW + 1) * 32;
+  TCfg cfg{nst, sd, smem};
   ::po::count_launch();
   set_smem(reinterpret_cast<const void*>(k), (int)cfg.smem);
-  k<<<nblk, TTH, cfg.smem, s>>>(maps, nsrc, N, ld, ngl, pchunk, cfg.nst, sa, M, out, ws, occ, xc,
+  k<<<nblk, nthreads, cfg.smem, s>>>(maps, nsrc, N, ld, ngl, pchunk, cfg.nst, sa, M, out, ws, occ, xc,
                                  rho, vxc, bvec, vext, dpart, sa_dev);
   const int64_t threads = (int64_t)N * N * 32;
   ::po::count_launch();
@@ -1400,31 +1451,46 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
   }
 }
 
-__global__ void gram_big_reduce_kernel(int GT_T, int N, int mt, int sym, int ntiles, int nsplit, double w,
-                                       const double* __restrict__ ws, double* __restrict__ G,
-                                       const double* __restrict__ guard) {
+// G(i, j) = w sum_k ws[k](tile of (i, j)); 8 split groups per element summed
+// in a fixed order (deterministic), 32 consecutive elements per block
+__global__ void __launch_bounds__(256) gram_big_reduce_kernel(int GT_T, int N, int mt, int sym,
+                                                              int ntiles, int nsplit, double w,
+                                                              const double* __restrict__ ws,
+                                                              double* __restrict__ G,
+                                                              const double* __restrict__ guard) {
   if (guard && *guard == 0.0) return;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)N * N) return;
-  int i = (int)(e / N), j = (int)(e % N);
-  if (sym && j < i) {
-    const int t = i;
-    i = j;
-    j = t;
-  }
-  const int tm = i / GT_T, tn = j / GT_T;
-  int tile;
-  if (!sym) {
-    tile = tm * mt + tn;
-  } else {
-    tile = 0;
-    for (int r = 0; r < tm; ++r) tile += mt - r;
-    tile += tn - tm;
-  }
-  const int64_t off = (int64_t)tile * GT_T * GT_T + (i - tm * GT_T) * GT_T + (j - tn * GT_T);
+  __shared__ double part[8][33];
+  const int64_t e = (int64_t)blockIdx.x * 32 + threadIdx.x;
   double s = 0.0;
-  for (int k = 0; k < nsplit; ++k) s += ws[(int64_t)k * ntiles * GT_T * GT_T + off];
-  G[e] = w * s;
+  int64_t off = 0;
+  if (e < (int64_t)N * N) {
+    int i = (int)(e / N), j = (int)(e % N);
+    if (sym && j < i) {
+      const int t = i;
+      i = j;
+      j = t;
+    }
+    const int tm = i / GT_T, tn = j / GT_T;
+    int tile;
+    if (!sym) {
+      tile = tm * mt + tn;
+    } else {
+      tile = 0;
+      for (int r = 0; r < tm; ++r) tile += mt - r;
+      tile += tn - tm;
+    }
+    off = (int64_t)tile * GT_T * GT_T + (i - tm * GT_T) * GT_T + (j - tn * GT_T);
+    const int64_t stride = (int64_t)ntiles * GT_T * GT_T;
+    for (int k = threadIdx.y; k < nsplit; k += 8) s += ws[k * stride + off];
+  }
+  part[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && e < (int64_t)N * N) {
+    double t = 0.0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) t += part[g][threadIdx.x];
+    G[e] = w * t;
+  }
 }
 
 struct BigPlan {
@@ -1837,8 +1903,8 @@ bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* 
                                                  nst, sa, sb, ws, guard);
   const int64_t total = (int64_t)N * N;
   ::po::count_launch();
-  gram_big_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(GT_T, N, p.mt, sym, p.ntiles,
-                                                                         p.nsplit, w, ws, G, guard);
+  gram_big_reduce_kernel<<<(unsigned)((total + 31) / 32), dim3(32, 8), 0, s>>>(GT_T, N, p.mt, sym, p.ntiles,
+                                                                               p.nsplit, w, ws, G, guard);
   return true;
 }
 
