@@ -760,8 +760,9 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
     const int c = warp * 8;
     // this lane's fragments of the upper-triangular L^{-T}; with R > 0 the last
     // fragment column (R real orbitals) is a per-lane FMA dot instead of DMMA
-    double mreg[CW == 8 ? 2 * F : 1][CW == 8 ? F : 1];
-    if constexpr (CW == 8) {
+    constexpr bool MREG = CW <= 8;  // L^{-T} fragments in registers
+    double mreg[MREG ? 2 * F : 1][MREG ? F : 1];
+    if constexpr (MREG) {
 #pragma unroll
       for (int ks = 0; ks < 2 * F; ++ks)
 #pragma unroll
@@ -803,7 +804,7 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
 #pragma unroll
           for (int fi = 0; fi < FD; ++fi) {
             if (4 * ks > 8 * fi + 7) continue;
-            if constexpr (CW == 8)
+            if constexpr (MREG)
               dmma_8x8x4(acc[fi], av[ks], mreg[ks][fi]);
             else
               dmma_8x8x4(acc[fi], av[ks], Ms[(4 * ks + t4) * NPAD + 8 * fi + gq]);
@@ -953,7 +954,7 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
   static const int cw_env = getenv("PO_RF_CW") ? atoi(getenv("PO_RF_CW")) : 8;  // measurement (12: slower, 228 vs 215 us at C2)
   const int R = (N % 8 == 1 || N % 8 == 2) && N > 8 ? N % 8 : 0;
   // 12 consumer warps where they fit 128 registers without spilling (N <= 33)
-  const int CW = cw_env == 8 || F > 5 || (F == 5 && R == 2) ? 8 : 12;
+  const int CW = cw_env == 6 ? 6 : (cw_env == 8 || F > 5 || (F == 5 && R == 2) ? 8 : 12);
   const int KS = 8 * CW, PW = KS + 8;
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
@@ -976,7 +977,9 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
   if (nblk > kb) nblk = (int)kb;
   const int64_t pchunk = ((kb + nblk - 1) / nblk) * KS;
   nblk = (int)((ld + pchunk - 1) / pchunk);
-  auto k = CW == 8 ? (F == 1 || R == 0 ? rotate_fused_kernel<F, 0, 8>
+  auto k = CW == 6 ? (F == 1 || R == 0 ? rotate_fused_kernel<F, 0, 6>
+                                       : R == 1 ? rotate_fused_kernel<F, 1, 6> : rotate_fused_kernel<F, 2, 6>)
+         : CW == 8 ? (F == 1 || R == 0 ? rotate_fused_kernel<F, 0, 8>
                                        : R == 1 ? rotate_fused_kernel<F, 1, 8> : rotate_fused_kernel<F, 2, 8>)
                    : (F == 1 || R == 0 ? rotate_fused_kernel<F, 0, 12>
                                        : rotate_fused_kernel<F, 1, (F <= 5 ? 12 : 8)>);
@@ -1001,34 +1004,43 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
 //   s_i  = W_i - WP_i, y_i = z_i - ZP_i [HIST]  (<s,s>, <s,y>, <y,y>)
 // Sources in the ring: 0 = W, 1 = HW, 2 = WP, 3 = ZP. Per-orbital partial rows
 // [zz | dd | ss | sy | yy] x gridDim.x (dd = 0 without DD).
-template <int F, bool DD, bool HIST>
-__global__ void __launch_bounds__(TTH, 1) directions_tma_kernel(
+// LDGH: W_prev / Z_prev are read by the consumers with plain loads issued at the
+// top of the stage (they are only needed elementwise, for the BB products), so
+// the TMA ring carries two sources and holds twice the stages
+// CW consumer warps (stage = 8 CW points): CW = 6 with a 52-point padded row
+// gives a three-deep ring for the four streamed sources at N = 33 (CW = 8: two
+// stages of 76 KB, i.e. one stage in flight while one is consumed)
+template <int F, bool DD, bool HIST, bool LDGH, int CW>
+__global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_tma_kernel(
     const __grid_constant__ Maps maps, int N, int64_t ld, int64_t ngl, int64_t pchunk, int nst,
     const double* __restrict__ Sigma, const double* __restrict__ sig, double* __restrict__ Z,
-    double* __restrict__ partials) {
+    double* __restrict__ partials, const double* __restrict__ WP, const double* __restrict__ ZP) {
   constexpr int NPAD = 8 * F;
-  constexpr int NSRC = HIST ? 4 : 2;
+  constexpr int NSRC = HIST && !LDGH ? 4 : 2;
   constexpr int NQ = HIST ? 5 : 2;
+  constexpr int KS = 8 * CW;
+  constexpr int PW = CW == 8 ? PADW : KS + 4;  // conflict-free padded row (see PADW)
+  constexpr int NT = CW == 8 ? TTH : (CW + 1) * 32;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
   uint64_t* empty = full + 8;
   double* stage0 = reinterpret_cast<double*>(tsm + 1024);
   const int NB = N;  // box rows: no zero-filled padding rows in the stream
-  const size_t qstride = qs_of(NB);
+  const size_t qstride = ((size_t)NB * PW + 15) & ~(size_t)15;
   const size_t sdoubles = NSRC * qstride;
   double* Ms = stage0 + (size_t)nst * sdoubles;  // [NPAD][NPAD] (DD)
   double* msig = Ms + NPAD * NPAD;               // [NPAD]: -sigma_ii
   double* nred = msig + NPAD;                    // [8][NQ][NPAD]
-  for (int e = threadIdx.x; e < NPAD * NPAD; e += TTH) {
+  for (int e = threadIdx.x; e < NPAD * NPAD; e += NT) {
     const int k = e / NPAD, i = e % NPAD;
     Ms[e] = (DD && k < N && i < N) ? Sigma[(int64_t)k * N + i] : 0.0;
   }
-  for (int i = threadIdx.x; i < NPAD; i += TTH) msig[i] = i < N ? -sig[i] : 0.0;
+  for (int i = threadIdx.x; i < NPAD; i += NT) msig[i] = i < N ? -sig[i] : 0.0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], TSC);
+      mbar_init(&empty[s], CW);
     }
     fence_mbar_init();
   }
@@ -1037,31 +1049,43 @@ __global__ void __launch_bounds__(TTH, 1) directions_tma_kernel(
   const int64_t pend = min(pbeg + pchunk, ld);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, t4 = lane & 3;
-  if (warp >= TSC) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-    produce(maps, NSRC, NB, pbeg, pend, nst, sdoubles, stage0, full, empty);
+  if (warp >= CW) {
+    if constexpr (CW == 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (warp == CW) tma_produce_w(maps.m, NSRC, NB, pbeg, pend, nst, sdoubles, stage0, full, empty, KS, PW);
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    if constexpr (CW == 8) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
     double nrm[NQ][F][2];
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
 #pragma unroll
       for (int fi = 0; fi < F; ++fi) nrm[q][fi][0] = nrm[q][fi][1] = 0.0;
-    const int nstage = pend > pbeg ? (int)((pend - pbeg + TKS - 1) / TKS) : 0;
+    const int nstage = pend > pbeg ? (int)((pend - pbeg + KS - 1) / KS) : 0;
     const int ksteps = (N + 3) / 4;
     const int c = warp * 8;
     for (int st = 0; st < nstage; ++st) {
       const int s = st % nst;
       mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
       const double* sbuf = stage0 + (size_t)s * sdoubles;
-      const int64_t p = pbeg + (int64_t)st * TKS + c + gq;
+      const int64_t p = pbeg + (int64_t)st * KS + c + gq;
       double acc[F][2];
 #pragma unroll
       for (int f = 0; f < F; ++f) acc[f][0] = acc[f][1] = 0.0;
+      double wpv[LDGH ? F : 1][2], zpv[LDGH ? F : 1][2];
+      if constexpr (HIST && LDGH) {
+#pragma unroll
+        for (int fi = 0; fi < F; ++fi)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int i = 8 * fi + 2 * t4 + j;
+            const bool ok = p < ngl && i < N;
+            wpv[fi][j] = ok ? __ldcs(WP + (int64_t)i * ld + p) : 0.0;
+            zpv[fi][j] = ok ? __ldcs(ZP + (int64_t)i * ld + p) : 0.0;
+          }
+      }
       if constexpr (DD) {
         for (int ks = 0; ks < ksteps; ++ks) {
           const int krow = 4 * ks + t4;
-          const double av = krow < N ? sbuf[pad(krow, c + gq)] : 0.0;
+          const double av = krow < N ? sbuf[(krow) * PW + c + gq] : 0.0;
 #pragma unroll
           for (int fi = 0; fi < F; ++fi) dmma_8x8x4(acc[fi], av, Ms[krow * NPAD + 8 * fi + gq]);
         }
@@ -1072,7 +1096,7 @@ __global__ void __launch_bounds__(TTH, 1) directions_tma_kernel(
         for (int j = 0; j < 2; ++j) {
           const int i = 8 * fi + 2 * t4 + j;
           if (p < ngl && i < N) {
-            const int off = pad(i, c + gq);
+            const int off = (i) * PW + c + gq;
             const double wv = sbuf[off], hv = sbuf[qstride + off];
             if constexpr (DD) {
               double d = -acc[fi][j];
@@ -1083,8 +1107,8 @@ __global__ void __launch_bounds__(TTH, 1) directions_tma_kernel(
             Z[(int64_t)i * ld + p] = z;
             nrm[0][fi][j] += z * z;
             if constexpr (HIST) {
-              const double sv = wv - sbuf[2 * qstride + off];
-              const double yv = z - sbuf[3 * qstride + off];
+              const double sv = wv - (LDGH ? wpv[fi][j] : sbuf[2 * qstride + off]);
+              const double yv = z - (LDGH ? zpv[fi][j] : sbuf[3 * qstride + off]);
               nrm[2][fi][j] += sv * sv;
               nrm[3][fi][j] += sv * yv;
               nrm[4][fi][j] += yv * yv;
@@ -1108,31 +1132,54 @@ __global__ void __launch_bounds__(TTH, 1) directions_tma_kernel(
         }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < NQ * N; e += TTH) {
+  for (int e = threadIdx.x; e < NQ * N; e += NT) {
     const int q = e / N, i = e % N;
     double sum = 0.0;
 #pragma unroll
-    for (int w = 0; w < TSC; ++w) sum += nred[(w * NQ + q) * NPAD + i];
+    for (int w = 0; w < CW; ++w) sum += nred[(w * NQ + q) * NPAD + i];
     partials[((int64_t)q * N + i) * gridDim.x + blockIdx.x] = sum;
   }
 }
 
 template <int F, bool DD, bool HIST>
-int launch_directions_fdh(const Maps& maps, int N, int64_t ld, int64_t ngl, const double* Sigma,
-                          const double* sig, double* Z, double* partials, cudaStream_t s) {
+int launch_directions_fdh(const double* W, const double* HW, int N, int64_t ld, int64_t ngl,
+                          const double* Sigma, const double* sig, double* Z, double* partials,
+                          cudaStream_t s, const double* WP, const double* ZP) {
   constexpr int NPAD = 8 * F;
   constexpr int NQ = HIST ? 5 : 2;
-  const size_t extra = (size_t)NPAD * NPAD + NPAD + (size_t)TSC * NQ * NPAD;
-  const TCfg cfg = tcfg(HIST ? 4 : 2, N, extra);
-  const int64_t kb = (ld + TKS - 1) / TKS;
+  // (measured and dropped: W_prev / Z_prev through direct loads instead of the
+  // ring, 286 vs 244 us at C2 — the kernel keeps the LDGH template switch)
+  const bool ldgh = false;
+  // six consumer warps where the 8-warp ring would hold only two stages of the
+  // four streamed sources (measurement switch PO_DIR_CW = 6 / 8)
+  static const int cw_env = getenv("PO_DIR_CW") ? atoi(getenv("PO_DIR_CW")) : 0;
+  const int nsrc = HIST && !ldgh ? 4 : 2;
+  const int CW = cw_env >= 4 && cw_env <= 8 && cw_env != 7 ? cw_env : (nsrc == 4 ? 6 : 8);
+  const int KS = 8 * CW, PW = CW == 8 ? PADW : KS + 4;
+  const size_t extra = (size_t)NPAD * NPAD + NPAD + (size_t)CW * NQ * NPAD;
+  const size_t sd = (size_t)nsrc * (((size_t)N * PW + 15) & ~(size_t)15);
+  int nst = (int)((tbudget() / 8 - extra) / sd);
+  if (nst > 8) nst = 8;
+  if (nst < 2) nst = 2;
+  const TCfg cfg{nst, sd, 3072 + (size_t)8 * PW * 8 + ((size_t)nst * sd + extra) * 8};
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  const double* srcs[4] = {W, HW, WP, ZP};
+  for (int q = 0; q < nsrc; ++q)
+    if (!make_map(&maps.m[q], srcs[q], ld, N, N, PW)) return -1;
+  const int64_t kb = (ld + KS - 1) / KS;
   int nblk = nsm();
   if (nblk > kb) nblk = (int)kb;
-  const int64_t pchunk = ((kb + nblk - 1) / nblk) * TKS;
+  const int64_t pchunk = ((kb + nblk - 1) / nblk) * KS;
   nblk = (int)((ld + pchunk - 1) / pchunk);
   ::po::count_launch();
-  auto k = directions_tma_kernel<F, DD, HIST>;
+  auto k = CW == 8   ? directions_tma_kernel<F, DD, HIST, false, 8>
+           : CW == 6 ? directions_tma_kernel<F, DD, HIST, false, 6>
+           : CW == 5 ? directions_tma_kernel<F, DD, HIST, false, 5>
+                     : directions_tma_kernel<F, DD, HIST, false, 4>;
   set_smem(reinterpret_cast<const void*>(k), (int)cfg.smem);
-  k<<<nblk, TTH, cfg.smem, s>>>(maps, N, ld, ngl, pchunk, cfg.nst, Sigma, sig, Z, partials);
+  k<<<nblk, CW == 8 ? TTH : (CW + 1) * 32, cfg.smem, s>>>(maps, N, ld, ngl, pchunk, cfg.nst, Sigma, sig, Z,
+                                                         partials, WP, ZP);
   return nblk;
 }
 
@@ -1140,18 +1187,12 @@ template <int F>
 int launch_directions_f(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
                         const double* WP, const double* ZP, const double* Sigma, const double* sig,
                         double* Z, double* partials, cudaStream_t s) {
-  constexpr int NPAD = 8 * F;
-  Maps maps;
-  std::memset(&maps, 0, sizeof maps);
   const bool hist = WP && ZP;
-  if (!make_map2(maps, 0, W, ld, N, NPAD) || !make_map2(maps, 1, HW, ld, N, NPAD)) return -1;
-  if (hist && (!make_map2(maps, 2, WP, ld, N, NPAD) || !make_map2(maps, 3, ZP, ld, N, NPAD)))
-    return -1;
   if (Sigma)
-    return hist ? launch_directions_fdh<F, true, true>(maps, N, ld, ngl, Sigma, sig, Z, partials, s)
-                : launch_directions_fdh<F, true, false>(maps, N, ld, ngl, Sigma, sig, Z, partials, s);
-  return hist ? launch_directions_fdh<F, false, true>(maps, N, ld, ngl, Sigma, sig, Z, partials, s)
-              : launch_directions_fdh<F, false, false>(maps, N, ld, ngl, Sigma, sig, Z, partials, s);
+    return hist ? launch_directions_fdh<F, true, true>(W, HW, N, ld, ngl, Sigma, sig, Z, partials, s, WP, ZP)
+                : launch_directions_fdh<F, true, false>(W, HW, N, ld, ngl, Sigma, sig, Z, partials, s, WP, ZP);
+  return hist ? launch_directions_fdh<F, false, true>(W, HW, N, ld, ngl, Sigma, sig, Z, partials, s, WP, ZP)
+              : launch_directions_fdh<F, false, false>(W, HW, N, ld, ngl, Sigma, sig, Z, partials, s, WP, ZP);
 }
 
 template <int F>
