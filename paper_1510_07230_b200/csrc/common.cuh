@@ -117,4 +117,40 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gsrc, ui
       : "memory");
 }
 
+// ------------------------------------------------ programmatic dependent launch
+// Kernels on the iteration path are launched with programmatic stream
+// serialization (launch_pdl): the next kernel may be scheduled while the
+// previous one drains, so its launch latency overlaps the tail. Each such
+// kernel starts with PO_PDL_ENTRY(): wait for the preceding grid (its memory
+// is then visible), then let the following grid start launching (it too waits
+// before touching memory). A grid's dependents launch only once every one of
+// its CTAs has started, so no waiting CTA can starve the kernel it waits on.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+#define PO_PDL_ENTRY() \
+  do {                 \
+    pdl_wait();        \
+    pdl_trigger();     \
+  } while (0)
+
+bool pdl_on();  // PO_PDL=0 disables the attribute (measurement)
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 }  // namespace po

@@ -332,6 +332,7 @@ __global__ void __launch_bounds__(TR * 32) cholesky_inv_gs_kernel(int N, const d
                                                                  double* __restrict__ M,
                                                                  double* __restrict__ stats,
                                                                  const double* __restrict__ guard) {
+  PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   constexpr int NMAX = TR * A;
   static_assert(TR * A == 32 * B, "square slot grid");
@@ -608,6 +609,7 @@ __global__ void __launch_bounds__(256) inv_sqrt_kernel(int N, const double* __re
 __global__ void __launch_bounds__(1024) matrix_stats_kernel(int N, const double* __restrict__ G,
                                                             double* __restrict__ out,
                                                             const double* __restrict__ guard) {
+  PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   __shared__ double red[4][32];
   double dev = 0.0, asym = 0.0, off = 0.0, dg = 0.0;
@@ -662,6 +664,7 @@ __global__ void trial_gram_kernel(int N, const double* __restrict__ gww,
                                   const double* __restrict__ S, const double* __restrict__ ghh,
                                   double tau, double* __restrict__ G0,
                                   const double* __restrict__ tau_dev) {
+  PO_PDL_ENTRY();
   if (tau_dev) tau = *tau_dev;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)N * N) return;
@@ -682,6 +685,7 @@ __global__ void bb_tau_kernel(int N, const double* __restrict__ zz, const double
                               const double* __restrict__ sy, const double* __restrict__ yy,
                               int history, int use_bb1, int trace_abs_diag, double tau_min,
                               double tau_max, double* __restrict__ out) {
+  PO_PDL_ENTRY();
   if (threadIdx.x != 0) return;
   double znorm2 = 0.0;
   for (int i = 0; i < N; ++i) znorm2 += zz[i];
@@ -711,7 +715,7 @@ void launch_bb_tau(int N, const double* zz, const double* ss, const double* sy, 
                    int history, int use_bb1, int trace_abs_diag, double tau_min, double tau_max,
                    double* out, cudaStream_t s) {
   ::po::count_launch();
-  bb_tau_kernel<<<1, 32, 0, s>>>(N, zz, ss, sy, yy, history, use_bb1, trace_abs_diag, tau_min,
+  launch_pdl(bb_tau_kernel, dim3(1), dim3(32), 0, s, N, zz, ss, sy, yy, history, use_bb1, trace_abs_diag, tau_min,
                                  tau_max, out);
 }
 
@@ -719,7 +723,7 @@ void launch_trial_gram(int N, const double* gww, const double* sigma, const doub
                        double tau, double* G0, cudaStream_t s, const double* tau_dev) {
   const int64_t total = (int64_t)N * N;
   ::po::count_launch();
-  trial_gram_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(N, gww, sigma, ghh, tau, G0,
+  launch_pdl(trial_gram_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, s, N, gww, sigma, ghh, tau, G0,
                                                                     tau_dev);
 }
 
@@ -743,11 +747,11 @@ void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, do
   static const int variant = getenv("PO_CHOL") ? atoi(getenv("PO_CHOL")) : 0;  // measurement
   if (variant == 0 && N <= 128) {  // one barrier per column, registers only
     if (N <= 32)
-      cholesky_inv_gs_kernel<32, 1, 1><<<1, 1024, 0, s>>>(N, G, M, stats, guard);
+      launch_pdl(cholesky_inv_gs_kernel<32, 1, 1>, dim3(1), dim3(1024), 0, s, N, G, M, stats, guard);
     else if (N <= 64)
-      cholesky_inv_gs_kernel<16, 4, 2><<<1, 512, 0, s>>>(N, G, M, stats, guard);
+      launch_pdl(cholesky_inv_gs_kernel<16, 4, 2>, dim3(1), dim3(512), 0, s, N, G, M, stats, guard);
     else
-      cholesky_inv_gs_kernel<32, 4, 4><<<1, 1024, 0, s>>>(N, G, M, stats, guard);
+      launch_pdl(cholesky_inv_gs_kernel<32, 4, 4>, dim3(1), dim3(1024), 0, s, N, G, M, stats, guard);
     return;
   }
   // measured (tools/kbench-style, one launch): register kernel 6 / 12 / 29 us at
@@ -807,7 +811,8 @@ void launch_inv_sqrt_from_eig(int N, const double* evals, const double* evecs, d
 void launch_matrix_stats(int N, const double* G, double* out, cudaStream_t s,
                          const double* guard) {
   ::po::count_launch();
-  matrix_stats_kernel<<<1, N <= 32 ? 256 : 1024, 0, s>>>(N, G, out, guard);
+  const int threads = N <= 32 ? 256 : 1024;
+  launch_pdl(matrix_stats_kernel, dim3(1), dim3(threads), 0, s, N, G, out, guard);
 }
 
 }  // namespace po

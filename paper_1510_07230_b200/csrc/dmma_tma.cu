@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
                                                           double* __restrict__ ws,
                                                           const double* __restrict__ guard,
                                                           int probe) {
+  PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   constexpr bool REM = DUAL && R > 0;
   constexpr int FD = REM ? F - 1 : F;  // DMMA fragments
@@ -462,6 +463,7 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
 __global__ void gram_tma_reduce_kernel(int N, int npad, int sym, int nsplit, double w,
                                        const double* __restrict__ ws, double* __restrict__ G,
                                        const double* __restrict__ guard) {
+  PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -531,15 +533,15 @@ bool launch_gram_tma_f(int N, int64_t ld, int sym, const double* A, const double
   set_smem(reinterpret_cast<const void*>(k), (int)cfg.smem);
   const char* pe = getenv("PO_GRAM_PROBE");  // measurement hook (TMA ring without math)
   const int probe = pe ? atoi(pe) : 0;
-  k<<<nsplit, TTH, cfg.smem, s>>>(maps, N, nsrc, qa_b, qb, qb_b, ld, kchunk, cfg.nst, sa, sb, ws,
+  launch_pdl(k, dim3(nsplit), dim3(TTH), cfg.smem, s, maps, N, nsrc, qa_b, qb, qb_b, ld, kchunk, cfg.nst, sa, sb, ws,
                                    guard, probe);
   const int64_t threads = (int64_t)N * N * 32;
   ::po::count_launch();
-  gram_tma_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(N, NPAD, sym, nsplit, w,
+  launch_pdl(gram_tma_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, N, NPAD, sym, nsplit, w,
                                                                            ws, G, guard);
   if (dual) {
     ::po::count_launch();
-    gram_tma_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+    launch_pdl(gram_tma_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, 
         N, NPAD, 1, nsplit, w, ws + (size_t)nsplit * NPAD * NPAD, G2, guard);
   }
   return true;
@@ -553,6 +555,7 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
     const __grid_constant__ Maps maps, int nsrc, int qc, int N, int64_t ld, int64_t ngl,
     int64_t pchunk, int nst, double sa, const double* __restrict__ M, double alpha, double beta,
     double* __restrict__ out, double* __restrict__ norms, const double* __restrict__ guard) {
+  PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   constexpr int NPAD = 8 * F;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
@@ -703,6 +706,7 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
     double* __restrict__ ws, double occ, int xc, double* __restrict__ rho, double* __restrict__ vxc,
     double* __restrict__ bvec, const double* __restrict__ vext, double* __restrict__ dpart,
     const double* __restrict__ sa_dev) {
+  PO_PDL_ENTRY();
   if (sa_dev) sa = *sa_dev;  // trial scale decided on the device (bb_tau_kernel)
   constexpr int NPAD = 8 * F;
   constexpr int FD = R > 0 ? F - 1 : F;
@@ -987,11 +991,11 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
   TCfg cfg{nst, sd, smem};
   ::po::count_launch();
   set_smem(reinterpret_cast<const void*>(k), (int)cfg.smem);
-  k<<<nblk, nthreads, cfg.smem, s>>>(maps, nsrc, N, ld, ngl, pchunk, cfg.nst, sa, M, out, ws, occ, xc,
+  launch_pdl(k, dim3(nblk), dim3(nthreads), cfg.smem, s, maps, nsrc, N, ld, ngl, pchunk, cfg.nst, sa, M, out, ws, occ, xc,
                                  rho, vxc, bvec, vext, dpart, sa_dev);
   const int64_t threads = (int64_t)N * N * 32;
   ::po::count_launch();
-  gram_tma_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(N, NPAD, 1, nblk, w, ws,
+  launch_pdl(gram_tma_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, N, NPAD, 1, nblk, w, ws,
                                                                            G, nullptr);
   return nblk;
 }
@@ -1015,6 +1019,7 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
     const __grid_constant__ Maps maps, int N, int64_t ld, int64_t ngl, int64_t pchunk, int nst,
     const double* __restrict__ Sigma, const double* __restrict__ sig, double* __restrict__ Z,
     double* __restrict__ partials, const double* __restrict__ WP, const double* __restrict__ ZP) {
+  PO_PDL_ENTRY();
   constexpr int NPAD = 8 * F;
   constexpr int NSRC = HIST && !LDGH ? 4 : 2;
   constexpr int NQ = HIST ? 5 : 2;
@@ -1178,7 +1183,7 @@ int launch_directions_fdh(const double* W, const double* HW, int N, int64_t ld, 
            : CW == 5 ? directions_tma_kernel<F, DD, HIST, false, 5>
                      : directions_tma_kernel<F, DD, HIST, false, 4>;
   set_smem(reinterpret_cast<const void*>(k), (int)cfg.smem);
-  k<<<nblk, CW == 8 ? TTH : (CW + 1) * 32, cfg.smem, s>>>(maps, N, ld, ngl, pchunk, cfg.nst, Sigma, sig, Z,
+  launch_pdl(k, dim3(nblk), dim3(CW == 8 ? TTH : (CW + 1) * 32), cfg.smem, s, maps, N, ld, ngl, pchunk, cfg.nst, Sigma, sig, Z,
                                                          partials, WP, ZP);
   return nblk;
 }
@@ -1220,12 +1225,12 @@ int launch_mix_tma_f(int N, int64_t ld, int64_t ngl, const double* A, const doub
   if (upper) {
     auto k = mix_tma_kernel<F, true>;
     set_smem(reinterpret_cast<const void*>(k), (int)cfg.smem);
-    k<<<nblk, TTH, cfg.smem, s>>>(maps, nsrc, qc, N, ld, ngl, pchunk, cfg.nst, sa, M, alpha, beta,
+    launch_pdl(k, dim3(nblk), dim3(TTH), cfg.smem, s, maps, nsrc, qc, N, ld, ngl, pchunk, cfg.nst, sa, M, alpha, beta,
                                    out, norms, guard);
   } else {
     auto k = mix_tma_kernel<F, false>;
     set_smem(reinterpret_cast<const void*>(k), (int)cfg.smem);
-    k<<<nblk, TTH, cfg.smem, s>>>(maps, nsrc, qc, N, ld, ngl, pchunk, cfg.nst, sa, M, alpha, beta,
+    launch_pdl(k, dim3(nblk), dim3(TTH), cfg.smem, s, maps, nsrc, qc, N, ld, ngl, pchunk, cfg.nst, sa, M, alpha, beta,
                                    out, norms, guard);
   }
   return nblk;
@@ -1279,6 +1284,7 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
                                                           int64_t kchunk, int nst, double sa,
                                                           double sb, double* __restrict__ ws,
                                                           const double* __restrict__ guard) {
+  PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
@@ -1499,6 +1505,7 @@ __global__ void __launch_bounds__(256) gram_big_reduce_kernel(int GT_T, int N, i
                                                               const double* __restrict__ ws,
                                                               double* __restrict__ G,
                                                               const double* __restrict__ guard) {
+  PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   __shared__ double part[8][33];
   const int64_t e = (int64_t)blockIdx.x * 32 + threadIdx.x;
@@ -1644,6 +1651,7 @@ __global__ void __launch_bounds__(XTH, 1) mix_big_kernel(
     int n_it, int upper, int nst, double sa, double alpha, const double* __restrict__ C,
     double beta, double* __restrict__ out, double* __restrict__ norms,
     const double* __restrict__ guard) {
+  PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
@@ -1815,6 +1823,7 @@ __global__ void __launch_bounds__(XTH, 1) mix_big_kernel(
 
 __global__ void transpose_pad_kernel(int N, int np, const double* __restrict__ M,
                                      double* __restrict__ Mt) {
+  PO_PDL_ENTRY();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)np * np) return;
   const int i = (int)(e / np), k = (int)(e % np);
@@ -1874,14 +1883,14 @@ int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double
 #undef PO_MB_FAIL
   const size_t smem = fixed + (size_t)nst * sdoubles * 8;
   ::po::count_launch();
-  transpose_pad_kernel<<<(unsigned)(((int64_t)np * np + 255) / 256), 256, 0, s>>>(N, np, M, mt);
+  launch_pdl(transpose_pad_kernel, dim3((unsigned)(((int64_t)np * np + 255) / 256)), dim3(256), 0, s, N, np, M, mt);
   const int n_pt = mix_big_nblk(ngl);
   const int n_it = (N + XI - 1) / XI;
   const int ntiles = n_pt * n_it;
   const int grid = ntiles < nsm() ? ntiles : nsm();
   set_smem(reinterpret_cast<const void*>(mix_big_kernel), (int)smem);
   ::po::count_launch();
-  mix_big_kernel<<<grid, XTH, smem, s>>>(maps, Ab ? 1 : 0, N, ld, ngl, n_pt, n_it, upper, nst, sa,
+  launch_pdl(mix_big_kernel, dim3(grid), dim3(XTH), smem, s, maps, Ab ? 1 : 0, N, ld, ngl, n_pt, n_it, upper, nst, sa,
                                          alpha, C, beta, out, norms, guard);
   return n_pt;
 }
@@ -1940,11 +1949,11 @@ bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* 
   auto k = GT_T == 64 ? gram_big_kernel<64> : gram_big_kernel<128>;
   const int threads = GT_T == 64 ? BigCfg<64>::THREADS : BigCfg<128>::THREADS;
   set_smem(reinterpret_cast<const void*>(k), (int)smem);
-  k<<<dim3(p.ntiles, p.nsplit), threads, smem, s>>>(maps, nsrc, qa_b, qb, qb_b, p.mt, sym, ld, p.kchunk,
+  launch_pdl(k, dim3(dim3(p.ntiles, p.nsplit)), dim3(threads), smem, s, maps, nsrc, qa_b, qb, qb_b, p.mt, sym, ld, p.kchunk,
                                                  nst, sa, sb, ws, guard);
   const int64_t total = (int64_t)N * N;
   ::po::count_launch();
-  gram_big_reduce_kernel<<<(unsigned)((total + 31) / 32), dim3(32, 8), 0, s>>>(GT_T, N, p.mt, sym, p.ntiles,
+  launch_pdl(gram_big_reduce_kernel, dim3((unsigned)((total + 31) / 32)), dim3(dim3(32, 8)), 0, s, GT_T, N, p.mt, sym, p.ntiles,
                                                                                p.nsplit, w, ws, G, guard);
   return true;
 }

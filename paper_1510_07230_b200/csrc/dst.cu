@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(PW * 32) dst_plane_kernel(double* __restrict__
                                                             int n2, const double* __restrict__ S1,
                                                             const double* __restrict__ S2,
                                                             const double* __restrict__ scale) {
+  PO_PDL_ENTRY();
   constexpr int WC = 4, RB = (NF + 3) / 4, CB = (NF + WC - 1) / WC;
   extern __shared__ double dsm[];
   const int nf = (max(n1, n2) + 7) / 8;
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(AW * 32) dst_axis0_kernel(const double* __rest
                                                             double* __restrict__ y, int n0,
                                                             int64_t plane,
                                                             const double* __restrict__ S0) {
+  PO_PDL_ENTRY();
   constexpr int WC = 2, RB = (NF + 3) / 4, CB = A0P / 8 / WC;
   extern __shared__ double dsm[];
   constexpr int xs = A0P + 4;
@@ -261,7 +263,7 @@ void launch_axis0(const DstPoisson& d, const double* x, double* y, cudaStream_t 
   auto ka = dst_axis0_kernel<NF, ASG, A0P>;
   set_smem(reinterpret_cast<const void*>(ka), (int)sh0);
   ::po::count_launch();
-  ka<<<(unsigned)((plane + A0P - 1) / A0P), AW * 32, sh0, s>>>(x, y, (int)d.n0, plane, d.S[0]);
+  launch_pdl(ka, dim3((unsigned)((plane + A0P - 1) / A0P)), dim3(AW * 32), sh0, s, x, y, (int)d.n0, plane, d.S[0]);
 }
 
 template <int NF>
@@ -291,7 +293,7 @@ void launch_fused(const DstPoisson& d, const double* b, double* x, cudaStream_t 
   set_smem(reinterpret_cast<const void*>(kp), (int)sh1);
   launch_axis0_pick<NF>(d, b, d.t0, s);
   ::po::count_launch();
-  kp<<<(unsigned)d.n0, PW * 32, sh1, s>>>(d.t0, (int)d.n0, (int)d.n1, (int)d.n2, d.S[1], d.S[2],
+  launch_pdl(kp, dim3((unsigned)d.n0), dim3(PW * 32), sh1, s, d.t0, (int)d.n0, (int)d.n1, (int)d.n2, d.S[1], d.S[2],
                                           d.scale);
   launch_axis0_pick<NF>(d, d.t0, x, s);
 }

@@ -15,8 +15,15 @@
 
 namespace po {
 
+bool pdl_on() {
+  static const bool on = !getenv("PO_PDL") || atoi(getenv("PO_PDL")) != 0;
+  return on;
+}
+
+
 namespace {
 __global__ void copy_diag_kernel(int N, const double* __restrict__ M, double* __restrict__ out) {
+  PO_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < N) out[i] = M[(int64_t)i * N + i];
 }
@@ -24,7 +31,7 @@ __global__ void copy_diag_kernel(int N, const double* __restrict__ M, double* __
 
 void launch_copy_diag(int N, const double* M, double* out, cudaStream_t s) {
   ::po::count_launch();
-  copy_diag_kernel<<<(N + 255) / 256, 256, 0, s>>>(N, M, out);
+  launch_pdl(copy_diag_kernel, dim3((N + 255) / 256), dim3(256), 0, s, N, M, out);
 }
 
 static std::atomic<long long> g_launches{0};
@@ -236,6 +243,7 @@ void Engine::free_state(DevState* st) {
 __global__ void publish_kernel(const double* __restrict__ src, double* dst, int n,
                                const int* __restrict__ isrc, int* idst,
                                volatile unsigned long long* flag, unsigned long long seq) {
+  PO_PDL_ENTRY();
   for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
   if (threadIdx.x < 2) idst[threadIdx.x] = isrc[threadIdx.x];
   __threadfence_system();
@@ -250,7 +258,7 @@ void Engine::fetch(size_t off, size_t n) {
   PO_CUDA(cudaGetLastError());
   const unsigned long long seq = ++pub_seq;
   ::po::count_launch();
-  publish_kernel<<<1, 256, 0, s>>>(dvec + off, hvec_dev + off, (int)n, cg_out_i, h_cg_i_dev,
+  launch_pdl(publish_kernel, dim3(1), dim3(256), 0, s, dvec + off, hvec_dev + off, (int)n, cg_out_i, h_cg_i_dev,
                                    hflag_dev, seq);
   PO_CUDA(cudaGetLastError());
   volatile unsigned long long* f = hflag;

@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(PT) density_xc_kernel(SlabGeom g, int N,
                                                         const double* __restrict__ vext,
                                                         double* __restrict__ partials,
                                                         const double* __restrict__ guard) {
+  PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;  // device-side branch (CholeskyQR2 repair)
   __shared__ double red[2 * 32];
   double acc[2] = {0.0, 0.0};
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(PT) vlocal_kernel(SlabGeom g, const double* __
                                                     const double* __restrict__ rho,
                                                     double* __restrict__ vloc,
                                                     double* __restrict__ partials) {
+  PO_PDL_ENTRY();
   __shared__ double red[32];
   double acc[1] = {0.0};
   for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < g.ngl;
@@ -202,6 +204,7 @@ __global__ void __launch_bounds__(PT) lincomb_kernel(int64_t total, const double
 __global__ void reduce_rows_kernel(const double* __restrict__ partials, int rows, int nblk,
                                    double scale, double* __restrict__ out,
                                    const double* __restrict__ guard) {
+  PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -362,7 +365,7 @@ void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupat
                        double* rho, double* v_xc, double* b, const double* v_ext, double* partials,
                        cudaStream_t s, const double* guard) {
   ::po::count_launch();
-  density_xc_kernel<<<points_nblk(g), PT, 0, s>>>(g, N, u, occupation, xc, rho, v_xc, b, v_ext,
+  launch_pdl(density_xc_kernel, dim3(points_nblk(g)), dim3(PT), 0, s, g, N, u, occupation, xc, rho, v_xc, b, v_ext,
                                                   partials, guard);
 }
 
@@ -370,7 +373,7 @@ void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h_src
                    const double* v_xc, const double* rho, double* v_local, double* partials,
                    cudaStream_t s) {
   ::po::count_launch();
-  vlocal_kernel<<<points_nblk(g), PT, 0, s>>>(g, v_ext, v_h_src, v_h, v_xc, rho, v_local,
+  launch_pdl(vlocal_kernel, dim3(points_nblk(g)), dim3(PT), 0, s, g, v_ext, v_h_src, v_h, v_xc, rho, v_local,
                                               partials);
 }
 
@@ -415,7 +418,7 @@ void launch_reduce_rows(const double* partials, int rows, int nblk, double scale
   const int threads = 256;
   const int blocks = (rows * 32 + threads - 1) / threads;
   ::po::count_launch();
-  reduce_rows_kernel<<<blocks, threads, 0, s>>>(partials, rows, nblk, scale, out, guard);
+  launch_pdl(reduce_rows_kernel, dim3(blocks), dim3(threads), 0, s, partials, rows, nblk, scale, out, guard);
 }
 
 void launch_external_potential(const SlabGeom& g, const double* h3, const double* atoms,

@@ -335,6 +335,7 @@ __global__ void __launch_bounds__(32 * (TYR + 1), 1) hamiltonian4_kernel(
     SlabGeom g, int N, int nst, int zc, const double* __restrict__ u, const double* __restrict__ halo_lo,
     const double* __restrict__ halo_hi, const double* __restrict__ vloc,
     const double* __restrict__ vext, double* __restrict__ out, double* __restrict__ partials) {
+  PO_PDL_ENTRY();
   extern __shared__ __align__(128) unsigned char hsm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(hsm);
   uint64_t* empty = full + 8;
@@ -505,7 +506,7 @@ void launch_h4(const SlabGeom& g, int N, const double* u, const double* lo, cons
   case JJ: {                                                                               \
     auto k = hamiltonian4_kernel<JJ, EXT, TYR>;                                             \
     set_smem(reinterpret_cast<const void*>(k), (int)r.smem);                               \
-    k<<<grid, block, r.smem, s>>>(g, N, r.nst, zc, u, lo, hi, vloc, vext, out, partials);  \
+    launch_pdl(k, dim3(grid), dim3(block), r.smem, s, g, N, r.nst, zc, u, lo, hi, vloc, vext, out, partials);  \
     break;                                                                                 \
   }
     PO_H4(1) PO_H4(2) PO_H4(3) PO_H4(4) PO_H4(5) PO_H4(6) PO_H4(7) PO_H4(8)
