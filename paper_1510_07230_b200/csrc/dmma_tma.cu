@@ -460,6 +460,145 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
   }
 }
 
+// Verification Gram G = W~^T W~ (symmetric) of a rotated block with the density
+// / Dirac xc of W~ in the same pass (energy.cpp:67-76, 212-226): rho = occ sum_i
+// W~_i^2, v_xc, 4 pi rho into bvec (when non-null), partial rows
+// [<eps, rho> | <V_ext, rho>] x grid in dpart. The split form of the trial
+// rotation (launch_rotate_fused): the rotation itself runs as the two-source
+// mix at ~90% of HBM, this pass reads W~ once.
+template <int F>
+__global__ void __launch_bounds__(TTH, 1) gram_density_kernel(
+    const __grid_constant__ Maps maps, int N, int64_t ld, int64_t ngl, int64_t kchunk, int nst,
+    double* __restrict__ ws, double occ, int xc, double* __restrict__ rho, double* __restrict__ vxc,
+    double* __restrict__ bvec, const double* __restrict__ vext, double* __restrict__ dpart) {
+  PO_PDL_ENTRY();
+  constexpr int NP = F * (F + 1) / 2;
+  constexpr int NPAD = 8 * F;
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
+  uint64_t* empty = full + 8;
+  double* stage0 = reinterpret_cast<double*>(tsm + 1024);
+  const size_t sdoubles = qs_of(N);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], TSC);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t kbeg = (int64_t)blockIdx.x * kchunk;
+  const int64_t kend = min(kbeg + kchunk, ld);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, t4 = lane & 3;
+  const double cx = dirac_cx();
+  const double four_pi = 4.0 * 3.141592653589793238462643383279502884;
+  double* red = stage0;  // after the loop: [8 warps][NP * 64], then energies
+  double* ered = red + (size_t)TSC * NP * 64;
+  if (warp >= TSC) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    produce(maps, 1, N, kbeg, kend, nst, sdoubles, stage0, full, empty);
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    double acc[NP][2];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) acc[q][0] = acc[q][1] = 0.0;
+    double eacc[2] = {0.0, 0.0};
+    const int nstage = kend > kbeg ? (int)((kend - kbeg + TKS - 1) / TKS) : 0;
+    const int c = warp * 8;  // this warp's 8 points of every stage
+    for (int st = 0; st < nstage; ++st) {
+      const int s = st % nst;
+      const int64_t p0 = kbeg + (int64_t)st * TKS + c + 2 * t4;  // this lane's two points
+      double vx[2] = {0.0, 0.0};
+      if (vext && gq == 0) {  // requested before the stage wait (latency under the TMA)
+        if (p0 < ngl) vx[0] = __ldg(vext + p0);
+        if (p0 + 1 < ngl) vx[1] = __ldg(vext + p0 + 1);
+      }
+      mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+      const double* sbuf = stage0 + (size_t)s * sdoubles;
+      double2 a[F];
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        a[f] = *reinterpret_cast<const double2*>(sbuf + pad(8 * f + gq, c + 2 * t4));
+        if (8 * f + gq < N) {  // rows past N are another area's data
+          d0 = fma(a[f].x, a[f].x, d0);
+          d1 = fma(a[f].y, a[f].y, d1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      int q = 0;
+#pragma unroll
+      for (int fm = 0; fm < F; ++fm)
+#pragma unroll
+        for (int fn = fm; fn < F; ++fn, ++q) {
+          dmma_8x8x4(acc[q], a[fm].x, a[fn].x);
+          dmma_8x8x4(acc[q], a[fm].y, a[fn].y);
+        }
+      // density of the lane's two points: sum over the 8 row groups (gq)
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+      }
+      if (gq == 0) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t p = p0 + e;
+          if (p >= ngl) continue;
+          const double dv = e ? d1 : d0;
+          const double r = occ == 1.0 ? dv : dv * occ;
+          rho[p] = r;
+          if (xc) {
+            const double eps = -cx * cbrt(r);
+            vxc[p] = eps * (4.0 / 3.0);
+            eacc[0] += eps * r;
+          } else {
+            vxc[p] = 0.0;
+          }
+          if (bvec) bvec[p] = r * four_pi;
+          eacc[1] += vx[e] * r;
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"n"(TSC * 32) : "memory");
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      red[(warp * NP + q) * 64 + lane * 2] = acc[q][0];
+      red[(warp * NP + q) * 64 + lane * 2 + 1] = acc[q][1];
+    }
+    const double e0 = warp_sum(eacc[0]), e1 = warp_sum(eacc[1]);
+    if (lane == 0) {
+      ered[warp] = e0;
+      ered[TSC + warp] = e1;
+    }
+  }
+  __syncthreads();
+  double* o = ws + (int64_t)blockIdx.x * NPAD * NPAD;
+  for (int e = threadIdx.x; e < NP * 64; e += TTH) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < TSC; ++w) sum += red[(w * NP) * 64 + e];
+    const int q = e / 64, l = (e % 64) / 2, j = e % 2;
+    int fm = 0, fn = 0, cq = 0;
+    for (int m = 0; m < F; ++m)
+      for (int n = m; n < F; ++n, ++cq)
+        if (cq == q) {
+          fm = m;
+          fn = n;
+        }
+    o[(8 * fm + (l >> 2)) * NPAD + 8 * fn + 2 * (l & 3) + j] = sum;
+  }
+  if (threadIdx.x < 2) {
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < TSC; ++w) sum += ered[threadIdx.x * TSC + w];
+    dpart[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = sum;
+  }
+}
+
 __global__ void gram_tma_reduce_kernel(int N, int npad, int sym, int nsplit, double w,
                                        const double* __restrict__ ws, double* __restrict__ G,
                                        const double* __restrict__ guard) {
@@ -554,9 +693,11 @@ template <int F, bool UPPER>
 __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
     const __grid_constant__ Maps maps, int nsrc, int qc, int N, int64_t ld, int64_t ngl,
     int64_t pchunk, int nst, double sa, const double* __restrict__ M, double alpha, double beta,
-    double* __restrict__ out, double* __restrict__ norms, const double* __restrict__ guard) {
+    double* __restrict__ out, double* __restrict__ norms, const double* __restrict__ guard,
+    const double* __restrict__ sa_dev) {
   PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
+  if (sa_dev) sa = *sa_dev;  // trial scale decided on the device (bb_tau_kernel)
   constexpr int NPAD = 8 * F;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   // SWIZZLE_128B boxes need 1024-byte aligned destinations
@@ -846,15 +987,15 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
       if (t4 == 0 && p < ngl) {
         const double r = occ == 1.0 ? dsum : dsum * occ;
         rho[p] = r;
-        if (xc) {
+        if (xc > 0) {
           const double eps = -cx * cbrt(r);
           vxc[p] = eps * (4.0 / 3.0);
           eacc[0] += eps * r;
-        } else {
+        } else if (xc == 0) {
           vxc[p] = 0.0;
-        }
+        }  // xc < 0: v_xc and the energies are formed by the v_local pass
         if (bvec) bvec[p] = r * four_pi;
-        if (vext) eacc[1] += vx * r;
+        if (vext && xc >= 0) eacc[1] += vx * r;
       }
       __syncwarp();  // rotated chunk visible to the whole warp
       if constexpr (R > 0) {
@@ -1203,7 +1344,8 @@ int launch_directions_f(int N, int64_t ld, int64_t ngl, const double* W, const d
 template <int F>
 int launch_mix_tma_f(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
                      const double* M, double alpha, const double* C, double beta, int upper,
-                     double* out, double* norms, cudaStream_t s, const double* guard) {
+                     double* out, double* norms, cudaStream_t s, const double* guard,
+                     const double* sa_dev = nullptr) {
   constexpr int NPAD = 8 * F;
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
@@ -1226,12 +1368,12 @@ int launch_mix_tma_f(int N, int64_t ld, int64_t ngl, const double* A, const doub
     auto k = mix_tma_kernel<F, true>;
     set_smem(reinterpret_cast<const void*>(k), (int)cfg.smem);
     launch_pdl(k, dim3(nblk), dim3(TTH), cfg.smem, s, maps, nsrc, qc, N, ld, ngl, pchunk, cfg.nst, sa, M, alpha, beta,
-                                   out, norms, guard);
+                                   out, norms, guard, sa_dev);
   } else {
     auto k = mix_tma_kernel<F, false>;
     set_smem(reinterpret_cast<const void*>(k), (int)cfg.smem);
     launch_pdl(k, dim3(nblk), dim3(TTH), cfg.smem, s, maps, nsrc, qc, N, ld, ngl, pchunk, cfg.nst, sa, M, alpha, beta,
-                                   out, norms, guard);
+                                   out, norms, guard, sa_dev);
   }
   return nblk;
 }
@@ -1977,10 +2119,56 @@ void set_smem(const void* k, int bytes) {
   done[k] = bytes;
 }
 
+// split trial rotation: two-source mix (W + sa Z) L^{-T} (device-side scale
+// possible), then the verification Gram + density / xc of W~ in one pass
+template <int F>
+int launch_rotation_split_f(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab,
+                            double sa, const double* M, double* out, double* ws, double* G, double w,
+                            double occ, int xc, double* rho, double* vxc, double* bvec,
+                            const double* vext, double* dpart, cudaStream_t s, const double* sa_dev) {
+  constexpr int NPAD = 8 * F;
+  if (launch_mix_tma_f<F>(N, ld, ngl, A, Ab, sa, M, 1.0, nullptr, 0.0, 1, out, nullptr, s, nullptr,
+                          sa_dev) < 0)
+    return -1;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  if (!make_map2(maps, 0, out, ld, N, NPAD)) return -1;
+  const size_t red = (size_t)TSC * (F * (F + 1) / 2) * 64 + 2 * TSC;
+  TCfg cfg = tcfg(1, N, 0);
+  if (cfg.smem < 3072 + red * 8) cfg.smem = 3072 + red * 8;
+  const int64_t kblocks = (ld + TKS - 1) / TKS;
+  int nsplit = nsm();
+  if (nsplit > kblocks) nsplit = (int)kblocks;
+  const int64_t kchunk = ((kblocks + nsplit - 1) / nsplit) * TKS;
+  nsplit = (int)((ld + kchunk - 1) / kchunk);
+  ::po::count_launch();
+  auto k = gram_density_kernel<F>;
+  set_smem(reinterpret_cast<const void*>(k), (int)cfg.smem);
+  launch_pdl(k, dim3(nsplit), dim3(TTH), cfg.smem, s, maps, N, ld, ngl, kchunk, cfg.nst, ws, occ, xc,
+             rho, vxc, bvec, vext, dpart);
+  const int64_t threads = (int64_t)N * N * 32;
+  ::po::count_launch();
+  launch_pdl(gram_tma_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, N, NPAD,
+             1, nsplit, w, ws, G, (const double*)nullptr);
+  return nsplit;
+}
+
 int launch_rotate_fused(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab,
                         double sa, const double* M, double* out, double* ws, double* G, double w,
                         double occ, int xc, double* rho, double* vxc, double* bvec,
                         const double* vext, double* dpart, cudaStream_t s, const double* sa_dev) {
+  // measurement switch: rotation as the two-source mix + a Gram/density pass (slower: 250 vs 218 us at C2)
+  static const int split = getenv("PO_ROT_SPLIT") ? atoi(getenv("PO_ROT_SPLIT")) : 0;
+  if (split) {
+    switch ((N + 7) / 8) {
+#define PO_RS(F) \
+  case F:        \
+    return launch_rotation_split_f<F>(N, ld, ngl, A, Ab, sa, M, out, ws, G, w, occ, xc, rho, vxc, bvec, vext, dpart, s, sa_dev);
+      PO_RS(1) PO_RS(2) PO_RS(3) PO_RS(4) PO_RS(5) PO_RS(6)
+#undef PO_RS
+    }
+    return -1;
+  }
   switch ((N + 7) / 8) {
 #define PO_RF(F) \
   case F:        \

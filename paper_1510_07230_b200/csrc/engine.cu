@@ -295,7 +295,7 @@ void Engine::build_state(const double* u, int hartree, int xc, DevState* st, int
                          bool density_done) {
   double* b_local = density_b_target(hartree);
   const int pn = points_nblk(g);
-  if (!density_done) {  // else: rho, v_xc, 4 pi rho and S_EXC/S_EEXT came from the rotation
+  if (!density_done) {  // else: rho and 4 pi rho came from the rotation; v_xc, E_xc, E_ext below
     launch_density_xc(g, N, u, occ, xc, st->rho, st->v_xc, b_local, v_ext, partials, s);
     launch_reduce_rows(partials, 2, pn, g.w, scal() + S_EXC, s);  // E_xc = <eps, rho>, E_ext
   }
@@ -318,8 +318,10 @@ void Engine::build_state(const double* u, int hartree, int xc, DevState* st, int
   }
   // v_H slab copied out of the Poisson solution by the same pass that forms v_local
   launch_vlocal(g, v_ext, hartree ? cg_x + g.z0 * g.plane : nullptr, st->v_h, st->v_xc, st->rho,
-               st->v_local, partials, s);
+               st->v_local, partials, s, density_done ? (xc ? 1 : 0) : -1);
   launch_reduce_rows(partials, 1, pn, 0.5 * g.w, scal() + S_EH, s);  // E_H = 1/2 <v_H, rho>
+  if (density_done)  // E_xc = w <eps, rho>, E_ext = w <V_ext, rho> (S_EXC, S_EEXT)
+    launch_reduce_rows(partials + pn, 2, pn, g.w, scal() + S_EXC, s);
   if (size > 1) comm->allreduce_sum(scal() + S_EXC, 3, s);          // S_EXC..S_EH
   PO_CUDA(cudaGetLastError());
   if (!xc) PO_CUDA(cudaMemsetAsync(scal() + S_EXC, 0, sizeof(double), s));

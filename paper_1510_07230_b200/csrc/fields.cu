@@ -70,26 +70,52 @@ __global__ void __launch_bounds__(PT) density_xc_kernel(SlabGeom g, int N,
 }
 
 // vh_src: the Poisson solution slab (copied into the state's v_H here) or null
-// for "no Hartree" (v_H = 0 written).
+// for "no Hartree" (v_H = 0 written). xc_here >= 0: v_xc is formed here from
+// rho (the Dirac term of energy.cpp:212-226 when xc_here = 1, zero when 0) and
+// the partials carry [<v_H, rho> | <eps, rho> | <V_ext, rho>] — the trial
+// rotation then only writes rho (its cube roots ran on 4 of 32 lanes there);
+// xc_here < 0: v_xc was written by the density pass, partials [<v_H, rho>].
 __global__ void __launch_bounds__(PT) vlocal_kernel(SlabGeom g, const double* __restrict__ vext,
                                                     const double* __restrict__ vh_src,
                                                     double* __restrict__ vh,
-                                                    const double* __restrict__ vxc,
+                                                    double* __restrict__ vxc,
                                                     const double* __restrict__ rho,
                                                     double* __restrict__ vloc,
-                                                    double* __restrict__ partials) {
+                                                    double* __restrict__ partials, int xc_here) {
   PO_PDL_ENTRY();
-  __shared__ double red[32];
-  double acc[1] = {0.0};
+  __shared__ double red[3 * 32];
+  double acc[3] = {0.0, 0.0, 0.0};
+  const double cx = dirac_cx();
   for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < g.ngl;
        p += (int64_t)gridDim.x * PT) {
     const double h = vh_src ? vh_src[p] : 0.0;
+    const double r = rho[p];
     vh[p] = h;
-    vloc[p] = vext[p] + (h + vxc[p]);
-    acc[0] += h * rho[p];
+    double x;
+    if (xc_here < 0) {
+      x = vxc[p];
+    } else if (xc_here) {
+      const double eps = -cx * cbrt(r);
+      x = eps * (4.0 / 3.0);
+      vxc[p] = x;
+      acc[1] += eps * r;
+    } else {
+      x = 0.0;
+      vxc[p] = 0.0;
+    }
+    const double ve = vext[p];
+    vloc[p] = ve + (h + x);
+    acc[0] += h * r;
+    acc[2] += ve * r;
   }
-  block_sum<1>(acc, red);
-  if (threadIdx.x == 0) partials[blockIdx.x] = acc[0];
+  block_sum<3>(acc, red);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = acc[0];
+    if (xc_here >= 0) {
+      partials[gridDim.x + blockIdx.x] = acc[1];
+      partials[2 * gridDim.x + blockIdx.x] = acc[2];
+    }
+  }
 }
 
 // grid: (nblk, N)
@@ -370,11 +396,11 @@ void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupat
 }
 
 void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h_src, double* v_h,
-                   const double* v_xc, const double* rho, double* v_local, double* partials,
-                   cudaStream_t s) {
+                   double* v_xc, const double* rho, double* v_local, double* partials,
+                   cudaStream_t s, int xc_here) {
   ::po::count_launch();
-  launch_pdl(vlocal_kernel, dim3(points_nblk(g)), dim3(PT), 0, s, g, v_ext, v_h_src, v_h, v_xc, rho, v_local,
-                                              partials);
+  launch_pdl(vlocal_kernel, dim3(points_nblk(g)), dim3(PT), 0, s, g, v_ext, v_h_src, v_h, v_xc, rho,
+             v_local, partials, xc_here);
 }
 
 void launch_residual_diag(const SlabGeom& g, int N, const double* u, const double* hu,

@@ -44,9 +44,11 @@ void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupat
                        double* rho, double* v_xc, double* b, const double* v_ext, double* partials,
                        cudaStream_t s, const double* guard = nullptr);
 // v_local = v_ext + (v_h + v_xc) (energy.cpp:241-244); partials [1][nblk]: sum v_h*rho.
+// xc_here >= 0: v_xc formed here from rho (Dirac when 1, zero when 0) and partials
+// [3][nblk]: sum v_h*rho, sum eps*rho, sum v_ext*rho.
 void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h_src, double* v_h,
-                   const double* v_xc, const double* rho, double* v_local, double* partials,
-                   cudaStream_t s);
+                   double* v_xc, const double* rho, double* v_local, double* partials,
+                   cudaStream_t s, int xc_here = -1);
 // z_i = hu_i - sigma_ii u_i (manifold.cpp:204-216); partials [1][N][nblk]: sum z^2.
 void launch_residual_diag(const SlabGeom& g, int N, const double* u, const double* hu,
                           const double* sigma_diag, double* z, double* partials, cudaStream_t s);

@@ -177,13 +177,15 @@ bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, doubl
   bool fused = false;
   if (st && E.N <= 48 && tma2d_available()) {
     // rotation + verification Gram + density/xc of the rotated block in one pass
+    // (xc = -1: the rotation writes rho and 4 pi rho only; v_xc, E_xc and E_ext
+    // come from the v_local pass of build_state(density_done))
+    (void)xc;
     const int nb = launch_rotate_fused(E.N, E.g.ld, E.g.ngl, A, Ab, sa, E.dmat[1], out, E.gram_ws,
-                                       E.dmat[2], E.g.w, E.occ, xc, st->rho, st->v_xc,
+                                       E.dmat[2], E.g.w, E.occ, -1, st->rho, st->v_xc,
                                        E.density_b_target(hartree), E.v_ext, E.partials, E.s,
                                        tau_dev ? tau_dev + 1 : nullptr);
     if (nb >= 0) {
       if (E.size > 1) E.comm->allreduce_sum(E.dmat[2], (size_t)E.N * E.N, E.s);
-      launch_reduce_rows(E.partials, 2, nb, E.g.w, sc + Engine::S_EXC, E.s);
       fused = true;
     }
   }
