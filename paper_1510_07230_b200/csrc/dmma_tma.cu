@@ -1788,11 +1788,20 @@ __device__ __forceinline__ void mix_big_slice(double (&acc)[2][16][2], const dou
   }
 }
 
+// DIR: the compute_directions pass for N > 64 (manifold.cpp:181-216,
+// optimizer.cpp:265-320, 386-397) on the same tiles: D = HW - W Sigma is formed
+// and reduced (never stored), and the epilogue also writes z = HW - sigma_ii W
+// and reduces ||z||^2 and the BB products ss, sy, yy against (W_prev, Z_prev):
+// partial rows [zz | dd | ss | sy | yy] x n_pt in dpart (the residual pass over
+// five blocks disappears; W rows come back from L2).
+template <bool DIR>
 __global__ void __launch_bounds__(XTH, 1) mix_big_kernel(
     const __grid_constant__ Maps maps, int has_ab, int N, int64_t ld, int64_t ngl, int n_pt,
     int n_it, int upper, int nst, double sa, double alpha, const double* __restrict__ C,
     double beta, double* __restrict__ out, double* __restrict__ norms,
-    const double* __restrict__ guard) {
+    const double* __restrict__ guard, const double* __restrict__ wraw,
+    const double* __restrict__ sig, const double* __restrict__ wp, const double* __restrict__ zp,
+    double* __restrict__ zout, double* __restrict__ dpart) {
   PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
@@ -1917,6 +1926,72 @@ __global__ void __launch_bounds__(XTH, 1) mix_big_kernel(
       }
       // epilogue: acc[q][2 g + e][j] = out(point 16 g + 2 gq + e, orbital i0 + 8 F_q + 2 t4 + j)
       const int64_t pb = (int64_t)pt * XP + 2 * gq;
+      if constexpr (DIR) {
+        const bool hist = wp != nullptr;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (!(q ? real1 : real0)) continue;
+          const int F = q ? F1 : F0;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int i = i0 + 8 * F + 2 * t4 + j;
+            double r5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // zz, dd, ss, sy, yy
+            if (i < N) {
+              const double ms = -sig[i];
+              const int64_t o = (int64_t)i * ld;
+#pragma unroll
+              for (int gg = 0; gg < 8; ++gg) {
+                const int64_t p = pb + 16 * gg;
+                if (p >= ngl) continue;
+                const int ne = p + 1 < ngl ? 2 : 1;
+                const bool two = ne == 2;
+                double2 hv, wv, wq = make_double2(0.0, 0.0), zq = make_double2(0.0, 0.0);
+                if (two) {
+                  hv = *reinterpret_cast<const double2*>(C + o + p);
+                  wv = *reinterpret_cast<const double2*>(wraw + o + p);
+                  if (hist) {
+                    wq = *reinterpret_cast<const double2*>(wp + o + p);
+                    zq = *reinterpret_cast<const double2*>(zp + o + p);
+                  }
+                } else {
+                  hv = make_double2(C[o + p], 0.0);
+                  wv = make_double2(wraw[o + p], 0.0);
+                  if (hist) {
+                    wq = make_double2(wp[o + p], 0.0);
+                    zq = make_double2(zp[o + p], 0.0);
+                  }
+                }
+                const double d0 = alpha * acc[q][2 * gg][j] + beta * hv.x;
+                const double d1 = two ? alpha * acc[q][2 * gg + 1][j] + beta * hv.y : 0.0;
+                r5[1] += d0 * d0 + d1 * d1;
+                // z = HW - sigma_ii W (residual_bb_kernel)
+                const double v0 = hv.x + ms * wv.x, v1 = two ? hv.y + ms * wv.y : 0.0;
+                if (two)
+                  *reinterpret_cast<double2*>(zout + o + p) = make_double2(v0, v1);
+                else
+                  zout[o + p] = v0;
+                r5[0] += v0 * v0 + v1 * v1;
+                if (hist) {
+                  const double s0 = wv.x - wq.x, y0 = v0 - zq.x;
+                  const double s1 = two ? wv.y - wq.y : 0.0, y1 = two ? v1 - zq.y : 0.0;
+                  r5[2] += s0 * s0 + s1 * s1;
+                  r5[3] += s0 * y0 + s1 * y1;
+                  r5[4] += y0 * y0 + y1 * y1;
+                }
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < 5; ++r) {
+              double v = r5[r];
+              v += __shfl_xor_sync(0xffffffffu, v, 4);
+              v += __shfl_xor_sync(0xffffffffu, v, 8);
+              v += __shfl_xor_sync(0xffffffffu, v, 16);
+              if (gq == 0 && i < N && (hist || r < 2)) dpart[((int64_t)r * N + i) * n_pt + pt] = v;
+            }
+          }
+        }
+        continue;
+      }
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         if (!(q ? real1 : real0)) continue;
@@ -2030,10 +2105,44 @@ int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double
   const int n_it = (N + XI - 1) / XI;
   const int ntiles = n_pt * n_it;
   const int grid = ntiles < nsm() ? ntiles : nsm();
-  set_smem(reinterpret_cast<const void*>(mix_big_kernel), (int)smem);
+  set_smem(reinterpret_cast<const void*>(mix_big_kernel<false>), (int)smem);
   ::po::count_launch();
-  launch_pdl(mix_big_kernel, dim3(grid), dim3(XTH), smem, s, maps, Ab ? 1 : 0, N, ld, ngl, n_pt, n_it, upper, nst, sa,
-                                         alpha, C, beta, out, norms, guard);
+  launch_pdl(mix_big_kernel<false>, dim3(grid), dim3(XTH), smem, s, maps, Ab ? 1 : 0, N, ld, ngl, n_pt,
+             n_it, upper, nst, sa, alpha, C, beta, out, norms, guard, (const double*)nullptr,
+             (const double*)nullptr, (const double*)nullptr, (const double*)nullptr, (double*)nullptr,
+             (double*)nullptr);
+  return n_pt;
+}
+
+int launch_directions_big(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
+                          const double* WP, const double* ZP, const double* Sigma, const double* sig,
+                          double* Z, double* partials, cudaStream_t s) {
+  static const int off = getenv("PO_NO_DIR_BIG") ? atoi(getenv("PO_NO_DIR_BIG")) : 0;  // measurement
+  if (off || N <= 64 || !tma2d_available()) return -1;
+  const int np = (N + 15) & ~15;
+  double* mt = mix_big_scratch(s, (size_t)np * np);
+  if (!mt) return -1;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  if (!make_map(&maps.m[0], W, ld, N, XK)) return -1;
+  if (!make_map(&maps.m[1], mt, np, np, XI)) return -1;
+  const size_t sdoubles = (size_t)2 * XP * XK;
+  const size_t fixed = 1024 + 1024;
+  int nst = (int)((200 * 1024 - fixed) / (sdoubles * 8));
+  if (nst > 8) nst = 8;
+  const size_t smem = fixed + (size_t)nst * sdoubles * 8;
+  ::po::count_launch();
+  launch_pdl(transpose_pad_kernel, dim3((unsigned)(((int64_t)np * np + 255) / 256)), dim3(256), 0, s, N,
+             np, Sigma, mt);
+  const int n_pt = mix_big_nblk(ngl);
+  const int n_it = (N + XI - 1) / XI;
+  const int ntiles = n_pt * n_it;
+  const int grid = ntiles < nsm() ? ntiles : nsm();
+  set_smem(reinterpret_cast<const void*>(mix_big_kernel<true>), (int)smem);
+  ::po::count_launch();
+  launch_pdl(mix_big_kernel<true>, dim3(grid), dim3(XTH), smem, s, maps, 0, N, ld, ngl, n_pt, n_it, 0,
+             nst, 0.0, -1.0, HW, 1.0, (double*)nullptr, (double*)nullptr, (const double*)nullptr, W, sig,
+             WP, ZP, Z, partials);
   return n_pt;
 }
 

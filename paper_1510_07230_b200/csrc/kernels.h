@@ -147,6 +147,12 @@ int launch_mix_tma(int N, int64_t ld, int64_t ngl, const double* A, const double
 int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
                    const double* M, double alpha, const double* C, double beta, int upper,
                    double* out, double* norms, cudaStream_t s, const double* guard);
+// compute_directions for N > 64 on the large-N mix tiles: writes Z = HW - diag(sig) W and
+// partial rows [zz | dd | ss | sy | yy] x n_pt (dd = ||HW - W Sigma||^2; the last three
+// only with WP / ZP). Returns n_pt or -1 when unavailable.
+int launch_directions_big(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
+                          const double* WP, const double* ZP, const double* Sigma, const double* sig,
+                          double* Z, double* partials, cudaStream_t s);
 // Batched left-multiply out_b = S X_b for X_b = rows [N][ld] at A + b * bstride
 // (valid row length ngl; ld multiple of 32, padding zero). DST transforms.
 void launch_mix_batched(int N, int64_t ld, int64_t ngl, int batch, int64_t bstride,

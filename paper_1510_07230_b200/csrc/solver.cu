@@ -467,7 +467,17 @@ void Solver::enqueue_phase1(int iter) {
         }
         launch_copy_diag(n, E.dmat[4], E.dvec + E.off_sig(), E.s);
       }
-      if (history_valid) {  // z, ||z||^2 and the BB products in one pass
+      int dnb = -1;
+      if (need_full && !mean_abs && E.size == 1)
+        // z, ||z||^2, ||HW - W Sigma||^2 and the BB products on the large-N mix tiles
+        dnb = launch_directions_big(n, E.g.ld, E.g.ngl, P(w), P(hw),
+                                    history_valid ? P(prev_w) : nullptr,
+                                    history_valid ? P(prev_z) : nullptr, E.dmat[4],
+                                    E.dvec + E.off_sig(), P(z), E.partials, E.s);
+      if (dnb >= 0) {
+        E.reduce_rows(E.partials, (history_valid ? 5 : 2) * n, dnb, E.g.w, E.dvec + E.off_zz(), true);
+        bb_done = history_valid;
+      } else if (history_valid) {  // z, ||z||^2 and the BB products in one pass
         launch_residual_bb(E.g, n, P(w), P(hw), E.dvec + E.off_sig(), P(prev_w), P(prev_z), P(z),
                            E.partials, E.s);
         E.reduce_rows(E.partials, n, onb, E.g.w, E.dvec + E.off_zz(), true);
@@ -477,7 +487,7 @@ void Solver::enqueue_phase1(int iter) {
         launch_residual_diag(E.g, n, P(w), P(hw), E.dvec + E.off_sig(), P(z), E.partials, E.s);
         E.reduce_rows(E.partials, n, onb, E.g.w, E.dvec + E.off_zz(), true);
       }
-      if (need_full) {
+      if (need_full && dnb < 0) {
         if (mean_abs) dscratch = pool.get();
         E.mix(P(w), nullptr, 0.0, E.dmat[4], -1.0, P(hw), 1.0, 0, dscratch ? P(dscratch) : nullptr,
               E.dvec + E.off_dd());
