@@ -2038,6 +2038,191 @@ __global__ void __launch_bounds__(XTH, 1) mix_big_kernel(
   }
 }
 
+
+// Upper-triangular mix (the orthonormalisation rotation W L^{-T}) with the
+// triangle balanced per SM sub-partition. A 128-point tile is split into two
+// 64-point halves: consumer warps 0-3 (one per sub-partition) walk the k
+// chunks of the first half forwards, warps 4-7 those of the second half
+// backwards, and warp a of either half owns output fragments
+// {a, 7-a, 8+a, 15-a}. In the diagonal block an 8-input slice kb meets the
+// fragments >= kb, so a sub-partition (warp a forwards at slice kb, warp 4+a
+// backwards at 15-kb) always has 4 or 5 active fragment groups — constant
+// DMMA pressure instead of 4 -> 1 over the block (mix_big_kernel: 60% of FP64
+// on the triangle vs 82% dense). A stage carries both halves' chunks and both
+// M^T boxes. N a multiple of 128 (every fragment real).
+template <int CNT>
+__device__ __forceinline__ void mix_tri_slice(double (&acc)[4][8][2], const double* sa_,
+                                              const double* mt, int h, int a, int gq, int t4) {
+  // the CNT highest of the warp's sorted fragments {a, 7-a, 8+a, 15-a} take part
+  const int fr[4] = {a, 7 - a, 8 + a, 15 - a};
+  double2 b[4];
+#pragma unroll
+  for (int f = 4 - CNT; f < 4; ++f)
+    b[f] = *reinterpret_cast<const double2*>(mt + swz(8 * fr[f] + gq, 8 * h + 2 * t4, XI));
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    double2 av[2];
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2)
+      av[s2] = *reinterpret_cast<const double2*>(sa_ + swz(8 * h + 2 * t4 + s2, 16 * g + 2 * gq, XK));
+#pragma unroll
+    for (int f = 4 - CNT; f < 4; ++f) {
+      dmma_8x8x4(acc[f][2 * g], av[0].x, b[f].x);
+      dmma_8x8x4(acc[f][2 * g + 1], av[0].y, b[f].x);
+      dmma_8x8x4(acc[f][2 * g], av[1].x, b[f].y);
+      dmma_8x8x4(acc[f][2 * g + 1], av[1].y, b[f].y);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
+    const __grid_constant__ Maps maps, int has_ab, int N, int64_t ld, int64_t ngl, int n_pt,
+    int n_it, int nst, double sa, double alpha, double* __restrict__ out,
+    const double* __restrict__ guard) {
+  PO_PDL_ENTRY();
+  if (guard && *guard == 0.0) return;
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
+  uint64_t* empty = full + 8;
+  uint64_t* ready = full + 16;
+  double* stage0 = reinterpret_cast<double*>(tsm + 1024);
+  constexpr size_t QH = (size_t)64 * XK;  // doubles per half per source per stage
+  constexpr size_t QM = (size_t)XI * XK;  // one M^T box
+  const int nsrc = has_ab ? 2 : 1;
+  // stage: [A half 0][A half 1]([Ab half 0][Ab half 1])[M^T chunk of half 0][M^T chunk of half 1]
+  const size_t mofs = (size_t)2 * nsrc * QH;
+  const size_t sdoubles = mofs + 2 * QM;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+      mbar_init(&ready[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int ntiles = n_pt * n_it;
+  auto tile_of = [&](int t, int& pt, int& it) {
+    it = n_it - 1 - t / n_pt;
+    pt = t % n_pt;
+  };
+  const int lane = threadIdx.x & 31;
+  int warp = threadIdx.x >> 5;
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (warp == 0 && lane == 0) {
+      for (int q = 0; q <= nsrc; ++q)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[q])));
+      const uint32_t bytes = (uint32_t)(sdoubles * 8);
+      int g = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int pt, it;
+        tile_of(t, pt, it);
+        const int nk = (it + 1) * XI / XK;  // upper: k < i0 + 128
+        for (int c = 0; c < nk; ++c, ++g) {
+          const int s = g % nst;
+          if (g >= nst) mbar_wait(&empty[s], ((uint32_t)(g / nst) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&full[s], bytes);
+          double* sb = stage0 + (size_t)s * sdoubles;
+          for (int hf = 0; hf < 2; ++hf) {
+            const int ck = hf ? nk - 1 - c : c;  // the second half walks k backwards
+            for (int q = 0; q < nsrc; ++q)
+              for (int b = 0; b < 4; ++b)
+                tma_load_2d(sb + (q * 2 + hf) * QH + b * BOX * XK, &maps.m[q],
+                            pt * XP + hf * 64 + b * BOX, ck * XK, &full[s]);
+            tma_load_2d(sb + mofs + hf * QM, &maps.m[nsrc], ck * XK, it * XI, &full[s]);
+          }
+        }
+      }
+    } else if (warp > 0 && has_ab) {  // A + sa Ab in place (both halves)
+      const int ct = threadIdx.x - 32;
+      int g = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int pt, it;
+        tile_of(t, pt, it);
+        const int nk = (it + 1) * XI / XK;
+        for (int c = 0; c < nk; ++c, ++g) {
+          const int s = g % nst;
+          mbar_wait(&full[s], (uint32_t)(g / nst) & 1u);
+          double2* a2 = reinterpret_cast<double2*>(stage0 + (size_t)s * sdoubles);
+          const double2* b2 = reinterpret_cast<const double2*>(stage0 + (size_t)s * sdoubles + 2 * QH);
+          for (int e = ct; e < (int)QH; e += 96) {  // 2 * QH doubles = QH double2
+            double2 v = a2[e];
+            const double2 z = b2[e];
+            v.x += sa * z.x;
+            v.y += sa * z.y;
+            a2[e] = v;
+          }
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          asm volatile("bar.sync 2, 96;\n" ::: "memory");
+          if (ct == 0) mbar_arrive(&ready[s]);
+        }
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    warp -= 4;
+    const int gq = lane >> 2, t4 = lane & 3;
+    const int hf = warp >> 2, a = warp & 3;  // half (0 forwards, 1 backwards), fragment set
+    const int fr[4] = {a, 7 - a, 8 + a, 15 - a};
+    int g = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int pt, it;
+      tile_of(t, pt, it);
+      const int i0 = it * XI;
+      const int nk = (it + 1) * XI / XK;
+      double acc[4][8][2];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) acc[f][m][0] = acc[f][m][1] = 0.0;
+      for (int c = 0; c < nk; ++c, ++g) {
+        const int s = g % nst;
+        mbar_wait(has_ab ? &ready[s] : &full[s], (uint32_t)(g / nst) & 1u);
+        const double* sb = stage0 + (size_t)s * sdoubles;
+        const double* sa_ = sb + hf * QH;
+        const double* mt = sb + mofs + hf * QM;
+        const int ck = hf ? nk - 1 - c : c;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int h = hf ? 1 - hh : hh;
+          const int kb = (ck * XK + 8 * h - i0) >> 3;  // slice index relative to the tile
+          const int cnt = (kb <= fr[0]) + (kb <= fr[1]) + (kb <= fr[2]) + (kb <= fr[3]);
+          if (cnt == 4)
+            mix_tri_slice<4>(acc, sa_, mt, h, a, gq, t4);
+          else if (cnt == 3)
+            mix_tri_slice<3>(acc, sa_, mt, h, a, gq, t4);
+          else if (cnt == 2)
+            mix_tri_slice<2>(acc, sa_, mt, h, a, gq, t4);
+          else if (cnt == 1)
+            mix_tri_slice<1>(acc, sa_, mt, h, a, gq, t4);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      // epilogue: acc[f][2 g + e][j] = out(point 64 hf + 16 g + 2 gq + e, orbital i0 + 8 fr[f] + 2 t4 + j)
+      const int64_t pb = (int64_t)pt * XP + 64 * hf + 2 * gq;
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = i0 + 8 * fr[f] + 2 * t4 + j;
+#pragma unroll
+          for (int gg = 0; gg < 4; ++gg) {
+            const int64_t p = pb + 16 * gg;
+            if (p >= ngl) continue;
+            const double v0 = alpha * acc[f][2 * gg][j], v1 = alpha * acc[f][2 * gg + 1][j];
+            if (p + 1 < ngl)
+              *reinterpret_cast<double2*>(out + (int64_t)i * ld + p) = make_double2(v0, v1);
+            else
+              out[(int64_t)i * ld + p] = v0;
+          }
+        }
+    }
+  }
+}
+
 __global__ void transpose_pad_kernel(int N, int np, const double* __restrict__ M,
                                      double* __restrict__ Mt) {
   PO_PDL_ENTRY();
@@ -2092,7 +2277,9 @@ int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double
   if (Ab && !make_map(&maps.m[q++], Ab, ld, N, XK)) PO_MB_FAIL("map Ab");
   if (!make_map(&maps.m[q++], mt, np, np, XI)) PO_MB_FAIL("map Mt");
   const int nsrc = Ab ? 2 : 1;
-  const size_t sdoubles = (size_t)(nsrc + 1) * XP * XK;
+  static const int tri_env = getenv("PO_MIX_TRI") ? atoi(getenv("PO_MIX_TRI")) : 1;  // measurement
+  const bool tri = tri_env && upper && !C && !norms && N % XI == 0;
+  const size_t sdoubles = tri ? (size_t)2 * nsrc * 64 * XK + 2 * XI * XK : (size_t)(nsrc + 1) * XP * XK;
   const size_t fixed = 1024 + 1024;  // barriers, alignment slack
   int nst = (int)((200 * 1024 - fixed) / (sdoubles * 8));
   if (nst > 8) nst = 8;
@@ -2105,6 +2292,13 @@ int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double
   const int n_it = (N + XI - 1) / XI;
   const int ntiles = n_pt * n_it;
   const int grid = ntiles < nsm() ? ntiles : nsm();
+  if (tri) {
+    set_smem(reinterpret_cast<const void*>(mix_tri_kernel), (int)smem);
+    ::po::count_launch();
+    launch_pdl(mix_tri_kernel, dim3(grid), dim3(XTH), smem, s, maps, Ab ? 1 : 0, N, ld, ngl, n_pt, n_it,
+               nst, sa, alpha, out, guard);
+    return n_pt;
+  }
   set_smem(reinterpret_cast<const void*>(mix_big_kernel<false>), (int)smem);
   ::po::count_launch();
   launch_pdl(mix_big_kernel<false>, dim3(grid), dim3(XTH), smem, s, maps, Ab ? 1 : 0, N, ld, ngl, n_pt,

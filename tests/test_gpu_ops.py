@@ -214,12 +214,14 @@ def test_dmma_multitile(port, native, n_orb, n):
 
 
 @pytest.mark.parametrize("n_orb,n", [(65, (9, 9, 11)), (67, (9, 9, 11)), (128, (12, 13, 14)),
-                                     (130, (9, 9, 11)), (200, (24, 20, 22)), (260, (10, 9, 11))])
+                                     (130, (9, 9, 11)), (200, (24, 20, 22)), (256, (10, 9, 11)),
+                                     (260, (10, 9, 11))])
 def test_mix_big(native, n_orb, n):
     """Large-N TMA mix (N > 64, manifold.cpp:67-85): full, upper-triangular
     (L^{-T}, manifold.cpp:97-114), the trial rotation (W - tau Z) L^{-T} and the
     gradient norms of D = HW - W Sigma (manifold.cpp:181-202); odd point counts
-    exercise the ragged last tile, N > 128 several orbital tiles."""
+    exercise the ragged last tile, N > 128 several orbital tiles; N = 128 / 256 take
+    the balanced triangular kernel (forward / backward point halves)."""
     spec = configs.ProblemSpec("mixbig", n, (5.0, 5.0, 5.0), [], n_orb, hartree=False, xc=False)
     e = native.engine_for(spec)
     rng = np.random.default_rng(11 + n_orb)
