@@ -333,9 +333,13 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
             v[m] = *reinterpret_cast<const double2*>(sbuf + q * qstride + pad(row, c + 2 * m));
         };
         auto dot8 = [](const double2 (&x)[4], const double2 (&y)[4], double t) {
-#pragma unroll
-          for (int m = 0; m < 4; ++m) t = fma(x[m].y, y[m].y, fma(x[m].x, y[m].x, t));
-          return t;
+          // four independent products chains instead of one 8-deep FMA chain
+          double p0 = x[0].x * y[0].x, p1 = x[0].y * y[0].y, p2 = x[1].x * y[1].x, p3 = x[1].y * y[1].y;
+          p0 = fma(x[2].x, y[2].x, p0);
+          p1 = fma(x[2].y, y[2].y, p1);
+          p2 = fma(x[3].x, y[3].x, p2);
+          p3 = fma(x[3].y, y[3].y, p3);
+          return t + ((p0 + p1) + (p2 + p3));
         };
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -1010,13 +1014,16 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
           for (int h = 0; h < 2; ++h) {
             const int i = lane + 32 * h;
             if (i >= N || i > rr) continue;
-            double t = racc[h][r];
+            double2 av[4];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
-              const double2 av = *reinterpret_cast<const double2*>(sbuf + (i) * PW + c + 2 * m);
-              t = fma(av.y, bv[m].y, fma(av.x, bv[m].x, t));
-            }
-            racc[h][r] = t;
+            for (int m = 0; m < 4; ++m) av[m] = *reinterpret_cast<const double2*>(sbuf + (i) * PW + c + 2 * m);
+            double p0 = av[0].x * bv[0].x, p1 = av[0].y * bv[0].y, p2 = av[1].x * bv[1].x,
+                   p3 = av[1].y * bv[1].y;
+            p0 = fma(av[2].x, bv[2].x, p0);
+            p1 = fma(av[2].y, bv[2].y, p1);
+            p2 = fma(av[3].x, bv[3].x, p2);
+            p3 = fma(av[3].y, bv[3].y, p3);
+            racc[h][r] += (p0 + p1) + (p2 + p3);
           }
         }
       }
