@@ -319,9 +319,12 @@ void Engine::build_state(const double* u, int hartree, int xc, DevState* st, int
   // v_H slab copied out of the Poisson solution by the same pass that forms v_local
   launch_vlocal(g, v_ext, hartree ? cg_x + g.z0 * g.plane : nullptr, st->v_h, st->v_xc, st->rho,
                st->v_local, partials, s, density_done ? (xc ? 1 : 0) : -1);
-  launch_reduce_rows(partials, 1, pn, 0.5 * g.w, scal() + S_EH, s);  // E_H = 1/2 <v_H, rho>
-  if (density_done)  // E_xc = w <eps, rho>, E_ext = w <V_ext, rho> (S_EXC, S_EEXT)
-    launch_reduce_rows(partials + pn, 2, pn, g.w, scal() + S_EXC, s);
+  if (density_done) {  // E_xc = w <eps, rho>, E_ext = w <V_ext, rho>, E_H = 1/2 w <v_H, rho>
+    const double sc[3] = {g.w, g.w, 0.5 * g.w};
+    launch_reduce_rows_grouped(partials, 1, 3, pn, sc, scal() + S_EXC, s);
+  } else {
+    launch_reduce_rows(partials, 1, pn, 0.5 * g.w, scal() + S_EH, s);  // E_H = 1/2 <v_H, rho>
+  }
   if (size > 1) comm->allreduce_sum(scal() + S_EXC, 3, s);          // S_EXC..S_EH
   PO_CUDA(cudaGetLastError());
   if (!xc) PO_CUDA(cudaMemsetAsync(scal() + S_EXC, 0, sizeof(double), s));
@@ -354,9 +357,9 @@ void Engine::apply_h(const double* u, double* out, const double* v_local, bool w
   const double* hi = (size > 1 && rank + 1 < size) ? halo_hi : nullptr;
   launch_hamiltonian2(g, N, u, lo, hi, v_local, with_ext ? v_ext : nullptr, out, partials, s);
   const int nb = hamiltonian2_nblk(g);
-  launch_reduce_rows(partials, N, nb, g.w, dvec + off_sig(), s);
-  launch_reduce_rows(partials + (size_t)N * nb, N, nb, -0.5 * g.w, dvec + off_kin(), s);
-  if (with_ext) launch_reduce_rows(partials + (size_t)2 * N * nb, N, nb, g.w, dvec + off_ext(), s);
+  // sigma_ii (w), kinetic (-w/2), external (w): one launch over the consecutive rows
+  const double sc[3] = {g.w, -0.5 * g.w, g.w};
+  launch_reduce_rows_grouped(partials, N, with_ext ? 3 : 2, nb, sc, dvec + off_sig(), s);
   if (size > 1) comm->allreduce_sum(dvec + off_sig(), (size_t)(with_ext ? 3 : 2) * N, s);
 }
 

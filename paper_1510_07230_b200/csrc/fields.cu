@@ -110,10 +110,12 @@ __global__ void __launch_bounds__(PT) vlocal_kernel(SlabGeom g, const double* __
   }
   block_sum<3>(acc, red);
   if (threadIdx.x == 0) {
-    partials[blockIdx.x] = acc[0];
-    if (xc_here >= 0) {
-      partials[gridDim.x + blockIdx.x] = acc[1];
-      partials[2 * gridDim.x + blockIdx.x] = acc[2];
+    if (xc_here >= 0) {  // rows in S_EXC, S_EEXT, S_EH order: one grouped reduction
+      partials[blockIdx.x] = acc[1];
+      partials[gridDim.x + blockIdx.x] = acc[2];
+      partials[2 * gridDim.x + blockIdx.x] = acc[0];
+    } else {
+      partials[blockIdx.x] = acc[0];
     }
   }
 }
@@ -227,9 +229,11 @@ __global__ void __launch_bounds__(PT) lincomb_kernel(int64_t total, const double
 }
 
 // One warp per row; lanes stride the partials, then a fixed shuffle tree.
+// rows in [grp, 2 grp) take scale2, rows from 2 grp on scale3 (grp = 0: one scale)
 __global__ void reduce_rows_kernel(const double* __restrict__ partials, int rows, int nblk,
                                    double scale, double* __restrict__ out,
-                                   const double* __restrict__ guard) {
+                                   const double* __restrict__ guard, int grp, double scale2,
+                                   double scale3) {
   PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -239,7 +243,8 @@ __global__ void reduce_rows_kernel(const double* __restrict__ partials, int rows
   double s = 0.0;
   for (int b = lane; b < nblk; b += 32) s += p[b];
   s = warp_sum(s);
-  if (lane == 0) out[warp] = scale * s;
+  const double sc = grp <= 0 || warp < grp ? scale : (warp < 2 * grp ? scale2 : scale3);
+  if (lane == 0) out[warp] = sc * s;
 }
 
 // energy.cpp:78-99 (softened Coulomb) or BASELINE C5 Gaussian wells.
@@ -444,7 +449,18 @@ void launch_reduce_rows(const double* partials, int rows, int nblk, double scale
   const int threads = 256;
   const int blocks = (rows * 32 + threads - 1) / threads;
   ::po::count_launch();
-  launch_pdl(reduce_rows_kernel, dim3(blocks), dim3(threads), 0, s, partials, rows, nblk, scale, out, guard);
+  launch_pdl(reduce_rows_kernel, dim3(blocks), dim3(threads), 0, s, partials, rows, nblk, scale, out, guard,
+             0, 0.0, 0.0);
+}
+
+void launch_reduce_rows_grouped(const double* partials, int grp, int ngroups, int nblk,
+                                const double* scales, double* out, cudaStream_t s) {
+  const int rows = grp * ngroups;
+  const int threads = 256;
+  const int blocks = (rows * 32 + threads - 1) / threads;
+  ::po::count_launch();
+  launch_pdl(reduce_rows_kernel, dim3(blocks), dim3(threads), 0, s, partials, rows, nblk, scales[0], out,
+             (const double*)nullptr, grp, ngroups > 1 ? scales[1] : 0.0, ngroups > 2 ? scales[2] : 0.0);
 }
 
 void launch_external_potential(const SlabGeom& g, const double* h3, const double* atoms,

@@ -45,7 +45,7 @@ void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupat
                        cudaStream_t s, const double* guard = nullptr);
 // v_local = v_ext + (v_h + v_xc) (energy.cpp:241-244); partials [1][nblk]: sum v_h*rho.
 // xc_here >= 0: v_xc formed here from rho (Dirac when 1, zero when 0) and partials
-// [3][nblk]: sum v_h*rho, sum eps*rho, sum v_ext*rho.
+// [3][nblk]: sum eps*rho, sum v_ext*rho, sum v_h*rho.
 void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h_src, double* v_h,
                    double* v_xc, const double* rho, double* v_local, double* partials,
                    cudaStream_t s, int xc_here = -1);
@@ -67,6 +67,9 @@ void launch_abs_sum(const SlabGeom& g, int N, const double* x, double* partials,
 // out[r] = scale * sum_b partials[r * nblk + b], fixed order (deterministic).
 void launch_reduce_rows(const double* partials, int rows, int nblk, double scale, double* out,
                         cudaStream_t s, const double* guard = nullptr);
+// ngroups (<= 3) consecutive groups of grp rows, group q scaled by scales[q], one launch.
+void launch_reduce_rows_grouped(const double* partials, int grp, int ngroups, int nblk,
+                                const double* scales, double* out, cudaStream_t s);
 // V_ext from softened-Coulomb atoms (energy.cpp:78-99) / Gaussian wells (C5).
 void launch_external_potential(const SlabGeom& g, const double* h3, const double* atoms,
                                int natoms, int gaussian, double* v, cudaStream_t s);
