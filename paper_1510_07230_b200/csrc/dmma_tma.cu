@@ -603,14 +603,25 @@ __global__ void __launch_bounds__(TTH, 1) gram_density_kernel(
   }
 }
 
+// G = w sum over splits (one warp per element); blockIdx.y = 1 reduces a second
+// matrix (the dual pass's G_HH: ws2 / G2, symmetric) in the same launch, and
+// diag (optional) receives G's diagonal (sigma_ii for the directions pass)
 __global__ void gram_tma_reduce_kernel(int N, int npad, int sym, int nsplit, double w,
                                        const double* __restrict__ ws, double* __restrict__ G,
-                                       const double* __restrict__ guard) {
+                                       const double* __restrict__ guard,
+                                       const double* __restrict__ ws2, double* __restrict__ G2,
+                                       double* __restrict__ diag) {
   PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (wid >= (int64_t)N * N) return;
+  const bool second = blockIdx.y == 1;
+  if (second) {
+    ws = ws2;
+    G = G2;
+    sym = 1;
+  }
   int i = (int)(wid / N), j = (int)(wid % N);
   if (sym && j < i) {
     const int t = i;
@@ -620,7 +631,10 @@ __global__ void gram_tma_reduce_kernel(int N, int npad, int sym, int nsplit, dou
   double s = 0.0;
   for (int k = lane; k < nsplit; k += 32) s += ws[(int64_t)k * npad * npad + i * npad + j];
   s = warp_sum(s);
-  if (lane == 0) G[wid] = w * s;
+  if (lane == 0) {
+    G[wid] = w * s;
+    if (diag && !second && i == j) diag[i] = w * s;
+  }
 }
 
 int g_nsm = 0;
@@ -636,7 +650,7 @@ int nsm() {
 template <int F>
 bool launch_gram_tma_f(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                        const double* B, const double* Bb, double sb, double* ws, double* G,
-                       double w, cudaStream_t s, const double* guard, double* G2) {
+                       double w, cudaStream_t s, const double* guard, double* G2, double* diag) {
   constexpr int NPAD = 8 * F;
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
@@ -680,13 +694,10 @@ bool launch_gram_tma_f(int N, int64_t ld, int sym, const double* A, const double
                                    guard, probe);
   const int64_t threads = (int64_t)N * N * 32;
   ::po::count_launch();
-  launch_pdl(gram_tma_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, N, NPAD, sym, nsplit, w,
-                                                                           ws, G, guard);
-  if (dual) {
-    ::po::count_launch();
-    launch_pdl(gram_tma_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, 
-        N, NPAD, 1, nsplit, w, ws + (size_t)nsplit * NPAD * NPAD, G2, guard);
-  }
+  launch_pdl(gram_tma_reduce_kernel, dim3((unsigned)((threads + 255) / 256), dual ? 2 : 1), dim3(256), 0, s,
+             N, NPAD, sym, nsplit, w, ws, G, guard,
+             dual ? (const double*)(ws + (size_t)nsplit * NPAD * NPAD) : (const double*)nullptr,
+             dual ? G2 : (double*)nullptr, diag);
   return true;
 }
 
@@ -1143,8 +1154,9 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
                                  rho, vxc, bvec, vext, dpart, sa_dev);
   const int64_t threads = (int64_t)N * N * 32;
   ::po::count_launch();
-  launch_pdl(gram_tma_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, N, NPAD, 1, nblk, w, ws,
-                                                                           G, nullptr);
+  launch_pdl(gram_tma_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, N, NPAD, 1,
+             nblk, w, ws, G, (const double*)nullptr, (const double*)nullptr, (double*)nullptr,
+             (double*)nullptr);
   return nblk;
 }
 
@@ -2459,7 +2471,8 @@ int launch_rotation_split_f(int N, int64_t ld, int64_t ngl, const double* A, con
   const int64_t threads = (int64_t)N * N * 32;
   ::po::count_launch();
   launch_pdl(gram_tma_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, N, NPAD,
-             1, nsplit, w, ws, G, (const double*)nullptr);
+             1, nsplit, w, ws, G, (const double*)nullptr, (const double*)nullptr, (double*)nullptr,
+             (double*)nullptr);
   return nsplit;
 }
 
@@ -2504,11 +2517,11 @@ int launch_directions(int N, int64_t ld, int64_t ngl, const double* W, const dou
 
 bool launch_gram_tma(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                      const double* B, const double* Bb, double sb, double* ws, double* G, double w,
-                     cudaStream_t s, const double* guard, double* G2) {
+                     cudaStream_t s, const double* guard, double* G2, double* diag) {
   switch ((N + 7) / 8) {
 #define PO_GT(F) \
   case F:        \
-    return launch_gram_tma_f<F>(N, ld, sym, A, Ab, sa, B, Bb, sb, ws, G, w, s, guard, G2);
+    return launch_gram_tma_f<F>(N, ld, sym, A, Ab, sa, B, Bb, sb, ws, G, w, s, guard, G2, diag);
     PO_GT(1) PO_GT(2) PO_GT(3) PO_GT(4) PO_GT(5) PO_GT(6)
 #undef PO_GT
   }

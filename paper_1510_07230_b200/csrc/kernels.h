@@ -102,9 +102,11 @@ bool tma2d_available();
 // once per kernel: max-shared carveout + dynamic shared-memory limit (bytes may be 0)
 void set_smem(const void* k, int bytes);
 // G2 != null with sym = 0: the same pass also writes G2 = w A^T A (symmetric).
+// diag (optional): G's diagonal also written there (one launch for the reduction).
 bool launch_gram_tma(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                      const double* B, const double* Bb, double sb, double* ws, double* G, double w,
-                     cudaStream_t s, const double* guard, double* G2 = nullptr);
+                     cudaStream_t s, const double* guard, double* G2 = nullptr,
+                     double* diag = nullptr);
 // Trial Gram of W - tau Z from the iteration's Grams, Z = HW - W diag(sigma):
 //   G0 = G_WW - tau (W^T Z + Z^T W) + tau^2 Z^T Z with W^T Z = Sigma^T - G_WW diag(sigma),
 //   Z^T Z = G_HH - Sigma diag(sigma) - diag(sigma) Sigma^T + diag(sigma) G_WW diag(sigma)

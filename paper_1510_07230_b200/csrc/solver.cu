@@ -335,8 +335,10 @@ struct Solver {
 
   // Sigma and G_HH = w (HW)^T HW in one pass (small N); false if unavailable
   bool sigma_dual(const BRef& w, const BRef& hw) {
+    // sigma_ii comes out of the same reduction launch (no copy_diag) on one rank
     if (!launch_gram_tma(E.N, E.g.ld, 0, P(hw), nullptr, 0.0, P(w), nullptr, 0.0, E.gram_ws,
-                         E.dmat[4], E.g.w, E.s, nullptr, E.dmat[7]))
+                         E.dmat[4], E.g.w, E.s, nullptr, E.dmat[7],
+                         E.size == 1 ? E.dvec + E.off_sig() : nullptr))
       return false;
     if (E.size > 1) {
       E.comm->allreduce_sum(E.dmat[4], (size_t)E.N * E.N, E.s);
@@ -436,7 +438,7 @@ void Solver::enqueue_phase1(int iter) {
       if (need_full || !sig_valid) {
         ghh_fresh = gww_valid && sigma_dual(w, hw);
         if (!ghh_fresh) sigma(w, hw);
-        launch_copy_diag(n, E.dmat[4], E.dvec + E.off_sig(), E.s);
+        if (!ghh_fresh || E.size > 1) launch_copy_diag(n, E.dmat[4], E.dvec + E.off_sig(), E.s);
       }
       const int nb = launch_directions(
           n, E.g.ld, E.g.ngl, P(w), P(hw), history_valid ? P(prev_w) : nullptr,
