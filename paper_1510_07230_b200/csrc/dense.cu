@@ -327,11 +327,26 @@ __global__ void __launch_bounds__(32) cholesky_inv_reg_kernel(int N, const doubl
 // both goes through shared memory (double-buffered), so a step is one
 // barrier and independent FMAs. Pivot failure (d_j <= 0 or NaN) is the LLT
 // failure; the stats follow manifold.cpp:106-112.
-template <int TR, int A, int B>
+// TrialArgs: form the line-search trial's Gram G0 of W - tau Z from the
+// iteration's Grams in the slots themselves (launch_trial_gram's formula),
+// store it (both triangles, exactly symmetric) and its matrix statistics
+// (launch_matrix_stats) — one launch instead of three.
+struct TrialArgs {
+  const double* gww;
+  const double* S;
+  const double* ghh;
+  double tau;
+  const double* tau_dev;
+  double* G0;
+  double* mstats;
+};
+
+template <int TR, int A, int B, bool TRIAL = false>
 __global__ void __launch_bounds__(TR * 32) cholesky_inv_gs_kernel(int N, const double* __restrict__ G,
                                                                  double* __restrict__ M,
                                                                  double* __restrict__ stats,
-                                                                 const double* __restrict__ guard) {
+                                                                 const double* __restrict__ guard,
+                                                                 TrialArgs ta) {
   PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   constexpr int NMAX = TR * A;
@@ -341,12 +356,35 @@ __global__ void __launch_bounds__(TR * 32) cholesky_inv_gs_kernel(int N, const d
   __shared__ double col[2][NMAX], piv[2][2], dj[NMAX];
   const int tc = threadIdx.x & 31, tr = threadIdx.x >> 5;
   double x[A][B];
+  double st4[4] = {0.0, 0.0, 0.0, 0.0};  // TRIAL: dev, asym (0), offdiag max, diag deviation max
+  const double tau = TRIAL && ta.tau_dev ? *ta.tau_dev : ta.tau;
 #pragma unroll
   for (int a = 0; a < A; ++a)
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const int p = tr + TR * a, q = tc + 32 * b;
-      x[a][b] = (p < N && q < N && p >= q) ? G[p * N + q] : 0.0;
+      if constexpr (TRIAL) {
+        double v = 0.0;
+        if (p < N && q < N && p >= q) {
+          // trial_gram_kernel with (i, j) = (q, p), i <= j
+          const int i = q, j = p;
+          const double si = ta.S[i * N + i], sj = ta.S[j * N + j];
+          const double sij = ta.S[i * N + j], sji = ta.S[j * N + i];
+          const double g = ta.gww[i * N + j];
+          const double wz = (sji - sj * g) + (sij - si * g);
+          const double zz = ((ta.ghh[i * N + j] - sj * sij) - si * sji) + (si * sj) * g;
+          v = (g - tau * wz) + (tau * tau) * zz;
+          ta.G0[i * N + j] = v;
+          ta.G0[j * N + i] = v;
+          const double d = fabs(v - (i == j ? 1.0 : 0.0));
+          st4[0] = (d > st4[0] || isnan(d)) ? d : st4[0];
+          if (i == j) st4[3] = fmax(st4[3], d);
+          else st4[2] = fmax(st4[2], d);
+        }
+        x[a][b] = v;
+      } else {
+        x[a][b] = (p < N && q < N && p >= q) ? G[p * N + q] : 0.0;
+      }
       if (q == 0 && p < N) {
         col[0][p] = p == 0 ? 1.0 : x[a][b];
         if (p == 0) {
@@ -355,6 +393,24 @@ __global__ void __launch_bounds__(TR * 32) cholesky_inv_gs_kernel(int N, const d
         }
       }
     }
+  if constexpr (TRIAL) {  // block max of the trial Gram's statistics (NaN wins, as matrix_stats)
+    __shared__ double sred[4][32];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double v = st4[q];
+      for (int o = 16; o > 0; o >>= 1) {
+        const double y = __shfl_xor_sync(0xffffffffu, v, o);
+        v = (y > v || isnan(y)) ? y : v;
+      }
+      if (tc == 0) sred[q][tr] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+      double m = 0.0;
+      for (int k = 0; k < TR; ++k) m = (sred[threadIdx.x][k] > m || isnan(sred[threadIdx.x][k])) ? sred[threadIdx.x][k] : m;
+      ta.mstats[threadIdx.x] = m;
+    }
+  }
   __syncthreads();
   bool fail = false;
   for (int j = 0; j < N; ++j) {
@@ -747,11 +803,11 @@ void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, do
   static const int variant = getenv("PO_CHOL") ? atoi(getenv("PO_CHOL")) : 0;  // measurement
   if (variant == 0 && N <= 128) {  // one barrier per column, registers only
     if (N <= 32)
-      launch_pdl(cholesky_inv_gs_kernel<32, 1, 1>, dim3(1), dim3(1024), 0, s, N, G, M, stats, guard);
+      launch_pdl(cholesky_inv_gs_kernel<32, 1, 1>, dim3(1), dim3(1024), 0, s, N, G, M, stats, guard, TrialArgs{});
     else if (N <= 64)
-      launch_pdl(cholesky_inv_gs_kernel<16, 4, 2>, dim3(1), dim3(512), 0, s, N, G, M, stats, guard);
+      launch_pdl(cholesky_inv_gs_kernel<16, 4, 2>, dim3(1), dim3(512), 0, s, N, G, M, stats, guard, TrialArgs{});
     else
-      launch_pdl(cholesky_inv_gs_kernel<32, 4, 4>, dim3(1), dim3(1024), 0, s, N, G, M, stats, guard);
+      launch_pdl(cholesky_inv_gs_kernel<32, 4, 4>, dim3(1), dim3(1024), 0, s, N, G, M, stats, guard, TrialArgs{});
     return;
   }
   // measured (tools/kbench-style, one launch): register kernel 6 / 12 / 29 us at
@@ -789,6 +845,26 @@ void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, do
     return;
   }
   cholesky_inv_kernel<<<1, DT, 0, s>>>(N, G, Lscratch, M, stats, guard);
+}
+
+bool launch_trial_cholesky(int N, const double* gww, const double* sigma, const double* ghh,
+                           double tau, const double* tau_dev, double* G0, double* mstats, double* M,
+                           double* stats, cudaStream_t s) {
+  static const int variant = getenv("PO_CHOL") ? atoi(getenv("PO_CHOL")) : 0;
+  static const int off = getenv("PO_NO_TRIAL_CHOL") ? atoi(getenv("PO_NO_TRIAL_CHOL")) : 0;  // measurement
+  if (variant != 0 || off || N > 128) return false;
+  const TrialArgs ta{gww, sigma, ghh, tau, tau_dev, G0, mstats};
+  ::po::count_launch();
+  if (N <= 32)
+    launch_pdl(cholesky_inv_gs_kernel<32, 1, 1, true>, dim3(1), dim3(1024), 0, s, N, (const double*)nullptr, M,
+               stats, (const double*)nullptr, ta);
+  else if (N <= 64)
+    launch_pdl(cholesky_inv_gs_kernel<16, 4, 2, true>, dim3(1), dim3(512), 0, s, N, (const double*)nullptr, M,
+               stats, (const double*)nullptr, ta);
+  else
+    launch_pdl(cholesky_inv_gs_kernel<32, 4, 4, true>, dim3(1), dim3(1024), 0, s, N, (const double*)nullptr, M,
+               stats, (const double*)nullptr, ta);
+  return true;
 }
 
 void launch_syev(int N, const double* A, double* work, double* evals, double* evecs,

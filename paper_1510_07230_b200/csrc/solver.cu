@@ -168,12 +168,18 @@ bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, doubl
                   bool g0_from_grams = false, const double* tau_dev = nullptr) {
   (void)measure;
   double* sc = E.scal();
-  if (g0_from_grams)  // G0 of W - tau Z from G_WW (dmat[8]), Sigma (dmat[4]), G_HH (dmat[7])
-    launch_trial_gram(E.N, E.dmat[8], E.dmat[4], E.dmat[7], -sa, E.dmat[0], E.s, tau_dev);
-  else
-    E.gram(A, Ab, sa, A, Ab, sa, 1, E.dmat[0]);
-  launch_matrix_stats(E.N, E.dmat[0], sc + Engine::S_MSTAT, E.s);
-  launch_cholesky_inv(E.N, E.dmat[0], E.chol_L, E.dmat[1], sc + Engine::S_CHOL, E.s);
+  // G0 of W - tau Z from G_WW (dmat[8]), Sigma (dmat[4]), G_HH (dmat[7]), its stats and
+  // its Cholesky in one launch where possible
+  if (!(g0_from_grams &&
+        launch_trial_cholesky(E.N, E.dmat[8], E.dmat[4], E.dmat[7], -sa, tau_dev, E.dmat[0],
+                              sc + Engine::S_MSTAT, E.dmat[1], sc + Engine::S_CHOL, E.s))) {
+    if (g0_from_grams)
+      launch_trial_gram(E.N, E.dmat[8], E.dmat[4], E.dmat[7], -sa, E.dmat[0], E.s, tau_dev);
+    else
+      E.gram(A, Ab, sa, A, Ab, sa, 1, E.dmat[0]);
+    launch_matrix_stats(E.N, E.dmat[0], sc + Engine::S_MSTAT, E.s);
+    launch_cholesky_inv(E.N, E.dmat[0], E.chol_L, E.dmat[1], sc + Engine::S_CHOL, E.s);
+  }
   bool fused = false;
   if (st && E.N <= 48 && tma2d_available()) {
     // rotation + verification Gram + density/xc of the rotated block in one pass
