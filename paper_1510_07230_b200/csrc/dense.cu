@@ -331,6 +331,35 @@ __global__ void __launch_bounds__(32) cholesky_inv_reg_kernel(int N, const doubl
 // iteration's Grams in the slots themselves (launch_trial_gram's formula),
 // store it (both triangles, exactly symmetric) and its matrix statistics
 // (launch_matrix_stats) — one launch instead of three.
+// the host mirror's loops (optimizer.cpp:376-411) in the same order: bitwise-equal tau
+__device__ __forceinline__ void bb_tau_compute(int N, const double* __restrict__ zz,
+                                               const double* __restrict__ ss,
+                                               const double* __restrict__ sy,
+                                               const double* __restrict__ yy, int history,
+                                               int use_bb1, int trace_abs_diag, double tau_min,
+                                               double tau_max, double* __restrict__ out) {
+  double znorm2 = 0.0;
+  for (int i = 0; i < N; ++i) znorm2 += zz[i];
+  double raw;
+  if (history) {
+    double tr_ss = 0.0, tr_yy = 0.0, sy_abs = 0.0, sy_tr = 0.0;
+    for (int i = 0; i < N; ++i) {
+      tr_ss += ss[i];
+      tr_yy += yy[i];
+      sy_abs += fabs(sy[i]);
+      sy_tr += sy[i];
+    }
+    const double tr_abs_sy = trace_abs_diag ? sy_abs : fabs(sy_tr);
+    raw = use_bb1 ? tr_ss / tr_abs_sy : tr_abs_sy / tr_yy;
+  } else {
+    raw = fmin(tau_max, 1.0 / sqrt(znorm2));
+  }
+  const double tau = isfinite(raw) ? fmin(fmax(raw, tau_min), tau_max) : tau_max;
+  out[0] = tau;
+  out[1] = -tau;
+  out[2] = znorm2;
+}
+
 struct TrialArgs {
   const double* gww;
   const double* S;
@@ -339,6 +368,8 @@ struct TrialArgs {
   const double* tau_dev;
   double* G0;
   double* mstats;
+  int has_bb;  // take the BB step first (bb_tau_kernel's computation), tau from there
+  BBArgs bb;
 };
 
 template <int TR, int A, int B, bool TRIAL = false>
@@ -357,7 +388,22 @@ __global__ void __launch_bounds__(TR * 32) cholesky_inv_gs_kernel(int N, const d
   const int tc = threadIdx.x & 31, tr = threadIdx.x >> 5;
   double x[A][B];
   double st4[4] = {0.0, 0.0, 0.0, 0.0};  // TRIAL: dev, asym (0), offdiag max, diag deviation max
-  const double tau = TRIAL && ta.tau_dev ? *ta.tau_dev : ta.tau;
+  double tau = ta.tau;
+  if constexpr (TRIAL) {
+    __shared__ double tau_s;
+    if (ta.has_bb) {  // the BB step of this iteration (one thread, the host mirror's order)
+      if (threadIdx.x == 0) {
+        const BBArgs& q = ta.bb;
+        bb_tau_compute(q.N, q.zz, q.ss, q.sy, q.yy, q.history, q.use_bb1, q.trace_abs_diag, q.tau_min,
+                       q.tau_max, q.out);
+        tau_s = q.out[0];
+      }
+      __syncthreads();
+      tau = tau_s;
+    } else if (ta.tau_dev) {
+      tau = *ta.tau_dev;
+    }
+  }
 #pragma unroll
   for (int a = 0; a < A; ++a)
 #pragma unroll
@@ -743,26 +789,7 @@ __global__ void bb_tau_kernel(int N, const double* __restrict__ zz, const double
                               double tau_max, double* __restrict__ out) {
   PO_PDL_ENTRY();
   if (threadIdx.x != 0) return;
-  double znorm2 = 0.0;
-  for (int i = 0; i < N; ++i) znorm2 += zz[i];
-  double raw;
-  if (history) {
-    double tr_ss = 0.0, tr_yy = 0.0, sy_abs = 0.0, sy_tr = 0.0;
-    for (int i = 0; i < N; ++i) {
-      tr_ss += ss[i];
-      tr_yy += yy[i];
-      sy_abs += fabs(sy[i]);
-      sy_tr += sy[i];
-    }
-    const double tr_abs_sy = trace_abs_diag ? sy_abs : fabs(sy_tr);
-    raw = use_bb1 ? tr_ss / tr_abs_sy : tr_abs_sy / tr_yy;
-  } else {
-    raw = fmin(tau_max, 1.0 / sqrt(znorm2));
-  }
-  const double tau = isfinite(raw) ? fmin(fmax(raw, tau_min), tau_max) : tau_max;
-  out[0] = tau;
-  out[1] = -tau;
-  out[2] = znorm2;
+  bb_tau_compute(N, zz, ss, sy, yy, history, use_bb1, trace_abs_diag, tau_min, tau_max, out);
 }
 
 }  // namespace
@@ -849,11 +876,15 @@ void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, do
 
 bool launch_trial_cholesky(int N, const double* gww, const double* sigma, const double* ghh,
                            double tau, const double* tau_dev, double* G0, double* mstats, double* M,
-                           double* stats, cudaStream_t s) {
+                           double* stats, cudaStream_t s, const BBArgs* bb) {
   static const int variant = getenv("PO_CHOL") ? atoi(getenv("PO_CHOL")) : 0;
   static const int off = getenv("PO_NO_TRIAL_CHOL") ? atoi(getenv("PO_NO_TRIAL_CHOL")) : 0;  // measurement
   if (variant != 0 || off || N > 128) return false;
-  const TrialArgs ta{gww, sigma, ghh, tau, tau_dev, G0, mstats};
+  TrialArgs ta{gww, sigma, ghh, tau, tau_dev, G0, mstats, 0, BBArgs{}};
+  if (bb) {
+    ta.has_bb = 1;
+    ta.bb = *bb;
+  }
   ::po::count_launch();
   if (N <= 32)
     launch_pdl(cholesky_inv_gs_kernel<32, 1, 1, true>, dim3(1), dim3(1024), 0, s, N, (const double*)nullptr, M,

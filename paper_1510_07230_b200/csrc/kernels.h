@@ -168,12 +168,21 @@ void launch_mix_batched(int N, int64_t ld, int64_t ngl, int batch, int64_t bstri
 // following manifold.cpp:97-114. stats: {pmin, pmax, cond, ok}.
 void launch_cholesky_inv(int N, const double* G, double* Lscratch, double* M, double* stats,
                          cudaStream_t s, const double* guard = nullptr);
-// trial_gram + matrix_stats(G0) + Cholesky / L^{-T} of G0 in one launch (N <= 128):
+// Arguments of the device-side BB step (launch_bb_tau), for fusing it into a later kernel.
+struct BBArgs {
+  int N;
+  const double *zz, *ss, *sy, *yy;
+  int history, use_bb1, trace_abs_diag;
+  double tau_min, tau_max;
+  double* out;
+};
+// trial_gram + matrix_stats(G0) + Cholesky / L^{-T} of G0 in one launch (N <= 128); with bb
+// the BB step runs first in the same kernel and tau comes from it (out[0]):
 // G0 of W - tau Z from G_WW, Sigma, G_HH (tau from tau_dev when non-null) into G0,
 // its statistics into mstats, then as launch_cholesky_inv. false when unavailable.
 bool launch_trial_cholesky(int N, const double* gww, const double* sigma, const double* ghh,
                            double tau, const double* tau_dev, double* G0, double* mstats, double* M,
-                           double* stats, cudaStream_t s);
+                           double* stats, cudaStream_t s, const BBArgs* bb = nullptr);
 // Device-side decisions of manifold.cpp:147-167 without a host round trip:
 // out[0] = 1 if the repair pass runs ((measure || cond > 100) && dev > 1e-12),
 // from the pass-1 Cholesky stats and the verification-Gram stats.

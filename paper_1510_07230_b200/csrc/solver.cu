@@ -165,14 +165,18 @@ bool orthonormalize_dev(Engine& E, const double* A, const double* Ab, double sa,
 // fallback (orthonormalize_dev).
 bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, double* out,
                   bool measure, DevState* st = nullptr, int hartree = 0, int xc = 0,
-                  bool g0_from_grams = false, const double* tau_dev = nullptr) {
+                  bool g0_from_grams = false, const double* tau_dev = nullptr,
+                  const BBArgs* bb = nullptr) {
   (void)measure;
   double* sc = E.scal();
   // G0 of W - tau Z from G_WW (dmat[8]), Sigma (dmat[4]), G_HH (dmat[7]), its stats and
   // its Cholesky in one launch where possible
   if (!(g0_from_grams &&
         launch_trial_cholesky(E.N, E.dmat[8], E.dmat[4], E.dmat[7], -sa, tau_dev, E.dmat[0],
-                              sc + Engine::S_MSTAT, E.dmat[1], sc + Engine::S_CHOL, E.s))) {
+                              sc + Engine::S_MSTAT, E.dmat[1], sc + Engine::S_CHOL, E.s, bb))) {
+    if (bb)  // the BB step as its own launch (the fused form is unavailable)
+      launch_bb_tau(bb->N, bb->zz, bb->ss, bb->sy, bb->yy, bb->history, bb->use_bb1,
+                    bb->trace_abs_diag, bb->tau_min, bb->tau_max, bb->out, E.s);
     if (g0_from_grams)
       launch_trial_gram(E.N, E.dmat[8], E.dmat[4], E.dmat[7], -sa, E.dmat[0], E.s, tau_dev);
     else
@@ -518,16 +522,17 @@ void Solver::enqueue_phase1(int iter) {
     if (orth_iter && fused && gww_valid && ghh_fresh && nonlinear && E.N <= 48 &&
         tma2d_available()) {
       double* st_tau = E.scal() + Engine::S_TAU;
-      launch_bb_tau(n, E.dvec + E.off_zz(), E.dvec + E.off_ss(), E.dvec + E.off_sy(),
-                    E.dvec + E.off_yy(), history_valid ? 1 : 0, use_bb1(p.bb_variant, iter) ? 1 : 0,
-                    p.bb_trace_abs == PO_TRACE_DIAG_ABS ? 1 : 0, p.tau_min, p.tau_max, st_tau,
-                    E.s);
+      // the BB step runs inside the trial's Cholesky launch (orth_enqueue)
+      const BBArgs bb{n, E.dvec + E.off_zz(), E.dvec + E.off_ss(), E.dvec + E.off_sy(),
+                      E.dvec + E.off_yy(), history_valid ? 1 : 0,
+                      use_bb1(p.bb_variant, iter) ? 1 : 0,
+                      p.bb_trace_abs == PO_TRACE_DIAG_ABS ? 1 : 0, p.tau_min, p.tau_max, st_tau};
       spec.wt = pool.get();
       spec.rep = pool.get();
       spec.pre = spool.get();
       const bool dens = orth_enqueue(E, P(w), P(z), 0.0, P(spec.wt),
                                      p.verify_orthonormality != 0, spec.pre.get(), p.hartree,
-                                     p.xc, true, st_tau);
+                                     p.xc, true, st_tau, &bb);
       spec.tstate = enqueue_state(spec.wt, spec.pre, dens);
       spec.hwt = pool.get();
       E.apply_h(P(spec.wt), P(spec.hwt), spec.tstate->v_local, false);
