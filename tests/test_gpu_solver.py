@@ -169,3 +169,35 @@ print(json.dumps([x["energy"] for x in r.records] + [r.energy["total"]]))
     a, b = outs
     assert len(a) == len(b)
     assert max(abs(x - y) for x, y in zip(a, b)) < 1e-10
+
+
+def test_launch_and_path_switches_agree(tmp_path):
+    """Measurement switches keep the numerics: plain launches instead of
+    programmatic dependent launch (PO_PDL=0) give bitwise the same trajectory;
+    the split trial rotation (PO_ROT_SPLIT=1: two-source mix + Gram/density
+    pass) and the 8-warp directions pass (PO_DIR_CW=8) agree to round-off."""
+    import json
+    import subprocess
+    import sys
+    code = r'''
+import json, sys
+sys.path.insert(0, %r)
+from paper_1510_07230_b200 import configs, native
+spec = configs.small_molecule(14, 9, L=8.0)
+e = native.engine_for(spec)
+w = native.random_orthonormal(e, 42)
+r = e.solve(w, "opt_par_mod", True, True, max_inner=8, n_org=1, n_diag=100)
+print(json.dumps([x["energy"] for x in r.records] + [r.energy["total"]]))
+''' % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),)
+    runs = {}
+    for name, env_over in [("base", {}), ("nopdl", {"PO_PDL": "0"}), ("split", {"PO_ROT_SPLIT": "1"}),
+                           ("dir8", {"PO_DIR_CW": "8"})]:
+        env = {k: v for k, v in os.environ.items() if not k.startswith("PO_")}
+        env.update(env_over)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+        assert r.returncode == 0, (name, r.stderr[-2000:])
+        runs[name] = json.loads(r.stdout.strip().split("\n")[-1])
+    assert runs["nopdl"] == runs["base"]
+    for name in ("split", "dir8"):
+        assert len(runs[name]) == len(runs["base"])
+        assert max(abs(x - y) for x, y in zip(runs[name], runs["base"])) < 1e-9, name
