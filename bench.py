@@ -332,6 +332,46 @@ def ours(args, spec):
     h_ms = time_kernel(torch, native, e, "hamiltonian", 20, a=cur, out=scratch)
     h_bytes = 16.0 * N * e.ngl + 8.0 * e.ngl  # read u + write Hu per orbital.point, + v_local
     g_ms = time_kernel(torch, native, e, "gram_sym", 20, a=cur)
+    # the step's other dominant kernels, same clock (measurement ops through po_enqueue)
+    fp64 = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            fp64 = float(json.load(f)["fp64_tflops"])
+    except Exception:
+        pass
+    step_kernels = []
+
+    def add_kernel(name, ms, nbytes, flops=None):
+        ent = {"kernel": name, "launch_ms": ms, "algorithmic_bytes": nbytes,
+               "hbm_frac": nbytes / (ms / 1e3) / 1e9 / hbm}
+        if flops is not None and fp64:
+            ent["algorithmic_flops"] = flops
+            ent["fp64_frac"] = flops / (ms / 1e3) / 1e12 / fp64
+        step_kernels.append(ent)
+
+    blk = float(N) * e.ngl * 8
+    add_kernel("hamiltonian4_kernel (H u)", h_ms, h_bytes)
+    hw_b, z_b = e.alloc(), e.alloc()
+    e.enqueue("hamiltonian", a=cur, out=hw_b)
+    sg_ms = time_kernel(torch, native, e, "gram", 10, a=hw_b, b=cur)  # Sigma = w (HW)^T W
+    add_kernel("Sigma Gram (HW)^T W", sg_ms, 2 * blk, 2.0 * N * N * ng)
+    add_kernel("symmetric Gram W^T W", g_ms, blk, float(N) * (N + 1) * ng)
+    if N <= 48:  # the small-N fused passes of the C2 step
+        e.enqueue("gram", a=hw_b, b=cur)
+        d_ms = time_kernel(torch, native, e, "directions", 10, a=cur, b=hw_b, out=z_b)
+        add_kernel("directions_tma_kernel (z, ||D||^2, BB)", d_ms, 5 * blk, 2.0 * N * N * ng)
+        e.enqueue("gram_sym", a=cur)
+        e.enqueue("cholesky")
+        r_ms = time_kernel(torch, native, e, "rotation_fused", 10, a=cur, b=z_b, out=scratch)
+        add_kernel("rotate_fused_kernel (rotation + G2 + density)", r_ms, 3 * blk,
+                   2.0 * N * (N + 1) * ng)
+    else:
+        e.enqueue("gram_sym", a=cur)
+        e.enqueue("cholesky")
+        r_ms = time_kernel(torch, native, e, "rotation", 10, a=cur, b=hw_b, out=scratch)
+        add_kernel("triangular rotation (W - tau Z) L^-T", r_ms, 3 * blk, float(N) * (N + 1) * ng)
+    e.free(hw_b)
+    e.free(z_b)
     e.enqueue("density_xc", a=cur)
     e.set_poisson_solver(args.poisson)
     p_ms = time_kernel(torch, native, e, "poisson", 5)
@@ -364,6 +404,7 @@ def ours(args, spec):
                              "max": max(step_wall)} if step_wall else None,
             "kernel_ms": {"hamiltonian": h_ms, "gram_sym": g_ms, "poisson_cg_solve": p_ms},
             "roofline": roofline,
+            "step_kernels": step_kernels,
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": block_bytes / e2e_iters,
                     "d2h_bytes_per_step": block_bytes / e2e_iters + 2 * (9 * N + 64) * 8,
