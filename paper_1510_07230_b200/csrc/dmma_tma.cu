@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(TTH, 1) gram_density_kernel(
       const int s = st % nst;
       const int64_t p0 = kbeg + (int64_t)st * TKS + c + 2 * t4;  // this lane's two points
       double vx[2] = {0.0, 0.0};
-      if (vext && gq == 0) {  // requested before the stage wait (latency under the TMA)
+      if (vext && xc >= 0 && gq == 0) {  // requested before the stage wait (latency under the TMA)
         if (p0 < ngl) vx[0] = __ldg(vext + p0);
         if (p0 + 1 < ngl) vx[1] = __ldg(vext + p0 + 1);
       }
@@ -555,15 +555,15 @@ __global__ void __launch_bounds__(TTH, 1) gram_density_kernel(
           const double dv = e ? d1 : d0;
           const double r = occ == 1.0 ? dv : dv * occ;
           rho[p] = r;
-          if (xc) {
+          if (xc > 0) {
             const double eps = -cx * cbrt(r);
             vxc[p] = eps * (4.0 / 3.0);
             eacc[0] += eps * r;
-          } else {
+          } else if (xc == 0) {
             vxc[p] = 0.0;
-          }
+          }  // xc < 0: v_xc and the energies come from the v_local pass
           if (bvec) bvec[p] = r * four_pi;
-          eacc[1] += vx[e] * r;
+          if (xc >= 0) eacc[1] += vx[e] * r;
         }
       }
     }
