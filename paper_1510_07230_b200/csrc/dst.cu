@@ -283,6 +283,118 @@ void launch_axis0_pick(const DstPoisson& d, const double* x, double* y, cudaStre
   }
 }
 
+
+// Column-split form of the per-plane transforms for n1 == n2 <= 96: the plane's
+// work (four n^3 DMMA GEMMs on one CTA per plane = 96 of 148 SMs at 96^3) runs
+// as two launches of (32-column part, plane) CTAs, two per SM (S from L1):
+//   out[:, cols] = [scale .] S1 (in S2[:, cols])
+// first on the axis-0-transformed plane (t0 -> t1, with the spectral scale),
+// then on the scaled plane (t1 -> t0). Each part needs the whole input plane
+// but only its own columns of the intermediate, so no CTA waits on another.
+constexpr int PP = 32;  // columns per part
+template <int NF>
+__global__ void __launch_bounds__(256, 2) dst_plane_part_kernel(const double* __restrict__ in,
+                                                               double* __restrict__ out, int n,
+                                                               const double* __restrict__ S1,
+                                                               const double* __restrict__ S2,
+                                                               const double* __restrict__ scale) {
+  PO_PDL_ENTRY();
+  constexpr int RB = NF / 4, CB = 2;  // 8 warps: 4 row groups x 2 column groups
+  extern __shared__ double dsm[];
+  const int n8 = 8 * NF, ps = n8 + 4, qs = PP + 4;
+  double* X = dsm;              // [n8][ps]: the input plane
+  double* P = dsm + n8 * ps;    // [n8][qs]: in S2[:, cols]
+  const int c0 = blockIdx.x * PP, k0 = blockIdx.y;
+  const double* ip = in + (int64_t)k0 * n * n;
+  for (int e = threadIdx.x; e < n8 * ps; e += blockDim.x) {
+    const int r = e / ps, c = e % ps;
+    X[e] = (r < n && c < n) ? ip[r * n + c] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, gq = lane >> 2, t4 = lane & 3;
+  const int warp = threadIdx.x >> 5, wr = warp >> 1, wc = warp & 1;
+  const int nks = (n + 3) / 4;
+  double acc[RB][CB][2];
+  // P = X S2[:, c0 + ...]
+#pragma unroll
+  for (int a = 0; a < RB; ++a)
+#pragma unroll
+    for (int b = 0; b < CB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int ks = 0; ks < nks; ++ks) {
+    const int k = 4 * ks + t4;
+    double af[RB], bf[CB];
+#pragma unroll
+    for (int a = 0; a < RB; ++a) af[a] = X[(8 * (wr * RB + a) + gq) * ps + k];
+#pragma unroll
+    for (int b = 0; b < CB; ++b) {
+      const int col = c0 + 8 * (wc * CB + b) + gq;
+      bf[b] = (k < n && col < n) ? __ldg(S2 + k * n + col) : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < RB; ++a)
+#pragma unroll
+      for (int b = 0; b < CB; ++b) dmma_8x8x4(acc[a][b], af[a], bf[b]);
+  }
+#pragma unroll
+  for (int a = 0; a < RB; ++a)
+#pragma unroll
+    for (int b = 0; b < CB; ++b)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        P[(8 * (wr * RB + a) + gq) * qs + 8 * (wc * CB + b) + 2 * t4 + j] = acc[a][b][j];
+  __syncthreads();
+  // out[:, cols] = S1 P
+#pragma unroll
+  for (int a = 0; a < RB; ++a)
+#pragma unroll
+    for (int b = 0; b < CB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int ks = 0; ks < nks; ++ks) {
+    const int k = 4 * ks + t4;
+    double af[RB], bf[CB];
+#pragma unroll
+    for (int a = 0; a < RB; ++a) {
+      const int row = 8 * (wr * RB + a) + gq;
+      af[a] = (row < n && k < n) ? __ldg(S1 + row * n + k) : 0.0;
+    }
+#pragma unroll
+    for (int b = 0; b < CB; ++b) bf[b] = P[k * qs + 8 * (wc * CB + b) + gq];
+#pragma unroll
+    for (int a = 0; a < RB; ++a)
+#pragma unroll
+      for (int b = 0; b < CB; ++b) dmma_8x8x4(acc[a][b], af[a], bf[b]);
+  }
+  double* op = out + (int64_t)k0 * n * n;
+  const double* sp = scale ? scale + (int64_t)k0 * n * n : nullptr;
+#pragma unroll
+  for (int a = 0; a < RB; ++a)
+#pragma unroll
+    for (int b = 0; b < CB; ++b)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int r = 8 * (wr * RB + a) + gq, c = c0 + 8 * (wc * CB + b) + 2 * t4 + j;
+        if (r < n && c < n) {
+          double v = acc[a][b][j];
+          if (sp) v *= __ldg(sp + r * n + c);
+          op[r * n + c] = v;
+        }
+      }
+}
+
+template <int NF>
+void launch_plane_parts(const DstPoisson& d, cudaStream_t s) {
+  const int n = (int)d.n1, n8 = 8 * NF;
+  const size_t sh = sizeof(double) * ((size_t)n8 * (n8 + 4) + (size_t)n8 * (PP + 4));
+  auto k = dst_plane_part_kernel<NF>;
+  set_smem(reinterpret_cast<const void*>(k), (int)sh);
+  const dim3 grid((unsigned)((n + PP - 1) / PP), (unsigned)d.n0);
+  ::po::count_launch();
+  launch_pdl(k, grid, dim3(256), sh, s, (const double*)d.t0, d.t1, n, (const double*)d.S[1],
+             (const double*)d.S[2], (const double*)d.scale);
+  ::po::count_launch();
+  launch_pdl(k, grid, dim3(256), sh, s, (const double*)d.t1, d.t0, n, (const double*)d.S[1],
+             (const double*)d.S[2], (const double*)nullptr);
+}
+
 template <int NF>
 void launch_fused(const DstPoisson& d, const double* b, double* x, cudaStream_t s) {
   const int n8 = 8 * (int)((std::max(d.n1, d.n2) + 7) / 8);
@@ -292,9 +404,14 @@ void launch_fused(const DstPoisson& d, const double* b, double* x, cudaStream_t 
   auto kp = p_sg ? dst_plane_kernel<NF, true> : dst_plane_kernel<NF, false>;
   set_smem(reinterpret_cast<const void*>(kp), (int)sh1);
   launch_axis0_pick<NF>(d, b, d.t0, s);
-  ::po::count_launch();
-  launch_pdl(kp, dim3((unsigned)d.n0), dim3(PW * 32), sh1, s, d.t0, (int)d.n0, (int)d.n1, (int)d.n2, d.S[1], d.S[2],
-                                          d.scale);
+  static const int parts_env = getenv("PO_DST_PARTS") ? atoi(getenv("PO_DST_PARTS")) : 1;  // measurement
+  if (parts_env && NF <= 12 && d.n1 == d.n2 && d.n1 > 8 * (NF - 4)) {
+    launch_plane_parts<NF>(d, s);
+  } else {
+    ::po::count_launch();
+    launch_pdl(kp, dim3((unsigned)d.n0), dim3(PW * 32), sh1, s, d.t0, (int)d.n0, (int)d.n1, (int)d.n2, d.S[1],
+               d.S[2], d.scale);
+  }
   launch_axis0_pick<NF>(d, d.t0, x, s);
 }
 
