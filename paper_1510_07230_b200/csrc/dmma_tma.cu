@@ -669,7 +669,8 @@ bool launch_gram_tma_f(int N, int64_t ld, int sym, const double* A, const double
     }
   }
   const bool dual = G2 != nullptr && !sym;
-  const int R = dual && F > 1 && (N % 8 == 1 || N % 8 == 2) ? N % 8 : 0;
+  static const int no_rem = getenv("PO_NO_REM") ? atoi(getenv("PO_NO_REM")) : 0;  // measurement
+  const int R = !no_rem && dual && F > 1 && (N % 8 == 1 || N % 8 == 2) ? N % 8 : 0;
   const int fd = R ? F - 1 : F;
   const int np = (sym ? fd * (fd + 1) / 2 : fd * fd) + (dual ? fd * (fd + 1) / 2 : 0);
   const size_t red = (size_t)TSC * np * 64 + (size_t)TSC * 12 * 32;
