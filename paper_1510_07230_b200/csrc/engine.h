@@ -52,6 +52,9 @@ struct DevState {
   double e_hartree = 0.0, e_xc = 0.0;
   double e_ext = 0.0;  // w <V_ext, rho> (= sum_i f <V_ext u_i, u_i>)
   int cg_iters = 0;
+  // DST solve whose CG-criterion check (||b - A x|| <= 1e-10 ||b||, energy.cpp:120-142)
+  // rode on the v_local pass; poisson_ok is known after the readback (state_results)
+  bool poisson_deferred = false, poisson_ok = true;
 };
 
 struct EnergyParts {  // EnergyBreakdown, energy.hpp:52-58
@@ -176,6 +179,7 @@ class Engine {
          S_TAU = 40 /* [0] tau_raw, [1] -tau_raw (trial scale), [2] znorm2 */ };
   double* scal() { return dvec + off_scal(); }
   // copy n doubles of dvec starting at off into hvec (same offsets) and synchronise
+  bool force_cg_verify = false;  // build_state: run the CG verification kernel (no deferral)
   void fetch(size_t off, size_t n);
   void fetch_all() { fetch(0, dvec_len()); }
   void sync();

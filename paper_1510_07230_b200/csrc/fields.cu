@@ -75,17 +75,26 @@ __global__ void __launch_bounds__(PT) density_xc_kernel(SlabGeom g, int N,
 // the partials carry [<v_H, rho> | <eps, rho> | <V_ext, rho>] — the trial
 // rotation then only writes rho (its cube roots ran on 4 of 32 lanes there);
 // xc_here < 0: v_xc was written by the density pass, partials [<v_H, rho>].
+// bfull / xfull (non-null, full grid): the Poisson check rides along — sums of
+// r^2 and b^2 with r = b - (-lap_h x) at the slab's points, partial rows 3 and 4
+// (and the CG status words cg_out = {0, 0}: no CG kernel ran).
 __global__ void __launch_bounds__(PT) vlocal_kernel(SlabGeom g, const double* __restrict__ vext,
                                                     const double* __restrict__ vh_src,
                                                     double* __restrict__ vh,
                                                     double* __restrict__ vxc,
                                                     const double* __restrict__ rho,
                                                     double* __restrict__ vloc,
-                                                    double* __restrict__ partials, int xc_here) {
+                                                    double* __restrict__ partials, int xc_here,
+                                                    const double* __restrict__ bfull,
+                                                    const double* __restrict__ xfull,
+                                                    int* __restrict__ cg_out) {
   PO_PDL_ENTRY();
-  __shared__ double red[3 * 32];
-  double acc[3] = {0.0, 0.0, 0.0};
+  __shared__ double red[5 * 32];
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   const double cx = dirac_cx();
+  if (cg_out && blockIdx.x == 0 && threadIdx.x < 2) cg_out[threadIdx.x] = 0;
+  const int n1 = (int)g.n1, n2 = (int)g.n2, n0 = (int)g.n0;
+  const int plane = n1 * n2;
   for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < g.ngl;
        p += (int64_t)gridDim.x * PT) {
     const double h = vh_src ? vh_src[p] : 0.0;
@@ -107,13 +116,31 @@ __global__ void __launch_bounds__(PT) vlocal_kernel(SlabGeom g, const double* __
     vloc[p] = ve + (h + x);
     acc[0] += h * r;
     acc[2] += ve * r;
+    if (xfull) {  // -lap_h x at this point (grid.cpp:94-122 stencil, zero outside the box)
+      const int q = (int)(g.z0 * plane + p);
+      const int z = q / plane, rem = q - z * plane, y = rem / n2, xx = rem - y * n2;
+      const double c = xfull[q];
+      const double zm = z > 0 ? xfull[q - plane] : 0.0, zp = z + 1 < n0 ? xfull[q + plane] : 0.0;
+      const double ym = y > 0 ? xfull[q - n2] : 0.0, yp = y + 1 < n1 ? xfull[q + n2] : 0.0;
+      const double xm = xx > 0 ? xfull[q - 1] : 0.0, xp = xx + 1 < n2 ? xfull[q + 1] : 0.0;
+      const double lap = ((zm - 2.0 * c + zp) * g.ih2[0] + (ym - 2.0 * c + yp) * g.ih2[1]) +
+                         (xm - 2.0 * c + xp) * g.ih2[2];
+      const double bq = bfull[q];
+      const double res = bq + lap;  // b - A x, A = -lap_h
+      acc[3] += res * res;
+      acc[4] += bq * bq;
+    }
   }
-  block_sum<3>(acc, red);
+  block_sum<5>(acc, red);
   if (threadIdx.x == 0) {
     if (xc_here >= 0) {  // rows in S_EXC, S_EEXT, S_EH order: one grouped reduction
       partials[blockIdx.x] = acc[1];
       partials[gridDim.x + blockIdx.x] = acc[2];
       partials[2 * gridDim.x + blockIdx.x] = acc[0];
+      if (xfull) {
+        partials[3 * gridDim.x + blockIdx.x] = acc[3];
+        partials[4 * gridDim.x + blockIdx.x] = acc[4];
+      }
     } else {
       partials[blockIdx.x] = acc[0];
     }
@@ -402,10 +429,11 @@ void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupat
 
 void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h_src, double* v_h,
                    double* v_xc, const double* rho, double* v_local, double* partials,
-                   cudaStream_t s, int xc_here) {
+                   cudaStream_t s, int xc_here, const double* bfull, const double* xfull,
+                   int* cg_out) {
   ::po::count_launch();
   launch_pdl(vlocal_kernel, dim3(points_nblk(g)), dim3(PT), 0, s, g, v_ext, v_h_src, v_h, v_xc, rho,
-             v_local, partials, xc_here);
+             v_local, partials, xc_here, bfull, xfull, cg_out);
 }
 
 void launch_residual_diag(const SlabGeom& g, int N, const double* u, const double* hu,
@@ -454,8 +482,8 @@ void launch_reduce_rows(const double* partials, int rows, int nblk, double scale
 }
 
 void launch_reduce_rows_grouped(const double* partials, int grp, int ngroups, int nblk,
-                                const double* scales, double* out, cudaStream_t s) {
-  const int rows = grp * ngroups;
+                                const double* scales, double* out, cudaStream_t s, int rows) {
+  if (rows <= 0) rows = grp * ngroups;
   const int threads = 256;
   const int blocks = (rows * 32 + threads - 1) / threads;
   ::po::count_launch();

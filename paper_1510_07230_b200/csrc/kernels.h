@@ -48,7 +48,8 @@ void launch_density_xc(const SlabGeom& g, int N, const double* u, double occupat
 // [3][nblk]: sum eps*rho, sum v_ext*rho, sum v_h*rho.
 void launch_vlocal(const SlabGeom& g, const double* v_ext, const double* v_h_src, double* v_h,
                    double* v_xc, const double* rho, double* v_local, double* partials,
-                   cudaStream_t s, int xc_here = -1);
+                   cudaStream_t s, int xc_here = -1, const double* bfull = nullptr,
+                   const double* xfull = nullptr, int* cg_out = nullptr);
 // z_i = hu_i - sigma_ii u_i (manifold.cpp:204-216); partials [1][N][nblk]: sum z^2.
 void launch_residual_diag(const SlabGeom& g, int N, const double* u, const double* hu,
                           const double* sigma_diag, double* z, double* partials, cudaStream_t s);
@@ -68,8 +69,9 @@ void launch_abs_sum(const SlabGeom& g, int N, const double* x, double* partials,
 void launch_reduce_rows(const double* partials, int rows, int nblk, double scale, double* out,
                         cudaStream_t s, const double* guard = nullptr);
 // ngroups (<= 3) consecutive groups of grp rows, group q scaled by scales[q], one launch.
+// (rows > grp * ngroups: the rows past the groups take the last scale.)
 void launch_reduce_rows_grouped(const double* partials, int grp, int ngroups, int nblk,
-                                const double* scales, double* out, cudaStream_t s);
+                                const double* scales, double* out, cudaStream_t s, int rows = 0);
 // V_ext from softened-Coulomb atoms (energy.cpp:78-99) / Gaussian wells (C5).
 void launch_external_potential(const SlabGeom& g, const double* h3, const double* atoms,
                                int natoms, int gaussian, double* v, cudaStream_t s);

@@ -695,7 +695,16 @@ bool Solver::step() {
           te = apply_and_energy(wt, hwt, *tstate);
         } else {
           if (st_fresh) finish(tstate);
-          te = energy_from_fetch(*tstate);
+          if (!tstate->poisson_ok) {  // DST solve missed the CG criterion: CG from it, then redo H
+            E.force_cg_verify = true;
+            enqueue_state(wt, tstate, true);
+            E.force_cg_verify = false;
+            E.fetch_all();
+            finish(tstate);
+            te = apply_and_energy(wt, hwt, *tstate);
+          } else {
+            te = energy_from_fetch(*tstate);
+          }
         }
         if (std::isfinite(te.total) && te.total <= nm_c - p.rho1 * tau * znorm2) {
           accepted = true;

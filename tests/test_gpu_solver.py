@@ -175,7 +175,9 @@ def test_launch_and_path_switches_agree(tmp_path):
     """Measurement switches keep the numerics: plain launches instead of
     programmatic dependent launch (PO_PDL=0) give bitwise the same trajectory;
     the split trial rotation (PO_ROT_SPLIT=1: two-source mix + Gram/density
-    pass) and the 8-warp directions pass (PO_DIR_CW=8) agree to round-off."""
+    pass), the 8-warp directions pass (PO_DIR_CW=8), the Poisson check by the CG
+    kernel (PO_POISSON_DEFER=0) and a forced CG repair of every line-search
+    trial's Poisson solve (PO_FORCE_POISSON_REPAIR=1) agree to round-off."""
     import json
     import subprocess
     import sys
@@ -191,13 +193,16 @@ print(json.dumps([x["energy"] for x in r.records] + [r.energy["total"]]))
 ''' % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),)
     runs = {}
     for name, env_over in [("base", {}), ("nopdl", {"PO_PDL": "0"}), ("split", {"PO_ROT_SPLIT": "1"}),
-                           ("dir8", {"PO_DIR_CW": "8"})]:
+                           ("dir8", {"PO_DIR_CW": "8"}), ("nodefer", {"PO_POISSON_DEFER": "0"}),
+                           ("repair", {"PO_FORCE_POISSON_REPAIR": "1"})]:
         env = {k: v for k, v in os.environ.items() if not k.startswith("PO_")}
         env.update(env_over)
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
         assert r.returncode == 0, (name, r.stderr[-2000:])
         runs[name] = json.loads(r.stdout.strip().split("\n")[-1])
     assert runs["nopdl"] == runs["base"]
-    for name in ("split", "dir8"):
+    # the Poisson check in the v_local pass (default) vs the CG verification kernel,
+    # and the forced CG repair of every trial's solve (Solver: DST -> CG warm start)
+    for name in ("split", "dir8", "nodefer", "repair"):
         assert len(runs[name]) == len(runs["base"])
         assert max(abs(x - y) for x, y in zip(runs[name], runs["base"])) < 1e-9, name
