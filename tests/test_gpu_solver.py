@@ -112,12 +112,13 @@ def test_remainder_orbital_counts(port, native, n_orb):
     check(ref, got, wg, spec)
 
 
-@pytest.mark.parametrize("n_org,n_orb", [(1, 52), (2, 52), (1, 70), (2, 70), (1, 130)])
+@pytest.mark.parametrize("n_org,n_orb", [(1, 52), (2, 52), (1, 70), (2, 70), (1, 128), (1, 130)])
 def test_large_n_paths(port, native, n_org, n_orb):
     """N > 48: tiled Gram kernels (circulant diagonal tiles), trial Grams from
     G_WW / Sigma / G_HH, the separate density pass; N > 64 adds the TMA mix
     (triangular rotation) and the directions pass on the mix tiles (z, ||D||^2
-    and the BB products in one epilogue) — the C3/C4 code paths."""
+    and the BB products in one epilogue; N = 128: that epilogue spread over the
+    k-loop and the balanced triangular rotation) — the C3/C4 code paths."""
     spec = configs.small_molecule(14, n_orb, L=8.0, max_inner=6)
     ref, got, wg = run_both(port, native, spec, "opt_par_mod", n_org=n_org, n_diag=100)
     check(ref, got, wg, spec)

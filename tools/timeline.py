@@ -46,7 +46,7 @@ for g, nm in gaps[:12]:
     print(f"  {g:7.1f}  {nm[:70]}")
 agg = {}
 for s, en, nm in ks:
-    key = nm.split("(")[0][:60]
+    key = nm.replace("(anonymous namespace)::", "").replace("void ", "").split("(")[0][:60]
     a = agg.setdefault(key, [0, 0.0])
     a[0] += 1
     a[1] += en - s
