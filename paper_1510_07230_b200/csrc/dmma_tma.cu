@@ -974,9 +974,14 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
         if constexpr (R > 0) {  // out_rr(point c + gq) = sum_k A_k M(k, rr), k split over t4
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            double t = 0.0;
+            // two independent chains (a 2F-deep dependent FMA chain sat on every stage)
+            double t = 0.0, t2 = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < 2 * F; ++ks) t = fma(av[ks], mrem[r][ks], t);
+            for (int ks = 0; ks < 2 * F; ks += 2) {
+              t = fma(av[ks], mrem[r][ks], t);
+              if (ks + 1 < 2 * F) t2 = fma(av[ks + 1], mrem[r][ks + 1], t2);
+            }
+            t += t2;
             t += __shfl_xor_sync(0xffffffffu, t, 1);
             t += __shfl_xor_sync(0xffffffffu, t, 2);
             acc[FD][r] = t;  // read back below for i = 8 FD + r (lanes with t4 == 0)
