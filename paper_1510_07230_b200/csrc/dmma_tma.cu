@@ -1254,11 +1254,28 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
           }
       }
       if constexpr (DD) {
-        for (int ks = 0; ks < ksteps; ++ks) {
+        // even / odd k-steps into separate accumulators: 2F independent DMMA chains
+        // instead of F chains of length 2F (the loop is unrolled over the 2F slots)
+        double acc2[F][2];
+#pragma unroll
+        for (int f = 0; f < F; ++f) acc2[f][0] = acc2[f][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 2 * F; ++ks) {
+          if (ks >= ksteps) break;
           const int krow = 4 * ks + t4;
           const double av = krow < N ? sbuf[(krow) * PW + c + gq] : 0.0;
 #pragma unroll
-          for (int fi = 0; fi < F; ++fi) dmma_8x8x4(acc[fi], av, Ms[krow * NPAD + 8 * fi + gq]);
+          for (int fi = 0; fi < F; ++fi) {
+            if (ks & 1)
+              dmma_8x8x4(acc2[fi], av, Ms[krow * NPAD + 8 * fi + gq]);
+            else
+              dmma_8x8x4(acc[fi], av, Ms[krow * NPAD + 8 * fi + gq]);
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          acc[f][0] += acc2[f][0];
+          acc[f][1] += acc2[f][1];
         }
       }
 #pragma unroll
