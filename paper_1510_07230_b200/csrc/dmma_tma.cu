@@ -868,7 +868,10 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
   constexpr int NPAD = 8 * F;
   constexpr int FD = R > 0 ? F - 1 : F;
   constexpr int KS = 8 * CW;                 // points per stage
-  constexpr int PW = KS + 8;                 // padded row (conflict-free, see PADW)
+  // padded row, PW = 4 mod 16 doubles: a half-warp's (gq < 4, t4) reads of
+  // rows 4 ks + t4 and writes of rows 2 t4 + j' land in 16 distinct 8-byte
+  // slots (64-bit shared accesses are served per half-warp)
+  constexpr int PW = KS + 4;
   constexpr int NT = CW == 8 ? TTH : (CW + 1) * 32;
   constexpr int NP = FD * (FD + 1) / 2;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
@@ -990,13 +993,14 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
       }
       __syncwarp();  // every lane is done reading the chunk's source values
       double dsum = 0.0;
+      const int jx = t4 >> 1;  // lanes t4 = 2, 3 store their pair swapped (rows mod 4 distinct)
 #pragma unroll
       for (int fi = 0; fi < F; ++fi)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const int i = 8 * fi + 2 * t4 + j;
+          const int i = 8 * fi + 2 * t4 + (j ^ jx);
           if (i < N) {
-            const double v = acc[fi][j];
+            const double v = jx ? acc[fi][j ^ 1] : acc[fi][j];
             if (p < ngl) out[(int64_t)i * ld + p] = v;
             sbuf[(i) * PW + c + gq] = v;
             dsum += v * v;
@@ -1023,17 +1027,21 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int rr = 8 * FD + r;
+          // point pairs visited in a lane-rotated order: rows i = lane (stride
+          // PW = 4 mod 16) then hit distinct banks within each quarter-warp
+          const int rot = lane >> 2;
           double2 bv[4];
 #pragma unroll
           for (int m = 0; m < 4; ++m)
-            bv[m] = *reinterpret_cast<const double2*>(sbuf + (rr) * PW + c + 2 * m);
+            bv[m] = *reinterpret_cast<const double2*>(sbuf + (rr) * PW + c + 2 * ((m + rot) & 3));
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int i = lane + 32 * h;
             if (i >= N || i > rr) continue;
             double2 av[4];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) av[m] = *reinterpret_cast<const double2*>(sbuf + (i) * PW + c + 2 * m);
+            for (int m = 0; m < 4; ++m)
+              av[m] = *reinterpret_cast<const double2*>(sbuf + (i) * PW + c + 2 * ((m + rot) & 3));
             double p0 = av[0].x * bv[0].x, p1 = av[0].y * bv[0].y, p2 = av[1].x * bv[1].x,
                    p3 = av[1].y * bv[1].y;
             p0 = fma(av[2].x, bv[2].x, p0);
@@ -1044,10 +1052,14 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
           }
         }
       }
+      // G2 fragments: k = points t4 and 4 + t4 of the chunk (two 64-bit reads,
+      // conflict-free at PW = 4 mod 16)
       double2 a[FD > 0 ? FD : 1];
 #pragma unroll
-      for (int f = 0; f < FD; ++f)
-        a[f] = *reinterpret_cast<const double2*>(sbuf + (8 * f + gq) * PW + c + 2 * t4);
+      for (int f = 0; f < FD; ++f) {
+        a[f].x = sbuf[(8 * f + gq) * PW + c + t4];
+        a[f].y = sbuf[(8 * f + gq) * PW + c + 4 + t4];
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       int q = 0;
@@ -1124,7 +1136,7 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
   const int R = (N % 8 == 1 || N % 8 == 2) && N > 8 ? N % 8 : 0;
   // 12 consumer warps where they fit 128 registers without spilling (N <= 33)
   const int CW = cw_env == 6 ? 6 : (cw_env == 8 || F > 5 || (F == 5 && R == 2) ? 8 : 12);
-  const int KS = 8 * CW, PW = KS + 8;
+  const int KS = 8 * CW, PW = KS + 4;
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   int nsrc = 0;

@@ -18,7 +18,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
     --log-file $OUT/bench_launches_C2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 echo "ncu bench rc=$?"
 # one full capture of each dominant kernel of the C2 iteration (dram traffic per launch)
-ncu --set full --import-source on --clock-control none \
-    -k regex:"hamiltonian4_kernel|directions_tma_kernel|rotate_fused_kernel|gram_tma_kernel" -c 6 \
+ncu --set full --import-source on --clock-control none --profile-from-start off \
+    -k regex:"hamiltonian4_kernel|directions_tma_kernel|rotate_fused_kernel|gram_tma_kernel" -c 8 \
     -o $OUT/c2_full python tools/step_profile.py --steps 1 --warmup 3 > /dev/null 2>&1
 echo "ncu full rc=$?"
