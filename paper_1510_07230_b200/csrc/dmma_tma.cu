@@ -326,11 +326,15 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
         continue;
       }
       if constexpr (REM) {
-        // 8 points of one row of source q as 4 double2
+        // 8 points of one row of source q as 4 double2, in a lane-rotated pair
+        // order: rows i = lane (stride PADW = 8 mod 16) then fall on distinct
+        // banks within each quarter-warp (the plain order was a 4-way conflict)
+        const int rot = (lane >> 1) & 3;
         auto row8 = [&](int row, int q, double2 (&v)[4]) {
 #pragma unroll
           for (int m = 0; m < 4; ++m)
-            v[m] = *reinterpret_cast<const double2*>(sbuf + q * qstride + pad(row, c + 2 * m));
+            v[m] = *reinterpret_cast<const double2*>(sbuf + q * qstride +
+                                                     pad(row, c + 2 * ((m + rot) & 3)));
         };
         auto dot8 = [](const double2 (&x)[4], const double2 (&y)[4], double t) {
           // four independent products chains instead of one 8-deep FMA chain
@@ -1212,11 +1216,14 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
   const int NB = N;  // box rows: no zero-filled padding rows in the stream
   const size_t qstride = ((size_t)NB * PW + 15) & ~(size_t)15;
   const size_t sdoubles = NSRC * qstride;
-  double* Ms = stage0 + (size_t)nst * sdoubles;  // [NPAD][NPAD] (DD)
-  double* msig = Ms + NPAD * NPAD;               // [NPAD]: -sigma_ii
+  // Sigma rows padded to MST = 4 mod 16 doubles: the fragment reads of rows
+  // 4 ks + t4 are then conflict-free per half-warp
+  constexpr int MST = NPAD + 4;
+  double* Ms = stage0 + (size_t)nst * sdoubles;  // [NPAD][MST] (DD)
+  double* msig = Ms + NPAD * MST;                // [NPAD]: -sigma_ii
   double* nred = msig + NPAD;                    // [8][NQ][NPAD]
-  for (int e = threadIdx.x; e < NPAD * NPAD; e += NT) {
-    const int k = e / NPAD, i = e % NPAD;
+  for (int e = threadIdx.x; e < NPAD * MST; e += NT) {
+    const int k = e / MST, i = e % MST;
     Ms[e] = (DD && k < N && i < N) ? Sigma[(int64_t)k * N + i] : 0.0;
   }
   for (int i = threadIdx.x; i < NPAD; i += NT) msig[i] = i < N ? -sig[i] : 0.0;
@@ -1259,7 +1266,7 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
         for (int fi = 0; fi < F; ++fi)
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
-            const int i = 8 * fi + 2 * t4 + j;
+            const int i = 8 * fi + 2 * t4 + (j ^ (t4 >> 1));
             const bool ok = p < ngl && i < N;
             wpv[fi][j] = ok ? __ldcs(WP + (int64_t)i * ld + p) : 0.0;
             zpv[fi][j] = ok ? __ldcs(ZP + (int64_t)i * ld + p) : 0.0;
@@ -1279,9 +1286,9 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
 #pragma unroll
           for (int fi = 0; fi < F; ++fi) {
             if (ks & 1)
-              dmma_8x8x4(acc2[fi], av, Ms[krow * NPAD + 8 * fi + gq]);
+              dmma_8x8x4(acc2[fi], av, Ms[krow * MST + 8 * fi + gq]);
             else
-              dmma_8x8x4(acc[fi], av, Ms[krow * NPAD + 8 * fi + gq]);
+              dmma_8x8x4(acc[fi], av, Ms[krow * MST + 8 * fi + gq]);
           }
         }
 #pragma unroll
@@ -1290,16 +1297,20 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
           acc[f][1] += acc2[f][1];
         }
       }
+      // lanes t4 = 2, 3 visit their pair of orbitals swapped: rows 2 t4 + j'
+      // then differ mod 4 across the half-warp (PW = 4 mod 16, conflict-free);
+      // slot j of nrm holds orbital 8 fi + 2 t4 + (j ^ jx)
+      const int jx = t4 >> 1;
 #pragma unroll
       for (int fi = 0; fi < F; ++fi)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const int i = 8 * fi + 2 * t4 + j;
+          const int i = 8 * fi + 2 * t4 + (j ^ jx);
           if (p < ngl && i < N) {
             const int off = (i) * PW + c + gq;
             const double wv = sbuf[off], hv = sbuf[qstride + off];
             if constexpr (DD) {
-              double d = -acc[fi][j];
+              double d = -(jx ? acc[fi][j ^ 1] : acc[fi][j]);
               d += hv;
               nrm[1][fi][j] += d * d;
             }
@@ -1328,7 +1339,7 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
           v += __shfl_xor_sync(0xffffffffu, v, 4);
           v += __shfl_xor_sync(0xffffffffu, v, 8);
           v += __shfl_xor_sync(0xffffffffu, v, 16);
-          if (gq == 0) nred[(warp * NQ + q) * NPAD + 8 * fi + 2 * t4 + j] = v;
+          if (gq == 0) nred[(warp * NQ + q) * NPAD + 8 * fi + 2 * t4 + (j ^ (t4 >> 1))] = v;
         }
   }
   __syncthreads();
@@ -1356,7 +1367,7 @@ int launch_directions_fdh(const double* W, const double* HW, int N, int64_t ld, 
   const int nsrc = HIST && !ldgh ? 4 : 2;
   const int CW = cw_env >= 4 && cw_env <= 8 && cw_env != 7 ? cw_env : (nsrc == 4 ? 6 : 8);
   const int KS = 8 * CW, PW = CW == 8 ? PADW : KS + 4;
-  const size_t extra = (size_t)NPAD * NPAD + NPAD + (size_t)CW * NQ * NPAD;
+  const size_t extra = (size_t)NPAD * (NPAD + 4) + NPAD + (size_t)CW * NQ * NPAD;
   const size_t sd = (size_t)nsrc * (((size_t)N * PW + 15) & ~(size_t)15);
   int nst = (int)((tbudget() / 8 - extra) / sd);
   if (nst > 8) nst = 8;
