@@ -860,13 +860,13 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
 // shared memory and has one producer warp (13 warps, at most 4 per SM
 // sub-partition: 128 registers; 1.5x the warps in flight for this
 // latency-bound pass)
-template <int F, int R, int CW>
+template <int F, int R, int CW, bool ZV = false>
 __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused_kernel(
     const __grid_constant__ Maps maps, int nsrc, int N, int64_t ld, int64_t ngl, int64_t pchunk,
     int nst, double sa, const double* __restrict__ M, double* __restrict__ out,
     double* __restrict__ ws, double occ, int xc, double* __restrict__ rho, double* __restrict__ vxc,
     double* __restrict__ bvec, const double* __restrict__ vext, double* __restrict__ dpart,
-    const double* __restrict__ sa_dev) {
+    const double* __restrict__ sa_dev, const double* __restrict__ zsig) {
   PO_PDL_ENTRY();
   if (sa_dev) sa = *sa_dev;  // trial scale decided on the device (bb_tau_kernel)
   constexpr int NPAD = 8 * F;
@@ -943,6 +943,13 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
 #pragma unroll
       for (int ks = 0; ks < 2 * F; ++ks)
         mrem[r][ks] = (R > 0 && 4 * ks + t4 < N) ? Ms[(4 * ks + t4) * NPAD + 8 * FD + r] : 0.0;
+    // zsig: the second source is HW and the direction z = HW - sigma W is rebuilt
+    // here with the directions pass's FMA (bitwise the value it would have stored)
+    double mz[ZV ? 2 * F : 1];
+    if constexpr (ZV) {
+#pragma unroll
+      for (int ks = 0; ks < 2 * F; ++ks) mz[ks] = 4 * ks + t4 < N ? -zsig[4 * ks + t4] : 0.0;
+    }
     // V_ext of the next chunk is requested one stage ahead (a global load in
     // the epilogue stalled every warp for its full latency)
     double vx_next = (vext && t4 == 0 && pbeg + c + gq < ngl) ? __ldg(vext + pbeg + c + gq) : 0.0;
@@ -963,7 +970,11 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
         for (int ks = 0; ks < 2 * F; ++ks) {
           const int off = (4 * ks + t4) * PW + c + gq;
           av[ks] = sbuf[off];
-          if (nsrc == 2) av[ks] += sa * sbuf[qstride + off];
+          if (nsrc == 2) {
+            double zb = sbuf[qstride + off];
+            if constexpr (ZV) zb = fma(mz[ZV ? ks : 0], av[ks], zb);
+            av[ks] += sa * zb;
+          }
           if (4 * ks + t4 >= N) av[ks] = 0.0;  // rows past N alias the next box
         }
 #pragma unroll
@@ -1134,12 +1145,12 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
                           double sa, const double* M, double* out, double* ws, double* G, double w,
                           double occ, int xc, double* rho, double* vxc, double* bvec,
                           const double* vext, double* dpart, cudaStream_t s,
-                          const double* sa_dev) {
+                          const double* sa_dev, const double* zsig) {
   constexpr int NPAD = 8 * F;
   static const int cw_env = getenv("PO_RF_CW") ? atoi(getenv("PO_RF_CW")) : 8;  // measurement (12: slower, 228 vs 215 us at C2)
   const int R = (N % 8 == 1 || N % 8 == 2) && N > 8 ? N % 8 : 0;
   // 12 consumer warps where they fit 128 registers without spilling (N <= 33)
-  const int CW = cw_env == 6 ? 6 : (cw_env == 8 || F > 5 || (F == 5 && R == 2) ? 8 : 12);
+  const int CW = zsig || cw_env == 8 ? 8 : cw_env == 6 ? 6 : (F > 5 || (F == 5 && R == 2) ? 8 : 12);
   const int KS = 8 * CW, PW = KS + 4;
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
@@ -1162,7 +1173,9 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
   if (nblk > kb) nblk = (int)kb;
   const int64_t pchunk = ((kb + nblk - 1) / nblk) * KS;
   nblk = (int)((ld + pchunk - 1) / pchunk);
-  auto k = CW == 6 ? (F == 1 || R == 0 ? rotate_fused_kernel<F, 0, 6>
+  auto k = zsig ? (F == 1 || R == 0 ? rotate_fused_kernel<F, 0, 8, true>
+                             : R == 1 ? rotate_fused_kernel<F, 1, 8, true> : rotate_fused_kernel<F, 2, 8, true>)
+         : CW == 6 ? (F == 1 || R == 0 ? rotate_fused_kernel<F, 0, 6>
                                        : R == 1 ? rotate_fused_kernel<F, 1, 6> : rotate_fused_kernel<F, 2, 6>)
          : CW == 8 ? (F == 1 || R == 0 ? rotate_fused_kernel<F, 0, 8>
                                        : R == 1 ? rotate_fused_kernel<F, 1, 8> : rotate_fused_kernel<F, 2, 8>)
@@ -1173,7 +1186,7 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
   ::po::count_launch();
   set_smem(reinterpret_cast<const void*>(k), (int)cfg.smem);
   launch_pdl(k, dim3(nblk), dim3(nthreads), cfg.smem, s, maps, nsrc, N, ld, ngl, pchunk, cfg.nst, sa, M, out, ws, occ, xc,
-                                 rho, vxc, bvec, vext, dpart, sa_dev);
+                                 rho, vxc, bvec, vext, dpart, sa_dev, zsig);
   const int64_t threads = (int64_t)N * N * 32;
   ::po::count_launch();
   launch_pdl(gram_tma_reduce_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, N, NPAD, 1,
@@ -1196,11 +1209,14 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
 // CW consumer warps (stage = 8 CW points): CW = 6 with a 52-point padded row
 // gives a three-deep ring for the four streamed sources at N = 33 (CW = 8: two
 // stages of 76 KB, i.e. one stage in flight while one is consumed)
-template <int F, bool DD, bool HIST, bool LDGH, int CW>
+// ZM: 0 = z stored, ZP is the previous z; 1 = z not stored (implicit), ZP is
+// the previous z; 2 = z not stored, ZP is the previous HW (previous z implicit)
+template <int F, bool DD, bool HIST, bool LDGH, int CW, int ZM = 0>
 __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_tma_kernel(
     const __grid_constant__ Maps maps, int N, int64_t ld, int64_t ngl, int64_t pchunk, int nst,
     const double* __restrict__ Sigma, const double* __restrict__ sig, double* __restrict__ Z,
-    double* __restrict__ partials, const double* __restrict__ WP, const double* __restrict__ ZP) {
+    double* __restrict__ partials, const double* __restrict__ WP, const double* __restrict__ ZP,
+    const double* __restrict__ psig, double* __restrict__ sig_out) {
   PO_PDL_ENTRY();
   constexpr int NPAD = 8 * F;
   constexpr int NSRC = HIST && !LDGH ? 4 : 2;
@@ -1221,12 +1237,17 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
   constexpr int MST = NPAD + 4;
   double* Ms = stage0 + (size_t)nst * sdoubles;  // [NPAD][MST] (DD)
   double* msig = Ms + NPAD * MST;                // [NPAD]: -sigma_ii
-  double* nred = msig + NPAD;                    // [8][NQ][NPAD]
+  double* mpsig = msig + NPAD;                   // [NPAD]: -sigma_ii of the previous iterate
+  double* nred = mpsig + NPAD;                   // [8][NQ][NPAD]
   for (int e = threadIdx.x; e < NPAD * MST; e += NT) {
     const int k = e / MST, i = e % MST;
     Ms[e] = (DD && k < N && i < N) ? Sigma[(int64_t)k * N + i] : 0.0;
   }
-  for (int i = threadIdx.x; i < NPAD; i += NT) msig[i] = i < N ? -sig[i] : 0.0;
+  for (int i = threadIdx.x; i < NPAD; i += NT) {
+    msig[i] = i < N ? -sig[i] : 0.0;
+    mpsig[i] = ZM == 2 && i < N ? -psig[i] : 0.0;
+    if (sig_out && blockIdx.x == 0 && i < N) sig_out[i] = sig[i];  // the sigma z is built from
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
@@ -1314,12 +1335,17 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
               d += hv;
               nrm[1][fi][j] += d * d;
             }
-            const double z = hv + msig[i] * wv;
-            Z[(int64_t)i * ld + p] = z;
+            // z = HW - sigma W (one FMA; rotate_fused and the previous-z term
+            // below rebuild exactly this value when z is not stored, Z == null)
+            const double z = fma(msig[i], wv, hv);
+            if constexpr (ZM == 0) Z[(int64_t)i * ld + p] = z;
             nrm[0][fi][j] += z * z;
             if constexpr (HIST) {
-              const double sv = wv - (LDGH ? wpv[fi][j] : sbuf[2 * qstride + off]);
-              const double yv = z - (LDGH ? zpv[fi][j] : sbuf[3 * qstride + off]);
+              const double wp = LDGH ? wpv[fi][j] : sbuf[2 * qstride + off];
+              double zp = LDGH ? zpv[fi][j] : sbuf[3 * qstride + off];
+              if constexpr (ZM == 2) zp = fma(mpsig[i], wp, zp);  // source 3 is the previous HW
+              const double sv = wv - wp;
+              const double yv = z - zp;
               nrm[2][fi][j] += sv * sv;
               nrm[3][fi][j] += sv * yv;
               nrm[4][fi][j] += yv * yv;
@@ -1355,7 +1381,8 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
 template <int F, bool DD, bool HIST>
 int launch_directions_fdh(const double* W, const double* HW, int N, int64_t ld, int64_t ngl,
                           const double* Sigma, const double* sig, double* Z, double* partials,
-                          cudaStream_t s, const double* WP, const double* ZP) {
+                          cudaStream_t s, const double* WP, const double* ZP, const double* psig,
+                          double* sig_out) {
   constexpr int NPAD = 8 * F;
   constexpr int NQ = HIST ? 5 : 2;
   // (measured and dropped: W_prev / Z_prev through direct loads instead of the
@@ -1365,9 +1392,10 @@ int launch_directions_fdh(const double* W, const double* HW, int N, int64_t ld, 
   // four streamed sources (measurement switch PO_DIR_CW = 6 / 8)
   static const int cw_env = getenv("PO_DIR_CW") ? atoi(getenv("PO_DIR_CW")) : 0;
   const int nsrc = HIST && !ldgh ? 4 : 2;
-  const int CW = cw_env >= 4 && cw_env <= 8 && cw_env != 7 ? cw_env : (nsrc == 4 ? 6 : 8);
+  const int zm = Z ? 0 : (HIST && psig ? 2 : 1);
+  const int CW = zm == 0 && cw_env >= 4 && cw_env <= 8 && cw_env != 7 ? cw_env : (nsrc == 4 ? 6 : 8);
   const int KS = 8 * CW, PW = CW == 8 ? PADW : KS + 4;
-  const size_t extra = (size_t)NPAD * (NPAD + 4) + NPAD + (size_t)CW * NQ * NPAD;
+  const size_t extra = (size_t)NPAD * (NPAD + 4) + 2 * NPAD + (size_t)CW * NQ * NPAD;
   const size_t sd = (size_t)nsrc * (((size_t)N * PW + 15) & ~(size_t)15);
   int nst = (int)((tbudget() / 8 - extra) / sd);
   if (nst > 8) nst = 8;
@@ -1384,26 +1412,30 @@ int launch_directions_fdh(const double* W, const double* HW, int N, int64_t ld, 
   const int64_t pchunk = ((kb + nblk - 1) / nblk) * KS;
   nblk = (int)((ld + pchunk - 1) / pchunk);
   ::po::count_launch();
-  auto k = CW == 8   ? directions_tma_kernel<F, DD, HIST, false, 8>
+  auto k = zm == 1   ? (HIST ? directions_tma_kernel<F, DD, HIST, false, 6, 1>
+                               : directions_tma_kernel<F, DD, HIST, false, 8, 1>)
+           : zm == 2 ? directions_tma_kernel<F, DD, HIST, false, 6, 2>
+           : CW == 8 ? directions_tma_kernel<F, DD, HIST, false, 8>
            : CW == 6 ? directions_tma_kernel<F, DD, HIST, false, 6>
            : CW == 5 ? directions_tma_kernel<F, DD, HIST, false, 5>
                      : directions_tma_kernel<F, DD, HIST, false, 4>;
   set_smem(reinterpret_cast<const void*>(k), (int)cfg.smem);
   launch_pdl(k, dim3(nblk), dim3(CW == 8 ? TTH : (CW + 1) * 32), cfg.smem, s, maps, N, ld, ngl, pchunk, cfg.nst, Sigma, sig, Z,
-                                                         partials, WP, ZP);
+             partials, WP, ZP, psig, sig_out);
   return nblk;
 }
 
 template <int F>
 int launch_directions_f(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
                         const double* WP, const double* ZP, const double* Sigma, const double* sig,
-                        double* Z, double* partials, cudaStream_t s) {
+                        double* Z, double* partials, cudaStream_t s, const double* psig,
+                        double* sig_out) {
   const bool hist = WP && ZP;
   if (Sigma)
-    return hist ? launch_directions_fdh<F, true, true>(W, HW, N, ld, ngl, Sigma, sig, Z, partials, s, WP, ZP)
-                : launch_directions_fdh<F, true, false>(W, HW, N, ld, ngl, Sigma, sig, Z, partials, s, WP, ZP);
-  return hist ? launch_directions_fdh<F, false, true>(W, HW, N, ld, ngl, Sigma, sig, Z, partials, s, WP, ZP)
-              : launch_directions_fdh<F, false, false>(W, HW, N, ld, ngl, Sigma, sig, Z, partials, s, WP, ZP);
+    return hist ? launch_directions_fdh<F, true, true>(W, HW, N, ld, ngl, Sigma, sig, Z, partials, s, WP, ZP, psig, sig_out)
+                : launch_directions_fdh<F, true, false>(W, HW, N, ld, ngl, Sigma, sig, Z, partials, s, WP, ZP, psig, sig_out);
+  return hist ? launch_directions_fdh<F, false, true>(W, HW, N, ld, ngl, Sigma, sig, Z, partials, s, WP, ZP, psig, sig_out)
+              : launch_directions_fdh<F, false, false>(W, HW, N, ld, ngl, Sigma, sig, Z, partials, s, WP, ZP, psig, sig_out);
 }
 
 template <int F>
@@ -2525,10 +2557,11 @@ int launch_rotation_split_f(int N, int64_t ld, int64_t ngl, const double* A, con
 int launch_rotate_fused(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab,
                         double sa, const double* M, double* out, double* ws, double* G, double w,
                         double occ, int xc, double* rho, double* vxc, double* bvec,
-                        const double* vext, double* dpart, cudaStream_t s, const double* sa_dev) {
+                        const double* vext, double* dpart, cudaStream_t s, const double* sa_dev,
+                        const double* zsig) {
   // measurement switch: rotation as the two-source mix + a Gram/density pass (slower: 250 vs 218 us at C2)
   static const int split = getenv("PO_ROT_SPLIT") ? atoi(getenv("PO_ROT_SPLIT")) : 0;
-  if (split) {
+  if (split && !zsig) {
     switch ((N + 7) / 8) {
 #define PO_RS(F) \
   case F:        \
@@ -2541,7 +2574,7 @@ int launch_rotate_fused(int N, int64_t ld, int64_t ngl, const double* A, const d
   switch ((N + 7) / 8) {
 #define PO_RF(F) \
   case F:        \
-    return launch_rotate_fused_f<F>(N, ld, ngl, A, Ab, sa, M, out, ws, G, w, occ, xc, rho, vxc, bvec, vext, dpart, s, sa_dev);
+    return launch_rotate_fused_f<F>(N, ld, ngl, A, Ab, sa, M, out, ws, G, w, occ, xc, rho, vxc, bvec, vext, dpart, s, sa_dev, zsig);
     PO_RF(1) PO_RF(2) PO_RF(3) PO_RF(4) PO_RF(5) PO_RF(6)
 #undef PO_RF
   }
@@ -2550,11 +2583,12 @@ int launch_rotate_fused(int N, int64_t ld, int64_t ngl, const double* A, const d
 
 int launch_directions(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
                       const double* WP, const double* ZP, const double* Sigma, const double* sig,
-                      double* Z, double* partials, cudaStream_t s) {
+                      double* Z, double* partials, cudaStream_t s, const double* psig,
+                      double* sig_out) {
   switch ((N + 7) / 8) {
 #define PO_DR(F) \
   case F:        \
-    return launch_directions_f<F>(N, ld, ngl, W, HW, WP, ZP, Sigma, sig, Z, partials, s);
+    return launch_directions_f<F>(N, ld, ngl, W, HW, WP, ZP, Sigma, sig, Z, partials, s, psig, sig_out);
     PO_DR(1) PO_DR(2) PO_DR(3) PO_DR(4) PO_DR(5) PO_DR(6)
 #undef PO_DR
   }

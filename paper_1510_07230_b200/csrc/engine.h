@@ -172,7 +172,9 @@ class Engine {
   size_t off_yy() const { return 7 * (size_t)N; }
   size_t off_abs() const { return 8 * (size_t)N; }
   size_t off_scal() const { return 9 * (size_t)N; }  // 64 scalars
-  size_t dvec_len() const { return 9 * (size_t)N + 64; }
+  // two sigma rows an implicit direction z = HW - sigma W was built from (solver)
+  size_t off_zsig(int k) const { return 9 * (size_t)N + 64 + (size_t)k * N; }
+  size_t dvec_len() const { return 11 * (size_t)N + 64; }
   // scalar slots
   enum { S_EXC = 0, S_EEXT = 1, S_EH = 2, S_CHOL = 8, S_EIG = 12, S_INVS = 16, S_MSTAT = 20,
          S_MSTAT2 = 24, S_SYM = 28, S_QR2 = 32, S_CHOL2 = 36,

@@ -255,6 +255,18 @@ __global__ void __launch_bounds__(PT) lincomb_kernel(int64_t total, const double
     out[p] = a[p] + sc * b[p];
 }
 
+// z = HW - sigma W written out (a direction the fused path kept implicit),
+// with the directions pass's FMA so the block is bitwise what it would have stored
+__global__ void __launch_bounds__(PT) z_from_hw_kernel(int64_t total, int64_t ld,
+                                                       const double* __restrict__ w,
+                                                       const double* __restrict__ hw,
+                                                       const double* __restrict__ sig,
+                                                       double* __restrict__ z) {
+  for (int64_t p = (int64_t)blockIdx.x * PT + threadIdx.x; p < total;
+       p += (int64_t)gridDim.x * PT)
+    z[p] = fma(-sig[p / ld], w[p], hw[p]);
+}
+
 // One warp per row; lanes stride the partials, then a fixed shuffle tree.
 // rows in [grp, 2 grp) take scale2, rows from 2 grp on scale3 (grp = 0: one scale)
 __global__ void reduce_rows_kernel(const double* __restrict__ partials, int rows, int nblk,
@@ -463,6 +475,13 @@ void launch_abs_sum(const SlabGeom& g, int N, const double* x, double* partials,
   dim3 grid(per_orbital_nblk(g, N), N);
   ::po::count_launch();
   abs_sum_kernel<<<grid, PT, 0, s>>>(g, N, x, partials);
+}
+
+void launch_z_from_hw(const SlabGeom& g, int N, const double* w, const double* hw,
+                      const double* sig, double* z, cudaStream_t s) {
+  const int64_t total = (int64_t)N * g.ld;
+  ::po::count_launch();
+  z_from_hw_kernel<<<nblk_for(total), PT, 0, s>>>(total, g.ld, w, hw, sig, z);
 }
 
 void launch_lincomb(const SlabGeom& g, int N, const double* a, double sc, const double* b,

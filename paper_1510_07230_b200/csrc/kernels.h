@@ -61,6 +61,8 @@ void launch_residual_bb(const SlabGeom& g, int N, const double* u, const double*
 void launch_bb(const SlabGeom& g, int N, const double* w, const double* wp, const double* z,
                const double* zp, double* partials, cudaStream_t s);
 // out = a + s * b over a whole block (grid.cpp:219-228).
+void launch_z_from_hw(const SlabGeom& g, int N, const double* w, const double* hw,
+                      const double* sig, double* z, cudaStream_t s);
 void launch_lincomb(const SlabGeom& g, int N, const double* a, double sc, const double* b,
                     double* out, cudaStream_t s);
 // Per-orbital sum of |x| (mean-abs convergence, optimizer.cpp:446-458): partials [1][N][nblk].
@@ -141,10 +143,14 @@ int launch_rotate_fused(int N, int64_t ld, int64_t ngl, const double* A, const d
                         double sa, const double* M, double* out, double* ws, double* G, double w,
                         double occ, int xc, double* rho, double* vxc, double* bvec,
                         const double* vext, double* dpart, cudaStream_t s,
-                        const double* sa_dev = nullptr);
+                        const double* sa_dev = nullptr, const double* zsig = nullptr);
+// zsig (rotate_fused): Ab is HW and the direction is z = HW - zsig W, rebuilt in
+// the kernel. Directions: Z may be null (z not stored); psig: ZP is the previous
+// HW and the previous z is HWP - psig WP; sig_out receives the sigma used.
 int launch_directions(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
                       const double* WP, const double* ZP, const double* Sigma, const double* sig,
-                      double* Z, double* partials, cudaStream_t s);
+                      double* Z, double* partials, cudaStream_t s, const double* psig = nullptr,
+                      double* sig_out = nullptr);
 int launch_mix_tma(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
                    const double* M, double alpha, const double* C, double beta, int upper,
                    double* out, double* norms, cudaStream_t s, const double* guard);

@@ -166,9 +166,13 @@ bool orthonormalize_dev(Engine& E, const double* A, const double* Ab, double sa,
 bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, double* out,
                   bool measure, DevState* st = nullptr, int hartree = 0, int xc = 0,
                   bool g0_from_grams = false, const double* tau_dev = nullptr,
-                  const BBArgs* bb = nullptr) {
+                  const BBArgs* bb = nullptr, const double* zsig = nullptr) {
   (void)measure;
   double* sc = E.scal();
+  // zsig: Ab is HW and the direction z = HW - zsig W is implicit; only the
+  // Grams-based trial Gram and the fused rotation can take it (callers check)
+  if (zsig && !(g0_from_grams && st && E.N <= 48 && tma2d_available()))
+    throw Error(PO_EINVAL, "implicit direction outside the fused trial path");
   // G0 of W - tau Z from G_WW (dmat[8]), Sigma (dmat[4]), G_HH (dmat[7]), its stats and
   // its Cholesky in one launch where possible
   if (!(g0_from_grams &&
@@ -193,14 +197,14 @@ bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, doubl
     const int nb = launch_rotate_fused(E.N, E.g.ld, E.g.ngl, A, Ab, sa, E.dmat[1], out, E.gram_ws,
                                        E.dmat[2], E.g.w, E.occ, -1, st->rho, st->v_xc,
                                        E.density_b_target(hartree), E.v_ext, E.partials, E.s,
-                                       tau_dev ? tau_dev + 1 : nullptr);
+                                       tau_dev ? tau_dev + 1 : nullptr, zsig);
     if (nb >= 0) {
       if (E.size > 1) E.comm->allreduce_sum(E.dmat[2], (size_t)E.N * E.N, E.s);
       fused = true;
     }
   }
   if (!fused) {
-    if (tau_dev) throw Error(PO_EINVAL, "device-side trial scale needs the fused rotation");
+    if (tau_dev || zsig) throw Error(PO_EINVAL, "device-side trial scale needs the fused rotation");
     E.mix(A, Ab, sa, E.dmat[1], 1.0, nullptr, 0.0, 1, out, nullptr);
     E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2]);
   }
@@ -254,6 +258,13 @@ struct Solver {
 
   // InnerLoop::run state (optimizer.cpp:358-372), kept across step() calls
   BRef w, hw, prev_w, prev_z, recovery_w;
+  // Implicit directions (fused small-N path, every iteration orthonormalised):
+  // z = HW - sigma W is never stored; the rotation rebuilds it from HW and the
+  // next iteration's BB products from the previous HW (prev_hw) with the sigma
+  // row saved in dvec zsig slot prev_zslot. Any other consumer materialises it.
+  BRef prev_hw;
+  bool prev_zv = false;
+  int prev_zslot = 0;
   SRef state, recovery_state;
   double nm_c = 0.0, nm_q = 1.0;
   std::vector<double> orth_energies;
@@ -375,6 +386,8 @@ struct Solver {
     bool valid = false;
     Clock::time_point t0;
     bool orth_iter = false, need_full = false, fused = false;
+    bool zv = false;  // z implicit (see prev_hw); zsig slot zslot
+    int zslot = 0;
     BRef z, dscratch;
     struct {
       BRef wt, rep, hwt;
@@ -384,6 +397,19 @@ struct Solver {
   };
   Phase1 ph1;
   void enqueue_phase1(int iter);  // iter: the iteration these directions belong to
+  const double* zsig(int slot) { return E.dvec + E.off_zsig(slot); }
+  // write out an implicit direction (block of hw - sigma w)
+  BRef materialize_z(const BRef& wb, const BRef& hwb, int slot) {
+    BRef zb = pool.get();
+    launch_z_from_hw(E.g, E.N, P(wb), P(hwb), zsig(slot), P(zb), E.s);
+    return zb;
+  }
+  void materialize_prev_z() {
+    if (!prev_zv) return;
+    prev_z = materialize_z(prev_w, prev_hw, prev_zslot);
+    prev_zv = false;
+    prev_hw.reset();
+  }
   void prefetch_next() {
     if (!ph1.valid && !finished && !converged && l < p.max_inner) enqueue_phase1(l);
   }
@@ -437,28 +463,44 @@ void Solver::enqueue_phase1(int iter) {
 
     // ---- compute_directions, optimizer.cpp:265-320
     BRef& z = ph.z;
-    z = pool.get();
     BRef& dscratch = ph.dscratch;
     const int onb = per_orbital_nblk(E.g, n);
     bool& fused = ph.fused;
     bool bb_done = false;
     ghh_fresh = false;  // G_HH (dmat[7]) belongs to this iteration's HW only
-    if (!full_grad && !(mean_abs && need_full) && n <= 48 && tma2d_available()) {
+    static const bool zfree_env = !std::getenv("PO_ZFREE") || std::atoi(std::getenv("PO_ZFREE")) != 0;
+    const bool fused_dir = !full_grad && !(mean_abs && need_full) && n <= 48 && tma2d_available();
+    // implicit z: only where every consumer is the fused rotation of a trial
+    // whose Gram comes from the iteration's Grams (nonlinear, orthonormalised
+    // every iteration); the rare other consumers materialise it
+    ph.zslot = prev_zv ? prev_zslot ^ 1 : 0;
+    if (!fused_dir) materialize_prev_z();
+    if (fused_dir) {
       // one pass: z, ||z||^2, ||HW - W Sigma||^2 and the BB products
       if (need_full || !sig_valid) {
         ghh_fresh = gww_valid && sigma_dual(w, hw);
         if (!ghh_fresh) sigma(w, hw);
         if (!ghh_fresh || E.size > 1) launch_copy_diag(n, E.dmat[4], E.dvec + E.off_sig(), E.s);
       }
+      ph.zv = zfree_env && orth_iter && n_org == 1 && nonlinear && gww_valid && ghh_fresh;
+      if (!ph.zv) {
+        z = pool.get();
+        materialize_prev_z();  // a stored z pairs with a stored previous z
+      }
       const int nb = launch_directions(
           n, E.g.ld, E.g.ngl, P(w), P(hw), history_valid ? P(prev_w) : nullptr,
-          history_valid ? P(prev_z) : nullptr, need_full ? E.dmat[4] : nullptr,
-          E.dvec + E.off_sig(), P(z), E.partials, E.s);
+          history_valid ? (prev_zv ? P(prev_hw) : P(prev_z)) : nullptr,
+          need_full ? E.dmat[4] : nullptr, E.dvec + E.off_sig(), ph.zv ? nullptr : P(z), E.partials,
+          E.s, history_valid && prev_zv ? zsig(prev_zslot) : nullptr,
+          ph.zv ? E.dvec + E.off_zsig(ph.zslot) : nullptr);
+      if (nb < 0 && ph.zv) throw Error(PO_EINVAL, "fused directions unavailable for an implicit z");
+      if (nb < 0) materialize_prev_z();
       if (nb >= 0) {
         E.reduce_rows(E.partials, (history_valid ? 5 : 2) * n, nb, E.g.w, E.dvec + E.off_zz(), true);
         fused = true;
       }
     }
+    if (!z && !ph.zv) z = pool.get();
     if (fused) {
     } else if (full_grad) {
       sigma(w, hw);
@@ -519,6 +561,10 @@ void Solver::enqueue_phase1(int iter) {
     // reads the directions and the trial together; a converged / failing
     // iteration simply discards the speculative trial.
     auto& spec = ph.spec;
+    if (ph.zv && !(orth_iter && fused && gww_valid && ghh_fresh && nonlinear)) {
+      z = materialize_z(w, hw, ph.zslot);  // no fused first trial: write z out
+      ph.zv = false;
+    }
     if (orth_iter && fused && gww_valid && ghh_fresh && nonlinear && E.N <= 48 &&
         tma2d_available()) {
       double* st_tau = E.scal() + Engine::S_TAU;
@@ -530,9 +576,9 @@ void Solver::enqueue_phase1(int iter) {
       spec.wt = pool.get();
       spec.rep = pool.get();
       spec.pre = spool.get();
-      const bool dens = orth_enqueue(E, P(w), P(z), 0.0, P(spec.wt),
+      const bool dens = orth_enqueue(E, P(w), ph.zv ? P(hw) : P(z), 0.0, P(spec.wt),
                                      p.verify_orthonormality != 0, spec.pre.get(), p.hartree,
-                                     p.xc, true, st_tau, &bb);
+                                     p.xc, true, st_tau, &bb, ph.zv ? zsig(ph.zslot) : nullptr);
       spec.tstate = enqueue_state(spec.wt, spec.pre, dens);
       spec.hwt = pool.get();
       E.apply_h(P(spec.wt), P(spec.hwt), spec.tstate->v_local, false);
@@ -556,6 +602,14 @@ bool Solver::step() {
     const bool orth_iter = ph.orth_iter;
     const bool need_full = ph.need_full;
     BRef z = ph.z;
+    bool zv = ph.zv;
+    const int zslot = ph.zslot;
+    auto need_z = [&]() {  // a consumer that reads z itself
+      if (zv) {
+        z = materialize_z(w, hw, zslot);
+        zv = false;
+      }
+    };
     BRef dscratch = ph.dscratch;
     const bool fused = ph.fused;
     auto& spec = ph.spec;
@@ -630,9 +684,12 @@ bool Solver::step() {
       double tau = tau_raw;
       if (last_accepted_tau > 0.0) tau = std::min(tau, 5.0 * last_accepted_tau);
       BRef wn = pool.get();
+      need_z();
       launch_lincomb(E.g, n, P(w), -tau, P(z), P(wn), E.s);
       prev_w = w;
       prev_z = z;
+      prev_zv = false;
+      prev_hw.reset();
       w = wn;
       history_valid = true;
       gww_valid = false;  // a raw step leaves the manifold
@@ -671,9 +728,11 @@ bool Solver::step() {
           rep = pool.get();
           // one device pipeline per trial, one readback (energy + decisions)
           SRef pre = nonlinear ? spool.get() : SRef();
-          const bool dens = orth_enqueue(E, P(w), P(z), -tau, P(wt),
+          const bool g0g = gww_valid && ghh_fresh;
+          if (!(g0g && nonlinear)) need_z();
+          const bool dens = orth_enqueue(E, P(w), zv ? P(hw) : P(z), -tau, P(wt),
                                          p.verify_orthonormality != 0, pre.get(), p.hartree, p.xc,
-                                         gww_valid && ghh_fresh);
+                                         g0g, nullptr, nullptr, zv ? zsig(zslot) : nullptr);
           tstate = enqueue_state(wt, pre, dens);
           hwt = pool.get();
           E.apply_h(P(wt), P(hwt), tstate->v_local, !nonlinear);
@@ -687,6 +746,7 @@ bool Solver::step() {
           te = apply_and_energy(wt, hwt, *tstate);
         } else if (oc == 1) {  // pass-1 Cholesky rejected: symmetric fallback, synchronously
           auto scratch = [&]() -> double* { return P(rep); };
+          need_z();
           if (!orthonormalize_dev(E, P(w), P(z), -tau, P(wt), scratch,
                                   p.verify_orthonormality != 0, orth))
             continue;
@@ -731,6 +791,8 @@ bool Solver::step() {
         history_valid = false;
         prev_w.reset();
         prev_z.reset();
+        prev_hw.reset();
+        prev_zv = false;
         steps_until_orth = 0;
         ++l;
         prefetch_next();
@@ -754,6 +816,9 @@ bool Solver::step() {
       }
       prev_w = w;
       prev_z = z;
+      prev_zv = zv;
+      prev_zslot = zslot;
+      prev_hw = zv ? hw : BRef();
       w = wt;
       state = tstate;
       hw = hwt;
@@ -797,6 +862,8 @@ bool Solver::step() {
         gww_valid = false;
         prev_w.reset();
         prev_z.reset();
+        prev_hw.reset();
+        prev_zv = false;
       }
       recovery_w = w;
       recovery_state = state;

@@ -174,7 +174,8 @@ print(json.dumps([x["energy"] for x in r.records] + [r.energy["total"]]))
 
 def test_launch_and_path_switches_agree(tmp_path):
     """Measurement switches keep the numerics: plain launches instead of
-    programmatic dependent launch (PO_PDL=0) give bitwise the same trajectory;
+    programmatic dependent launch (PO_PDL=0) and stored directions z instead of
+    the implicit z = HW - sigma W (PO_ZFREE=0) give bitwise the same trajectory;
     the split trial rotation (PO_ROT_SPLIT=1: two-source mix + Gram/density
     pass), the 8-warp directions pass (PO_DIR_CW=8), the Poisson check by the CG
     kernel (PO_POISSON_DEFER=0) and a forced CG repair of every line-search
@@ -195,13 +196,14 @@ print(json.dumps([x["energy"] for x in r.records] + [r.energy["total"]]))
     runs = {}
     for name, env_over in [("base", {}), ("nopdl", {"PO_PDL": "0"}), ("split", {"PO_ROT_SPLIT": "1"}),
                            ("dir8", {"PO_DIR_CW": "8"}), ("nodefer", {"PO_POISSON_DEFER": "0"}),
-                           ("repair", {"PO_FORCE_POISSON_REPAIR": "1"})]:
+                           ("repair", {"PO_FORCE_POISSON_REPAIR": "1"}), ("zstored", {"PO_ZFREE": "0"})]:
         env = {k: v for k, v in os.environ.items() if not k.startswith("PO_")}
         env.update(env_over)
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
         assert r.returncode == 0, (name, r.stderr[-2000:])
         runs[name] = json.loads(r.stdout.strip().split("\n")[-1])
     assert runs["nopdl"] == runs["base"]
+    assert runs["zstored"] == runs["base"]
     # the Poisson check in the v_local pass (default) vs the CG verification kernel,
     # and the forced CG repair of every trial's solve (Solver: DST -> CG warm start)
     for name in ("split", "dir8", "nodefer", "repair"):
