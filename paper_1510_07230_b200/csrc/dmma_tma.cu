@@ -787,7 +787,8 @@ __global__ void __launch_bounds__(TTH, 1) mix_tma_kernel(
         }
 #pragma unroll
         for (int ks = 0; ks < 2 * F; ++ks) {
-          if (ks >= ksteps) break;
+          // no runtime trip count: k rows >= N are zero in both operands, and a
+          // data-dependent exit serialised the unrolled k-steps (load, DMMA, branch)
 #pragma unroll
           for (int fi = 0; fi < F; ++fi) {
             if (4 * ks > 8 * fi + 7) continue;
@@ -924,7 +925,6 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
       for (int r = 0; r < (R > 0 ? R : 1); ++r) racc[h][r] = 0.0;
     double eacc[2] = {0.0, 0.0};
     const int nstage = pend > pbeg ? (int)((pend - pbeg + KS - 1) / KS) : 0;
-    const int ksteps = (N + 3) / 4;
     const int c = warp * 8;
     // this lane's fragments of the upper-triangular L^{-T}; with R > 0 the last
     // fragment column (R real orbitals) is a per-lane FMA dot instead of DMMA
@@ -979,7 +979,8 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
         }
 #pragma unroll
         for (int ks = 0; ks < 2 * F; ++ks) {
-          if (ks >= ksteps) break;
+          // no runtime trip count: k rows >= N are zero in both operands, and a
+          // data-dependent exit serialised the unrolled k-steps (load, DMMA, branch)
 #pragma unroll
           for (int fi = 0; fi < FD; ++fi) {
             if (4 * ks > 8 * fi + 7) continue;
@@ -1271,7 +1272,6 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
 #pragma unroll
       for (int fi = 0; fi < F; ++fi) nrm[q][fi][0] = nrm[q][fi][1] = 0.0;
     const int nstage = pend > pbeg ? (int)((pend - pbeg + KS - 1) / KS) : 0;
-    const int ksteps = (N + 3) / 4;
     const int c = warp * 8;
     for (int st = 0; st < nstage; ++st) {
       const int s = st % nst;
@@ -1301,7 +1301,8 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
         for (int f = 0; f < F; ++f) acc2[f][0] = acc2[f][1] = 0.0;
 #pragma unroll
         for (int ks = 0; ks < 2 * F; ++ks) {
-          if (ks >= ksteps) break;
+          // no runtime trip count: k rows >= N are zero in both operands, and a
+          // data-dependent exit serialised the unrolled k-steps (load, DMMA, branch)
           const int krow = 4 * ks + t4;
           const double av = krow < N ? sbuf[(krow) * PW + c + gq] : 0.0;
 #pragma unroll
