@@ -392,10 +392,22 @@ __global__ void __launch_bounds__(TR * 32) cholesky_inv_gs_kernel(int N, const d
   if constexpr (TRIAL) {
     __shared__ double tau_s;
     if (ta.has_bb) {  // the BB step of this iteration (one thread, the host mirror's order)
+      // the four rows are staged in shared memory by the whole CTA first: the
+      // serial sums then no longer wait on one global load per term
+      __shared__ double bbv[4][NMAX];
+      const BBArgs& q = ta.bb;
+      for (int i = threadIdx.x; i < q.N; i += TR * 32) {
+        bbv[0][i] = q.zz[i];
+        if (q.history) {
+          bbv[1][i] = q.ss[i];
+          bbv[2][i] = q.sy[i];
+          bbv[3][i] = q.yy[i];
+        }
+      }
+      __syncthreads();
       if (threadIdx.x == 0) {
-        const BBArgs& q = ta.bb;
-        bb_tau_compute(q.N, q.zz, q.ss, q.sy, q.yy, q.history, q.use_bb1, q.trace_abs_diag, q.tau_min,
-                       q.tau_max, q.out);
+        bb_tau_compute(q.N, bbv[0], bbv[1], bbv[2], bbv[3], q.history, q.use_bb1, q.trace_abs_diag,
+                       q.tau_min, q.tau_max, q.out);
         tau_s = q.out[0];
       }
       __syncthreads();
