@@ -359,10 +359,11 @@ def ours(args, spec):
     if N <= 48:  # the small-N fused passes of the C2 step
         e.enqueue("gram", a=hw_b, b=cur)
         d_ms = time_kernel(torch, native, e, "directions", 10, a=cur, b=hw_b, out=z_b)
-        add_kernel("directions_tma_kernel (z, ||D||^2, BB)", d_ms, 5 * blk, 2.0 * N * N * ng)
+        # implicit z (the iteration's form): reads W, HW, W_prev, HW_prev, writes nothing
+        add_kernel("directions_tma_kernel (||z||^2, ||D||^2, BB)", d_ms, 4 * blk, 2.0 * N * N * ng)
         e.enqueue("gram_sym", a=cur)
         e.enqueue("cholesky")
-        r_ms = time_kernel(torch, native, e, "rotation_fused", 10, a=cur, b=z_b, out=scratch)
+        r_ms = time_kernel(torch, native, e, "rotation_fused", 10, a=cur, b=hw_b, out=scratch)
         add_kernel("rotate_fused_kernel (rotation + G2 + density)", r_ms, 3 * blk,
                    2.0 * N * (N + 1) * ng)
     else:

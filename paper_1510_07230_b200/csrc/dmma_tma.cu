@@ -1273,6 +1273,21 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
       for (int fi = 0; fi < F; ++fi) nrm[q][fi][0] = nrm[q][fi][1] = 0.0;
     const int nstage = pend > pbeg ? (int)((pend - pbeg + KS - 1) / KS) : 0;
     const int c = warp * 8;
+    // lanes t4 = 2, 3 visit their pair of orbitals swapped: rows 2 t4 + j'
+    // then differ mod 4 across the half-warp (PW = 4 mod 16, conflict-free);
+    // slot j of nrm holds orbital 8 fi + 2 t4 + (j ^ jx)
+    const int jx = t4 >> 1;
+    // this lane's -sigma values in registers (the ring waits clobber memory,
+    // so shared-memory copies would be re-read every stage)
+    double msr[F][2], mpr[ZM == 2 ? F : 1][2];
+#pragma unroll
+    for (int fi = 0; fi < F; ++fi)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int i = 8 * fi + 2 * t4 + (j ^ jx);
+        msr[fi][j] = msig[i];
+        if constexpr (ZM == 2) mpr[fi][j] = mpsig[i];
+      }
     for (int st = 0; st < nstage; ++st) {
       const int s = st % nst;
       mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
@@ -1319,10 +1334,6 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
           acc[f][1] += acc2[f][1];
         }
       }
-      // lanes t4 = 2, 3 visit their pair of orbitals swapped: rows 2 t4 + j'
-      // then differ mod 4 across the half-warp (PW = 4 mod 16, conflict-free);
-      // slot j of nrm holds orbital 8 fi + 2 t4 + (j ^ jx)
-      const int jx = t4 >> 1;
 #pragma unroll
       for (int fi = 0; fi < F; ++fi)
 #pragma unroll
@@ -1338,13 +1349,13 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
             }
             // z = HW - sigma W (one FMA; rotate_fused and the previous-z term
             // below rebuild exactly this value when z is not stored, Z == null)
-            const double z = fma(msig[i], wv, hv);
+            const double z = fma(msr[fi][j], wv, hv);
             if constexpr (ZM == 0) Z[(int64_t)i * ld + p] = z;
             nrm[0][fi][j] += z * z;
             if constexpr (HIST) {
               const double wp = LDGH ? wpv[fi][j] : sbuf[2 * qstride + off];
               double zp = LDGH ? zpv[fi][j] : sbuf[3 * qstride + off];
-              if constexpr (ZM == 2) zp = fma(mpsig[i], wp, zp);  // source 3 is the previous HW
+              if constexpr (ZM == 2) zp = fma(mpr[ZM == 2 ? fi : 0][j], wp, zp);  // source 3: previous HW
               const double sv = wv - wp;
               const double yv = z - zp;
               nrm[2][fi][j] += sv * sv;

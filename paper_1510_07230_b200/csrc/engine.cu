@@ -888,14 +888,21 @@ extern "C" int po_enqueue(po_engine* h, int op, int a, int b, int out) {
                      E.blk(out), nullptr, E.s);
       break;
     case PO_OP_ROTATION_FUSED:
+      // the iteration's form: b is HW and z = HW - sigma W is implicit (sigma row:
+      // dvec), rho and 4 pi rho only (v_xc and the energies belong to v_local)
       if (po::launch_rotate_fused(E.N, E.g.ld, E.g.ngl, E.blk(a), E.blk(b), -0.3, E.dmat[1],
-                                  E.blk(out), E.gram_ws, E.dmat[2], E.g.w, E.occ, 1, st->rho,
-                                  st->v_xc, E.density_b_target(1), E.v_ext, E.partials, E.s) < 0)
+                                  E.blk(out), E.gram_ws, E.dmat[2], E.g.w, E.occ, -1, st->rho,
+                                  st->v_xc, E.density_b_target(1), E.v_ext, E.partials, E.s,
+                                  nullptr, E.dvec + E.off_sig()) < 0)
         throw Error(PO_EINVAL, "fused rotation unavailable for this N");
       break;
     case PO_OP_DIRECTIONS:
+      // the iteration's form: z implicit (not stored), previous z from the previous
+      // HW (here b again) and sigma row; out is not written
+      (void)out;
       if (po::launch_directions(E.N, E.g.ld, E.g.ngl, E.blk(a), E.blk(b), E.blk(a), E.blk(b),
-                                E.dmat[0], E.dvec, E.blk(out), E.partials, E.s) < 0)
+                                E.dmat[0], E.dvec, nullptr, E.partials, E.s, E.dvec,
+                                E.dvec + E.off_zsig(0)) < 0)
         throw Error(PO_EINVAL, "directions kernel unavailable for this N");
       break;
     default:

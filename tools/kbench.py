@@ -70,7 +70,7 @@ tri, full = N * (N + 1) * ng, 2 * N * N * ng
 flops = {"gram_sym(G2)": tri, "gram_trial(G0)": tri, "gram_nonsym(Sigma)": full, "rotation": tri,
          "mix_upper": tri, "mix_full": full, "rotation_fused": 2 * tri}
 bytes_ = {"hamiltonian": 2 * blk, "gram_sym(G2)": blk, "gram_trial(G0)": 2 * blk,
-          "gram_nonsym(Sigma)": 2 * blk, "rotation": 3 * blk, "rotation_fused": 3 * blk, "directions": 5 * blk,
+          "gram_nonsym(Sigma)": 2 * blk, "rotation": 3 * blk, "rotation_fused": 3 * blk, "directions": 4 * blk,
           "density_xc": blk, "mix_upper": 2 * blk, "mix_full": 2 * blk}
 for k, v in res.items():
     frac = f"{bytes_[k] / v / 1e3 / hbm:.2f} of HBM" if k in bytes_ else ""
