@@ -887,9 +887,11 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
   const int NB = N;  // box rows: no zero-filled padding rows in the stream
   const size_t qstride = ((size_t)NB * PW + 15) & ~(size_t)15;
   const size_t sdoubles = (size_t)nsrc * qstride;
-  double* Ms = stage0 + (size_t)nst * sdoubles;  // [NPAD][NPAD]
-  for (int e = threadIdx.x; e < NPAD * NPAD; e += NT) {
-    const int k = e / NPAD, i = e % NPAD;
+  // L^{-T} rows padded to MST = 4 mod 16 doubles (conflict-free fragment reads)
+  constexpr int MST = NPAD + 4;
+  double* Ms = stage0 + (size_t)nst * sdoubles;  // [NPAD][MST]
+  for (int e = threadIdx.x; e < NPAD * MST; e += NT) {
+    const int k = e / MST, i = e % MST;
     Ms[e] = (k < N && i < N) ? M[(int64_t)k * N + i] : 0.0;
   }
   if (threadIdx.x == 0) {
@@ -935,14 +937,14 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
       for (int ks = 0; ks < 2 * F; ++ks)
 #pragma unroll
         for (int fi = 0; fi < F; ++fi)
-          mreg[ks][fi] = 4 * ks > 8 * fi + 7 ? 0.0 : Ms[(4 * ks + t4) * NPAD + 8 * fi + gq];
+          mreg[ks][fi] = 4 * ks > 8 * fi + 7 ? 0.0 : Ms[(4 * ks + t4) * MST + 8 * fi + gq];
     }
     double mrem[R > 0 ? R : 1][2 * F];
 #pragma unroll
     for (int r = 0; r < (R > 0 ? R : 1); ++r)
 #pragma unroll
       for (int ks = 0; ks < 2 * F; ++ks)
-        mrem[r][ks] = (R > 0 && 4 * ks + t4 < N) ? Ms[(4 * ks + t4) * NPAD + 8 * FD + r] : 0.0;
+        mrem[r][ks] = (R > 0 && 4 * ks + t4 < N) ? Ms[(4 * ks + t4) * MST + 8 * FD + r] : 0.0;
     // zsig: the second source is HW and the direction z = HW - sigma W is rebuilt
     // here with the directions pass's FMA (bitwise the value it would have stored)
     double mz[ZV ? 2 * F : 1];
@@ -987,7 +989,7 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
             if constexpr (MREG)
               dmma_8x8x4(acc[fi], av[ks], mreg[ks][fi]);
             else
-              dmma_8x8x4(acc[fi], av[ks], Ms[(4 * ks + t4) * NPAD + 8 * fi + gq]);
+              dmma_8x8x4(acc[fi], av[ks], Ms[(4 * ks + t4) * MST + 8 * fi + gq]);
           }
         }
         if constexpr (R > 0) {  // out_rr(point c + gq) = sum_k A_k M(k, rr), k split over t4
@@ -1160,7 +1162,7 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
   if (Ab && !make_map(&maps.m[nsrc++], Ab, ld, N, N, PW)) return -1;
   const int fd = R ? F - 1 : F;
   const size_t red = (size_t)CW * (fd * (fd + 1) / 2) * 64 + (size_t)CW * 2 * 2 * 32 + 2 * CW;
-  const size_t extra = (size_t)NPAD * NPAD;
+  const size_t extra = (size_t)NPAD * (NPAD + 4);
   // ring: stages of KS points, padded rows; tail for fragment rows past N
   const size_t qs = ((size_t)N * PW + 15) & ~(size_t)15;
   const size_t sd = (size_t)nsrc * qs;
