@@ -220,6 +220,9 @@ __global__ void __launch_bounds__(AW * 32) dst_axis0_kernel(const double* __rest
 #pragma unroll
     for (int b = 0; b < CB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int nks = (n0 + 3) / 4;
+  // unrolled by 4: the S / X fragment loads of later k-steps issue ahead of the
+  // DMMAs (a k-step at a time exposed the L1 / shared-memory latency)
+#pragma unroll 4
   for (int ks = 0; ks < nks; ++ks) {
     const int k = 4 * ks + t4;
     double af[RB], bf[CB];
