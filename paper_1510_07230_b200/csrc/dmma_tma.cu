@@ -1407,7 +1407,12 @@ int launch_directions_fdh(const double* W, const double* HW, int N, int64_t ld, 
   static const int cw_env = getenv("PO_DIR_CW") ? atoi(getenv("PO_DIR_CW")) : 0;
   const int nsrc = HIST && !ldgh ? 4 : 2;
   const int zm = Z ? 0 : (HIST && psig ? 2 : 1);
-  const int CW = zm == 0 && cw_env >= 4 && cw_env <= 8 && cw_env != 7 ? cw_env : (nsrc == 4 ? 6 : 8);
+  // implicit z (zm = 2, no stores): eight consumer warps with a two-deep ring
+  // measured 173 vs 197 us for six warps / three stages at C2 (PO_DIR_CW=6 compares)
+  // (F <= 5: two stages of the four sources fit shared memory)
+  const int CW = zm == 2 ? (cw_env == 6 || F > 5 ? 6 : 8)
+                         : zm == 0 && cw_env >= 4 && cw_env <= 8 && cw_env != 7 ? cw_env
+                                                                                 : (nsrc == 4 ? 6 : 8);
   const int KS = 8 * CW, PW = CW == 8 ? PADW : KS + 4;
   const size_t extra = (size_t)NPAD * (NPAD + 4) + 2 * NPAD + (size_t)CW * NQ * NPAD;
   const size_t sd = (size_t)nsrc * (((size_t)N * PW + 15) & ~(size_t)15);
@@ -1428,7 +1433,8 @@ int launch_directions_fdh(const double* W, const double* HW, int N, int64_t ld, 
   ::po::count_launch();
   auto k = zm == 1   ? (HIST ? directions_tma_kernel<F, DD, HIST, false, 6, 1>
                                : directions_tma_kernel<F, DD, HIST, false, 8, 1>)
-           : zm == 2 ? directions_tma_kernel<F, DD, HIST, false, 6, 2>
+           : zm == 2 ? (CW == 8 ? directions_tma_kernel<F, DD, HIST, false, 8, 2>
+                                : directions_tma_kernel<F, DD, HIST, false, 6, 2>)
            : CW == 8 ? directions_tma_kernel<F, DD, HIST, false, 8>
            : CW == 6 ? directions_tma_kernel<F, DD, HIST, false, 6>
            : CW == 5 ? directions_tma_kernel<F, DD, HIST, false, 5>

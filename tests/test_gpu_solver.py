@@ -174,8 +174,10 @@ print(json.dumps([x["energy"] for x in r.records] + [r.energy["total"]]))
 
 def test_launch_and_path_switches_agree(tmp_path):
     """Measurement switches keep the numerics: plain launches instead of
-    programmatic dependent launch (PO_PDL=0) and stored directions z instead of
-    the implicit z = HW - sigma W (PO_ZFREE=0) give bitwise the same trajectory;
+    programmatic dependent launch (PO_PDL=0) give bitwise the same trajectory;
+    stored directions z instead of the implicit z = HW - sigma W (PO_ZFREE=0: z is
+    bitwise the same, the directions pass then runs 6 instead of 8 warps, so its
+    per-orbital sums are reduced in another order) agree to round-off, as do
     the split trial rotation (PO_ROT_SPLIT=1: two-source mix + Gram/density
     pass), the 8-warp directions pass (PO_DIR_CW=8), the Poisson check by the CG
     kernel (PO_POISSON_DEFER=0) and a forced CG repair of every line-search
@@ -203,9 +205,8 @@ print(json.dumps([x["energy"] for x in r.records] + [r.energy["total"]]))
         assert r.returncode == 0, (name, r.stderr[-2000:])
         runs[name] = json.loads(r.stdout.strip().split("\n")[-1])
     assert runs["nopdl"] == runs["base"]
-    assert runs["zstored"] == runs["base"]
     # the Poisson check in the v_local pass (default) vs the CG verification kernel,
     # and the forced CG repair of every trial's solve (Solver: DST -> CG warm start)
-    for name in ("split", "dir8", "nodefer", "repair"):
+    for name in ("split", "dir8", "nodefer", "repair", "zstored"):
         assert len(runs[name]) == len(runs["base"])
         assert max(abs(x - y) for x, y in zip(runs[name], runs["base"])) < 1e-9, name
