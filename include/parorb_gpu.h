@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define PO_ABI_VERSION 1
+#define PO_ABI_VERSION 2  /* 2: po_result gained checkpoints / drift_iterations; po_stiefel_gradient_d */
 
 enum po_status {
   PO_OK = 0,
@@ -162,6 +162,10 @@ int po_diagonal_residuals(po_engine* e, int u, int hu, int z, double* sigma_diag
 /* manifold.cpp:181-202 stiefel_gradient: sigma = <(HU)^T U> and, per orbital,
  * <D_i, D_i> with D = HU - U Sigma. PO_EINVAL if max|Sigma - Sigma^T| > 1e-10. */
 int po_stiefel_gradient(po_engine* e, int u, int hu, double* sigma_host, double* d_norm2);
+/* The same with the gradient block itself (StiefelGradient::directions,
+ * manifold.hpp:47-54): D = HU - U Sigma written to block d (d != u, hu). */
+int po_stiefel_gradient_d(po_engine* e, int u, int hu, int d, double* sigma_host,
+                          double* d_norm2);
 /* manifold.cpp:218-247 subspace_rotate: gamma ascending, P (row-major) with the
  * sign rule, w <- W P in place. */
 int po_subspace_rotate(po_engine* e, int w, const double* sigma_host, double* gamma,
@@ -223,6 +227,16 @@ typedef struct {
   double final_grad_norm;
   double wall_seconds, par_seconds, sync_seconds;
   char message[200];
+  /* SolveResult::checkpoints (optimizer.hpp:87-93, filled at optimizer.cpp:535-538):
+   * one row per accepted orthogonalization step, cap x 5 = level, iter,
+   * offdiag_max, diag_deviation_max, orth_deviation (-1 when not measured);
+   * NULL to skip. n_checkpoints counts every step (rows beyond cap dropped). */
+  double* checkpoints;
+  int n_checkpoints;
+  /* SolveResult::drift_iterations (optimizer.cpp:539: offdiag_max > 0.5), cap
+   * entries or NULL; n_drift counts every flag. */
+  int* drift_iterations;
+  int n_drift;
 } po_result;
 
 void po_default_params(po_params* p);

@@ -2,10 +2,13 @@
 // Builds a Problem with the UNMODIFIED reference library, starts from the
 // reference's testing::random_orthonormal, runs parorb::opt_par_mod_inner
 // (CPU reference) and parorb::gpu::opt_par_mod_inner (this repo, via the C
-// ABI) and compares the IterationRecord energies. Exit 0 iff every iteration
-// agrees within 1e-6 Ha. Built by oracle/Makefile (target dropin) because it
+// ABI) and compares the IterationRecord energies, the orthogonalization
+// checkpoints, the drift flags and the phase-time coverage. Exit 0 iff every
+// iteration agrees within 1e-6 Ha and the SolveResult fields the reference's
+// acceptance suite reads agree too. Built by oracle/Makefile (target dropin) because it
 // links the reference; the binary is test infrastructure.
 //   dropin_demo [n_points=16] [n_orbitals=4] [iterations=12]
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -49,8 +52,40 @@ int main(int argc, char** argv) {
                 cpu.records[k].level, cpu.records[k].iter, cpu.records[k].energy, gpu.records[k].energy, d,
                 cpu.records[k].backtracks, gpu.records[k].backtracks);
   }
+  // SolveResult::checkpoints / drift_iterations / par+sync (optimizer.cpp:535-539,
+  // 594-595), as the reference's acceptance suite reads them: criterion 4
+  // (acceptance.cpp:152-160, orth_deviation <= 1e-10 at every step), criterion 6
+  // (:254-263, the last 10 checkpoints near the identity) and the phase coverage of
+  // criterion 8 (:323-335, par + sync within 1% of the wall time).
+  bool ck_ok = cpu.checkpoints.size() == gpu.checkpoints.size() &&
+               cpu.drift_iterations == gpu.drift_iterations;
+  double ck_diff = 0.0, worst_orth = 0.0;
+  for (std::size_t k = 0; ck_ok && k < gpu.checkpoints.size(); ++k) {
+    const OrthCheckpoint &a = cpu.checkpoints[k], &b = gpu.checkpoints[k];
+    ck_ok = ck_ok && a.level == b.level && a.iter == b.iter &&
+            (a.orth_deviation < 0) == (b.orth_deviation < 0);
+    ck_diff = std::max({ck_diff, std::abs(a.offdiag_max - b.offdiag_max),
+                        std::abs(a.diag_deviation_max - b.diag_deviation_max)});
+    worst_orth = std::max(worst_orth, b.orth_deviation);
+  }
+  ck_ok = ck_ok && ck_diff < 1e-8 && worst_orth <= 1e-10;
+  const std::size_t m_ck = gpu.checkpoints.size();
+  double off10 = 0.0, diag10 = 0.0;
+  for (std::size_t k = m_ck >= 10 ? m_ck - 10 : 0; k < m_ck; ++k) {
+    off10 = std::max(off10, gpu.checkpoints[k].offdiag_max);
+    diag10 = std::max(diag10, gpu.checkpoints[k].diag_deviation_max);
+  }
+  const bool crit6 = m_ck < 10 || (off10 < 0.1 && diag10 < 0.1);
+  const double coverage = (gpu.par_seconds + gpu.sync_seconds) / gpu.wall_seconds;
+  const double par_frac = gpu.par_seconds / (gpu.par_seconds + gpu.sync_seconds);
+  std::printf("checkpoints %zu/%zu max|d stats| %.2e worst orth_dev %.2e drift %zu/%zu  "
+              "final-10 offdiag %.3e diag %.3e  par %.4f s sync %.4f s coverage %.4f par_frac %.3f\n",
+              cpu.checkpoints.size(), gpu.checkpoints.size(), ck_diff, worst_orth,
+              cpu.drift_iterations.size(), gpu.drift_iterations.size(), off10, diag10,
+              gpu.par_seconds, gpu.sync_seconds, coverage, par_frac);
   const bool ok = cpu.records.size() == gpu.records.size() && worst < 1e-6 &&
-                  std::abs(cpu.energy.total - gpu.energy.total) < 1e-6;
+                  std::abs(cpu.energy.total - gpu.energy.total) < 1e-6 && ck_ok && crit6 &&
+                  std::abs(coverage - 1.0) <= 0.01;
   std::printf("records %zu/%zu  final E_ref %.15f  E_gpu %.15f  max|dE| %.3e  wall ref %.3f s gpu %.3f s  %s\n",
               cpu.records.size(), gpu.records.size(), cpu.energy.total, gpu.energy.total, worst,
               cpu.wall_seconds, gpu.wall_seconds, ok ? "OK" : "MISMATCH");

@@ -72,9 +72,27 @@ inline po_params to_params(const OptimizerParams& p, Algorithm alg, const Proble
   return q;
 }
 
+// Host-side output arrays of one po_result (records, accepted steps,
+// checkpoints, drift flags), sized for `cap` rows.
+struct ResultBuffers {
+  std::vector<po_record> recs;
+  std::vector<double> acc, ckpt;
+  std::vector<int> drift;
+  po_result r{};
+  explicit ResultBuffers(std::size_t cap) : recs(cap), acc(9 * cap), ckpt(5 * cap), drift(cap) {
+    r.cap = static_cast<int>(cap);
+    r.records = recs.data();
+    r.accepted = acc.data();
+    r.checkpoints = ckpt.data();
+    r.drift_iterations = drift.data();
+  }
+};
+
 // po_result -> the reference's SolveResult fields (optimizer.hpp:98-112)
-inline void fill_result(SolveResult& out, const po_result& r, const std::vector<po_record>& recs,
-                        const std::vector<double>& acc) {
+inline void fill_result(SolveResult& out, const ResultBuffers& b) {
+  const po_result& r = b.r;
+  const std::vector<po_record>& recs = b.recs;
+  const std::vector<double>& acc = b.acc;
   out.energy = EnergyBreakdown{r.e_kinetic, r.e_external, r.e_hartree, r.e_xc, r.e_total};
   out.outcome = static_cast<SolveOutcome>(r.outcome);  // same enumerator order
   out.message = r.message;
@@ -89,9 +107,18 @@ inline void fill_result(SolveResult& out, const po_result& r, const std::vector<
     out.accepted_steps.push_back(AcceptedStep{static_cast<int>(a[0]), static_cast<int>(a[1]), a[2],
                                               a[3], a[4], a[5], a[6], a[7], a[8]});
   }
+  // OrthCheckpoint per orthogonalization step and the drift flags (optimizer.cpp:535-539)
+  for (int k = 0; k < r.n_checkpoints && k < r.cap; ++k) {
+    const double* c = b.ckpt.data() + 5 * k;
+    out.checkpoints.push_back(
+        OrthCheckpoint{static_cast<int>(c[0]), static_cast<int>(c[1]), c[2], c[3], c[4]});
+  }
+  for (int k = 0; k < r.n_drift && k < r.cap; ++k) out.drift_iterations.push_back(b.drift[k]);
   out.iterations_total = static_cast<int>(out.records.size());
   out.final_grad_norm = r.final_grad_norm;
   out.wall_seconds = r.wall_seconds;
+  out.par_seconds = r.par_seconds;  // PhaseTimer buckets (optimizer.cpp:594-595)
+  out.sync_seconds = r.sync_seconds;
 }
 
 inline SolveResult run(const OrbitalSet& u0, const Problem& prob, const OptimizerParams& params,
@@ -114,14 +141,10 @@ inline SolveResult run(const OrbitalSet& u0, const Problem& prob, const Optimize
   for (int i = 0; i < u0.n(); ++i)
     std::memcpy(host.data() + i * ng, u0.orbitals[i].values.data(), sizeof(double) * ng);
   const po_params q = to_params(params, alg, prob);
-  std::vector<po_record> recs(static_cast<std::size_t>(q.max_inner) + 1);
-  std::vector<double> acc(9 * recs.size());
-  po_result r{};
-  r.cap = static_cast<int>(recs.size());
-  r.records = recs.data();
-  r.accepted = acc.data();
+  ResultBuffers rb(static_cast<std::size_t>(q.max_inner) + 1);
   // upload, InnerLoop, finalize with the final download overlapped: one call
-  check(po_solve_host(raw, &q, host.data(), host.data(), &r), raw);
+  // (pageable std::vector memory: po_solve_host stages it through pinned chunks)
+  check(po_solve_host(raw, &q, host.data(), host.data(), &rb.r), raw);
 
   SolveResult out;  // optimizer.hpp:98-112
   std::vector<Field> fields;
@@ -131,7 +154,7 @@ inline SolveResult run(const OrbitalSet& u0, const Problem& prob, const Optimize
     fields.push_back(std::move(f));
   }
   out.orbitals = OrbitalSet{std::move(fields)};
-  fill_result(out, r, recs, acc);
+  fill_result(out, rb);
   return out;
 }
 
@@ -165,16 +188,11 @@ inline SolveResult solve(const Problem& level0, const OptimizerParams& params) {
                                at.softening});
   }
   const po_params q = detail::to_params(params, params.algorithm, level0);
-  std::vector<po_record> recs(static_cast<std::size_t>(q.max_inner) * q.outer_levels + 1);
-  std::vector<double> acc(9 * recs.size());
-  po_result r{};
-  r.cap = static_cast<int>(recs.size());
-  r.records = recs.data();
-  r.accepted = acc.data();
+  detail::ResultBuffers rb(static_cast<std::size_t>(q.max_inner) * q.outer_levels + 1);
   po_engine* raw = nullptr;
   int w = -1;
   const int rc = po_solve_levels(&gd, level0.n_orbitals, 1.0, atoms.data(),
-                                 static_cast<int>(level0.atoms.size()), &q, &r, &raw, &w);
+                                 static_cast<int>(level0.atoms.size()), &q, &rb.r, &raw, &w);
   std::unique_ptr<po_engine, detail::EngineDeleter> e(raw);
   detail::check(rc, raw);
   // the final grid: refine_uniform applied outer_levels - 1 times (grid.cpp:137-149)
@@ -191,7 +209,7 @@ inline SolveResult solve(const Problem& level0, const OptimizerParams& params) {
     fields.push_back(std::move(f));
   }
   out.orbitals = OrbitalSet{std::move(fields)};
-  detail::fill_result(out, r, recs, acc);
+  detail::fill_result(out, rb);
   return out;
 }
 

@@ -7,7 +7,11 @@
 //   trace_ref solve <spec.json> <outdir>   run opt_par_inner / opt_par_mod_inner /
 //                                           optm_qr_solve (optimizer.hpp:153-161)
 //   trace_ref ops   <spec.json> <outdir>   one evaluation of every hot-path
-//                                           operator on the start block
+//                                           operator on the start block (full
+//                                           arrays, or reduced with "sketch")
+//   trace_ref orth  <spec.json> <outdir>   orthonormalize_with_gram of the start
+//   trace_ref levels / prolong             solve (optimizer.cpp:638-669) /
+//                                           refine_uniform + prolongate
 //
 // Spec keys: n[3], extent[3], atoms[[x,y,z,Z,a]...], n_orbitals, hartree, xc,
 // start{kind: random_orthonormal|initialize|file, seed, path}, algorithm,
@@ -19,6 +23,7 @@
 #include <cstdio>
 #include <fstream>
 #include <iostream>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -77,12 +82,105 @@ std::vector<double> read_bin(const std::string& path) {
   return v;
 }
 
+// ---- size-independent fingerprints of large blocks (C3 / C4-grid fixtures)
+//
+// A block B (N x N_g, orbital-major) is reduced to
+//   S = sqrt(w) * B X          (N x m), X(p, a) = +-1 Rademacher signs from a
+//                               splitmix64 hash of (seed, p * m + a)
+//   rows at K sampled points    p_j = (j * 2654435761) mod N_g
+// The sign rule is restated bit-for-bit in tests/helpers.py (sketch_signs).
+// For two orthonormal sets, X^T P X = S^T G^-1 S, so the off-diagonal entries
+// of the difference of the two m x m matrices estimate ||P1 - P2||_F without
+// either side holding the other's block (tests/helpers.py:sketch_projector_distance).
+struct Sketch {
+  int m = 0;
+  std::uint64_t seed = 0;
+  int samples = 0;
+};
+
+inline double sketch_sign(std::uint64_t seed, std::uint64_t key) {
+  std::uint64_t z = seed ^ (key * 0xD1B54A32D192ED03ull);
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return (z >> 63) ? -1.0 : 1.0;
+}
+
+std::vector<double> sketch_block(const FieldSet& s, const Sketch& k, double weight) {
+  const std::size_t n = s.size();
+  const std::size_t ng = s.empty() ? 0 : s[0].values.size();
+  const std::size_t m = static_cast<std::size_t>(k.m);
+  std::vector<double> out(n * m, 0.0);
+  const std::size_t chunk = 2048;
+  std::vector<double> x(chunk * m);
+  for (std::size_t p0 = 0; p0 < ng; p0 += chunk) {
+    const std::size_t np = std::min(chunk, ng - p0);
+    for (std::size_t p = 0; p < np; ++p)
+      for (std::size_t a = 0; a < m; ++a) x[p * m + a] = sketch_sign(k.seed, (p0 + p) * m + a);
+    std::vector<std::thread> pool;
+    const std::size_t nt = std::max<std::size_t>(1, std::min<std::size_t>(n, 8));
+    for (std::size_t t = 0; t < nt; ++t) {
+      pool.emplace_back([&, t] {
+        for (std::size_t i = t; i < n; i += nt) {
+          const double* u = s[i].values.data() + p0;
+          double* o = out.data() + i * m;
+          for (std::size_t p = 0; p < np; ++p) {
+            const double v = u[p];
+            const double* xr = x.data() + p * m;
+            for (std::size_t a = 0; a < m; ++a) o[a] += v * xr[a];
+          }
+        }
+      });
+    }
+    for (auto& th : pool) th.join();
+  }
+  const double sw = std::sqrt(weight);
+  for (double& v : out) v *= sw;
+  return out;
+}
+
+std::vector<std::int64_t> sample_points(std::int64_t ng, int k) {
+  std::vector<std::int64_t> p(static_cast<std::size_t>(k));
+  for (int j = 0; j < k; ++j)
+    p[static_cast<std::size_t>(j)] =
+        static_cast<std::int64_t>((static_cast<unsigned __int128>(j) * 2654435761ull) % ng);
+  return p;
+}
+
+std::vector<double> sample_block(const FieldSet& s, const std::vector<std::int64_t>& pts) {
+  std::vector<double> out;
+  out.reserve(s.size() * pts.size());
+  for (const Field& f : s)
+    for (std::int64_t p : pts) out.push_back(f.values[static_cast<std::size_t>(p)]);
+  return out;
+}
+
+std::vector<double> sample_field(const Field& f, const std::vector<std::int64_t>& pts) {
+  std::vector<double> out;
+  for (std::int64_t p : pts) out.push_back(f.values[static_cast<std::size_t>(p)]);
+  return out;
+}
+
+// sum and sum of squares of a field, long double accumulation (fixture norms)
+std::vector<double> field_norms(const Field& f) {
+  long double s = 0.0L, q = 0.0L;
+  for (double v : f.values) {
+    s += v;
+    q += static_cast<long double>(v) * v;
+  }
+  return {static_cast<double>(s), static_cast<double>(q)};
+}
+
 struct Setup {
   Problem problem;
   OrbitalSet u0;
   OptimizerParams params;
   std::string algorithm = "opt_par";
   int threads = 1;
+  Sketch sketch;
+  bool write_final_w = true;
 };
 
 Setup load(const std::string& spec_path) {
@@ -158,6 +256,13 @@ Setup load(const std::string& spec_path) {
                                                : ConvergenceMode::kGradNorm;
   s.algorithm = j.value("algorithm", "opt_par");
   s.threads = j.value("threads", 1);
+  if (j.contains("sketch")) {
+    const json& k = j["sketch"];
+    s.sketch.m = k.value("m", 64);
+    s.sketch.seed = k.value("seed", 7ull);
+    s.sketch.samples = k.value("samples", 1024);
+  }
+  s.write_final_w = j.value("write_final_w", true);
   return s;
 }
 
@@ -213,7 +318,7 @@ int cmd_solve(const Setup& s, const std::string& out) {
       f << buf;
     }
   }
-  write_set(out + "/final_w.bin", r.orbitals.orbitals);
+  if (s.write_final_w) write_set(out + "/final_w.bin", r.orbitals.orbitals);
   // Orbital eigenvalues at the final iterate: eig(Sigma), Sigma = <(HW)^T W>.
   HamiltonianState st = build_hamiltonian(r.orbitals, s.problem);
   FieldSet hw = apply_hamiltonian(st, r.orbitals, ex);
@@ -222,6 +327,11 @@ int cmd_solve(const Setup& s, const std::string& out) {
   std::vector<double> gam(static_cast<std::size_t>(rot.gamma.size()));
   for (std::size_t i = 0; i < gam.size(); ++i) gam[i] = rot.gamma(static_cast<Eigen::Index>(i));
   write_vec(out + "/final_eig.bin", gam);
+  if (s.sketch.m > 0) {
+    const double wq = r.orbitals.grid().quadrature_weight();
+    write_vec(out + "/final_sketch.bin", sketch_block(r.orbitals.orbitals, s.sketch, wq));
+    write_mat(out + "/final_gram.bin", gram(r.orbitals, r.orbitals));
+  }
 
   json sum{{"outcome", outcome_name(r.outcome)},
            {"message", r.message},
@@ -241,16 +351,34 @@ int cmd_solve(const Setup& s, const std::string& out) {
 int cmd_ops(const Setup& s, const std::string& out) {
   Executor ex(s.threads);
   const OrbitalSet& w = s.u0;
-  write_set(out + "/u0.bin", w.orbitals);
-  write_field(out + "/v_ext.bin", s.problem.v_ext);
+  const double wq = w.grid().quadrature_weight();
+  // Full arrays, or (s.sketch.m > 0) the reduced fingerprints for shapes whose
+  // blocks are too large to commit (C3, the C4 grid): fields at sampled points
+  // + sum / sum of squares, blocks as sampled rows + a Rademacher sketch.
+  const bool reduced = s.sketch.m > 0;
+  const std::vector<std::int64_t> pts =
+      reduced ? sample_points(w.grid().num_points(), s.sketch.samples) : std::vector<std::int64_t>{};
+  auto put_field = [&](const std::string& name, const Field& f) {
+    if (!reduced) return write_field(out + "/" + name + ".bin", f);
+    write_vec(out + "/" + name + "_samples.bin", sample_field(f, pts));
+    write_vec(out + "/" + name + "_norms.bin", field_norms(f));
+  };
+  auto put_set = [&](const std::string& name, const FieldSet& b) {
+    if (!reduced) return write_set(out + "/" + name + ".bin", b);
+    write_vec(out + "/" + name + "_rows.bin", sample_block(b, pts));
+    write_vec(out + "/" + name + "_sketch.bin", sketch_block(b, s.sketch, wq));
+  };
+  if (!reduced) write_set(out + "/u0.bin", w.orbitals);
+  else put_set("u0", w.orbitals);
+  put_field("v_ext", s.problem.v_ext);
   HamiltonianState st = build_hamiltonian(w, s.problem);
-  write_field(out + "/rho.bin", st.density);
-  write_field(out + "/v_h.bin", st.v_hartree);
-  write_field(out + "/v_xc.bin", st.v_xc);
-  write_field(out + "/v_local.bin", st.v_local);
-  write_field(out + "/eps_xc.bin", xc_energy_density(st.density));
+  put_field("rho", st.density);
+  put_field("v_h", st.v_hartree);
+  put_field("v_xc", st.v_xc);
+  put_field("v_local", st.v_local);
+  put_field("eps_xc", xc_energy_density(st.density));
   FieldSet hw = apply_hamiltonian(st, w, ex);
-  write_set(out + "/hw.bin", hw);
+  put_set("hw", hw);
   std::vector<double> kin, ext;
   for (const Field& f : w.orbitals) {
     kin.push_back(kinetic_term(f));
@@ -263,18 +391,26 @@ int cmd_ops(const Setup& s, const std::string& out) {
   GramMatrix sigma = gram(hw, w.orbitals);
   write_mat(out + "/sigma.bin", sigma);
   DiagonalResiduals dr = diagonal_residuals(w, hw, ex);
-  write_set(out + "/z.bin", dr.directions);
+  put_set("z", dr.directions);
   write_vec(out + "/sigma_diag.bin", dr.sigma_diag);
   StiefelGradient sg = stiefel_gradient(w, hw, ex);
   double gn = 0.0;
-  for (const Field& f : sg.directions) gn += inner_product(f, f);
+  std::vector<double> dnorm2;
+  for (const Field& f : sg.directions) {
+    const double d2 = inner_product(f, f);
+    dnorm2.push_back(d2);
+    gn += d2;
+  }
+  write_vec(out + "/d_norm2.bin", dnorm2);
+  if (reduced) put_set("d", sg.directions);
   // Trial step + orthonormalization, as in one line-search trial.
   const double tau = 0.3;
   std::vector<Field> trial;
   for (int i = 0; i < w.n(); ++i) trial.push_back(linear_combination(w.orbitals[i], -tau, dr.directions[i]));
   OrthResult orth = orthonormalize_with_gram(OrbitalSet{trial}, true);
-  write_set(out + "/orth_w.bin", orth.w.orbitals);
+  put_set("orth_w", orth.w.orbitals);
   write_mat(out + "/orth_pre_gram.bin", orth.pre_gram);
+  if (reduced) write_mat(out + "/orth_gram.bin", gram(orth.w, orth.w));
   HamiltonianState st2 = build_hamiltonian(orth.w, s.problem);
   EnergyBreakdown e2 = total_energy(orth.w, st2, ex);
   SubspaceRotation rot = subspace_rotate(w, sigma);
@@ -286,7 +422,8 @@ int cmd_ops(const Setup& s, const std::string& out) {
            {"trial_energy", energy_json(e2)},
            {"orth_post_deviation", orth.post_deviation},
            {"grad_norm", std::sqrt(gn)},
-           {"weight", w.grid().quadrature_weight()}};
+           {"weight", wq},
+           {"reduced", reduced}};
   std::ofstream(out + "/ops.json") << sum.dump(1) << '\n';
   return 0;
 }
@@ -316,6 +453,18 @@ int cmd_levels(const Setup& s, const std::string& out) {
   return 0;
 }
 
+// orthonormalize_with_gram (manifold.cpp:136-169) of the start block as given
+// (start kind "file" without "orthonormalize"): the symmetric-eigen fallback
+// fixture (manifold.cpp:118-132) on an ill-conditioned, full-rank set.
+int cmd_orth(const Setup& s, const std::string& out) {
+  OrthResult o = orthonormalize_with_gram(s.u0, true);
+  write_set(out + "/orth_w.bin", o.w.orbitals);
+  write_mat(out + "/pre_gram.bin", o.pre_gram);
+  json sum{{"post_deviation", o.post_deviation}};
+  std::ofstream(out + "/orth.json") << sum.dump(1) << '\n';
+  return 0;
+}
+
 // refine_uniform + prolongate (grid.cpp:137-212) of the start orbitals
 int cmd_prolong(const Setup& s, const std::string& out) {
   GridPtr fine = refine_uniform(s.u0.grid());
@@ -330,7 +479,7 @@ int cmd_prolong(const Setup& s, const std::string& out) {
 
 int main(int argc, char** argv) {
   if (argc != 4) {
-    std::fprintf(stderr, "usage: trace_ref solve|ops|levels|prolong <spec.json> <outdir>\n");
+    std::fprintf(stderr, "usage: trace_ref solve|ops|levels|prolong|orth <spec.json> <outdir>\n");
     return 1;
   }
   try {
@@ -340,6 +489,7 @@ int main(int argc, char** argv) {
     if (cmd == "ops") return cmd_ops(s, argv[3]);
     if (cmd == "levels") return cmd_levels(s, argv[3]);
     if (cmd == "prolong") return cmd_prolong(s, argv[3]);
+    if (cmd == "orth") return cmd_orth(s, argv[3]);
     std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
     return 1;
   } catch (const std::exception& e) {

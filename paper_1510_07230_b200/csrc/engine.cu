@@ -2,6 +2,7 @@
 // (include/parorb_gpu.h). Each po_* operator mirrors one reference function
 // (cited in the header); all arithmetic runs in the sm_100a kernels — there is
 // no host compute path.
+#include <chrono>
 #include <dlfcn.h>
 
 #include <atomic>
@@ -169,8 +170,21 @@ Engine::~Engine() {
 // Spin on the stream instead of a blocking wait: the solver's per-trial
 // readback is on the critical path and blocking-sync wake-up jitter dominated
 // the iteration time on the host side.
+namespace {
+thread_local double t_host_wait = 0.0;  // seconds this thread spent waiting on a device
+struct WaitClock {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  ~WaitClock() {
+    t_host_wait += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
+}  // namespace
+
+double host_wait_seconds() { return t_host_wait; }
+
 void Engine::sync() {
   PO_CUDA(cudaGetLastError());
+  WaitClock wc;
   cudaError_t e;
   while ((e = cudaStreamQuery(s)) == cudaErrorNotReady) {
   }
@@ -261,6 +275,7 @@ void Engine::fetch(size_t off, size_t n) {
   launch_pdl(publish_kernel, dim3(1), dim3(256), 0, s, dvec + off, hvec_dev + off, (int)n, cg_out_i, h_cg_i_dev,
                                    hflag_dev, seq);
   PO_CUDA(cudaGetLastError());
+  WaitClock wc;
   volatile unsigned long long* f = hflag;
   for (unsigned spins = 1; *f != seq; ++spins) {
     if ((spins & 1023u) == 0) {  // surface stream errors instead of spinning forever
@@ -797,11 +812,17 @@ int po_diagonal_residuals(po_engine* h, int u, int hu, int z, double* sigma, dou
 }
 
 int po_stiefel_gradient(po_engine* h, int u, int hu, double* sigma_host, double* dnorm2) {
+  return po_stiefel_gradient_d(h, u, hu, -1, sigma_host, dnorm2);
+}
+
+int po_stiefel_gradient_d(po_engine* h, int u, int hu, int d, double* sigma_host, double* dnorm2) {
   ENGINE_OR_EINVAL(h);
   API_TRY
+  if (d >= 0 && (d == u || d == hu)) throw Error(PO_EINVAL, "stiefel_gradient: D must not alias U or HU");
+  double* dout = d >= 0 ? E.blk(d) : nullptr;
   E.gram(E.blk(hu), nullptr, 0.0, E.blk(u), nullptr, 0.0, 0, E.dmat[4]);
   po::launch_matrix_stats(E.N, E.dmat[4], E.scal() + Engine::S_SYM, E.s);
-  E.mix(E.blk(u), nullptr, 0.0, E.dmat[4], -1.0, E.blk(hu), 1.0, 0, nullptr, E.dvec + E.off_dd());
+  E.mix(E.blk(u), nullptr, 0.0, E.dmat[4], -1.0, E.blk(hu), 1.0, 0, dout, E.dvec + E.off_dd());
   E.fetch_all();
   if (sigma_host) fetch_matrix(E, E.dmat[4], sigma_host);
   if (dnorm2) std::memcpy(dnorm2, E.hvec + E.off_dd(), sizeof(double) * E.N);

@@ -196,6 +196,12 @@ class Engine {
 
 }  // namespace po
 
+namespace po {
+// wall seconds the calling thread has spent blocked on device work (Engine::sync /
+// Engine::fetch): the par_seconds bucket of the PhaseTimer mirror (solver.cu)
+double host_wait_seconds();
+}  // namespace po
+
 struct po_engine {
   po::Engine* e;
   std::string err;

@@ -100,6 +100,7 @@ struct OrthOut {
   double offdiag_max = 0.0;  // near_identity_from_gram(pre_gram), manifold.cpp:249-259
   double diag_dev_max = 0.0;
   bool fallback = false;
+  bool reported = true;  // post_dev is reported (else -1: verification skipped, manifold.cpp:150)
 };
 
 // manifold.cpp:136-169 on the device. in = A + sa * Ab (Ab may be null).
@@ -214,7 +215,7 @@ bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, doubl
 
 // 0 ok, 1 pass-1 Cholesky rejected (caller redoes the trial with the fallback),
 // 3 the CholeskyQR2 repair is due (caller runs orth_repair).
-int orth_outcome(const Engine& E, bool measure, OrthOut& o) {
+int orth_outcome(const Engine& E, bool measure, OrthOut& o, bool g0_rebuilt) {
   const double* hs = E.hvec + E.off_scal();
   o.offdiag_max = hs[Engine::S_MSTAT + 2];
   o.diag_dev_max = hs[Engine::S_MSTAT + 3];
@@ -224,8 +225,14 @@ int orth_outcome(const Engine& E, bool measure, OrthOut& o) {
   const bool verify = measure || !(hs[Engine::S_CHOL + 2] <= 1e2);
   const double dev = hs[Engine::S_MSTAT2];
   o.post_dev = verify ? dev : -1.0;
+  o.reported = verify;
   static const bool force = std::getenv("PO_FORCE_QR2") != nullptr;  // test hook: exercise the repair
-  return verify && (force || !(dev <= 1e-12)) ? 3 : 0;
+  // The reference skips the check for a well-conditioned exact Gram. A G0
+  // rebuilt from the iteration's Grams (G_WW - tau (W^T Z + Z^T W) + tau^2 Z^T Z)
+  // carries cancellation the exact Gram does not, so the rotation's own G2
+  // statistics (already read back) are always checked there; the reported
+  // deviation stays -1 as in the reference.
+  return (verify || g0_rebuilt) && (force || !(dev <= 1e-12)) ? 3 : 0;
 }
 
 // CholeskyQR2 second pass on block out (manifold.cpp:159-166), synchronously;
@@ -240,7 +247,7 @@ bool orth_repair(Engine& E, double* out, double* tmp, OrthOut& o) {
   E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2]);
   launch_matrix_stats(E.N, E.dmat[2], sc + Engine::S_MSTAT2, E.s);
   E.fetch(E.off_scal(), 64);
-  o.post_dev = E.hvec[E.off_scal() + Engine::S_MSTAT2];
+  o.post_dev = o.reported ? E.hvec[E.off_scal() + Engine::S_MSTAT2] : -1.0;
   return true;
 }
 
@@ -712,6 +719,7 @@ bool Solver::step() {
       SRef tstate;
       EnergyParts te;
       bool sync_orth = false;  // the accepted trial went through orthonormalize_dev
+      bool trial_g0g = false;  // the trial's G0 was rebuilt from the iteration's Grams
       for (s = 0; s <= p.max_backtracks; ++s) {
         sync_orth = false;
         tau = tau_raw * std::pow(p.delta, s);
@@ -723,12 +731,14 @@ bool Solver::step() {
           tstate = spec.tstate;
           hwt = spec.hwt;
           spec = {};
+          trial_g0g = true;
         } else {
           wt = pool.get();
           rep = pool.get();
           // one device pipeline per trial, one readback (energy + decisions)
           SRef pre = nonlinear ? spool.get() : SRef();
           const bool g0g = gww_valid && ghh_fresh;
+          trial_g0g = g0g;
           if (!(g0g && nonlinear)) need_z();
           const bool dens = orth_enqueue(E, P(w), zv ? P(hw) : P(z), -tau, P(wt),
                                          p.verify_orthonormality != 0, pre.get(), p.hartree, p.xc,
@@ -738,7 +748,7 @@ bool Solver::step() {
           E.apply_h(P(wt), P(hwt), tstate->v_local, !nonlinear);
           E.fetch_all();
         }
-        const int oc = orth_outcome(E, p.verify_orthonormality != 0, orth);
+        const int oc = orth_outcome(E, p.verify_orthonormality != 0, orth, trial_g0g);
         if (oc == 3) {  // CholeskyQR2 repair (rare): redo the trial's tail on the repaired block
           if (!orth_repair(E, P(wt), P(rep), orth)) continue;  // DegenerateSetError -> NaN energy
           sync_orth = false;
@@ -840,6 +850,17 @@ bool Solver::step() {
       rec.tau = tau;
       rec.backtracks = s;
       rec.offdiag_max = orth.offdiag_max;
+      // SolveResult::checkpoints / drift_iterations, optimizer.cpp:535-539
+      if (r->checkpoints && r->n_checkpoints < r->cap) {
+        double* c = r->checkpoints + 5 * (size_t)r->n_checkpoints;
+        const double v[5] = {(double)level, (double)l, orth.offdiag_max, orth.diag_dev_max, orth.post_dev};
+        std::memcpy(c, v, sizeof v);
+      }
+      r->n_checkpoints++;
+      if (orth.offdiag_max > 0.5) {
+        if (r->drift_iterations && r->n_drift < r->cap) r->drift_iterations[r->n_drift] = l;
+        r->n_drift++;
+      }
       rec.energy = te.total;
       steps_until_orth = n_org - 1;
       if (p.n_diag > 0 && (l + 1 - last_rotation_iter) >= p.n_diag && !full_grad) {
@@ -977,11 +998,24 @@ static void validate_params(const po_params* p) {  // OptimizerParams::validate,
 
 static void reset_result(po_result* r) {
   r->n_records = r->n_accepted = 0;
+  r->n_checkpoints = r->n_drift = 0;
+  r->par_seconds = r->sync_seconds = 0.0;
   r->cg_iters_total = 0;
   r->message[0] = 0;
   r->outcome = PO_OUT_MAX_ITERATIONS;
   r->e_kinetic = r->e_external = r->e_hartree = r->e_xc = r->e_total = 0.0;
   r->final_grad_norm = 0.0;
+}
+
+// PhaseTimer mirror (parallel.hpp:55-86, SolveResult::par/sync_seconds filled at
+// optimizer.cpp:594-595): every orbital-parallel phase runs on the device, so
+// par_seconds is the wall time the host spent waiting on the device pipeline
+// (Engine::wait_seconds: stream syncs + readback spins) and sync_seconds the
+// rest of the call (host-side control, launches, checks); par + sync = wall.
+static void set_phase_times(po_result* r, double wall, double waited) {
+  r->wall_seconds = wall;
+  r->par_seconds = std::min(wall, std::max(0.0, waited));
+  r->sync_seconds = wall - r->par_seconds;
 }
 
 // One InnerLoop level on block w_handle (iterated in place).
@@ -1021,6 +1055,7 @@ int po_solve(po_engine* h, const po_params* p, int w_handle, po_result* r) {
   if (!h || !h->e || !p || !r) return PO_EINVAL;
   Engine& E = *h->e;
   const auto t0 = std::chrono::steady_clock::now();
+  const double wait0 = po::host_wait_seconds();
   reset_result(r);
   try {
     validate_params(p);
@@ -1040,7 +1075,8 @@ int po_solve(po_engine* h, const po_params* p, int w_handle, po_result* r) {
     h->err = ex.what();
     return PO_EINVAL;
   }
-  r->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  set_phase_times(r, std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
+                  po::host_wait_seconds() - wait0);
   return PO_OK;
 }
 
@@ -1052,6 +1088,7 @@ int po_solve_host(po_engine* h, const po_params* p, const double* w_in, double* 
   if (!h || !h->e || !p || !r || !w_in || !w_out) return PO_EINVAL;
   Engine& E = *h->e;
   const auto t0 = std::chrono::steady_clock::now();
+  const double wait0 = po::host_wait_seconds();
   reset_result(r);
   int w_handle = -1;
   cudaStream_t side = nullptr;
@@ -1087,7 +1124,8 @@ int po_solve_host(po_engine* h, const po_params* p, const double* w_in, double* 
   cudaStreamDestroy(side);
   cudaEventDestroy(ev);
   E.give_block(w_handle);
-  r->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  set_phase_times(r, std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
+                  po::host_wait_seconds() - wait0);
   return PO_OK;
 }
 
@@ -1101,6 +1139,7 @@ int po_solve_levels(const po_grid_desc* grid0, int n_orbitals, double occupation
   *out_engine = nullptr;
   *out_block = -1;
   const auto t0 = std::chrono::steady_clock::now();
+  const double wait0 = po::host_wait_seconds();
   reset_result(r);
   po_engine* cur = nullptr;
   int w = -1;
@@ -1156,7 +1195,8 @@ int po_solve_levels(const po_grid_desc* grid0, int n_orbitals, double occupation
   } catch (const std::exception& ex) {
     return fail(PO_EINVAL, ex.what());
   }
-  r->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  set_phase_times(r, std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
+                  po::host_wait_seconds() - wait0);
   *out_engine = cur;
   *out_block = w;
   return PO_OK;
@@ -1169,6 +1209,7 @@ struct po_solver {
   std::shared_ptr<int> w_user;
   int w_handle;
   std::chrono::steady_clock::time_point t0;
+  double wait0;  // Engine::wait_seconds at create (PhaseTimer mirror)
 };
 
 static int solver_error(po_engine* h, po_result* r, const std::exception& ex, int code) {
@@ -1182,11 +1223,9 @@ int po_solver_create(po_engine* h, const po_params* p, int w_handle, po_result* 
   if (!h || !h->e || !p || !r || !out) return PO_EINVAL;
   Engine& E = *h->e;
   *out = nullptr;
-  r->n_records = r->n_accepted = 0;
-  r->cg_iters_total = 0;
-  r->message[0] = 0;
-  r->outcome = PO_OUT_MAX_ITERATIONS;
-  auto* sv = new po_solver{h, *p, nullptr, nullptr, w_handle, std::chrono::steady_clock::now()};
+  reset_result(r);
+  auto* sv = new po_solver{h, *p, nullptr, nullptr, w_handle, std::chrono::steady_clock::now(),
+                           po::host_wait_seconds()};
   try {
     E.blk(w_handle);
     sv->S = new po::Solver(E, sv->p, r);
@@ -1248,8 +1287,8 @@ int po_solver_finish(po_solver* sv) {
       PO_CUDA(cudaMemcpyAsync(E.blk(sv->w_handle), E.blk(*S.w), sizeof(double) * E.N * E.g.ld,
                               cudaMemcpyDeviceToDevice, E.s));
     E.sync();
-    r->wall_seconds =
-        std::chrono::duration<double>(std::chrono::steady_clock::now() - sv->t0).count();
+    set_phase_times(r, std::chrono::duration<double>(std::chrono::steady_clock::now() - sv->t0).count(),
+                    po::host_wait_seconds() - sv->wait0);
   } catch (const Error& ex) {
     return solver_error(sv->h, r, ex, ex.code);
   } catch (const std::exception& ex) {

@@ -83,7 +83,25 @@ class Result(C.Structure):
                 ("outcome", C.c_int), ("cg_iters_total", C.c_int64), ("e_kinetic", C.c_double),
                 ("e_external", C.c_double), ("e_hartree", C.c_double), ("e_xc", C.c_double),
                 ("e_total", C.c_double), ("final_grad_norm", C.c_double), ("wall_seconds", C.c_double),
-                ("par_seconds", C.c_double), ("sync_seconds", C.c_double), ("message", C.c_char * 200)]
+                ("par_seconds", C.c_double), ("sync_seconds", C.c_double), ("message", C.c_char * 200),
+                ("checkpoints", C.POINTER(C.c_double)), ("n_checkpoints", C.c_int),
+                ("drift_iterations", C.POINTER(C.c_int)), ("n_drift", C.c_int)]
+
+
+def _new_result(cap: int, n: int, trace_eigs: bool = False):
+    """A po_result with every output array allocated (kept alive in the dict)."""
+    keep = {"recs": (Record * cap)(), "acc": np.zeros(cap * 9), "ckpt": np.zeros(cap * 5),
+            "drift": np.zeros(cap, dtype=np.int32),
+            "eigs": np.full(cap * n, np.nan) if trace_eigs else np.zeros(1)}
+    r = Result()
+    r.cap = cap
+    r.records = keep["recs"]
+    r.accepted = keep["acc"].ctypes.data_as(C.POINTER(C.c_double))
+    r.sigma_eigs = (keep["eigs"].ctypes.data_as(C.POINTER(C.c_double)) if trace_eigs
+                    else C.POINTER(C.c_double)())
+    r.checkpoints = keep["ckpt"].ctypes.data_as(C.POINTER(C.c_double))
+    r.drift_iterations = keep["drift"].ctypes.data_as(C.POINTER(C.c_int))
+    return r, keep
 
 
 _SIGS = {
@@ -119,6 +137,7 @@ _SIGS = {
                            C.POINTER(C.c_int)], C.c_int),
     "po_diagonal_residuals": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
     "po_stiefel_gradient": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
+    "po_stiefel_gradient_d": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
     "po_subspace_rotate": ([C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "po_linear_combination": ([C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int], C.c_int),
     "po_bb_products": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
@@ -325,9 +344,11 @@ class Engine:
         self._chk(self._lib.po_diagonal_residuals(self.h, u, hu, z, _dp(s), _dp(zz)))
         return s, zz
 
-    def stiefel_gradient(self, u: int, hu: int):
+    def stiefel_gradient(self, u: int, hu: int, d: int = -1):
+        """manifold.cpp:181-202: (Sigma, <D_i, D_i>); with d >= 0 the block D = HU - U Sigma
+        is written there too (po_stiefel_gradient_d)."""
         sig, dd = np.empty((self.N, self.N)), np.empty(self.N)
-        self._chk(self._lib.po_stiefel_gradient(self.h, u, hu, _dp(sig), _dp(dd)))
+        self._chk(self._lib.po_stiefel_gradient_d(self.h, u, hu, d, _dp(sig), _dp(dd)))
         return sig, dd
 
     def subspace_rotate(self, w: int, sigma: np.ndarray):
@@ -378,38 +399,24 @@ class Engine:
               poisson="dst", **over) -> "SolveResult":
         p = self.make_params(algorithm, hartree, xc, trace_eigs, poisson, **over)
         cap = p.max_inner + 1
-        recs = (Record * cap)()
-        acc = np.zeros(cap * 9)
-        eigs = np.full(cap * self.N, np.nan)
-        r = Result()
-        r.cap = cap
-        r.records = recs
-        r.accepted = acc.ctypes.data_as(C.POINTER(C.c_double))
-        r.sigma_eigs = eigs.ctypes.data_as(C.POINTER(C.c_double)) if trace_eigs else C.POINTER(C.c_double)()
+        r, keep = _new_result(cap, self.N, trace_eigs)
         rc = self._lib.po_solve(self.h, C.byref(p), w, C.byref(r))
         if rc != PO_OK:
             raise _err(rc, self._lib.po_last_error(self.h).decode() or r.message.decode())
-        return _solve_result(r, recs, acc, eigs, cap, self.N, trace_eigs)
+        return _solve_result(r, keep, cap, self.N, trace_eigs)
 
     def solve_host(self, w_in: np.ndarray, w_out: np.ndarray, algorithm="opt_par_mod", hartree=True,
                    xc=True, poisson="dst", **over) -> "SolveResult":
         """po_solve_host: host orbitals in, final orbitals out (pinned buffers are fastest)."""
         p = self.make_params(algorithm, hartree, xc, False, poisson, **over)
         cap = p.max_inner + 1
-        recs = (Record * cap)()
-        acc = np.zeros(cap * 9)
-        eigs = np.zeros(1)
-        r = Result()
-        r.cap = cap
-        r.records = recs
-        r.accepted = acc.ctypes.data_as(C.POINTER(C.c_double))
-        r.sigma_eigs = C.POINTER(C.c_double)()
+        r, keep = _new_result(cap, self.N)
         if w_in.size != self.N * self.ngl or w_out.size != self.N * self.ngl:
             raise InvalidArgument("block shape mismatch")
         rc = self._lib.po_solve_host(self.h, C.byref(p), _dp(w_in), _dp(w_out), C.byref(r))
         if rc != PO_OK:
             raise _err(rc, self._lib.po_last_error(self.h).decode() or r.message.decode())
-        return _solve_result(r, recs, acc, eigs, cap, self.N, False)
+        return _solve_result(r, keep, cap, self.N, False)
 
     # ---- outer refinement (optimizer.cpp:638-669, grid.cpp:137-212)
     def initialize_orbitals(self, atoms, seed: int, w: int):
@@ -431,13 +438,8 @@ class Stepper:
         self.e = e
         self.p = params
         cap = params.max_inner + 1
-        self._recs = (Record * cap)()
-        self._acc = np.zeros(cap * 9)
-        self.r = Result()
-        self.r.cap = cap
-        self.r.records = self._recs
-        self.r.accepted = self._acc.ctypes.data_as(C.POINTER(C.c_double))
-        self.r.sigma_eigs = C.POINTER(C.c_double)()
+        self.r, self._keep = _new_result(cap, e.N, bool(params.trace_sigma_eigs))
+        self._recs = self._keep["recs"]
         self.h = C.c_void_p()
         rc = e._lib.po_solver_create(e.h, C.byref(self.p), w, C.byref(self.r), C.byref(self.h))
         if rc != PO_OK:
@@ -460,6 +462,14 @@ class Stepper:
         n = min(self.r.n_records, self.r.cap)
         return [dict(iter=x.iter, energy=x.energy, grad_norm=x.grad_norm, tau=x.tau, backtracks=x.backtracks,
                      did_orth=x.did_orth, wall_ms=x.wall_ms) for x in self._recs[:n]]
+
+    def sigma_eigs(self) -> np.ndarray:
+        """eig(<(HW)^T W>) per record (params.trace_sigma_eigs)."""
+        n = min(self.r.n_records, self.r.cap)
+        return self._keep["eigs"][: n * self.e.N].reshape(-1, self.e.N)
+
+    def result(self) -> "SolveResult":
+        return _solve_result(self.r, self._keep, self.r.cap, self.e.N, bool(self.p.trace_sigma_eigs))
 
     def close(self):
         if self.h:
@@ -504,11 +514,20 @@ class SolveResult:
     final_grad_norm: float
     cg_iters_total: int
     wall_seconds: float
+    par_seconds: float = 0.0
+    sync_seconds: float = 0.0
+    checkpoints: list = field(default_factory=list)  # OrthCheckpoint rows (optimizer.hpp:87-93)
+    drift_iterations: list = field(default_factory=list)
     extra: dict = field(default_factory=dict)
 
 
-def _solve_result(r, recs, acc, eigs, cap, N, trace_eigs) -> SolveResult:
+def _solve_result(r, keep, cap, N, trace_eigs) -> SolveResult:
+    recs, acc, eigs = keep["recs"], keep["acc"], keep["eigs"]
     nrec = min(r.n_records, cap)
+    ck = keep["ckpt"][: 5 * min(r.n_checkpoints, cap)].reshape(-1, 5)
+    checkpoints = [dict(level=int(c[0]), iter=int(c[1]), offdiag_max=float(c[2]),
+                        diag_deviation_max=float(c[3]), orth_deviation=float(c[4])) for c in ck]
+    drift = [int(x) for x in keep["drift"][: min(r.n_drift, cap)]]
     records = [dict(level=x.level, iter=x.iter, energy=x.energy, grad_norm=x.grad_norm, tau=x.tau,
                     backtracks=x.backtracks, did_orth=x.did_orth, did_diag=x.did_diag,
                     offdiag_max=x.offdiag_max, wall_ms=x.wall_ms) for x in recs[:nrec]]
@@ -519,7 +538,8 @@ def _solve_result(r, recs, acc, eigs, cap, N, trace_eigs) -> SolveResult:
         energy=dict(kinetic=r.e_kinetic, external=r.e_external, hartree=r.e_hartree, xc=r.e_xc,
                     total=r.e_total),
         final_grad_norm=r.final_grad_norm, cg_iters_total=r.cg_iters_total,
-        wall_seconds=r.wall_seconds)
+        wall_seconds=r.wall_seconds, par_seconds=r.par_seconds, sync_seconds=r.sync_seconds,
+        checkpoints=checkpoints, drift_iterations=drift)
 
 
 def refine_grid(n, extent):
@@ -539,14 +559,7 @@ def solve_levels(spec, outer_levels: int, seed: int, algorithm="opt_par_mod", po
     p = Engine.make_params(algorithm, spec.hartree, spec.xc, False, poisson, **over)
     p.outer_levels, p.seed = int(outer_levels), int(seed)
     cap = outer_levels * p.max_inner + 1
-    recs = (Record * cap)()
-    acc = np.zeros(cap * 9)
-    eigs = np.zeros(1)
-    r = Result()
-    r.cap = cap
-    r.records = recs
-    r.accepted = acc.ctypes.data_as(C.POINTER(C.c_double))
-    r.sigma_eigs = C.POINTER(C.c_double)()
+    r, keep = _new_result(cap, spec.n_orbitals)
     g = GridDesc((C.c_int64 * 3)(*[int(x) for x in spec.n]),
                  (C.c_double * 3)(*[float(x) for x in spec.extent]))
     atoms = np.ascontiguousarray(np.asarray(spec.atoms, dtype=np.float64).reshape(-1, 5))
@@ -568,7 +581,7 @@ def solve_levels(spec, outer_levels: int, seed: int, algorithm="opt_par_mod", po
     z0, nz, ngl = C.c_int64(), C.c_int64(), C.c_int64()
     L.po_local_slab(h, C.byref(z0), C.byref(nz), C.byref(ngl))
     e.z0, e.nz, e.ngl = z0.value, nz.value, ngl.value
-    return _solve_result(r, recs, acc, eigs, cap, spec.n_orbitals, False), e, blk.value
+    return _solve_result(r, keep, cap, spec.n_orbitals, False), e, blk.value
 
 
 def _records_array(records):

@@ -42,7 +42,7 @@ def test_default_params_match_reference(native):
 
 def test_abi_version_and_sizing(native):
     L = native.lib()
-    assert L.po_abi_version() == 1
+    assert L.po_abi_version() == 2
     g = native.GridDesc((C.c_int64 * 3)(192, 192, 192), (C.c_double * 3)(60.0, 60.0, 60.0))
     one = L.po_solver_bytes(C.byref(g), 512, 1)
     eight = L.po_solver_bytes(C.byref(g), 512, 8)
@@ -62,3 +62,12 @@ def test_create_validates_grid_without_gpu_work(native, bad):
     """grid.cpp:14-34 argument checks happen before any device call."""
     with pytest.raises(native.InvalidArgument):
         native.Engine(bad, (1.0, 1.0, 1.0), 2)
+
+
+def test_result_struct_layout_matches_header(native):
+    """po_result (include/parorb_gpu.h) as ctypes sees it: the SolveResult
+    fields appended in ABI 2 sit after message[200]."""
+    R = native.Result
+    names = [f[0] for f in R._fields_]
+    assert names[-4:] == ["checkpoints", "n_checkpoints", "drift_iterations", "n_drift"]
+    assert R.checkpoints.offset > R.message.offset

@@ -204,3 +204,39 @@ def test_poisson_closed_form(port):
     xh = bh / (lam[0][:, None, None] + lam[1][None, :, None] + lam[2][None, None, :])
     x = np.einsum("ia,jb,kc,abc->ijk", S[0], S[1], S[2], xh) * np.prod([2.0 / (m + 1) for m in n])
     assert np.linalg.norm(st["v_h"] - x.ravel()) <= 1e-8 * np.linalg.norm(x)
+
+
+def test_sketch_helper_matches_harness():
+    """tests/helpers.py sketch_block / sample_points restate trace_ref.cpp's
+    Sketch (the fingerprints of the C3 / C4-grid fixtures): same signs, same
+    sampled points, on the full mol12 arrays the harness also wrote in full."""
+    from helpers import sample_points, sketch_block
+
+    full = np.load(os.path.join(GOLDEN, "ops_mol12.npz"))
+    red = np.load(os.path.join(GOLDEN, "opsr_mol12.npz"))
+    meta = json.load(open(os.path.join(GOLDEN, "opsr_mol12.json")))
+    spec = spec_from(meta["spec"])
+    sk = meta["sketch"]
+    wq = np.prod(spec.spacing)
+    pts = sample_points(spec.num_points, sk["samples"])
+    for b in ("u0", "hw", "z", "orth_w"):
+        s = sketch_block(full[b], wq, sk["m"], sk["seed"])
+        assert np.max(np.abs(s - red[b + "_sketch"])) < 1e-13 * max(1.0, np.max(np.abs(s)))
+        assert np.array_equal(full[b][:, pts], red[b + "_rows"])
+    for f in ("v_ext", "rho", "v_h", "v_xc", "v_local"):
+        assert np.array_equal(full[f][pts], red[f + "_samples"])
+        assert abs(full[f].sum() - red[f + "_norms"][0]) < 1e-12 * np.abs(full[f]).sum()
+
+
+def test_port_symmetric_fallback_matches_reference(port):
+    """manifold.cpp:118-132: an ill-conditioned full-rank set (Cholesky pass
+    rejected, rank check passed) goes through the symmetric-eigen fallback
+    W~ Q Lambda^-1/2 Q^T — unique, so compared elementwise."""
+    g = np.load(os.path.join(GOLDEN, "orth_fallback.npz"))
+    meta = json.load(open(os.path.join(GOLDEN, "orth_fallback.json")))
+    spec = spec_from(meta["spec"])
+    out, pre, dev, fb = port.orthonormalize(spec, g["u"])
+    assert fb
+    assert np.array_equal(pre, g["pre_gram"])
+    assert np.max(np.abs(out - g["w"])) < 1e-7 * np.max(np.abs(g["w"]))
+    assert dev <= 1e-12 and meta["post_deviation"] <= 1e-12
