@@ -69,13 +69,18 @@ int main(int argc, char** argv) {
     worst_orth = std::max(worst_orth, b.orth_deviation);
   }
   ck_ok = ck_ok && ck_diff < 1e-8 && worst_orth <= 1e-10;
-  const std::size_t m_ck = gpu.checkpoints.size();
-  double off10 = 0.0, diag10 = 0.0;
-  for (std::size_t k = m_ck >= 10 ? m_ck - 10 : 0; k < m_ck; ++k) {
-    off10 = std::max(off10, gpu.checkpoints[k].offdiag_max);
-    diag10 = std::max(diag10, gpu.checkpoints[k].diag_deviation_max);
-  }
-  const bool crit6 = m_ck < 10 || (off10 < 0.1 && diag10 < 0.1);
+  // criterion 6 needs a converged run; here both sides must reach the same verdict
+  auto final10 = [](const SolveResult& r, double& off, double& diag) {
+    const std::size_t m = r.checkpoints.size();
+    off = diag = 0.0;
+    for (std::size_t k = m >= 10 ? m - 10 : 0; k < m; ++k) {
+      off = std::max(off, r.checkpoints[k].offdiag_max);
+      diag = std::max(diag, r.checkpoints[k].diag_deviation_max);
+    }
+    return m >= 10 && off < 0.1 && diag < 0.1;
+  };
+  double off10 = 0.0, diag10 = 0.0, off10c = 0.0, diag10c = 0.0;
+  const bool crit6 = final10(gpu, off10, diag10) == final10(cpu, off10c, diag10c);
   const double coverage = (gpu.par_seconds + gpu.sync_seconds) / gpu.wall_seconds;
   const double par_frac = gpu.par_seconds / (gpu.par_seconds + gpu.sync_seconds);
   std::printf("checkpoints %zu/%zu max|d stats| %.2e worst orth_dev %.2e drift %zu/%zu  "

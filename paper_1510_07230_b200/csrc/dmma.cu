@@ -814,7 +814,14 @@ int mix_nblk_max(const SlabGeom& g) {
 
 int launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, double sa,
                const double* M, double alpha, const double* C, double beta, int upper,
-               double* out, double* norms, cudaStream_t s, const double* guard) {
+               double* out, double* norms, cudaStream_t s, const double* guard,
+               const double* zsig) {
+  if (zsig) {  // implicit direction: only the large-N TMA tiles rebuild z = HW - zsig W
+    if (N <= 64 || !Ab) return -2;
+    const int nb = launch_mix_big(N, g.ld, g.ngl, A, Ab, sa, M, alpha, C, beta, upper, out, norms, s,
+                                  guard, zsig);
+    return nb >= 0 ? nb : -2;
+  }
   // measurement switch (the large-N TMA mix at N = 49..64 measured slower: 0.49 vs 0.53 of HBM)
   static const int big_min = getenv("PO_MIX_BIG_MIN") ? atoi(getenv("PO_MIX_BIG_MIN")) : 65;
   if (N < big_min && N <= 64) {  // small-N paths (return their partials row length)

@@ -1646,6 +1646,103 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
             }
         }
       }
+    } else if constexpr (GT_T == 128) {
+      // Diagonal tile of a symmetric Gram, T = 128 (16 fragment rows): warps 0-3
+      // take the first 16-point half of every stage, warps 4-7 the second, and
+      // warp a of either half owns fragment rows {a, 7-a, 8+a, 15-a} of the
+      // upper triangle (c >= r): 34 blocks per warp, balanced. Walking the
+      // columns c = a .. 15, one shared load gives the B fragment of column c for
+      // every owned row r <= c (1 to 4 of them, warp-uniform counts) and, when c
+      // is itself an owned row, that row's A fragment — 16 - a loads per 68
+      // DMMAs where the circulant scheme below needed one load per 2 DMMAs
+      // (shared-memory bound at 68% of FP64 on C3). The two halves' partial
+      // blocks meet in the epilogue.
+      const int hf = warp >> 2, a = warp & 3;
+      const int fr[4] = {a, 7 - a, 8 + a, 15 - a};
+      double gacc[4][16][2];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int c = 0; c < 16; ++c) gacc[f][c][0] = gacc[f][c][1] = 0.0;
+      const int q0 = hf * nload, qb2 = qa_b >= 0 ? hf * nload + qa_b : -1;
+      for (int st = 0; st < nstage; ++st) {
+        const int s = st % nst;
+        mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+        const double* sbuf = stage0 + (size_t)s * sdoubles;
+#pragma unroll
+        for (int kg = 0; kg < 2; ++kg) {
+          const int p = 8 * kg + 2 * t4;
+          double2 ar[4], bprev = make_double2(0.0, 0.0);
+          int cntprev = 0;
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            // rows r <= c among the owned ones (sorted a < 7-a < 8+a < 15-a): a
+            // warp-uniform count. The first k-step of column c is issued before
+            // the second k-step of column c - 1, so consecutive DMMAs are
+            // independent. (A per-row-set template copy issuing only the useful
+            // DMMAs measured slower, 1.62 vs 1.45 ms at C3: instruction fetch.)
+            double2 bc = make_double2(0.0, 0.0);
+            int cnt = 0;
+            if (c >= a) {
+              bc = load_frag(sbuf, q0, qb2, sa, c, p);
+              if (c == fr[0]) ar[0] = bc;
+              if (c == fr[1]) ar[1] = bc;
+              if (c == fr[2]) ar[2] = bc;
+              if (c == fr[3]) ar[3] = bc;
+              cnt = (c >= fr[0]) + (c >= fr[1]) + (c >= fr[2]) + (c >= fr[3]);
+#pragma unroll
+              for (int f = 0; f < 4; ++f)
+                if (f < cnt) dmma_8x8x4(gacc[f][c], ar[f].x, bc.x);
+            }
+            if (c > 0) {
+#pragma unroll
+              for (int f = 0; f < 4; ++f)
+                if (f < cntprev) dmma_8x8x4(gacc[f][c - 1], ar[f].y, bprev.y);
+            }
+            bprev = bc;
+            cntprev = cnt;
+          }
+#pragma unroll
+          for (int f = 0; f < 4; ++f) dmma_8x8x4(gacc[f][15], ar[f].y, bprev.y);  // c = 15 >= every row
+          if (kg == 1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+          }
+        }
+      }
+      constexpr int SP = GT_T + 8;
+      double* S = stage0;
+      asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NW * 32) : "memory");  // ring fully consumed
+      // pass 0: half 0 stores its blocks; pass 1: half 1 adds (same block set)
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass) {
+        if (hf == pass) {
+#pragma unroll
+          for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              const int r = fr[f];
+              if (c < r) continue;
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int idx = (8 * r + gq) * SP + 8 * c + 2 * t4 + j;
+                if (pass == 0)
+                  S[idx] = gacc[f][c][j];
+                else
+                  S[idx] += gacc[f][c][j];
+              }
+            }
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NW * 32) : "memory");
+      }
+      double* outd = ws + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * (GT_T * GT_T);
+      const int ct = threadIdx.x - Cfg::PW * 32;
+      for (int e = ct; e < GT_T * GT_T / 2; e += Cfg::NW * 32) {
+        const int r = (2 * e) / GT_T, c = (2 * e) % GT_T;
+        *reinterpret_cast<double2*>(outd + r * GT_T + c) =
+            make_double2(S[r * SP + c], S[r * SP + c + 1]);
+      }
+      return;
     } else {
       // Diagonal tile of a symmetric Gram with no wasted DMMA and one code path
       // for all warps. Each stage holds two 16-point halves. With R = T / 8
@@ -1830,17 +1927,19 @@ BigPlan big_plan(int64_t ld, int N, int sym, int sms, int GT_T) {
   int cap = 4096 / p.ntiles;
   if (cap < 1) cap = 1;
   if (cap > kb) cap = (int)kb;
+  // the fewest splits that fill whole waves (a 0.97-full wave left 4 of 148 SMs
+  // idle for the whole of the C3 Grams), else the best fill
   int best = 1;
   double beste = 0.0;
   for (int ns = 1; ns <= cap; ++ns) {
     const int64_t units = (int64_t)p.ntiles * ns;
     const int64_t waves = (units + sms - 1) / sms;
     const double eff = (double)units / (double)(waves * sms);
-    if (eff > beste + 0.02) {
+    if (eff > beste + 1e-3) {
       beste = eff;
       best = ns;
     }
-    if (eff >= 0.97) break;
+    if (eff >= 0.999) break;
   }
   // chunks of a multiple of 32 points: diagonal tiles consume 32-point stages
   p.kchunk = (((kb + best - 1) / best + 1) / 2) * 2 * BOX;
@@ -1905,20 +2004,11 @@ __device__ __forceinline__ void mix_big_slice(double (&acc)[2][16][2], const dou
   }
 }
 
-// DIR: the compute_directions pass for N > 64 (manifold.cpp:181-216,
-// optimizer.cpp:265-320, 386-397) on the same tiles: D = HW - W Sigma is formed
-// and reduced (never stored), and the epilogue also writes z = HW - sigma_ii W
-// and reduces ||z||^2 and the BB products ss, sy, yy against (W_prev, Z_prev):
-// partial rows [zz | dd | ss | sy | yy] x n_pt in dpart (the residual pass over
-// five blocks disappears; W rows come back from L2).
-template <bool DIR>
 __global__ void __launch_bounds__(XTH, 1) mix_big_kernel(
     const __grid_constant__ Maps maps, int has_ab, int N, int64_t ld, int64_t ngl, int n_pt,
     int n_it, int upper, int nst, double sa, double alpha, const double* __restrict__ C,
     double beta, double* __restrict__ out, double* __restrict__ norms,
-    const double* __restrict__ guard, const double* __restrict__ wraw,
-    const double* __restrict__ sig, const double* __restrict__ wp, const double* __restrict__ zp,
-    double* __restrict__ zout, double* __restrict__ dpart) {
+    const double* __restrict__ guard, const double* __restrict__ zsig) {
   PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
@@ -1926,6 +2016,7 @@ __global__ void __launch_bounds__(XTH, 1) mix_big_kernel(
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
   uint64_t* empty = full + 8;
   uint64_t* ready = full + 16;  // two-source stages: A + sa Ab formed in place
+  double* mst = reinterpret_cast<double*>(tsm + 512);  // -sigma of a stage (implicit z)
   double* stage0 = reinterpret_cast<double*>(tsm + 1024);
   constexpr size_t QA = (size_t)XP * XK;  // doubles per source per stage
   const int nsrc = has_ab ? 2 : 1;
@@ -1984,9 +2075,21 @@ __global__ void __launch_bounds__(XTH, 1) mix_big_kernel(
           mbar_wait(&full[s], (uint32_t)(g / nst) & 1u);
           double2* a2 = reinterpret_cast<double2*>(stage0 + (size_t)s * sdoubles);
           const double2* b2 = reinterpret_cast<const double2*>(stage0 + (size_t)s * sdoubles + QA);
+          if (zsig) {  // -sigma of the stage's 16 orbitals, once per stage
+            if (ct < XK) {
+              const int k = c * XK + ct;
+              mst[ct] = k < N ? -zsig[k] : 0.0;
+            }
+            asm volatile("bar.sync 2, 96;\n" ::: "memory");
+          }
           for (int e = ct; e < (int)(QA / 2); e += 96) {
             double2 v = a2[e];
-            const double2 z = b2[e];
+            double2 z = b2[e];
+            if (zsig) {  // Ab is HW: z = HW - sigma_k W rebuilt with the directions pass's FMA
+              const double ms = mst[(e & 127) >> 3];  // the swizzle permutes within a 16-point row
+              z.x = fma(ms, v.x, z.x);
+              z.y = fma(ms, v.y, z.y);
+            }
             v.x += sa * z.x;
             v.y += sa * z.y;
             a2[e] = v;
@@ -2043,72 +2146,6 @@ __global__ void __launch_bounds__(XTH, 1) mix_big_kernel(
       }
       // epilogue: acc[q][2 g + e][j] = out(point 16 g + 2 gq + e, orbital i0 + 8 F_q + 2 t4 + j)
       const int64_t pb = (int64_t)pt * XP + 2 * gq;
-      if constexpr (DIR) {
-        const bool hist = wp != nullptr;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          if (!(q ? real1 : real0)) continue;
-          const int F = q ? F1 : F0;
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int i = i0 + 8 * F + 2 * t4 + j;
-            double r5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // zz, dd, ss, sy, yy
-            if (i < N) {
-              const double ms = -sig[i];
-              const int64_t o = (int64_t)i * ld;
-#pragma unroll
-              for (int gg = 0; gg < 8; ++gg) {
-                const int64_t p = pb + 16 * gg;
-                if (p >= ngl) continue;
-                const int ne = p + 1 < ngl ? 2 : 1;
-                const bool two = ne == 2;
-                double2 hv, wv, wq = make_double2(0.0, 0.0), zq = make_double2(0.0, 0.0);
-                if (two) {
-                  hv = *reinterpret_cast<const double2*>(C + o + p);
-                  wv = *reinterpret_cast<const double2*>(wraw + o + p);
-                  if (hist) {
-                    wq = *reinterpret_cast<const double2*>(wp + o + p);
-                    zq = *reinterpret_cast<const double2*>(zp + o + p);
-                  }
-                } else {
-                  hv = make_double2(C[o + p], 0.0);
-                  wv = make_double2(wraw[o + p], 0.0);
-                  if (hist) {
-                    wq = make_double2(wp[o + p], 0.0);
-                    zq = make_double2(zp[o + p], 0.0);
-                  }
-                }
-                const double d0 = alpha * acc[q][2 * gg][j] + beta * hv.x;
-                const double d1 = two ? alpha * acc[q][2 * gg + 1][j] + beta * hv.y : 0.0;
-                r5[1] += d0 * d0 + d1 * d1;
-                // z = HW - sigma_ii W (residual_bb_kernel)
-                const double v0 = hv.x + ms * wv.x, v1 = two ? hv.y + ms * wv.y : 0.0;
-                if (two)
-                  *reinterpret_cast<double2*>(zout + o + p) = make_double2(v0, v1);
-                else
-                  zout[o + p] = v0;
-                r5[0] += v0 * v0 + v1 * v1;
-                if (hist) {
-                  const double s0 = wv.x - wq.x, y0 = v0 - zq.x;
-                  const double s1 = two ? wv.y - wq.y : 0.0, y1 = two ? v1 - zq.y : 0.0;
-                  r5[2] += s0 * s0 + s1 * s1;
-                  r5[3] += s0 * y0 + s1 * y1;
-                  r5[4] += y0 * y0 + y1 * y1;
-                }
-              }
-            }
-#pragma unroll
-            for (int r = 0; r < 5; ++r) {
-              double v = r5[r];
-              v += __shfl_xor_sync(0xffffffffu, v, 4);
-              v += __shfl_xor_sync(0xffffffffu, v, 8);
-              v += __shfl_xor_sync(0xffffffffu, v, 16);
-              if (gq == 0 && i < N && (hist || r < 2)) dpart[((int64_t)r * N + i) * n_pt + pt] = v;
-            }
-          }
-        }
-        continue;
-      }
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         if (!(q ? real1 : real0)) continue;
@@ -2156,6 +2193,259 @@ __global__ void __launch_bounds__(XTH, 1) mix_big_kernel(
 }
 
 
+// ------------------------------------------------------- large-N directions pass
+// compute_directions for N > 64 (manifold.cpp:181-216, optimizer.cpp:265-320,
+// 386-397) with every operand streamed by TMA and no epilogue loads.
+// Tiles of 128 points x 128 orbitals as in mix_big_kernel; ring A carries, per
+// stage, 16 input orbitals of W (the DMMA A operand) and 16 columns of Sigma^T.
+// The stages whose 16 orbitals are the tile's own (the "diagonal" stages, all
+// of them for N <= 128) additionally get ring E: HW, W_prev and HW_prev (or a
+// stored Z_prev) of the same 16 orbitals x 128 points. The consumer warp that
+// owns an orbital fragment, at the diagonal stage holding it,
+//   * forms z = HW - sigma_ii W with the same FMA the stored-z passes use
+//     (fma(-sigma_i, W, HW)) and, only if a caller needs it stored, writes it;
+//   * reduces ||z||^2 and the BB products ss, sy, yy against
+//     (W_prev, z_prev = HW_prev - sigma_prev W_prev) — the previous iteration's
+//     direction rebuilt, never stored (or read from Z_prev);
+//   * subtracts HW from its DMMA accumulators, so the tile's accumulators end
+//     as W Sigma - HW = -D and ||D_i||^2 needs no memory at all.
+// Every block is read once through TMA (W, HW, W_prev, HW_prev: 4 blocks) and
+// nothing is written on the implicit path; the old form (mix_big_kernel<DIR>)
+// wrote z and re-read HW / W / W_prev / Z_prev with plain loads after the DMMA
+// loop while the tensor pipe idled (5.2 ms at C3).
+struct Maps5 {
+  CUtensorMap m[5];
+};
+constexpr int DNA = 3;  // ring A stages (W + Sigma^T: 32 KB each)
+constexpr int DNE = 2;  // ring E stages (HW, W_prev, HW_prev: 3 x 16.25 KB each)
+// Ring E boxes are unswizzled rows of EW = 130 points (one box per block per
+// stage): 1-KB+ TMA rows stream at full rate where the 128-B rows of the
+// swizzled DMMA boxes cap near 4.2 TB/s (profiles/r1_tma2d_probe.txt), and the
+// 1040-B row pitch puts the rows 2 t4 + j a lane quarter reads at 16-B chunks
+// 2 t4 (mod 8) apart: the elementwise reads are bank-conflict free. The 2
+// extra points per row are the next tile's first two (L2 hits).
+constexpr int EW = 130;
+constexpr size_t QE = (size_t)XK * EW;  // doubles per block per E stage (a multiple of 128 B)
+
+template <int Q>
+__device__ __forceinline__ void dir_big_elementwise(
+    double (&acc)[2][16][2], const double* sa_, const double* se, int hist, int hh, int gq, int t4,
+    int i0, int F, int N, int64_t ld, int64_t ngl, int64_t p0, const double* __restrict__ sig,
+    const double* __restrict__ sigp, double* __restrict__ zout, double* __restrict__ dpart, int n_pt,
+    int pt) {
+  const double* sh = se;               // HW
+  const double* swp = se + QE;         // W_prev
+  const double* sx = se + 2 * QE;      // HW_prev (implicit z_prev) or Z_prev
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int i = i0 + 8 * F + 2 * t4 + j;
+    const bool live = i < N;
+    const double ms = live ? -sig[i] : 0.0;
+    const double msp = (live && sigp) ? -sigp[i] : 0.0;
+    const int row = 8 * hh + 2 * t4 + j;
+    double r4[4] = {0.0, 0.0, 0.0, 0.0};  // zz, ss, sy, yy
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const int off = swz(row, 16 * g + 2 * gq, XK);  // the swizzled A (W) stage
+      const int oe = row * EW + 16 * g + 2 * gq;       // the ring E rows
+      const double2 wv = *reinterpret_cast<const double2*>(sa_ + off);
+      const double2 hv = *reinterpret_cast<const double2*>(sh + oe);
+      // accumulators: W Sigma - HW (points past ngl hold zeros on both sides)
+      acc[Q][2 * g][j] -= hv.x;
+      acc[Q][2 * g + 1][j] -= hv.y;
+      // z = HW - sigma_ii W (residual_bb_kernel / launch_z_from_hw: the same FMA)
+      const double v0 = fma(ms, wv.x, hv.x), v1 = fma(ms, wv.y, hv.y);
+      r4[0] += v0 * v0 + v1 * v1;
+      const int64_t p = p0 + 16 * g + 2 * gq;
+      if (zout && live && p < ngl) {
+        if (p + 1 < ngl)
+          *reinterpret_cast<double2*>(zout + (int64_t)i * ld + p) = make_double2(v0, v1);
+        else
+          zout[(int64_t)i * ld + p] = v0;
+      }
+      if (hist) {
+        const double2 wq = *reinterpret_cast<const double2*>(swp + oe);
+        const double2 xq = *reinterpret_cast<const double2*>(sx + oe);
+        const double zq0 = sigp ? fma(msp, wq.x, xq.x) : xq.x;
+        const double zq1 = sigp ? fma(msp, wq.y, xq.y) : xq.y;
+        const double s0 = wv.x - wq.x, y0 = v0 - zq0;
+        const double s1 = wv.y - wq.y, y1 = v1 - zq1;
+        r4[1] += s0 * s0 + s1 * s1;
+        r4[2] += s0 * y0 + s1 * y1;
+        r4[3] += y0 * y0 + y1 * y1;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double v = r4[r];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      const int row_out = r == 0 ? 0 : r + 1;  // [zz | dd | ss | sy | yy]
+      if (gq == 0 && live && (hist || r == 0)) dpart[((int64_t)row_out * N + i) * n_pt + pt] = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(XTH, 1) dir_big_kernel(
+    const __grid_constant__ Maps5 maps, int N, int64_t ld, int64_t ngl, int n_pt, int n_it, int hist,
+    const double* __restrict__ sig, const double* __restrict__ sigp, double* __restrict__ zout,
+    double* __restrict__ sig_save, double* __restrict__ dpart) {
+  PO_PDL_ENTRY();
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(tsm);
+  uint64_t* emptyA = fullA + 8;
+  uint64_t* fullE = fullA + 16;
+  uint64_t* emptyE = fullA + 24;
+  constexpr size_t QA = (size_t)XP * XK;  // doubles per block per stage
+  constexpr size_t SA = 2 * QA;           // ring A stage: W + Sigma^T box
+  constexpr size_t SE = 3 * QE;           // ring E stage: HW, W_prev, HW_prev / Z_prev
+  double* ringA = reinterpret_cast<double*>(tsm + 1024);
+  double* ringE = ringA + DNA * SA;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < DNA; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&emptyA[s], 8);
+    }
+    for (int s = 0; s < DNE; ++s) {
+      mbar_init(&fullE[s], 1);
+      // every consumer warp waits on and releases every E stage (only the two
+      // owning the stage's fragments read it): with parity waits a warp must
+      // never skip a phase of a slot, or a stale phase could satisfy its wait
+      mbar_init(&emptyE[s], 8);
+    }
+    fence_mbar_init();
+  }
+  if (sig_save && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sig_save[i] = sig[i];
+  __syncthreads();
+  const int ntiles = n_pt * n_it;
+  const int nk = (N + XK - 1) / XK;
+  auto tile_of = [&](int t, int& pt, int& it) {
+    it = n_it - 1 - t / n_pt;
+    pt = t % n_pt;
+  };
+  const int lane = threadIdx.x & 31;
+  int warp = threadIdx.x >> 5;
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (warp == 0 && lane == 0) {  // ring A: W + Sigma^T for every stage
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[0])));
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[1])));
+      int g = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int pt, it;
+        tile_of(t, pt, it);
+        for (int c = 0; c < nk; ++c, ++g) {
+          const int s = g % DNA;
+          if (g >= DNA) mbar_wait(&emptyA[s], ((uint32_t)(g / DNA) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&fullA[s], (uint32_t)(SA * 8));
+          double* sb = ringA + (size_t)s * SA;
+          for (int b = 0; b < XP / BOX; ++b)
+            tma_load_2d(sb + b * BOX * XK, &maps.m[0], pt * XP + b * BOX, c * XK, &fullA[s]);
+          tma_load_2d(sb + QA, &maps.m[1], c * XK, it * XI, &fullA[s]);
+        }
+      }
+    } else if (warp == 1 && lane == 0) {  // ring E: the tile's own orbitals only
+      const int ne = hist ? 3 : 1;
+      for (int q = 0; q < ne; ++q)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[2 + q])));
+      int ge = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int pt, it;
+        tile_of(t, pt, it);
+        const int c1 = min(nk, (it + 1) * (XI / XK));
+        for (int c = it * (XI / XK); c < c1; ++c, ++ge) {
+          const int s = ge % DNE;
+          if (ge >= DNE) mbar_wait(&emptyE[s], ((uint32_t)(ge / DNE) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&fullE[s], (uint32_t)(ne * QE * 8));
+          double* sb = ringE + (size_t)s * SE;
+          for (int q = 0; q < ne; ++q)
+            tma_load_2d(sb + q * QE, &maps.m[2 + q], pt * XP, c * XK, &fullE[s]);
+        }
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    warp -= 4;
+    const int gq = lane >> 2, t4 = lane & 3;
+    const int F0 = warp, F1 = 15 - warp;  // this warp's output fragments
+    int g = 0, ge = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int pt, it;
+      tile_of(t, pt, it);
+      const int i0 = it * XI;
+      const bool real0 = i0 + 8 * F0 < N, real1 = i0 + 8 * F1 < N;  // padding fragments
+      const int64_t p0 = (int64_t)pt * XP;
+      double acc[2][16][2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 16; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+      for (int c = 0; c < nk; ++c, ++g) {
+        const int s = g % DNA;
+        mbar_wait(&fullA[s], (uint32_t)(g / DNA) & 1u);
+        const double* sb = ringA + (size_t)s * SA;
+        const double* mt = sb + QA;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k8 = c * XK + 8 * h;
+          if (k8 >= N) break;
+          const double2 b0 = *reinterpret_cast<const double2*>(mt + swz(8 * F0 + gq, 8 * h + 2 * t4, XI));
+          const double2 b1 = *reinterpret_cast<const double2*>(mt + swz(8 * F1 + gq, 8 * h + 2 * t4, XI));
+          if (real0 && real1)
+            mix_big_slice<true, true>(acc, sb, nullptr, 0.0, b0, b1, h, gq, t4);
+          else if (real0)
+            mix_big_slice<true, false>(acc, sb, nullptr, 0.0, b0, b1, h, gq, t4);
+        }
+        const int crel = c - it * (XI / XK);  // diagonal stage index within the tile
+        if (crel >= 0 && crel < XI / XK) {
+          const bool upper_half = crel >= 4;  // fragments 2 crel, 2 crel + 1 are >= 8: the F1 side
+          const int F = upper_half ? F1 : F0;
+          const int se = ge % DNE;
+          mbar_wait(&fullE[se], (uint32_t)(ge / DNE) & 1u);
+          if ((F >> 1) == crel && (upper_half ? real1 : real0)) {
+            const double* sbe = ringE + (size_t)se * SE;
+            if (upper_half)
+              dir_big_elementwise<1>(acc, sb, sbe, hist, F & 1, gq, t4, i0, F, N, ld, ngl, p0, sig,
+                                     sigp, zout, dpart, n_pt, pt);
+            else
+              dir_big_elementwise<0>(acc, sb, sbe, hist, F & 1, gq, t4, i0, F, N, ld, ngl, p0, sig,
+                                     sigp, zout, dpart, n_pt, pt);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&emptyE[se]);
+          ++ge;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyA[s]);
+      }
+      // ||D_i||^2 from the registers: acc = W Sigma - HW = -D
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (!(q ? real1 : real0)) continue;
+        const int F = q ? F1 : F0;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = i0 + 8 * F + 2 * t4 + j;
+          double v = 0.0;
+#pragma unroll
+          for (int gg = 0; gg < 8; ++gg) {
+            const double d0 = acc[q][2 * gg][j], d1 = acc[q][2 * gg + 1][j];
+            v += d0 * d0 + d1 * d1;
+          }
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          if (gq == 0 && i < N) dpart[((int64_t)N + i) * n_pt + pt] = v;
+        }
+      }
+    }
+  }
+}
+
+
 // Upper-triangular mix (the orthonormalisation rotation W L^{-T}) with the
 // triangle balanced per SM sub-partition. A 128-point tile is split into two
 // 64-point halves: consumer warps 0-3 (one per sub-partition) walk the k
@@ -2195,7 +2485,7 @@ __device__ __forceinline__ void mix_tri_slice(double (&acc)[4][8][2], const doub
 __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
     const __grid_constant__ Maps maps, int has_ab, int N, int64_t ld, int64_t ngl, int n_pt,
     int n_it, int nst, double sa, double alpha, double* __restrict__ out,
-    const double* __restrict__ guard) {
+    const double* __restrict__ guard, const double* __restrict__ zsig) {
   PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
@@ -2203,6 +2493,7 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm);
   uint64_t* empty = full + 8;
   uint64_t* ready = full + 16;
+  double* mst = reinterpret_cast<double*>(tsm + 512);  // -sigma of a stage (implicit z)
   double* stage0 = reinterpret_cast<double*>(tsm + 1024);
   constexpr size_t QH = (size_t)64 * XK;  // doubles per half per source per stage
   constexpr size_t QM = (size_t)XI * XK;  // one M^T box
@@ -2264,9 +2555,21 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
           mbar_wait(&full[s], (uint32_t)(g / nst) & 1u);
           double2* a2 = reinterpret_cast<double2*>(stage0 + (size_t)s * sdoubles);
           const double2* b2 = reinterpret_cast<const double2*>(stage0 + (size_t)s * sdoubles + 2 * QH);
+          if (zsig) {  // -sigma of the stage's 2 x 16 orbitals (half 1 walks k backwards)
+            if (ct < 2 * XK) {
+              const int k = ((ct >= XK) ? nk - 1 - c : c) * XK + (ct & (XK - 1));
+              mst[ct] = k < N ? -zsig[k] : 0.0;
+            }
+            asm volatile("bar.sync 2, 96;\n" ::: "memory");
+          }
           for (int e = ct; e < (int)QH; e += 96) {  // 2 * QH doubles = QH double2
             double2 v = a2[e];
-            const double2 z = b2[e];
+            double2 z = b2[e];
+            if (zsig) {  // Ab is HW: z = HW - sigma_k W (the directions pass's FMA)
+              const double ms = mst[((2 * e) / (int)QH) * XK + ((e & 127) >> 3)];
+              z.x = fma(ms, v.x, z.x);
+              z.y = fma(ms, v.y, z.y);
+            }
             v.x += sa * z.x;
             v.y += sa * z.y;
             a2[e] = v;
@@ -2375,7 +2678,8 @@ int mix_big_nblk(int64_t ngl) { return (int)((ngl + XP - 1) / XP); }
 
 int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
                    const double* M, double alpha, const double* C, double beta, int upper,
-                   double* out, double* norms, cudaStream_t s, const double* guard) {
+                   double* out, double* norms, cudaStream_t s, const double* guard,
+                   const double* zsig) {
   static const bool off = getenv("PO_NO_MIX_BIG") != nullptr;  // measurement: tiled LDG mix
   static const bool dbg = getenv("PO_MIX_DEBUG") != nullptr;
 #define PO_MB_FAIL(why)                                                 \
@@ -2413,35 +2717,34 @@ int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double
     set_smem(reinterpret_cast<const void*>(mix_tri_kernel), (int)smem);
     ::po::count_launch();
     launch_pdl(mix_tri_kernel, dim3(grid), dim3(XTH), smem, s, maps, Ab ? 1 : 0, N, ld, ngl, n_pt, n_it,
-               nst, sa, alpha, out, guard);
+               nst, sa, alpha, out, guard, Ab ? zsig : (const double*)nullptr);
     return n_pt;
   }
-  set_smem(reinterpret_cast<const void*>(mix_big_kernel<false>), (int)smem);
+  set_smem(reinterpret_cast<const void*>(mix_big_kernel), (int)smem);
   ::po::count_launch();
-  launch_pdl(mix_big_kernel<false>, dim3(grid), dim3(XTH), smem, s, maps, Ab ? 1 : 0, N, ld, ngl, n_pt,
-             n_it, upper, nst, sa, alpha, C, beta, out, norms, guard, (const double*)nullptr,
-             (const double*)nullptr, (const double*)nullptr, (const double*)nullptr, (double*)nullptr,
-             (double*)nullptr);
+  launch_pdl(mix_big_kernel, dim3(grid), dim3(XTH), smem, s, maps, Ab ? 1 : 0, N, ld, ngl, n_pt,
+             n_it, upper, nst, sa, alpha, C, beta, out, norms, guard, Ab ? zsig : (const double*)nullptr);
   return n_pt;
 }
 
 int launch_directions_big(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
-                          const double* WP, const double* ZP, const double* Sigma, const double* sig,
-                          double* Z, double* partials, cudaStream_t s) {
+                          const double* WP, const double* XP_, const double* sig_prev,
+                          const double* Sigma, const double* sig, double* Z, double* sig_save,
+                          double* partials, cudaStream_t s) {
   static const int off = getenv("PO_NO_DIR_BIG") ? atoi(getenv("PO_NO_DIR_BIG")) : 0;  // measurement
   if (off || N <= 64 || !tma2d_available()) return -1;
+  const int hist = WP != nullptr;
   const int np = (N + 15) & ~15;
   double* mt = mix_big_scratch(s, (size_t)np * np);
   if (!mt) return -1;
-  Maps maps;
+  Maps5 maps;
   std::memset(&maps, 0, sizeof maps);
   if (!make_map(&maps.m[0], W, ld, N, XK)) return -1;
   if (!make_map(&maps.m[1], mt, np, np, XI)) return -1;
-  const size_t sdoubles = (size_t)2 * XP * XK;
-  const size_t fixed = 1024 + 1024;
-  int nst = (int)((200 * 1024 - fixed) / (sdoubles * 8));
-  if (nst > 8) nst = 8;
-  const size_t smem = fixed + (size_t)nst * sdoubles * 8;
+  if (!make_map(&maps.m[2], HW, ld, N, XK, EW)) return -1;
+  if (hist && (!make_map(&maps.m[3], WP, ld, N, XK, EW) || !make_map(&maps.m[4], XP_, ld, N, XK, EW)))
+    return -1;
+  const size_t smem = 2048 + ((size_t)DNA * 2 * XP * XK + (size_t)DNE * 3 * QE) * 8;
   ::po::count_launch();
   launch_pdl(transpose_pad_kernel, dim3((unsigned)(((int64_t)np * np + 255) / 256)), dim3(256), 0, s, N,
              np, Sigma, mt);
@@ -2449,11 +2752,10 @@ int launch_directions_big(int N, int64_t ld, int64_t ngl, const double* W, const
   const int n_it = (N + XI - 1) / XI;
   const int ntiles = n_pt * n_it;
   const int grid = ntiles < nsm() ? ntiles : nsm();
-  set_smem(reinterpret_cast<const void*>(mix_big_kernel<true>), (int)smem);
+  set_smem(reinterpret_cast<const void*>(dir_big_kernel), (int)smem);
   ::po::count_launch();
-  launch_pdl(mix_big_kernel<true>, dim3(grid), dim3(XTH), smem, s, maps, 0, N, ld, ngl, n_pt, n_it, 0,
-             nst, 0.0, -1.0, HW, 1.0, (double*)nullptr, (double*)nullptr, (const double*)nullptr, W, sig,
-             WP, ZP, Z, partials);
+  launch_pdl(dir_big_kernel, dim3(grid), dim3(XTH), smem, s, maps, N, ld, ngl, n_pt, n_it, hist, sig,
+             hist ? sig_prev : (const double*)nullptr, Z, sig_save, partials);
   return n_pt;
 }
 

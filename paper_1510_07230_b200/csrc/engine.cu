@@ -138,6 +138,7 @@ Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist
 }
 
 Engine::~Engine() {
+  free_staging();
   if (s) cudaStreamSynchronize(s);
   for (double* b : blocks_)
     if (b) cudaFree(b);
@@ -404,9 +405,10 @@ void Engine::gram(const double* A, const double* Ab, double sa, const double* B,
 
 void Engine::mix(const double* A, const double* Ab, double sa, const double* M, double alpha,
                  const double* C, double beta, int upper, double* out, double* norm_rows,
-                 const double* guard) {
+                 const double* guard, const double* zsig) {
   const int nb = launch_mix(g, N, A, Ab, sa, M, alpha, C, beta, upper, out,
-                            norm_rows ? partials : nullptr, s, guard);
+                            norm_rows ? partials : nullptr, s, guard, zsig);
+  if (nb == -2) throw Error(PO_EINVAL, "mix: implicit direction unavailable on this path");
   if (norm_rows) reduce_rows(partials, N, nb, g.w, norm_rows, true);
 }
 
@@ -511,8 +513,8 @@ int po_free_block(po_engine* h, int block) {
 int po_upload_block(po_engine* h, int block, const double* host) {
   ENGINE_OR_EINVAL(h);
   API_TRY
-  PO_CUDA(cudaMemcpy2DAsync(E.blk(block), E.g.ld * 8, host, E.g.ngl * 8, E.g.ngl * 8, E.N,
-                            cudaMemcpyHostToDevice, E.s));
+  if (!host) throw Error(PO_EINVAL, "upload_block: null host buffer");
+  E.upload_host(E.blk(block), host, E.s);  // pageable buffers: pinned chunk pipeline (staging.cu)
   E.sync();
   API_CATCH(h)
 }
@@ -520,9 +522,8 @@ int po_upload_block(po_engine* h, int block, const double* host) {
 int po_download_block(po_engine* h, int block, double* host) {
   ENGINE_OR_EINVAL(h);
   API_TRY
-  PO_CUDA(cudaMemcpy2DAsync(host, E.g.ngl * 8, E.blk(block), E.g.ld * 8, E.g.ngl * 8, E.N,
-                            cudaMemcpyDeviceToHost, E.s));
-  E.sync();
+  if (!host) throw Error(PO_EINVAL, "download_block: null host buffer");
+  E.download_host(host, E.blk(block), E.s);
   API_CATCH(h)
 }
 
@@ -921,10 +922,19 @@ extern "C" int po_enqueue(po_engine* h, int op, int a, int b, int out) {
       // the iteration's form: z implicit (not stored), previous z from the previous
       // HW (here b again) and sigma row; out is not written
       (void)out;
-      if (po::launch_directions(E.N, E.g.ld, E.g.ngl, E.blk(a), E.blk(b), E.blk(a), E.blk(b),
-                                E.dmat[0], E.dvec, nullptr, E.partials, E.s, E.dvec,
-                                E.dvec + E.off_zsig(0)) < 0)
+      if ((E.N > 64 ? po::launch_directions_big(E.N, E.g.ld, E.g.ngl, E.blk(a), E.blk(b), E.blk(a),
+                                                E.blk(b), E.dvec, E.dmat[0], E.dvec, nullptr,
+                                                E.dvec + E.off_zsig(0), E.partials, E.s)
+                    : po::launch_directions(E.N, E.g.ld, E.g.ngl, E.blk(a), E.blk(b), E.blk(a),
+                                            E.blk(b), E.dmat[0], E.dvec, nullptr, E.partials, E.s,
+                                            E.dvec, E.dvec + E.off_zsig(0))) < 0)
         throw Error(PO_EINVAL, "directions kernel unavailable for this N");
+      break;
+    case PO_OP_ROTATION_IMPLICIT:
+      // the large-N trial rotation: b is HW, z = HW - sigma W rebuilt per element
+      if (po::launch_mix(E.g, E.N, E.blk(a), E.blk(b), -0.3, E.dmat[1], 1.0, nullptr, 0.0, 1,
+                         E.blk(out), nullptr, E.s, nullptr, E.dvec + E.off_sig()) < 0)
+        throw Error(PO_EINVAL, "implicit rotation unavailable for this N");
       break;
     default:
       if (op >= PO_OP_HAMILTONIAN_VARIANT &&

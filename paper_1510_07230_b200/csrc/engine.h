@@ -122,7 +122,7 @@ class Engine {
             double sb, int sym, double* Gdev, const double* guard = nullptr);
   void mix(const double* A, const double* Ab, double sa, const double* M, double alpha,
            const double* C, double beta, int upper, double* out, double* norm_rows,
-           const double* guard = nullptr);
+           const double* guard = nullptr, const double* zsig = nullptr);
   // CG outcome + E_H / E_xc / E_ext of the last build from the last fetch (no sync)
   void state_results(DevState* st);
   void reduce_rows(const double* partials, int rows, int nblk, double scale, double* out,
@@ -141,6 +141,17 @@ class Engine {
   unsigned long long pub_seq = 0;
   double* dmat[10] = {};       // N x N device matrices ([7] G_HH, [8] G_WW of the iterate)
   double* hmat = nullptr;      // pinned N x N host
+  // host <-> device block transfers (staging.cu): pinned buffers go straight to
+  // the copy engine, pageable ones through two pinned chunks filled / drained by
+  // several host threads while the other chunk is in flight
+  static constexpr size_t kStageBytes = size_t(32) << 20;
+  double* stage_h[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  void ensure_staging();
+  void free_staging();
+  int host_threads() const;
+  void upload_host(double* dev, const double* host, cudaStream_t st);    // async for pinned
+  void download_host(double* host, const double* dev, cudaStream_t st);  // returns when complete
   double* chol_L = nullptr;    // N x N scratch
   double* syev_work = nullptr;
   double* halo_lo = nullptr;   // recv planes (N x plane) or null

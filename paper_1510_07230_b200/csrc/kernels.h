@@ -96,9 +96,13 @@ void launch_gram(const SlabGeom& g, int N, const double* A, const double* Ab, do
 // (may be null) receives partials [N][nblk] of sum_p out_i[p]^2.
 int mix_nblk(const SlabGeom& g);
 int mix_nblk_max(const SlabGeom& g);  // partials buffer sizing (any mix path)
+// zsig (nullable, large-N TMA paths only): Ab is HW and the second source is the
+// implicit direction z = HW - zsig_k W (rebuilt per element with the FMA the
+// directions pass uses); -2 when no path can take it.
 int launch_mix(const SlabGeom& g, int N, const double* A, const double* Ab, double sa,
                 const double* M, double alpha, const double* C, double beta, int upper,
-                double* out, double* norms, cudaStream_t s, const double* guard = nullptr);
+                double* out, double* norms, cudaStream_t s, const double* guard = nullptr,
+                const double* zsig = nullptr);
 
 // dmma_tma.cu: 2D tensor-map TMA versions of the small-N Gram / mix (false / -1
 // when unavailable: no driver entry point or N out of range).
@@ -159,13 +163,16 @@ int launch_mix_tma(int N, int64_t ld, int64_t ngl, const double* A, const double
 // norm-partials row length (= mix_nblk) or -1 when unavailable.
 int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double* Ab, double sa,
                    const double* M, double alpha, const double* C, double beta, int upper,
-                   double* out, double* norms, cudaStream_t s, const double* guard);
-// compute_directions for N > 64 on the large-N mix tiles: writes Z = HW - diag(sig) W and
-// partial rows [zz | dd | ss | sy | yy] x n_pt (dd = ||HW - W Sigma||^2; the last three
-// only with WP / ZP). Returns n_pt or -1 when unavailable.
+                   double* out, double* norms, cudaStream_t s, const double* guard,
+                   const double* zsig = nullptr);
+// compute_directions for N > 64 (dir_big_kernel): partial rows [zz | dd | ss | sy | yy]
+// x n_pt. History (WP != null): XP_ is HW_prev with sig_prev (implicit z_prev =
+// HW_prev - sig_prev W_prev) or a stored Z_prev (sig_prev null). Z null: z stays
+// implicit; sig_save (nullable) receives sig for the next iteration's z_prev.
 int launch_directions_big(int N, int64_t ld, int64_t ngl, const double* W, const double* HW,
-                          const double* WP, const double* ZP, const double* Sigma, const double* sig,
-                          double* Z, double* partials, cudaStream_t s);
+                          const double* WP, const double* XP_, const double* sig_prev,
+                          const double* Sigma, const double* sig, double* Z, double* sig_save,
+                          double* partials, cudaStream_t s);
 // Batched left-multiply out_b = S X_b for X_b = rows [N][ld] at A + b * bstride
 // (valid row length ngl; ld multiple of 32, padding zero). DST transforms.
 void launch_mix_batched(int N, int64_t ld, int64_t ngl, int batch, int64_t bstride,

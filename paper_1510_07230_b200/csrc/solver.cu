@@ -19,9 +19,11 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <functional>
 #include <limits>
 #include <memory>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -171,9 +173,10 @@ bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, doubl
   (void)measure;
   double* sc = E.scal();
   // zsig: Ab is HW and the direction z = HW - zsig W is implicit; only the
-  // Grams-based trial Gram and the fused rotation can take it (callers check)
-  if (zsig && !(g0_from_grams && st && E.N <= 48 && tma2d_available()))
-    throw Error(PO_EINVAL, "implicit direction outside the fused trial path");
+  // Grams-based trial Gram and the TMA rotations (fused small-N / large-N
+  // tiles) can take it (callers check)
+  if (zsig && !(g0_from_grams && st && tma2d_available() && (E.N <= 48 || E.N > 64)))
+    throw Error(PO_EINVAL, "implicit direction outside the TMA trial paths");
   // G0 of W - tau Z from G_WW (dmat[8]), Sigma (dmat[4]), G_HH (dmat[7]), its stats and
   // its Cholesky in one launch where possible
   if (!(g0_from_grams &&
@@ -205,8 +208,8 @@ bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, doubl
     }
   }
   if (!fused) {
-    if (tau_dev || zsig) throw Error(PO_EINVAL, "device-side trial scale needs the fused rotation");
-    E.mix(A, Ab, sa, E.dmat[1], 1.0, nullptr, 0.0, 1, out, nullptr);
+    if (tau_dev) throw Error(PO_EINVAL, "device-side trial scale needs the fused rotation");
+    E.mix(A, Ab, sa, E.dmat[1], 1.0, nullptr, 0.0, 1, out, nullptr, nullptr, zsig);
     E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2]);
   }
   launch_matrix_stats(E.N, E.dmat[2], sc + Engine::S_MSTAT2, E.s);
@@ -394,6 +397,7 @@ struct Solver {
     Clock::time_point t0;
     bool orth_iter = false, need_full = false, fused = false;
     bool zv = false;  // z implicit (see prev_hw); zsig slot zslot
+    bool bigdir = false;  // the directions ran as dir_big_kernel (N > 64)
     int zslot = 0;
     BRef z, dscratch;
     struct {
@@ -477,11 +481,14 @@ void Solver::enqueue_phase1(int iter) {
     ghh_fresh = false;  // G_HH (dmat[7]) belongs to this iteration's HW only
     static const bool zfree_env = !std::getenv("PO_ZFREE") || std::atoi(std::getenv("PO_ZFREE")) != 0;
     const bool fused_dir = !full_grad && !(mean_abs && need_full) && n <= 48 && tma2d_available();
+    // N > 64: dir_big_kernel (z implicit or stored, z_prev implicit or stored)
+    const bool big_dir = !fused_dir && !full_grad && need_full && !mean_abs && E.size == 1 && n > 64 &&
+                         tma2d_available();
     // implicit z: only where every consumer is the fused rotation of a trial
     // whose Gram comes from the iteration's Grams (nonlinear, orthonormalised
     // every iteration); the rare other consumers materialise it
     ph.zslot = prev_zv ? prev_zslot ^ 1 : 0;
-    if (!fused_dir) materialize_prev_z();
+    if (!fused_dir && !big_dir) materialize_prev_z();
     if (fused_dir) {
       // one pass: z, ||z||^2, ||HW - W Sigma||^2 and the BB products
       if (need_full || !sig_valid) {
@@ -507,6 +514,8 @@ void Solver::enqueue_phase1(int iter) {
         fused = true;
       }
     }
+    if (big_dir)  // z stays implicit where every consumer can rebuild it (see the fused path)
+      ph.zv = zfree_env && orth_iter && n_org == 1 && nonlinear && gww_valid;
     if (!z && !ph.zv) z = pool.get();
     if (fused) {
     } else if (full_grad) {
@@ -529,12 +538,27 @@ void Solver::enqueue_phase1(int iter) {
         launch_copy_diag(n, E.dmat[4], E.dvec + E.off_sig(), E.s);
       }
       int dnb = -1;
-      if (need_full && !mean_abs && E.size == 1)
-        // z, ||z||^2, ||HW - W Sigma||^2 and the BB products on the large-N mix tiles
-        dnb = launch_directions_big(n, E.g.ld, E.g.ngl, P(w), P(hw),
-                                    history_valid ? P(prev_w) : nullptr,
-                                    history_valid ? P(prev_z) : nullptr, E.dmat[4],
-                                    E.dvec + E.off_sig(), P(z), E.partials, E.s);
+      if (big_dir) {
+        if (ph.zv && !ghh_fresh) {  // the trial Grams need G_HH: no implicit z without it
+          ph.zv = false;
+          z = pool.get();
+        }
+        // z (implicit or stored), ||z||^2, ||HW - W Sigma||^2 and the BB products
+        // against (W_prev, z_prev) in one TMA pass (dir_big_kernel)
+        dnb = launch_directions_big(
+            n, E.g.ld, E.g.ngl, P(w), P(hw), history_valid ? P(prev_w) : nullptr,
+            history_valid ? (prev_zv ? P(prev_hw) : P(prev_z)) : nullptr,
+            history_valid && prev_zv ? zsig(prev_zslot) : nullptr, E.dmat[4], E.dvec + E.off_sig(),
+            ph.zv ? nullptr : P(z), ph.zv ? E.dvec + E.off_zsig(ph.zslot) : nullptr, E.partials, E.s);
+        if (dnb < 0) {  // unavailable: the stored-direction passes below
+          if (ph.zv) {
+            ph.zv = false;
+            z = pool.get();
+          }
+          materialize_prev_z();
+        }
+        ph.bigdir = dnb >= 0;
+      }
       if (dnb >= 0) {
         E.reduce_rows(E.partials, (history_valid ? 5 : 2) * n, dnb, E.g.w, E.dvec + E.off_zz(), true);
         bb_done = history_valid;
@@ -568,7 +592,7 @@ void Solver::enqueue_phase1(int iter) {
     // reads the directions and the trial together; a converged / failing
     // iteration simply discards the speculative trial.
     auto& spec = ph.spec;
-    if (ph.zv && !(orth_iter && fused && gww_valid && ghh_fresh && nonlinear)) {
+    if (ph.zv && !(orth_iter && (fused || ph.bigdir) && gww_valid && ghh_fresh && nonlinear)) {
       z = materialize_z(w, hw, ph.zslot);  // no fused first trial: write z out
       ph.zv = false;
     }
@@ -1096,8 +1120,7 @@ int po_solve_host(po_engine* h, const po_params* p, const double* w_in, double* 
   try {
     validate_params(p);
     w_handle = E.take_block();
-    PO_CUDA(cudaMemcpy2DAsync(E.blk(w_handle), E.g.ld * 8, w_in, E.g.ngl * 8, E.g.ngl * 8, E.N,
-                              cudaMemcpyHostToDevice, E.s));
+    E.upload_host(E.blk(w_handle), w_in, E.s);  // pageable input: pinned chunk pipeline
     E.gram(E.blk(w_handle), nullptr, 0.0, E.blk(w_handle), nullptr, 0.0, 1, E.dmat[2]);
     po::launch_matrix_stats(E.N, E.dmat[2], E.scal() + Engine::S_MSTAT2, E.s);
     E.fetch(E.off_scal(), 64);
@@ -1108,10 +1131,24 @@ int po_solve_host(po_engine* h, const po_params* p, const double* w_in, double* 
     PO_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     PO_CUDA(cudaEventRecord(ev, E.s));
     PO_CUDA(cudaStreamWaitEvent(side, ev, 0));
-    PO_CUDA(cudaMemcpy2DAsync(w_out, E.g.ngl * 8, E.blk(w_handle), E.g.ld * 8, E.g.ngl * 8, E.N,
-                              cudaMemcpyDeviceToHost, side));
-    finalize_grad(E, p, w_handle, r);
-    PO_CUDA(cudaStreamSynchronize(side));
+    // the download (a host thread drives the staging pipeline for pageable
+    // output) overlaps the finalize pass, which only reads W
+    std::exception_ptr dl_err;
+    std::thread dl([&] {
+      try {
+        E.download_host(w_out, E.blk(w_handle), side);
+      } catch (...) {
+        dl_err = std::current_exception();
+      }
+    });
+    try {
+      finalize_grad(E, p, w_handle, r);
+    } catch (...) {
+      dl.join();
+      throw;
+    }
+    dl.join();
+    if (dl_err) std::rethrow_exception(dl_err);
   } catch (const Error& ex) {
     if (side) cudaStreamSynchronize(side);
     if (side) cudaStreamDestroy(side);

@@ -210,3 +210,50 @@ print(json.dumps([x["energy"] for x in r.records] + [r.energy["total"]]))
     for name in ("split", "dir8", "nodefer", "repair", "zstored"):
         assert len(runs[name]) == len(runs["base"])
         assert max(abs(x - y) for x, y in zip(runs[name], runs["base"])) < 1e-9, name
+
+
+@pytest.mark.parametrize("n_orb", [80, 128])
+def test_large_n_direction_paths_agree(port, native, n_orb):
+    """N > 64 directions (dir_big_kernel): the implicit z = HW - sigma W (default;
+    the rotation rebuilds it per element), the stored z (PO_ZFREE=0, written by
+    the same kernel) and the separate residual / BB / gradient-norm passes
+    (PO_NO_DIR_BIG=1) give the same trajectory (bitwise z; sums reduced in
+    another order) and match the C restatement. N = 80 takes the dense
+    mix_big rotation, N = 128 the balanced triangular one."""
+    import json
+    import subprocess
+    import sys
+    spec = configs.small_molecule(14, n_orb, L=8.0, max_inner=6)
+    spec.algorithm = "opt_par_mod"
+    u0 = port.random_orthonormal(spec)
+    ref = port.solve(spec, u0=u0, trace_eigs=False)
+    code = r'''
+import json, sys
+import numpy as np
+sys.path.insert(0, %r)
+from paper_1510_07230_b200 import configs, native
+spec = configs.small_molecule(14, %d, L=8.0)
+e = native.engine_for(spec)
+w = e.block_from(np.load(sys.argv[1]))
+r = e.solve(w, "opt_par_mod", True, True, max_inner=6, n_org=1, n_diag=100)
+print(json.dumps([[x["energy"], x["backtracks"], x["grad_norm"]] for x in r.records] + [r.energy["total"]]))
+''' % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), n_orb)
+    import tempfile
+    runs = {}
+    with tempfile.TemporaryDirectory() as d:
+        np.save(os.path.join(d, "u0.npy"), u0)
+        for name, env_over in [("implicit", {}), ("stored", {"PO_ZFREE": "0"}),
+                               ("separate", {"PO_NO_DIR_BIG": "1"})]:
+            env = {k: v for k, v in os.environ.items() if not k.startswith("PO_")}
+            env.update(env_over)
+            r = subprocess.run([sys.executable, "-c", code, os.path.join(d, "u0.npy")], capture_output=True,
+                               text=True, env=env, timeout=300)
+            assert r.returncode == 0, (name, r.stderr[-2000:])
+            runs[name] = json.loads(r.stdout.strip().split("\n")[-1])
+    base = runs["implicit"]
+    for name in ("stored", "separate"):
+        for a, b in zip(runs[name][:-1], base[:-1]):
+            assert a[1] == b[1] and abs(a[0] - b[0]) < 1e-9 and abs(a[2] - b[2]) < 1e-9 * max(1.0, b[2]), name
+    for a, b in zip(base[:-1], ref["records"]):
+        assert abs(a[0] - b["energy"]) < TOL_E and a[1] == b["backtracks"]
+        assert abs(a[2] - b["grad_norm"]) < 1e-8 * max(1.0, b["grad_norm"])

@@ -59,6 +59,8 @@ res["mix_upper"] = timeit(e, lambda: e.enqueue("mix_upper", a=w, out=out))
 res["mix_full"] = timeit(e, lambda: e.enqueue("mix", a=w, out=out))
 res["rotation_fused"] = timeit(e, lambda: e.enqueue("rotation_fused", a=w, b=z, out=out))
 e.enqueue("gram", a=hw, b=w)
+res["rotation_implicit"] = timeit(e, lambda: e.enqueue("rotation_implicit", a=w, b=hw, out=out))
+e.enqueue("gram", a=hw, b=w)
 res["directions"] = timeit(e, lambda: e.enqueue("directions", a=w, b=hw, out=out))
 res["density_xc"] = timeit(e, lambda: e.enqueue("density_xc", a=w))
 res["poisson"] = timeit(e, lambda: e.enqueue("poisson"), reps=10)
@@ -68,9 +70,11 @@ fp64 = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["fp64_t
 ng = spec.num_points
 tri, full = N * (N + 1) * ng, 2 * N * N * ng
 flops = {"gram_sym(G2)": tri, "gram_trial(G0)": tri, "gram_nonsym(Sigma)": full, "rotation": tri,
-         "mix_upper": tri, "mix_full": full, "rotation_fused": 2 * tri}
+         "mix_upper": tri, "mix_full": full, "rotation_fused": 2 * tri, "rotation_implicit": tri,
+         "directions": full}
 bytes_ = {"hamiltonian": 2 * blk, "gram_sym(G2)": blk, "gram_trial(G0)": 2 * blk,
           "gram_nonsym(Sigma)": 2 * blk, "rotation": 3 * blk, "rotation_fused": 3 * blk, "directions": 4 * blk,
+          "rotation_implicit": 3 * blk,
           "density_xc": blk, "mix_upper": 2 * blk, "mix_full": 2 * blk}
 for k, v in res.items():
     frac = f"{bytes_[k] / v / 1e3 / hbm:.2f} of HBM" if k in bytes_ else ""
