@@ -47,6 +47,10 @@ void run(const char* name, void (*k)(double*, int), double flops_per_inst_warp, 
     k<<<sms, warps * 32>>>(d, iters);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
+    if (cudaGetLastError() != cudaSuccess) {  // e.g. too many registers for the block size
+      printf("%s chains=%d warps/SM=%2d : launch failed\n", name, CH, warps);
+      continue;
+    }
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     const double fl = (double)sms * warps * iters * CH * flops_per_inst_warp;
