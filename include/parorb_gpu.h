@@ -278,7 +278,8 @@ enum {
   PO_OP_DIRECTIONS = 11, /* fused directions: W = a, HW = b, history (a, b), Sigma = last Gram */
   PO_OP_ROTATION_FUSED = 12, /* rotation + verification Gram + density/xc (default state) */
   PO_OP_ROTATION_IMPLICIT = 13, /* out = (a - 0.3 z) M with z = b - sigma a implicit (b = HW; N > 64) */
-  PO_OP_HAMILTONIAN_VARIANT = 100  /* + v: H a design-space variants (measurement only) */
+  PO_OP_HAMILTONIAN_VARIANT = 100  /* + v: H a design-space variants (measurement builds only:
+                                      make VARIANTS=1; else PO_EINVAL) */
 };
 int po_enqueue(po_engine* e, int op, int a, int b, int out);
 int po_set_matrix(po_engine* e, const double* m_host);

@@ -937,11 +937,13 @@ extern "C" int po_enqueue(po_engine* h, int op, int a, int b, int out) {
         throw Error(PO_EINVAL, "implicit rotation unavailable for this N");
       break;
     default:
+#ifdef PO_MEASUREMENT_VARIANTS  // make VARIANTS=1: the H u design-space probes (tools/hu_*.py)
       if (op >= PO_OP_HAMILTONIAN_VARIANT &&
           po::launch_hamiltonian_variant(op - PO_OP_HAMILTONIAN_VARIANT, E.g, E.N, E.blk(a),
                                          st->v_local, E.v_ext, out >= 0 ? E.blk(out) : nullptr,
                                          E.partials, E.s) == 0)
         break;
+#endif
       throw Error(PO_EINVAL, "unknown op");
   }
   PO_CUDA(cudaGetLastError());

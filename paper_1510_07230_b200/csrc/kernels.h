@@ -26,9 +26,11 @@ int hamiltonian2_nblk(const SlabGeom& g);
 void launch_hamiltonian2(const SlabGeom& g, int N, const double* u, const double* halo_lo,
                          const double* halo_hi, const double* v_local, const double* v_ext,
                          double* hu, double* partials, cudaStream_t s);
+#ifdef PO_MEASUREMENT_VARIANTS  // make VARIANTS=1 (measurement-only H u variants)
 int launch_hamiltonian_variant(int v, const SlabGeom& g, int N, const double* u,
                                const double* v_local, const double* v_ext, double* hu,
                                double* partials, cudaStream_t s);
+#endif
 // Plain 7-point Dirichlet Laplacian of every orbital (grid.cpp:94-122).
 void launch_laplacian(const SlabGeom& g, int N, const double* u, const double* halo_lo,
                       const double* halo_hi, double* out, cudaStream_t s);

@@ -188,14 +188,16 @@ __global__ void __launch_bounds__(TX * TY, MINB) hamiltonian2_kernel(
   }
 }
 
+constexpr int MAXJ = 8;  // row-length bound of the full-row kernels: n2 <= 32 * MAXJ
+
+#ifdef PO_MEASUREMENT_VARIANTS
 // ---------------------------------------------------------------- v3
 // Full-row tiles: a CTA owns TY whole x-rows (rows y0..y0+7 of a plane are one
 // contiguous TY*n2*8-byte chunk) for a z-range of one orbital; each thread holds
 // the J = ceil(n2/32) columns x = lane + 32 j of its row, so all x-neighbours
 // come from shuffles (chunk boundaries via lane-0/31 broadcasts) and every
 // plane is streamed as large contiguous pieces. y-neighbours are __ldg (L1:
-// the adjacent warps stream those rows). MAXJ bounds n2 <= 32 * MAXJ.
-constexpr int MAXJ = 8;
+// the adjacent warps stream those rows).
 
 template <int J, bool EXT>
 __global__ void __launch_bounds__(TX * TY, 2) hamiltonian3_kernel(
@@ -294,6 +296,8 @@ void launch_h3(const SlabGeom& g, int N, const double* u, const double* lo, cons
 #undef PO_H3
   }
 }
+
+#endif  // PO_MEASUREMENT_VARIANTS
 
 // ---------------------------------------------------------------- v4 (TMA)
 // Plane ring: a CTA owns TY full x-rows (y0 .. y0+TY-1) of ONE orbital over a
@@ -541,10 +545,6 @@ bool h4_supported(const SlabGeom& g) {
 
 }  // namespace
 
-int hamiltonian3_nblk(const SlabGeom& g) {
-  return (int)((g.n1 + TY - 1) / TY) * (int)((g.nz + ZCHUNK2 - 1) / ZCHUNK2);
-}
-
 int hamiltonian2_nblk(const SlabGeom& g) {
   if (h4_supported(g)) {  // TMA ring: (y-tile, z-chunk) grid
     const H4Shape h = h4_shape(g);
@@ -586,6 +586,7 @@ void launch_hamiltonian2(const SlabGeom& g, int N, const double* u, const double
                                                             v_local, nullptr, hu, partials);
 }
 
+#ifdef PO_MEASUREMENT_VARIANTS
 // Design-space probe (po_enqueue(PO_OP_HAMILTONIAN_VARIANT + v)): same math,
 // different register-group depth / occupancy; v = 0 is the first-generation
 // kernel (per-point neighbour loads, with V_ext).
@@ -710,6 +711,7 @@ int launch_hamiltonian_variant(int v, const SlabGeom& g, int N, const double* u,
   }
   return -1;
 }
+#endif  // PO_MEASUREMENT_VARIANTS
 
 int hamiltonian_nblk(const SlabGeom& g) {
   HGrid h = hgrid(g);

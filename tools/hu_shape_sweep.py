@@ -1,4 +1,5 @@
-"""H.u ring-shape sweep across grid sizes (BASELINE configs 2/3/5 grids): every
+"""Needs the measurement build: make -C paper_1510_07230_b200 -B VARIANTS=1.
+H.u ring-shape sweep across grid sizes (BASELINE configs 2/3/5 grids): every
 TMA plane-ring variant (rows per CTA, planes per CTA, ring budget) of
 po_enqueue(PO_OP_HAMILTONIAN_VARIANT + v), CUDA events, HBM fraction of the
 16 B per orbital.point + 8 B per point algorithmic traffic."""

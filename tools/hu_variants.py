@@ -1,6 +1,8 @@
-"""Time the batched H u design variants (C2 block) with CUDA events."""
+"""Needs the measurement build: make -C paper_1510_07230_b200 -B VARIANTS=1.
+Time the batched H u design variants (C2 block) with CUDA events."""
 import sys
-sys.path.insert(0, "/root/repo")
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1510_07230_b200 import configs, native
 
