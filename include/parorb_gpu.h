@@ -86,6 +86,12 @@ int po_create(const po_grid_desc* grid, int n_orbitals, double occupation,
 int po_destroy(po_engine* e);
 const char* po_last_error(const po_engine* e);
 /* Local slab of this rank: first plane and plane count along axis 0. */
+/* The engine's slab decomposition along axis 0 (host only; no GPU needed):
+ * rank r of `size` owns planes [z0, z0 + nz), nz = n0 / size (+1 for the first
+ * n0 % size ranks); its halo planes come from lo_peer / hi_peer (-1 at the
+ * global boundary, where the Dirichlet zero applies, grid.cpp:109-119). */
+int po_slab_plan(int64_t n0, int size, int rank, int64_t* z0, int64_t* nz, int* lo_peer,
+                 int* hi_peer);
 int po_local_slab(const po_engine* e, int64_t* z0, int64_t* nz, int64_t* ng_local);
 /* Total device bytes an engine with these parameters needs for the solver
  * (before allocation); lets callers report "does not fit" instead of failing. */
@@ -116,6 +122,10 @@ int po_gaussian_potential(po_engine* e, const double* wells, int nwells);
 /* i.i.d. N(0,1) block from parorb::Rng(seed) (rng.hpp:13-41), orbital-major,
  * exactly the reference's bits; generated on the host for this rank's slab. */
 int po_random_block(po_engine* e, int block, uint64_t seed);
+/* i.i.d. N(0,1) block filled ON THE DEVICE from a counter hash of (seed, global
+ * point, orbital): independent of the slab decomposition, NOT the reference's
+ * Rng bits — for measurement blocks too large for the host draw (C5). */
+int po_fill_normal(po_engine* e, int block, uint64_t seed);
 /* optimizer.cpp:156-197 initialize_orbitals: Gaussians centred on the atoms
  * (x, y, z, Z, a per atom, cycled over the orbitals; the box centre without
  * atoms) with widths ~ U(0.5, 2) and 1e-2 U(-1, 1) noise from Rng(seed +

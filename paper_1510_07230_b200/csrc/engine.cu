@@ -64,8 +64,8 @@ Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist
   if ((int64_t)n > g.n0 * g.n1 * g.n2)
     throw Error(PO_EINVAL, "make_problem: more orbitals than grid points");
   const int64_t base = g.n0 / size, rem = g.n0 % size;
-  g.nz = base + (rank < rem ? 1 : 0);
-  g.z0 = rank * base + (rank < rem ? rank : rem);
+  int lo_peer, hi_peer;
+  po_slab_plan(g.n0, size, rank, &g.z0, &g.nz, &lo_peer, &hi_peer);
   g.plane = g.n1 * g.n2;
   g.ngl = g.nz * g.plane;
   g.ld = round_up(g.ngl, 32);
@@ -89,6 +89,8 @@ Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist
   size_t pc = 0;
   auto upd = [&](size_t v) { pc = v > pc ? v : pc; };
   upd((size_t)3 * N * hamiltonian_nblk(g));
+  upd((size_t)3 * N * hamiltonian2_nblk(g));
+  if (hamiltonian_split_ok(g)) upd((size_t)3 * N * hamiltonian_split_nblk(g));
   upd((size_t)5 * N * mix_nblk_max(g));  // fused directions: 5 partial rows
   upd((size_t)4 * N * per_orbital_nblk(g, N));  // residual + BB rows
   upd((size_t)2 * points_nblk(g));
@@ -115,6 +117,9 @@ Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist
     PO_CUDA(cudaMalloc(&send_hi, hb));
     PO_CUDA(cudaMemsetAsync(halo_lo, 0, hb, s));
     PO_CUDA(cudaMemsetAsync(halo_hi, 0, hb, s));
+    PO_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    PO_CUDA(cudaEventCreateWithFlags(&ev_pack, cudaEventDisableTiming));
+    PO_CUDA(cudaEventCreateWithFlags(&ev_halo, cudaEventDisableTiming));
   }
   // replicated full-grid Poisson buffers (+ gather staging for size > 1)
   // [full grid | size x max_slab gather staging | max_slab local send slab]
@@ -165,6 +170,10 @@ Engine::~Engine() {
   if (h_cg_d) cudaFreeHost(h_cg_d);
   dst.release();
   comm.reset();
+  if (cs) cudaStreamSynchronize(cs);
+  if (ev_pack) cudaEventDestroy(ev_pack);
+  if (ev_halo) cudaEventDestroy(ev_halo);
+  if (cs) cudaStreamDestroy(cs);
   if (s) cudaStreamDestroy(s);
 }
 
@@ -386,11 +395,30 @@ void Engine::halo_exchange(const double* u) {
 }
 
 void Engine::apply_h(const double* u, double* out, const double* v_local, bool with_ext) {
-  halo_exchange(u);
   const double* lo = (size > 1 && rank > 0) ? halo_lo : nullptr;
   const double* hi = (size > 1 && rank + 1 < size) ? halo_hi : nullptr;
-  launch_hamiltonian2(g, N, u, lo, hi, v_local, with_ext ? v_ext : nullptr, out, partials, s);
-  const int nb = hamiltonian2_nblk(g);
+  const double* ve = with_ext ? v_ext : nullptr;
+  static const bool overlap = !std::getenv("PO_HALO_OVERLAP") || std::atoi(std::getenv("PO_HALO_OVERLAP"));
+  int nb;
+  if (size > 1 && overlap && hamiltonian_split_ok(g)) {
+    // grid.cpp:109-119's axis-0 taps across ranks: the boundary planes go out on
+    // the comm stream while s computes planes 1 .. nz-2 (no remote tap), then
+    // planes 0 and nz-1 with the received neighbours
+    launch_pack_plane(g, N, u, 0, send_lo, s);
+    launch_pack_plane(g, N, u, g.nz - 1, send_hi, s);
+    PO_CUDA(cudaEventRecord(ev_pack, s));
+    PO_CUDA(cudaStreamWaitEvent(cs, ev_pack, 0));
+    launch_hamiltonian_interior(g, N, u, v_local, ve, out, partials, s);
+    comm->halo(send_lo, send_hi, halo_lo, halo_hi, (size_t)N * g.plane, cs);
+    PO_CUDA(cudaEventRecord(ev_halo, cs));
+    PO_CUDA(cudaStreamWaitEvent(s, ev_halo, 0));
+    launch_hamiltonian_boundary(g, N, u, lo, hi, v_local, ve, out, partials, s);
+    nb = hamiltonian_split_nblk(g);
+  } else {
+    halo_exchange(u);
+    launch_hamiltonian2(g, N, u, lo, hi, v_local, ve, out, partials, s);
+    nb = hamiltonian2_nblk(g);
+  }
   // sigma_ii (w), kinetic (-w/2), external (w): one launch over the consecutive rows
   const double sc[3] = {g.w, -0.5 * g.w, g.w};
   launch_reduce_rows_grouped(partials, N, with_ext ? 3 : 2, nb, sc, dvec + off_sig(), s);
@@ -466,6 +494,17 @@ int po_destroy(po_engine* h) {
 }
 
 const char* po_last_error(const po_engine* h) { return h ? h->err.c_str() : "null engine"; }
+
+int po_slab_plan(int64_t n0, int size, int rank, int64_t* z0, int64_t* nz, int* lo_peer,
+                 int* hi_peer) {
+  if (size < 1 || rank < 0 || rank >= size || n0 < size) return PO_EINVAL;
+  const int64_t base = n0 / size, rem = n0 % size;
+  if (nz) *nz = base + (rank < rem ? 1 : 0);
+  if (z0) *z0 = rank * base + (rank < rem ? rank : rem);
+  if (lo_peer) *lo_peer = rank > 0 ? rank - 1 : -1;          // sends it plane z0 - 1
+  if (hi_peer) *hi_peer = rank + 1 < size ? rank + 1 : -1;  // sends it plane z0 + nz
+  return PO_OK;
+}
 
 int po_local_slab(const po_engine* h, int64_t* z0, int64_t* nz, int64_t* ngl) {
   if (!h || !h->e) return PO_EINVAL;
@@ -605,6 +644,14 @@ int po_random_block(po_engine* h, int block, uint64_t seed) {
   po::rng_normals_slab(seed, E.N, E.ng_full, E.g.z0 * E.g.plane, E.g.ngl, host.data());
   PO_CUDA(cudaMemcpy2DAsync(E.blk(block), E.g.ld * 8, host.data(), E.g.ngl * 8, E.g.ngl * 8, E.N,
                             cudaMemcpyHostToDevice, E.s));
+  E.sync();
+  API_CATCH(h)
+}
+
+int po_fill_normal(po_engine* h, int block, uint64_t seed) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  po::launch_fill_normal(E.g, E.N, E.ng_full, seed, E.blk(block), E.s);
   E.sync();
   API_CATCH(h)
 }

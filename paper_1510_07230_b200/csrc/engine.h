@@ -72,6 +72,9 @@ class Engine {
   double h[3], ext[3];
   int rank = 0, size = 1;
   cudaStream_t s = nullptr;
+  // size > 1: the halo exchange runs on cs while s computes the interior planes
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
   std::unique_ptr<Comm> comm;
   std::string err;
 

@@ -26,6 +26,16 @@ int hamiltonian2_nblk(const SlabGeom& g);
 void launch_hamiltonian2(const SlabGeom& g, int N, const double* u, const double* halo_lo,
                          const double* halo_hi, const double* v_local, const double* v_ext,
                          double* hu, double* partials, cudaStream_t s);
+// Slab H u with the halo exchange overlapped: interior planes 1 .. nz-2 (no
+// halo needed) and, once the neighbours' planes arrived, planes 0 and nz-1;
+// both fill one partials layout of hamiltonian_split_nblk columns (nz >= 3).
+bool hamiltonian_split_ok(const SlabGeom& g);
+int hamiltonian_split_nblk(const SlabGeom& g);
+void launch_hamiltonian_interior(const SlabGeom& g, int N, const double* u, const double* v_local,
+                                 const double* v_ext, double* hu, double* partials, cudaStream_t s);
+void launch_hamiltonian_boundary(const SlabGeom& g, int N, const double* u, const double* halo_lo,
+                                 const double* halo_hi, const double* v_local, const double* v_ext,
+                                 double* hu, double* partials, cudaStream_t s);
 #ifdef PO_MEASUREMENT_VARIANTS  // make VARIANTS=1 (measurement-only H u variants)
 int launch_hamiltonian_variant(int v, const SlabGeom& g, int N, const double* u,
                                const double* v_local, const double* v_ext, double* hu,
@@ -227,6 +237,10 @@ void launch_copy_diag(int N, const double* M, double* out, cudaStream_t s);
 // parorb::Rng(seed) normals (rng.hpp:13-41) drawn orbital-major over the full
 // grid (tests/problems.hpp:59-68); keeps points [offset, offset+count) of each
 // of the N orbitals: out[i * count + k].
+// i.i.d. N(0,1) device fill from a counter hash of (seed, global point, orbital)
+// — measurement blocks (C5), not the reference's Rng bits; padding untouched
+void launch_fill_normal(const SlabGeom& g, int N, int64_t ng_full, uint64_t seed, double* out,
+                        cudaStream_t s);
 void rng_normals_slab(uint64_t seed, int N, int64_t ng_full, int64_t offset, int64_t count,
                       double* out);
 

@@ -338,7 +338,12 @@ template <int J, bool EXT, int TYR>
 __global__ void __launch_bounds__(32 * (TYR + 1), 1) hamiltonian4_kernel(
     SlabGeom g, int N, int nst, int zc, const double* __restrict__ u, const double* __restrict__ halo_lo,
     const double* __restrict__ halo_hi, const double* __restrict__ vloc,
-    const double* __restrict__ vext, double* __restrict__ out, double* __restrict__ partials) {
+    const double* __restrict__ vext, double* __restrict__ out, double* __restrict__ partials,
+    int64_t lo_ld, int64_t hi_ld, int nbtot, int boff) {
+  // lo_ld / hi_ld: orbital stride of the halo planes (g.plane for the exchange
+  // buffers; g.ld when a "halo" is a plane of u itself — the interior / boundary
+  // split of a slab, Engine::apply_h); partials of block b land at column boff + b
+  // of rows of length nbtot (several launches share one reduction)
   PO_PDL_ENTRY();
   extern __shared__ __align__(128) unsigned char hsm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(hsm);
@@ -388,8 +393,8 @@ __global__ void __launch_bounds__(32 * (TYR + 1), 1) hamiltonian4_kernel(
         mbar_arrive_expect_tx(&full[s], bytes);
         if (real) {
           const double* src;
-          if (p < 0) src = halo_lo + (int64_t)i * plane;
-          else if (p >= g.nz) src = halo_hi + (int64_t)i * plane;
+          if (p < 0) src = halo_lo + (int64_t)i * lo_ld;
+          else if (p >= g.nz) src = halo_hi + (int64_t)i * hi_ld;
           else src = ui + p * plane;
           tma_load_1d(us + ra * n2, src + (y0 - 1 + ra) * n2, (uint32_t)((rb - ra) * n2 * 8),
                       &full[s]);
@@ -489,28 +494,35 @@ __global__ void __launch_bounds__(32 * (TYR + 1), 1) hamiltonian4_kernel(
 #pragma unroll
       for (int q = 0; q < 3; ++q) v[q] = warp_sum(lane < TYR ? red[q * 32 + lane] : 0.0);
       if (lane == 0) {
-        const int nblk = gridDim.y * gridDim.z;
-        const int b = blockIdx.y + gridDim.y * blockIdx.z;
+        const int b = boff + blockIdx.y + gridDim.y * blockIdx.z;
 #pragma unroll
-        for (int q = 0; q < 3; ++q) partials[((int64_t)q * N + i) * nblk + b] = v[q];
+        for (int q = 0; q < 3; ++q) partials[((int64_t)q * N + i) * nbtot + b] = v[q];
       }
     }
   }
 }
 
+struct H4Part {  // a launch's place in a shared partials layout + its halo strides
+  int64_t lo_ld = -1, hi_ld = -1;  // -1: g.plane (the exchange buffers)
+  int nbtot = -1, boff = 0;        // -1: this launch's own block count
+};
+
 template <bool EXT, int TYR = 8>
 void launch_h4(const SlabGeom& g, int N, const double* u, const double* lo, const double* hi,
                const double* vloc, const double* vext, double* out, double* partials,
-               cudaStream_t s, int zc = ZCHUNK2, size_t budget = 100 * 1024) {
+               cudaStream_t s, int zc = ZCHUNK2, size_t budget = 100 * 1024, H4Part pt = H4Part()) {
   const PlaneRing r = plane_ring(g, TYR, budget);
   dim3 grid((unsigned)N, (unsigned)((g.n1 + TYR - 1) / TYR), (unsigned)((g.nz + zc - 1) / zc));
   dim3 block(TX, TYR + 1);
+  const int64_t lo_ld = pt.lo_ld < 0 ? g.plane : pt.lo_ld, hi_ld = pt.hi_ld < 0 ? g.plane : pt.hi_ld;
+  const int nbtot = pt.nbtot < 0 ? (int)(grid.y * grid.z) : pt.nbtot;
   switch ((g.n2 + 31) / 32) {
 #define PO_H4(JJ)                                                                          \
   case JJ: {                                                                               \
     auto k = hamiltonian4_kernel<JJ, EXT, TYR>;                                             \
     set_smem(reinterpret_cast<const void*>(k), (int)r.smem);                               \
-    launch_pdl(k, dim3(grid), dim3(block), r.smem, s, g, N, r.nst, zc, u, lo, hi, vloc, vext, out, partials);  \
+    launch_pdl(k, dim3(grid), dim3(block), r.smem, s, g, N, r.nst, zc, u, lo, hi, vloc, vext, out, partials, \
+               lo_ld, hi_ld, nbtot, pt.boff);                                               \
     break;                                                                                 \
   }
     PO_H4(1) PO_H4(2) PO_H4(3) PO_H4(4) PO_H4(5) PO_H4(6) PO_H4(7) PO_H4(8)
@@ -584,6 +596,72 @@ void launch_hamiltonian2(const SlabGeom& g, int N, const double* u, const double
   else
     hamiltonian2_kernel<false, 4, 3><<<grid, block, 0, s>>>(g, N, h.ntx, u, halo_lo, halo_hi,
                                                             v_local, nullptr, hu, partials);
+}
+
+// H u of a slab with the halo exchange overlapped (Engine::apply_h, size > 1):
+// `interior` launches planes 1 .. nz-2, whose z-neighbours are all local (the
+// "halos" of that view are planes 0 and nz-1 of u itself, orbital stride ld);
+// `boundary` (after the exchange) launches planes 0 and nz-1 with the received
+// planes. Both write one partials layout of hamiltonian_split_nblk columns.
+// Returns false where the split is unavailable (caller: launch_hamiltonian2).
+int hamiltonian_split_nblk(const SlabGeom& g) {
+  const H4Shape h = h4_shape(g);
+  const int ny = (int)((g.n1 + h.tyr - 1) / h.tyr);
+  return ny * (int)((g.nz - 2 + h.zc - 1) / h.zc) + 2 * ny;
+}
+
+bool hamiltonian_split_ok(const SlabGeom& g) { return h4_supported(g) && g.nz >= 3; }
+
+namespace {
+template <int TYR>
+void h4_any(bool ext, const SlabGeom& g, int N, const double* u, const double* lo, const double* hi,
+            const double* vloc, const double* vext, double* out, double* partials, cudaStream_t s,
+            int zc, size_t budget, H4Part pt) {
+  if (ext)
+    launch_h4<true, TYR>(g, N, u, lo, hi, vloc, vext, out, partials, s, zc, budget, pt);
+  else
+    launch_h4<false, TYR>(g, N, u, lo, hi, vloc, nullptr, out, partials, s, zc, budget, pt);
+}
+
+void h4_view(const SlabGeom& g, int64_t z0, int64_t nz, int N, const double* u, const double* lo,
+             int64_t lo_ld, const double* hi, int64_t hi_ld, const double* vloc, const double* vext,
+             double* out, double* partials, int boff, cudaStream_t s) {
+  SlabGeom v = g;
+  v.nz = nz;
+  const int64_t off = z0 * g.plane;
+  const H4Shape h = h4_shape(g);
+  H4Part pt;
+  pt.lo_ld = lo_ld;
+  pt.hi_ld = hi_ld;
+  pt.nbtot = hamiltonian_split_nblk(g);
+  pt.boff = boff;
+  ::po::count_launch();
+  if (h.tyr == 8)
+    h4_any<8>(vext != nullptr, v, N, u + off, lo, hi, vloc + off, vext ? vext + off : nullptr,
+              out ? out + off : nullptr, partials, s, h.zc, h.budget, pt);
+  else
+    h4_any<6>(vext != nullptr, v, N, u + off, lo, hi, vloc + off, vext ? vext + off : nullptr,
+              out ? out + off : nullptr, partials, s, h.zc, h.budget, pt);
+}
+}  // namespace
+
+void launch_hamiltonian_interior(const SlabGeom& g, int N, const double* u, const double* v_local,
+                                 const double* v_ext, double* hu, double* partials, cudaStream_t s) {
+  h4_view(g, 1, g.nz - 2, N, u, u, g.ld, u + (g.nz - 1) * g.plane, g.ld, v_local, v_ext, hu, partials, 0,
+          s);
+}
+
+void launch_hamiltonian_boundary(const SlabGeom& g, int N, const double* u, const double* halo_lo,
+                                 const double* halo_hi, const double* v_local, const double* v_ext,
+                                 double* hu, double* partials, cudaStream_t s) {
+  const H4Shape h = h4_shape(g);
+  const int ny = (int)((g.n1 + h.tyr - 1) / h.tyr);
+  const int nbi = ny * (int)((g.nz - 2 + h.zc - 1) / h.zc);
+  // plane 0: below it the received plane (or zero at the global boundary), above it plane 1
+  h4_view(g, 0, 1, N, u, halo_lo, g.plane, u + g.plane, g.ld, v_local, v_ext, hu, partials, nbi, s);
+  // plane nz-1: below it plane nz-2, above it the received plane
+  h4_view(g, g.nz - 1, 1, N, u, u + (g.nz - 2) * g.plane, g.ld, halo_hi, g.plane, v_local, v_ext, hu,
+          partials, nbi + ny, s);
 }
 
 #ifdef PO_MEASUREMENT_VARIANTS

@@ -111,6 +111,8 @@ _SIGS = {
     "po_last_error": ([C.c_void_p], C.c_char_p),
     "po_local_slab": ([C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
     "po_solver_bytes": ([C.POINTER(GridDesc), C.c_int, C.c_int], C.c_int64),
+    "po_slab_plan": ([C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                      C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
     "po_stream": ([C.c_void_p], C.c_void_p),
     "po_synchronize": ([C.c_void_p], C.c_int),
     "po_thread_group_create": ([C.c_int, C.POINTER(C.c_void_p)], C.c_int),
@@ -125,6 +127,7 @@ _SIGS = {
     "po_external_potential": ([C.c_void_p, C.c_void_p, C.c_int], C.c_int),
     "po_gaussian_potential": ([C.c_void_p, C.c_void_p, C.c_int], C.c_int),
     "po_random_block": ([C.c_void_p, C.c_int, C.c_uint64], C.c_int),
+    "po_fill_normal": ([C.c_void_p, C.c_int, C.c_uint64], C.c_int),
     "po_build_hamiltonian": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
                               C.POINTER(C.c_double), C.POINTER(C.c_int)], C.c_int),
     "po_apply_hamiltonian": ([C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
@@ -281,6 +284,10 @@ class Engine:
 
     def random_block(self, b: int, seed: int):
         self._chk(self._lib.po_random_block(self.h, b, C.c_uint64(seed)))
+
+    def fill_normal(self, b: int, seed: int):
+        """po_fill_normal: device counter-hash N(0,1) fill (measurement blocks)."""
+        self._chk(self._lib.po_fill_normal(self.h, b, C.c_uint64(seed)))
 
     # ---- fields
     def set_field(self, f: int, host: np.ndarray):
@@ -483,6 +490,15 @@ def nccl_unique_id() -> bytes:
     if rc != PO_OK:
         raise DeviceError("ncclGetUniqueId failed")
     return buf.raw
+
+
+def slab_plan(n0: int, size: int, rank: int):
+    """po_slab_plan: the engine's own axis-0 partition (host only) -> (z0, nz, lo_peer, hi_peer)."""
+    z0, nz, lo, hi = C.c_int64(), C.c_int64(), C.c_int(), C.c_int()
+    rc = lib().po_slab_plan(int(n0), int(size), int(rank), C.byref(z0), C.byref(nz), C.byref(lo), C.byref(hi))
+    if rc != PO_OK:
+        raise InvalidArgument("slab_plan: invalid partition")
+    return z0.value, nz.value, lo.value, hi.value
 
 
 def thread_group(size: int) -> int:

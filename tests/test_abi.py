@@ -71,3 +71,20 @@ def test_result_struct_layout_matches_header(native):
     names = [f[0] for f in R._fields_]
     assert names[-4:] == ["checkpoints", "n_checkpoints", "drift_iterations", "n_drift"]
     assert R.checkpoints.offset > R.message.offset
+
+
+@pytest.mark.parametrize("N,ng,off,cnt", [(3, 1001, 0, 1001), (3, 1001, 17, 300), (4, 999, 998, 1),
+                                          (5, 7, 0, 3), (2, 10, 3, 7)])
+def test_rank_slab_normals_are_the_reference_draw(port, native, N, ng, off, cnt):
+    """rng.cu rng_normals_slab (host, no GPU): a rank's slab of the reference's
+    Rng(seed) orbital-major draw (rng.hpp:13-41, tests/problems.hpp:59-68) is
+    bit-identical to the full draw sliced, for odd row lengths (the Box-Muller
+    spare crosses orbital rows) and slabs at either end."""
+    lib = C.CDLL(native.LIB_PATH)
+    f = getattr(lib, "_ZN2po16rng_normals_slabEmilllPd")
+    f.argtypes = [C.c_uint64, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]
+    import numpy as np
+    ref = port.random_normals(42, N * ng).reshape(N, ng)[:, off:off + cnt]
+    out = np.empty((N, cnt))
+    f(42, N, ng, off, cnt, out.ctypes.data)
+    assert np.array_equal(out, ref)

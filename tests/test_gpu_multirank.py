@@ -38,8 +38,11 @@ def run_ranks(native, spec, size, body):
     return out
 
 
-@pytest.mark.parametrize("size", [2, 3])
+@pytest.mark.parametrize("size", [2, 3, 7])
 def test_sharded_operators(port, native, size):
+    """size 2 / 3: slabs of >= 3 planes take the overlapped H u (interior planes
+    while the halo planes travel, then the two boundary planes); size 7 leaves
+    2 planes per rank: the exchange-then-stencil path."""
     spec = configs.small_molecule(14, 4, L=8.0)
     u0 = port.random_orthonormal(spec)
     plane = spec.n[1] * spec.n[2]
@@ -94,3 +97,48 @@ def test_sharded_solver(port, native, size):
         for a, b in zip(x["got"].records, ref["records"]):
             assert abs(a["energy"] - b["energy"]) < 1e-6 and a["backtracks"] == b["backtracks"]
     assert projector_distance(ref["w"], w, np.prod(spec.spacing)) < 1e-6
+
+
+def test_c4_slab_geometry(native):
+    """The C4 grid (192^3, L = 60, the C4 nuclei) cut into 3 slabs of 64 planes
+    (the 8-GPU C4 run has 24) with N = 8 orbitals: sharded operators and two
+    solver iterations vs the single-domain engine on the same start (itself
+    pinned to the reference at this grid by test_gpu_parity_big)."""
+    spec = configs.config4()
+    spec.n_orbitals = 8
+    spec.max_inner = 2
+    e1 = native.engine_for(spec)
+    w1 = native.random_orthonormal(e1, spec.start_seed)
+    u0 = e1.download(w1)
+    e1.build_hamiltonian(w1)
+    h1 = e1.alloc()
+    sig1, kin1, ext1 = e1.apply_hamiltonian(w1, h1)
+    hu1 = e1.download(h1)
+    g1 = e1.gram(w1, w1)
+    vh1 = e1.get_field(native.PO_VH)
+    en1 = e1.total_energy(w1)
+    r1 = e1.solve(w1, algorithm="opt_par_mod", **spec.optimizer_params())
+    e1.close()
+    plane = spec.n[1] * spec.n[2]
+
+    def body(e, r):
+        sl = slice(e.z0 * plane, (e.z0 + e.nz) * plane)
+        u = e.block_from(np.ascontiguousarray(u0[:, sl]))
+        e.build_hamiltonian(u)
+        hu = e.alloc()
+        sig, kin, ext = e.apply_hamiltonian(u, hu)
+        out = dict(sl=sl, nz=e.nz, hu=e.download(hu), sig=sig, kin=kin, gram=e.gram(u, u),
+                   vh=e.get_field(native.PO_VH), tot=e.total_energy(u))
+        out["solve"] = e.solve(u, algorithm="opt_par_mod", **spec.optimizer_params())
+        return out
+
+    res = run_ranks(native, spec, 3, body)
+    for x in res:
+        assert x["nz"] == 64
+        assert np.max(np.abs(x["hu"] - hu1[:, x["sl"]])) < 1e-10 * np.abs(hu1).max()
+        assert np.max(np.abs(x["vh"] - vh1[x["sl"]])) < 1e-9 * np.abs(vh1).max()
+        assert np.allclose(x["sig"], sig1, rtol=1e-11) and np.allclose(x["kin"], kin1, rtol=1e-11)
+        assert np.max(np.abs(x["gram"] - g1)) < 1e-13
+        assert abs(x["tot"]["total"] - en1["total"]) < 1e-8
+        for a, b in zip(x["solve"].records, r1.records):
+            assert a["backtracks"] == b["backtracks"] and abs(a["energy"] - b["energy"]) < 1e-8

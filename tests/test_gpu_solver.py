@@ -179,7 +179,8 @@ def test_launch_and_path_switches_agree(tmp_path):
     bitwise the same, the directions pass then runs 6 instead of 8 warps, so its
     per-orbital sums are reduced in another order) agree to round-off, as do
     the split trial rotation (PO_ROT_SPLIT=1: two-source mix + Gram/density
-    pass), the 8-warp directions pass (PO_DIR_CW=8), the Poisson check by the CG
+    pass), the 6-warp implicit-z directions pass (PO_DIR_CW=6; 8 is the default),
+    the Poisson check by the CG
     kernel (PO_POISSON_DEFER=0) and a forced CG repair of every line-search
     trial's Poisson solve (PO_FORCE_POISSON_REPAIR=1) agree to round-off."""
     import json
@@ -197,7 +198,7 @@ print(json.dumps([x["energy"] for x in r.records] + [r.energy["total"]]))
 ''' % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),)
     runs = {}
     for name, env_over in [("base", {}), ("nopdl", {"PO_PDL": "0"}), ("split", {"PO_ROT_SPLIT": "1"}),
-                           ("dir8", {"PO_DIR_CW": "8"}), ("nodefer", {"PO_POISSON_DEFER": "0"}),
+                           ("dir6", {"PO_DIR_CW": "6"}), ("nodefer", {"PO_POISSON_DEFER": "0"}),
                            ("repair", {"PO_FORCE_POISSON_REPAIR": "1"}), ("zstored", {"PO_ZFREE": "0"})]:
         env = {k: v for k, v in os.environ.items() if not k.startswith("PO_")}
         env.update(env_over)
@@ -207,7 +208,7 @@ print(json.dumps([x["energy"] for x in r.records] + [r.energy["total"]]))
     assert runs["nopdl"] == runs["base"]
     # the Poisson check in the v_local pass (default) vs the CG verification kernel,
     # and the forced CG repair of every trial's solve (Solver: DST -> CG warm start)
-    for name in ("split", "dir8", "nodefer", "repair", "zstored"):
+    for name in ("split", "dir6", "nodefer", "repair", "zstored"):
         assert len(runs[name]) == len(runs["base"])
         assert max(abs(x - y) for x, y in zip(runs[name], runs["base"])) < 1e-9, name
 

@@ -1,17 +1,19 @@
 """BASELINE configs[4] (C5) kernel microbenchmark sweep on one B200.
 
-Grids 64^3/128^3/192^3/256^3 x N in {64, 256, 1024, 2048}, i.i.d. N(0,1)
-orbital block (device-generated bits of parorb::Rng are not needed for
-timing: the block is filled from a host RNG slice only for small sizes; large
-blocks are orthonormalised once on the device), smooth seeded potential of 32
+Grids 64^3/128^3/192^3/256^3 x N in {64, 256, 1024, 2048}; every block is
+FILLED on the device with i.i.d. N(0,1) values (po_fill_normal: a counter hash,
+not the reference's Rng bits — the C5 spec allows a device generator) and each
+row records filled: true. Local potential: a smooth seeded field of 32
 Gaussians (width 2 bohr, A ~ U(-5, 0)). Timed separately with CUDA events on
 the engine stream (median of reps): batched H.u, density (+ LDA xc fused),
-Gram U^T U (symmetric), and the U L^-T rotation. Points that do not fit one
-GPU are reported as such (never skipped silently). Writes profiles/r1_c5_sweep.json.
+Gram U^T U (symmetric), and the U L^-T rotation with L from the Cholesky of
+that block's Gram. Points that do not fit one GPU are reported as such (never
+skipped silently). Writes gpurun_out/c5_sweep.json.
 
 Rooflines: H.u / density against the measured HBM peak (MEASURED_PEAKS.json);
 Gram (N(N+1) N_g flops) and rotation (N(N+1) N_g flops, triangular) against the
-measured FP64 DGEMM peak (profiles/fp64_peak.json) and against HBM.
+measured FP64 DMMA issue rate (profiles/fp64_peak.json; cuBLAS DGEMM reaches
+~95% of it) and against HBM.
 """
 import json
 import os
@@ -26,7 +28,8 @@ from paper_1510_07230_b200 import configs, native  # noqa: E402
 
 HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
-FP64 = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["fp64_tflops"]
+_fp = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+FP64 = _fp.get("dmma_issue_tflops") or _fp["fp64_tflops"]
 free = torch.cuda.mem_get_info()[0]
 
 
@@ -61,7 +64,7 @@ for n in sizes:
             continue
         e = native.engine_for(spec)
         u = e.alloc()
-        e.random_block(u, 42) if N * ng <= 2e8 else None
+        e.fill_normal(u, 42)  # every point, every row (filled: true)
         out = e.alloc()
         e.build_hamiltonian(u, hartree=False, xc=True)  # v_local = V(r) + v_xc
         bytes_h = 16.0 * N * e.ngl + 8.0 * e.ngl
@@ -71,10 +74,12 @@ for n in sizes:
         t_g = timeit(e, lambda: e.enqueue("gram_sym", a=u))
         fl_g = float(N) * (N + 1) * ng
         # L^{-T} from the Cholesky of this block's Gram (the rotation of manifold.cpp:97-114)
+        e.enqueue("gram_sym", a=u)
         e.enqueue("cholesky", a=u)
         t_r = timeit(e, lambda: e.enqueue("mix_upper", a=u, out=out))
         fl_r = float(N) * (N + 1) * ng
         row.update({
+            "filled": True,
             "hamiltonian_us": 1e3 * t_h, "hamiltonian_GBs": bytes_h / t_h / 1e6,
             "hamiltonian_frac_hbm": bytes_h / t_h / 1e6 / HBM,
             "density_xc_us": 1e3 * t_d, "density_frac_hbm": bytes_d / t_d / 1e6 / HBM,
