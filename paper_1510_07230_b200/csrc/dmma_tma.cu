@@ -2216,8 +2216,12 @@ __global__ void __launch_bounds__(XTH, 1) mix_big_kernel(
 struct Maps5 {
   CUtensorMap m[5];
 };
-constexpr int DNA = 3;  // ring A stages (W + Sigma^T: 32 KB each)
-constexpr int DNE = 2;  // ring E stages (HW, W_prev, HW_prev: 3 x 16.25 KB each)
+constexpr int DNA = 4;  // ring A stages (16 input orbitals of W: 16 KB each)
+constexpr int DNE = 3;  // ring E stages (HW, W_prev, HW_prev: 3 x 16.25 KB each)
+// Sigma^T is not staged: its B fragments come from the padded transpose in
+// global memory (128 KB at N = 128, L2-resident), one stage ahead in
+// registers, so the shared memory goes to ring depth (ncu: the consumers'
+// dominant stall was the wait for ring E with 3 A + 2 E stages of 32 / 48 KB)
 // Ring E boxes are unswizzled rows of EW = 130 points (one box per block per
 // stage): 1-KB+ TMA rows stream at full rate where the 128-B rows of the
 // swizzled DMMA boxes cap near 4.2 TB/s (profiles/r1_tma2d_probe.txt), and the
@@ -2290,7 +2294,7 @@ __device__ __forceinline__ void dir_big_elementwise(
 __global__ void __launch_bounds__(XTH, 1) dir_big_kernel(
     const __grid_constant__ Maps5 maps, int N, int64_t ld, int64_t ngl, int n_pt, int n_it, int hist,
     const double* __restrict__ sig, const double* __restrict__ sigp, double* __restrict__ zout,
-    double* __restrict__ sig_save, double* __restrict__ dpart) {
+    double* __restrict__ sig_save, double* __restrict__ dpart, const double* __restrict__ mtg, int np) {
   PO_PDL_ENTRY();
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   unsigned char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);
@@ -2299,7 +2303,7 @@ __global__ void __launch_bounds__(XTH, 1) dir_big_kernel(
   uint64_t* fullE = fullA + 16;
   uint64_t* emptyE = fullA + 24;
   constexpr size_t QA = (size_t)XP * XK;  // doubles per block per stage
-  constexpr size_t SA = 2 * QA;           // ring A stage: W + Sigma^T box
+  constexpr size_t SA = QA;               // ring A stage: W
   constexpr size_t SE = 3 * QE;           // ring E stage: HW, W_prev, HW_prev / Z_prev
   double* ringA = reinterpret_cast<double*>(tsm + 1024);
   double* ringE = ringA + DNA * SA;
@@ -2330,9 +2334,8 @@ __global__ void __launch_bounds__(XTH, 1) dir_big_kernel(
   int warp = threadIdx.x >> 5;
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-    if (warp == 0 && lane == 0) {  // ring A: W + Sigma^T for every stage
+    if (warp == 0 && lane == 0) {  // ring A: W for every stage
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[0])));
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[1])));
       int g = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         int pt, it;
@@ -2344,7 +2347,6 @@ __global__ void __launch_bounds__(XTH, 1) dir_big_kernel(
           double* sb = ringA + (size_t)s * SA;
           for (int b = 0; b < XP / BOX; ++b)
             tma_load_2d(sb + b * BOX * XK, &maps.m[0], pt * XP + b * BOX, c * XK, &fullA[s]);
-          tma_load_2d(sb + QA, &maps.m[1], c * XK, it * XI, &fullA[s]);
         }
       }
     } else if (warp == 1 && lane == 0) {  // ring E: the tile's own orbitals only
@@ -2371,6 +2373,24 @@ __global__ void __launch_bounds__(XTH, 1) dir_big_kernel(
     warp -= 4;
     const int gq = lane >> 2, t4 = lane & 3;
     const int F0 = warp, F1 = 15 - warp;  // this warp's output fragments
+    // B fragments (Sigma^T rows i, the stage's k pairs) of stage (c, it), from global
+    auto load_b = [&](int c, int it, double2 (&b)[2][2]) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int i = it * XI + 8 * (q ? F1 : F0) + gq;
+          const int k = c * XK + 8 * h + 2 * t4;
+          b[h][q] = i < np ? __ldg(reinterpret_cast<const double2*>(mtg + (int64_t)i * np + k))
+                           : make_double2(0.0, 0.0);
+        }
+    };
+    double2 bnext[2][2];
+    if (blockIdx.x < ntiles) {
+      int pt, it;
+      tile_of(blockIdx.x, pt, it);
+      load_b(0, it, bnext);
+    }
     int g = 0, ge = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int pt, it;
@@ -2378,26 +2398,35 @@ __global__ void __launch_bounds__(XTH, 1) dir_big_kernel(
       const int i0 = it * XI;
       const bool real0 = i0 + 8 * F0 < N, real1 = i0 + 8 * F1 < N;  // padding fragments
       const int64_t p0 = (int64_t)pt * XP;
+      int ptn = 0, itn = 0;  // the next tile (B prefetch across the tile boundary)
+      if (t + (int)gridDim.x < ntiles) tile_of(t + gridDim.x, ptn, itn);
       double acc[2][16][2];
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int b = 0; b < 16; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
       for (int c = 0; c < nk; ++c, ++g) {
+        double2 bcur[2][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          bcur[h][0] = bnext[h][0];
+          bcur[h][1] = bnext[h][1];
+        }
+        if (c + 1 < nk)
+          load_b(c + 1, it, bnext);
+        else if (t + (int)gridDim.x < ntiles)
+          load_b(0, itn, bnext);
         const int s = g % DNA;
         mbar_wait(&fullA[s], (uint32_t)(g / DNA) & 1u);
         const double* sb = ringA + (size_t)s * SA;
-        const double* mt = sb + QA;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int k8 = c * XK + 8 * h;
           if (k8 >= N) break;
-          const double2 b0 = *reinterpret_cast<const double2*>(mt + swz(8 * F0 + gq, 8 * h + 2 * t4, XI));
-          const double2 b1 = *reinterpret_cast<const double2*>(mt + swz(8 * F1 + gq, 8 * h + 2 * t4, XI));
           if (real0 && real1)
-            mix_big_slice<true, true>(acc, sb, nullptr, 0.0, b0, b1, h, gq, t4);
+            mix_big_slice<true, true>(acc, sb, nullptr, 0.0, bcur[h][0], bcur[h][1], h, gq, t4);
           else if (real0)
-            mix_big_slice<true, false>(acc, sb, nullptr, 0.0, b0, b1, h, gq, t4);
+            mix_big_slice<true, false>(acc, sb, nullptr, 0.0, bcur[h][0], bcur[h][1], h, gq, t4);
         }
         const int crel = c - it * (XI / XK);  // diagonal stage index within the tile
         if (crel >= 0 && crel < XI / XK) {
@@ -2740,11 +2769,10 @@ int launch_directions_big(int N, int64_t ld, int64_t ngl, const double* W, const
   Maps5 maps;
   std::memset(&maps, 0, sizeof maps);
   if (!make_map(&maps.m[0], W, ld, N, XK)) return -1;
-  if (!make_map(&maps.m[1], mt, np, np, XI)) return -1;
-  if (!make_map(&maps.m[2], HW, ld, N, XK, EW)) return -1;
+  if (!make_map(&maps.m[2], HW, ld, N, XK, EW)) return -1;  // m[1] unused (Sigma^T from global)
   if (hist && (!make_map(&maps.m[3], WP, ld, N, XK, EW) || !make_map(&maps.m[4], XP_, ld, N, XK, EW)))
     return -1;
-  const size_t smem = 2048 + ((size_t)DNA * 2 * XP * XK + (size_t)DNE * 3 * QE) * 8;
+  const size_t smem = 2048 + ((size_t)DNA * XP * XK + (size_t)DNE * 3 * QE) * 8;
   ::po::count_launch();
   launch_pdl(transpose_pad_kernel, dim3((unsigned)(((int64_t)np * np + 255) / 256)), dim3(256), 0, s, N,
              np, Sigma, mt);
@@ -2755,7 +2783,7 @@ int launch_directions_big(int N, int64_t ld, int64_t ngl, const double* W, const
   set_smem(reinterpret_cast<const void*>(dir_big_kernel), (int)smem);
   ::po::count_launch();
   launch_pdl(dir_big_kernel, dim3(grid), dim3(XTH), smem, s, maps, N, ld, ngl, n_pt, n_it, hist, sig,
-             hist ? sig_prev : (const double*)nullptr, Z, sig_save, partials);
+             hist ? sig_prev : (const double*)nullptr, Z, sig_save, partials, (const double*)mt, np);
   return n_pt;
 }
 
