@@ -2547,7 +2547,13 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
   const int lane = threadIdx.x & 31;
   int warp = threadIdx.x >> 5;
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    // 88 registers (not 40): the three combining warps form W - tau z for every
+    // stage and were the consumers' dominant wait (ncu: `ready` barrier); the
+    // headroom keeps four independent element chains in flight (C3 implicit
+    // rotation 1.81 -> 1.75 ms; forming the trial values in the consumers
+    // instead, at their fragment loads, measured 2.5 ms: the per-load branch and
+    // the 4x redundant forms broke the DMMA schedule even on one source)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
     if (warp == 0 && lane == 0) {
       for (int q = 0; q <= nsrc; ++q)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[q])));
@@ -2591,6 +2597,7 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
             }
             asm volatile("bar.sync 2, 96;\n" ::: "memory");
           }
+#pragma unroll 4
           for (int e = ct; e < (int)QH; e += 96) {  // 2 * QH doubles = QH double2
             double2 v = a2[e];
             double2 z = b2[e];
@@ -2610,7 +2617,7 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
     warp -= 4;
     const int gq = lane >> 2, t4 = lane & 3;
     const int hf = warp >> 2, a = warp & 3;  // half (0 forwards, 1 backwards), fragment set
