@@ -1542,7 +1542,14 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
                                                           int mt, int sym, int64_t ld,
                                                           int64_t kchunk, int nst, double sa,
                                                           double sb, double* __restrict__ ws,
-                                                          const double* __restrict__ guard) {
+                                                          const double* __restrict__ guard,
+                                                          double* __restrict__ rho,
+                                                          double* __restrict__ bvec, double occ,
+                                                          int64_t ngl) {
+  // rho (T = 128, one symmetric diagonal tile, one source): the verification
+  // Gram of a rotated trial also yields its density (energy.cpp:67-76) and
+  // 4 pi rho — producer warp 1 sums the squares of all N orbitals per point
+  // straight from each stage, so the trial needs no separate density pass
   PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
@@ -1558,10 +1565,11 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
   // sources fetched per 16-point half: A (+Ab); B (+Bb) unless this is a symmetric diagonal tile
   const int nload = diag ? (qa_b >= 0 ? 2 : 1) : nsrc;
   using Cfg = BigCfg<GT_T>;
+  const bool dens = GT_T == 128 && rho && diag && nload == 1;
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], Cfg::NW);
+      mbar_init(&empty[s], Cfg::NW + (dens ? 1 : 0));
     }
     fence_mbar_init();
   }
@@ -1596,6 +1604,30 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
             tma_load_2d(sbuf + q * QS, &maps.m[q], x, row0, &full[s]);
           }
         }
+      }
+    } else if (dens && warp == 1) {
+      // lane l: point 16 (l >> 4) + (l & 15) of the stage's two halves; orbitals
+      // in ascending order (energy.cpp:67-76); a half-warp reads one 128-B row
+      // per orbital (conflict-free under the swizzle)
+      const int h = lane >> 4, o = lane & 15;
+      const double four_pi = 4.0 * 3.141592653589793238462643383279502884;
+      for (int st = 0; st < nstage; ++st) {
+        const int s = st % nst;
+        mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+        const double* area = stage0 + (size_t)s * sdoubles + (size_t)h * QS;
+        double acc = 0.0;
+        for (int i = 0; i < GT_T; ++i) {
+          const double v = area[swz(i, o, GT_T)];
+          acc += v * v;
+        }
+        const int64_t p = kbeg + (int64_t)st * pps + 16 * h + o;
+        if (p < ngl) {
+          const double r = occ == 1.0 ? acc : acc * occ;
+          rho[p] = r;
+          if (bvec) bvec[p] = r * four_pi;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
       }
     }
   } else {
@@ -2808,8 +2840,11 @@ size_t gram_big_workspace_doubles(int64_t ld, int N) {
 
 bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                      const double* B, const double* Bb, double sb, double* ws, size_t ws_doubles,
-                     double* G, double w, cudaStream_t s, const double* guard) {
+                     double* G, double w, cudaStream_t s, const double* guard, double* rho,
+                     double* bvec, double occ, int64_t ngl) {
   const int GT_T = big_tile(N, sym, Ab != nullptr || !sym);
+  // the fused density needs the whole orbital set in one diagonal tile
+  if (rho && !(sym && !Ab && GT_T == 128 && N <= 128 && N > 64)) return false;
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   int nsrc = 0, qa_b = -1, qb = 0, qb_b = -1;
@@ -2849,7 +2884,7 @@ bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* 
   const int threads = GT_T == 64 ? BigCfg<64>::THREADS : BigCfg<128>::THREADS;
   set_smem(reinterpret_cast<const void*>(k), (int)smem);
   launch_pdl(k, dim3(dim3(p.ntiles, p.nsplit)), dim3(threads), smem, s, maps, nsrc, qa_b, qb, qb_b, p.mt, sym, ld, p.kchunk,
-                                                 nst, sa, sb, ws, guard);
+                                                 nst, sa, sb, ws, guard, rho, bvec, occ, ngl);
   const int64_t total = (int64_t)N * N;
   ::po::count_launch();
   launch_pdl(gram_big_reduce_kernel, dim3((unsigned)((total + 31) / 32)), dim3(dim3(32, 8)), 0, s, GT_T, N, p.mt, sym, p.ntiles,

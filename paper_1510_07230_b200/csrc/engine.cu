@@ -431,6 +431,16 @@ void Engine::gram(const double* A, const double* Ab, double sa, const double* B,
   if (size > 1) comm->allreduce_sum(Gdev, (size_t)N * N, s);
 }
 
+bool Engine::gram_density(const double* A, double* Gdev, double* rho, double* bvec) {
+  static const bool off = std::getenv("PO_NO_GRAM_DENSITY") != nullptr;  // measurement switch
+  if (off || N <= 64 || N > 128 || !tma2d_available()) return false;
+  if (!launch_gram_big(N, g.ld, 1, A, nullptr, 0.0, A, nullptr, 0.0, gram_ws,
+                       gram_workspace_doubles(g, N), Gdev, g.w, s, nullptr, rho, bvec, occ, g.ngl))
+    return false;
+  if (size > 1) comm->allreduce_sum(Gdev, (size_t)N * N, s);
+  return true;
+}
+
 void Engine::mix(const double* A, const double* Ab, double sa, const double* M, double alpha,
                  const double* C, double beta, int upper, double* out, double* norm_rows,
                  const double* guard, const double* zsig) {

@@ -123,6 +123,9 @@ class Engine {
   void halo_exchange(const double* u);
   void gram(const double* A, const double* Ab, double sa, const double* B, const double* Bb,
             double sb, int sym, double* Gdev, const double* guard = nullptr);
+  // symmetric Gram of A that also writes A's density rho (+ 4 pi rho into bvec);
+  // false (nothing enqueued) where the fused form is unavailable
+  bool gram_density(const double* A, double* Gdev, double* rho, double* bvec);
   void mix(const double* A, const double* Ab, double sa, const double* M, double alpha,
            const double* C, double beta, int upper, double* out, double* norm_rows,
            const double* guard = nullptr, const double* zsig = nullptr);

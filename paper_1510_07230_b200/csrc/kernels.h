@@ -143,9 +143,13 @@ void launch_bb_tau(int N, const double* zz, const double* ss, const double* sy, 
 // Large-N (N > 48) Gram: 128x128 (or 64x64) orbital tiles x point splits,
 // one 16-point 2D box per source per stage; returns false when unavailable.
 size_t gram_big_workspace_doubles(int64_t ld, int N);
+// rho (nullable): with one source, sym and 64 < N <= 128 (one diagonal tile) the
+// Gram also writes the density occ sum_i A_i^2 (+ 4 pi rho into bvec) of the
+// ngl points; false (nothing launched) where that is unavailable
 bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                      const double* B, const double* Bb, double sb, double* ws, size_t ws_doubles,
-                     double* G, double w, cudaStream_t s, const double* guard);
+                     double* G, double w, cudaStream_t s, const double* guard, double* rho = nullptr,
+                     double* bvec = nullptr, double occ = 1.0, int64_t ngl = 0);
 // Fused compute_directions + BB products for N <= 48 (one pass over W, HW
 // [, WP, ZP]): writes Z = HW - diag(sig) W and per-orbital partial rows
 // [zz | dd | ss | sy | yy] (dd = ||HW - W Sigma||^2 when Sigma != null; the

@@ -210,7 +210,12 @@ bool orth_enqueue(Engine& E, const double* A, const double* Ab, double sa, doubl
   if (!fused) {
     if (tau_dev) throw Error(PO_EINVAL, "device-side trial scale needs the fused rotation");
     E.mix(A, Ab, sa, E.dmat[1], 1.0, nullptr, 0.0, 1, out, nullptr, nullptr, zsig);
-    E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2]);
+    // 64 < N <= 128: the verification Gram of the rotated block also writes its
+    // density and 4 pi rho (xc and the energies come from the v_local pass)
+    if (st && E.gram_density(out, E.dmat[2], st->rho, E.density_b_target(hartree)))
+      fused = true;
+    else
+      E.gram(out, nullptr, 0.0, out, nullptr, 0.0, 1, E.dmat[2]);
   }
   launch_matrix_stats(E.N, E.dmat[2], sc + Engine::S_MSTAT2, E.s);
   return fused;
