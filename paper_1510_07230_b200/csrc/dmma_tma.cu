@@ -1629,6 +1629,8 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
+      // the consumers reuse the ring for the tile epilogue after this barrier
+      asm volatile("bar.sync 3, %0;\n" ::"n"((Cfg::NW + 1) * 32) : "memory");
     }
   } else {
     if constexpr (Cfg::PW == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
@@ -1744,7 +1746,11 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
       }
       constexpr int SP = GT_T + 8;
       double* S = stage0;
-      asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NW * 32) : "memory");  // ring fully consumed
+      // ring fully consumed — by the density warp too, before the ring becomes S
+      if (dens)
+        asm volatile("bar.sync 3, %0;\n" ::"n"((Cfg::NW + 1) * 32) : "memory");
+      else
+        asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NW * 32) : "memory");
       // pass 0: half 0 stores its blocks; pass 1: half 1 adds (same block set)
 #pragma unroll
       for (int pass = 0; pass < 2; ++pass) {
