@@ -451,7 +451,7 @@ def ours(args, spec):
         dom_bound = "hbm"
     else:  # the large-N tiles of the C3 step
         sig = add_kernel("gram_big_kernel<128> Sigma = w (HW)^T W", sg_ms, 2 * blk, 2.0 * N * N * ng)
-        add_kernel("gram_big_kernel<128> symmetric (G_HH, verification G2)", g_ms, blk,
+        add_kernel("gram_big_kernel<128> symmetric (G_HH; verification G2 + the trial's density)", g_ms, blk,
                    float(N) * (N + 1) * ng, per_iter=2)
         e.enqueue("gram", a=hw_b, b=cur)
         d_ms = time_kernel(torch, native, e, "directions", 10, a=cur, b=hw_b, out=z_b)
@@ -460,9 +460,7 @@ def ours(args, spec):
         e.enqueue("cholesky")
         r_ms = time_kernel(torch, native, e, "rotation_implicit", 10, a=cur, b=hw_b, out=scratch)
         add_kernel("mix_tri_kernel (W - tau z) L^-T, implicit z", r_ms, 3 * blk, float(N) * (N + 1) * ng)
-        e.enqueue("density_xc", a=cur)
-        dx_ms = time_kernel(torch, native, e, "density_xc", 10, a=cur)
-        add_kernel("density_xc_kernel", dx_ms, blk + 16.0 * e.ngl)
+        # (no density pass: 64 < N <= 128 trials get rho from the verification Gram)
         # gram_big_kernel over its three launches of the iteration (Sigma, G_HH, the
         # verification G2): the kernel with the largest share of the step
         tot_ms = sg_ms + 2 * g_ms
