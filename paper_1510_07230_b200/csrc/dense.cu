@@ -927,6 +927,65 @@ void launch_inv_sqrt_from_eig(int N, const double* evals, const double* evecs, d
   inv_sqrt_kernel<<<blocks, 256, 0, s>>>(N, evals, evecs, M, stats);
 }
 
+// ||D_i||^2 of the Stiefel gradient D = HW - W Sigma (manifold.cpp:181-202)
+// from the iteration's Grams instead of a pass over the blocks:
+//   ||D_i||^2 = G_HH(i,i) - 2 sum_k Sigma(k,i) Sigma(i,k) + sum_kl Sigma(k,i) G_WW(k,l) Sigma(l,i)
+// (Sigma(a,b) = <HW_a, W_b>, every term weighted like the Grams). It cancels as
+// D -> 0, so err[i] bounds its rounding: 1e-13 x the sum of the magnitudes of the
+// three terms (the Grams are fp64 sums accurate to ~1e-15 relative; a 100x
+// margin). The solver takes these values only when sum dd >= 1e8 sum err
+// (relative error <= 1e-8) and the gradient is far from grad_tol; otherwise
+// it runs the direct pass. One CTA per column i, fixed-order reductions.
+// Block i also copies sigma_i into sig_save (the next iteration's z_prev).
+__global__ void __launch_bounds__(128) dnorm_grams_kernel(int N, const double* __restrict__ S,
+                                                           const double* __restrict__ Gww,
+                                                           const double* __restrict__ Ghh,
+                                                           double* __restrict__ dd,
+                                                           double* __restrict__ err,
+                                                           const double* __restrict__ sig,
+                                                           double* __restrict__ sig_save) {
+  PO_PDL_ENTRY();
+  __shared__ double red[4][4];
+  const int i = blockIdx.x;
+  double t2 = 0.0, t3 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const double ski = S[(int64_t)k * N + i];
+    double u = 0.0, ua = 0.0;  // (G_WW Sigma)(k, i) and its magnitude bound
+    for (int l = 0; l < N; ++l) {
+      const double gs = Gww[(int64_t)k * N + l] * S[(int64_t)l * N + i];
+      u += gs;
+      ua += fabs(gs);
+    }
+    t2 += ski * S[(int64_t)i * N + k];
+    a2 += fabs(ski * S[(int64_t)i * N + k]);
+    t3 += ski * u;
+    a3 += fabs(ski) * ua;
+  }
+  double v[4] = {t2, t3, a2, a3};
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+    if (lane == 0) red[q][wid] = v[q];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) r[q] = (red[q][0] + red[q][1]) + (red[q][2] + red[q][3]);
+    const double t1 = Ghh[(int64_t)i * N + i];
+    dd[i] = (t1 - 2.0 * r[0]) + r[1];
+    err[i] = 1e-13 * (fabs(t1) + 2.0 * r[2] + r[3]);
+    if (sig_save) sig_save[i] = sig[i];
+  }
+}
+
+void launch_dnorm_grams(int N, const double* S, const double* Gww, const double* Ghh, double* dd,
+                        double* err, const double* sig, double* sig_save, cudaStream_t s) {
+  ::po::count_launch();
+  launch_pdl(dnorm_grams_kernel, dim3(N), dim3(128), 0, s, N, S, Gww, Ghh, dd, err, sig, sig_save);
+}
+
 void launch_matrix_stats(int N, const double* G, double* out, cudaStream_t s,
                          const double* guard) {
   ::po::count_launch();

@@ -234,6 +234,65 @@ __global__ void __launch_bounds__(PT) residual_bb_kernel(SlabGeom g, int N,
   }
 }
 
+// The elementwise half of compute_directions for N > 64 when ||D_i||^2 comes
+// from the Grams (launch_dnorm_grams): z_i = fma(-sigma_ii, u_i, hu_i) (the
+// FMA every z path uses; written only when z is stored), ||z_i||^2 and the BB
+// products against (u_prev, z_prev), z_prev = fma(-sigma_prev, u_prev, hu_prev)
+// rebuilt (sigp) or read (xp is a stored z_prev). Four streams, 16-byte loads.
+// partials [4][N][nblk]: zz, ss, sy, yy (rows 1..3 only with a history).
+template <bool HIST, bool ZPI>
+__global__ void __launch_bounds__(PT) residual_bb_stream_kernel(
+    SlabGeom g, int N, const double* __restrict__ u, const double* __restrict__ hu,
+    const double* __restrict__ sig, const double* __restrict__ up, const double* __restrict__ xp,
+    const double* __restrict__ sigp, double* __restrict__ z, double* __restrict__ partials) {
+  PO_PDL_ENTRY();
+  __shared__ double red[4 * 32];
+  const int i = blockIdx.y;
+  const double ms = -sig[i];
+  const double msp = ZPI ? -sigp[i] : 0.0;
+  const int64_t o = (int64_t)i * g.ld;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int64_t npair = g.ngl >> 1;
+  auto point = [&](double w, double h, double wq, double xq, double& zv) {
+    zv = fma(ms, w, h);
+    acc[0] += zv * zv;
+    if (HIST) {
+      const double zq = ZPI ? fma(msp, wq, xq) : xq;
+      const double sv = w - wq, yv = zv - zq;
+      acc[1] += sv * sv;
+      acc[2] += sv * yv;
+      acc[3] += yv * yv;
+    }
+  };
+  for (int64_t q = (int64_t)blockIdx.x * PT + threadIdx.x; q < npair; q += (int64_t)gridDim.x * PT) {
+    const int64_t p = o + 2 * q;
+    const double2 w = __ldg(reinterpret_cast<const double2*>(u + p));
+    const double2 h = __ldg(reinterpret_cast<const double2*>(hu + p));
+    double2 wq = make_double2(0.0, 0.0), xq = make_double2(0.0, 0.0);
+    if (HIST) {
+      wq = __ldg(reinterpret_cast<const double2*>(up + p));
+      xq = __ldg(reinterpret_cast<const double2*>(xp + p));
+    }
+    double2 zz;
+    point(w.x, h.x, wq.x, xq.x, zz.x);
+    point(w.y, h.y, wq.y, xq.y, zz.y);
+    if (z) *reinterpret_cast<double2*>(z + p) = zz;
+  }
+  if ((g.ngl & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd point count: the last point
+    const int64_t p = o + g.ngl - 1;
+    double zv;
+    point(u[p], hu[p], HIST ? up[p] : 0.0, HIST ? xp[p] : 0.0, zv);
+    if (z) z[p] = zv;
+  }
+  block_sum<4>(acc, red);
+  if (threadIdx.x == 0) {
+    const int nb = gridDim.x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q == 0 || HIST) partials[((int64_t)q * N + i) * nb + blockIdx.x] = acc[q];
+  }
+}
+
 __global__ void __launch_bounds__(PT) abs_sum_kernel(SlabGeom g, int N,
                                                      const double* __restrict__ x,
                                                      double* __restrict__ partials) {
@@ -461,6 +520,24 @@ void launch_residual_bb(const SlabGeom& g, int N, const double* u, const double*
   dim3 grid(per_orbital_nblk(g, N), N);
   ::po::count_launch();
   residual_bb_kernel<<<grid, PT, 0, s>>>(g, N, u, hu, sigma_diag, up, zp, z, partials);
+}
+
+int launch_residual_bb_stream(const SlabGeom& g, int N, const double* u, const double* hu,
+                              const double* sigma_diag, const double* up, const double* xp,
+                              const double* sig_prev, double* z, double* partials, cudaStream_t s) {
+  const int nb = per_orbital_nblk(g, N);
+  dim3 grid(nb, N);
+  ::po::count_launch();
+  if (!up)
+    launch_pdl(residual_bb_stream_kernel<false, false>, grid, dim3(PT), 0, s, g, N, u, hu, sigma_diag,
+               up, xp, sig_prev, z, partials);
+  else if (sig_prev)
+    launch_pdl(residual_bb_stream_kernel<true, true>, grid, dim3(PT), 0, s, g, N, u, hu, sigma_diag, up,
+               xp, sig_prev, z, partials);
+  else
+    launch_pdl(residual_bb_stream_kernel<true, false>, grid, dim3(PT), 0, s, g, N, u, hu, sigma_diag, up,
+               xp, sig_prev, z, partials);
+  return nb;
 }
 
 void launch_bb(const SlabGeom& g, int N, const double* w, const double* wp, const double* z,

@@ -69,6 +69,13 @@ void launch_residual_diag(const SlabGeom& g, int N, const double* u, const doubl
 void launch_residual_bb(const SlabGeom& g, int N, const double* u, const double* hu,
                         const double* sigma_diag, const double* up, const double* zp, double* z,
                         double* partials, cudaStream_t s);
+// The elementwise directions pass (N > 64 with ||D||^2 from the Grams): z = fma(-sigma, u, hu)
+// (written only if z != null), partials [4][N][nblk]: zz, ss, sy, yy (raw) against
+// (up, z_prev), z_prev = fma(-sig_prev, up, xp) when sig_prev else xp; no history when
+// up is null (row 0 only). Returns nblk.
+int launch_residual_bb_stream(const SlabGeom& g, int N, const double* u, const double* hu,
+                              const double* sigma_diag, const double* up, const double* xp,
+                              const double* sig_prev, double* z, double* partials, cudaStream_t s);
 // BB products (optimizer.cpp:386-397); partials [3][N][nblk]: ss, sy, yy (raw).
 void launch_bb(const SlabGeom& g, int N, const double* w, const double* wp, const double* z,
                const double* zp, double* partials, cudaStream_t s);
@@ -236,6 +243,10 @@ void launch_matrix_stats(int N, const double* G, double* out, cudaStream_t s,
                          const double* guard = nullptr);
 // out[i] = M(i, i)
 void launch_copy_diag(int N, const double* M, double* out, cudaStream_t s);
+// ||D_i||^2 of D = HW - W Sigma from Sigma, G_WW, G_HH (dd) with a rounding bound
+// (err); sig_save (nullable) <- sig (dense.cu dnorm_grams_kernel)
+void launch_dnorm_grams(int N, const double* S, const double* Gww, const double* Ghh, double* dd,
+                        double* err, const double* sig, double* sig_save, cudaStream_t s);
 
 // ------------------------------------------------------------------ rng.cu
 // parorb::Rng(seed) normals (rng.hpp:13-41) drawn orbital-major over the full

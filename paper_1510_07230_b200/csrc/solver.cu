@@ -402,7 +402,8 @@ struct Solver {
     Clock::time_point t0;
     bool orth_iter = false, need_full = false, fused = false;
     bool zv = false;  // z implicit (see prev_hw); zsig slot zslot
-    bool bigdir = false;  // the directions ran as dir_big_kernel (N > 64)
+    bool bigdir = false;  // the directions ran on the N > 64 passes (z may be implicit)
+    bool dd_grams = false;  // ||D_i||^2 came from the Grams (checked at the readback)
     int zslot = 0;
     BRef z, dscratch;
     struct {
@@ -543,28 +544,52 @@ void Solver::enqueue_phase1(int iter) {
         launch_copy_diag(n, E.dmat[4], E.dvec + E.off_sig(), E.s);
       }
       int dnb = -1;
+      bool stream_done = false;
       if (big_dir) {
         if (ph.zv && !ghh_fresh) {  // the trial Grams need G_HH: no implicit z without it
           ph.zv = false;
           z = pool.get();
         }
-        // z (implicit or stored), ||z||^2, ||HW - W Sigma||^2 and the BB products
-        // against (W_prev, z_prev) in one TMA pass (dir_big_kernel)
-        dnb = launch_directions_big(
-            n, E.g.ld, E.g.ngl, P(w), P(hw), history_valid ? P(prev_w) : nullptr,
-            history_valid ? (prev_zv ? P(prev_hw) : P(prev_z)) : nullptr,
-            history_valid && prev_zv ? zsig(prev_zslot) : nullptr, E.dmat[4], E.dvec + E.off_sig(),
-            ph.zv ? nullptr : P(z), ph.zv ? E.dvec + E.off_zsig(ph.zslot) : nullptr, E.partials, E.s);
-        if (dnb < 0) {  // unavailable: the stored-direction passes below
-          if (ph.zv) {
-            ph.zv = false;
-            z = pool.get();
+        static const bool dd_grams_env =
+            !std::getenv("PO_DNORM_GRAMS") || std::atoi(std::getenv("PO_DNORM_GRAMS")) != 0;
+        const double* xprev =
+            history_valid ? (prev_zv ? P(prev_hw) : P(prev_z)) : nullptr;
+        const double* sprev = history_valid && prev_zv ? zsig(prev_zslot) : nullptr;
+        double* zsave = ph.zv ? E.dvec + E.off_zsig(ph.zslot) : nullptr;
+        if (dd_grams_env && gww_valid && ghh_fresh && tma2d_available()) {
+          // ||D_i||^2 from Sigma, G_WW, G_HH (checked against its rounding bound at
+          // the readback; the direct pass when it is not provably accurate) and
+          // the elementwise half — z, ||z||^2, BB products — as one streaming pass
+          launch_dnorm_grams(n, E.dmat[4], E.dmat[8], E.dmat[7], E.dvec + E.off_dd(),
+                             E.dvec + E.off_abs(), E.dvec + E.off_sig(), zsave, E.s);
+          const int nb = launch_residual_bb_stream(
+              E.g, n, P(w), P(hw), E.dvec + E.off_sig(), history_valid ? P(prev_w) : nullptr, xprev,
+              sprev, ph.zv ? nullptr : P(z), E.partials, E.s);
+          E.reduce_rows(E.partials, n, nb, E.g.w, E.dvec + E.off_zz(), true);
+          if (history_valid)
+            E.reduce_rows(E.partials + (size_t)n * nb, 3 * n, nb, E.g.w, E.dvec + E.off_ss(), true);
+          ph.dd_grams = true;
+          stream_done = true;
+          bb_done = history_valid;
+        } else {
+          // z (implicit or stored), ||z||^2, ||HW - W Sigma||^2 and the BB products
+          // against (W_prev, z_prev) in one TMA pass (dir_big_kernel)
+          dnb = launch_directions_big(n, E.g.ld, E.g.ngl, P(w), P(hw),
+                                      history_valid ? P(prev_w) : nullptr, xprev, sprev, E.dmat[4],
+                                      E.dvec + E.off_sig(), ph.zv ? nullptr : P(z), zsave,
+                                      E.partials, E.s);
+          if (dnb < 0) {  // unavailable: the stored-direction passes below
+            if (ph.zv) {
+              ph.zv = false;
+              z = pool.get();
+            }
+            materialize_prev_z();
           }
-          materialize_prev_z();
         }
-        ph.bigdir = dnb >= 0;
+        ph.bigdir = stream_done || dnb >= 0;
       }
-      if (dnb >= 0) {
+      if (stream_done) {
+      } else if (dnb >= 0) {
         E.reduce_rows(E.partials, (history_valid ? 5 : 2) * n, dnb, E.g.w, E.dvec + E.off_zz(), true);
         bb_done = history_valid;
       } else if (history_valid) {  // z, ||z||^2 and the BB products in one pass
@@ -577,7 +602,7 @@ void Solver::enqueue_phase1(int iter) {
         launch_residual_diag(E.g, n, P(w), P(hw), E.dvec + E.off_sig(), P(z), E.partials, E.s);
         E.reduce_rows(E.partials, n, onb, E.g.w, E.dvec + E.off_zz(), true);
       }
-      if (need_full && dnb < 0) {
+      if (need_full && dnb < 0 && !stream_done) {
         if (mean_abs) dscratch = pool.get();
         E.mix(P(w), nullptr, 0.0, E.dmat[4], -1.0, P(hw), 1.0, 0, dscratch ? P(dscratch) : nullptr,
               E.dvec + E.off_dd());
@@ -652,6 +677,22 @@ bool Solver::step() {
     (void)dscratch;
     E.fetch_all();
     const double* hv = E.hvec;
+    if (ph.dd_grams) {
+      // ||D||^2 from the Grams is used only when provably accurate: its rounding
+      // bound below 1e-8 of the value, and the gradient far from grad_tol (the
+      // convergence decision cannot flip); else the direct pass over the blocks
+      double sdd = 0.0, serr = 0.0;
+      for (int i = 0; i < n; ++i) {
+        sdd += hv[E.off_dd() + i];
+        serr += hv[E.off_abs() + i];
+      }
+      static const bool dbg = std::getenv("PO_DEBUG_DD") != nullptr;
+      if (dbg) std::fprintf(stderr, "dd_grams: sum dd %.17g sum err %.6g\n", sdd, serr);
+      if (!(sdd >= 1e8 * serr && sdd >= 100.0 * p.grad_tol * p.grad_tol)) {
+        E.mix(P(w), nullptr, 0.0, E.dmat[4], -1.0, P(hw), 1.0, 0, nullptr, E.dvec + E.off_dd());
+        E.fetch_all();
+      }
+    }
     if ((full_grad || need_full) && hv[E.off_scal() + Engine::S_SYM + 1] > 1e-10)
       throw Error(PO_EINVAL, "stiefel_gradient: <(HU)^T U> is not symmetric; inconsistent H or U");
     double znorm2 = 0.0, grad_norm = -1.0, mean_abs_v = -1.0;

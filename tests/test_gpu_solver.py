@@ -215,11 +215,13 @@ print(json.dumps([x["energy"] for x in r.records] + [r.energy["total"]]))
 
 @pytest.mark.parametrize("n_orb", [80, 128])
 def test_large_n_direction_paths_agree(port, native, n_orb):
-    """N > 64 directions (dir_big_kernel): the implicit z = HW - sigma W (default;
-    the rotation rebuilds it per element), the stored z (PO_ZFREE=0, written by
-    the same kernel) and the separate residual / BB / gradient-norm passes
-    (PO_NO_DIR_BIG=1) give the same trajectory (bitwise z; sums reduced in
-    another order) and match the C restatement. N = 80 takes the dense
+    """N > 64 directions: ||D||^2 from the Grams + the streaming z / BB pass
+    with an implicit z = HW - sigma W (default; the rotation rebuilds it per
+    element), the stored z (PO_ZFREE=0), ||D||^2 by the direct TMA pass
+    (dir_big_kernel, PO_DNORM_GRAMS=0) and the separate residual / BB /
+    gradient-norm passes (PO_NO_DIR_BIG=1) give the same trajectory and
+    gradient norms (bitwise z; sums reduced in another order) and match the C
+    restatement. N = 80 takes the dense
     mix_big rotation, N = 128 the balanced triangular one."""
     import json
     import subprocess
@@ -244,7 +246,8 @@ print(json.dumps([[x["energy"], x["backtracks"], x["grad_norm"]] for x in r.reco
     with tempfile.TemporaryDirectory() as d:
         np.save(os.path.join(d, "u0.npy"), u0)
         for name, env_over in [("implicit", {}), ("stored", {"PO_ZFREE": "0"}),
-                               ("separate", {"PO_NO_DIR_BIG": "1"})]:
+                               ("direct_dd", {"PO_DNORM_GRAMS": "0"}),
+                               ("separate", {"PO_NO_DIR_BIG": "1", "PO_DNORM_GRAMS": "0"})]:
             env = {k: v for k, v in os.environ.items() if not k.startswith("PO_")}
             env.update(env_over)
             r = subprocess.run([sys.executable, "-c", code, os.path.join(d, "u0.npy")], capture_output=True,
@@ -252,7 +255,7 @@ print(json.dumps([[x["energy"], x["backtracks"], x["grad_norm"]] for x in r.reco
             assert r.returncode == 0, (name, r.stderr[-2000:])
             runs[name] = json.loads(r.stdout.strip().split("\n")[-1])
     base = runs["implicit"]
-    for name in ("stored", "separate"):
+    for name in ("stored", "direct_dd", "separate"):
         for a, b in zip(runs[name][:-1], base[:-1]):
             assert a[1] == b[1] and abs(a[0] - b[0]) < 1e-9 and abs(a[2] - b[2]) < 1e-9 * max(1.0, b[2]), name
     for a, b in zip(base[:-1], ref["records"]):
