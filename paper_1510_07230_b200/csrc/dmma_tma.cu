@@ -1536,6 +1536,70 @@ struct BigCfg {  // consumer warps WM x WN, warp tile (T/WM) x (T/WN)
   static constexpr int FM = GT_T / (8 * WM), FN = GT_T / (8 * WN);
 };
 
+// Stage loop of a T = 128 symmetric diagonal tile (gram_big_kernel): warp a of
+// each half owns fragment rows fr = {a, 7-a, 8+a, 15-a}; TWO: the operand is
+// A + sa Ab, formed at the fragment load.
+template <bool TWO>
+__device__ __forceinline__ void sym_diag_stages(double (&gacc)[4][16][2], int a, const int (&fr)[4],
+                                                const double* stage0, size_t sdoubles, int nstage,
+                                                int nst, uint64_t* full, uint64_t* empty, int q0,
+                                                int qb2, double sa, int t4, int gq, int lane) {
+  constexpr size_t QS = (size_t)128 * BOX;
+      for (int st = 0; st < nstage; ++st) {
+        const int s = st % nst;
+        mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+        const double* sbuf = stage0 + (size_t)s * sdoubles;
+#pragma unroll
+        for (int kg = 0; kg < 2; ++kg) {
+          const int p = 8 * kg + 2 * t4;
+          double2 ar[4], bprev = make_double2(0.0, 0.0);
+          int cntprev = 0;
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            // rows r <= c among the owned ones (sorted a < 7-a < 8+a < 15-a): a
+            // warp-uniform count. The first k-step of column c is issued before
+            // the second k-step of column c - 1, so consecutive DMMAs are
+            // independent. (A per-row-set template copy issuing only the useful
+            // DMMAs measured slower, 1.62 vs 1.45 ms at C3: instruction fetch.)
+            double2 bc = make_double2(0.0, 0.0);
+            int cnt = 0;
+            if (c >= a) {
+              {
+                const int off = swz(8 * c + gq, p, 128);
+                bc = *reinterpret_cast<const double2*>(sbuf + (size_t)q0 * QS + off);
+                if (TWO) {
+                  const double2 zb = *reinterpret_cast<const double2*>(sbuf + (size_t)qb2 * QS + off);
+                  bc.x += sa * zb.x;
+                  bc.y += sa * zb.y;
+                }
+              }
+              if (c == fr[0]) ar[0] = bc;
+              if (c == fr[1]) ar[1] = bc;
+              if (c == fr[2]) ar[2] = bc;
+              if (c == fr[3]) ar[3] = bc;
+              cnt = (c >= fr[0]) + (c >= fr[1]) + (c >= fr[2]) + (c >= fr[3]);
+#pragma unroll
+              for (int f = 0; f < 4; ++f)
+                if (f < cnt) dmma_8x8x4(gacc[f][c], ar[f].x, bc.x);
+            }
+            if (c > 0) {
+#pragma unroll
+              for (int f = 0; f < 4; ++f)
+                if (f < cntprev) dmma_8x8x4(gacc[f][c - 1], ar[f].y, bprev.y);
+            }
+            bprev = bc;
+            cntprev = cnt;
+          }
+#pragma unroll
+          for (int f = 0; f < 4; ++f) dmma_8x8x4(gacc[f][15], ar[f].y, bprev.y);  // c = 15 >= every row
+          if (kg == 1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+          }
+        }
+      }
+}
+
 template <int GT_T>
 __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(const __grid_constant__ Maps maps,
                                                           int nsrc, int qa_b, int qb, int qb_b,
@@ -1655,31 +1719,40 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
       return v;
     };
     if (!diag) {
-      for (int st = 0; st < nstage; ++st) {
-        const int s = st % nst;
-        mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
-        const double* sbuf = stage0 + (size_t)s * sdoubles;
+      // one-source operands (Sigma, off-diagonal symmetric tiles) get a loop with
+      // no predicated combine in their fragment loads (as the diagonal tiles)
+      auto stages = [&](auto two) {
+        constexpr bool TWO = decltype(two)::value;
+        for (int st = 0; st < nstage; ++st) {
+          const int s = st % nst;
+          mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+          const double* sbuf = stage0 + (size_t)s * sdoubles;
 #pragma unroll
-        for (int kg = 0; kg < 2; ++kg) {
-          const int p = 8 * kg + 2 * t4;
-          double2 a[FM], b[FN];
+          for (int kg = 0; kg < 2; ++kg) {
+            const int p = 8 * kg + 2 * t4;
+            double2 a[FM], b[FN];
 #pragma unroll
-          for (int f = 0; f < FM; ++f) a[f] = load_frag(sbuf, 0, qa_b, sa, WM * f + wm, p);
+            for (int f = 0; f < FM; ++f) a[f] = load_frag(sbuf, 0, TWO ? qa_b : -1, sa, WM * f + wm, p);
 #pragma unroll
-          for (int f = 0; f < FN; ++f) b[f] = load_frag(sbuf, qb, qb_b, sb, WN * f + wn, p);
-          if (kg == 1) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);  // all fragments of the stage are in registers
-          }
-#pragma unroll
-          for (int fm = 0; fm < FM; ++fm)
-#pragma unroll
-            for (int fn = 0; fn < FN; ++fn) {
-              dmma_8x8x4(acc[fm][fn], a[fm].x, b[fn].x);
-              dmma_8x8x4(acc[fm][fn], a[fm].y, b[fn].y);
+            for (int f = 0; f < FN; ++f) b[f] = load_frag(sbuf, qb, TWO ? qb_b : -1, sb, WN * f + wn, p);
+            if (kg == 1) {
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&empty[s]);  // all fragments of the stage are in registers
             }
+#pragma unroll
+            for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+              for (int fn = 0; fn < FN; ++fn) {
+                dmma_8x8x4(acc[fm][fn], a[fm].x, b[fn].x);
+                dmma_8x8x4(acc[fm][fn], a[fm].y, b[fn].y);
+              }
+          }
         }
-      }
+      };
+      if (qa_b >= 0 || qb_b >= 0)
+        stages(std::true_type{});
+      else
+        stages(std::false_type{});
     } else if constexpr (GT_T == 128) {
       // Diagonal tile of a symmetric Gram, T = 128 (16 fragment rows): warps 0-3
       // take the first 16-point half of every stage, warps 4-7 the second, and
@@ -1699,51 +1772,14 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
 #pragma unroll
         for (int c = 0; c < 16; ++c) gacc[f][c][0] = gacc[f][c][1] = 0.0;
       const int q0 = hf * nload, qb2 = qa_b >= 0 ? hf * nload + qa_b : -1;
-      for (int st = 0; st < nstage; ++st) {
-        const int s = st % nst;
-        mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
-        const double* sbuf = stage0 + (size_t)s * sdoubles;
-#pragma unroll
-        for (int kg = 0; kg < 2; ++kg) {
-          const int p = 8 * kg + 2 * t4;
-          double2 ar[4], bprev = make_double2(0.0, 0.0);
-          int cntprev = 0;
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            // rows r <= c among the owned ones (sorted a < 7-a < 8+a < 15-a): a
-            // warp-uniform count. The first k-step of column c is issued before
-            // the second k-step of column c - 1, so consecutive DMMAs are
-            // independent. (A per-row-set template copy issuing only the useful
-            // DMMAs measured slower, 1.62 vs 1.45 ms at C3: instruction fetch.)
-            double2 bc = make_double2(0.0, 0.0);
-            int cnt = 0;
-            if (c >= a) {
-              bc = load_frag(sbuf, q0, qb2, sa, c, p);
-              if (c == fr[0]) ar[0] = bc;
-              if (c == fr[1]) ar[1] = bc;
-              if (c == fr[2]) ar[2] = bc;
-              if (c == fr[3]) ar[3] = bc;
-              cnt = (c >= fr[0]) + (c >= fr[1]) + (c >= fr[2]) + (c >= fr[3]);
-#pragma unroll
-              for (int f = 0; f < 4; ++f)
-                if (f < cnt) dmma_8x8x4(gacc[f][c], ar[f].x, bc.x);
-            }
-            if (c > 0) {
-#pragma unroll
-              for (int f = 0; f < 4; ++f)
-                if (f < cntprev) dmma_8x8x4(gacc[f][c - 1], ar[f].y, bprev.y);
-            }
-            bprev = bc;
-            cntprev = cnt;
-          }
-#pragma unroll
-          for (int f = 0; f < 4; ++f) dmma_8x8x4(gacc[f][15], ar[f].y, bprev.y);  // c = 15 >= every row
-          if (kg == 1) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-          }
-        }
-      }
+      // one-source (G_HH, G2) and two-source (a trial's G0) loops are separate
+      // instantiations: the one-source loop carries no predicated combine
+      if (qb2 >= 0)
+        sym_diag_stages<true>(gacc, a, fr, stage0, sdoubles, nstage, nst, full, empty, q0, qb2, sa, t4,
+                              gq, lane);
+      else
+        sym_diag_stages<false>(gacc, a, fr, stage0, sdoubles, nstage, nst, full, empty, q0, qb2, sa, t4,
+                               gq, lane);
       constexpr int SP = GT_T + 8;
       double* S = stage0;
       // ring fully consumed — by the density warp too, before the ring becomes S
@@ -2552,7 +2588,11 @@ __device__ __forceinline__ void mix_tri_slice(double (&acc)[4][8][2], const doub
 __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
     const __grid_constant__ Maps maps, int has_ab, int N, int64_t ld, int64_t ngl, int n_pt,
     int n_it, int nst, double sa, double alpha, double* __restrict__ out,
-    const double* __restrict__ guard, const double* __restrict__ zsig) {
+    const double* __restrict__ guard, const double* __restrict__ zsig, int mres) {
+  // mres (one orbital tile, N = 128): M^T stays resident in shared memory for
+  // the whole kernel (8 boxes = 128 KB, loaded once) instead of two 16 KB boxes
+  // per stage — per tile that was as much TMA traffic (L2) as the operands, all
+  // in 128-B rows, the request-rate-bound kind (profiles/r1_tma2d_probe.txt)
   PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
@@ -2566,14 +2606,18 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
   constexpr size_t QM = (size_t)XI * XK;  // one M^T box
   const int nsrc = has_ab ? 2 : 1;
   // stage: [A half 0][A half 1]([Ab half 0][Ab half 1])[M^T chunk of half 0][M^T chunk of half 1]
+  // (mres: no M^T chunks; the resident M^T follows the ring)
   const size_t mofs = (size_t)2 * nsrc * QH;
-  const size_t sdoubles = mofs + 2 * QM;
+  const size_t sdoubles = mofs + (mres ? 0 : 2 * QM);
+  double* mtres = stage0 + (size_t)nst * sdoubles;  // [XI / XK boxes][QM]
+  uint64_t* mbar_res = full + 24;
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 8);
       mbar_init(&ready[s], 1);
     }
+    mbar_init(mbar_res, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -2596,6 +2640,11 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
       for (int q = 0; q <= nsrc; ++q)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[q])));
       const uint32_t bytes = (uint32_t)(sdoubles * 8);
+      if (mres) {  // the whole (padded) M^T once: box ck holds k = 16 ck .. 16 ck + 15
+        mbar_arrive_expect_tx(mbar_res, (uint32_t)((XI / XK) * QM * 8));
+        for (int ck = 0; ck < XI / XK; ++ck)
+          tma_load_2d(mtres + (size_t)ck * QM, &maps.m[nsrc], ck * XK, 0, mbar_res);
+      }
       int g = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         int pt, it;
@@ -2612,7 +2661,7 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
               for (int b = 0; b < 4; ++b)
                 tma_load_2d(sb + (q * 2 + hf) * QH + b * BOX * XK, &maps.m[q],
                             pt * XP + hf * 64 + b * BOX, ck * XK, &full[s]);
-            tma_load_2d(sb + mofs + hf * QM, &maps.m[nsrc], ck * XK, it * XI, &full[s]);
+            if (!mres) tma_load_2d(sb + mofs + hf * QM, &maps.m[nsrc], ck * XK, it * XI, &full[s]);
           }
         }
       }
@@ -2660,6 +2709,7 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
     const int gq = lane >> 2, t4 = lane & 3;
     const int hf = warp >> 2, a = warp & 3;  // half (0 forwards, 1 backwards), fragment set
     const int fr[4] = {a, 7 - a, 8 + a, 15 - a};
+    if (mres) mbar_wait(mbar_res, 0);
     int g = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int pt, it;
@@ -2676,8 +2726,8 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
         mbar_wait(has_ab ? &ready[s] : &full[s], (uint32_t)(g / nst) & 1u);
         const double* sb = stage0 + (size_t)s * sdoubles;
         const double* sa_ = sb + hf * QH;
-        const double* mt = sb + mofs + hf * QM;
         const int ck = hf ? nk - 1 - c : c;
+        const double* mt = mres ? mtres + (size_t)ck * QM : sb + mofs + hf * QM;
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int h = hf ? 1 - hh : hh;
@@ -2774,13 +2824,17 @@ int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double
   const int nsrc = Ab ? 2 : 1;
   static const int tri_env = getenv("PO_MIX_TRI") ? atoi(getenv("PO_MIX_TRI")) : 1;  // measurement
   const bool tri = tri_env && upper && !C && !norms && N % XI == 0;
-  const size_t sdoubles = tri ? (size_t)2 * nsrc * 64 * XK + 2 * XI * XK : (size_t)(nsrc + 1) * XP * XK;
+  static const int mres_env = getenv("PO_MT_RESIDENT") ? atoi(getenv("PO_MT_RESIDENT")) : 1;
+  const bool mres = tri && N == XI && mres_env;  // resident M^T (128 KB) + a 3..6-stage ring
+  const size_t sdoubles = tri ? (size_t)2 * nsrc * 64 * XK + (mres ? 0 : 2 * XI * XK)
+                              : (size_t)(nsrc + 1) * XP * XK;
   const size_t fixed = 1024 + 1024;  // barriers, alignment slack
-  int nst = (int)((200 * 1024 - fixed) / (sdoubles * 8));
+  const size_t resd = mres ? (size_t)XI * XI : 0;
+  int nst = (int)(((mres ? 227 : 200) * 1024 - fixed - resd * 8) / (sdoubles * 8));
   if (nst > 8) nst = 8;
   if (nst < 2) PO_MB_FAIL("shared memory");
 #undef PO_MB_FAIL
-  const size_t smem = fixed + (size_t)nst * sdoubles * 8;
+  const size_t smem = fixed + ((size_t)nst * sdoubles + resd) * 8;
   ::po::count_launch();
   launch_pdl(transpose_pad_kernel, dim3((unsigned)(((int64_t)np * np + 255) / 256)), dim3(256), 0, s, N, np, M, mt);
   const int n_pt = mix_big_nblk(ngl);
@@ -2791,7 +2845,7 @@ int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double
     set_smem(reinterpret_cast<const void*>(mix_tri_kernel), (int)smem);
     ::po::count_launch();
     launch_pdl(mix_tri_kernel, dim3(grid), dim3(XTH), smem, s, maps, Ab ? 1 : 0, N, ld, ngl, n_pt, n_it,
-               nst, sa, alpha, out, guard, Ab ? zsig : (const double*)nullptr);
+               nst, sa, alpha, out, guard, Ab ? zsig : (const double*)nullptr, mres ? 1 : 0);
     return n_pt;
   }
   set_smem(reinterpret_cast<const void*>(mix_big_kernel), (int)smem);
