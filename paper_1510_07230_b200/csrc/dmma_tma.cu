@@ -1536,68 +1536,77 @@ struct BigCfg {  // consumer warps WM x WN, warp tile (T/WM) x (T/WN)
   static constexpr int FM = GT_T / (8 * WM), FN = GT_T / (8 * WN);
 };
 
-// Stage loop of a T = 128 symmetric diagonal tile (gram_big_kernel): warp a of
-// each half owns fragment rows fr = {a, 7-a, 8+a, 15-a}; TWO: the operand is
-// A + sa Ab, formed at the fragment load.
+// Stage loop of a T = 128 symmetric diagonal tile (gram_big_kernel). The 16
+// fragment rows form an 8 x 8 grid of 16 x 16 super-blocks; warp a of each
+// half owns super-rows a and a + 4 and the circulant slots (R, (R + k) mod 8),
+// k = 0..3, plus the one slot (a, a + 4): 9 super-blocks = 36 DMMA blocks per
+// k-step, the same straight-line code for every warp (8 of the 144 issued
+// blocks, the lower halves of the diagonal super-blocks, are wasted; every
+// unordered super-block pair appears exactly once). Per 8 points a warp loads
+// the 16 fragments once (16 LDS.128) for 72 DMMAs. acc0[k] = (a, a + k),
+// acc1[k] = (a + 4, (a + 4 + k) mod 8). TWO: the operand is A + sa Ab, formed at
+// the fragment load.
 template <bool TWO>
-__device__ __forceinline__ void sym_diag_stages(double (&gacc)[4][16][2], int a, const int (&fr)[4],
-                                                const double* stage0, size_t sdoubles, int nstage,
-                                                int nst, uint64_t* full, uint64_t* empty, int q0,
-                                                int qb2, double sa, int t4, int gq, int lane) {
-  constexpr size_t QS = (size_t)128 * BOX;
-      for (int st = 0; st < nstage; ++st) {
-        const int s = st % nst;
-        mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
-        const double* sbuf = stage0 + (size_t)s * sdoubles;
+__device__ __forceinline__ void sym_diag_stages(double (&acc0)[5][2][2][2], double (&acc1)[4][2][2][2],
+                                                int a, const double* stage0, size_t sdoubles,
+                                                int nstage, int nst, uint64_t* full, uint64_t* empty,
+                                                int q0, int qb2, double sa, int t4, int gq, int lane) {
+  constexpr int QS = 128 * BOX;
+  // doubles offset of fragment (2 sr(j), row gq, points 2 t4 ..) in an area; the
+  // second fragment of the super-row is + 8 rows, the second 8 points ^ 8
+  int off[8];
 #pragma unroll
-        for (int kg = 0; kg < 2; ++kg) {
-          const int p = 8 * kg + 2 * t4;
-          double2 ar[4], bprev = make_double2(0.0, 0.0);
-          int cntprev = 0;
+  for (int j = 0; j < 8; ++j) off[j] = q0 * QS + swz(16 * ((a + j) & 7) + gq, 2 * t4, 128);
+  const int dz = TWO ? (qb2 - q0) * QS : 0;
+  for (int st = 0; st < nstage; ++st) {
+    const int s = st % nst;
+    mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+    const double* sbuf = stage0 + (size_t)s * sdoubles;
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            // rows r <= c among the owned ones (sorted a < 7-a < 8+a < 15-a): a
-            // warp-uniform count. The first k-step of column c is issued before
-            // the second k-step of column c - 1, so consecutive DMMAs are
-            // independent. (A per-row-set template copy issuing only the useful
-            // DMMAs measured slower, 1.62 vs 1.45 ms at C3: instruction fetch.)
-            double2 bc = make_double2(0.0, 0.0);
-            int cnt = 0;
-            if (c >= a) {
-              {
-                const int off = swz(8 * c + gq, p, 128);
-                bc = *reinterpret_cast<const double2*>(sbuf + (size_t)q0 * QS + off);
-                if (TWO) {
-                  const double2 zb = *reinterpret_cast<const double2*>(sbuf + (size_t)qb2 * QS + off);
-                  bc.x += sa * zb.x;
-                  bc.y += sa * zb.y;
-                }
-              }
-              if (c == fr[0]) ar[0] = bc;
-              if (c == fr[1]) ar[1] = bc;
-              if (c == fr[2]) ar[2] = bc;
-              if (c == fr[3]) ar[3] = bc;
-              cnt = (c >= fr[0]) + (c >= fr[1]) + (c >= fr[2]) + (c >= fr[3]);
+    for (int kg = 0; kg < 2; ++kg) {
+      double2 f[8][2];
 #pragma unroll
-              for (int f = 0; f < 4; ++f)
-                if (f < cnt) dmma_8x8x4(gacc[f][c], ar[f].x, bc.x);
-            }
-            if (c > 0) {
+      for (int j = 0; j < 8; ++j)
 #pragma unroll
-              for (int f = 0; f < 4; ++f)
-                if (f < cntprev) dmma_8x8x4(gacc[f][c - 1], ar[f].y, bprev.y);
-            }
-            bprev = bc;
-            cntprev = cnt;
-          }
-#pragma unroll
-          for (int f = 0; f < 4; ++f) dmma_8x8x4(gacc[f][15], ar[f].y, bprev.y);  // c = 15 >= every row
-          if (kg == 1) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+        for (int e = 0; e < 2; ++e) {
+          const double* src = sbuf + ((off[j] + e * 8 * BOX) ^ (8 * kg));
+          f[j][e] = *reinterpret_cast<const double2*>(src);
+          if (TWO) {
+            const double2 zb = *reinterpret_cast<const double2*>(src + dz);
+            f[j][e].x += sa * zb.x;
+            f[j][e].y += sa * zb.y;
           }
         }
+      if (kg == 1) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);  // all fragments of the stage are in registers
       }
+#pragma unroll
+      for (int k = 0; k < 5; ++k)
+#pragma unroll
+        for (int ea = 0; ea < 2; ++ea)
+#pragma unroll
+          for (int eb = 0; eb < 2; ++eb) dmma_8x8x4(acc0[k][ea][eb], f[0][ea].x, f[k][eb].x);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int ea = 0; ea < 2; ++ea)
+#pragma unroll
+          for (int eb = 0; eb < 2; ++eb) dmma_8x8x4(acc1[k][ea][eb], f[4][ea].x, f[4 + k][eb].x);
+#pragma unroll
+      for (int k = 0; k < 5; ++k)
+#pragma unroll
+        for (int ea = 0; ea < 2; ++ea)
+#pragma unroll
+          for (int eb = 0; eb < 2; ++eb) dmma_8x8x4(acc0[k][ea][eb], f[0][ea].y, f[k][eb].y);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int ea = 0; ea < 2; ++ea)
+#pragma unroll
+          for (int eb = 0; eb < 2; ++eb) dmma_8x8x4(acc1[k][ea][eb], f[4][ea].y, f[4 + k][eb].y);
+    }
+  }
 }
 
 template <int GT_T>
@@ -1765,21 +1774,24 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
       // (shared-memory bound at 68% of FP64 on C3). The two halves' partial
       // blocks meet in the epilogue.
       const int hf = warp >> 2, a = warp & 3;
-      const int fr[4] = {a, 7 - a, 8 + a, 15 - a};
-      double gacc[4][16][2];
+      double acc0[5][2][2][2], acc1[4][2][2][2];
 #pragma unroll
-      for (int f = 0; f < 4; ++f)
+      for (int k = 0; k < 5; ++k)
 #pragma unroll
-        for (int c = 0; c < 16; ++c) gacc[f][c][0] = gacc[f][c][1] = 0.0;
+        for (int e = 0; e < 4; ++e) acc0[k][e >> 1][e & 1][0] = acc0[k][e >> 1][e & 1][1] = 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc1[k][e >> 1][e & 1][0] = acc1[k][e >> 1][e & 1][1] = 0.0;
       const int q0 = hf * nload, qb2 = qa_b >= 0 ? hf * nload + qa_b : -1;
       // one-source (G_HH, G2) and two-source (a trial's G0) loops are separate
-      // instantiations: the one-source loop carries no predicated combine
+      // instantiations: the one-source loop carries no combine
       if (qb2 >= 0)
-        sym_diag_stages<true>(gacc, a, fr, stage0, sdoubles, nstage, nst, full, empty, q0, qb2, sa, t4,
+        sym_diag_stages<true>(acc0, acc1, a, stage0, sdoubles, nstage, nst, full, empty, q0, qb2, sa, t4,
                               gq, lane);
       else
-        sym_diag_stages<false>(gacc, a, fr, stage0, sdoubles, nstage, nst, full, empty, q0, qb2, sa, t4,
-                               gq, lane);
+        sym_diag_stages<false>(acc0, acc1, a, stage0, sdoubles, nstage, nst, full, empty, q0, qb2, sa,
+                               t4, gq, lane);
       constexpr int SP = GT_T + 8;
       double* S = stage0;
       // ring fully consumed — by the density warp too, before the ring becomes S
@@ -1787,25 +1799,33 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
         asm volatile("bar.sync 3, %0;\n" ::"n"((Cfg::NW + 1) * 32) : "memory");
       else
         asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NW * 32) : "memory");
-      // pass 0: half 0 stores its blocks; pass 1: half 1 adds (same block set)
+      // pass 0: half 0 stores its blocks; pass 1: half 1 adds (same block set).
+      // Slots whose column wrapped below their row land transposed; the lower
+      // block of a diagonal super-block is dropped.
+      auto put = [&](int pass, int R, int C, int ea, int eb, const double (&v)[2]) {
+        if (R == C && ea > eb) return;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int r = 16 * R + 8 * ea + gq, c = 16 * C + 8 * eb + 2 * t4 + j;
+          const int idx = R <= C ? r * SP + c : c * SP + r;
+          if (pass == 0)
+            S[idx] = v[j];
+          else
+            S[idx] += v[j];
+        }
+      };
 #pragma unroll
       for (int pass = 0; pass < 2; ++pass) {
         if (hf == pass) {
 #pragma unroll
-          for (int f = 0; f < 4; ++f)
+          for (int k = 0; k < 5; ++k)
 #pragma unroll
-            for (int c = 0; c < 16; ++c) {
-              const int r = fr[f];
-              if (c < r) continue;
+            for (int e = 0; e < 4; ++e) put(pass, a, a + k, e >> 1, e & 1, acc0[k][e >> 1][e & 1]);
 #pragma unroll
-              for (int j = 0; j < 2; ++j) {
-                const int idx = (8 * r + gq) * SP + 8 * c + 2 * t4 + j;
-                if (pass == 0)
-                  S[idx] = gacc[f][c][j];
-                else
-                  S[idx] += gacc[f][c][j];
-              }
-            }
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              put(pass, a + 4, (a + 4 + k) & 7, e >> 1, e & 1, acc1[k][e >> 1][e & 1]);
         }
         asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NW * 32) : "memory");
       }
