@@ -1609,7 +1609,27 @@ __device__ __forceinline__ void sym_diag_stages(double (&acc0)[5][2][2][2], doub
   }
 }
 
-template <int GT_T>
+// BB: the elementwise half of compute_directions rides on the Sigma Gram
+// (N <= 128, one non-symmetric tile: area 0 holds HW, area qb holds W — every
+// orbital of both blocks passes through shared memory anyway). Two warps of the
+// producer group own two orbitals per lane (i, i + 32) and, per stage, read
+// their 16 points of HW, W and — from two extra ring areas — W_prev and HW_prev
+// (or a stored Z_prev): z = fma(-sigma_i, W, HW) (the FMA of every z path),
+// ||z_i||^2 and the BB products <s,s>, <s,y>, <y,y> against (W_prev, z_prev)
+// (manifold.cpp:204-216, optimizer.cpp:386-397) accumulate in registers over
+// the CTA's point range; one partial per (sum, orbital, split). sigma_i is the
+// H u pass's own <HW_i, W_i> (the Gram's diagonal does not exist yet). The
+// separate streaming pass over four blocks (1.24 ms at C3) disappears; the
+// FP64-bound Gram hides the two extra streams.
+struct GramBBArgs {
+  const double* sig;    // sigma_i of the current iterate (device, N)
+  const double* sigp;   // previous sigma (z_prev implicit) or null (area holds Z_prev)
+  double* part;         // [4][N][nsplit]: zz, ss, sy, yy (raw sums)
+  int hist;             // history valid: W_prev / X_prev areas are streamed
+  int N;
+};
+
+template <int GT_T, bool BB = false>
 __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(const __grid_constant__ Maps maps,
                                                           int nsrc, int qa_b, int qb, int qb_b,
                                                           int mt, int sym, int64_t ld,
@@ -1618,7 +1638,7 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
                                                           const double* __restrict__ guard,
                                                           double* __restrict__ rho,
                                                           double* __restrict__ bvec, double occ,
-                                                          int64_t ngl) {
+                                                          int64_t ngl, const GramBBArgs bb) {
   // rho (T = 128, one symmetric diagonal tile, one source): the verification
   // Gram of a rotated trial also yields its density (energy.cpp:67-76) and
   // 4 pi rho — producer warp 1 sums the squares of all N orbitals per point
@@ -1631,10 +1651,11 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
   uint64_t* empty = full + 8;
   double* stage0 = reinterpret_cast<double*>(tsm + 1024);
   constexpr size_t QS = (size_t)GT_T * BOX;  // doubles per source per stage
-  const size_t sdoubles = (size_t)nsrc * QS;
+  const int nbb = BB && bb.hist ? 2 : 0;     // extra ring areas: W_prev, X_prev
+  const size_t sdoubles = (size_t)(nsrc + nbb) * QS;
   int tm, tn;
   big_tile_index(blockIdx.x, mt, sym, tm, tn);
-  const bool diag = sym && tm == tn;
+  const bool diag = !BB && sym && tm == tn;
   // sources fetched per 16-point half: A (+Ab); B (+Bb) unless this is a symmetric diagonal tile
   const int nload = diag ? (qa_b >= 0 ? 2 : 1) : nsrc;
   using Cfg = BigCfg<GT_T>;
@@ -1642,7 +1663,7 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], Cfg::NW + (dens ? 1 : 0));
+      mbar_init(&empty[s], Cfg::NW + (dens ? 1 : 0) + (BB ? 4 : 0));
     }
     fence_mbar_init();
   }
@@ -1655,7 +1676,99 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
   const int lane = threadIdx.x & 31;
   int warp = threadIdx.x >> 5;
   if (warp < Cfg::PW) {
-    if constexpr (Cfg::PW == 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if constexpr (Cfg::PW == 4) {
+      // BB: the two elementwise warps need ~70 registers; the consumers of the
+      // non-symmetric tile fit 208 (80 x 128 + 208 x 256 <= the 168 x 384 registers the
+      // CTA was launched with — setmaxnreg.inc waits forever for more than that)
+      if constexpr (BB)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
+      else
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    }
+    if constexpr (BB) {
+      // All four warps of the producer group do the elementwise work, one orbital
+      // per lane (a quarter-warp reads 8 consecutive rows, one 16-byte chunk each,
+      // distinct under the 128-B swizzle). Measured at C3 (1.92 ms plain Gram):
+      // streaming the two extra sources costs nothing (1.96 ms with the
+      // elementwise work switched off, 1.98 ms with its shared loads only); the
+      // DFMAs interleaved with the consumers' DMMAs on the FP64 pipe cost the
+      // rest — 2.40 ms with ||z||^2 alone, 2.66 ms with the BB products, the
+      // same with two or four warps, split accumulators or one burst per
+      // stage — still 0.5 ms less than the separate pass (1.24 ms). Lane 0 of
+      // warp 0 is also the TMA producer: before its warp works on stage st it
+      // refills the slot stage st - 1 used (stage st + nst - 1), as early as a
+      // dedicated producer could.
+      const int i = 32 * warp + lane;
+      const double ms = i < bb.N ? -bb.sig[i] : 0.0;
+      const double msp = (bb.sigp && i < bb.N) ? -bb.sigp[i] : 0.0;
+      double r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
+      const bool hist = bb.hist != 0, zpi = bb.sigp != nullptr;
+      const int ro = i * BOX, sw = i & 7;
+      const uint32_t bytes = (uint32_t)((nload + nbb) * QS * 8);
+      auto issue = [&](int g) {  // stage g into slot g % nst (its previous use released)
+        const int s = g % nst;
+        if (g >= nst) mbar_wait(&empty[s], ((uint32_t)(g / nst) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&full[s], bytes);
+        const int x = (int)(kbeg + (int64_t)g * pps);
+        double* sbuf = stage0 + (size_t)s * sdoubles;
+        for (int q = 0; q < nload; ++q)
+          tma_load_2d(sbuf + q * QS, &maps.m[q], x, (q == qb ? tn : tm) * GT_T, &full[s]);
+        for (int q = nload; q < nload + nbb; ++q)  // W_prev, X_prev of the same points
+          tma_load_2d(sbuf + q * QS, &maps.m[q], x, 0, &full[s]);
+      };
+      if (warp == 0 && lane == 0) {
+        for (int q = 0; q < nload + nbb; ++q)
+          asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[q])));
+        for (int g = 0; g < nst && g < nstage; ++g) issue(g);
+      }
+      for (int st = 0; st < nstage; ++st) {
+        if (warp == 0) {
+          if (lane == 0 && st >= 1 && st + nst - 1 < nstage) issue(st + nst - 1);
+          __syncwarp();
+        }
+        const int s = st % nst;
+        mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+        const double* sbuf = stage0 + (size_t)s * sdoubles;
+        const double* hA = sbuf + ro;                        // HW rows (area 0)
+        const double* wA = sbuf + (size_t)qb * QS + ro;      // W rows
+        const double* pA = sbuf + (size_t)nsrc * QS + ro;    // W_prev
+        const double* xA = pA + QS;                          // HW_prev or Z_prev
+#pragma unroll 4
+        for (int c = 0; c < 8; ++c) {
+          const int off = (c ^ sw) << 1;
+          const double2 h = *reinterpret_cast<const double2*>(hA + off);
+          const double2 w = *reinterpret_cast<const double2*>(wA + off);
+          const double z0 = fma(ms, w.x, h.x), z1 = fma(ms, w.y, h.y);
+          r0 += z0 * z0;
+          r0 += z1 * z1;
+          if (hist) {
+            const double2 wq = *reinterpret_cast<const double2*>(pA + off);
+            const double2 xq = *reinterpret_cast<const double2*>(xA + off);
+            const double q0 = zpi ? fma(msp, wq.x, xq.x) : xq.x;
+            const double q1 = zpi ? fma(msp, wq.y, xq.y) : xq.y;
+            const double s0 = w.x - wq.x, y0 = z0 - q0;
+            const double s1 = w.y - wq.y, y1 = z1 - q1;
+            r1 += s0 * s0;
+            r1 += s1 * s1;
+            r2 += s0 * y0;
+            r2 += s1 * y1;
+            r3 += y0 * y0;
+            r3 += y1 * y1;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      if (i < bb.N) {
+        const int64_t nb = gridDim.y;
+        bb.part[((int64_t)0 * bb.N + i) * nb + blockIdx.y] = r0;
+        if (hist) {
+          bb.part[((int64_t)1 * bb.N + i) * nb + blockIdx.y] = r1;
+          bb.part[((int64_t)2 * bb.N + i) * nb + blockIdx.y] = r2;
+          bb.part[((int64_t)3 * bb.N + i) * nb + blockIdx.y] = r3;
+        }
+      }
+    } else
     if (warp == 0 && lane == 0) {
       for (int q = 0; q < nload; ++q)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[q])));
@@ -1706,7 +1819,12 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
       asm volatile("bar.sync 3, %0;\n" ::"n"((Cfg::NW + 1) * 32) : "memory");
     }
   } else {
-    if constexpr (Cfg::PW == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    if constexpr (Cfg::PW == 4) {
+      if constexpr (BB)
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
+      else
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    }
     warp -= Cfg::PW;
     const int gq = lane >> 2, t4 = lane & 3;
     constexpr int FM = Cfg::FM, FN = Cfg::FN, WM = Cfg::WM, WN = Cfg::WN;
@@ -1762,6 +1880,8 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
         stages(std::true_type{});
       else
         stages(std::false_type{});
+    } else if constexpr (BB) {
+      return;  // (never: a BB launch has no symmetric tiles)
     } else if constexpr (GT_T == 128) {
       // Diagonal tile of a symmetric Gram, T = 128 (16 fragment rows): warps 0-3
       // take the first 16-point half of every stage, warps 4-7 the second, and
@@ -2921,8 +3041,11 @@ size_t gram_big_workspace_doubles(int64_t ld, int N) {
 bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                      const double* B, const double* Bb, double sb, double* ws, size_t ws_doubles,
                      double* G, double w, cudaStream_t s, const double* guard, double* rho,
-                     double* bvec, double occ, int64_t ngl) {
+                     double* bvec, double occ, int64_t ngl, GramBB* bbl) {
   const int GT_T = big_tile(N, sym, Ab != nullptr || !sym);
+  // the fused elementwise pass: Sigma = <(HW)^T W> as one non-symmetric 128-tile
+  static const bool bb_off = getenv("PO_NO_GRAM_BB") != nullptr;  // measurement switch
+  if (bbl && (bb_off || sym || Ab || Bb || GT_T != 128 || N > 128 || N <= 64 || rho)) return false;
   // the fused density needs the whole orbital set in one diagonal tile
   if (rho && !(sym && !Ab && GT_T == 128 && N <= 128 && N > 64)) return false;
   Maps maps;
@@ -2954,17 +3077,28 @@ bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* 
   }
   const BigPlan p = big_plan(ld, N, sym, nsm(), GT_T);
   if ((size_t)p.nsplit * p.ntiles * GT_T * GT_T > ws_doubles) return false;
-  const size_t sdoubles = (size_t)nsrc * GT_T * BOX;
-  int nst = (int)((200 * 1024 / 8) / sdoubles);
+  GramBBArgs bba{nullptr, nullptr, nullptr, 0, N};
+  int nbb = 0;
+  if (bbl) {
+    if (bbl->wp) {  // history: W_prev and HW_prev / Z_prev ride in two more ring areas
+      if (!make_map(&maps.m[nsrc], bbl->wp, ld, N, GT_T) || !make_map(&maps.m[nsrc + 1], bbl->xp, ld, N, GT_T))
+        return false;
+      nbb = 2;
+    }
+    bba = GramBBArgs{bbl->sig, bbl->wp ? bbl->sigp : nullptr, bbl->partials, bbl->wp ? 1 : 0, N};
+    bbl->nsplit = p.nsplit;
+  }
+  const size_t sdoubles = (size_t)(nsrc + nbb) * GT_T * BOX;
+  int nst = (int)(((bbl ? 224 : 200) * 1024 / 8) / sdoubles);
   if (nst > 8) nst = 8;
   if (nst < 2) return false;
   const size_t smem = 2048 + (size_t)nst * sdoubles * 8;
   ::po::count_launch();
-  auto k = GT_T == 64 ? gram_big_kernel<64> : gram_big_kernel<128>;
+  auto k = bbl ? gram_big_kernel<128, true> : GT_T == 64 ? gram_big_kernel<64> : gram_big_kernel<128>;
   const int threads = GT_T == 64 ? BigCfg<64>::THREADS : BigCfg<128>::THREADS;
   set_smem(reinterpret_cast<const void*>(k), (int)smem);
   launch_pdl(k, dim3(dim3(p.ntiles, p.nsplit)), dim3(threads), smem, s, maps, nsrc, qa_b, qb, qb_b, p.mt, sym, ld, p.kchunk,
-                                                 nst, sa, sb, ws, guard, rho, bvec, occ, ngl);
+                                                 nst, sa, sb, ws, guard, rho, bvec, occ, ngl, bba);
   const int64_t total = (int64_t)N * N;
   ::po::count_launch();
   launch_pdl(gram_big_reduce_kernel, dim3((unsigned)((total + 31) / 32)), dim3(dim3(32, 8)), 0, s, GT_T, N, p.mt, sym, p.ntiles,

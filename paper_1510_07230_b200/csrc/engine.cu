@@ -441,6 +441,13 @@ bool Engine::gram_density(const double* A, double* Gdev, double* rho, double* bv
   return true;
 }
 
+bool Engine::gram_sigma_bb(const double* hw, const double* w, double* Gdev, GramBB* bb) {
+  if (size > 1 || N <= 64 || N > 128 || !tma2d_available()) return false;
+  return launch_gram_big(N, g.ld, 0, hw, nullptr, 0.0, w, nullptr, 0.0, gram_ws,
+                         gram_workspace_doubles(g, N), Gdev, g.w, s, nullptr, nullptr, nullptr, 1.0, 0,
+                         bb);
+}
+
 void Engine::mix(const double* A, const double* Ab, double sa, const double* M, double alpha,
                  const double* C, double beta, int upper, double* out, double* norm_rows,
                  const double* guard, const double* zsig) {
@@ -987,6 +994,16 @@ extern "C" int po_enqueue(po_engine* h, int op, int a, int b, int out) {
                                             E.dvec, E.dvec + E.off_zsig(0))) < 0)
         throw Error(PO_EINVAL, "directions kernel unavailable for this N");
       break;
+    case PO_OP_GRAM_SIGMA_BB: {
+      // the iteration's Sigma Gram (a = HW, b = W) carrying ||z||^2 and the BB
+      // products (history: the same blocks, previous z implicit); 64 < N <= 128
+      po::GramBB gb{E.dvec + E.off_sig(), E.dvec + E.off_sig(), E.blk(b), E.blk(a), E.partials, 0};
+      if (!E.gram_sigma_bb(E.blk(a), E.blk(b), E.dmat[0], &gb))
+        throw Error(PO_EINVAL, "Sigma Gram with fused directions unavailable for this N");
+      E.reduce_rows(E.partials, E.N, gb.nsplit, E.g.w, E.dvec + E.off_zz(), true);
+      E.reduce_rows(E.partials + (size_t)E.N * gb.nsplit, 3 * E.N, gb.nsplit, E.g.w, E.dvec + E.off_ss(), true);
+      break;
+    }
     case PO_OP_ROTATION_IMPLICIT:
       // the large-N trial rotation: b is HW, z = HW - sigma W rebuilt per element
       if (po::launch_mix(E.g, E.N, E.blk(a), E.blk(b), -0.3, E.dmat[1], 1.0, nullptr, 0.0, 1,

@@ -126,6 +126,9 @@ class Engine {
   // symmetric Gram of A that also writes A's density rho (+ 4 pi rho into bvec);
   // false (nothing enqueued) where the fused form is unavailable
   bool gram_density(const double* A, double* Gdev, double* rho, double* bvec);
+  // Sigma = w (HW)^T W with the elementwise half of compute_directions fused
+  // (64 < N <= 128, one rank); false if unavailable (nothing launched)
+  bool gram_sigma_bb(const double* hw, const double* w, double* Gdev, GramBB* bb);
   void mix(const double* A, const double* Ab, double sa, const double* M, double alpha,
            const double* C, double beta, int upper, double* out, double* norm_rows,
            const double* guard = nullptr, const double* zsig = nullptr);

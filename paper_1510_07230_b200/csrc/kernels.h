@@ -153,10 +153,21 @@ size_t gram_big_workspace_doubles(int64_t ld, int N);
 // rho (nullable): with one source, sym and 64 < N <= 128 (one diagonal tile) the
 // Gram also writes the density occ sum_i A_i^2 (+ 4 pi rho into bvec) of the
 // ngl points; false (nothing launched) where that is unavailable
+// bbl (64 < N <= 128, A = HW, B = W, non-symmetric): the Gram also does the
+// elementwise half of compute_directions (||z_i||^2 and, with wp / xp, the BB
+// products; z = HW - sig W implicit) — partials [4][N][nsplit]: zz, ss, sy, yy.
+struct GramBB {
+  const double* sig;   // sigma_i (device, N): the H u pass's <HW_i, W_i>
+  const double* sigp;  // previous sigma when xp is the previous HW, null when xp is a stored Z_prev
+  const double* wp;    // W_prev (null: no history, only ||z||^2)
+  const double* xp;    // HW_prev or Z_prev
+  double* partials;
+  int nsplit;          // out: partial columns per (sum, orbital)
+};
 bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* Ab, double sa,
                      const double* B, const double* Bb, double sb, double* ws, size_t ws_doubles,
                      double* G, double w, cudaStream_t s, const double* guard, double* rho = nullptr,
-                     double* bvec = nullptr, double occ = 1.0, int64_t ngl = 0);
+                     double* bvec = nullptr, double occ = 1.0, int64_t ngl = 0, GramBB* bbl = nullptr);
 // Fused compute_directions + BB products for N <= 48 (one pass over W, HW
 // [, WP, ZP]): writes Z = HW - diag(sig) W and per-orbital partial rows
 // [zz | dd | ss | sy | yy] (dd = ||HW - W Sigma||^2 when Sigma != null; the

@@ -532,8 +532,25 @@ void Solver::enqueue_phase1(int iter) {
         E.reduce_rows(E.partials, n, onb, 1.0, E.dvec + E.off_abs(), true);
       }
     } else {
+      static const bool dd_grams_env =
+          !std::getenv("PO_DNORM_GRAMS") || std::atoi(std::getenv("PO_DNORM_GRAMS")) != 0;
+      // 64 < N <= 128 with z implicit and ||D||^2 from the Grams: the elementwise
+      // half of the directions (||z||^2, BB products) rides on the Sigma Gram,
+      // with sigma_i from the H u pass (dvec sigma row) — no pass of its own
+      int bb_nb = -1;
       if (need_full || !sig_valid) {
-        sigma(w, hw);
+        if (big_dir && ph.zv && dd_grams_env && gww_valid && sig_valid && tma2d_available()) {
+          GramBB gb{E.dvec + E.off_sig(),
+                    history_valid && prev_zv ? zsig(prev_zslot) : nullptr,
+                    history_valid ? P(prev_w) : nullptr,
+                    history_valid ? (prev_zv ? P(prev_hw) : P(prev_z)) : nullptr,
+                    E.partials, 0};
+          if (E.gram_sigma_bb(P(hw), P(w), E.dmat[4], &gb)) {
+            launch_matrix_stats(E.N, E.dmat[4], E.scal() + Engine::S_SYM, E.s);
+            bb_nb = gb.nsplit;
+          }
+        }
+        if (bb_nb < 0) sigma(w, hw);
         if (gww_valid) {
           // G_HH = w (HW)^T HW: the line search's trial Grams then come from
           // G_WW, Sigma and G_HH (launch_trial_gram) instead of a two-source
@@ -541,7 +558,7 @@ void Solver::enqueue_phase1(int iter) {
           E.gram(P(hw), nullptr, 0.0, P(hw), nullptr, 0.0, 1, E.dmat[7]);
           ghh_fresh = true;
         }
-        launch_copy_diag(n, E.dmat[4], E.dvec + E.off_sig(), E.s);
+        if (bb_nb < 0) launch_copy_diag(n, E.dmat[4], E.dvec + E.off_sig(), E.s);
       }
       int dnb = -1;
       bool stream_done = false;
@@ -550,8 +567,6 @@ void Solver::enqueue_phase1(int iter) {
           ph.zv = false;
           z = pool.get();
         }
-        static const bool dd_grams_env =
-            !std::getenv("PO_DNORM_GRAMS") || std::atoi(std::getenv("PO_DNORM_GRAMS")) != 0;
         const double* xprev =
             history_valid ? (prev_zv ? P(prev_hw) : P(prev_z)) : nullptr;
         const double* sprev = history_valid && prev_zv ? zsig(prev_zslot) : nullptr;
@@ -562,9 +577,11 @@ void Solver::enqueue_phase1(int iter) {
           // the elementwise half — z, ||z||^2, BB products — as one streaming pass
           launch_dnorm_grams(n, E.dmat[4], E.dmat[8], E.dmat[7], E.dvec + E.off_dd(),
                              E.dvec + E.off_abs(), E.dvec + E.off_sig(), zsave, E.s);
-          const int nb = launch_residual_bb_stream(
-              E.g, n, P(w), P(hw), E.dvec + E.off_sig(), history_valid ? P(prev_w) : nullptr, xprev,
-              sprev, ph.zv ? nullptr : P(z), E.partials, E.s);
+          const int nb = bb_nb >= 0 ? bb_nb
+                                    : launch_residual_bb_stream(
+                                          E.g, n, P(w), P(hw), E.dvec + E.off_sig(),
+                                          history_valid ? P(prev_w) : nullptr, xprev, sprev,
+                                          ph.zv ? nullptr : P(z), E.partials, E.s);
           E.reduce_rows(E.partials, n, nb, E.g.w, E.dvec + E.off_zz(), true);
           if (history_valid)
             E.reduce_rows(E.partials + (size_t)n * nb, 3 * n, nb, E.g.w, E.dvec + E.off_ss(), true);

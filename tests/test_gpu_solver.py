@@ -215,9 +215,11 @@ print(json.dumps([x["energy"] for x in r.records] + [r.energy["total"]]))
 
 @pytest.mark.parametrize("n_orb", [80, 128])
 def test_large_n_direction_paths_agree(port, native, n_orb):
-    """N > 64 directions: ||D||^2 from the Grams + the streaming z / BB pass
-    with an implicit z = HW - sigma W (default; the rotation rebuilds it per
-    element), the stored z (PO_ZFREE=0), ||D||^2 by the direct TMA pass
+    """N > 64 directions: ||D||^2 from the Grams + ||z||^2 and the BB products
+    on the Sigma Gram (N <= 128: gram_big_kernel<128, BB>; PO_NO_GRAM_BB=1: the
+    separate streaming pass) with an implicit z = HW - sigma W (default; the
+    rotation rebuilds it per element), the stored z (PO_ZFREE=0), ||D||^2 by the
+    direct TMA pass
     (dir_big_kernel, PO_DNORM_GRAMS=0) and the separate residual / BB /
     gradient-norm passes (PO_NO_DIR_BIG=1) give the same trajectory and
     gradient norms (bitwise z; sums reduced in another order) and match the C
@@ -239,13 +241,14 @@ spec = configs.small_molecule(14, %d, L=8.0)
 e = native.engine_for(spec)
 w = e.block_from(np.load(sys.argv[1]))
 r = e.solve(w, "opt_par_mod", True, True, max_inner=6, n_org=1, n_diag=100)
-print(json.dumps([[x["energy"], x["backtracks"], x["grad_norm"]] for x in r.records] + [r.energy["total"]]))
+print(json.dumps([[x["energy"], x["backtracks"], x["grad_norm"], x["tau"]] for x in r.records] + [r.energy["total"]]))
 ''' % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), n_orb)
     import tempfile
     runs = {}
     with tempfile.TemporaryDirectory() as d:
         np.save(os.path.join(d, "u0.npy"), u0)
         for name, env_over in [("implicit", {}), ("stored", {"PO_ZFREE": "0"}),
+                               ("stream_bb", {"PO_NO_GRAM_BB": "1"}),
                                ("direct_dd", {"PO_DNORM_GRAMS": "0"}),
                                ("separate", {"PO_NO_DIR_BIG": "1", "PO_DNORM_GRAMS": "0"})]:
             env = {k: v for k, v in os.environ.items() if not k.startswith("PO_")}
@@ -255,9 +258,11 @@ print(json.dumps([[x["energy"], x["backtracks"], x["grad_norm"]] for x in r.reco
             assert r.returncode == 0, (name, r.stderr[-2000:])
             runs[name] = json.loads(r.stdout.strip().split("\n")[-1])
     base = runs["implicit"]
-    for name in ("stored", "direct_dd", "separate"):
+    for name in ("stored", "stream_bb", "direct_dd", "separate"):
         for a, b in zip(runs[name][:-1], base[:-1]):
             assert a[1] == b[1] and abs(a[0] - b[0]) < 1e-9 and abs(a[2] - b[2]) < 1e-9 * max(1.0, b[2]), name
+            assert abs(a[3] - b[3]) < 1e-9 * max(1.0, abs(b[3])), name  # the BB step (ss, sy, yy sums)
     for a, b in zip(base[:-1], ref["records"]):
         assert abs(a[0] - b["energy"]) < TOL_E and a[1] == b["backtracks"]
         assert abs(a[2] - b["grad_norm"]) < 1e-8 * max(1.0, b["grad_norm"])
+        assert abs(a[3] - b["tau"]) < 1e-8 * max(1.0, abs(b["tau"]))
