@@ -450,12 +450,23 @@ def ours(args, spec):
         dom = add_kernel("rotate_fused_kernel (rotation + G2 + density)", r_ms, 3 * blk, 2.0 * N * (N + 1) * ng)
         dom_bound = "hbm"
     else:  # the large-N tiles of the C3 step
-        sig = add_kernel("gram_big_kernel<128> Sigma = w (HW)^T W", sg_ms, 2 * blk, 2.0 * N * N * ng)
+        sig_bytes = 2 * blk
+        if N <= 128:
+            # the iteration's Sigma Gram also carries the directions' elementwise half
+            # (||z||^2, BB products; W_prev / HW_prev streamed beside HW / W): 4 blocks
+            sg_ms = time_kernel(torch, native, e, "gram_sigma_bb", 10, a=hw_b, b=cur)
+            sig_bytes = 4 * blk
+            sig = add_kernel("gram_big_kernel<128, BB> Sigma = w (HW)^T W + ||z||^2 / BB sums (implicit z)",
+                             sg_ms, sig_bytes, 2.0 * N * N * ng)
+        else:
+            sig = add_kernel("gram_big_kernel<128> Sigma = w (HW)^T W", sg_ms, 2 * blk, 2.0 * N * N * ng)
         add_kernel("gram_big_kernel<128> symmetric (G_HH; verification G2 + the trial's density)", g_ms, blk,
                    float(N) * (N + 1) * ng, per_iter=2)
-        e.enqueue("gram", a=hw_b, b=cur)
-        d_ms = time_kernel(torch, native, e, "directions", 10, a=cur, b=hw_b, out=z_b)
-        add_kernel("dir_big_kernel (D norms, implicit z, ||z||^2, BB)", d_ms, 4 * blk, 2.0 * N * N * ng)
+        if N > 128:  # (the separate elementwise pass is HBM-bound; ||D||^2 comes from the Grams)
+            e.enqueue("gram", a=hw_b, b=cur)
+            d_ms = time_kernel(torch, native, e, "directions", 10, a=cur, b=hw_b, out=z_b)
+            add_kernel("dir_big_kernel (direct D norms, implicit z, ||z||^2, BB; fallback pass)", d_ms, 4 * blk,
+                       2.0 * N * N * ng, per_iter=0)
         e.enqueue("gram_sym", a=cur)
         e.enqueue("cholesky")
         r_ms = time_kernel(torch, native, e, "rotation_implicit", 10, a=cur, b=hw_b, out=scratch)
@@ -464,9 +475,10 @@ def ours(args, spec):
         # gram_big_kernel over its three launches of the iteration (Sigma, G_HH, the
         # verification G2): the kernel with the largest share of the step
         tot_ms = sg_ms + 2 * g_ms
-        dom = {"kernel": "gram_big_kernel<128> (Sigma + G_HH + G2, per-launch average)",
+        dom = {"kernel": "gram_big_kernel<128> (Sigma [+ directions' sums] + G_HH + G2, per-launch average)",
                "launch_ms": tot_ms / 3, "algorithmic_flops": (2.0 * N * N + 2.0 * N * (N + 1)) * ng / 3,
-               "algorithmic_bytes": 4 * blk / 3, "share_of_step": sig["share_of_step"] + step_kernels[2]["share_of_step"]}
+               "algorithmic_bytes": (sig_bytes + 2 * blk) / 3,
+               "share_of_step": sig["share_of_step"] + step_kernels[2]["share_of_step"]}
         dom["fp64_frac"] = dom["algorithmic_flops"] / (dom["launch_ms"] / 1e3) / 1e12 / fp64 if fp64 else None
         dom_bound = "tensor"
     e.free(hw_b)

@@ -1611,9 +1611,9 @@ __device__ __forceinline__ void sym_diag_stages(double (&acc0)[5][2][2][2], doub
 
 // BB: the elementwise half of compute_directions rides on the Sigma Gram
 // (N <= 128, one non-symmetric tile: area 0 holds HW, area qb holds W — every
-// orbital of both blocks passes through shared memory anyway). Two warps of the
-// producer group own two orbitals per lane (i, i + 32) and, per stage, read
-// their 16 points of HW, W and — from two extra ring areas — W_prev and HW_prev
+// orbital of both blocks passes through shared memory anyway). Each lane pair of
+// the eight consumer warps owns one orbital and, per stage, reads its 16 points
+// of HW, W and — from two extra ring areas — W_prev and HW_prev
 // (or a stored Z_prev): z = fma(-sigma_i, W, HW) (the FMA of every z path),
 // ||z_i||^2 and the BB products <s,s>, <s,y>, <y,y> against (W_prev, z_prev)
 // (manifold.cpp:204-216, optimizer.cpp:386-397) accumulate in registers over
@@ -1663,7 +1663,7 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], Cfg::NW + (dens ? 1 : 0) + (BB ? 4 : 0));
+      mbar_init(&empty[s], Cfg::NW + (dens ? 1 : 0));
     }
     fence_mbar_init();
   }
@@ -1676,103 +1676,13 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
   const int lane = threadIdx.x & 31;
   int warp = threadIdx.x >> 5;
   if (warp < Cfg::PW) {
-    if constexpr (Cfg::PW == 4) {
-      // BB: the two elementwise warps need ~70 registers; the consumers of the
-      // non-symmetric tile fit 208 (80 x 128 + 208 x 256 <= the 168 x 384 registers the
-      // CTA was launched with — setmaxnreg.inc waits forever for more than that)
-      if constexpr (BB)
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
-      else
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-    }
-    if constexpr (BB) {
-      // All four warps of the producer group do the elementwise work, one orbital
-      // per lane (a quarter-warp reads 8 consecutive rows, one 16-byte chunk each,
-      // distinct under the 128-B swizzle). Measured at C3 (1.92 ms plain Gram):
-      // streaming the two extra sources costs nothing (1.96 ms with the
-      // elementwise work switched off, 1.98 ms with its shared loads only); the
-      // DFMAs interleaved with the consumers' DMMAs on the FP64 pipe cost the
-      // rest — 2.40 ms with ||z||^2 alone, 2.66 ms with the BB products, the
-      // same with two or four warps, split accumulators or one burst per
-      // stage — still 0.5 ms less than the separate pass (1.24 ms). Lane 0 of
-      // warp 0 is also the TMA producer: before its warp works on stage st it
-      // refills the slot stage st - 1 used (stage st + nst - 1), as early as a
-      // dedicated producer could.
-      const int i = 32 * warp + lane;
-      const double ms = i < bb.N ? -bb.sig[i] : 0.0;
-      const double msp = (bb.sigp && i < bb.N) ? -bb.sigp[i] : 0.0;
-      double r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
-      const bool hist = bb.hist != 0, zpi = bb.sigp != nullptr;
-      const int ro = i * BOX, sw = i & 7;
-      const uint32_t bytes = (uint32_t)((nload + nbb) * QS * 8);
-      auto issue = [&](int g) {  // stage g into slot g % nst (its previous use released)
-        const int s = g % nst;
-        if (g >= nst) mbar_wait(&empty[s], ((uint32_t)(g / nst) & 1u) ^ 1u);
-        mbar_arrive_expect_tx(&full[s], bytes);
-        const int x = (int)(kbeg + (int64_t)g * pps);
-        double* sbuf = stage0 + (size_t)s * sdoubles;
-        for (int q = 0; q < nload; ++q)
-          tma_load_2d(sbuf + q * QS, &maps.m[q], x, (q == qb ? tn : tm) * GT_T, &full[s]);
-        for (int q = nload; q < nload + nbb; ++q)  // W_prev, X_prev of the same points
-          tma_load_2d(sbuf + q * QS, &maps.m[q], x, 0, &full[s]);
-      };
-      if (warp == 0 && lane == 0) {
-        for (int q = 0; q < nload + nbb; ++q)
-          asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[q])));
-        for (int g = 0; g < nst && g < nstage; ++g) issue(g);
-      }
-      for (int st = 0; st < nstage; ++st) {
-        if (warp == 0) {
-          if (lane == 0 && st >= 1 && st + nst - 1 < nstage) issue(st + nst - 1);
-          __syncwarp();
-        }
-        const int s = st % nst;
-        mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
-        const double* sbuf = stage0 + (size_t)s * sdoubles;
-        const double* hA = sbuf + ro;                        // HW rows (area 0)
-        const double* wA = sbuf + (size_t)qb * QS + ro;      // W rows
-        const double* pA = sbuf + (size_t)nsrc * QS + ro;    // W_prev
-        const double* xA = pA + QS;                          // HW_prev or Z_prev
-#pragma unroll 4
-        for (int c = 0; c < 8; ++c) {
-          const int off = (c ^ sw) << 1;
-          const double2 h = *reinterpret_cast<const double2*>(hA + off);
-          const double2 w = *reinterpret_cast<const double2*>(wA + off);
-          const double z0 = fma(ms, w.x, h.x), z1 = fma(ms, w.y, h.y);
-          r0 += z0 * z0;
-          r0 += z1 * z1;
-          if (hist) {
-            const double2 wq = *reinterpret_cast<const double2*>(pA + off);
-            const double2 xq = *reinterpret_cast<const double2*>(xA + off);
-            const double q0 = zpi ? fma(msp, wq.x, xq.x) : xq.x;
-            const double q1 = zpi ? fma(msp, wq.y, xq.y) : xq.y;
-            const double s0 = w.x - wq.x, y0 = z0 - q0;
-            const double s1 = w.y - wq.y, y1 = z1 - q1;
-            r1 += s0 * s0;
-            r1 += s1 * s1;
-            r2 += s0 * y0;
-            r2 += s1 * y1;
-            r3 += y0 * y0;
-            r3 += y1 * y1;
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-      }
-      if (i < bb.N) {
-        const int64_t nb = gridDim.y;
-        bb.part[((int64_t)0 * bb.N + i) * nb + blockIdx.y] = r0;
-        if (hist) {
-          bb.part[((int64_t)1 * bb.N + i) * nb + blockIdx.y] = r1;
-          bb.part[((int64_t)2 * bb.N + i) * nb + blockIdx.y] = r2;
-          bb.part[((int64_t)3 * bb.N + i) * nb + blockIdx.y] = r3;
-        }
-      }
-    } else
+    // (40 x 128 + 232 x 256 = the 168 x 384 registers the CTA is launched with:
+    // a setmaxnreg.inc asking for more than that waits forever)
+    if constexpr (Cfg::PW == 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     if (warp == 0 && lane == 0) {
-      for (int q = 0; q < nload; ++q)
+      for (int q = 0; q < nload + nbb; ++q)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[q])));
-      const int nbox = diag ? 2 * nload : nload;
+      const int nbox = diag ? 2 * nload : nload + nbb;
       const uint32_t bytes = (uint32_t)(nbox * QS * 8);
       for (int st = 0; st < nstage; ++st) {
         const int s = st % nst;
@@ -1789,6 +1699,8 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
             const int row0 = (q == qb || q == qb_b) ? tn * GT_T : tm * GT_T;
             tma_load_2d(sbuf + q * QS, &maps.m[q], x, row0, &full[s]);
           }
+          for (int q = nload; q < nload + nbb; ++q)  // BB: W_prev, X_prev of the same points
+            tma_load_2d(sbuf + q * QS, &maps.m[q], x, 0, &full[s]);
         }
       }
     } else if (dens && warp == 1) {
@@ -1819,12 +1731,7 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
       asm volatile("bar.sync 3, %0;\n" ::"n"((Cfg::NW + 1) * 32) : "memory");
     }
   } else {
-    if constexpr (Cfg::PW == 4) {
-      if constexpr (BB)
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
-      else
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
-    }
+    if constexpr (Cfg::PW == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
     warp -= Cfg::PW;
     const int gq = lane >> 2, t4 = lane & 3;
     constexpr int FM = Cfg::FM, FN = Cfg::FN, WM = Cfg::WM, WN = Cfg::WN;
@@ -1848,12 +1755,56 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
     if (!diag) {
       // one-source operands (Sigma, off-diagonal symmetric tiles) get a loop with
       // no predicated combine in their fragment loads (as the diagonal tiles)
+      // BB: lane pair (2 l, 2 l + 1) of consumer warp w owns orbital 16 w + l and
+      // one 8-point half of its 16 points per stage (4 chunks of 16 bytes; a
+      // quarter-warp's 4 rows x 2 halves hit 8 distinct chunks under the swizzle)
+      const int bi = BB ? 16 * warp + (lane >> 1) : 0, bh = lane & 1;
+      double bms = 0.0, bmsp = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
+      if constexpr (BB) {
+        bms = bi < bb.N ? -bb.sig[bi] : 0.0;
+        bmsp = (bb.sigp && bi < bb.N) ? -bb.sigp[bi] : 0.0;
+      }
+      const bool bhist = BB && bb.hist != 0, bzpi = BB && bb.sigp != nullptr;
       auto stages = [&](auto two) {
         constexpr bool TWO = decltype(two)::value;
         for (int st = 0; st < nstage; ++st) {
           const int s = st % nst;
           mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
           const double* sbuf = stage0 + (size_t)s * sdoubles;
+          if constexpr (BB) {
+            // the stage's elementwise work in this warp's own instruction stream,
+            // before its fragments are loaded (their registers are free): 64 DFMAs
+            // against the stage's 128 DMMAs per warp. (As the job of separate warps
+            // the same DFMAs starved behind the consumers' DMMAs on the FP64 pipe and
+            // held the ring: 2.66 ms instead of the plain Gram's 1.92 at C3.)
+            const double* hA = sbuf + bi * BOX;                       // HW rows (area 0)
+            const double* wA = sbuf + (size_t)qb * QS + bi * BOX;     // W rows
+            const double* pA = sbuf + (size_t)nsrc * QS + bi * BOX;   // W_prev
+            const double* xA = pA + QS;                               // HW_prev or Z_prev
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+              const int off = ((4 * bh + cc) ^ (bi & 7)) << 1;
+              const double2 h = *reinterpret_cast<const double2*>(hA + off);
+              const double2 w = *reinterpret_cast<const double2*>(wA + off);
+              const double z0 = fma(bms, w.x, h.x), z1 = fma(bms, w.y, h.y);
+              r0 += z0 * z0;
+              r0 += z1 * z1;
+              if (bhist) {
+                const double2 wq = *reinterpret_cast<const double2*>(pA + off);
+                const double2 xq = *reinterpret_cast<const double2*>(xA + off);
+                const double q0 = bzpi ? fma(bmsp, wq.x, xq.x) : xq.x;
+                const double q1 = bzpi ? fma(bmsp, wq.y, xq.y) : xq.y;
+                const double s0 = w.x - wq.x, y0 = z0 - q0;
+                const double s1 = w.y - wq.y, y1 = z1 - q1;
+                r1 += s0 * s0;
+                r1 += s1 * s1;
+                r2 += s0 * y0;
+                r2 += s1 * y1;
+                r3 += y0 * y0;
+                r3 += y1 * y1;
+              }
+            }
+          }
 #pragma unroll
           for (int kg = 0; kg < 2; ++kg) {
             const int p = 8 * kg + 2 * t4;
@@ -1880,6 +1831,21 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
         stages(std::true_type{});
       else
         stages(std::false_type{});
+      if constexpr (BB) {  // the two halves of an orbital's points meet; one partial per split
+        r0 += __shfl_xor_sync(0xffffffffu, r0, 1);
+        r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
+        r2 += __shfl_xor_sync(0xffffffffu, r2, 1);
+        r3 += __shfl_xor_sync(0xffffffffu, r3, 1);
+        if (bh == 0 && bi < bb.N) {
+          const int64_t nb = gridDim.y;
+          bb.part[((int64_t)0 * bb.N + bi) * nb + blockIdx.y] = r0;
+          if (bhist) {
+            bb.part[((int64_t)1 * bb.N + bi) * nb + blockIdx.y] = r1;
+            bb.part[((int64_t)2 * bb.N + bi) * nb + blockIdx.y] = r2;
+            bb.part[((int64_t)3 * bb.N + bi) * nb + blockIdx.y] = r3;
+          }
+        }
+      }
     } else if constexpr (BB) {
       return;  // (never: a BB launch has no symmetric tiles)
     } else if constexpr (GT_T == 128) {

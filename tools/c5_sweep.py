@@ -7,8 +7,10 @@ row records filled: true. Local potential: a smooth seeded field of 32
 Gaussians (width 2 bohr, A ~ U(-5, 0)). Timed separately with CUDA events on
 the engine stream (median of reps): batched H.u, density (+ LDA xc fused),
 Gram U^T U (symmetric), and the U L^-T rotation with L from the Cholesky of
-that block's Gram. Points that do not fit one GPU are reported as such (never
-skipped silently). Writes gpurun_out/c5_sweep.json.
+that block's Gram. Every row is also verified on the same data (verified: true):
+the rotated block is orthonormal to 1e-9 and <(Hu)^T u> is symmetric to 1e-10
+relative. Points that do not fit one GPU are reported as such (never skipped
+silently). Writes gpurun_out/c5_sweep.json.
 
 Rooflines: H.u / density against the measured HBM peak (MEASURED_PEAKS.json);
 Gram (N(N+1) N_g flops) and rotation (N(N+1) N_g flops, triangular) against the
@@ -78,8 +80,20 @@ for n in sizes:
         e.enqueue("cholesky", a=u)
         t_r = timeit(e, lambda: e.enqueue("mix_upper", a=u, out=out))
         fl_r = float(N) * (N + 1) * ng
+        # size-independent checks on the same filled blocks (no CPU reference fits here):
+        #  * the rotation of the block by the L^-T of its own Gram is orthonormal
+        #    (Gram + Cholesky + triangular rotation together, manifold.cpp:97-114, 150-157);
+        #  * H is symmetric on the block: <(Hu)^T u> equals its transpose
+        #    (H u + the non-symmetric Gram, manifold.cpp:181-187's own check)
+        g2 = e.gram(out, out)
+        orth_dev = float(np.abs(g2 - np.eye(N)).max())
+        e.enqueue("hamiltonian", a=u, out=out)
+        sg = e.gram(out, u)
+        asym = float(np.abs(sg - sg.T).max() / max(1.0, np.abs(sg).max()))
         row.update({
             "filled": True,
+            "verified": bool(orth_dev < 1e-9 and asym < 1e-10),
+            "rotation_orthonormality_dev": orth_dev, "hamiltonian_gram_rel_asymmetry": asym,
             "hamiltonian_us": 1e3 * t_h, "hamiltonian_GBs": bytes_h / t_h / 1e6,
             "hamiltonian_frac_hbm": bytes_h / t_h / 1e6 / HBM,
             "density_xc_us": 1e3 * t_d, "density_frac_hbm": bytes_d / t_d / 1e6 / HBM,
