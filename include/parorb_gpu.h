@@ -288,6 +288,7 @@ enum {
   PO_OP_DIRECTIONS = 11, /* fused directions: W = a, HW = b, history (a, b), Sigma = last Gram */
   PO_OP_ROTATION_FUSED = 12, /* rotation + verification Gram + density/xc (default state) */
   PO_OP_ROTATION_IMPLICIT = 13, /* out = (a - 0.3 z) M with z = b - sigma a implicit (b = HW; N > 64) */
+  PO_OP_GRAM_DENSITY = 15, /* G = <a^T a> + rho, 4 pi rho of block a in the same pass (64 < N <= 128) */
   PO_OP_GRAM_SIGMA_BB = 14, /* G = <a^T b> (a = HW, b = W) + the directions' ||z||^2 / BB sums (64 < N <= 128) */
   PO_OP_HAMILTONIAN_VARIANT = 100  /* + v: H a design-space variants (measurement builds only:
                                       make VARIANTS=1; else PO_EINVAL) */

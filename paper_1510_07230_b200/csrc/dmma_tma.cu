@@ -1546,11 +1546,20 @@ struct BigCfg {  // consumer warps WM x WN, warp tile (T/WM) x (T/WN)
 // the 16 fragments once (16 LDS.128) for 72 DMMAs. acc0[k] = (a, a + k),
 // acc1[k] = (a + 4, (a + 4 + k) mod 8). TWO: the operand is A + sa Ab, formed at
 // the fragment load.
-template <bool TWO>
+struct DensArgs {  // DENS: the tile's density rides on the stage loop (see gram_big_kernel)
+  double* rho;
+  double* bvec;
+  double occ;
+  int64_t p0, ngl;  // first point of the CTA's range, points of the slab
+  int w8;           // consumer warp 0..7
+};
+
+template <bool TWO, bool DENS>
 __device__ __forceinline__ void sym_diag_stages(double (&acc0)[5][2][2][2], double (&acc1)[4][2][2][2],
                                                 int a, const double* stage0, size_t sdoubles,
                                                 int nstage, int nst, uint64_t* full, uint64_t* empty,
-                                                int q0, int qb2, double sa, int t4, int gq, int lane) {
+                                                int q0, int qb2, double sa, int t4, int gq, int lane,
+                                                const DensArgs& da) {
   constexpr int QS = 128 * BOX;
   // doubles offset of fragment (2 sr(j), row gq, points 2 t4 ..) in an area; the
   // second fragment of the super-row is + 8 rows, the second 8 points ^ 8
@@ -1562,6 +1571,33 @@ __device__ __forceinline__ void sym_diag_stages(double (&acc0)[5][2][2][2], doub
     const int s = st % nst;
     mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
     const double* sbuf = stage0 + (size_t)s * sdoubles;
+    if constexpr (DENS) {
+      // rho of 4 of the stage's 32 points per warp, before the fragments are
+      // loaded: lane (q, c) sums the squares of orbitals 8 j + c at point
+      // 4 (w8 & 3) + q of half w8 >> 2 (a half-warp's 8 rows x 2 points are 16
+      // distinct 8-byte slots under the swizzle), then the 8 classes meet by
+      // shuffles. 16 DFMAs per lane in the warp's own stream (a separate density
+      // warp's DFMAs waited behind the consumers' DMMAs on the FP64 pipe).
+      const int o = 4 * (da.w8 & 3) + (lane >> 3), c = lane & 7;
+      const double* area = sbuf + (size_t)(da.w8 >> 2) * QS;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        const double v0 = area[swz(8 * j + c, o, 128)], v1 = area[swz(8 * j + 8 + c, o, 128)];
+        d0 = fma(v0, v0, d0);
+        d1 = fma(v1, v1, d1);
+      }
+      double d = d0 + d1;
+      d += __shfl_xor_sync(0xffffffffu, d, 1);
+      d += __shfl_xor_sync(0xffffffffu, d, 2);
+      d += __shfl_xor_sync(0xffffffffu, d, 4);
+      const int64_t p = da.p0 + (int64_t)st * 2 * BOX + 16 * (da.w8 >> 2) + o;
+      if (c == 0 && p < da.ngl) {
+        const double r = da.occ == 1.0 ? d : d * da.occ;
+        da.rho[p] = r;
+        if (da.bvec) da.bvec[p] = r * (4.0 * 3.141592653589793238462643383279502884);
+      }
+    }
 #pragma unroll
     for (int kg = 0; kg < 2; ++kg) {
       double2 f[8][2];
@@ -1641,8 +1677,9 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
                                                           int64_t ngl, const GramBBArgs bb) {
   // rho (T = 128, one symmetric diagonal tile, one source): the verification
   // Gram of a rotated trial also yields its density (energy.cpp:67-76) and
-  // 4 pi rho — producer warp 1 sums the squares of all N orbitals per point
-  // straight from each stage, so the trial needs no separate density pass
+  // 4 pi rho — each consumer warp sums the squares of all N orbitals at 4 of a
+  // stage's 32 points (sym_diag_stages<.., DENS>), so the trial needs no
+  // separate density pass
   PO_PDL_ENTRY();
   if (guard && *guard == 0.0) return;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
@@ -1663,7 +1700,7 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], Cfg::NW + (dens ? 1 : 0));
+      mbar_init(&empty[s], Cfg::NW);
     }
     fence_mbar_init();
   }
@@ -1703,32 +1740,6 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
             tma_load_2d(sbuf + q * QS, &maps.m[q], x, 0, &full[s]);
         }
       }
-    } else if (dens && warp == 1) {
-      // lane l: point 16 (l >> 4) + (l & 15) of the stage's two halves; orbitals
-      // in ascending order (energy.cpp:67-76); a half-warp reads one 128-B row
-      // per orbital (conflict-free under the swizzle)
-      const int h = lane >> 4, o = lane & 15;
-      const double four_pi = 4.0 * 3.141592653589793238462643383279502884;
-      for (int st = 0; st < nstage; ++st) {
-        const int s = st % nst;
-        mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
-        const double* area = stage0 + (size_t)s * sdoubles + (size_t)h * QS;
-        double acc = 0.0;
-        for (int i = 0; i < GT_T; ++i) {
-          const double v = area[swz(i, o, GT_T)];
-          acc += v * v;
-        }
-        const int64_t p = kbeg + (int64_t)st * pps + 16 * h + o;
-        if (p < ngl) {
-          const double r = occ == 1.0 ? acc : acc * occ;
-          rho[p] = r;
-          if (bvec) bvec[p] = r * four_pi;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-      }
-      // the consumers reuse the ring for the tile epilogue after this barrier
-      asm volatile("bar.sync 3, %0;\n" ::"n"((Cfg::NW + 1) * 32) : "memory");
     }
   } else {
     if constexpr (Cfg::PW == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
@@ -1872,19 +1883,19 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
       const int q0 = hf * nload, qb2 = qa_b >= 0 ? hf * nload + qa_b : -1;
       // one-source (G_HH, G2) and two-source (a trial's G0) loops are separate
       // instantiations: the one-source loop carries no combine
+      const DensArgs da{rho, bvec, occ, kbeg, ngl, warp};
       if (qb2 >= 0)
-        sym_diag_stages<true>(acc0, acc1, a, stage0, sdoubles, nstage, nst, full, empty, q0, qb2, sa, t4,
-                              gq, lane);
+        sym_diag_stages<true, false>(acc0, acc1, a, stage0, sdoubles, nstage, nst, full, empty, q0, qb2,
+                                     sa, t4, gq, lane, da);
+      else if (dens)
+        sym_diag_stages<false, true>(acc0, acc1, a, stage0, sdoubles, nstage, nst, full, empty, q0, qb2,
+                                     sa, t4, gq, lane, da);
       else
-        sym_diag_stages<false>(acc0, acc1, a, stage0, sdoubles, nstage, nst, full, empty, q0, qb2, sa,
-                               t4, gq, lane);
+        sym_diag_stages<false, false>(acc0, acc1, a, stage0, sdoubles, nstage, nst, full, empty, q0, qb2,
+                                      sa, t4, gq, lane, da);
       constexpr int SP = GT_T + 8;
       double* S = stage0;
-      // ring fully consumed — by the density warp too, before the ring becomes S
-      if (dens)
-        asm volatile("bar.sync 3, %0;\n" ::"n"((Cfg::NW + 1) * 32) : "memory");
-      else
-        asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NW * 32) : "memory");
+      asm volatile("bar.sync 1, %0;\n" ::"n"(Cfg::NW * 32) : "memory");  // ring fully consumed
       // pass 0: half 0 stores its blocks; pass 1: half 1 adds (same block set).
       // Slots whose column wrapped below their row land transposed; the lower
       // block of a diagonal super-block is dropped.
@@ -2694,7 +2705,9 @@ __device__ __forceinline__ void mix_tri_slice(double (&acc)[4][8][2], const doub
 __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
     const __grid_constant__ Maps maps, int has_ab, int N, int64_t ld, int64_t ngl, int n_pt,
     int n_it, int nst, double sa, double alpha, double* __restrict__ out,
-    const double* __restrict__ guard, const double* __restrict__ zsig, int mres) {
+    const double* __restrict__ guard, const double* __restrict__ zsig, int mres, int qform) {
+  // qform: zsig holds q_k and M^T is already scaled by sa (transpose_pad_kernel):
+  // the trial point is sa (HW_k + q_k W_k), one FMA per element
   // mres (one orbital tile, N = 128): M^T stays resident in shared memory for
   // the whole kernel (8 boxes = 128 KB, loaded once) instead of two 16 KB boxes
   // per stage — per tile that was as much TMA traffic (L2) as the operands, all
@@ -2786,22 +2799,34 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
           if (zsig) {  // -sigma of the stage's 2 x 16 orbitals (half 1 walks k backwards)
             if (ct < 2 * XK) {
               const int k = ((ct >= XK) ? nk - 1 - c : c) * XK + (ct & (XK - 1));
-              mst[ct] = k < N ? -zsig[k] : 0.0;
+              mst[ct] = k < N ? (qform ? zsig[k] : -zsig[k]) : 0.0;
             }
             asm volatile("bar.sync 2, 96;\n" ::: "memory");
           }
+          if (qform) {
 #pragma unroll 4
-          for (int e = ct; e < (int)QH; e += 96) {  // 2 * QH doubles = QH double2
-            double2 v = a2[e];
-            double2 z = b2[e];
-            if (zsig) {  // Ab is HW: z = HW - sigma_k W (the directions pass's FMA)
-              const double ms = mst[((2 * e) / (int)QH) * XK + ((e & 127) >> 3)];
-              z.x = fma(ms, v.x, z.x);
-              z.y = fma(ms, v.y, z.y);
+            for (int e = ct; e < (int)QH; e += 96) {
+              double2 v = a2[e];
+              const double2 z = b2[e];
+              const double q = mst[((2 * e) / (int)QH) * XK + ((e & 127) >> 3)];
+              v.x = fma(q, v.x, z.x);
+              v.y = fma(q, v.y, z.y);
+              a2[e] = v;
             }
-            v.x += sa * z.x;
-            v.y += sa * z.y;
-            a2[e] = v;
+          } else {
+#pragma unroll 4
+            for (int e = ct; e < (int)QH; e += 96) {  // 2 * QH doubles = QH double2
+              double2 v = a2[e];
+              double2 z = b2[e];
+              if (zsig) {  // Ab is HW: z = HW - sigma_k W (the directions pass's FMA)
+                const double ms = mst[((2 * e) / (int)QH) * XK + ((e & 127) >> 3)];
+                z.x = fma(ms, v.x, z.x);
+                z.y = fma(ms, v.y, z.y);
+              }
+              v.x += sa * z.x;
+              v.y += sa * z.y;
+              a2[e] = v;
+            }
           }
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           asm volatile("bar.sync 2, 96;\n" ::: "memory");
@@ -2873,13 +2898,23 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
   }
 }
 
+// Mt = (padded) M^T. With zq != null (the implicit-z trial rotation of
+// mix_tri_kernel): W - tau z = sa (HW_k + q_k W_k) with sa = -tau and
+// q_k = (1 - sa sigma_k) / sa, so M^T is scaled by sa here and q_k goes to zq —
+// the combine is then ONE FMA per element, fma(q_k, W, HW) (it was z = fma(-sigma, W,
+// HW), then W + sa z: the combining warps' DFMAs queue behind the consumers'
+// DMMAs on the FP64 pipe, so their count is what the consumers wait for).
 __global__ void transpose_pad_kernel(int N, int np, const double* __restrict__ M,
-                                     double* __restrict__ Mt) {
+                                     double* __restrict__ Mt, double sa = 1.0,
+                                     const double* __restrict__ zsig = nullptr,
+                                     double* __restrict__ zq = nullptr) {
   PO_PDL_ENTRY();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)np * np) return;
   const int i = (int)(e / np), k = (int)(e % np);
-  Mt[e] = (i < N && k < N) ? M[(int64_t)k * N + i] : 0.0;
+  const double v = (i < N && k < N) ? M[(int64_t)k * N + i] : 0.0;
+  Mt[e] = zq ? sa * v : v;
+  if (zq && i == 0) zq[k] = k < N ? (1.0 - sa * zsig[k]) / sa : 0.0;
 }
 
 }  // namespace
@@ -2919,7 +2954,7 @@ int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double
   } while (0)
   if (off || !tma2d_available()) PO_MB_FAIL("disabled / no TMA");
   const int np = (N + 15) & ~15;
-  double* mt = mix_big_scratch(s, (size_t)np * np);
+  double* mt = mix_big_scratch(s, (size_t)np * np + np);
   if (!mt) PO_MB_FAIL("scratch");
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
@@ -2942,7 +2977,11 @@ int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double
 #undef PO_MB_FAIL
   const size_t smem = fixed + ((size_t)nst * sdoubles + resd) * 8;
   ::po::count_launch();
-  launch_pdl(transpose_pad_kernel, dim3((unsigned)(((int64_t)np * np + 255) / 256)), dim3(256), 0, s, N, np, M, mt);
+  // implicit-z triangular rotation: one-FMA combine against a scaled M^T (q_k after the matrix)
+  const bool qform = tri && Ab && zsig && sa != 0.0;
+  double* zq = mt + (size_t)np * np;
+  launch_pdl(transpose_pad_kernel, dim3((unsigned)(((int64_t)np * np + 255) / 256)), dim3(256), 0, s, N, np, M, mt,
+             qform ? sa : 1.0, qform ? zsig : (const double*)nullptr, qform ? zq : (double*)nullptr);
   const int n_pt = mix_big_nblk(ngl);
   const int n_it = (N + XI - 1) / XI;
   const int ntiles = n_pt * n_it;
@@ -2951,7 +2990,8 @@ int launch_mix_big(int N, int64_t ld, int64_t ngl, const double* A, const double
     set_smem(reinterpret_cast<const void*>(mix_tri_kernel), (int)smem);
     ::po::count_launch();
     launch_pdl(mix_tri_kernel, dim3(grid), dim3(XTH), smem, s, maps, Ab ? 1 : 0, N, ld, ngl, n_pt, n_it,
-               nst, sa, alpha, out, guard, Ab ? zsig : (const double*)nullptr, mres ? 1 : 0);
+               nst, sa, alpha, out, guard, qform ? (const double*)zq : (Ab ? zsig : (const double*)nullptr),
+               mres ? 1 : 0, qform ? 1 : 0);
     return n_pt;
   }
   set_smem(reinterpret_cast<const void*>(mix_big_kernel), (int)smem);
@@ -2980,7 +3020,7 @@ int launch_directions_big(int N, int64_t ld, int64_t ngl, const double* W, const
   const size_t smem = 2048 + ((size_t)DNA * XP * XK + (size_t)DNE * 3 * QE) * 8;
   ::po::count_launch();
   launch_pdl(transpose_pad_kernel, dim3((unsigned)(((int64_t)np * np + 255) / 256)), dim3(256), 0, s, N,
-             np, Sigma, mt);
+             np, Sigma, mt, 1.0, (const double*)nullptr, (double*)nullptr);
   const int n_pt = mix_big_nblk(ngl);
   const int n_it = (N + XI - 1) / XI;
   const int ntiles = n_pt * n_it;

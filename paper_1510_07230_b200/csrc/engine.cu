@@ -1004,6 +1004,11 @@ extern "C" int po_enqueue(po_engine* h, int op, int a, int b, int out) {
       E.reduce_rows(E.partials + (size_t)E.N * gb.nsplit, 3 * E.N, gb.nsplit, E.g.w, E.dvec + E.off_ss(), true);
       break;
     }
+    case PO_OP_GRAM_DENSITY:
+      // the trial's verification Gram that also writes rho and 4 pi rho (64 < N <= 128)
+      if (!E.gram_density(E.blk(a), E.dmat[0], st->rho, E.density_b_target(1)))
+        throw Error(PO_EINVAL, "Gram with fused density unavailable for this N");
+      break;
     case PO_OP_ROTATION_IMPLICIT:
       // the large-N trial rotation: b is HW, z = HW - sigma W rebuilt per element
       if (po::launch_mix(E.g, E.N, E.blk(a), E.blk(b), -0.3, E.dmat[1], 1.0, nullptr, 0.0, 1,

@@ -169,7 +169,7 @@ _SIGS = {
 }
 
 OPS = dict(hamiltonian=0, gram_sym=1, gram=2, mix=3, mix_upper=4, density_xc=5, poisson=6, cholesky=7,
-           laplacian=8, gram_trial=9, rotation=10, directions=11, rotation_fused=12, rotation_implicit=13, gram_sigma_bb=14)
+           laplacian=8, gram_trial=9, rotation=10, directions=11, rotation_fused=12, rotation_implicit=13, gram_sigma_bb=14, gram_density=15)
 
 EXPORTED_SYMBOLS = tuple(_SIGS)
 

@@ -51,6 +51,7 @@ res["hamiltonian"] = timeit(e, lambda: e.enqueue("hamiltonian", a=w, out=out))
 res["gram_sym(G2)"] = timeit(e, lambda: e.enqueue("gram_sym", a=w))
 res["gram_trial(G0)"] = timeit(e, lambda: e.enqueue("gram_trial", a=w, b=z))
 res["gram_nonsym(Sigma)"] = timeit(e, lambda: e.enqueue("gram", a=hw, b=w))
+res["gram_sym+density"] = timeit(e, lambda: e.enqueue("gram_density", a=w))
 res["gram_sigma+bb"] = timeit(e, lambda: e.enqueue("gram_sigma_bb", a=hw, b=w))
 e.enqueue("gram_sym", a=w)
 e.enqueue("cholesky")
@@ -71,12 +72,12 @@ _fp = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
 fp64 = _fp.get("dmma_issue_tflops") or _fp["fp64_tflops"]  # the measured DMMA issue rate
 ng = spec.num_points
 tri, full = N * (N + 1) * ng, 2 * N * N * ng
-flops = {"gram_sym(G2)": tri, "gram_trial(G0)": tri, "gram_nonsym(Sigma)": full, "gram_sigma+bb": full,
+flops = {"gram_sym(G2)": tri, "gram_trial(G0)": tri, "gram_nonsym(Sigma)": full, "gram_sigma+bb": full, "gram_sym+density": tri,
          "rotation": tri,
          "mix_upper": tri, "mix_full": full, "rotation_fused": 2 * tri, "rotation_implicit": tri,
          "directions": full}
 bytes_ = {"hamiltonian": 2 * blk, "gram_sym(G2)": blk, "gram_trial(G0)": 2 * blk,
-          "gram_nonsym(Sigma)": 2 * blk, "gram_sigma+bb": 4 * blk, "rotation": 3 * blk, "rotation_fused": 3 * blk, "directions": 4 * blk,
+          "gram_nonsym(Sigma)": 2 * blk, "gram_sigma+bb": 4 * blk, "gram_sym+density": blk, "rotation": 3 * blk, "rotation_fused": 3 * blk, "directions": 4 * blk,
           "rotation_implicit": 3 * blk,
           "density_xc": blk, "mix_upper": 2 * blk, "mix_full": 2 * blk}
 for k, v in res.items():
