@@ -2734,7 +2734,7 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 8);
-      mbar_init(&ready[s], 1);
+      mbar_init(&ready[s], 3);  // one arrival per combining warp
     }
     mbar_init(mbar_res, 1);
     fence_mbar_init();
@@ -2796,7 +2796,7 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
           mbar_wait(&full[s], (uint32_t)(g / nst) & 1u);
           double2* a2 = reinterpret_cast<double2*>(stage0 + (size_t)s * sdoubles);
           const double2* b2 = reinterpret_cast<const double2*>(stage0 + (size_t)s * sdoubles + 2 * QH);
-          if (zsig) {  // -sigma of the stage's 2 x 16 orbitals (half 1 walks k backwards)
+          if (zsig && !qform) {  // -sigma of the stage's 2 x 16 orbitals (half 1 walks k backwards)
             if (ct < 2 * XK) {
               const int k = ((ct >= XK) ? nk - 1 - c : c) * XK + (ct & (XK - 1));
               mst[ct] = k < N ? (qform ? zsig[k] : -zsig[k]) : 0.0;
@@ -2808,7 +2808,9 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
             for (int e = ct; e < (int)QH; e += 96) {
               double2 v = a2[e];
               const double2 z = b2[e];
-              const double q = mst[((2 * e) / (int)QH) * XK + ((e & 127) >> 3)];
+              // q_k straight from the 1-KB vector (L1): no staging, no CTA-level barrier
+              const int k = (((2 * e) / (int)QH) ? nk - 1 - c : c) * XK + ((e & 127) >> 3);
+              const double q = __ldg(zsig + k);
               v.x = fma(q, v.x, z.x);
               v.y = fma(q, v.y, z.y);
               a2[e] = v;
@@ -2829,8 +2831,8 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
             }
           }
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          asm volatile("bar.sync 2, 96;\n" ::: "memory");
-          if (ct == 0) mbar_arrive(&ready[s]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ready[s]);
         }
       }
     }
