@@ -442,10 +442,12 @@ bool Engine::gram_density(const double* A, double* Gdev, double* rho, double* bv
 }
 
 bool Engine::gram_sigma_bb(const double* hw, const double* w, double* Gdev, GramBB* bb) {
-  if (size > 1 || N <= 64 || N > 128 || !tma2d_available()) return false;
-  return launch_gram_big(N, g.ld, 0, hw, nullptr, 0.0, w, nullptr, 0.0, gram_ws,
-                         gram_workspace_doubles(g, N), Gdev, g.w, s, nullptr, nullptr, nullptr, 1.0, 0,
-                         bb);
+  if (N <= 64 || N > 128 || !tma2d_available()) return false;
+  if (!launch_gram_big(N, g.ld, 0, hw, nullptr, 0.0, w, nullptr, 0.0, gram_ws,
+                       gram_workspace_doubles(g, N), Gdev, g.w, s, nullptr, nullptr, nullptr, 1.0, 0, bb))
+    return false;
+  if (size > 1) comm->allreduce_sum(Gdev, (size_t)N * N, s);  // (the sums' partials: reduce_rows)
+  return true;
 }
 
 void Engine::mix(const double* A, const double* Ab, double sa, const double* M, double alpha,

@@ -488,8 +488,11 @@ void Solver::enqueue_phase1(int iter) {
     static const bool zfree_env = !std::getenv("PO_ZFREE") || std::atoi(std::getenv("PO_ZFREE")) != 0;
     const bool fused_dir = !full_grad && !(mean_abs && need_full) && n <= 48 && tma2d_available();
     // N > 64: dir_big_kernel (z implicit or stored, z_prev implicit or stored)
-    const bool big_dir = !fused_dir && !full_grad && need_full && !mean_abs && E.size == 1 && n > 64 &&
-                         tma2d_available();
+    // (every rank runs it on its slab: the partial sums and the Grams are all-reduced)
+    static const bool big_dir_sharded =
+        !std::getenv("PO_BIG_DIR_SHARDED") || std::atoi(std::getenv("PO_BIG_DIR_SHARDED")) != 0;
+    const bool big_dir = !fused_dir && !full_grad && need_full && !mean_abs &&
+                         (E.size == 1 || big_dir_sharded) && n > 64 && tma2d_available();
     // implicit z: only where every consumer is the fused rotation of a trial
     // whose Gram comes from the iteration's Grams (nonlinear, orthonormalised
     // every iteration); the rare other consumers materialise it
