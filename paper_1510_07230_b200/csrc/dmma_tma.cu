@@ -1861,15 +1861,9 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
       return;  // (never: a BB launch has no symmetric tiles)
     } else if constexpr (GT_T == 128) {
       // Diagonal tile of a symmetric Gram, T = 128 (16 fragment rows): warps 0-3
-      // take the first 16-point half of every stage, warps 4-7 the second, and
-      // warp a of either half owns fragment rows {a, 7-a, 8+a, 15-a} of the
-      // upper triangle (c >= r): 34 blocks per warp, balanced. Walking the
-      // columns c = a .. 15, one shared load gives the B fragment of column c for
-      // every owned row r <= c (1 to 4 of them, warp-uniform counts) and, when c
-      // is itself an owned row, that row's A fragment — 16 - a loads per 68
-      // DMMAs where the circulant scheme below needed one load per 2 DMMAs
-      // (shared-memory bound at 68% of FP64 on C3). The two halves' partial
-      // blocks meet in the epilogue.
+      // take the first 16-point half of every stage, warps 4-7 the second; warp a
+      // of either half owns the circulant super-block slots described at
+      // sym_diag_stages. The two halves' partial blocks meet in the epilogue.
       const int hf = warp >> 2, a = warp & 3;
       double acc0[5][2][2][2], acc1[4][2][2][2];
 #pragma unroll
