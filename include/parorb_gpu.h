@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define PO_ABI_VERSION 2  /* 2: po_result gained checkpoints / drift_iterations; po_stiefel_gradient_d */
+#define PO_ABI_VERSION 3  /* 2: po_result gained checkpoints / drift_iterations; po_stiefel_gradient_d; 3: po_direction_sums */
 
 enum po_status {
   PO_OK = 0,
@@ -185,6 +185,18 @@ int po_linear_combination(po_engine* e, int a, double s, int b, int out);
 /* optimizer.cpp:376-397 per-orbital BB products (weighted). */
 int po_bb_products(po_engine* e, int w, int w_prev, int z, int z_prev, double* ss,
                    double* sy, double* yy);
+
+/* The direction step of one iteration as the solver runs it (optimizer.cpp:265-320 with
+ * manifold.cpp:204-216, and the BB products of optimizer.cpp:386-397), the direction
+ * z_i = HU_i - sigma_ii U_i never stored: sigma_ii = <hu_i, u_i>, ||z_i||^2 and — with a
+ * history (u_prev, hu_prev >= 0, sigma_prev the previous iterate's sigma_ii) — <s_i, s_i>,
+ * <s_i, y_i>, <y_i, y_i> for s = u - u_prev, y = z - z_prev, z_prev = hu_prev - sigma_prev u_prev.
+ * sigma_full (row-major N x N, may be null) receives <(HU)^T U> (manifold.cpp:183). For
+ * 64 < N <= 128 all of it is ONE pass (the Sigma Gram carries the sums); other N take the Gram
+ * and a streaming pass. Host outputs of length N; any may be null. */
+int po_direction_sums(po_engine* e, int u, int hu, int u_prev, int hu_prev, const double* sigma_prev,
+                      double* sigma_diag, double* sigma_full, double* zz, double* ss, double* sy,
+                      double* yy);
 
 /* -------------------------------------------------------------- solver */
 

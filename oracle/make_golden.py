@@ -198,13 +198,20 @@ def gen_ops_reduced(name, spec, threads=8):
         json.dump({"spec": json.loads(spec.to_json()), "sketch": SKETCH, **meta}, f, indent=1)
 
 
-def gen_prefix(name, spec, iters, threads=8):
+def gen_prefix(name, spec, iters, threads=8, extend=False):
     """Truncated re-runs (max_inner = 1..iters) of the unmodified reference: the
     k-th run's final W is the reference's iterate after k iterations (finalize,
-    optimizer.cpp:581-597, does not change W)."""
+    optimizer.cpp:581-597, does not change W). extend: keep the committed runs
+    k = 1..K0 of prefix_<name>.npz and only add k = K0 + 1..iters (the reference
+    is deterministic; C3 costs ~4 min per iteration on 8 cores)."""
     n = spec.n_orbitals
     eigs, sketches, grams, last = [], [], [], None
-    for k in range(1, iters + 1):
+    k0 = 1
+    if extend:
+        old = np.load(os.path.join(GOLDEN, f"prefix_{name}.npz"))
+        eigs, sketches, grams = list(old["eig"]), list(old["sketch"]), list(old["gram"])
+        k0 = len(eigs) + 1
+    for k in range(k0, iters + 1):
         d_spec = spec.trace_ref_spec(threads=threads)
         d_spec["params"]["max_inner"] = k
         d_spec["sketch"] = SKETCH
@@ -265,6 +272,8 @@ def main_big(which):
         gen_ops_reduced("C3", configs.config3())
     if "C3p" in which:
         gen_prefix("C3", configs.config3(), 3)
+    if "C3p5" in which:  # two more iterations on top of the committed three
+        gen_prefix("C3", configs.config3(), 5, threads=int(os.environ.get("GOLDEN_THREADS", "8")), extend=True)
     if "C4ops" in which:
         gen_ops_reduced("C4g64", c4_grid_spec(64))
 
@@ -297,7 +306,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true", help="skip the C1/C2 trajectories")
     ap.add_argument("--from-dir", default="/tmp/golden_runs", help="reuse finished C1/C2 trace_ref runs")
-    ap.add_argument("--big", default="", help="comma list of C1eig,C2eig,C2p,C3ops,C3p,C4ops (long runs)")
+    ap.add_argument("--big", default="", help="comma list of C1eig,C2eig,C2p,C3ops,C3p,C3p5,C4ops (long runs)")
     args = ap.parse_args()
     if args.big:
         return main_big(args.big.split(","))

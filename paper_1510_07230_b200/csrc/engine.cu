@@ -862,6 +862,47 @@ int po_bb_products(po_engine* h, int w, int wp, int z, int zp, double* ss, doubl
   API_CATCH(h)
 }
 
+int po_direction_sums(po_engine* h, int u, int hu, int u_prev, int hu_prev, const double* sigma_prev,
+                      double* sigma_diag, double* sigma_full, double* zz, double* ss, double* sy,
+                      double* yy) {
+  ENGINE_OR_EINVAL(h);
+  API_TRY
+  const bool hist = u_prev >= 0 && hu_prev >= 0;
+  if (hist && !sigma_prev) throw Error(PO_EINVAL, "direction_sums: a history needs sigma_prev");
+  const int onb = po::per_orbital_nblk(E.g, E.N);
+  // sigma_ii = <hu_i, u_i> (the s*y product of the BB kernel with zero "previous" blocks)
+  po::launch_bb(E.g, E.N, E.blk(hu), nullptr, E.blk(u), nullptr, E.partials, E.s);
+  E.reduce_rows(E.partials + (size_t)E.N * onb, E.N, onb, E.g.w, E.dvec + E.off_sig(), true);
+  double* sp = E.dvec + E.off_zsig(0);
+  if (hist) {
+    std::memcpy(E.hmat, sigma_prev, sizeof(double) * E.N);
+    PO_CUDA(cudaMemcpyAsync(sp, E.hmat, sizeof(double) * E.N, cudaMemcpyHostToDevice, E.s));
+  }
+  po::GramBB gb{E.dvec + E.off_sig(), hist ? sp : nullptr, hist ? E.blk(u_prev) : nullptr,
+                hist ? E.blk(hu_prev) : nullptr, E.partials, 0};
+  int nb;
+  if (E.gram_sigma_bb(E.blk(hu), E.blk(u), E.dmat[4], &gb)) {
+    nb = gb.nsplit;
+  } else {
+    E.gram(E.blk(hu), nullptr, 0.0, E.blk(u), nullptr, 0.0, 0, E.dmat[4]);
+    nb = po::launch_residual_bb_stream(E.g, E.N, E.blk(u), E.blk(hu), E.dvec + E.off_sig(),
+                                       hist ? E.blk(u_prev) : nullptr, hist ? E.blk(hu_prev) : nullptr,
+                                       hist ? sp : nullptr, nullptr, E.partials, E.s);
+  }
+  E.reduce_rows(E.partials, E.N, nb, E.g.w, E.dvec + E.off_zz(), true);
+  if (hist) E.reduce_rows(E.partials + (size_t)E.N * nb, 3 * E.N, nb, E.g.w, E.dvec + E.off_ss(), true);
+  E.fetch_all();
+  if (sigma_full) fetch_matrix(E, E.dmat[4], sigma_full);
+  if (sigma_diag) std::memcpy(sigma_diag, E.hvec + E.off_sig(), sizeof(double) * E.N);
+  if (zz) std::memcpy(zz, E.hvec + E.off_zz(), sizeof(double) * E.N);
+  if (hist) {
+    if (ss) std::memcpy(ss, E.hvec + E.off_ss(), sizeof(double) * E.N);
+    if (sy) std::memcpy(sy, E.hvec + E.off_sy(), sizeof(double) * E.N);
+    if (yy) std::memcpy(yy, E.hvec + E.off_yy(), sizeof(double) * E.N);
+  }
+  API_CATCH(h)
+}
+
 int po_diagonal_residuals(po_engine* h, int u, int hu, int z, double* sigma, double* znorm2) {
   ENGINE_OR_EINVAL(h);
   API_TRY

@@ -143,6 +143,8 @@ _SIGS = {
     "po_stiefel_gradient_d": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
     "po_subspace_rotate": ([C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "po_linear_combination": ([C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int], C.c_int),
+    "po_direction_sums": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "po_bb_products": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                         C.c_void_p], C.c_int),
     "po_default_params": ([C.POINTER(Params)], None),
@@ -370,6 +372,20 @@ class Engine:
         ss, sy, yy = np.empty(self.N), np.empty(self.N), np.empty(self.N)
         self._chk(self._lib.po_bb_products(self.h, w, wp, z, zp, _dp(ss), _dp(sy), _dp(yy)))
         return ss, sy, yy
+
+    def direction_sums(self, u: int, hu: int, u_prev: int = -1, hu_prev: int = -1, sigma_prev=None):
+        """po_direction_sums: sigma_ii, Sigma, ||z_i||^2 and (with a history) the BB products of
+        the implicit directions z = HU - sigma U (optimizer.cpp:265-320, 386-397)."""
+        n = self.N
+        sd, sf = np.empty(n), np.empty((n, n))
+        zz, ss, sy, yy = np.empty(n), np.empty(n), np.empty(n), np.empty(n)
+        spv = None if sigma_prev is None else _dp(np.ascontiguousarray(sigma_prev, dtype=np.float64))
+        self._chk(self._lib.po_direction_sums(self.h, u, hu, u_prev, hu_prev, spv, _dp(sd), _dp(sf),
+                                              _dp(zz), _dp(ss), _dp(sy), _dp(yy)))
+        out = dict(sigma_diag=sd, sigma=sf, zz=zz)
+        if u_prev >= 0:
+            out.update(ss=ss, sy=sy, yy=yy)
+        return out
 
     # ---- measurement helpers (pure launches on self.stream, no sync)
     def enqueue(self, op: str, a: int = -1, b: int = -1, out: int = -1):

@@ -42,7 +42,7 @@ def test_default_params_match_reference(native):
 
 def test_abi_version_and_sizing(native):
     L = native.lib()
-    assert L.po_abi_version() == 2
+    assert L.po_abi_version() == 3
     g = native.GridDesc((C.c_int64 * 3)(192, 192, 192), (C.c_double * 3)(60.0, 60.0, 60.0))
     one = L.po_solver_bytes(C.byref(g), 512, 1)
     eight = L.po_solver_bytes(C.byref(g), 512, 8)

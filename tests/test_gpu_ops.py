@@ -354,3 +354,40 @@ def test_gram_fused_trial(native, n_orb):
     assert np.array_equal(g, g.T)
     assert rel(g, wq * t @ t.T) < 1e-12
     e.close()
+
+
+@pytest.mark.parametrize("n_orb,hist", [(128, True), (128, False), (80, True), (33, True), (130, True)])
+def test_direction_sums(native, n_orb, hist):
+    """po_direction_sums — the iteration's direction step with z implicit
+    (optimizer.cpp:265-320, 386-397; manifold.cpp:183, 204-216): sigma_ii,
+    Sigma = <(HU)^T U>, ||z_i||^2 and the BB products against (u_prev, z_prev =
+    hu_prev - sigma_prev u_prev), vs the same formulas in numpy fp64. N = 128 / 80
+    take the one-pass form (the Sigma Gram's DMMA warps carry the sums), N = 33 /
+    130 the Gram + the streaming pass. Sums of ~2700 terms in another order:
+    1e-12 relative."""
+    spec = configs.small_molecule(14, n_orb, L=8.0)
+    rng = np.random.default_rng(5)
+    wq = float(np.prod(spec.spacing))
+    u = rng.standard_normal((n_orb, spec.num_points))
+    hu = 0.7 * u + 0.3 * rng.standard_normal(u.shape)
+    up = u + 0.05 * rng.standard_normal(u.shape)
+    hup = hu + 0.05 * rng.standard_normal(u.shape)
+    e = native.engine_for(spec)
+    bu, bhu = e.block_from(u), e.block_from(hu)
+    sig = wq * np.einsum("ip,ip->i", hu, u)
+    z = hu - sig[:, None] * u
+    want = dict(sigma_diag=sig, sigma=wq * hu @ u.T, zz=wq * np.einsum("ip,ip->i", z, z))
+    if hist:
+        bup, bhup = e.block_from(up), e.block_from(hup)
+        sigp = wq * np.einsum("ip,ip->i", hup, up)
+        zp = hup - sigp[:, None] * up
+        s, y = u - up, z - zp
+        want.update(ss=wq * np.einsum("ip,ip->i", s, s), sy=wq * np.einsum("ip,ip->i", s, y),
+                    yy=wq * np.einsum("ip,ip->i", y, y))
+        got = e.direction_sums(bu, bhu, bup, bhup, sigp)
+    else:
+        got = e.direction_sums(bu, bhu)
+    assert set(got) == set(want)
+    for k, v in want.items():
+        assert rel(got[k], v) < 1e-12, k
+    e.close()
