@@ -130,6 +130,36 @@ def test_sharded_solver_large_n(port, native, n_orb, size):
     assert projector_distance(ref["w"], w, np.prod(spec.spacing)) < 1e-6
 
 
+@pytest.mark.parametrize("size", [2, 4, 8])
+def test_c3_slabs_prefix(native, size):
+    """BASELINE configs[2] at its full shape (128^3, N = 128) on 2 / 4 / 8 slabs —
+    the multi-GPU runs of the config, here as in-process ranks on one GPU:
+    Rng(42) start drawn per rank slab, sharded Orth, three outer iterations.
+    Every rank's energies, backtracks and gradient norms match the unmodified
+    reference's prefix (tests/golden/prefix_C3.json, single domain)."""
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "prefix_C3.json")))
+    spec = configs.config3()
+    k = 3
+
+    def body(e, r):
+        w = native.random_orthonormal(e, spec.start_seed)
+        got = e.solve(w, algorithm="opt_par_mod", **{**spec.optimizer_params(), "max_inner": k})
+        return got
+
+    res = run_ranks(native, spec, size, body)
+    for got in res:
+        assert len(got.records) == k
+        for a, b in zip(got.records, gold["records"][:k]):
+            assert a["backtracks"] == b["backtracks"]
+            assert abs(a["energy"] - float(b["energy"])) < 1e-6, (a, b)
+            gref = float(b["grad_norm"])
+            assert abs(a["grad_norm"] - gref) <= 1e-8 * max(1.0, gref)
+    for got in res[1:]:  # replicated decisions: bitwise the same on every rank
+        assert got.records[-1]["energy"] == res[0].records[-1]["energy"]
+
+
 def test_c4_slab_geometry(native):
     """The C4 grid (192^3, L = 60, the C4 nuclei) cut into 3 slabs of 64 planes
     (the 8-GPU C4 run has 24) with N = 8 orbitals: sharded operators and two
