@@ -93,6 +93,7 @@ Engine::Engine(const po_grid_desc* grid, int n, double occupation, const po_dist
   if (hamiltonian_split_ok(g)) upd((size_t)3 * N * hamiltonian_split_nblk(g));
   upd((size_t)5 * N * mix_nblk_max(g));  // fused directions: 5 partial rows
   upd((size_t)4 * N * per_orbital_nblk(g, N));  // residual + BB rows
+  upd((size_t)4 * N * 512);  // the same rows from the Sigma Gram's splits (at most one wave of CTAs)
   upd((size_t)2 * points_nblk(g));
   partials_cap = pc;
   PO_CUDA(cudaMalloc(&partials, pc * sizeof(double)));

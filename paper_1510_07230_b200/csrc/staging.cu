@@ -11,6 +11,7 @@
 // memcpy overlap. The block layout on the device is pitched (ld), on the host
 // dense (ngl): pieces never cross an orbital row.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -84,6 +85,8 @@ void Engine::free_staging() {
 }
 
 int Engine::host_threads() const {
+  static const int forced = std::getenv("PO_HOST_THREADS") ? std::atoi(std::getenv("PO_HOST_THREADS")) : 0;
+  if (forced > 0) return forced;
   const unsigned hc = std::thread::hardware_concurrency();
   return (int)std::max(1u, std::min(8u, hc ? hc / 2 : 1u));
 }
