@@ -272,8 +272,10 @@ def main_big(which):
         gen_ops_reduced("C3", configs.config3())
     if "C3p" in which:
         gen_prefix("C3", configs.config3(), 3)
-    if "C3p5" in which:  # two more iterations on top of the committed three
-        gen_prefix("C3", configs.config3(), 5, threads=int(os.environ.get("GOLDEN_THREADS", "8")), extend=True)
+    for w in which:  # C3p<K>, K > 3: more iterations on top of the committed ones
+        if w.startswith("C3p") and w[3:].isdigit():
+            gen_prefix("C3", configs.config3(), int(w[3:]), threads=int(os.environ.get("GOLDEN_THREADS", "8")),
+                       extend=True)
     if "C4ops" in which:
         gen_ops_reduced("C4g64", c4_grid_spec(64))
 
@@ -306,7 +308,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true", help="skip the C1/C2 trajectories")
     ap.add_argument("--from-dir", default="/tmp/golden_runs", help="reuse finished C1/C2 trace_ref runs")
-    ap.add_argument("--big", default="", help="comma list of C1eig,C2eig,C2p,C3ops,C3p,C3p5,C4ops (long runs)")
+    ap.add_argument("--big", default="", help="comma list of C1eig,C2eig,C2p,C3ops,C3p,C3p<K>,C4ops (long runs; C3p<K> extends the committed C3 prefix to K iterations)")
     args = ap.parse_args()
     if args.big:
         return main_big(args.big.split(","))
