@@ -192,7 +192,7 @@ int po_bb_products(po_engine* e, int w, int w_prev, int z, int z_prev, double* s
  * history (u_prev, hu_prev >= 0, sigma_prev the previous iterate's sigma_ii) — <s_i, s_i>,
  * <s_i, y_i>, <y_i, y_i> for s = u - u_prev, y = z - z_prev, z_prev = hu_prev - sigma_prev u_prev.
  * sigma_full (row-major N x N, may be null) receives <(HU)^T U> (manifold.cpp:183). For
- * 64 < N <= 128 all of it is ONE pass (the Sigma Gram carries the sums); other N take the Gram
+ * N > 64 all of it is ONE pass (the Sigma Gram carries the sums); smaller N take the Gram
  * and a streaming pass. Host outputs of length N; any may be null. */
 int po_direction_sums(po_engine* e, int u, int hu, int u_prev, int hu_prev, const double* sigma_prev,
                       double* sigma_diag, double* sigma_full, double* zz, double* ss, double* sy,
@@ -301,7 +301,7 @@ enum {
   PO_OP_ROTATION_FUSED = 12, /* rotation + verification Gram + density/xc (default state) */
   PO_OP_ROTATION_IMPLICIT = 13, /* out = (a - 0.3 z) M with z = b - sigma a implicit (b = HW; N > 64) */
   PO_OP_GRAM_DENSITY = 15, /* G = <a^T a> + rho, 4 pi rho of block a in the same pass (64 < N <= 128) */
-  PO_OP_GRAM_SIGMA_BB = 14, /* G = <a^T b> (a = HW, b = W) + the directions' ||z||^2 / BB sums (64 < N <= 128) */
+  PO_OP_GRAM_SIGMA_BB = 14, /* G = <a^T b> (a = HW, b = W) + the directions' ||z||^2 / BB sums (N > 64) */
   PO_OP_HAMILTONIAN_VARIANT = 100  /* + v: H a design-space variants (measurement builds only:
                                       make VARIANTS=1; else PO_EINVAL) */
 };

@@ -1646,8 +1646,9 @@ __device__ __forceinline__ void sym_diag_stages(double (&acc0)[5][2][2][2], doub
 }
 
 // BB: the elementwise half of compute_directions rides on the Sigma Gram
-// (N <= 128, one non-symmetric tile: area 0 holds HW, area qb holds W — every
-// orbital of both blocks passes through shared memory anyway). Each lane pair of
+// (N > 64, non-symmetric 128-tiles: area 0 holds HW rows of tile tm, area qb W
+// rows of tile tn — on the tiles with tm == tn every orbital of both blocks
+// passes through shared memory anyway; for N <= 128 that is the only tile). Each lane pair of
 // the eight consumer warps owns one orbital and, per stage, reads its 16 points
 // of HW, W and — from two extra ring areas — W_prev and HW_prev
 // (or a stored Z_prev): z = fma(-sigma_i, W, HW) (the FMA of every z path),
@@ -1688,11 +1689,16 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
   uint64_t* empty = full + 8;
   double* stage0 = reinterpret_cast<double*>(tsm + 1024);
   constexpr size_t QS = (size_t)GT_T * BOX;  // doubles per source per stage
-  const int nbb = BB && bb.hist ? 2 : 0;     // extra ring areas: W_prev, X_prev
-  const size_t sdoubles = (size_t)(nsrc + nbb) * QS;
+  const int nbb_areas = BB && bb.hist ? 2 : 0;  // extra ring areas: W_prev, X_prev
+  const size_t sdoubles = (size_t)(nsrc + nbb_areas) * QS;
   int tm, tn;
   big_tile_index(blockIdx.x, mt, sym, tm, tn);
   const bool diag = !BB && sym && tm == tn;
+  // BB on N > 128: the tiles with tm == tn hold HW_i and W_i of the same 128
+  // orbitals — they carry the sums (and the two extra streams); the others are
+  // plain Sigma tiles with the same stage layout
+  const bool bbt = BB && tm == tn;
+  const int nbb = bbt ? nbb_areas : 0;
   // sources fetched per 16-point half: A (+Ab); B (+Bb) unless this is a symmetric diagonal tile
   const int nload = diag ? (qa_b >= 0 ? 2 : 1) : nsrc;
   using Cfg = BigCfg<GT_T>;
@@ -1736,8 +1742,8 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
             const int row0 = (q == qb || q == qb_b) ? tn * GT_T : tm * GT_T;
             tma_load_2d(sbuf + q * QS, &maps.m[q], x, row0, &full[s]);
           }
-          for (int q = nload; q < nload + nbb; ++q)  // BB: W_prev, X_prev of the same points
-            tma_load_2d(sbuf + q * QS, &maps.m[q], x, 0, &full[s]);
+          for (int q = nload; q < nload + nbb; ++q)  // BB: W_prev, X_prev of the same points / orbitals
+            tma_load_2d(sbuf + q * QS, &maps.m[q], x, tm * GT_T, &full[s]);
         }
       }
     }
@@ -1770,19 +1776,21 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
       // one 8-point half of its 16 points per stage (4 chunks of 16 bytes; a
       // quarter-warp's 4 rows x 2 halves hit 8 distinct chunks under the swizzle)
       const int bi = BB ? 16 * warp + (lane >> 1) : 0, bh = lane & 1;
+      const int gi = tm * GT_T + bi;  // the orbital (bi: its row in the tile)
       double bms = 0.0, bmsp = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
       if constexpr (BB) {
-        bms = bi < bb.N ? -bb.sig[bi] : 0.0;
-        bmsp = (bb.sigp && bi < bb.N) ? -bb.sigp[bi] : 0.0;
+        bms = (bbt && gi < bb.N) ? -bb.sig[gi] : 0.0;
+        bmsp = (bbt && bb.sigp && gi < bb.N) ? -bb.sigp[gi] : 0.0;
       }
       const bool bhist = BB && bb.hist != 0, bzpi = BB && bb.sigp != nullptr;
-      auto stages = [&](auto two) {
+      auto stages = [&](auto two, auto dobb) {
         constexpr bool TWO = decltype(two)::value;
+        constexpr bool DOBB = decltype(dobb)::value;  // this tile carries the sums (compile-time loop variant)
         for (int st = 0; st < nstage; ++st) {
           const int s = st % nst;
           mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
           const double* sbuf = stage0 + (size_t)s * sdoubles;
-          if constexpr (BB) {
+          if constexpr (DOBB) {
             // the stage's elementwise work in this warp's own instruction stream,
             // before its fragments are loaded (their registers are free): 64 DFMAs
             // against the stage's 128 DMMAs per warp. (As the job of separate warps
@@ -1838,22 +1846,24 @@ __global__ void __launch_bounds__(BigCfg<GT_T>::THREADS, 1) gram_big_kernel(cons
           }
         }
       };
-      if (qa_b >= 0 || qb_b >= 0)
-        stages(std::true_type{});
+      if (BB && bbt)
+        stages(std::false_type{}, std::integral_constant<bool, BB>{});
+      else if (qa_b >= 0 || qb_b >= 0)
+        stages(std::true_type{}, std::false_type{});
       else
-        stages(std::false_type{});
+        stages(std::false_type{}, std::false_type{});
       if constexpr (BB) {  // the two halves of an orbital's points meet; one partial per split
         r0 += __shfl_xor_sync(0xffffffffu, r0, 1);
         r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
         r2 += __shfl_xor_sync(0xffffffffu, r2, 1);
         r3 += __shfl_xor_sync(0xffffffffu, r3, 1);
-        if (bh == 0 && bi < bb.N) {
+        if (bbt && bh == 0 && gi < bb.N) {
           const int64_t nb = gridDim.y;
-          bb.part[((int64_t)0 * bb.N + bi) * nb + blockIdx.y] = r0;
+          bb.part[((int64_t)0 * bb.N + gi) * nb + blockIdx.y] = r0;
           if (bhist) {
-            bb.part[((int64_t)1 * bb.N + bi) * nb + blockIdx.y] = r1;
-            bb.part[((int64_t)2 * bb.N + bi) * nb + blockIdx.y] = r2;
-            bb.part[((int64_t)3 * bb.N + bi) * nb + blockIdx.y] = r3;
+            bb.part[((int64_t)1 * bb.N + gi) * nb + blockIdx.y] = r1;
+            bb.part[((int64_t)2 * bb.N + gi) * nb + blockIdx.y] = r2;
+            bb.part[((int64_t)3 * bb.N + gi) * nb + blockIdx.y] = r3;
           }
         }
       }
@@ -3047,7 +3057,7 @@ bool launch_gram_big(int N, int64_t ld, int sym, const double* A, const double* 
   const int GT_T = big_tile(N, sym, Ab != nullptr || !sym);
   // the fused elementwise pass: Sigma = <(HW)^T W> as one non-symmetric 128-tile
   static const bool bb_off = getenv("PO_NO_GRAM_BB") != nullptr;  // measurement switch
-  if (bbl && (bb_off || sym || Ab || Bb || GT_T != 128 || N > 128 || N <= 64 || rho)) return false;
+  if (bbl && (bb_off || sym || Ab || Bb || GT_T != 128 || N <= 64 || rho)) return false;
   // the fused density needs the whole orbital set in one diagonal tile
   if (rho && !(sym && !Ab && GT_T == 128 && N <= 128 && N > 64)) return false;
   Maps maps;

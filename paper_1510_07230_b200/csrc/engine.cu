@@ -443,7 +443,7 @@ bool Engine::gram_density(const double* A, double* Gdev, double* rho, double* bv
 }
 
 bool Engine::gram_sigma_bb(const double* hw, const double* w, double* Gdev, GramBB* bb) {
-  if (N <= 64 || N > 128 || !tma2d_available()) return false;
+  if (N <= 64 || !tma2d_available()) return false;
   if (!launch_gram_big(N, g.ld, 0, hw, nullptr, 0.0, w, nullptr, 0.0, gram_ws,
                        gram_workspace_doubles(g, N), Gdev, g.w, s, nullptr, nullptr, nullptr, 1.0, 0, bb))
     return false;
@@ -1040,7 +1040,7 @@ extern "C" int po_enqueue(po_engine* h, int op, int a, int b, int out) {
       break;
     case PO_OP_GRAM_SIGMA_BB: {
       // the iteration's Sigma Gram (a = HW, b = W) carrying ||z||^2 and the BB
-      // products (history: the same blocks, previous z implicit); 64 < N <= 128
+      // products (history: the same blocks, previous z implicit); N > 64
       po::GramBB gb{E.dvec + E.off_sig(), E.dvec + E.off_sig(), E.blk(b), E.blk(a), E.partials, 0};
       if (!E.gram_sigma_bb(E.blk(a), E.blk(b), E.dmat[0], &gb))
         throw Error(PO_EINVAL, "Sigma Gram with fused directions unavailable for this N");

@@ -127,7 +127,7 @@ class Engine {
   // false (nothing enqueued) where the fused form is unavailable
   bool gram_density(const double* A, double* Gdev, double* rho, double* bvec);
   // Sigma = w (HW)^T W with the elementwise half of compute_directions fused
-  // (64 < N <= 128; all-reduced over the ranks); false if unavailable (nothing launched)
+  // (N > 64; all-reduced over the ranks); false if unavailable (nothing launched)
   bool gram_sigma_bb(const double* hw, const double* w, double* Gdev, GramBB* bb);
   void mix(const double* A, const double* Ab, double sa, const double* M, double alpha,
            const double* C, double beta, int upper, double* out, double* norm_rows,

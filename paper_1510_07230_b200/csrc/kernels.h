@@ -153,7 +153,7 @@ size_t gram_big_workspace_doubles(int64_t ld, int N);
 // rho (nullable): with one source, sym and 64 < N <= 128 (one diagonal tile) the
 // Gram also writes the density occ sum_i A_i^2 (+ 4 pi rho into bvec) of the
 // ngl points; false (nothing launched) where that is unavailable
-// bbl (64 < N <= 128, A = HW, B = W, non-symmetric): the Gram also does the
+// bbl (N > 64, A = HW, B = W, non-symmetric): the Gram also does the
 // elementwise half of compute_directions (||z_i||^2 and, with wp / xp, the BB
 // products; z = HW - sig W implicit) — partials [4][N][nsplit]: zz, ss, sy, yy.
 struct GramBB {

@@ -537,7 +537,7 @@ void Solver::enqueue_phase1(int iter) {
     } else {
       static const bool dd_grams_env =
           !std::getenv("PO_DNORM_GRAMS") || std::atoi(std::getenv("PO_DNORM_GRAMS")) != 0;
-      // 64 < N <= 128 with z implicit and ||D||^2 from the Grams: the elementwise
+      // N > 64 with z implicit and ||D||^2 from the Grams: the elementwise
       // half of the directions (||z||^2, BB products) rides on the Sigma Gram,
       // with sigma_i from the H u pass (dvec sigma row) — no pass of its own
       int bb_nb = -1;

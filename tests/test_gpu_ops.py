@@ -356,15 +356,15 @@ def test_gram_fused_trial(native, n_orb):
     e.close()
 
 
-@pytest.mark.parametrize("n_orb,hist", [(128, True), (128, False), (80, True), (33, True), (130, True)])
+@pytest.mark.parametrize("n_orb,hist", [(128, True), (128, False), (80, True), (33, True), (130, True), (260, True)])
 def test_direction_sums(native, n_orb, hist):
     """po_direction_sums — the iteration's direction step with z implicit
     (optimizer.cpp:265-320, 386-397; manifold.cpp:183, 204-216): sigma_ii,
     Sigma = <(HU)^T U>, ||z_i||^2 and the BB products against (u_prev, z_prev =
-    hu_prev - sigma_prev u_prev), vs the same formulas in numpy fp64. N = 128 / 80
-    take the one-pass form (the Sigma Gram's DMMA warps carry the sums), N = 33 /
-    130 the Gram + the streaming pass. Sums of ~2700 terms in another order:
-    1e-12 relative."""
+    hu_prev - sigma_prev u_prev), vs the same formulas in numpy fp64. N > 64 takes
+    the one-pass form (the Sigma Gram's DMMA warps carry the sums; N = 130 / 260:
+    several 128-tiles, the sums on the diagonal ones), N = 33 the Gram + a
+    streaming pass. Sums of ~2700 terms in another order: 1e-12 relative."""
     spec = configs.small_molecule(14, n_orb, L=8.0)
     rng = np.random.default_rng(5)
     wq = float(np.prod(spec.spacing))
