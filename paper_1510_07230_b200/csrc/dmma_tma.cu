@@ -1012,18 +1012,42 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
       __syncwarp();  // every lane is done reading the chunk's source values
       double dsum = 0.0;
       const int jx = t4 >> 1;  // lanes t4 = 2, 3 store their pair swapped (rows mod 4 distinct)
+      // The loop is issue-bound (~800 instructions per stage and warp, most of them
+      // integer / control): every fragment below the last holds 8 real orbitals, so
+      // only the last one checks i < N; the row offsets are lane constants and the
+      // stores are predicated on one point test (same values, same summation order).
+      const bool pin = p < ngl;
+      double* const outp = out + (int64_t)(2 * t4) * ld + p;
+      double* const sp = sbuf + (2 * t4) * PW + c + gq;
+      const int64_t lda = jx ? ld : 0, ldb = jx ? 0 : ld;  // first / second stored row of the pair
+      const int pwa = jx ? PW : 0, pwb = jx ? 0 : PW;
 #pragma unroll
-      for (int fi = 0; fi < F; ++fi)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int i = 8 * fi + 2 * t4 + (j ^ jx);
-          if (i < N) {
-            const double v = jx ? acc[fi][j ^ 1] : acc[fi][j];
-            if (p < ngl) out[(int64_t)i * ld + p] = v;
-            sbuf[(i) * PW + c + gq] = v;
-            dsum += v * v;
+      for (int fi = 0; fi < F; ++fi) {
+        const double va = jx ? acc[fi][1] : acc[fi][0];  // element j ^ jx for j = 0, 1
+        const double vb = jx ? acc[fi][0] : acc[fi][1];
+        if (fi < F - 1) {
+          if (pin) {
+            outp[(int64_t)(8 * fi) * ld + lda] = va;
+            outp[(int64_t)(8 * fi) * ld + ldb] = vb;
+          }
+          sp[8 * fi * PW + pwa] = va;
+          sp[8 * fi * PW + pwb] = vb;
+          dsum += va * va;
+          dsum += vb * vb;
+        } else {
+          const int ia = 8 * fi + 2 * t4 + jx, ib = 8 * fi + 2 * t4 + (jx ^ 1);
+          if (ia < N) {
+            if (pin) outp[(int64_t)(8 * fi) * ld + lda] = va;
+            sp[8 * fi * PW + pwa] = va;
+            dsum += va * va;
+          }
+          if (ib < N) {
+            if (pin) outp[(int64_t)(8 * fi) * ld + ldb] = vb;
+            sp[8 * fi * PW + pwb] = vb;
+            dsum += vb * vb;
           }
         }
+      }
       // density of the rotated chunk: sum over the 4 lanes sharing point c + gq
       dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
       dsum += __shfl_xor_sync(0xffffffffu, dsum, 2);
