@@ -955,13 +955,14 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
     // V_ext of the next chunk is requested one stage ahead (a global load in
     // the epilogue stalled every warp for its full latency)
     double vx_next = (vext && t4 == 0 && pbeg + c + gq < ngl) ? __ldg(vext + pbeg + c + gq) : 0.0;
+    int s = 0;         // ring slot and phase parity, stepped without a division
+    uint32_t fph = 0;
     for (int st = 0; st < nstage; ++st) {
-      const int s = st % nst;
       const int64_t p = pbeg + (int64_t)st * KS + c + gq;
       const double vx = vx_next;
       const int64_t pn = p + KS;
       if (vext && t4 == 0 && st + 1 < nstage && pn < ngl) vx_next = __ldg(vext + pn);
-      mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+      mbar_wait(&full[s], fph);
       double* sbuf = stage0 + (size_t)s * sdoubles;
       double acc[F][2];
 #pragma unroll
@@ -972,12 +973,14 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
         for (int ks = 0; ks < 2 * F; ++ks) {
           const int off = (4 * ks + t4) * PW + c + gq;
           av[ks] = sbuf[off];
-          if (nsrc == 2) {
+          if (ZV || nsrc == 2) {
             double zb = sbuf[qstride + off];
             if constexpr (ZV) zb = fma(mz[ZV ? ks : 0], av[ks], zb);
             av[ks] += sa * zb;
           }
-          if (4 * ks + t4 >= N) av[ks] = 0.0;  // rows past N alias the next box
+          // rows past N alias the next box (N > 8 (F - 1): only the last k-steps can hold one)
+          if (4 * ks + 3 > 8 * (F - 1))
+            if (4 * ks + t4 >= N) av[ks] = 0.0;
         }
 #pragma unroll
         for (int ks = 0; ks < 2 * F; ++ks) {
@@ -1076,10 +1079,24 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
 #pragma unroll
           for (int m = 0; m < 4; ++m)
             bv[m] = *reinterpret_cast<const double2*>(sbuf + (rr) * PW + c + 2 * ((m + rot) & 3));
+          if (R == 1 && 8 * FD == 32) {
+            // rows 0 .. 31 below take all 32 lanes; the one entry left, (rr, rr), is
+            // lane 0's own bv (same products, same order as the general form, which
+            // ran 4 loads and 8 FP64 instructions for one live lane)
+            if (lane == 0) {
+              double p0 = bv[0].x * bv[0].x, p1 = bv[0].y * bv[0].y, p2 = bv[1].x * bv[1].x,
+                     p3 = bv[1].y * bv[1].y;
+              p0 = fma(bv[2].x, bv[2].x, p0);
+              p1 = fma(bv[2].y, bv[2].y, p1);
+              p2 = fma(bv[3].x, bv[3].x, p2);
+              p3 = fma(bv[3].y, bv[3].y, p3);
+              racc[1][r] += (p0 + p1) + (p2 + p3);
+            }
+          }
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < ((R == 1 && 8 * FD == 32) ? 1 : 2); ++h) {
             const int i = lane + 32 * h;
-            if (i >= N || i > rr) continue;
+            if (!(R == 1 && 8 * FD == 32) && (i >= N || i > rr)) continue;
             double2 av[4];
 #pragma unroll
             for (int m = 0; m < 4; ++m)
@@ -1112,6 +1129,10 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) rotate_fused
           dmma_8x8x4(gacc[q], a[fm].x, a[fn].x);
           dmma_8x8x4(gacc[q], a[fm].y, a[fn].y);
         }
+      if (++s == nst) {
+        s = 0;
+        fph ^= 1u;
+      }
     }
     // CTA reductions (consumers only, ring reused): G2 partial tile -> ws[block];
     // energies -> dpart[2][grid]
