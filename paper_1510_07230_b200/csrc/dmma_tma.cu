@@ -1335,9 +1335,10 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
         msr[fi][j] = msig[i];
         if constexpr (ZM == 2) mpr[fi][j] = mpsig[i];
       }
+    int s = 0;         // ring slot and phase parity, stepped without a division
+    uint32_t fph = 0;
     for (int st = 0; st < nstage; ++st) {
-      const int s = st % nst;
-      mbar_wait(&full[s], (uint32_t)(st / nst) & 1u);
+      mbar_wait(&full[s], fph);
       const double* sbuf = stage0 + (size_t)s * sdoubles;
       const int64_t p = pbeg + (int64_t)st * KS + c + gq;
       double acc[F][2];
@@ -1366,7 +1367,8 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
           // no runtime trip count: k rows >= N are zero in both operands, and a
           // data-dependent exit serialised the unrolled k-steps (load, DMMA, branch)
           const int krow = 4 * ks + t4;
-          const double av = krow < N ? sbuf[(krow) * PW + c + gq] : 0.0;
+          // (N > 8 (F - 1): only the last k-steps can hold a row past N, which aliases the next area)
+          const double av = (4 * ks + 3 <= 8 * (F - 1) || krow < N) ? sbuf[(krow) * PW + c + gq] : 0.0;
 #pragma unroll
           for (int fi = 0; fi < F; ++fi) {
             if (ks & 1)
@@ -1386,7 +1388,10 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int i = 8 * fi + 2 * t4 + (j ^ jx);
-          if (p < ngl && i < N) {
+          // the loop is issue-bound: fragments below the last hold 8 real orbitals
+          // (no row test), and points past ngl are zero padding in every block —
+          // they add exact zeros to the sums, only a stored z needs the point test
+          if (fi < F - 1 || i < N) {
             const int off = (i) * PW + c + gq;
             const double wv = sbuf[off], hv = sbuf[qstride + off];
             if constexpr (DD) {
@@ -1397,7 +1402,9 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
             // z = HW - sigma W (one FMA; rotate_fused and the previous-z term
             // below rebuild exactly this value when z is not stored, Z == null)
             const double z = fma(msr[fi][j], wv, hv);
-            if constexpr (ZM == 0) Z[(int64_t)i * ld + p] = z;
+            if constexpr (ZM == 0) {
+              if (p < ngl) Z[(int64_t)i * ld + p] = z;
+            }
             nrm[0][fi][j] += z * z;
             if constexpr (HIST) {
               const double wp = LDGH ? wpv[fi][j] : sbuf[2 * qstride + off];
@@ -1413,6 +1420,10 @@ __global__ void __launch_bounds__(CW == 8 ? TTH : (CW + 1) * 32, 1) directions_t
         }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == nst) {
+        s = 0;
+        fph ^= 1u;
+      }
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
