@@ -351,10 +351,19 @@ __global__ void __launch_bounds__(TTH, 1) gram_tma_kernel(const __grid_constant_
           double2 ar[4], br[4];
           row8(rr, 0, ar);
           row8(rr, qb, br);
+          // N = 33 (R = 1, 32 DMMA rows): rows 0 .. 31 take all 32 lanes below; the
+          // entries of row rr itself come from lane 0's own ar / br (the same
+          // products in the same order as the general form, which ran a whole
+          // pass of loads and dots for that one live lane)
+          constexpr bool ONE = R == 1 && 8 * FD == 32;
+          if (ONE && lane == 0) {
+            racc[1][r][0] = dot8(ar, br, racc[1][r][0]);  // Sigma(rr, rr)
+            racc[1][r][2] = dot8(ar, ar, racc[1][r][2]);  // G_HH(rr, rr)
+          }
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < (ONE ? 1 : 2); ++h) {
             const int i = lane + 32 * h;
-            if (i >= N) continue;
+            if (!ONE && i >= N) continue;
             double2 ai[4];
             row8(i, 0, ai);
             racc[h][r][0] = dot8(ai, br, racc[h][r][0]);  // Sigma(i, rr)
