@@ -2949,6 +2949,21 @@ __global__ void __launch_bounds__(XTH, 1) mix_tri_kernel(
       }
       // epilogue: acc[f][2 g + e][j] = out(point 64 hf + 16 g + 2 gq + e, orbital i0 + 8 fr[f] + 2 t4 + j)
       const int64_t pb = (int64_t)pt * XP + 64 * hf + 2 * gq;
+      if (alpha == 1.0 && (int64_t)(pt + 1) * XP <= ngl) {
+        // interior tile of the rotation (every tile but the last): plain stores, no
+        // per-store point tests or scaling (the general form below issues ~12
+        // instructions per store, 32 stores per lane and tile)
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            double* o = out + (int64_t)(i0 + 8 * fr[f] + 2 * t4 + j) * ld + pb;
+#pragma unroll
+            for (int gg = 0; gg < 4; ++gg)
+              *reinterpret_cast<double2*>(o + 16 * gg) = make_double2(acc[f][2 * gg][j], acc[f][2 * gg + 1][j]);
+          }
+        continue;
+      }
 #pragma unroll
       for (int f = 0; f < 4; ++f)
 #pragma unroll
