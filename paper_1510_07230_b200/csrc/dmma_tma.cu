@@ -1645,14 +1645,17 @@ __device__ __forceinline__ void sym_diag_stages(double (&acc0)[5][2][2][2], doub
       // warp's DFMAs waited behind the consumers' DMMAs on the FP64 pipe).
       const int o = 4 * (da.w8 & 3) + (lane >> 3), c = lane & 7;
       const double* area = sbuf + (size_t)(da.w8 >> 2) * QS;
-      double d0 = 0.0, d1 = 0.0;
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;  // four independent chains of four
 #pragma unroll
-      for (int j = 0; j < 16; j += 2) {
+      for (int j = 0; j < 16; j += 4) {
         const double v0 = area[swz(8 * j + c, o, 128)], v1 = area[swz(8 * j + 8 + c, o, 128)];
+        const double v2 = area[swz(8 * j + 16 + c, o, 128)], v3 = area[swz(8 * j + 24 + c, o, 128)];
         d0 = fma(v0, v0, d0);
         d1 = fma(v1, v1, d1);
+        d2 = fma(v2, v2, d2);
+        d3 = fma(v3, v3, d3);
       }
-      double d = d0 + d1;
+      double d = (d0 + d1) + (d2 + d3);
       d += __shfl_xor_sync(0xffffffffu, d, 1);
       d += __shfl_xor_sync(0xffffffffu, d, 2);
       d += __shfl_xor_sync(0xffffffffu, d, 4);
