@@ -109,7 +109,7 @@ def _prefix(native, name, start_from_port=None):
 @pytest.mark.parametrize("name", ["C2", "C3"])
 def test_prefix_full_shape(native, port, name):
     """C2 (96^3, N = 33; 3 iterations) and C3 (128^3, N = 128; as many as the
-    fixture holds, >= 5): the first outer iterations against truncated re-runs
+    fixture holds: 8): the first outer iterations against truncated re-runs
     of the unmodified reference — energy and backtracks per iteration, eig(Sigma) after every iteration (1e-6 Ha), the
     subspace projector of every iterate (sketched ||dP||_F <= 1e-6) and the
     orthogonalization checkpoints."""
