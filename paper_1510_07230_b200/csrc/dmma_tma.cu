@@ -1204,6 +1204,7 @@ int launch_rotate_fused_f(int N, int64_t ld, int64_t ngl, const double* A, const
                           const double* vext, double* dpart, cudaStream_t s,
                           const double* sa_dev, const double* zsig) {
   constexpr int NPAD = 8 * F;
+  if (xc < 0) vext = nullptr;  // <V_ext, rho> belongs to the v_local pass then: no per-stage V_ext prefetch
   static const int cw_env = getenv("PO_RF_CW") ? atoi(getenv("PO_RF_CW")) : 8;  // measurement (12: slower, 228 vs 215 us at C2)
   const int R = (N % 8 == 1 || N % 8 == 2) && N > 8 ? N % 8 : 0;
   // 12 consumer warps where they fit 128 registers without spilling (N <= 33)
