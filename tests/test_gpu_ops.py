@@ -356,7 +356,8 @@ def test_gram_fused_trial(native, n_orb):
     e.close()
 
 
-@pytest.mark.parametrize("n_orb,hist", [(128, True), (128, False), (80, True), (33, True), (130, True), (260, True)])
+@pytest.mark.parametrize("n_orb,hist", [(128, True), (128, False), (80, True), (65, True), (33, True), (130, True),
+                                        (260, True)])
 def test_direction_sums(native, n_orb, hist):
     """po_direction_sums — the iteration's direction step with z implicit
     (optimizer.cpp:265-320, 386-397; manifold.cpp:183, 204-216): sigma_ii,
@@ -365,7 +366,9 @@ def test_direction_sums(native, n_orb, hist):
     the one-pass form (the Sigma Gram's DMMA warps carry the sums; N = 130 / 260:
     several 128-tiles, the sums on the diagonal ones), N = 33 the Gram + a
     streaming pass. Sums of ~2700 terms in another order: 1e-12 relative."""
-    spec = configs.small_molecule(14, n_orb, L=8.0)
+    # N = 65: an odd point count too (13 x 11 x 15: the last 16-point stage is ragged)
+    spec = (configs.ProblemSpec("odd", (13, 11, 15), (7.0, 6.0, 9.0), [(3.0, 2.5, 4.0, 3.0, 1.0)], n_orb)
+            if n_orb == 65 else configs.small_molecule(14, n_orb, L=8.0))
     rng = np.random.default_rng(5)
     wq = float(np.prod(spec.spacing))
     u = rng.standard_normal((n_orb, spec.num_points))
