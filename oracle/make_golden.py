@@ -278,6 +278,8 @@ def main_big(which):
                        extend=True)
     if "C4ops" in which:
         gen_ops_reduced("C4g64", c4_grid_spec(64))
+    if "C4p" in which:  # two solver iterations at the C4 grid (192^3, the C4 nuclei, N = 64)
+        gen_prefix("C4g64", c4_grid_spec(64), 2, threads=int(os.environ.get("GOLDEN_THREADS", "8")))
 
 
 def gen_orth_fallback(name="orth_fallback", eps=1e-5):
@@ -308,7 +310,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true", help="skip the C1/C2 trajectories")
     ap.add_argument("--from-dir", default="/tmp/golden_runs", help="reuse finished C1/C2 trace_ref runs")
-    ap.add_argument("--big", default="", help="comma list of C1eig,C2eig,C2p,C3ops,C3p,C3p<K>,C4ops (long runs; C3p<K> extends the committed C3 prefix to K iterations)")
+    ap.add_argument("--big", default="", help="comma list of C1eig,C2eig,C2p,C3ops,C3p,C3p<K>,C4ops,C4p (long runs; C3p<K> extends the committed C3 prefix to K iterations)")
     args = ap.parse_args()
     if args.big:
         return main_big(args.big.split(","))

@@ -106,13 +106,16 @@ def _prefix(native, name, start_from_port=None):
     return gold, arr, eig, res, recs, dists
 
 
-@pytest.mark.parametrize("name", ["C2", "C3"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4g64"])
 def test_prefix_full_shape(native, port, name):
     """C2 (96^3, N = 33; 3 iterations) and C3 (128^3, N = 128; as many as the
     fixture holds: 8): the first outer iterations against truncated re-runs
     of the unmodified reference — energy and backtracks per iteration, eig(Sigma) after every iteration (1e-6 Ha), the
     subspace projector of every iterate (sketched ||dP||_F <= 1e-6) and the
-    orthogonalization checkpoints."""
+    orthogonalization checkpoints. C4g64: the same for two iterations at the C4
+    grid (192^3, L = 60, the C4 nuclei) with N = 64 orbitals."""
+    if not os.path.exists(os.path.join(GOLDEN, f"prefix_{name}.json")):
+        pytest.skip(f"prefix_{name} fixture not generated (oracle/make_golden.py --big)")
     gold, arr, eig, res, recs, dists = _prefix(
         native, name, start_from_port=port.random_orthonormal if name == "C2" else None)
     ref_recs = gold["records"]
